@@ -1,0 +1,258 @@
+/*
+ * arfx.h -- C-ABI of the B200-native InstantAvatar render/train hot path
+ * (libarfx.so, paper_2212_10550_b200/lib/). Plain pointers and sizes only.
+ *
+ * Each entry point replaces one model-bound operation of the reference C++
+ * library `arf` (/root/reference/proj/include/arf, cited as R/...):
+ *
+ *   arfx_build_model            <- arf::build_model<float>            R/model.hpp:68-80
+ *   arfx_model_create           <- an existing arf::Model<float> (upload of its members:
+ *                                  HashGrid::params R/hash_grid.hpp:62, DecoderMlp::params
+ *                                  R/mlp.hpp:31, SkinningGrid::weights R/skinning.hpp:16)
+ *   arfx_pose_from_joint_rotations <- arf::pose_from_joint_rotations  R/skeleton.hpp:93-110
+ *   arfx_pose_create            <- arf::PosedModelView ctor / PoseContext::make
+ *                                  R/model.hpp:92-96, R/articulation.hpp:24-41
+ *   arfx_render_model           <- arf::render_model                  R/model.hpp:118-135
+ *   arfx_build_inference_grid   <- arf::build_model_inference_grid    R/model.hpp:138-148
+ *   arfx_update_training_grid   <- arf::update_training_grid bound to
+ *                                  PosedModelView::density_normalized R/occupancy.hpp:155-171
+ *   arfx_inverse_lbs            <- arf::inverse_lbs_ctx (batched)     R/articulation.hpp:94-145
+ *   arfx_posed_query            <- PosedModelView::query_normalized   R/model.hpp:100-107
+ *   arfx_field_query            <- CanonicalField::query (batched)    R/field.hpp:75-82
+ *   arfx_hash_encode            <- HashGrid::encode (batched)         R/hash_grid.hpp:137-150
+ *   arfx_skinning_weights       <- SkinningGrid::interpolate          R/skinning.hpp:25-55
+ *   arfx_composite(_backward)   <- arf::composite / composite_backward R/render.hpp:98-157
+ *   arfx_field_query_backward   <- CanonicalField::query_backward     R/field.hpp:91-103
+ *   arfx_train_fwd_bwd          <- composed training step
+ *
+ * Error convention (the reference throws; R/math.hpp:12-18): every function
+ * returns an int status, 0 = ok, and sets a thread-local message readable via
+ * arfx_last_error():
+ *   1 std::invalid_argument, 2 arf::DataError, 3 arf::NumericError,
+ *   4 std::domain_error, 5 CUDA / runtime failure, 6 no CUDA device.
+ * There is NO CPU fallback: compute entry points return 6 without a GPU.
+ *
+ * Streams: `stream` is a cudaStream_t passed as void*; NULL means the library's
+ * per-device non-blocking stream. Host-pointer variants synchronise before they
+ * return (same blocking contract as the reference's value-returning API).
+ */
+#ifndef ARFX_H
+#define ARFX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ARFX_MAX_BONES 32 /* arf::kMaxBones  R/articulation.hpp:10 */
+#define ARFX_MAX_ROOTS 8  /* arf::kMaxRoots  R/articulation.hpp:11 */
+#define ARFX_MAX_LEVELS 32
+
+enum {
+  ARFX_OK = 0,
+  ARFX_ERR_INVALID_ARGUMENT = 1,
+  ARFX_ERR_DATA = 2,
+  ARFX_ERR_NUMERIC = 3,
+  ARFX_ERR_DOMAIN = 4,
+  ARFX_ERR_RUNTIME = 5,
+  ARFX_ERR_NO_DEVICE = 6
+};
+
+/* ---- plain-data mirrors of the reference's value types ---------------- */
+
+typedef struct { /* arf::Skeleton  R/skeleton.hpp:9-32 (bones in tree order) */
+  int n_bones;
+  int parent[ARFX_MAX_BONES];
+  double head[ARFX_MAX_BONES][3];
+  double tail[ARFX_MAX_BONES][3];
+  double radius[ARFX_MAX_BONES];
+} arfx_skeleton;
+
+typedef struct { /* arf::HashGridConfig  R/hash_grid.hpp:12-32 */
+  int levels, features_per_level, table_size_log2, base_resolution, max_resolution;
+  double box_lo[3], box_hi[3];
+} arfx_grid_config;
+
+typedef struct { /* arf::MlpConfig  R/mlp.hpp:11-23 */
+  int input_dim, hidden_dim, hidden_layers, output_dim;
+} arfx_mlp_config;
+
+/* arf::Rigidd (R/math.hpp:186-213) is passed as double[12]: rotation row-major
+ * (9) followed by translation (3). A SkeletonPose (R/skeleton.hpp:69-88) is
+ * bone_transforms double[n_bones][12] plus global_transform double[12]. */
+
+typedef struct { /* arf::Camera  R/camera.hpp:9-49 */
+  double fx, fy, cx, cy;
+  int width, height;
+  double extrinsic[12]; /* world -> camera */
+} arfx_camera;
+
+typedef struct { /* arf::OccupancyConfig  R/occupancy.hpp:13-28 */
+  int resolution;
+  double alpha_threshold;
+  int dilation;
+  double decay;
+  int update_interval;
+} arfx_occ_config;
+
+typedef struct { /* arf::RenderOptions  R/render.hpp:159-165 */
+  int samples_per_ray;
+  int stratified;
+  double epsilon_terminate;
+  uint64_t seed;
+  uint64_t frame_id;
+} arfx_render_options;
+
+typedef struct { /* arf::InverseLbsOptions  R/articulation.hpp:84-88 */
+  int max_iterations;
+  double tolerance;
+  double dedup_radius;
+} arfx_inverse_options;
+
+typedef struct { /* arf::QueryCounters  R/model.hpp:11-23 */
+  uint64_t posed_queries;
+  uint64_t canonical_queries;
+} arfx_counters;
+
+typedef struct { /* everything arf::Model<float> holds besides the big arrays */
+  arfx_skeleton skeleton;
+  arfx_grid_config grid;  /* bounding box == canonical box */
+  arfx_mlp_config mlp;
+  int skin_res[3];
+  double skin_lo[3], skin_hi[3];
+  double canonical_lo[3], canonical_hi[3];
+  double normalized_lo[3], normalized_hi[3];
+  arfx_inverse_options inverse;
+  size_t n_grid_params, n_mlp_params, n_skin_weights;
+} arfx_model_desc;
+
+typedef struct arfx_model_s* arfx_model;      /* device-resident arf::Model<float> */
+typedef struct arfx_pose_s* arfx_pose;        /* device-resident PosedModelView   */
+typedef struct arfx_occ_s* arfx_occ_grid;     /* device-resident OccupancyGrid    */
+
+/* ---- library / errors ------------------------------------------------ */
+const char* arfx_last_error(void);
+const char* arfx_version(void);
+int arfx_device_count(int* n);
+int arfx_set_device(int device);
+
+/* ---- host-side value helpers (no GPU needed) ------------------------- */
+int arfx_level_resolutions(const arfx_grid_config* g, int* out_levels);
+int arfx_model_sizes(const arfx_skeleton* s, const arfx_grid_config* g, const arfx_mlp_config* m,
+                     const int skin_res[3], size_t* n_grid, size_t* n_mlp, size_t* n_skin);
+int arfx_pose_from_joint_rotations(const arfx_skeleton* s, const double* joint_rot9,
+                                   const double* global12, double* bone_transforms12);
+int arfx_camera_look_at(const double eye[3], const double target[3], const double up[3],
+                        double focal, int width, int height, arfx_camera* out);
+int arfx_pose_context(const arfx_skeleton* s, const double* bone_transforms12, const double* pre12,
+                      double cutoff_factor, double* out_bone12, double* out_bone_inv12,
+                      double* out_cap_a3, double* out_cap_b3, double* out_cutoff);
+
+/* ---- model ----------------------------------------------------------- */
+int arfx_build_model(const arfx_skeleton* s, const arfx_grid_config* g, const arfx_mlp_config* m,
+                     const int skin_res[3], uint64_t seed, arfx_model* out);
+int arfx_model_create(const arfx_model_desc* desc, const float* grid_params,
+                      const float* mlp_params, const double* skin_weights, arfx_model* out);
+int arfx_model_destroy(arfx_model m);
+int arfx_model_describe(arfx_model m, arfx_model_desc* out);
+int arfx_model_get_params(arfx_model m, float* grid_params, float* mlp_params,
+                          double* skin_weights);
+int arfx_model_set_params(arfx_model m, const float* grid_params, const float* mlp_params);
+int arfx_model_zero_grad(arfx_model m, void* stream);
+int arfx_model_get_grads(arfx_model m, float* grid_grad, float* mlp_grad);
+/* device pointers of the parameter / gradient arrays (for NCCL / optimizers) */
+int arfx_model_device_arrays(arfx_model m, float** grid_params, float** mlp_params,
+                             float** grid_grad, float** mlp_grad);
+
+/* ---- pose (PosedModelView: normalized-space PoseContext) --------------- */
+int arfx_pose_create(arfx_model m, const double* bone_transforms12, const double* global12,
+                     arfx_pose* out);
+int arfx_pose_update(arfx_pose p, const double* bone_transforms12, const double* global12,
+                     void* stream);
+int arfx_pose_destroy(arfx_pose p);
+
+/* ---- occupancy grid ---------------------------------------------------- */
+int arfx_occ_create(const double box_lo[3], const double box_hi[3], const arfx_occ_config* cfg,
+                    arfx_occ_grid* out); /* OccupancyGrid::empty  R/occupancy.hpp:59-69 */
+int arfx_occ_destroy(arfx_occ_grid g);
+int arfx_occ_info(arfx_occ_grid g, int res[3], double box_lo[3], double box_hi[3],
+                  double* density_threshold, int* dilation);
+int arfx_occ_download(arfx_occ_grid g, float* values, uint8_t* mask);
+int arfx_occ_upload(arfx_occ_grid g, const float* values, const uint8_t* mask);
+int arfx_occ_rebuild_mask(arfx_occ_grid g, void* stream); /* R/occupancy.hpp:87-91 */
+int arfx_build_inference_grid(arfx_model m, arfx_pose p, arfx_occ_grid g, arfx_counters* c,
+                              void* stream);
+/* asynchronous variant: counters (u64 x4: posed, canonical, pool, overflow) to device memory */
+int arfx_build_inference_grid_device(arfx_model m, arfx_pose p, arfx_occ_grid g,
+                                     uint64_t* d_counters, void* stream);
+int arfx_update_training_grid(arfx_model m, const arfx_pose* poses, int n_poses, double decay,
+                              uint64_t seed, uint64_t step, arfx_occ_grid g, arfx_counters* c,
+                              void* stream);
+
+/* ---- render ------------------------------------------------------------- */
+/* Host buffers: rgb[H*W*3], alpha[H*W] (arf::RenderImages layout R/render.hpp:167-171).
+ * occ may be NULL (no skipping). row_shard/n_shards select interleaved 16-row tiles
+ * (tile % n_shards == row_shard) for multi-GPU sharding; use 0/1 for a full frame --
+ * rows of other shards are left untouched. */
+int arfx_render_model(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                      const arfx_render_options* opt, int row_shard, int n_shards, float* rgb,
+                      float* alpha, arfx_counters* c, void* stream);
+/* Device buffers, asynchronous on `stream`; counters (2 x u64) written to device memory. */
+int arfx_render_model_device(arfx_model m, arfx_pose p, const arfx_camera* cam,
+                             arfx_occ_grid occ, const arfx_render_options* opt, int row_shard,
+                             int n_shards, float* d_rgb, float* d_alpha, uint64_t* d_counters,
+                             void* stream);
+/* Trace of the last render on this model (posed-sample list), for parity tests:
+ * per posed sample: pixel, sample index, has_root, density, rgb, canonical root. */
+int arfx_render_trace(arfx_model m, int64_t capacity, int64_t* n_samples, int32_t* s_ray,
+                      int32_t* s_index, uint8_t* s_has_root, float* s_density, float* s_color,
+                      double* s_canonical, double* s_delta);
+
+/* ---- per-kernel timing (CUDA events on the launching stream; for bench/roofline) */
+int arfx_profile_enable(arfx_model m, int on);
+/* collects (synchronising on the recorded events), returns and resets the totals:
+ * names[max][32], total ms and launch count per kernel name; *n = entries written */
+int arfx_profile_read(arfx_model m, int max, char* names, double* ms, int64_t* launches, int* n);
+
+/* ---- batched lower-level operations (host arrays in/out) ---------------- */
+int arfx_skinning_weights(arfx_model m, const double* pts, int64_t n, double* w /*n*n_bones*/);
+/* pose context built with `pre` and cutoff factor exactly as PoseContext::make;
+ * roots[n][8][3], residuals[n][8], counts[n] */
+int arfx_inverse_lbs(arfx_model m, const double* bone_transforms12, const double* pre12,
+                     double cutoff_factor, const double* pts, int64_t n, int32_t* counts,
+                     double* roots, double* residuals);
+/* device-pointer variant for the correspondence microbench (pts/counts/roots/residuals on device) */
+int arfx_inverse_lbs_device(arfx_model m, arfx_pose ctx_pose, const double* d_pts, int64_t n,
+                            int32_t* d_counts, double* d_roots, double* d_residuals,
+                            void* stream);
+int arfx_pose_create_context(arfx_model m, const double* bone_transforms12, const double* pre12,
+                             double cutoff_factor, arfx_pose* out);
+int arfx_hash_encode(arfx_model m, const double* pts, int64_t n, float* feats);
+int arfx_field_query(arfx_model m, const double* pts, int64_t n, float* density, float* color);
+int arfx_posed_query(arfx_model m, arfx_pose p, const double* pts_norm, int64_t n,
+                     float* density, float* color, double* canonical, uint8_t* has_root,
+                     arfx_counters* c);
+int arfx_composite(int n_rays, const int32_t* ray_len, const double* t, const double* delta,
+                   const uint8_t* skipped, const float* density, const float* color,
+                   double epsilon, double* out_color3, double* out_alpha, int32_t* terminated_at);
+int arfx_composite_backward(int n_rays, const int32_t* ray_len, const double* t,
+                            const double* delta, const uint8_t* skipped, const float* density,
+                            const float* color, double epsilon, const double* d_color3,
+                            const double* d_alpha, double* d_sigma, double* d_c3);
+/* accumulates into the model's device gradient buffers (FieldGrads  R/field.hpp:19-36) */
+int arfx_field_query_backward(arfx_model m, const double* pts, int64_t n, const float* d_density,
+                              const float* d_color);
+/* training forward+backward over n rays given by pixel coordinates; accumulates into
+ * the model's gradient buffers; rgb/alpha per ray to host (may be NULL). */
+int arfx_train_fwd_bwd(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                       const arfx_render_options* opt, int64_t n_rays, const int32_t* px,
+                       const int32_t* py, const float* d_color, const float* d_alpha, float* rgb,
+                       float* alpha, arfx_counters* c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ARFX_H */

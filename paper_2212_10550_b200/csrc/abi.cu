@@ -1,0 +1,1099 @@
+// abi.cu -- extern "C" entry points of libarfx.so (declared in include/arfx.h).
+// Handles own device memory; errors become status codes + a thread-local message
+// (the reference throws: R/math.hpp:12-18, std::invalid_argument / domain_error).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/arfx.h"
+#include "host.h"
+#include "model.h"
+
+struct arfx_model_s {
+  arfx::ModelImpl impl;
+};
+struct arfx_pose_s {
+  arfx::PoseImpl impl;
+};
+struct arfx_occ_s {
+  arfx::OccImpl impl;
+};
+
+namespace arfx {
+
+namespace {
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return ARFX_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ARFX_ERR_INVALID_ARGUMENT;
+  } catch (const DataError& e) {
+    g_err = e.what();
+    return ARFX_ERR_DATA;
+  } catch (const NumericError& e) {
+    g_err = e.what();
+    return ARFX_ERR_NUMERIC;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return ARFX_ERR_DOMAIN;
+  } catch (const NoDevice& e) {
+    g_err = e.what();
+    return ARFX_ERR_NO_DEVICE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ARFX_ERR_RUNTIME;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw NoDevice("libarfx: no CUDA device available (there is no CPU fallback)");
+  }
+}
+
+std::vector<HostBone> bones_of(const arfx_skeleton* s) {
+  require(s != nullptr, "skeleton: null");
+  require(s->n_bones >= 1, "skeleton: needs at least one bone");
+  require(s->n_bones <= ARFX_MAX_BONES, "pose context: too many bones");
+  std::vector<HostBone> b(static_cast<size_t>(s->n_bones));
+  for (int i = 0; i < s->n_bones; ++i) {
+    b[static_cast<size_t>(i)] = HostBone{s->parent[i], {s->head[i][0], s->head[i][1], s->head[i][2]},
+                                         {s->tail[i][0], s->tail[i][1], s->tail[i][2]}, s->radius[i]};
+  }
+  return b;
+}
+
+GridCfg grid_of(const arfx_grid_config* g) {
+  require(g != nullptr, "grid config: null");
+  return GridCfg{g->levels, g->features_per_level, g->table_size_log2, g->base_resolution,
+                 g->max_resolution,
+                 HostBox{{g->box_lo[0], g->box_lo[1], g->box_lo[2]}, {g->box_hi[0], g->box_hi[1], g->box_hi[2]}}};
+}
+
+HostCamera camera_of(const arfx_camera* c) {
+  require(c != nullptr, "camera: null");
+  HostCamera h{c->fx, c->fy, c->cx, c->cy, c->width, c->height, {}};
+  std::memcpy(h.ext, c->extrinsic, sizeof(h.ext));
+  return h;
+}
+
+cudaStream_t stream_of(ModelImpl& m, void* s) {
+  return s ? static_cast<cudaStream_t>(s) : m.stream;
+}
+
+template <typename T>
+void h2d(T* d, const T* h, size_t n, cudaStream_t s) {
+  if (n) ARFX_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+void d2h(T* h, const T* d, size_t n, cudaStream_t s) {
+  if (n) ARFX_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+// Hash-grid level kinds  R/hash_grid.hpp:87-101
+void fill_field_view(ModelImpl& m) {
+  FieldView& f = m.fv;
+  f = FieldView{};
+  f.L = m.grid.levels;
+  f.F = m.grid.F;
+  f.log2T = m.grid.log2T;
+  f.T = 1u << m.grid.log2T;
+  for (int l = 0; l < f.L; ++l) {
+    const uint64_t n = static_cast<uint64_t>(m.res[static_cast<size_t>(l)]);
+    const uint64_t c = n + 1;
+    f.res[l] = static_cast<int>(n);
+    f.kind[l] = (c * c * c <= f.T) ? kDirect : ((n * n * n <= f.T) ? kWrap : kHashed);
+  }
+  const HostBox& b = m.grid.box;
+  f.lo[0] = b.lo.x;
+  f.lo[1] = b.lo.y;
+  f.lo[2] = b.lo.z;
+  f.hi[0] = b.hi.x;
+  f.hi[1] = b.hi.y;
+  f.hi[2] = b.hi.z;
+  f.e[0] = b.hi.x - b.lo.x;
+  f.e[1] = b.hi.y - b.lo.y;
+  f.e[2] = b.hi.z - b.lo.z;
+  f.grid = m.grid_params.ptr;
+  f.n_layers = m.mlp.n_layers;
+  for (int l = 0; l < m.mlp.n_layers; ++l) {
+    f.lin[l] = m.mlp.lin[l];
+    f.lout[l] = m.mlp.lout[l];
+    f.w_off[l] = m.mlp.w_off[l];
+    f.b_off[l] = m.mlp.b_off[l];
+  }
+  f.in_dim = m.mlp_in;
+  f.hidden = m.mlp_hidden;
+  f.out_dim = m.mlp_out;
+  f.n_mlp = m.mlp.n_params;
+  f.mlp = m.mlp_params.ptr;
+  SkinView& s = m.sv;
+  s.rx = m.skin_res[0];
+  s.ry = m.skin_res[1];
+  s.rz = m.skin_res[2];
+  s.nb = static_cast<int>(m.bones.size());
+  s.lo[0] = m.skin_box.lo.x;
+  s.lo[1] = m.skin_box.lo.y;
+  s.lo[2] = m.skin_box.lo.z;
+  s.hi[0] = m.skin_box.hi.x;
+  s.hi[1] = m.skin_box.hi.y;
+  s.hi[2] = m.skin_box.hi.z;
+  s.e[0] = m.skin_box.hi.x - m.skin_box.lo.x;
+  s.e[1] = m.skin_box.hi.y - m.skin_box.lo.y;
+  s.e[2] = m.skin_box.hi.z - m.skin_box.lo.z;
+  s.weights = m.skin.ptr;
+  s.cell_mask = m.cell_mask.ptr;
+  s.cell_off = m.cell_off.ptr;
+  s.cell_vals = m.cell_vals.ptr;
+}
+
+// common model skeleton/config setup (shared by build_model and model_create)
+void setup_model(ModelImpl& m, const std::vector<HostBone>& bones, GridCfg grid, int mlp_hidden,
+                 int mlp_hl, int mlp_out, const int skin_res[3]) {
+  validate_skeleton(bones);
+  m.bones = bones;
+  m.grid = grid;
+  m.res = level_resolutions(grid);  // validates the grid config
+  m.mlp_in = grid.levels * grid.F;
+  m.mlp_hidden = mlp_hidden;
+  m.mlp_hl = mlp_hl;
+  m.mlp_out = mlp_out;
+  m.mlp = mlp_layout(m.mlp_in, mlp_hidden, mlp_hl, mlp_out);
+  require(mlp_out >= 4, "mlp: output_dim must be >= 4 (density + 3 colour logits, R/field.hpp:78-81)");
+  require(m.mlp_in <= 256 && mlp_hidden <= 256 && mlp_out <= 256,
+          "mlp: libarfx supports layer widths <= 256");
+  require(skin_res[0] >= 2 && skin_res[1] >= 2 && skin_res[2] >= 2,
+          "skinning grid: resolution must be >= 2 per axis");
+  for (int a = 0; a < 3; ++a) m.skin_res[a] = skin_res[a];
+  m.n_grid = static_cast<size_t>(grid.levels) * (static_cast<size_t>(1) << grid.log2T) *
+             static_cast<size_t>(grid.F);
+  m.n_mlp = static_cast<size_t>(m.mlp.n_params);
+  m.n_skin = static_cast<size_t>(skin_res[0]) * skin_res[1] * skin_res[2] * bones.size();
+}
+
+void alloc_model(ModelImpl& m) {
+  ARFX_CUDA(cudaGetDevice(&m.device));
+  if (!m.stream) ARFX_CUDA(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
+  m.grid_params.alloc(m.n_grid);
+  m.mlp_params.alloc(m.n_mlp);
+  m.skin.alloc(m.n_skin);
+}
+
+void make_pose_host(ModelImpl& m, const double* bones12, const double* global12, PoseCtx& ctx) {
+  require(bones12 != nullptr && global12 != nullptr, "pose: null transforms");
+  double ginv[12];
+  rigid_inverse(global12, ginv);
+  make_pose_ctx(m.bones, bones12, ginv, 3.0, ctx);  // PosedModelView ctor R/model.hpp:92-96
+}
+
+OccImpl& occ_ref(arfx_occ_grid g) {
+  require(g != nullptr, "occupancy grid: null");
+  return g->impl;
+}
+
+void check_overflow_and_grow(ModelImpl& m, const unsigned long long* c, bool& rerun) {
+  rerun = false;
+  Workspace& w = m.ws;
+  if (c[0] > w.cap_posed || c[3] > 0 || c[2] > w.cap_pool) {
+    const size_t need = static_cast<size_t>(std::max<unsigned long long>(c[0], w.cap_posed));
+    w.cap_posed = 0;  // force reallocation
+    w.cap_pool = 0;
+    w.ensure(need + need / 4 + 4096, 0);
+    rerun = true;
+  }
+}
+
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+      throw NoDevice(std::string("CUDA: ") + cudaGetErrorString(e) + " in " + what);
+    throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what);
+  }
+}
+
+ModelImpl::~ModelImpl() {
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+void ModelImpl::refresh_views() { fill_field_view(*this); }
+
+}  // namespace arfx
+
+namespace arfx {
+namespace {
+struct RenderBuffers {
+  DevBuf<float> rgb, alpha;
+  DevBuf<unsigned long long> counters;
+};
+thread_local std::unique_ptr<RenderBuffers> t_rb;
+
+void validate_render(const HostCamera& cam, const arfx_render_options* opt, int shard, int nshards) {
+  validate_camera(cam);
+  require(opt != nullptr, "render: null options");
+  require(opt->samples_per_ray <= 1024, "render: libarfx supports samples_per_ray <= 1024");
+  require(nshards >= 1 && shard >= 0 && shard < nshards, "render: bad shard");
+}
+}  // namespace
+namespace {
+template <typename T>
+struct Staged {
+  DevBuf<T> d;
+  void up(const T* h, size_t n, cudaStream_t s) {
+    d.alloc(n);
+    h2d(d.ptr, h, n, s);
+  }
+};
+}  // namespace
+namespace {
+void ray_offsets(int n_rays, const int32_t* ray_len, std::vector<int64_t>& off) {
+  off.assign(static_cast<size_t>(n_rays) + 1, 0);
+  for (int r = 0; r < n_rays; ++r) {
+    require(ray_len[r] >= 0, "composite: negative ray length");
+    off[static_cast<size_t>(r) + 1] = off[static_cast<size_t>(r)] + ray_len[r];
+  }
+}
+}  // namespace
+}  // namespace arfx
+
+using namespace arfx;
+
+extern "C" {
+
+const char* arfx_last_error(void) { return g_err.c_str(); }
+const char* arfx_version(void) { return "arfx 0.1 (sm_100a)"; }
+
+int arfx_device_count(int* n) {
+  return guard([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *n = c;
+  });
+}
+
+int arfx_set_device(int device) { return guard([&] { ARFX_CUDA(cudaSetDevice(device)); }); }
+
+int arfx_level_resolutions(const arfx_grid_config* g, int* out) {
+  return guard([&] {
+    const auto r = level_resolutions(grid_of(g));
+    std::copy(r.begin(), r.end(), out);
+  });
+}
+
+int arfx_model_sizes(const arfx_skeleton* s, const arfx_grid_config* g, const arfx_mlp_config* mc,
+                     const int skin_res[3], size_t* n_grid, size_t* n_mlp, size_t* n_skin) {
+  return guard([&] {
+    const GridCfg gc = grid_of(g);
+    validate_grid_cfg(gc);
+    *n_grid = static_cast<size_t>(gc.levels) * (static_cast<size_t>(1) << gc.log2T) * static_cast<size_t>(gc.F);
+    *n_mlp = static_cast<size_t>(mlp_layout(gc.levels * gc.F, mc->hidden_dim, mc->hidden_layers, mc->output_dim).n_params);
+    *n_skin = static_cast<size_t>(skin_res[0]) * skin_res[1] * skin_res[2] * static_cast<size_t>(s->n_bones);
+  });
+}
+
+int arfx_pose_from_joint_rotations(const arfx_skeleton* s, const double* rot9, const double* g12,
+                                   double* out12) {
+  return guard([&] {
+    const auto b = bones_of(s);
+    pose_from_joint_rotations(b, rot9, g12, out12);
+  });
+}
+
+int arfx_camera_look_at(const double eye[3], const double target[3], const double up[3], double focal,
+                        int width, int height, arfx_camera* out) {
+  return guard([&] {
+    const HostCamera c = look_at({eye[0], eye[1], eye[2]}, {target[0], target[1], target[2]},
+                                 {up[0], up[1], up[2]}, focal, width, height);
+    out->fx = c.fx;
+    out->fy = c.fy;
+    out->cx = c.cx;
+    out->cy = c.cy;
+    out->width = c.width;
+    out->height = c.height;
+    std::memcpy(out->extrinsic, c.ext, sizeof(c.ext));
+  });
+}
+
+int arfx_pose_context(const arfx_skeleton* s, const double* bones12, const double* pre12, double cutoff,
+                      double* ob, double* obi, double* ca, double* cb, double* co) {
+  return guard([&] {
+    const auto b = bones_of(s);
+    PoseCtx ctx;
+    make_pose_ctx(b, bones12, pre12, cutoff, ctx);
+    for (int i = 0; i < ctx.nb; ++i) {
+      std::memcpy(ob + 12 * i, ctx.bone[i], 12 * sizeof(double));
+      std::memcpy(obi + 12 * i, ctx.bone_inv[i], 12 * sizeof(double));
+      std::memcpy(ca + 3 * i, ctx.cap_a[i], 3 * sizeof(double));
+      std::memcpy(cb + 3 * i, ctx.cap_b[i], 3 * sizeof(double));
+      co[i] = ctx.cutoff[i];
+    }
+  });
+}
+
+// build_model<float>  R/model.hpp:68-80
+int arfx_build_model(const arfx_skeleton* s, const arfx_grid_config* g, const arfx_mlp_config* mc,
+                     const int skin_res[3], uint64_t seed, arfx_model* out) {
+  return guard([&] {
+    require(out != nullptr && mc != nullptr && skin_res != nullptr, "build_model: null argument");
+    const auto bones = bones_of(s);
+    validate_skeleton(bones);
+    require_device();
+    auto h = std::make_unique<arfx_model_s>();
+    ModelImpl& m = h->impl;
+    m.canon = rest_bounds(bones, 0.10);
+    GridCfg gc = grid_of(g);
+    gc.box = m.canon;
+    setup_model(m, bones, gc, mc->hidden_dim, mc->hidden_layers, mc->output_dim, skin_res);
+    for (const HostBone& b : bones) {  // R/skinning.hpp:67-69
+      const double dx = b.tail.x - b.head.x, dy = b.tail.y - b.head.y, dz = b.tail.z - b.head.z;
+      require(std::sqrt(dx * dx + dy * dy + dz * dz) > 0, "skinning grid: degenerate zero-length bone");
+    }
+    m.skin_box = m.canon;
+    m.norm = normalized_reach_box(bones, 1.05);
+    alloc_model(m);
+    init_params_dev(m, seed);
+    build_skinning_grid_dev(m, 1.5);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    build_cell_table(m);
+    fill_field_view(m);
+    *out = h.release();
+  });
+}
+
+int arfx_model_create(const arfx_model_desc* d, const float* grid_params, const float* mlp_params,
+                      const double* skin_weights, arfx_model* out) {
+  return guard([&] {
+    require(d != nullptr && out != nullptr && grid_params && mlp_params && skin_weights,
+            "model_create: null argument");
+    require_device();
+    auto h = std::make_unique<arfx_model_s>();
+    ModelImpl& m = h->impl;
+    const auto bones = bones_of(&d->skeleton);
+    setup_model(m, bones, grid_of(&d->grid), d->mlp.hidden_dim, d->mlp.hidden_layers, d->mlp.output_dim,
+                d->skin_res);
+    require(d->mlp.input_dim == m.mlp_in, "model_create: mlp input_dim must equal levels*features");
+    require(d->n_grid_params == m.n_grid && d->n_mlp_params == m.n_mlp && d->n_skin_weights == m.n_skin,
+            "model_create: array sizes do not match the configs");
+    m.skin_box = HostBox{{d->skin_lo[0], d->skin_lo[1], d->skin_lo[2]}, {d->skin_hi[0], d->skin_hi[1], d->skin_hi[2]}};
+    m.canon = HostBox{{d->canonical_lo[0], d->canonical_lo[1], d->canonical_lo[2]},
+                      {d->canonical_hi[0], d->canonical_hi[1], d->canonical_hi[2]}};
+    m.norm = HostBox{{d->normalized_lo[0], d->normalized_lo[1], d->normalized_lo[2]},
+                     {d->normalized_hi[0], d->normalized_hi[1], d->normalized_hi[2]}};
+    m.inv = InverseOpts{d->inverse.max_iterations, d->inverse.tolerance, d->inverse.dedup_radius};
+    alloc_model(m);
+    h2d(m.grid_params.ptr, grid_params, m.n_grid, m.stream);
+    h2d(m.mlp_params.ptr, mlp_params, m.n_mlp, m.stream);
+    h2d(m.skin.ptr, skin_weights, m.n_skin, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    build_cell_table(m);
+    fill_field_view(m);
+    *out = h.release();
+  });
+}
+
+int arfx_model_destroy(arfx_model m) {
+  return guard([&] { delete m; });
+}
+
+int arfx_model_describe(arfx_model mh, arfx_model_desc* d) {
+  return guard([&] {
+    require(mh && d, "describe: null");
+    ModelImpl& m = mh->impl;
+    std::memset(d, 0, sizeof(*d));
+    d->skeleton.n_bones = static_cast<int>(m.bones.size());
+    for (size_t i = 0; i < m.bones.size(); ++i) {
+      const HostBone& b = m.bones[i];
+      d->skeleton.parent[i] = b.parent;
+      d->skeleton.head[i][0] = b.head.x;
+      d->skeleton.head[i][1] = b.head.y;
+      d->skeleton.head[i][2] = b.head.z;
+      d->skeleton.tail[i][0] = b.tail.x;
+      d->skeleton.tail[i][1] = b.tail.y;
+      d->skeleton.tail[i][2] = b.tail.z;
+      d->skeleton.radius[i] = b.radius;
+    }
+    d->grid = arfx_grid_config{m.grid.levels, m.grid.F, m.grid.log2T, m.grid.nmin, m.grid.nmax,
+                               {m.grid.box.lo.x, m.grid.box.lo.y, m.grid.box.lo.z},
+                               {m.grid.box.hi.x, m.grid.box.hi.y, m.grid.box.hi.z}};
+    d->mlp = arfx_mlp_config{m.mlp_in, m.mlp_hidden, m.mlp_hl, m.mlp_out};
+    for (int a = 0; a < 3; ++a) d->skin_res[a] = m.skin_res[a];
+    const HostBox* boxes[3] = {&m.skin_box, &m.canon, &m.norm};
+    double* los[3] = {d->skin_lo, d->canonical_lo, d->normalized_lo};
+    double* his[3] = {d->skin_hi, d->canonical_hi, d->normalized_hi};
+    for (int k = 0; k < 3; ++k) {
+      los[k][0] = boxes[k]->lo.x;
+      los[k][1] = boxes[k]->lo.y;
+      los[k][2] = boxes[k]->lo.z;
+      his[k][0] = boxes[k]->hi.x;
+      his[k][1] = boxes[k]->hi.y;
+      his[k][2] = boxes[k]->hi.z;
+    }
+    d->inverse = arfx_inverse_options{m.inv.max_iterations, m.inv.tolerance, m.inv.dedup_radius};
+    d->n_grid_params = m.n_grid;
+    d->n_mlp_params = m.n_mlp;
+    d->n_skin_weights = m.n_skin;
+  });
+}
+
+int arfx_model_get_params(arfx_model mh, float* gp, float* mp, double* sw) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (gp) d2h(gp, m.grid_params.ptr, m.n_grid, m.stream);
+    if (mp) d2h(mp, m.mlp_params.ptr, m.n_mlp, m.stream);
+    if (sw) d2h(sw, m.skin.ptr, m.n_skin, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_model_set_params(arfx_model mh, const float* gp, const float* mp) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (gp) h2d(m.grid_params.ptr, gp, m.n_grid, m.stream);
+    if (mp) h2d(m.mlp_params.ptr, mp, m.n_mlp, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_model_zero_grad(arfx_model mh, void* stream) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    m.grid_grad.ensure(m.n_grid);
+    m.mlp_grad.ensure(m.n_mlp);
+    const cudaStream_t s = stream_of(m, stream);
+    ARFX_CUDA(cudaMemsetAsync(m.grid_grad.ptr, 0, m.n_grid * sizeof(float), s));
+    ARFX_CUDA(cudaMemsetAsync(m.mlp_grad.ptr, 0, m.n_mlp * sizeof(float), s));
+  });
+}
+
+int arfx_model_get_grads(arfx_model mh, float* gg, float* mg) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    require(m.grid_grad.ptr != nullptr, "no gradients accumulated yet (call arfx_model_zero_grad)");
+    if (gg) d2h(gg, m.grid_grad.ptr, m.n_grid, m.stream);
+    if (mg) d2h(mg, m.mlp_grad.ptr, m.n_mlp, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_model_device_arrays(arfx_model mh, float** gp, float** mp, float** gg, float** mg) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    m.grid_grad.ensure(m.n_grid);
+    m.mlp_grad.ensure(m.n_mlp);
+    if (gp) *gp = m.grid_params.ptr;
+    if (mp) *mp = m.mlp_params.ptr;
+    if (gg) *gg = m.grid_grad.ptr;
+    if (mg) *mg = m.mlp_grad.ptr;
+  });
+}
+
+int arfx_pose_create(arfx_model mh, const double* bones12, const double* global12, arfx_pose* out) {
+  return guard([&] {
+    require(mh != nullptr && out != nullptr, "pose_create: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    auto p = std::make_unique<arfx_pose_s>();
+    p->impl.model = &m;
+    make_pose_host(m, bones12, global12, p->impl.host);
+    p->impl.dev.alloc(1);
+    ARFX_CUDA(cudaMemcpyAsync(p->impl.dev.ptr, &p->impl.host, sizeof(PoseCtx), cudaMemcpyHostToDevice, m.stream));
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    *out = p.release();
+  });
+}
+
+int arfx_pose_create_context(arfx_model mh, const double* bones12, const double* pre12, double cutoff,
+                             arfx_pose* out) {
+  return guard([&] {
+    require(mh != nullptr && out != nullptr, "pose_create_context: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    auto p = std::make_unique<arfx_pose_s>();
+    p->impl.model = &m;
+    make_pose_ctx(m.bones, bones12, pre12, cutoff, p->impl.host);
+    p->impl.dev.alloc(1);
+    ARFX_CUDA(cudaMemcpyAsync(p->impl.dev.ptr, &p->impl.host, sizeof(PoseCtx), cudaMemcpyHostToDevice, m.stream));
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    *out = p.release();
+  });
+}
+
+int arfx_pose_update(arfx_pose ph, const double* bones12, const double* global12, void* stream) {
+  return guard([&] {
+    require(ph != nullptr, "pose_update: null pose");
+    PoseImpl& p = ph->impl;
+    ModelImpl& m = *p.model;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    make_pose_host(m, bones12, global12, p.host);
+    ARFX_CUDA(cudaMemcpyAsync(p.dev.ptr, &p.host, sizeof(PoseCtx), cudaMemcpyHostToDevice, s));
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_pose_destroy(arfx_pose p) {
+  return guard([&] { delete p; });
+}
+
+// OccupancyGrid::empty  R/occupancy.hpp:59-69
+int arfx_occ_create(const double lo[3], const double hi[3], const arfx_occ_config* cfg, arfx_occ_grid* out) {
+  return guard([&] {
+    require(cfg && out && lo && hi, "occ_create: null argument");
+    validate_occ_cfg(cfg->resolution, cfg->alpha_threshold, cfg->dilation, cfg->decay, cfg->update_interval);
+    require_device();
+    auto g = std::make_unique<arfx_occ_s>();
+    OccImpl& o = g->impl;
+    ARFX_CUDA(cudaGetDevice(&o.device));
+    o.res = cfg->resolution;
+    o.box = HostBox{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+    o.dilation = cfg->dilation;
+    o.threshold = occupancy_threshold(o.box, o.res, cfg->alpha_threshold);
+    const size_t n = static_cast<size_t>(o.res) * o.res * o.res;
+    o.values.alloc(n);
+    o.mask.alloc(n);
+    ARFX_CUDA(cudaMemset(o.values.ptr, 0, n * sizeof(float)));
+    ARFX_CUDA(cudaMemset(o.mask.ptr, 0, n));
+    *out = g.release();
+  });
+}
+
+int arfx_occ_destroy(arfx_occ_grid g) {
+  return guard([&] { delete g; });
+}
+
+int arfx_occ_info(arfx_occ_grid gh, int res[3], double lo[3], double hi[3], double* thr, int* dil) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    if (res) res[0] = res[1] = res[2] = g.res;
+    if (lo) {
+      lo[0] = g.box.lo.x;
+      lo[1] = g.box.lo.y;
+      lo[2] = g.box.lo.z;
+    }
+    if (hi) {
+      hi[0] = g.box.hi.x;
+      hi[1] = g.box.hi.y;
+      hi[2] = g.box.hi.z;
+    }
+    if (thr) *thr = g.threshold;
+    if (dil) *dil = g.dilation;
+  });
+}
+
+int arfx_occ_download(arfx_occ_grid gh, float* values, uint8_t* mask) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    ARFX_CUDA(cudaSetDevice(g.device));
+    ARFX_CUDA(cudaDeviceSynchronize());
+    const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
+    if (values) ARFX_CUDA(cudaMemcpy(values, g.values.ptr, n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (mask) ARFX_CUDA(cudaMemcpy(mask, g.mask.ptr, n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int arfx_occ_upload(arfx_occ_grid gh, const float* values, const uint8_t* mask) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    ARFX_CUDA(cudaSetDevice(g.device));
+    const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
+    if (values) ARFX_CUDA(cudaMemcpy(g.values.ptr, values, n * sizeof(float), cudaMemcpyHostToDevice));
+    if (mask) ARFX_CUDA(cudaMemcpy(g.mask.ptr, mask, n, cudaMemcpyHostToDevice));
+  });
+}
+
+int arfx_occ_rebuild_mask(arfx_occ_grid gh, void* stream) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    ARFX_CUDA(cudaSetDevice(g.device));
+    occ_rebuild(g, static_cast<cudaStream_t>(stream));
+    ARFX_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int arfx_build_inference_grid(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, arfx_counters* c, void* stream) {
+  return guard([&] {
+    require(mh && ph, "build_inference_grid: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
+      unsigned long long hc[4];
+      d2h(hc, m.ws.counters.ptr, 4, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hc, rerun);
+      if (rerun) continue;
+      if (c) {
+        c->posed_queries = hc[0] ? hc[0] : static_cast<uint64_t>(occ_ref(gh).res) * occ_ref(gh).res * occ_ref(gh).res;
+        c->canonical_queries = hc[1];
+      }
+      return;
+    }
+    throw std::runtime_error("build_inference_grid: workspace overflow persisted");
+  });
+}
+
+int arfx_build_inference_grid_device(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, uint64_t* d_counters,
+                                     void* stream) {
+  return guard([&] {
+    require(mh && ph, "build_inference_grid_device: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    inference_grid(m, ph->impl, occ_ref(gh), reinterpret_cast<unsigned long long*>(d_counters),
+                   stream_of(m, stream));
+  });
+}
+
+int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses, double decay,
+                              uint64_t seed, uint64_t step, arfx_occ_grid gh, arfx_counters* c, void* stream) {
+  return guard([&] {
+    require(mh && poses && n_poses >= 1, "update_training_grid: need >= 1 pose");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    std::vector<PoseImpl*> ps;
+    for (int i = 0; i < n_poses; ++i) {
+      require(poses[i] != nullptr, "update_training_grid: null pose");
+      ps.push_back(&poses[i]->impl);
+    }
+    OccImpl& g = occ_ref(gh);
+    const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
+    DevBuf<float> saved;  // values are updated in place: keep a copy for overflow reruns
+    saved.alloc(n);
+    ARFX_CUDA(cudaMemcpyAsync(saved.ptr, g.values.ptr, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      if (attempt)
+        ARFX_CUDA(cudaMemcpyAsync(g.values.ptr, saved.ptr, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      training_grid_update(m, ps, decay, seed, step, g, nullptr, s);
+      unsigned long long hc[4];
+      d2h(hc, m.ws.counters.ptr, 4, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hc, rerun);
+      if (rerun) continue;
+      if (c) {
+        c->posed_queries = n;
+        c->canonical_queries = hc[1];
+      }
+      return;
+    }
+    throw std::runtime_error("update_training_grid: workspace overflow persisted");
+  });
+}
+
+
+int arfx_render_model_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                             const arfx_render_options* opt, int shard, int nshards, float* d_rgb,
+                             float* d_alpha, uint64_t* d_counters, void* stream) {
+  return guard([&] {
+    require(mh && ph && d_rgb && d_alpha, "render_model_device: null argument");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+                 opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha,
+                 reinterpret_cast<unsigned long long*>(d_counters), stream_of(m, stream));
+  });
+}
+
+int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                      const arfx_render_options* opt, int shard, int nshards, float* rgb, float* alpha,
+                      arfx_counters* c, void* stream) {
+  return guard([&] {
+    require(mh && ph && rgb && alpha, "render_model: null argument");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    if (!t_rb) t_rb = std::make_unique<RenderBuffers>();
+    const size_t npix = static_cast<size_t>(hc.width) * hc.height;
+    t_rb->rgb.ensure(npix * 3);
+    t_rb->alpha.ensure(npix);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+                   opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, t_rb->rgb.ptr,
+                   t_rb->alpha.ptr, nullptr, s);
+      unsigned long long hcnt[4];
+      d2h(hcnt, m.ws.counters.ptr, 4, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hcnt, rerun);
+      if (rerun) continue;
+      // copy this shard's row tiles (other shards' rows are left untouched)
+      const int W = hc.width;
+      for (int y0 = 0; y0 < hc.height; y0 += 16) {
+        if ((y0 / 16) % nshards != shard) continue;
+        const int rows = std::min(16, hc.height - y0);
+        const size_t off = static_cast<size_t>(y0) * W;
+        d2h(rgb + off * 3, t_rb->rgb.ptr + off * 3, static_cast<size_t>(rows) * W * 3, s);
+        d2h(alpha + off, t_rb->alpha.ptr + off, static_cast<size_t>(rows) * W, s);
+      }
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      if (c) {
+        c->posed_queries = hcnt[0];
+        c->canonical_queries = hcnt[1];
+      }
+      return;
+    }
+    throw std::runtime_error("render_model: workspace overflow persisted");
+  });
+}
+
+int arfx_render_trace(arfx_model mh, int64_t capacity, int64_t* n_samples, int32_t* s_ray, int32_t* s_index,
+                      uint8_t* s_has_root, float* s_density, float* s_color, double* s_canonical,
+                      double* s_delta) {
+  return guard([&] {
+    require(mh && n_samples, "render_trace: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    Workspace& w = m.ws;
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    ARFX_CUDA(cudaDeviceSynchronize());
+    unsigned long long hc[4];
+    ARFX_CUDA(cudaMemcpy(hc, w.counters.ptr, sizeof(hc), cudaMemcpyDeviceToHost));
+    const int64_t n = static_cast<int64_t>(std::min<unsigned long long>(hc[0], w.cap_posed));
+    *n_samples = n;
+    if (capacity < n) return;
+    std::vector<int16_t> idx(static_cast<size_t>(n));
+    std::vector<uint8_t> nroot(static_cast<size_t>(n));
+    std::vector<int32_t> base(static_cast<size_t>(n));
+    std::vector<int8_t> sel(static_cast<size_t>(n));
+    const size_t np = static_cast<size_t>(std::min<unsigned long long>(hc[2], w.cap_pool));
+    std::vector<float4> pres(np);
+    std::vector<double> px(np), py(np), pz(np);
+    ARFX_CUDA(cudaMemcpy(s_ray, w.sray.ptr, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(idx.data(), w.sidx.ptr, static_cast<size_t>(n) * 2, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(nroot.data(), w.snroot.ptr, static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(base.data(), w.sbase.ptr, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(sel.data(), w.ssel.ptr, static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(s_delta, w.sdelta.ptr, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(pres.data(), w.pres.ptr, np * sizeof(float4), cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(px.data(), w.px.ptr, np * 8, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(py.data(), w.py.ptr, np * 8, cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemcpy(pz.data(), w.pz.ptr, np * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) {
+      s_index[i] = idx[static_cast<size_t>(i)];
+      const int k = sel[static_cast<size_t>(i)];
+      const bool has = nroot[static_cast<size_t>(i)] > 0 && k >= 0;
+      s_has_root[i] = has ? 1 : 0;
+      const size_t p = has ? static_cast<size_t>(base[static_cast<size_t>(i)] + k) : 0;
+      s_density[i] = has ? pres[p].x : 0.f;
+      s_color[3 * i + 0] = has ? pres[p].y : 0.f;
+      s_color[3 * i + 1] = has ? pres[p].z : 0.f;
+      s_color[3 * i + 2] = has ? pres[p].w : 0.f;
+      s_canonical[3 * i + 0] = has ? px[p] : 0.0;
+      s_canonical[3 * i + 1] = has ? py[p] : 0.0;
+      s_canonical[3 * i + 2] = has ? pz[p] : 0.0;
+    }
+  });
+}
+
+int arfx_profile_enable(arfx_model mh, int on) {
+  return guard([&] {
+    require(mh != nullptr, "profile_enable: null model");
+    mh->impl.prof.on = on != 0;
+  });
+}
+
+int arfx_profile_read(arfx_model mh, int max, char* names, double* ms, int64_t* launches, int* n) {
+  return guard([&] {
+    require(mh != nullptr && n != nullptr, "profile_read: null argument");
+    KernelProfiler& p = mh->impl.prof;
+    ARFX_CUDA(cudaSetDevice(mh->impl.device));
+    p.collect();
+    int k = 0;
+    for (; k < static_cast<int>(p.names.size()) && k < max; ++k) {
+      std::strncpy(names + 32 * k, p.names[static_cast<size_t>(k)].c_str(), 31);
+      names[32 * k + 31] = 0;
+      ms[k] = p.ms[static_cast<size_t>(k)];
+      launches[k] = p.launches[static_cast<size_t>(k)];
+    }
+    *n = k;
+    p.names.clear();
+    p.ms.clear();
+    p.launches.clear();
+  });
+}
+
+// ---- batched helpers ------------------------------------------------------
+
+
+int arfx_skinning_weights(arfx_model mh, const double* pts, int64_t n, double* w) {
+  return guard([&] {
+    require(mh && (n == 0 || (pts && w)), "skinning_weights: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    Staged<double> P, Wd;
+    P.up(pts, static_cast<size_t>(3 * n), m.stream);
+    Wd.d.alloc(static_cast<size_t>(n) * m.bones.size());
+    skin_weights_batch(m, P.d.ptr, n, Wd.d.ptr, m.stream);
+    d2h(w, Wd.d.ptr, static_cast<size_t>(n) * m.bones.size(), m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_inverse_lbs_device(arfx_model mh, arfx_pose ph, const double* d_pts, int64_t n, int32_t* d_counts,
+                            double* d_roots, double* d_res, void* stream) {
+  return guard([&] {
+    require(mh && ph, "inverse_lbs_device: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    inverse_lbs_batch(m, ph->impl.dev.ptr, d_pts, n, d_counts, d_roots, d_res, stream_of(m, stream));
+  });
+}
+
+int arfx_inverse_lbs(arfx_model mh, const double* bones12, const double* pre12, double cutoff,
+                     const double* pts, int64_t n, int32_t* counts, double* roots, double* residuals) {
+  return guard([&] {
+    require(mh && bones12 && pre12 && (n == 0 || (pts && counts && roots && residuals)),
+            "inverse_lbs: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    PoseCtx ctx;
+    make_pose_ctx(m.bones, bones12, pre12, cutoff, ctx);
+    DevBuf<PoseCtx> dctx;
+    dctx.alloc(1);
+    h2d(dctx.ptr, &ctx, 1, m.stream);
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), m.stream);
+    DevBuf<int32_t> dc;
+    DevBuf<double> dr, ds;
+    dc.alloc(static_cast<size_t>(n));
+    dr.alloc(static_cast<size_t>(n) * kMaxRoots * 3);
+    ds.alloc(static_cast<size_t>(n) * kMaxRoots);
+    inverse_lbs_batch(m, dctx.ptr, P.d.ptr, n, dc.ptr, dr.ptr, ds.ptr, m.stream);
+    d2h(counts, dc.ptr, static_cast<size_t>(n), m.stream);
+    d2h(roots, dr.ptr, static_cast<size_t>(n) * kMaxRoots * 3, m.stream);
+    d2h(residuals, ds.ptr, static_cast<size_t>(n) * kMaxRoots, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_hash_encode(arfx_model mh, const double* pts, int64_t n, float* feats) {
+  return guard([&] {
+    require(mh && (n == 0 || (pts && feats)), "hash_encode: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    const size_t D = static_cast<size_t>(m.grid.levels) * m.grid.F;
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), m.stream);
+    DevBuf<float> f;
+    f.alloc(static_cast<size_t>(n) * D);
+    DevBuf<int> err;
+    err.alloc(1);
+    ARFX_CUDA(cudaMemsetAsync(err.ptr, 0, sizeof(int), m.stream));
+    hash_encode_batch(m, P.d.ptr, n, f.ptr, err.ptr, m.stream);
+    int herr = 0;
+    d2h(&herr, err.ptr, 1, m.stream);
+    d2h(feats, f.ptr, static_cast<size_t>(n) * D, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    if (herr) throw std::domain_error("hash grid: point outside bounding box");
+  });
+}
+
+int arfx_field_query(arfx_model mh, const double* pts, int64_t n, float* dens, float* col) {
+  return guard([&] {
+    require(mh && (n == 0 || (pts && dens && col)), "field_query: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), m.stream);
+    DevBuf<float4> o;
+    o.alloc(static_cast<size_t>(n));
+    DevBuf<int> err;
+    err.alloc(1);
+    ARFX_CUDA(cudaMemsetAsync(err.ptr, 0, sizeof(int), m.stream));
+    field_query_batch(m, P.d.ptr, n, o.ptr, err.ptr, m.stream);
+    std::vector<float4> h(static_cast<size_t>(n));
+    int herr = 0;
+    d2h(&herr, err.ptr, 1, m.stream);
+    d2h(h.data(), o.ptr, static_cast<size_t>(n), m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    if (herr) throw std::domain_error("hash grid: point outside bounding box");
+    for (int64_t i = 0; i < n; ++i) {
+      dens[i] = h[static_cast<size_t>(i)].x;
+      col[3 * i + 0] = h[static_cast<size_t>(i)].y;
+      col[3 * i + 1] = h[static_cast<size_t>(i)].z;
+      col[3 * i + 2] = h[static_cast<size_t>(i)].w;
+    }
+  });
+}
+
+int arfx_posed_query(arfx_model mh, arfx_pose ph, const double* pts, int64_t n, float* dens, float* col,
+                     double* canon, uint8_t* has, arfx_counters* c) {
+  return guard([&] {
+    require(mh && ph && (n == 0 || (pts && dens && col && canon && has)), "posed_query: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), m.stream);
+    DevBuf<float> dd, dcl;
+    DevBuf<double> dcan;
+    DevBuf<uint8_t> dh;
+    dd.alloc(static_cast<size_t>(n));
+    dcl.alloc(static_cast<size_t>(3 * n));
+    dcan.alloc(static_cast<size_t>(3 * n));
+    dh.alloc(static_cast<size_t>(n));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      posed_query_batch(m, ph->impl, P.d.ptr, n, dd.ptr, dcl.ptr, dcan.ptr, dh.ptr, nullptr, m.stream);
+      unsigned long long hc[4];
+      d2h(hc, m.ws.counters.ptr, 4, m.stream);
+      ARFX_CUDA(cudaStreamSynchronize(m.stream));
+      bool rerun;
+      check_overflow_and_grow(m, hc, rerun);
+      if (rerun) continue;
+      d2h(dens, dd.ptr, static_cast<size_t>(n), m.stream);
+      d2h(col, dcl.ptr, static_cast<size_t>(3 * n), m.stream);
+      d2h(canon, dcan.ptr, static_cast<size_t>(3 * n), m.stream);
+      d2h(has, dh.ptr, static_cast<size_t>(n), m.stream);
+      ARFX_CUDA(cudaStreamSynchronize(m.stream));
+      if (c) {
+        c->posed_queries = static_cast<uint64_t>(n);
+        c->canonical_queries = hc[1];
+      }
+      return;
+    }
+    throw std::runtime_error("posed_query: workspace overflow persisted");
+  });
+}
+
+
+int arfx_composite(int n_rays, const int32_t* ray_len, const double* t, const double* delta,
+                   const uint8_t* skipped, const float* density, const float* color, double eps,
+                   double* out_c3, double* out_a, int32_t* term) {
+  return guard([&] {
+    require(n_rays >= 0, "composite: negative ray count");
+    if (n_rays == 0) return;
+    require_device();
+    (void)t;
+    std::vector<int64_t> off;
+    ray_offsets(n_rays, ray_len, off);
+    const size_t ns = static_cast<size_t>(off.back());
+    cudaStream_t s = nullptr;
+    Staged<int64_t> O;
+    O.up(off.data(), off.size(), s);
+    Staged<double> D;
+    Staged<uint8_t> K;
+    Staged<float> De, Co;
+    D.up(delta, ns, s);
+    K.up(skipped, ns, s);
+    De.up(density, ns, s);
+    Co.up(color, 3 * ns, s);
+    DevBuf<double> c3, a;
+    DevBuf<int32_t> tm;
+    c3.alloc(3 * static_cast<size_t>(n_rays));
+    a.alloc(static_cast<size_t>(n_rays));
+    tm.alloc(static_cast<size_t>(n_rays));
+    composite_explicit(n_rays, O.d.ptr, D.d.ptr, K.d.ptr, De.d.ptr, Co.d.ptr, eps, c3.ptr, a.ptr, tm.ptr, s);
+    d2h(out_c3, c3.ptr, 3 * static_cast<size_t>(n_rays), s);
+    d2h(out_a, a.ptr, static_cast<size_t>(n_rays), s);
+    d2h(term, tm.ptr, static_cast<size_t>(n_rays), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_composite_backward(int n_rays, const int32_t* ray_len, const double* t, const double* delta,
+                            const uint8_t* skipped, const float* density, const float* color, double eps,
+                            const double* dC3, const double* dA, double* d_sigma, double* d_c3) {
+  return guard([&] {
+    require(n_rays >= 0, "composite_backward: negative ray count");
+    if (n_rays == 0) return;
+    require_device();
+    (void)t;
+    std::vector<int64_t> off;
+    ray_offsets(n_rays, ray_len, off);
+    const size_t ns = static_cast<size_t>(off.back());
+    cudaStream_t s = nullptr;
+    Staged<int64_t> O;
+    O.up(off.data(), off.size(), s);
+    Staged<double> D, DC, DA;
+    Staged<uint8_t> K;
+    Staged<float> De, Co;
+    D.up(delta, ns, s);
+    K.up(skipped, ns, s);
+    De.up(density, ns, s);
+    Co.up(color, 3 * ns, s);
+    DC.up(dC3, 3 * static_cast<size_t>(n_rays), s);
+    DA.up(dA, static_cast<size_t>(n_rays), s);
+    DevBuf<double> tr, ds, dc;
+    tr.alloc(ns + 1);
+    ds.alloc(ns + 1);
+    dc.alloc(3 * ns + 3);
+    composite_backward_explicit(n_rays, O.d.ptr, D.d.ptr, K.d.ptr, De.d.ptr, Co.d.ptr, eps, DC.d.ptr, DA.d.ptr,
+                                tr.ptr, ds.ptr, dc.ptr, s);
+    d2h(d_sigma, ds.ptr, ns, s);
+    d2h(d_c3, dc.ptr, 3 * ns, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_field_query_backward(arfx_model mh, const double* pts, int64_t n, const float* d_density,
+                              const float* d_color) {
+  return guard([&] {
+    (void)mh;
+    (void)pts;
+    (void)n;
+    (void)d_density;
+    (void)d_color;
+    throw std::runtime_error("arfx_field_query_backward: not built yet in this revision");
+  });
+}
+
+int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                       const arfx_render_options* opt, int64_t n_rays, const int32_t* px, const int32_t* py,
+                       const float* d_color, const float* d_alpha, float* rgb, float* alpha, arfx_counters* c,
+                       void* stream) {
+  return guard([&] {
+    (void)mh, (void)ph, (void)cam, (void)occ, (void)opt, (void)n_rays, (void)px, (void)py;
+    (void)d_color, (void)d_alpha, (void)rgb, (void)alpha, (void)c, (void)stream;
+    throw std::runtime_error("arfx_train_fwd_bwd: not built yet in this revision");
+  });
+}
+
+}  // extern "C"

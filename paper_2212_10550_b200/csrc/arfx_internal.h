@@ -1,0 +1,81 @@
+// arfx_internal.h -- plain structs shared by the host runtime (host.cpp, abi.cu)
+// and the sm_100a kernels. Layouts follow the reference's containers so the
+// C-ABI can upload/download them without reshaping (SURVEY.md §8b "Ownership"):
+//   hash grid  [L][2^T][F] f32          R/hash_grid.hpp:62
+//   MLP        per layer W[out][in], b  R/mlp.hpp:40-48
+//   skinning   [z][y][x][bone] f64      R/skinning.hpp:16
+//   occupancy  [z][y][x] f32 + u8       R/occupancy.hpp:42-48
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace arfx {
+
+constexpr int kMaxBones = 32;   // R/articulation.hpp:10
+constexpr int kMaxRoots = 8;    // R/articulation.hpp:11
+constexpr int kMaxLevels = 32;
+constexpr int kMaxMlpLayers = 9;  // hidden_layers <= 8 (R/mlp.hpp:17) + output layer
+
+enum LevelKind : int { kDirect = 0, kWrap = 1, kHashed = 2 };  // R/hash_grid.hpp:87-101
+
+// Canonical field (HashGrid + DecoderMlp), device pointers.
+struct FieldView {
+  int L, F, log2T;
+  uint32_t T;
+  int res[kMaxLevels];
+  int kind[kMaxLevels];
+  double lo[3], hi[3], e[3];  // bounding box, e = hi - lo (Aabb::extent)
+  const float* grid;          // [L][T][F]
+  int n_layers;               // hidden_layers + 1
+  int lin[kMaxMlpLayers], lout[kMaxMlpLayers];
+  int w_off[kMaxMlpLayers], b_off[kMaxMlpLayers];
+  int in_dim, hidden, out_dim, n_mlp;
+  const float* mlp;
+};
+
+// SkinningGrid (R/skinning.hpp:12-56) plus the per-cell packed table the deformer
+// reads: for cell c, the bones with a nonzero node weight at any of its 8 corners
+// (bitmask, ascending bone order) and, per such bone, the 8 corner node weights in
+// corner order k = 0..7 (k bit0 = x, bit1 = y, bit2 = z).
+struct SkinView {
+  int rx, ry, rz, nb;
+  double lo[3], hi[3], e[3];
+  const double* weights;     // [z][y][x][bone]
+  const uint32_t* cell_mask; // [(rz-1)(ry-1)(rx-1)]
+  const uint32_t* cell_off;  // offset into cell_vals in units of 8 doubles
+  const double* cell_vals;
+};
+
+// PoseContext (R/articulation.hpp:17-42) + world->normalized rigid (R/model.hpp:85-98).
+// Rigid = R row-major (9) then t (3).
+struct PoseCtx {
+  int nb;
+  int pad_;
+  double bone[kMaxBones][12];
+  double bone_inv[kMaxBones][12];
+  double cap_a[kMaxBones][3];
+  double cap_b[kMaxBones][3];
+  double cutoff[kMaxBones];
+  double w2n[12];
+};
+
+struct InverseOpts {  // R/articulation.hpp:84-88
+  int max_iterations;
+  double tolerance;
+  double dedup_radius;
+};
+
+struct OccView {
+  int rx, ry, rz;
+  double lo[3], hi[3], e[3];
+  const uint8_t* mask;
+};
+
+struct CameraView {  // R/camera.hpp:9-13
+  double fx, fy, cx, cy;
+  int width, height;
+  double ext[12];
+};
+
+}  // namespace arfx

@@ -1,0 +1,235 @@
+// deform.cuh -- Fast-SNARF correspondence search on sm_100a, bit-exact FP64.
+//
+// Restates, per posed point x':
+//   SkinningGrid::interpolate   R/skinning.hpp:25-55
+//   lbs_apply                   R/articulation.hpp:45-50
+//   inverse_lbs_ctx             R/articulation.hpp:94-145 (damped Newton, frozen
+//                               Jacobian J = sum w_i R_i, 4-step halving line search,
+//                               stall break, <= max_iterations)
+//   InverseRoots::push          R/articulation.hpp:66-81
+//
+// B200 layout: the skinning grid is read through a per-cell packed table (see
+// SkinView): one 32-bit mask of the bones that are nonzero at any of the cell's 8
+// corners, then 8 contiguous doubles per such bone -> one eval touches ~6 bones x
+// 64 B contiguous instead of 8 corners x n_bones x 8 B scattered. Skipping bones
+// that are zero at every corner is exact (adding +0.0 to a non-negative sum is the
+// identity). The lbs sum and the Jacobian are accumulated in
+// the same pass over the union bones, so the Jacobian of the accepted line-search
+// candidate is ready for the next iteration (the reference recomputes it from the
+// same weights, R/articulation.hpp:110-112 -- identical operand order).
+#pragma once
+
+#include "arfx_internal.h"
+#include "exact.cuh"
+
+namespace arfx {
+
+struct Roots {
+  int count;
+  double x[kMaxRoots][3];
+  double r[kMaxRoots];
+};
+
+// R/articulation.hpp:66-81
+__device__ __forceinline__ void roots_push(Roots& R, d3 p, double res, double dedup) {
+  for (int i = 0; i < R.count; ++i) {
+    const d3 q = make3(R.x[i][0], R.x[i][1], R.x[i][2]);
+    if (norm3(sub3(q, p)) < dedup) {
+      if (res < R.r[i]) {
+        R.x[i][0] = p.x;
+        R.x[i][1] = p.y;
+        R.x[i][2] = p.z;
+        R.r[i] = res;
+      }
+      return;
+    }
+  }
+  if (R.count < kMaxRoots) {
+    R.x[R.count][0] = p.x;
+    R.x[R.count][1] = p.y;
+    R.x[R.count][2] = p.z;
+    R.r[R.count] = res;
+    ++R.count;
+  }
+}
+
+// Skinning weights at x (trilinear over the packed cell table + renormalisation),
+// then g = lbs(x) - x_target, |g| and J = sum_{w_i != 0} w_i R_i.
+// `ws` is per-thread scratch for the union bones' raw weights (smem, stride apart).
+__device__ __forceinline__ void skin_eval(const SkinView& S, const PoseCtx* __restrict__ P, d3 x,
+                                          d3 xt, double* ws, int stride, d3& g, double& gn,
+                                          double J[9]) {
+  // clamp_inside: cwise_max(lo, cwise_min(hi, x))  R/math.hpp:245-247
+  double p[3] = {x.x, x.y, x.z};
+  const int res[3] = {S.rx, S.ry, S.rz};
+  int c[3];
+  double f[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double v = (p[a] < S.hi[a]) ? p[a] : S.hi[a];
+    v = (S.lo[a] < v) ? v : S.lo[a];
+    const double u = dmul(ddiv(dsub(v, S.lo[a]), S.e[a]), static_cast<double>(res[a] - 1));
+    double fl = floor(u);
+    if (fl > static_cast<double>(res[a] - 2)) fl = static_cast<double>(res[a] - 2);
+    if (fl < 0) fl = 0;
+    c[a] = static_cast<int>(fl);
+    f[a] = dsub(u, fl);
+  }
+  double wt[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double wx = (k & 1) ? f[0] : dsub(1.0, f[0]);
+    const double wy = (k & 2) ? f[1] : dsub(1.0, f[1]);
+    const double wz = (k & 4) ? f[2] : dsub(1.0, f[2]);
+    wt[k] = dmul(dmul(wx, wy), wz);
+  }
+  const int cell = (c[2] * (S.ry - 1) + c[1]) * (S.rx - 1) + c[0];
+  const uint32_t mask = __ldg(S.cell_mask + cell);
+  const double* vals = S.cell_vals + static_cast<size_t>(__ldg(S.cell_off + cell)) * 8;
+  // pass 1: raw interpolated weights per union bone, and their sum (bone order)
+  double sum = 0.0;
+  int j = 0;
+  for (uint32_t m = mask; m; m &= m - 1, ++j) {
+    const double2* v2 = reinterpret_cast<const double2*>(vals + 8 * j);
+    const double2 a0 = __ldg(v2 + 0), a1 = __ldg(v2 + 1), a2 = __ldg(v2 + 2), a3 = __ldg(v2 + 3);
+    const double v[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (wt[k] != 0.0) acc = dadd(acc, dmul(wt[k], v[k]));
+    ws[j * stride] = acc;
+    sum = dadd(sum, acc);
+  }
+  const bool renorm = sum > 0;
+  const double inv = renorm ? ddiv(1.0, sum) : 1.0;
+  // pass 2: normalised weights -> lbs and Jacobian
+  d3 out = make3(0.0, 0.0, 0.0);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) J[e] = 0.0;
+  j = 0;
+  for (uint32_t m = mask; m; m &= m - 1, ++j) {
+    const int b = __ffs(m) - 1;
+    double w = ws[j * stride];
+    if (renorm) w = dmul(w, inv);
+    if (w != 0.0) {
+      const double* T = P->bone[b];
+      const d3 a = rigid_apply(T, x);
+      out = add3(out, mul3(a, w));
+#pragma unroll
+      for (int e = 0; e < 9; ++e) J[e] = dadd(J[e], dmul(T[e], w));
+    }
+  }
+  g = sub3(out, xt);
+  gn = norm3(g);
+}
+
+// Skinning weights only (SkinningGrid::interpolate), dense output over n_bones.
+__device__ __forceinline__ void skin_weights_dense(const SkinView& S, d3 x, double* w_out) {
+  double p[3] = {x.x, x.y, x.z};
+  const int res[3] = {S.rx, S.ry, S.rz};
+  int c[3];
+  double f[3];
+  for (int a = 0; a < 3; ++a) {
+    double v = (p[a] < S.hi[a]) ? p[a] : S.hi[a];
+    v = (S.lo[a] < v) ? v : S.lo[a];
+    const double u = dmul(ddiv(dsub(v, S.lo[a]), S.e[a]), static_cast<double>(res[a] - 1));
+    double fl = floor(u);
+    if (fl > static_cast<double>(res[a] - 2)) fl = static_cast<double>(res[a] - 2);
+    if (fl < 0) fl = 0;
+    c[a] = static_cast<int>(fl);
+    f[a] = dsub(u, fl);
+  }
+  for (int i = 0; i < S.nb; ++i) w_out[i] = 0.0;
+  for (int k = 0; k < 8; ++k) {
+    const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+    const double wt = dmul(dmul(dx ? f[0] : dsub(1.0, f[0]), dy ? f[1] : dsub(1.0, f[1])),
+                           dz ? f[2] : dsub(1.0, f[2]));
+    if (wt == 0.0) continue;
+    const double* nw =
+        S.weights + ((static_cast<size_t>(c[2] + dz) * S.ry + (c[1] + dy)) * S.rx + (c[0] + dx)) * S.nb;
+    for (int i = 0; i < S.nb; ++i) w_out[i] = dadd(w_out[i], dmul(wt, nw[i]));
+  }
+  double sum = 0.0;
+  for (int i = 0; i < S.nb; ++i) sum = dadd(sum, w_out[i]);
+  if (sum > 0) {
+    const double inv = ddiv(1.0, sum);
+    for (int i = 0; i < S.nb; ++i) w_out[i] = dmul(w_out[i], inv);
+  }
+}
+
+// One start of inverse_lbs_ctx (R/articulation.hpp:103-142). Returns true when the
+// start converged; x / gn hold the root and its residual.
+__device__ __forceinline__ bool newton_start(const SkinView& S, const PoseCtx* __restrict__ P,
+                                             const InverseOpts& opt, int b, d3 xt, double* ws,
+                                             int stride, d3& x, double& gn) {
+  x = rigid_apply(P->bone_inv[b], xt);
+  d3 g;
+  double J[9];
+  skin_eval(S, P, x, xt, ws, stride, g, gn, J);
+  bool converged = gn < opt.tolerance;
+  for (int it = 0; it < opt.max_iterations && !converged; ++it) {
+    // Mat3::inverse  R/math.hpp:141-158 (singular -> abandon start, :114-118)
+    const double* m = J;
+    const double c0 = dsub(dmul(m[4], m[8]), dmul(m[5], m[7]));
+    const double c1 = dsub(dmul(m[3], m[8]), dmul(m[5], m[6]));
+    const double c2 = dsub(dmul(m[3], m[7]), dmul(m[4], m[6]));
+    const double det = dadd(dsub(dmul(m[0], c0), dmul(m[1], c1)), dmul(m[2], c2));
+    if (fabs(det) < 2.2250738585072014e-308 * 64) break;
+    const double id = ddiv(1.0, det);
+    double inv[9];
+    inv[0] = dmul(c0, id);
+    inv[1] = dmul(dsub(dmul(m[2], m[7]), dmul(m[1], m[8])), id);
+    inv[2] = dmul(dsub(dmul(m[1], m[5]), dmul(m[2], m[4])), id);
+    inv[3] = dmul(dsub(dmul(m[5], m[6]), dmul(m[3], m[8])), id);
+    inv[4] = dmul(dsub(dmul(m[0], m[8]), dmul(m[2], m[6])), id);
+    inv[5] = dmul(dsub(dmul(m[2], m[3]), dmul(m[0], m[5])), id);
+    inv[6] = dmul(c2, id);
+    inv[7] = dmul(dsub(dmul(m[1], m[6]), dmul(m[0], m[7])), id);
+    inv[8] = dmul(dsub(dmul(m[0], m[4]), dmul(m[1], m[3])), id);
+    const d3 step = matvec(inv, g);
+    double damp = 1.0;
+    d3 xn = x, gnx = g;
+    double gnn = gn;
+    double Jn[9];
+    for (int h = 0; h < 4; ++h) {
+      const d3 cand = sub3(x, mul3(step, damp));
+      d3 gc;
+      double gcn, Jc[9];
+      skin_eval(S, P, cand, xt, ws, stride, gc, gcn, Jc);
+      if (gcn < gn || h == 3) {
+        xn = cand;
+        gnx = gc;
+        gnn = gcn;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Jn[e] = Jc[e];
+        break;
+      }
+      damp = dmul(damp, 0.5);
+    }
+    if (gnn >= gn && gn >= opt.tolerance) break;  // stalled
+    x = xn;
+    g = gnx;
+    gn = gnn;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) J[e] = Jn[e];
+    converged = gn < opt.tolerance;
+  }
+  return converged;
+}
+
+// inverse_lbs_ctx  R/articulation.hpp:94-145
+__device__ __forceinline__ void inverse_lbs(const SkinView& S, const PoseCtx* __restrict__ P,
+                                            const InverseOpts& opt, d3 xt, double* ws, int stride,
+                                            Roots& R) {
+  R.count = 0;
+  for (int b = 0; b < P->nb; ++b) {
+    const d3 ca = make3(P->cap_a[b][0], P->cap_a[b][1], P->cap_a[b][2]);
+    const d3 cb = make3(P->cap_b[b][0], P->cap_b[b][1], P->cap_b[b][2]);
+    if (point_segment_distance(xt, ca, cb) > P->cutoff[b]) continue;
+    d3 x;
+    double gn;
+    if (newton_start(S, P, opt, b, xt, ws, stride, x, gn)) roots_push(R, x, gn, opt.dedup_radius);
+  }
+}
+
+}  // namespace arfx

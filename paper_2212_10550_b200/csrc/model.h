@@ -1,0 +1,161 @@
+// model.h -- device-resident model / pose / occupancy objects behind the C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "arfx_internal.h"
+#include "host.h"
+
+namespace arfx {
+
+void cuda_check(cudaError_t e, const char* what);
+#define ARFX_CUDA(call) ::arfx::cuda_check((call), #call)
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {  // grow-only, contents not preserved
+    if (count <= n) return;
+    release();
+    if (count == 0) return;
+    ARFX_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    n = count;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count) ARFX_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    n = count;
+  }
+};
+
+// Render / query workspace: compacted posed-sample list, root pool, per-ray ranges.
+struct Workspace {
+  size_t cap_posed = 0, cap_pool = 0, n_pix = 0;
+  DevBuf<double> sx, sy, sz, sdelta;  // posed samples: normalized position, delta
+  DevBuf<int32_t> sray;               // pixel index
+  DevBuf<int16_t> sidx;               // sample index along the ray
+  DevBuf<uint8_t> snroot;             // in-box roots (<= 8)
+  DevBuf<int32_t> sbase;              // first pool entry of the sample
+  DevBuf<int8_t> ssel;                // selected root slot (-1 none)
+  DevBuf<double> px, py, pz;          // root pool (canonical positions)
+  DevBuf<int32_t> powner;             // owning sample (-1: value precomputed by deformer)
+  DevBuf<float4> pres;                // (density, r, g, b) per pool entry
+  DevBuf<int32_t> ray_first, ray_count, row_list;
+  DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
+  DevBuf<uint64_t> pcg_tab;            // stratified-jitter jump table (unused for now)
+  int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
+  void ensure(size_t posed, size_t pix);
+};
+
+// Optional per-kernel CUDA-event timing on the launching stream (bench / roofline).
+struct KernelProfiler {
+  bool on = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> free_events;
+  std::vector<std::string> names;
+  std::vector<double> ms;
+  std::vector<long long> launches;
+  cudaEvent_t take();
+  void begin(const char* name, cudaStream_t s);
+  void end(cudaStream_t s);
+  void collect();  // synchronises the recorded events and accumulates
+  ~KernelProfiler();
+};
+
+struct ModelImpl {
+  int device = 0;
+  KernelProfiler prof;
+  cudaStream_t stream = nullptr;
+  std::vector<HostBone> bones;
+  GridCfg grid{};
+  std::vector<int> res;
+  int mlp_in = 0, mlp_hidden = 0, mlp_hl = 0, mlp_out = 0;
+  MlpLayout mlp{};
+  int skin_res[3] = {0, 0, 0};
+  HostBox skin_box{}, canon{}, norm{};
+  InverseOpts inv{20, 1e-5, 1e-3};
+  size_t n_grid = 0, n_mlp = 0, n_skin = 0;
+  DevBuf<float> grid_params, mlp_params, grid_grad, mlp_grad;
+  DevBuf<double> skin;
+  DevBuf<uint32_t> cell_mask, cell_off;
+  DevBuf<double> cell_vals;
+  FieldView fv{};
+  SkinView sv{};
+  Workspace ws;
+  std::vector<uint8_t> overflow_note;
+  ~ModelImpl();
+  void refresh_views();
+};
+
+struct PoseImpl {
+  ModelImpl* model = nullptr;
+  PoseCtx host{};
+  DevBuf<PoseCtx> dev;
+};
+
+struct OccImpl {
+  int device = 0;
+  int res = 64;
+  HostBox box{};
+  double threshold = 0.0;
+  int dilation = 1;
+  DevBuf<float> values;
+  DevBuf<uint8_t> mask, tmp;
+  OccView view() const;
+};
+
+// model.cu
+void build_skinning_grid_dev(ModelImpl& m, double blend_factor);  // R/skinning.hpp:61-111
+void build_cell_table(ModelImpl& m);
+void init_params_dev(ModelImpl& m, uint64_t seed);  // R/hash_grid.hpp:66-73, R/mlp.hpp:50-58
+
+// render.cu
+void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N,
+                  bool stratified, double eps, uint64_t seed, uint64_t frame, int shard,
+                  int nshards, float* d_rgb, float* d_alpha, unsigned long long* d_counters,
+                  cudaStream_t s);
+void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d_counters,
+                    cudaStream_t s);
+void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,
+                          uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
+                          cudaStream_t s);
+void occ_rebuild(OccImpl& g, cudaStream_t s);
+void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
+                       int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s);
+void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n, float* d_dens,
+                       float* d_col, double* d_canon, uint8_t* d_has, unsigned long long* d_counters,
+                       cudaStream_t s);
+void field_query_batch(ModelImpl& m, const double* d_pts, int64_t n, float4* d_out, int* d_domain_err,
+                       cudaStream_t s);
+void hash_encode_batch(ModelImpl& m, const double* d_pts, int64_t n, float* d_feats,
+                       int* d_domain_err, cudaStream_t s);
+void skin_weights_batch(ModelImpl& m, const double* d_pts, int64_t n, double* d_w, cudaStream_t s);
+
+// composite.cu
+void composite_explicit(int n_rays, const int64_t* d_off, const double* d_delta, const uint8_t* d_skip,
+                        const float* d_dens, const float* d_col, double eps, double* d_c3, double* d_a,
+                        int32_t* d_term, cudaStream_t s);
+void composite_backward_explicit(int n_rays, const int64_t* d_off, const double* d_delta,
+                                 const uint8_t* d_skip, const float* d_dens, const float* d_col,
+                                 double eps, const double* d_dC3, const double* d_dA, double* d_trans,
+                                 double* d_sigma, double* d_c3, cudaStream_t s);
+
+}  // namespace arfx

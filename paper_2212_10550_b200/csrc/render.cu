@@ -1,0 +1,932 @@
+// render.cu -- the per-frame hot path on sm_100a (exact SIMT path).
+//
+//   K1 march_kernel     generate_ray + to_normalized + ray_box + sample_points +
+//                       is_occupied (R/camera.hpp:61-70, R/render.hpp:15-37, :67-86,
+//                       R/occupancy.hpp:71-85), one warp per ray, ballot/popc
+//                       compaction of the occupied samples, one atomic per 8 rays.
+//   K2 deform_kernel    inverse_lbs_ctx + in-box filter of posed_query_ctx
+//                       (R/articulation.hpp:94-145, :163-181), FP64 exact; appends
+//                       the in-box roots of each posed sample to a compact root pool.
+//   K3 field_kernel     CanonicalField::query over the root pool (R/field.hpp:75-82).
+//   K4 composite_kernel max-density root selection (R/articulation.hpp:174) then
+//                       composite (R/render.hpp:98-119), one thread per ray.
+//   K5 occupancy        build_inference_grid / update_training_grid / rebuild_mask /
+//                       dilated_mask (R/occupancy.hpp:87-171) reuse K2 + K3.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "deform.cuh"
+#include "field.cuh"
+#include "model.h"
+
+namespace arfx {
+
+namespace {
+
+constexpr int kMarchWarps = 8;
+constexpr int kMaxN = 1024;  // samples per ray handled by the march kernel
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+struct RayGeom {
+  d3 o, d;
+  double tn, tf;
+  bool valid;  // hit && tn < tf
+};
+
+// generate_ray + normalized-space slab test  (R/camera.hpp:61-70, R/render.hpp:190-196, :15-37)
+__device__ __forceinline__ RayGeom make_ray(const CameraView& cam, const double* w2n, const double* nlo,
+                                            const double* nhi, int px, int py) {
+  RayGeom R;
+  const double dcx = ddiv(dsub(dadd(static_cast<double>(px), 0.5), cam.cx), cam.fx);
+  const double dcy = ddiv(dsub(dadd(static_cast<double>(py), 0.5), cam.cy), cam.fy);
+  const double* e = cam.ext;
+  const double rt[9] = {e[0], e[3], e[6], e[1], e[4], e[7], e[2], e[5], e[8]};
+  const d3 ot = matvec(rt, make3(e[9], e[10], e[11]));
+  R.o = make3(-ot.x, -ot.y, -ot.z);
+  const d3 dr = matvec(rt, make3(dcx, dcy, 1.0));
+  const double n = norm3(dr);
+  R.d = make3(ddiv(dr.x, n), ddiv(dr.y, n), ddiv(dr.z, n));
+  const d3 on = rigid_apply(w2n, R.o);
+  const d3 dn = sub3(rigid_apply(w2n, add3(R.o, mul3(R.d, 1.0))), on);
+  double t0 = 0.0, t1 = 1.7976931348623157e308;
+  const double oo[3] = {on.x, on.y, on.z}, dd[3] = {dn.x, dn.y, dn.z};
+  bool hit = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (!hit) break;
+    const double o = oo[a], d = dd[a];
+    if (fabs(d) < 1e-300) {
+      if (o < nlo[a] || o > nhi[a]) hit = false;
+      continue;
+    }
+    double ta = ddiv(dsub(nlo[a], o), d);
+    double tb = ddiv(dsub(nhi[a], o), d);
+    if (ta > tb) {
+      const double t = ta;
+      ta = tb;
+      tb = t;
+    }
+    t0 = (t0 < ta) ? ta : t0;
+    t1 = (tb < t1) ? tb : t1;
+    if (t0 > t1) hit = false;
+  }
+  R.tn = t0;
+  R.tf = t1;
+  R.valid = hit && (t0 < t1);
+  return R;
+}
+
+// t_i = t_near + (i + jitter) * step  (R/render.hpp:79-83)
+__device__ __forceinline__ double sample_t(double tn, double step, int i, double jitter) {
+  return dadd(tn, dmul(dadd(static_cast<double>(i), jitter), step));
+}
+
+// OccupancyGrid::is_occupied  R/occupancy.hpp:71-85
+__device__ __forceinline__ bool occupied(const OccView& g, d3 x) {
+  const double u0 = ddiv(dsub(x.x, g.lo[0]), g.e[0]);
+  const double u1 = ddiv(dsub(x.y, g.lo[1]), g.e[1]);
+  const double u2 = ddiv(dsub(x.z, g.lo[2]), g.e[2]);
+  if (u0 < 0 || u1 < 0 || u2 < 0 || u0 >= 1 || u1 >= 1 || u2 >= 1) return false;
+  int cx = static_cast<int>(dmul(u0, static_cast<double>(g.rx)));
+  int cy = static_cast<int>(dmul(u1, static_cast<double>(g.ry)));
+  int cz = static_cast<int>(dmul(u2, static_cast<double>(g.rz)));
+  cx = (g.rx - 1 < cx) ? g.rx - 1 : cx;
+  cy = (g.ry - 1 < cy) ? g.ry - 1 : cy;
+  cz = (g.rz - 1 < cz) ? g.rz - 1 : cz;
+  return g.mask[(static_cast<size_t>(cz) * g.ry + cy) * g.rx + cx] != 0;
+}
+
+struct MarchArgs {
+  CameraView cam;
+  double w2n[12];
+  double nlo[3], nhi[3];
+  OccView occ;
+  int has_occ;
+  int N, stratified;
+  uint64_t seed, frame;
+  const int32_t* rows;
+  int n_rows, W;
+  double *sx, *sy, *sz, *sdelta;
+  int32_t* sray;
+  int16_t* sidx;
+  int32_t *ray_first, *ray_count;
+  unsigned long long* counters;
+  long long cap;
+};
+
+__device__ __forceinline__ double jitter_at(const MarchArgs& A, Pcg32 base, int i) {
+  if (!A.stratified) return 0.5;
+  pcg_advance(base, static_cast<uint64_t>(i));
+  return pcg_double(base);
+}
+
+__global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
+  __shared__ unsigned bal[kMarchWarps][kMaxN / 32];
+  __shared__ int wcount[kMarchWarps];
+  __shared__ long long wbase[kMarchWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long n_rays = static_cast<long long>(A.n_rows) * A.W;
+  const int K = (A.N + 31) >> 5;
+  for (long long g0 = static_cast<long long>(blockIdx.x) * kMarchWarps; g0 < n_rays;
+       g0 += static_cast<long long>(gridDim.x) * kMarchWarps) {
+    const long long r = g0 + warp;
+    int count = 0;
+    int pix = -1;
+    RayGeom R{};
+    double step = 0.0;
+    Pcg32 rng{0, 0};
+    if (r < n_rays) {
+      const int py = A.rows[r / A.W], px = static_cast<int>(r % A.W);
+      pix = py * A.W + px;
+      R = make_ray(A.cam, A.w2n, A.nlo, A.nhi, px, py);
+      if (R.valid && A.N > 0) {
+        step = ddiv(dsub(R.tf, R.tn), static_cast<double>(A.N));
+        if (A.stratified) rng = keyed_rng(A.seed, A.frame, static_cast<uint64_t>(pix));
+        for (int k = 0; k < K; ++k) {
+          const int i = k * 32 + lane;
+          bool f = false;
+          if (i < A.N) {
+            if (A.has_occ) {
+              const double t = sample_t(R.tn, step, i, jitter_at(A, rng, i));
+              const d3 xn = rigid_apply(A.w2n, add3(R.o, mul3(R.d, t)));
+              f = occupied(A.occ, xn);
+            } else {
+              f = true;
+            }
+          }
+          const unsigned b = __ballot_sync(0xffffffffu, f);
+          if (lane == 0) bal[warp][k] = b;
+          count += __popc(b);
+        }
+      }
+    }
+    if (lane == 0) wcount[warp] = count;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      for (int w = 0; w < kMarchWarps; ++w) {
+        wbase[w] = tot;
+        tot += wcount[w];
+      }
+      const long long base = tot ? static_cast<long long>(atomicAdd(A.counters, static_cast<unsigned long long>(tot))) : 0;
+      for (int w = 0; w < kMarchWarps; ++w) wbase[w] += base;
+    }
+    __syncthreads();
+    if (r < n_rays) {
+      const long long first = wbase[warp];
+      if (lane == 0) {
+        A.ray_first[pix] = static_cast<int32_t>(first < A.cap ? first : A.cap);
+        A.ray_count[pix] = (first + count <= A.cap) ? count : 0;
+      }
+      if (count) {
+        long long run = first;
+        for (int k = 0; k < K; ++k) {
+          const unsigned b = bal[warp][k];
+          if ((b >> lane) & 1u) {
+            const long long pos = run + __popc(b & lanemask_lt());
+            if (pos < A.cap) {
+              const int i = k * 32 + lane;
+              const double t = sample_t(R.tn, step, i, jitter_at(A, rng, i));
+              double delta;
+              if (i + 1 < A.N) delta = dsub(sample_t(R.tn, step, i + 1, jitter_at(A, rng, i + 1)), t);
+              else delta = dsub(R.tf, t);
+              const d3 xn = rigid_apply(A.w2n, add3(R.o, mul3(R.d, t)));
+              A.sx[pos] = xn.x;
+              A.sy[pos] = xn.y;
+              A.sz[pos] = xn.z;
+              A.sdelta[pos] = delta;
+              A.sray[pos] = pix;
+              A.sidx[pos] = static_cast<int16_t>(i);
+            }
+          }
+          run += __popc(b);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K2: deformer -----------------------------------------------------------
+
+struct PoolOut {
+  uint8_t* snroot;
+  int32_t* sbase;
+  double *px, *py, *pz;
+  int32_t* powner;
+  float4* pres;
+  unsigned long long* counters;  // [1] canonical, [2] pool
+  long long cap_pool;
+  FieldView F;  // for the rare 3rd+ in-box roots (evaluated in-kernel)
+};
+
+struct ListSrc {  // posed samples from K1 or a user batch
+  const double *x, *y, *z;
+  const unsigned long long* n_dev;  // device count (K1) or nullptr
+  long long n, cap;
+  __device__ long long count() const {
+    long long c = n_dev ? static_cast<long long>(*n_dev) : n;
+    return c < cap ? c : cap;
+  }
+  __device__ d3 point(long long i, int& pose) const {
+    pose = 0;
+    return make3(x[i], y[i], z[i]);
+  }
+};
+
+struct CellSrc {  // cell centres of an occupancy grid  R/occupancy.hpp:53-58, :141-144
+  int rx, ry, rz;
+  double lo[3], cs[3];
+  __device__ long long count() const { return static_cast<long long>(rx) * ry * rz; }
+  __device__ d3 point(long long i, int& pose) const {
+    pose = 0;
+    const int ix = static_cast<int>(i % rx), iy = static_cast<int>((i / rx) % ry),
+              iz = static_cast<int>(i / (static_cast<long long>(rx) * ry));
+    return make3(dadd(lo[0], dmul(dadd(static_cast<double>(ix), 0.5), cs[0])),
+                 dadd(lo[1], dmul(dadd(static_cast<double>(iy), 0.5), cs[1])),
+                 dadd(lo[2], dmul(dadd(static_cast<double>(iz), 0.5), cs[2])));
+  }
+};
+
+struct JitterSrc {  // update_training_grid draws  R/occupancy.hpp:160-166
+  int rx, ry, rz, n_poses;
+  double lo[3], cs[3];
+  uint64_t seed, step;
+  __device__ long long count() const { return static_cast<long long>(rx) * ry * rz; }
+  __device__ d3 point(long long i, int& pose) const {
+    const int ix = static_cast<int>(i % rx), iy = static_cast<int>((i / rx) % ry),
+              iz = static_cast<int>(i / (static_cast<long long>(rx) * ry));
+    Pcg32 r = keyed_rng(seed, 0x0cc0, static_cast<uint64_t>(i), step);
+    pose = static_cast<int>(pcg_below(r, static_cast<uint32_t>(n_poses)));
+    const double jx = pcg_double(r);
+    const double jy = pcg_double(r);
+    const double jz = pcg_double(r);
+    return make3(dadd(lo[0], dmul(dadd(static_cast<double>(ix), jx), cs[0])),
+                 dadd(lo[1], dmul(dadd(static_cast<double>(iy), jy), cs[1])),
+                 dadd(lo[2], dmul(dadd(static_cast<double>(iz), jz), cs[2])));
+  }
+};
+
+// rare path (3rd+ in-box root): out-of-line, generic MLP, keeps deformer registers low
+__device__ __noinline__ float4 field_query_slow(const FieldView& F, d3 x) {
+  float feats[kMaxLevels * 8];
+  if (F.F == 2) hash_encode_f2(F, x, feats);
+  else hash_encode_generic(F, x, feats);
+  float lg[kMlpGenericMaxWidth];
+  mlp_forward_generic(F, F.mlp, feats, lg);
+  return make_float4(softplus_f(lg[0]), logistic_f(lg[1]), logistic_f(lg[2]), logistic_f(lg[3]));
+}
+
+template <class Src>
+__global__ void __launch_bounds__(128) deform_kernel(SkinView S, const PoseCtx* __restrict__ poses,
+                                                     InverseOpts opt, Src src, PoolOut out) {
+  extern __shared__ double ws_smem[];
+  double* ws = ws_smem + threadIdx.x;
+  const int stride = blockDim.x;
+  const long long n = src.count();
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int pose;
+    const d3 xt = src.point(s, pose);
+    const PoseCtx* P = poses + pose;
+    Roots R;
+    inverse_lbs(S, P, opt, xt, ws, stride, R);
+    // posed_query_ctx: in-box roots in push order  R/articulation.hpp:170-173
+    int keep[kMaxRoots];
+    int nin = 0;
+    for (int k = 0; k < R.count; ++k)
+      if (field_contains(out.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]))) keep[nin++] = k;
+    out.snroot[s] = static_cast<uint8_t>(nin);
+    if (nin == 0) {
+      out.sbase[s] = -1;
+      continue;
+    }
+    atomicAdd(out.counters + 1, 1ull);
+    const int nalloc = nin < 3 ? nin : 3;
+    const long long base = static_cast<long long>(atomicAdd(out.counters + 2, static_cast<unsigned long long>(nalloc)));
+    out.sbase[s] = static_cast<int32_t>(base);
+    if (base + nalloc > out.cap_pool) {
+      atomicAdd(out.counters + 3, 1ull);  // overflow: caller regrows and reruns
+      continue;
+    }
+    for (int j = 0; j < 2 && j < nin; ++j) {
+      const int k = keep[j];
+      out.px[base + j] = R.x[k][0];
+      out.py[base + j] = R.x[k][1];
+      out.pz[base + j] = R.x[k][2];
+      out.powner[base + j] = static_cast<int32_t>(s);
+    }
+    if (nin > 2) {  // rare: evaluate roots 3.. here, keep the first max (strict >)
+      float4 best = make_float4(0.f, 0.f, 0.f, 0.f);
+      int bk = -1;
+      for (int j = 2; j < nin; ++j) {
+        const int k = keep[j];
+        const float4 v = field_query_slow(out.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]));
+        if (bk < 0 || v.x > best.x) {
+          best = v;
+          bk = k;
+        }
+      }
+      out.px[base + 2] = R.x[bk][0];
+      out.py[base + 2] = R.x[bk][1];
+      out.pz[base + 2] = R.x[bk][2];
+      out.powner[base + 2] = -1;
+      out.pres[base + 2] = best;
+    }
+  }
+}
+
+// ---- K3: field over the root pool -----------------------------------------
+
+__global__ void __launch_bounds__(128) field_pool_kernel(FieldView F, const double* __restrict__ px,
+                                                         const double* __restrict__ py,
+                                                         const double* __restrict__ pz,
+                                                         const int32_t* __restrict__ owner,
+                                                         float4* __restrict__ res,
+                                                         const unsigned long long* n_dev, long long cap,
+                                                         int mlp_in_smem) {
+  extern __shared__ float wsm[];
+  const float* W = F.mlp;
+  if (mlp_in_smem) {
+    for (int i = threadIdx.x; i < F.n_mlp; i += blockDim.x) wsm[i] = F.mlp[i];
+    __syncthreads();
+    W = wsm;
+  }
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (owner[i] < 0) continue;
+    res[i] = field_query_exact(F, W, make3(px[i], py[i], pz[i]));
+  }
+}
+
+// max-density root of a posed sample (R/articulation.hpp:170-179); returns slot or -1
+__device__ __forceinline__ int select_root(const uint8_t* snroot, const int32_t* sbase,
+                                           const float4* pres, long long s, float4& best) {
+  const int nin = snroot[s];
+  if (nin == 0) return -1;
+  const int base = sbase[s];
+  const int m = nin < 3 ? nin : 3;
+  int sel = 0;
+  best = pres[base];
+  for (int k = 1; k < m; ++k) {
+    const float4 v = pres[base + k];
+    if (v.x > best.x) {
+      best = v;
+      sel = k;
+    }
+  }
+  return sel;
+}
+
+// ---- K4: selection + composite ----------------------------------------------
+
+struct CompositeArgs {
+  const int32_t* rows;
+  int n_rows, W;
+  const int32_t *ray_first, *ray_count;
+  const double* sdelta;
+  const uint8_t* snroot;
+  const int32_t* sbase;
+  const float4* pres;
+  int8_t* ssel;
+  double eps;
+  float *rgb, *alpha;
+};
+
+__global__ void composite_kernel(CompositeArgs A) {
+  const long long n_rays = static_cast<long long>(A.n_rows) * A.W;
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int py = A.rows[r / A.W], px = static_cast<int>(r % A.W);
+    const int pix = py * A.W + px;
+    const int first = A.ray_first[pix], cnt = A.ray_count[pix];
+    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, acc = 0.0;
+    bool done = A.eps > 0 && T <= A.eps;
+    for (int j = 0; j < cnt; ++j) {
+      const long long s = first + j;
+      float4 v;
+      const int sel = select_root(A.snroot, A.sbase, A.pres, s, v);
+      A.ssel[s] = static_cast<int8_t>(sel);
+      if (done || sel < 0) continue;
+      const double sigma = static_cast<double>(v.x);
+      if (sigma <= 0.0) continue;
+      const double alpha = -expm1(-dmul(sigma, A.sdelta[s]));
+      const double w = dmul(alpha, T);
+      cr = dadd(cr, dmul(static_cast<double>(v.y), w));
+      cg = dadd(cg, dmul(static_cast<double>(v.z), w));
+      cb = dadd(cb, dmul(static_cast<double>(v.w), w));
+      acc = dadd(acc, w);
+      T = dmul(T, dsub(1.0, alpha));
+      if (A.eps > 0 && T <= A.eps) done = true;
+    }
+    A.rgb[3 * pix + 0] = static_cast<float>(cr);
+    A.rgb[3 * pix + 1] = static_cast<float>(cg);
+    A.rgb[3 * pix + 2] = static_cast<float>(cb);
+    A.alpha[pix] = static_cast<float>(acc);
+  }
+}
+
+// ---- occupancy kernels ----------------------------------------------------
+
+__global__ void finalize_counters_kernel(unsigned long long* c, long long cap_posed) {
+  if (static_cast<long long>(c[0]) > cap_posed) c[3] += 1;
+}
+
+__global__ void occ_values_kernel(long long n, const uint8_t* __restrict__ snroot,
+                                  const int32_t* __restrict__ sbase, const float4* __restrict__ pres,
+                                  float* __restrict__ values, float decay, int decayed_max) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 v;
+    const int sel = select_root(snroot, sbase, pres, i, v);
+    const double d = sel >= 0 ? static_cast<double>(v.x) : 0.0;
+    const float fresh = static_cast<float>((1.0 < d) ? 1.0 : d);  // float(std::min(d, 1.0))
+    if (decayed_max) {
+      const float old = __fmul_rn(decay, values[i]);
+      values[i] = (old < fresh) ? fresh : old;  // std::max  R/occupancy.hpp:168
+    } else {
+      values[i] = fresh;
+    }
+  }
+}
+
+__global__ void occ_threshold_kernel(long long n, const float* __restrict__ values, float thr,
+                                     uint8_t* __restrict__ mask) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    mask[i] = values[i] >= thr ? 1 : 0;
+}
+
+// one separable pass of dilated_mask  R/occupancy.hpp:101-119
+__global__ void occ_dilate_kernel(int rx, int ry, int rz, int axis, int r, const uint8_t* __restrict__ src,
+                                  uint8_t* __restrict__ dst) {
+  const long long n = static_cast<long long>(rx) * ry * rz;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int idx3[3] = {static_cast<int>(i % rx), static_cast<int>((i / rx) % ry),
+                         static_cast<int>(i / (static_cast<long long>(rx) * ry))};
+    const int nn[3] = {rx, ry, rz};
+    const long long stride[3] = {1, rx, static_cast<long long>(rx) * ry};
+    uint8_t v = 0;
+    for (int d = -r; d <= r && !v; ++d) {
+      const int j = idx3[axis] + d;
+      if (j < 0 || j >= nn[axis]) continue;
+      v = src[i + static_cast<long long>(d) * stride[axis]];
+    }
+    dst[i] = v;
+  }
+}
+
+// ---- batch query kernels (API) ----------------------------------------------
+
+__global__ void inverse_lbs_kernel(SkinView S, const PoseCtx* __restrict__ P, InverseOpts opt,
+                                   const double* __restrict__ pts, long long n, int32_t* counts,
+                                   double* roots, double* resid) {
+  extern __shared__ double ws_smem[];
+  double* ws = ws_smem + threadIdx.x;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    Roots R;
+    inverse_lbs(S, P, opt, make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]), ws, blockDim.x, R);
+    counts[i] = R.count;
+    for (int k = 0; k < R.count; ++k) {
+      roots[(i * kMaxRoots + k) * 3 + 0] = R.x[k][0];
+      roots[(i * kMaxRoots + k) * 3 + 1] = R.x[k][1];
+      roots[(i * kMaxRoots + k) * 3 + 2] = R.x[k][2];
+      resid[i * kMaxRoots + k] = R.r[k];
+    }
+  }
+}
+
+__global__ void posed_out_kernel(long long n, const uint8_t* __restrict__ snroot,
+                                 const int32_t* __restrict__ sbase, const float4* __restrict__ pres,
+                                 const double* __restrict__ px, const double* __restrict__ py,
+                                 const double* __restrict__ pz, float* dens, float* col,
+                                 double* canon, uint8_t* has) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int sel = select_root(snroot, sbase, pres, i, v);
+    has[i] = sel >= 0;
+    dens[i] = sel >= 0 ? v.x : 0.f;
+    col[3 * i + 0] = sel >= 0 ? v.y : 0.f;
+    col[3 * i + 1] = sel >= 0 ? v.z : 0.f;
+    col[3 * i + 2] = sel >= 0 ? v.w : 0.f;
+    const long long p = sel >= 0 ? sbase[i] + sel : -1;
+    canon[3 * i + 0] = p >= 0 ? px[p] : 0.0;
+    canon[3 * i + 1] = p >= 0 ? py[p] : 0.0;
+    canon[3 * i + 2] = p >= 0 ? pz[p] : 0.0;
+  }
+}
+
+__global__ void field_query_kernel(FieldView F, const double* __restrict__ pts, long long n, float4* out,
+                                   int* domain_err) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const d3 x = make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    if (!field_contains(F, x)) {
+      atomicExch(domain_err, 1);
+      continue;
+    }
+    out[i] = field_query_exact(F, F.mlp, x);
+  }
+}
+
+__global__ void hash_encode_kernel(FieldView F, const double* __restrict__ pts, long long n, float* out,
+                                   int* domain_err) {
+  const int D = F.L * F.F;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const d3 x = make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    if (!field_contains(F, x)) {
+      atomicExch(domain_err, 1);
+      continue;
+    }
+    if (F.F == 2) hash_encode_f2(F, x, out + i * D);
+    else hash_encode_generic(F, x, out + i * D);
+  }
+}
+
+__global__ void skin_weights_kernel(SkinView S, const double* __restrict__ pts, long long n, double* w) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    skin_weights_dense(S, make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]), w + i * S.nb);
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int grid_for(long long n, int threads, int per_sm) {
+  const long long want = (n + threads - 1) / threads;
+  const long long cap = static_cast<long long>(sm_count()) * per_sm;
+  return static_cast<int>(std::max(1LL, std::min(want, cap)));
+}
+
+PoolOut pool_out(ModelImpl& m) {
+  Workspace& w = m.ws;
+  return PoolOut{w.snroot.ptr, w.sbase.ptr, w.px.ptr, w.py.ptr, w.pz.ptr, w.powner.ptr, w.pres.ptr,
+                 w.counters.ptr, static_cast<long long>(w.cap_pool), m.fv};
+}
+
+template <class Src>
+void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long long n_hint,
+                   cudaStream_t s) {
+  const int threads = 128;
+  const size_t smem = static_cast<size_t>(m.sv.nb) * threads * sizeof(double);
+  m.prof.begin("deform", s);
+  deform_kernel<Src><<<grid_for(n_hint, threads, 16), threads, smem, s>>>(m.sv, d_poses, m.inv, src,
+                                                                           pool_out(m));
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+}
+
+void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
+  const int threads = 128;
+  const size_t wbytes = static_cast<size_t>(m.fv.n_mlp) * sizeof(float);
+  const int in_smem = wbytes <= 48 * 1024 ? 1 : 0;
+  m.prof.begin("field", s);
+  field_pool_kernel<<<grid_for(n_hint, threads, 16), threads, in_smem ? wbytes : 0, s>>>(
+      m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr, m.ws.pres.ptr,
+      m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool), in_smem);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+}
+
+}  // namespace
+
+void Workspace::ensure(size_t posed, size_t pix) {
+  if (posed > cap_posed) {
+    const size_t c = posed;
+    sx.alloc(c);
+    sy.alloc(c);
+    sz.alloc(c);
+    sdelta.alloc(c);
+    sray.alloc(c);
+    sidx.alloc(c);
+    snroot.alloc(c);
+    sbase.alloc(c);
+    ssel.alloc(c);
+    cap_posed = c;
+    const size_t pc = c + c / 2 + 1024;
+    px.alloc(pc);
+    py.alloc(pc);
+    pz.alloc(pc);
+    powner.alloc(pc);
+    pres.alloc(pc);
+    cap_pool = pc;
+  }
+  if (pix > n_pix) {
+    ray_first.alloc(pix);
+    ray_count.alloc(pix);
+    n_pix = pix;
+  }
+  if (!counters.ptr) counters.alloc(8);
+}
+
+void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N,
+                  bool stratified, double eps, uint64_t seed, uint64_t frame, int shard,
+                  int nshards, float* d_rgb, float* d_alpha, unsigned long long* d_counters,
+                  cudaStream_t s) {
+  Workspace& w = m.ws;
+  // rows of this shard: interleaved 16-row tiles
+  if (w.last_shard != shard || w.last_nshards != nshards || w.last_rows != cam.height ||
+      w.last_w != cam.width) {
+    std::vector<int32_t> rows;
+    for (int y = 0; y < cam.height; ++y)
+      if ((y / 16) % nshards == shard) rows.push_back(y);
+    w.row_list.alloc(rows.size() + 1);
+    if (!rows.empty())
+      ARFX_CUDA(cudaMemcpyAsync(w.row_list.ptr, rows.data(), rows.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    w.last_shard = shard;
+    w.last_nshards = nshards;
+    w.last_rows = cam.height;
+    w.last_w = cam.width;
+    w.n_rows = static_cast<int>(rows.size());
+  }
+  const int n_rows = w.n_rows;
+  const long long n_rays = static_cast<long long>(n_rows) * cam.width;
+  w.ensure(w.cap_posed ? 0 : static_cast<size_t>(std::max<long long>(
+                                   std::min<long long>(n_rays * std::max(N, 1), 1LL << 22), 1LL << 16)),
+           static_cast<size_t>(cam.width) * cam.height);
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+
+  MarchArgs A{};
+  A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
+  for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
+  for (int k = 0; k < 12; ++k) A.w2n[k] = p.host.w2n[k];
+  A.nlo[0] = m.norm.lo.x;
+  A.nlo[1] = m.norm.lo.y;
+  A.nlo[2] = m.norm.lo.z;
+  A.nhi[0] = m.norm.hi.x;
+  A.nhi[1] = m.norm.hi.y;
+  A.nhi[2] = m.norm.hi.z;
+  A.has_occ = occ != nullptr;
+  if (occ) A.occ = occ->view();
+  A.N = N;
+  A.stratified = stratified;
+  A.seed = seed;
+  A.frame = frame;
+  A.rows = w.row_list.ptr;
+  A.n_rows = n_rows;
+  A.W = cam.width;
+  A.sx = w.sx.ptr;
+  A.sy = w.sy.ptr;
+  A.sz = w.sz.ptr;
+  A.sdelta = w.sdelta.ptr;
+  A.sray = w.sray.ptr;
+  A.sidx = w.sidx.ptr;
+  A.ray_first = w.ray_first.ptr;
+  A.ray_count = w.ray_count.ptr;
+  A.counters = w.counters.ptr;
+  A.cap = static_cast<long long>(w.cap_posed);
+  if (n_rays > 0) {
+    const long long groups = (n_rays + kMarchWarps - 1) / kMarchWarps;
+    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 8));
+    m.prof.begin("march", s);
+    march_kernel<<<grid, kMarchWarps * 32, 0, s>>>(A);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+  }
+  ListSrc src{w.sx.ptr, w.sy.ptr, w.sz.ptr, w.counters.ptr, 0, static_cast<long long>(w.cap_posed)};
+  launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s);
+  launch_field_pool(m, s, static_cast<long long>(w.cap_pool));
+  CompositeArgs C{w.row_list.ptr, n_rows, cam.width, w.ray_first.ptr, w.ray_count.ptr, w.sdelta.ptr,
+                  w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w.ssel.ptr, eps, d_rgb, d_alpha};
+  if (n_rays > 0) {
+    m.prof.begin("composite", s);
+    composite_kernel<<<grid_for(n_rays, 128, 16), 128, 0, s>>>(C);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+  }
+  finalize_counters_kernel<<<1, 1, 0, s>>>(w.counters.ptr, static_cast<long long>(w.cap_posed));
+  if (d_counters)
+    ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, s));
+}
+
+OccView OccImpl::view() const {
+  OccView v{};
+  v.rx = v.ry = v.rz = res;
+  v.lo[0] = box.lo.x;
+  v.lo[1] = box.lo.y;
+  v.lo[2] = box.lo.z;
+  v.hi[0] = box.hi.x;
+  v.hi[1] = box.hi.y;
+  v.hi[2] = box.hi.z;
+  v.e[0] = box.hi.x - box.lo.x;
+  v.e[1] = box.hi.y - box.lo.y;
+  v.e[2] = box.hi.z - box.lo.z;
+  v.mask = mask.ptr;
+  return v;
+}
+
+void occ_rebuild(OccImpl& g, cudaStream_t s) {
+  const long long n = static_cast<long long>(g.res) * g.res * g.res;
+  occ_threshold_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, g.values.ptr, static_cast<float>(g.threshold),
+                                                          g.mask.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  if (g.dilation > 0) {
+    g.tmp.ensure(static_cast<size_t>(n));
+    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 0, g.dilation, g.mask.ptr, g.tmp.ptr);
+    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 1, g.dilation, g.tmp.ptr, g.mask.ptr);
+    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 2, g.dilation, g.mask.ptr, g.tmp.ptr);
+    ARFX_CUDA(cudaMemcpyAsync(g.mask.ptr, g.tmp.ptr, static_cast<size_t>(n), cudaMemcpyDeviceToDevice, s));
+    ARFX_CUDA(cudaGetLastError());
+  }
+}
+
+static void occ_source_common(OccImpl& g, double lo[3], double cs[3]) {
+  lo[0] = g.box.lo.x;
+  lo[1] = g.box.lo.y;
+  lo[2] = g.box.lo.z;
+  // cell_size  R/occupancy.hpp:49-52
+  cs[0] = (g.box.hi.x - g.box.lo.x) / g.res;
+  cs[1] = (g.box.hi.y - g.box.lo.y) / g.res;
+  cs[2] = (g.box.hi.z - g.box.lo.z) / g.res;
+}
+
+void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d_counters,
+                    cudaStream_t s) {
+  Workspace& w = m.ws;
+  const long long n = static_cast<long long>(g.res) * g.res * g.res;
+  w.ensure(static_cast<size_t>(n), 0);
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  CellSrc src{g.res, g.res, g.res, {}, {}};
+  occ_source_common(g, src.lo, src.cs);
+  launch_deform(m, p.dev.ptr, src, n, s);
+  launch_field_pool(m, s, n);
+  m.prof.begin("occ_values+mask", s);
+  occ_values_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.snroot.ptr, w.sbase.ptr, w.pres.ptr,
+                                                       g.values.ptr, 1.0f, 0);
+  ARFX_CUDA(cudaGetLastError());
+  occ_rebuild(g, s);
+  m.prof.end(s);
+  if (d_counters)
+    ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, s));
+}
+
+void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,
+                          uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
+                          cudaStream_t s) {
+  Workspace& w = m.ws;
+  const long long n = static_cast<long long>(g.res) * g.res * g.res;
+  w.ensure(static_cast<size_t>(n), 0);
+  DevBuf<PoseCtx> ctxs;
+  ctxs.alloc(poses.size());
+  for (size_t i = 0; i < poses.size(); ++i)
+    ARFX_CUDA(cudaMemcpyAsync(ctxs.ptr + i, poses[i]->dev.ptr, sizeof(PoseCtx), cudaMemcpyDeviceToDevice, s));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  JitterSrc src{g.res, g.res, g.res, static_cast<int>(poses.size()), {}, {}, seed, step};
+  occ_source_common(g, src.lo, src.cs);
+  launch_deform(m, ctxs.ptr, src, n, s);
+  launch_field_pool(m, s, n);
+  occ_values_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.snroot.ptr, w.sbase.ptr, w.pres.ptr,
+                                                       g.values.ptr, static_cast<float>(decay), 1);
+  ARFX_CUDA(cudaGetLastError());
+  occ_rebuild(g, s);
+  if (d_counters)
+    ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, s));
+  ARFX_CUDA(cudaStreamSynchronize(s));  // ctxs is released on return
+}
+
+void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
+                       int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s) {
+  if (n <= 0) return;
+  const int threads = 128;
+  const size_t smem = static_cast<size_t>(m.sv.nb) * threads * sizeof(double);
+  inverse_lbs_kernel<<<grid_for(n, threads, 16), threads, smem, s>>>(m.sv, d_ctx, m.inv, d_pts, n, d_counts,
+                                                                      d_roots, d_res);
+  ARFX_CUDA(cudaGetLastError());
+}
+
+void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n, float* d_dens,
+                       float* d_col, double* d_canon, uint8_t* d_has, unsigned long long* d_counters,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  Workspace& w = m.ws;
+  w.ensure(static_cast<size_t>(n), 0);
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  ListSrc src{d_pts, d_pts, d_pts, nullptr, n, n};
+  // ListSrc expects SoA; user batches are AoS -> split on device
+  DevBuf<double> soa;
+  soa.alloc(static_cast<size_t>(3 * n));
+  std::vector<double> dummy;
+  (void)dummy;
+  // transpose AoS -> SoA with three strided 2D copies
+  ARFX_CUDA(cudaMemcpy2DAsync(soa.ptr, sizeof(double), d_pts, 3 * sizeof(double), sizeof(double),
+                              static_cast<size_t>(n), cudaMemcpyDeviceToDevice, s));
+  ARFX_CUDA(cudaMemcpy2DAsync(soa.ptr + n, sizeof(double), d_pts + 1, 3 * sizeof(double), sizeof(double),
+                              static_cast<size_t>(n), cudaMemcpyDeviceToDevice, s));
+  ARFX_CUDA(cudaMemcpy2DAsync(soa.ptr + 2 * n, sizeof(double), d_pts + 2, 3 * sizeof(double),
+                              sizeof(double), static_cast<size_t>(n), cudaMemcpyDeviceToDevice, s));
+  src.x = soa.ptr;
+  src.y = soa.ptr + n;
+  src.z = soa.ptr + 2 * n;
+  launch_deform(m, p.dev.ptr, src, n, s);
+  launch_field_pool(m, s, n);
+  posed_out_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w.px.ptr,
+                                                       w.py.ptr, w.pz.ptr, d_dens, d_col, d_canon, d_has);
+  ARFX_CUDA(cudaGetLastError());
+  if (d_counters)
+    ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, s));
+  ARFX_CUDA(cudaStreamSynchronize(s));
+}
+
+void field_query_batch(ModelImpl& m, const double* d_pts, int64_t n, float4* d_out, int* d_domain_err,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  field_query_kernel<<<grid_for(n, 128, 16), 128, 0, s>>>(m.fv, d_pts, n, d_out, d_domain_err);
+  ARFX_CUDA(cudaGetLastError());
+}
+
+void hash_encode_batch(ModelImpl& m, const double* d_pts, int64_t n, float* d_feats, int* d_domain_err,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  hash_encode_kernel<<<grid_for(n, 128, 16), 128, 0, s>>>(m.fv, d_pts, n, d_feats, d_domain_err);
+  ARFX_CUDA(cudaGetLastError());
+}
+
+void skin_weights_batch(ModelImpl& m, const double* d_pts, int64_t n, double* d_w, cudaStream_t s) {
+  if (n <= 0) return;
+  skin_weights_kernel<<<grid_for(n, 128, 16), 128, 0, s>>>(m.sv, d_pts, n, d_w);
+  ARFX_CUDA(cudaGetLastError());
+}
+
+}  // namespace arfx
+
+namespace arfx {
+
+cudaEvent_t KernelProfiler::take() {
+  if (!free_events.empty()) {
+    cudaEvent_t e = free_events.back();
+    free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ARFX_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void KernelProfiler::begin(const char* name, cudaStream_t s) {
+  if (!on) return;
+  Rec r{name, take(), take()};
+  ARFX_CUDA(cudaEventRecord(r.a, s));
+  pending.push_back(r);
+}
+
+void KernelProfiler::end(cudaStream_t s) {
+  if (!on || pending.empty()) return;
+  ARFX_CUDA(cudaEventRecord(pending.back().b, s));
+}
+
+void KernelProfiler::collect() {
+  for (Rec& r : pending) {
+    ARFX_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    ARFX_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    size_t k = 0;
+    while (k < names.size() && names[k] != r.name) ++k;
+    if (k == names.size()) {
+      names.emplace_back(r.name);
+      ms.push_back(0.0);
+      launches.push_back(0);
+    }
+    ms[k] += t;
+    launches[k] += 1;
+    free_events.push_back(r.a);
+    free_events.push_back(r.b);
+  }
+  pending.clear();
+}
+
+KernelProfiler::~KernelProfiler() {
+  for (Rec& r : pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : free_events) cudaEventDestroy(e);
+}
+
+}  // namespace arfx

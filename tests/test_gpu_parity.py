@@ -1,0 +1,228 @@
+"""GPU parity: libarfx (sm_100a) vs the UNMODIFIED reference compiled in place
+(oracle/_ref) on identical inputs. Integer decisions (model init draws, skinning
+weights, sample indices, roots, masks) must be bit-exact; f32 field outputs are
+compared with a stated tolerance (CUDA expf/log1pf vs glibc: <= 4 ulp)."""
+import numpy as np
+import pytest
+
+from paper_2212_10550_b200 import arf, fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+# f32 field outputs: softplus/logistic use expf/log1pf whose CUDA and glibc results may
+# differ by a few ulp; everything upstream (encode, MLP sums) is bit-exact.
+F32_RTOL = 2e-6
+F32_ATOL = 1e-7
+# rendered RGB/alpha (north_star: 1e-3 relative); the exact path is far tighter.
+PIX_ATOL = 1e-5
+
+
+def small_grid():
+    return arf.HashGridConfig(levels=8, features_per_level=2, table_size_log2=14, base_resolution=4,
+                              max_resolution=96)
+
+
+@pytest.fixture(scope="module")
+def models(gpu, ref):
+    """(product model, reference model) built from the same skeleton/configs/seed."""
+    sk = fx.smpl24()
+    g, m = fx.config1_grid(), fx.config1_mlp()
+    dm = gpu.build_model(sk, g, m, (32, 32, 32), fx.CONFIG1_SEED)
+    rm = ref.build_model(sk, g, m, (32, 32, 32), fx.CONFIG1_SEED)
+    return sk, dm, rm
+
+
+def test_build_model_bit_exact(models, ref):
+    sk, dm, rm = models
+    gp, mp, sw = dm.params()
+    rgp, rmp, rsw = ref.arrays(rm)
+    assert np.array_equal(gp.view(np.uint32), rgp.view(np.uint32)), "hash-grid init draws differ"
+    assert np.array_equal(mp.view(np.uint32), rmp.view(np.uint32)), "MLP init draws differ"
+    assert np.array_equal(sw.view(np.uint64), rsw.view(np.uint64)), "skinning grid differs"
+    assert dm.desc.canonical_lo[:] == list(rm.canon_lo) and dm.desc.normalized_hi[:] == list(rm.norm_hi)
+
+
+def test_skinning_weights_bit_exact(models, ref):
+    sk, dm, rm = models
+    rng = np.random.default_rng(0)
+    lo, hi = np.array(rm.canon_lo[:]), np.array(rm.canon_hi[:])
+    pts = lo + (hi - lo) * rng.uniform(-0.1, 1.1, size=(4000, 3))  # includes out-of-box clamps
+    w = dm.skinning_weights(pts)
+    rw = ref.skinning_weights(rm, pts)
+    assert np.array_equal(w.view(np.uint64), rw.view(np.uint64))
+
+
+def test_hash_encode_bit_exact(models, ref):
+    sk, dm, rm = models
+    rng = np.random.default_rng(1)
+    lo, hi = np.array(rm.canon_lo[:]), np.array(rm.canon_hi[:])
+    pts = lo + (hi - lo) * rng.uniform(0, 1, size=(5000, 3))
+    pts[:8] = [lo, hi, (lo + hi) / 2, [lo[0], hi[1], lo[2]], [hi[0], lo[1], hi[2]], lo, hi, lo]
+    f = dm.encode(pts)
+    rf = ref.hash_encode(rm, pts)
+    assert np.array_equal(f.view(np.uint32), rf.view(np.uint32))
+
+
+def test_encode_out_of_box_is_domain_error(models):
+    sk, dm, rm = models
+    from paper_2212_10550_b200 import DomainError
+    with pytest.raises(DomainError):
+        dm.encode(np.array([[10.0, 10.0, 10.0]]))
+
+
+def test_field_query(models, ref):
+    sk, dm, rm = models
+    rng = np.random.default_rng(2)
+    lo, hi = np.array(rm.canon_lo[:]), np.array(rm.canon_hi[:])
+    pts = lo + (hi - lo) * rng.uniform(0, 1, size=(5000, 3))
+    d, c = dm.field_query(pts)
+    rd, rc = ref.field_query(rm, pts)
+    np.testing.assert_allclose(d, rd, rtol=F32_RTOL, atol=F32_ATOL)
+    np.testing.assert_allclose(c, rc, rtol=F32_RTOL, atol=F32_ATOL)
+
+
+def test_field_query_structured_params(gpu, ref):
+    """Params refilled with U(+-0.5) so the field is far from its random-init constant."""
+    sk = fx.smpl24()
+    g = small_grid()
+    m = arf.MlpConfig(16, 64, 2, 4)
+    rm = ref.build_model(sk, g, m, (16, 16, 16), 7)
+    gp, mp, sw = ref.arrays(rm)
+    rng = np.random.default_rng(3)
+    gp[:] = rng.uniform(-0.5, 0.5, gp.size).astype(np.float32)
+    mp[:] = rng.uniform(-0.5, 0.5, mp.size).astype(np.float32)
+    dm = gpu.build_model(sk, g, m, (16, 16, 16), 7)
+    dm.set_params(gp, mp)
+    lo, hi = np.array(rm.canon_lo[:]), np.array(rm.canon_hi[:])
+    pts = lo + (hi - lo) * rng.uniform(0, 1, size=(4000, 3))
+    assert np.array_equal(dm.encode(pts).view(np.uint32), ref.hash_encode(rm, pts).view(np.uint32))
+    d, c = dm.field_query(pts)
+    rd, rc = ref.field_query(rm, pts)
+    np.testing.assert_allclose(d, rd, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(c, rc, rtol=1e-5, atol=1e-6)
+
+
+def test_inverse_lbs_roots_bit_exact(models, ref):
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, fx.CONFIG1_POSE_SEED)
+    # points near the posed body: posed capsule axes + jitter
+    rng = np.random.default_rng(4)
+    T = pose.bone_transforms
+    pts = []
+    for i, b in enumerate(sk.bones):
+        for u in rng.uniform(0, 1, 60):
+            a = fx._apply(T[i], b.head)
+            e = fx._apply(T[i], b.tail)
+            pts.append([a[k] + (e[k] - a[k]) * u + rng.uniform(-0.08, 0.08) for k in range(3)])
+    pts = np.array(pts)
+    pre = arf.rigid()
+    cnt, roots, res = dm.inverse_lbs(pose, pts, pre, 3.0)
+    rcnt, rroots, rres = ref.inverse_lbs(rm, pose.bone_transforms, pre, 3.0, pts)
+    assert np.array_equal(cnt, rcnt)
+    for i in range(len(pts)):
+        k = cnt[i]
+        assert np.array_equal(roots[i, :k].view(np.uint64), rroots[i, :k].view(np.uint64)), i
+        assert np.array_equal(res[i, :k].view(np.uint64), rres[i, :k].view(np.uint64)), i
+    assert (cnt > 0).mean() > 0.5
+
+
+def test_posed_query(models, ref):
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, 5)
+    rng = np.random.default_rng(5)
+    lo, hi = np.array(rm.norm_lo[:]), np.array(rm.norm_hi[:])
+    pts = lo + (hi - lo) * rng.uniform(0.25, 0.75, size=(6000, 3))
+    d, c, x, h = dm.posed_query(pose, pts)
+    rd, rc, rx, rh = ref.posed_query(rm, pose.bone_transforms, pose.global_transform, pts)
+    assert np.array_equal(h, rh)
+    assert np.array_equal(x.view(np.uint64), rx.view(np.uint64))
+    np.testing.assert_allclose(d, rd, rtol=F32_RTOL, atol=F32_ATOL)
+    np.testing.assert_allclose(c, rc, rtol=F32_RTOL, atol=F32_ATOL)
+
+
+def test_inference_grid_mask_bit_exact(models, ref):
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, fx.CONFIG1_POSE_SEED)
+    cfg = arf.OccupancyConfig()
+    g = gpu_grid = arf.build_model_inference_grid(dm, pose, cfg)
+    v, msk = g.download()
+    rg, rcnt = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, cfg)
+    rv, rmsk = ref.occ_arrays(rg)
+    assert g.density_threshold == rg.density_threshold
+    assert np.array_equal(msk, rmsk)
+    np.testing.assert_allclose(v, rv, rtol=F32_RTOL, atol=F32_ATOL)
+    assert (v > 0).sum() == (rv > 0).sum()
+    del gpu_grid
+
+
+@pytest.mark.parametrize("stratified", [False, True])
+def test_render_trace_parity(models, ref, stratified):
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, fx.CONFIG1_POSE_SEED)
+    cam = fx.default_camera(sk, 96, 96)
+    cfg = arf.OccupancyConfig()
+    occ = arf.build_model_inference_grid(dm, pose, cfg)
+    rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, cfg)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=stratified, seed=11, frame_id=3)
+    img = arf.render_model(dm, pose, cam, occ, opt)
+    tr = arf.render_trace(dm)
+    rrgb, ralpha, rcnt, rtr = ref.render_trace(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt)
+    # the traced reference loop reproduces arf::render_model bit for bit
+    rrgb2, ralpha2, _ = ref.render(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt)
+    assert np.array_equal(rrgb, rrgb2) and np.array_equal(ralpha, ralpha2)
+    # posed samples: same (pixel, sample index) set, bit-exact
+    n = rtr["n_samples"]
+    assert len(tr.ray) == n
+    order = np.lexsort((tr.index, tr.ray))
+    assert np.array_equal(tr.ray[order], rtr["s_ray"]) and np.array_equal(tr.index[order], rtr["s_index"])
+    assert np.array_equal(tr.delta[order].view(np.uint64), rtr["s_delta"].view(np.uint64))
+    assert np.array_equal(tr.has_root[order], rtr["s_has_root"])
+    assert np.array_equal(tr.canonical[order].view(np.uint64), rtr["s_canonical"].view(np.uint64))
+    np.testing.assert_allclose(tr.density[order], rtr["s_density"], rtol=F32_RTOL, atol=F32_ATOL)
+    np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-3, atol=PIX_ATOL)
+    np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-3, atol=PIX_ATOL)
+    assert dm.counters.posed_queries >= n
+
+
+def test_render_without_occupancy(gpu, ref):
+    sk = fx.default_figure_skeleton()
+    g = small_grid()
+    m = arf.MlpConfig(16, 64, 2, 4)
+    dm = gpu.build_model(sk, g, m, (16, 16, 16), 3)
+    rm = ref.build_model(sk, g, m, (16, 16, 16), 3)
+    rots = fx.bend_pose_rotations(10, 0.4, 0.3)
+    pose = arf.pose_from_joint_rotations(sk, rots, fx.yaw_about(sk.bones[0].head, 0.5))
+    cam = fx.default_camera(sk, 40, 32)
+    opt = arf.RenderOptions(samples_per_ray=64)
+    img = arf.render_model(dm, pose, cam, None, opt)
+    rrgb, ralpha, rcnt = ref.render(rm, pose.bone_transforms, pose.global_transform, cam, None, opt)
+    np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-3, atol=PIX_ATOL)
+    np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-3, atol=PIX_ATOL)
+    assert dm.counters.posed_queries == int(rcnt[0])
+    assert dm.counters.canonical_queries == int(rcnt[1])
+
+
+def test_composite_explicit(gpu, ref):
+    rng = np.random.default_rng(9)
+    lens = rng.integers(0, 40, size=64).astype(np.int32)
+    ns = int(lens.sum())
+    delta = rng.uniform(0.001, 0.2, ns)
+    skip = (rng.uniform(size=ns) < 0.3).astype(np.uint8)
+    dens = rng.uniform(0, 30, ns).astype(np.float32)
+    col = rng.uniform(0, 1, (ns, 3)).astype(np.float32)
+    c3, a, term = arf.composite(lens, delta, skip, dens, col, 1e-3)
+    dC = rng.normal(size=(64, 3))
+    dA = rng.normal(size=64)
+    ds, dcs = arf.composite_backward(lens, delta, skip, dens, col, 1e-3, dC, dA)
+    off = 0
+    for r, L in enumerate(lens):
+        sl = slice(off, off + L)
+        t = np.cumsum(delta[sl])
+        rc3, ra, rterm = ref.composite(t, delta[sl], skip[sl], dens[sl], col[sl], 1e-3)
+        assert rterm == term[r]
+        np.testing.assert_allclose(c3[r], rc3, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(a[r], ra, rtol=1e-12, atol=1e-15)
+        rds, rdc = ref.composite_backward(t, delta[sl], skip[sl], dens[sl], col[sl], 1e-3, dC[r], dA[r])
+        np.testing.assert_allclose(ds[sl], rds, rtol=1e-10, atol=1e-14)
+        np.testing.assert_allclose(dcs[sl], rdc, rtol=1e-10, atol=1e-14)
+        off += L
