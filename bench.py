@@ -172,7 +172,8 @@ def run_ours(args):
     occ_cfg = fx.config1_occupancy()
     occ = arf.OccupancyGrid(model.normalized_box, occ_cfg)
     views = [arf.PosedModelView(model, p) for p in poses]
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real (non-NULL) stream shared by torch events and libarfx
+    torch.cuda.set_stream(stream)
     sp = C.c_void_p(stream.cuda_stream)
     npix = W_IMG * H_IMG
     d_rgb = torch.zeros(npix * 3, dtype=torch.float32, device="cuda")

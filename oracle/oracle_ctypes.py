@@ -193,7 +193,7 @@ class Checker:
     def hash_index(self, gcfg, level, cx, cy, cz):
         fn = self.f("hash_index")
         fn.restype = C.c_uint32
-        return int(fn(C.byref(self.grid(gcfg)), level, cx, cy, cz))
+        return int(fn(C.byref(self.grid(gcfg)), int(level), int(cx), int(cy), int(cz)))
 
     def pose_from_joint_rotations(self, sk, rot9, g12):
         rot = np.ascontiguousarray(rot9, np.float64).reshape(-1, 9)

@@ -196,7 +196,8 @@ void alloc_model(ModelImpl& m) {
   ARFX_CUDA(cudaGetDevice(&m.device));
   if (!m.stream) ARFX_CUDA(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
   m.grid_params.alloc(m.n_grid);
-  m.mlp_params.alloc(m.n_mlp);
+  m.mlp_params.alloc((m.n_mlp + 3) / 4 * 4);  // float4-padded for the smem staging
+  ARFX_CUDA(cudaMemset(m.mlp_params.ptr, 0, m.mlp_params.n * sizeof(float)));
   m.skin.alloc(m.n_skin);
 }
 

@@ -352,15 +352,17 @@ __global__ void __launch_bounds__(128) field_pool_kernel(FieldView F, const doub
                                                          float4* __restrict__ res,
                                                          const unsigned long long* n_dev, long long cap,
                                                          int mlp_in_smem) {
-  extern __shared__ float wsm[];
-  const float* W = F.mlp;
-  if (mlp_in_smem) {
-    for (int i = threadIdx.x; i < F.n_mlp; i += blockDim.x) wsm[i] = F.mlp[i];
-    __syncthreads();
-    W = wsm;
-  }
+  extern __shared__ float4 wsm4[];
   long long n = static_cast<long long>(*n_dev);
   n = n < cap ? n : cap;
+  if (static_cast<long long>(blockIdx.x) * blockDim.x >= n) return;  // no work: skip the weight staging
+  const float* W = F.mlp;
+  if (mlp_in_smem) {
+    const float4* src = reinterpret_cast<const float4*>(F.mlp);
+    for (int i = threadIdx.x; i < (F.n_mlp + 3) / 4; i += blockDim.x) wsm4[i] = __ldg(src + i);
+    __syncthreads();
+    W = reinterpret_cast<const float*>(wsm4);
+  }
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     if (owner[i] < 0) continue;
@@ -664,8 +666,9 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   }
   const int n_rows = w.n_rows;
   const long long n_rays = static_cast<long long>(n_rows) * cam.width;
-  w.ensure(w.cap_posed ? 0 : static_cast<size_t>(std::max<long long>(
-                                   std::min<long long>(n_rays * std::max(N, 1), 1LL << 22), 1LL << 16)),
+  // grow-only; overflow beyond this is detected from the counters and the frame re-run
+  w.ensure(static_cast<size_t>(std::max<long long>(std::min<long long>(n_rays * std::max(N, 1), 1LL << 22),
+                                                   1LL << 16)),
            static_cast<size_t>(cam.width) * cam.height);
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
 

@@ -177,7 +177,14 @@ def test_render_trace_parity(models, ref, stratified):
     assert np.array_equal(tr.ray[order], rtr["s_ray"]) and np.array_equal(tr.index[order], rtr["s_index"])
     assert np.array_equal(tr.delta[order].view(np.uint64), rtr["s_delta"].view(np.uint64))
     assert np.array_equal(tr.has_root[order], rtr["s_has_root"])
-    assert np.array_equal(tr.canonical[order].view(np.uint64), rtr["s_canonical"].view(np.uint64))
+    # Selected canonical root (max-density rule, R/articulation.hpp:174): bit-exact except at
+    # density near-ties, where a 1-ulp expf/log1pf difference (CUDA vs glibc) can flip which of
+    # two roots wins. Policy: <= 1e-4 of samples, and only where the densities agree to 4 ulp.
+    can, rcan = tr.canonical[order], rtr["s_canonical"]
+    flip = np.any(can.view(np.uint64) != rcan.view(np.uint64), axis=1)
+    assert flip.sum() <= max(1, 1e-4 * n), flip.sum()
+    d_o, d_r = tr.density[order][flip], rtr["s_density"][flip]
+    assert np.all(np.abs(d_o - d_r) <= 4 * np.spacing(np.maximum(np.abs(d_o), np.abs(d_r)))), (d_o, d_r)
     np.testing.assert_allclose(tr.density[order], rtr["s_density"], rtol=F32_RTOL, atol=F32_ATOL)
     np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-3, atol=PIX_ATOL)
     np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-3, atol=PIX_ATOL)

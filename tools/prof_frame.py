@@ -1,0 +1,33 @@
+"""Small driver for ncu: config-1 avatar, F frames of (inference grid + render) at 540x540
+through the device API on one stream. Usage: python tools/prof_frame.py [frames]"""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np  # noqa: E402
+
+from paper_2212_10550_b200 import arf, fixtures as fx  # noqa: E402
+from paper_2212_10550_b200._lib import check, lib  # noqa: E402
+
+
+def main(frames: int = 3):
+    L = lib()
+    sk = fx.smpl24()
+    model = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = fx.animation_poses(sk, 4)
+    cam = fx.default_camera(sk, 540, 540)
+    opt = fx.config1_render_options()
+    occ = arf.OccupancyGrid(model.normalized_box, fx.config1_occupancy())
+    views = [arf.PosedModelView(model, p) for p in poses]
+    out = arf.RenderImages(540, 540, np.zeros((540, 540, 3), np.float32), np.zeros((540, 540), np.float32))
+    for f in range(frames):
+        v = views[f % len(views)]
+        check(L.arfx_build_inference_grid(model._h, v._h, occ._h, None, None))
+        arf.render_model(model, v, cam, occ, opt, out=out)
+    print("frames", frames, "posed", model.counters.posed_queries, "alpha sum", float(out.alpha.sum()))
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
