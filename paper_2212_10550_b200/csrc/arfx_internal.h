@@ -58,6 +58,11 @@ struct PoseCtx {
   double cap_b[kMaxBones][3];
   double cutoff[kMaxBones];
   double w2n[12];
+  // Conservative f32 bounding sphere of each posed capsule's start region: centre and
+  // (half length + cutoff + 1e-4 m)^2. A target outside it is provably farther than the
+  // cutoff from the segment (triangle inequality), so the exact FP64 distance test of
+  // R/articulation.hpp:101-102 is only run for bones whose sphere contains the target.
+  float sph[kMaxBones][4];
 };
 
 struct InverseOpts {  // R/articulation.hpp:84-88

@@ -86,20 +86,38 @@ __device__ __forceinline__ void skin_eval(const SkinView& S, const PoseCtx* __re
   const int cell = (c[2] * (S.ry - 1) + c[1]) * (S.rx - 1) + c[0];
   const uint32_t mask = __ldg(S.cell_mask + cell);
   const double* vals = S.cell_vals + static_cast<size_t>(__ldg(S.cell_off + cell)) * 8;
-  // pass 1: raw interpolated weights per union bone, and their sum (bone order)
+  // pass 1: raw interpolated weights per union bone, and their sum (bone order); two
+  // bones per trip so 8 independent 16-byte loads are in flight before the math
   double sum = 0.0;
-  int j = 0;
-  for (uint32_t m = mask; m; m &= m - 1, ++j) {
+  const int nu = __popc(mask);
+  for (int j = 0; j < nu; j += 2) {
+    const bool two = j + 1 < nu;
     const double2* v2 = reinterpret_cast<const double2*>(vals + 8 * j);
     const double2 a0 = __ldg(v2 + 0), a1 = __ldg(v2 + 1), a2 = __ldg(v2 + 2), a3 = __ldg(v2 + 3);
-    const double v[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
-    double acc = 0.0;
+    double2 b0 = make_double2(0, 0), b1 = b0, b2 = b0, b3 = b0;
+    if (two) {
+      b0 = __ldg(v2 + 4);
+      b1 = __ldg(v2 + 5);
+      b2 = __ldg(v2 + 6);
+      b3 = __ldg(v2 + 7);
+    }
+    const double va[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+    const double vb[8] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x, b3.y};
+    double acc = 0.0, acc2 = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (wt[k] != 0.0) acc = dadd(acc, dmul(wt[k], v[k]));
+      if (wt[k] != 0.0) {
+        acc = dadd(acc, dmul(wt[k], va[k]));
+        acc2 = dadd(acc2, dmul(wt[k], vb[k]));
+      }
     ws[j * stride] = acc;
     sum = dadd(sum, acc);
+    if (two) {
+      ws[(j + 1) * stride] = acc2;
+      sum = dadd(sum, acc2);
+    }
   }
+  int j = 0;
   const bool renorm = sum > 0;
   const double inv = renorm ? ddiv(1.0, sum) : 1.0;
   // pass 2: normalised weights -> lbs and Jacobian

@@ -263,6 +263,13 @@ void make_pose_ctx(const std::vector<HostBone>& bones, const double* bones12, co
     ctx.cap_b[i][1] = b.y;
     ctx.cap_b[i][2] = b.z;
     ctx.cutoff[i] = cutoff_factor * bones[static_cast<size_t>(i)].radius;
+    const HV c = (a + b) * 0.5;
+    const double R = 0.5 * norm(b - a) + ctx.cutoff[i] + 1e-4;
+    const double R2 = R * R;
+    ctx.sph[i][0] = static_cast<float>(c.x);
+    ctx.sph[i][1] = static_cast<float>(c.y);
+    ctx.sph[i][2] = static_cast<float>(c.z);
+    ctx.sph[i][3] = R2 < 3.0e38 ? static_cast<float>(R2) : 3.0e38f;
   }
   for (int k = 0; k < 12; ++k) ctx.w2n[k] = pre12[k];
 }

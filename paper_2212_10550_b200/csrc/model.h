@@ -56,7 +56,7 @@ struct Workspace {
   DevBuf<float4> pres;                // (density, r, g, b) per pool entry
   DevBuf<int32_t> ray_first, ray_count, row_list;
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
-  DevBuf<uint64_t> pcg_tab;            // stratified-jitter jump table (unused for now)
+  DevBuf<uint2> work;                  // K2a -> K2b work list: (sample, start mask)
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
 };

@@ -18,6 +18,7 @@
 #include <cstdio>
 
 #include "deform.cuh"
+#include "deform_persistent.cuh"
 #include "field.cuh"
 #include "model.h"
 
@@ -214,20 +215,10 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
   }
 }
 
-// ---- K2: deformer -----------------------------------------------------------
-
-struct PoolOut {
-  uint8_t* snroot;
-  int32_t* sbase;
-  double *px, *py, *pz;
-  int32_t* powner;
-  float4* pres;
-  unsigned long long* counters;  // [1] canonical, [2] pool
-  long long cap_pool;
-  FieldView F;  // for the rare 3rd+ in-box roots (evaluated in-kernel)
-};
+// ---- K2 sources: where the posed targets x' come from ---------------------------
 
 struct ListSrc {  // posed samples from K1 or a user batch
+  static constexpr bool kSinglePose = true;
   const double *x, *y, *z;
   const unsigned long long* n_dev;  // device count (K1) or nullptr
   long long n, cap;
@@ -241,7 +232,19 @@ struct ListSrc {  // posed samples from K1 or a user batch
   }
 };
 
+struct AosSrc {  // user batch of xyz triples (inverse_lbs API / microbench)
+  static constexpr bool kSinglePose = true;
+  const double* p;
+  long long n;
+  __device__ long long count() const { return n; }
+  __device__ d3 point(long long i, int& pose) const {
+    pose = 0;
+    return make3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+  }
+};
+
 struct CellSrc {  // cell centres of an occupancy grid  R/occupancy.hpp:53-58, :141-144
+  static constexpr bool kSinglePose = true;
   int rx, ry, rz;
   double lo[3], cs[3];
   __device__ long long count() const { return static_cast<long long>(rx) * ry * rz; }
@@ -256,6 +259,7 @@ struct CellSrc {  // cell centres of an occupancy grid  R/occupancy.hpp:53-58, :
 };
 
 struct JitterSrc {  // update_training_grid draws  R/occupancy.hpp:160-166
+  static constexpr bool kSinglePose = false;
   int rx, ry, rz, n_poses;
   double lo[3], cs[3];
   uint64_t seed, step;
@@ -273,75 +277,6 @@ struct JitterSrc {  // update_training_grid draws  R/occupancy.hpp:160-166
                  dadd(lo[2], dmul(dadd(static_cast<double>(iz), jz), cs[2])));
   }
 };
-
-// rare path (3rd+ in-box root): out-of-line, generic MLP, keeps deformer registers low
-__device__ __noinline__ float4 field_query_slow(const FieldView& F, d3 x) {
-  float feats[kMaxLevels * 8];
-  if (F.F == 2) hash_encode_f2(F, x, feats);
-  else hash_encode_generic(F, x, feats);
-  float lg[kMlpGenericMaxWidth];
-  mlp_forward_generic(F, F.mlp, feats, lg);
-  return make_float4(softplus_f(lg[0]), logistic_f(lg[1]), logistic_f(lg[2]), logistic_f(lg[3]));
-}
-
-template <class Src>
-__global__ void __launch_bounds__(128) deform_kernel(SkinView S, const PoseCtx* __restrict__ poses,
-                                                     InverseOpts opt, Src src, PoolOut out) {
-  extern __shared__ double ws_smem[];
-  double* ws = ws_smem + threadIdx.x;
-  const int stride = blockDim.x;
-  const long long n = src.count();
-  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
-       s += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int pose;
-    const d3 xt = src.point(s, pose);
-    const PoseCtx* P = poses + pose;
-    Roots R;
-    inverse_lbs(S, P, opt, xt, ws, stride, R);
-    // posed_query_ctx: in-box roots in push order  R/articulation.hpp:170-173
-    int keep[kMaxRoots];
-    int nin = 0;
-    for (int k = 0; k < R.count; ++k)
-      if (field_contains(out.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]))) keep[nin++] = k;
-    out.snroot[s] = static_cast<uint8_t>(nin);
-    if (nin == 0) {
-      out.sbase[s] = -1;
-      continue;
-    }
-    atomicAdd(out.counters + 1, 1ull);
-    const int nalloc = nin < 3 ? nin : 3;
-    const long long base = static_cast<long long>(atomicAdd(out.counters + 2, static_cast<unsigned long long>(nalloc)));
-    out.sbase[s] = static_cast<int32_t>(base);
-    if (base + nalloc > out.cap_pool) {
-      atomicAdd(out.counters + 3, 1ull);  // overflow: caller regrows and reruns
-      continue;
-    }
-    for (int j = 0; j < 2 && j < nin; ++j) {
-      const int k = keep[j];
-      out.px[base + j] = R.x[k][0];
-      out.py[base + j] = R.x[k][1];
-      out.pz[base + j] = R.x[k][2];
-      out.powner[base + j] = static_cast<int32_t>(s);
-    }
-    if (nin > 2) {  // rare: evaluate roots 3.. here, keep the first max (strict >)
-      float4 best = make_float4(0.f, 0.f, 0.f, 0.f);
-      int bk = -1;
-      for (int j = 2; j < nin; ++j) {
-        const int k = keep[j];
-        const float4 v = field_query_slow(out.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]));
-        if (bk < 0 || v.x > best.x) {
-          best = v;
-          bk = k;
-        }
-      }
-      out.px[base + 2] = R.x[bk][0];
-      out.py[base + 2] = R.x[bk][1];
-      out.pz[base + 2] = R.x[bk][2];
-      out.powner[base + 2] = -1;
-      out.pres[base + 2] = best;
-    }
-  }
-}
 
 // ---- K3: field over the root pool -----------------------------------------
 
@@ -376,10 +311,9 @@ __device__ __forceinline__ int select_root(const uint8_t* snroot, const int32_t*
   const int nin = snroot[s];
   if (nin == 0) return -1;
   const int base = sbase[s];
-  const int m = nin < 3 ? nin : 3;
   int sel = 0;
   best = pres[base];
-  for (int k = 1; k < m; ++k) {
+  for (int k = 1; k < nin; ++k) {
     const float4 v = pres[base + k];
     if (v.x > best.x) {
       best = v;
@@ -581,22 +515,47 @@ int grid_for(long long n, int threads, int per_sm) {
   return static_cast<int>(std::max(1LL, std::min(want, cap)));
 }
 
-PoolOut pool_out(ModelImpl& m) {
-  Workspace& w = m.ws;
-  return PoolOut{w.snroot.ptr, w.sbase.ptr, w.px.ptr, w.py.ptr, w.pz.ptr, w.powner.ptr, w.pres.ptr,
-                 w.counters.ptr, static_cast<long long>(w.cap_pool), m.fv};
+template <class Kern>
+int persistent_grid(Kern kernel, size_t smem, long long n_hint) {
+  int per_sm = 0;
+  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDfThreads, smem));
+  per_sm = std::max(per_sm, 1);
+  const long long want = (n_hint + kDfThreads - 1) / kDfThreads;
+  return static_cast<int>(std::max(1LL, std::min(want, static_cast<long long>(sm_count()) * per_sm)));
 }
 
+// K2a prune + K2b persistent state-machine deformer (deform_persistent.cuh).
+template <class Src, class Sink>
+void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, const Sink& K, long long n_hint,
+                        const char* name, cudaStream_t s) {
+  Workspace& w = m.ws;
+  constexpr bool single = Src::kSinglePose;
+  w.work.ensure(static_cast<size_t>(std::max<long long>(n_hint, 1)));
+  const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
+  m.prof.begin("prune", s);
+  prune_kernel<Src, Sink, single><<<grid_for(n_hint, 256, 8), 256, pose_smem, s>>>(d_poses, src, K, w.work.ptr,
+                                                                                  w.counters.ptr + 5);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+  const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDfThreads * sizeof(double);
+  auto kern = deform_persistent_kernel<Src, Sink, single>;
+  const int grid = persistent_grid(kern, smem, n_hint);
+  m.prof.begin(name, s);
+  kern<<<grid, kDfThreads, smem, s>>>(m.sv, d_poses, m.inv, src, K, w.work.ptr, w.counters.ptr + 5,
+                                      w.counters.ptr + 4);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+}
+
+// K2 feeding the root pool.
 template <class Src>
 void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long long n_hint,
                    cudaStream_t s) {
-  const int threads = 128;
-  const size_t smem = static_cast<size_t>(m.sv.nb) * threads * sizeof(double);
-  m.prof.begin("deform", s);
-  deform_kernel<Src><<<grid_for(n_hint, threads, 16), threads, smem, s>>>(m.sv, d_poses, m.inv, src,
-                                                                           pool_out(m));
-  ARFX_CUDA(cudaGetLastError());
-  m.prof.end(s);
+  Workspace& w = m.ws;
+  PoolSink K{w.snroot.ptr, w.sbase.ptr, w.px.ptr, w.py.ptr, w.pz.ptr, w.powner.ptr,
+             w.counters.ptr, static_cast<long long>(w.cap_pool), m.fv};
+  launch_deform_sink(m, d_poses, src, K, n_hint, "deform", s);
 }
 
 void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
@@ -626,7 +585,9 @@ void Workspace::ensure(size_t posed, size_t pix) {
     sbase.alloc(c);
     ssel.alloc(c);
     cap_posed = c;
-    const size_t pc = c + c / 2 + 1024;
+    // root pool: <= 3 slots per sample in practice ~0.6; plus one partially used chunk per
+    // resident deformer warp (148 SMs x 64 warps x kDfPoolChunk)
+    const size_t pc = c + c / 2 + static_cast<size_t>(148) * 64 * kDfPoolChunk;
     px.alloc(pc);
     py.alloc(pc);
     pz.alloc(pc);
@@ -816,11 +777,10 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
                        int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s) {
   if (n <= 0) return;
-  const int threads = 128;
-  const size_t smem = static_cast<size_t>(m.sv.nb) * threads * sizeof(double);
-  inverse_lbs_kernel<<<grid_for(n, threads, 16), threads, smem, s>>>(m.sv, d_ctx, m.inv, d_pts, n, d_counts,
-                                                                      d_roots, d_res);
-  ARFX_CUDA(cudaGetLastError());
+  if (!m.ws.counters.ptr) m.ws.counters.alloc(8);
+  const AosSrc src{d_pts, n};
+  const RootsSink K{d_counts, d_roots, d_res};
+  launch_deform_sink(m, d_ctx, src, K, n, "inverse_lbs", s);
 }
 
 void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n, float* d_dens,
