@@ -230,6 +230,100 @@ __device__ __forceinline__ void mlp_forward_generic(const FieldView& F, const fl
   for (int q = 0; q < F.out_dim; ++q) logits[q] = cur[q];
 }
 
+// One level of HashGrid::encode for F == 2 from precomputed normalized coords u (f64).
+__device__ __forceinline__ float2 encode_level_f2(const FieldView& F, int l, const double u[3]) {
+  LevelCorners lc;
+  level_corners(F, l, u, lc);
+  const float2* t = reinterpret_cast<const float2*>(F.grid) + static_cast<size_t>(l) * F.T;
+  float2 row[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) row[k] = __ldg(t + lc.idx[k]);
+  float o0 = 0.0f, o1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o0 = fadd(o0, fmul(lc.w[k], row[k].x));
+    o1 = fadd(o1, fmul(lc.w[k], row[k].y));
+  }
+  return make_float2(o0, o1);
+}
+
+// Exact MLP, feature-major first layer: acc[o] accumulates in input order i = 0..IN-1
+// exactly as DecoderMlp::forward (R/mlp.hpp:100-104), reading inputs one at a time from
+// shared memory and W0 transposed (W0T[i][o]) so 4 consecutive outputs share an LDS.128.
+// Wr points at the flat params after W0 (b0, W1, b1, ..., W_out, b_out).
+template <int IN, int HID, int NH, int OUT>
+__device__ __forceinline__ void mlp_forward_fm(const float* __restrict__ W0T, const float* __restrict__ Wr,
+                                               const float* in, float* logits) {
+  float a[HID];
+  {
+    const float* b0 = Wr;
+#pragma unroll
+    for (int o = 0; o < HID; ++o) a[o] = b0[o];
+#pragma unroll 4
+    for (int i = 0; i < IN; ++i) {
+      const float x = in[i];
+      const float4* w4 = reinterpret_cast<const float4*>(W0T + i * HID);
+#pragma unroll
+      for (int o4 = 0; o4 < HID / 4; ++o4) {
+        const float4 q = w4[o4];
+        a[4 * o4 + 0] = fadd(a[4 * o4 + 0], fmul(q.x, x));
+        a[4 * o4 + 1] = fadd(a[4 * o4 + 1], fmul(q.y, x));
+        a[4 * o4 + 2] = fadd(a[4 * o4 + 2], fmul(q.z, x));
+        a[4 * o4 + 3] = fadd(a[4 * o4 + 3], fmul(q.w, x));
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < HID; ++o) a[o] = (a[o] < 0.0f) ? 0.0f : a[o];
+  }
+  const float* p = Wr + HID;
+#pragma unroll
+  for (int l = 1; l < NH - 1; ++l) {  // middle hidden layers (none for NH == 2)
+    float b[HID];
+    const float* bias = p + HID * HID;
+#pragma unroll
+    for (int o = 0; o < HID; ++o) {
+      float acc = bias[o];
+      const float4* wr = reinterpret_cast<const float4*>(p + o * HID);
+#pragma unroll
+      for (int i = 0; i < HID / 4; ++i) {
+        const float4 q = wr[i];
+        acc = fadd(acc, fmul(q.x, a[4 * i + 0]));
+        acc = fadd(acc, fmul(q.y, a[4 * i + 1]));
+        acc = fadd(acc, fmul(q.z, a[4 * i + 2]));
+        acc = fadd(acc, fmul(q.w, a[4 * i + 3]));
+      }
+      b[o] = (acc < 0.0f) ? 0.0f : acc;
+    }
+#pragma unroll
+    for (int o = 0; o < HID; ++o) a[o] = b[o];
+    p += HID * HID + HID;
+  }
+  const float* bias = p + HID * HID;
+  const float* wo = bias + HID;
+  const float* bo = wo + OUT * HID;
+  float out[OUT];
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) out[q] = bo[q];
+#pragma unroll 2
+  for (int o = 0; o < HID; ++o) {
+    float acc = bias[o];
+    const float4* wr = reinterpret_cast<const float4*>(p + o * HID);
+#pragma unroll
+    for (int i = 0; i < HID / 4; ++i) {
+      const float4 q = wr[i];
+      acc = fadd(acc, fmul(q.x, a[4 * i + 0]));
+      acc = fadd(acc, fmul(q.y, a[4 * i + 1]));
+      acc = fadd(acc, fmul(q.z, a[4 * i + 2]));
+      acc = fadd(acc, fmul(q.w, a[4 * i + 3]));
+    }
+    const float h = (acc < 0.0f) ? 0.0f : acc;
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) out[q] = fadd(out[q], fmul(wo[q * HID + o], h));
+  }
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) logits[q] = out[q];
+}
+
 __device__ __forceinline__ bool field_is_standard(const FieldView& F) {
   return F.F == 2 && F.L == 16 && F.in_dim == 32 && F.hidden == 64 && F.n_layers == 3 &&
          F.out_dim == 4;

@@ -279,6 +279,89 @@ struct JitterSrc {  // update_training_grid draws  R/occupancy.hpp:160-166
 };
 
 // ---- K3: field over the root pool -----------------------------------------
+//
+// Standard config (16 levels x 2 features, 32-64-64-4): tiles of 128 pool queries.
+//  1. thread q: normalized coords u of query q (3 f64 divisions, once per query);
+//  2. thread (q, level): one level of the encode -- 8 independent float2 gathers per
+//     thread, 16x more gathers in flight than a thread-per-query encode;
+//  3. thread q: exact MLP (feature-major first layer) from the shared-memory features.
+constexpr int kFieldTile = 128;
+
+template <int L, int HID>
+__global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, const double* __restrict__ px,
+                                                                const double* __restrict__ py,
+                                                                const double* __restrict__ pz,
+                                                                const int32_t* __restrict__ owner,
+                                                                float4* __restrict__ res,
+                                                                const unsigned long long* n_dev, long long cap) {
+  constexpr int IN = 2 * L;
+  extern __shared__ float4 ft_smem4[];
+  float* W0T = reinterpret_cast<float*>(ft_smem4);          // [IN][HID]
+  float* Wr = W0T + IN * HID;                                // b0, W1, b1, W2, b2
+  const int n_rest = F.n_mlp - IN * HID;
+  float* feats = Wr + ((n_rest + 3) / 4) * 4;                // [tile][IN + 1]
+  double* U = reinterpret_cast<double*>(feats + kFieldTile * (IN + 1) + (kFieldTile * (IN + 1)) % 2);  // [tile][3]
+  int* valid = reinterpret_cast<int*>(U + 3 * kFieldTile);
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  if (static_cast<long long>(blockIdx.x) * kFieldTile >= n) return;
+  for (int i = threadIdx.x; i < IN * HID; i += kFieldTile) {  // W0 transposed
+    const int o = i / IN, k = i % IN;
+    W0T[k * HID + o] = __ldg(F.mlp + i);
+  }
+  for (int i = threadIdx.x; i < n_rest; i += kFieldTile) Wr[i] = __ldg(F.mlp + IN * HID + i);
+  for (long long t0 = static_cast<long long>(blockIdx.x) * kFieldTile; t0 < n;
+       t0 += static_cast<long long>(gridDim.x) * kFieldTile) {
+    __syncthreads();
+    {
+      const long long q = t0 + threadIdx.x;
+      const bool ok = q < n && owner[q] >= 0;
+      valid[threadIdx.x] = ok;
+      if (ok) {
+        double u[3];
+        normalize_point(F, make3(px[q], py[q], pz[q]), u);
+        U[3 * threadIdx.x + 0] = u[0];
+        U[3 * threadIdx.x + 1] = u[1];
+        U[3 * threadIdx.x + 2] = u[2];
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int pass = 0; pass < L; ++pass) {
+      // warp-uniform level (no divergence on the direct/wrap/hash kind), 32 queries per warp
+      const int l = pass;
+      const int ql = threadIdx.x;
+      if (valid[ql]) {
+        const double u[3] = {U[3 * ql], U[3 * ql + 1], U[3 * ql + 2]};
+        const float2 o = encode_level_f2(F, l, u);
+        feats[ql * (IN + 1) + 2 * l] = o.x;
+        feats[ql * (IN + 1) + 2 * l + 1] = o.y;
+      }
+    }
+    __syncthreads();
+    if (valid[threadIdx.x]) {
+      float logits[4];
+      mlp_forward_fm<IN, HID, 2, 4>(W0T, Wr, feats + threadIdx.x * (IN + 1), logits);
+      res[t0 + threadIdx.x] = make_float4(softplus_f(logits[0]), logistic_f(logits[1]), logistic_f(logits[2]),
+                                          logistic_f(logits[3]));
+    }
+  }
+}
+
+bool field_is_standard_host(const FieldView& F) {
+  return F.F == 2 && F.L == 16 && F.in_dim == 32 && F.hidden == 64 && F.n_layers == 3 && F.out_dim == 4;
+}
+
+size_t field_tile_smem(const FieldView& F) {
+  const int IN = 32, HID = 64;
+  const int n_rest = F.n_mlp - IN * HID;
+  size_t b = static_cast<size_t>(IN * HID + (n_rest + 3) / 4 * 4) * 4;
+  b += static_cast<size_t>(kFieldTile * (IN + 1) + (kFieldTile * (IN + 1)) % 2) * 4;
+  b += static_cast<size_t>(3 * kFieldTile) * 8 + kFieldTile * 4;
+  return b;
+}
+
+// Generic configs: one thread per query.
 
 __global__ void __launch_bounds__(128) field_pool_kernel(FieldView F, const double* __restrict__ px,
                                                          const double* __restrict__ py,
@@ -559,6 +642,27 @@ void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long lo
 }
 
 void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
+  if (field_is_standard_host(m.fv)) {
+    static bool attr_set = false;
+    const size_t smem = field_tile_smem(m.fv);
+    auto kern = field_tile_kernel<16, 64>;
+    if (!attr_set) {
+      ARFX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      attr_set = true;
+    }
+    int per_sm = 0;
+    ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFieldTile, smem));
+    const long long tiles = (n_hint + kFieldTile - 1) / kFieldTile;
+    const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sm_count()) *
+                                                                        std::max(per_sm, 1))));
+    m.prof.begin("field", s);
+    kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
+                                         m.ws.pres.ptr, m.ws.counters.ptr + 2,
+                                         static_cast<long long>(m.ws.cap_pool));
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+    return;
+  }
   const int threads = 128;
   const size_t wbytes = static_cast<size_t>(m.fv.n_mlp) * sizeof(float);
   const int in_smem = wbytes <= 48 * 1024 ? 1 : 0;
