@@ -217,6 +217,16 @@ def run_ours(args):
         dist.barrier()
     prof = read_profile(model, L)
     check(L.arfx_profile_enable(model._h, 0))
+    # deterministic work counts of the same K frames (re-run untimed with counters on)
+    check(L.arfx_stats_enable(model._h, 1))
+    for k in range(K):
+        frame(Wm + k, Wm + K)
+    torch.cuda.synchronize()
+    stats = np.zeros(16, np.uint64)
+    check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
+    check(L.arfx_stats_enable(model._h, 0))
+    p64, p32 = C.c_double(), C.c_double()
+    check(L.arfx_pipe_peaks(C.byref(p64), C.byref(p32)))
     ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(ms))
     cnt = d_cnt.cpu().numpy()
@@ -251,7 +261,16 @@ def run_ours(args):
                 "clocks": clk, "e2e": e2e,
                 "gpu_launches": int(sum(v[1] for v in prof.values())),
                 "peaks_kind": peak_kind}
-        line["roofline"] = roofline(prof, K, posed_all / world, peaks, peak_kind)
+        rays_rank = sum(1 for y in range(H_IMG) if (y // 16) % world == rank) * W_IMG
+        dom, per_kernel = roofline(prof, stats, K, rays_rank, opt.samples_per_ray, posed, peaks, peak_kind,
+                                   (p64.value, p32.value))
+        line["roofline"] = dom
+        line["roofline_kernels"] = per_kernel
+        line["work_counts"] = {"evals": int(stats[0]), "union_bone_visits": int(stats[1]),
+                               "newton_steps": int(stats[2]), "starts": int(stats[3]),
+                               "exact_prune_tests": int(stats[4]), "field_queries": int(stats[5]),
+                               "frames": K}
+        line["pipe_peaks_tflops"] = {"fp64_addmul": p64.value, "fp32_addmul": p32.value}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
     if world > 1:
@@ -277,13 +296,49 @@ def read_profile(model, L):
     return out
 
 
-def roofline(prof, K, posed_per_frame, peaks, peak_kind):
-    """Dominant kernel vs its bound. Filled in with algorithmic work per DESIGN.md §roofline."""
-    if not prof:
-        return None
-    name, (ms, n) = max(prof.items(), key=lambda kv: kv[1][0])
-    return {"kernel": name, "ms_per_launch": ms / max(n, 1), "launches": n, "bound": None, "achieved": None,
-            "peak": None, "unit": None, "frac": None, "traffic": None, "peak_source": peak_kind}
+def ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full summaries (profiles/)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
+    """Per-kernel achieved vs bound, algorithmic work per DESIGN.md §4 (Roofline accounting).
+
+    stats (deterministic, summed over the same K frames): evals E, union-bone visits U,
+    Newton steps I, starts S, exact prune tests P, field queries Q.
+    """
+    E, U, I, S, P, Q = (float(x) for x in stats[:6])
+    fp64_peak, fp32_peak = pipe
+    traffic = ncu_traffic()
+    out = {}
+
+    def entry(name, bound, work, unit, peak, peak_src, note):
+        if name not in prof:
+            return
+        ms, n = prof[name]
+        ach = work / (ms * 1e-3) / (1e12 if unit == "TFLOP/s" else 1e9)
+        out[name] = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                     "frac": ach / peak if peak else None, "ms_per_launch": ms / max(n, 1), "launches": n,
+                     "work_per_launch": work / max(n, 1),
+                     "traffic": traffic.get(name), "peak_source": peak_src, "work": note}
+
+    f64src = "fp64 add/mul issue roof measured by bench.py (arfx_pipe_peaks; not in MEASURED_PEAKS.json)"
+    f32src = "fp32 add/mul issue roof measured by bench.py (arfx_pipe_peaks)"
+    # K2b deformer: 41/eval + 60/union bone + 66/Newton step + 18/start + 7/rejected line-search candidate
+    entry("deform", "fp64", 41 * E + 60 * U + 66 * I + 18 * S + 7 * max(E - S - I, 0.0), "TFLOP/s", fp64_peak,
+          f64src, "FP64 add/mul/div/sqrt of inverse_lbs_ctx as written (no FMA)")
+    # K3 field: exact MLP 6400 mul + 6400 add + 512 encode accumulations (f32) per query
+    entry("field", "fp32", Q * 13312, "TFLOP/s", fp32_peak, f32src, "f32 mul+add of encode+MLP, 13312/query")
+    # K1 march: ~80 FP64 per ray + 36 per sample (ray.at, to_normalized, t, cell_of)
+    entry("march", "fp64", rays * K * (80 + 36 * N), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64")
+    entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
+    hbm = peaks.get("hbm_gbs")
+    # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
+    entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
+          f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")
+    dom = max(out.values(), key=lambda e: e["ms_per_launch"] * e["launches"]) if out else None
+    return dom, out
 
 
 def run_e2e(args, model, poses, cam, opt, occ, rank, world, views):

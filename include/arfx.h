@@ -216,6 +216,14 @@ int arfx_profile_enable(arfx_model m, int on);
  * names[max][32], total ms and launch count per kernel name; *n = entries written */
 int arfx_profile_read(arfx_model m, int max, char* names, double* ms, int64_t* launches, int* n);
 
+/* deterministic work counters for roofline accounting (off by default):
+ * out[0] skinning evals, [1] union-bone visits, [2] Newton steps, [3] starts,
+ * [4] exact prune distance tests, [5] field queries. arfx_stats_read resets them. */
+int arfx_stats_enable(arfx_model m, int on);
+int arfx_stats_read(arfx_model m, uint64_t* out16);
+/* measured FP64 / FP32 add+mul issue roofs of this GPU (TFLOP/s, 1 flop per add or mul) */
+int arfx_pipe_peaks(double* fp64_tflops, double* fp32_tflops);
+
 /* ---- batched lower-level operations (host arrays in/out) ---------------- */
 int arfx_skinning_weights(arfx_model m, const double* pts, int64_t n, double* w /*n*n_bones*/);
 /* pose context built with `pre` and cutoff factor exactly as PoseContext::make;

@@ -107,6 +107,9 @@ _PROTOS = {
     "arfx_occ_rebuild_mask": (C.c_int, [H, P]),
     "arfx_build_inference_grid": (C.c_int, [H, H, H, C.POINTER(ArfxCounters), P]),
     "arfx_build_inference_grid_device": (C.c_int, [H, H, H, P, P]),
+    "arfx_stats_enable": (C.c_int, [H, C.c_int]),
+    "arfx_stats_read": (C.c_int, [H, c_uint64_p]),
+    "arfx_pipe_peaks": (C.c_int, [c_double_p, c_double_p]),
     "arfx_profile_enable": (C.c_int, [H, C.c_int]),
     "arfx_profile_read": (C.c_int, [H, C.c_int, C.c_char_p, c_double_p, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "arfx_update_training_grid": (C.c_int, [H, C.POINTER(H), C.c_int, C.c_double, C.c_uint64, C.c_uint64, H,

@@ -857,6 +857,40 @@ int arfx_profile_read(arfx_model mh, int max, char* names, double* ms, int64_t* 
   });
 }
 
+int arfx_stats_enable(arfx_model mh, int on) {
+  return guard([&] {
+    require(mh != nullptr, "stats_enable: null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (!m.stats.ptr) m.stats.alloc(16);
+    ARFX_CUDA(cudaMemset(m.stats.ptr, 0, 16 * sizeof(unsigned long long)));
+    m.stats_on = on != 0;
+  });
+}
+
+int arfx_stats_read(arfx_model mh, uint64_t* out16) {
+  return guard([&] {
+    require(mh != nullptr && out16 != nullptr, "stats_read: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    ARFX_CUDA(cudaDeviceSynchronize());
+    if (!m.stats.ptr) {
+      std::memset(out16, 0, 16 * sizeof(uint64_t));
+      return;
+    }
+    ARFX_CUDA(cudaMemcpy(out16, m.stats.ptr, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    ARFX_CUDA(cudaMemset(m.stats.ptr, 0, 16 * sizeof(unsigned long long)));
+  });
+}
+
+int arfx_pipe_peaks(double* fp64, double* fp32) {
+  return guard([&] {
+    require(fp64 && fp32, "pipe_peaks: null argument");
+    require_device();
+    measure_pipe_peaks(fp64, fp32);
+  });
+}
+
 // ---- batched helpers ------------------------------------------------------
 
 

@@ -56,9 +56,10 @@ __device__ __forceinline__ void roots_push(Roots& R, d3 p, double res, double de
 // Skinning weights at x (trilinear over the packed cell table + renormalisation),
 // then g = lbs(x) - x_target, |g| and J = sum_{w_i != 0} w_i R_i.
 // `ws` is per-thread scratch for the union bones' raw weights (smem, stride apart).
-__device__ __forceinline__ void skin_eval(const SkinView& S, const PoseCtx* __restrict__ P, d3 x,
-                                          d3 xt, double* ws, int stride, d3& g, double& gn,
-                                          double J[9]) {
+// Returns the number of union bones visited (work accounting for the roofline).
+__device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __restrict__ P, d3 x,
+                                         d3 xt, double* ws, int stride, d3& g, double& gn,
+                                         double J[9]) {
   // clamp_inside: cwise_max(lo, cwise_min(hi, x))  R/math.hpp:245-247
   double p[3] = {x.x, x.y, x.z};
   const int res[3] = {S.rx, S.ry, S.rz};
@@ -139,6 +140,7 @@ __device__ __forceinline__ void skin_eval(const SkinView& S, const PoseCtx* __re
   }
   g = sub3(out, xt);
   gn = norm3(g);
+  return nu;
 }
 
 // Skinning weights only (SkinningGrid::interpolate), dense output over n_bones.

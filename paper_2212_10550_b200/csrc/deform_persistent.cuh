@@ -41,13 +41,14 @@ __device__ __forceinline__ unsigned df_lanemask_lt() {
 }
 
 // Surviving starts of inverse_lbs_ctx: bit b set iff cap_dist(x', b) <= cutoff_b (exact).
-__device__ __forceinline__ uint32_t df_prune(const PoseCtx* __restrict__ P, d3 xt) {
+__device__ __forceinline__ uint32_t df_prune(const PoseCtx* __restrict__ P, d3 xt, int& exact_tests) {
   const float fx = static_cast<float>(xt.x), fy = static_cast<float>(xt.y), fz = static_cast<float>(xt.z);
   uint32_t mask = 0;
   for (int b = 0; b < P->nb; ++b) {
     const float dx = fx - P->sph[b][0], dy = fy - P->sph[b][1], dz = fz - P->sph[b][2];
     const float d2 = dx * dx + dy * dy + dz * dz;
     if (d2 > P->sph[b][3]) continue;  // provably pruned (see PoseCtx::sph)
+    ++exact_tests;
     const d3 ca = make3(P->cap_a[b][0], P->cap_a[b][1], P->cap_a[b][2]);
     const d3 cb = make3(P->cap_b[b][0], P->cap_b[b][1], P->cap_b[b][2]);
     if (point_segment_distance(xt, ca, cb) > P->cutoff[b]) continue;
@@ -168,12 +169,14 @@ __device__ __forceinline__ const PoseCtx* df_stage_pose(const PoseCtx* poses, do
 // K2a: prune + compaction. One thread per target, grid-stride with warp-uniform trips.
 template <class Src, class Sink, bool kSinglePose>
 __global__ void __launch_bounds__(256) prune_kernel(const PoseCtx* __restrict__ poses, Src src, Sink sink,
-                                                    uint2* __restrict__ work, unsigned long long* work_len) {
+                                                    uint2* __restrict__ work, unsigned long long* work_len,
+                                                    unsigned long long* stats) {
   extern __shared__ double pr_smem[];
   const PoseCtx* Pb = df_stage_pose<kSinglePose>(poses, pr_smem);
   const int lane = threadIdx.x & 31;
   const long long n = src.count();
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  int exact = 0;
   for (long long base = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
        base < n; base += warps * 32) {
     const long long s = base + lane;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(256) prune_kernel(const PoseCtx* __restrict__ 
     if (s < n) {
       int pose;
       const d3 xt = src.point(s, pose);
-      mask = df_prune(kSinglePose ? Pb : Pb + pose, xt);
+      mask = df_prune(kSinglePose ? Pb : Pb + pose, xt, exact);
       if (!mask) sink.empty(s);
     }
     const unsigned b = __ballot_sync(0xffffffffu, mask != 0);
@@ -191,15 +194,23 @@ __global__ void __launch_bounds__(256) prune_kernel(const PoseCtx* __restrict__ 
     off = __shfl_sync(0xffffffffu, off, 0);
     if (mask) work[off + __popc(b & df_lanemask_lt())] = make_uint2(static_cast<unsigned>(s), mask);
   }
+  if (stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
+    if (lane == 0 && exact) atomicAdd(stats + 4, static_cast<unsigned long long>(exact));
+  }
 }
 
-// K2b: the Newton state machine over the work list.
-template <class Src, class Sink, bool kSinglePose>
+// K2b: the Newton state machine over the work list. kStats: count evals / union bones /
+// Newton steps / starts into stats[0..3] (deterministic per frame; used for the roofline).
+template <class Src, class Sink, bool kSinglePose, bool kStats>
 __global__ void __launch_bounds__(kDfThreads) deform_persistent_kernel(SkinView S, const PoseCtx* __restrict__ poses,
                                                                         InverseOpts opt, Src src, Sink sink,
                                                                         const uint2* __restrict__ work,
                                                                         const unsigned long long* work_len,
-                                                                        unsigned long long* cursor) {
+                                                                        unsigned long long* cursor,
+                                                                        unsigned long long* stats) {
+  unsigned long long st_e = 0, st_u = 0, st_i = 0, st_s = 0;
   extern __shared__ double df_smem[];
   const PoseCtx* Pbase = df_stage_pose<kSinglePose>(poses, df_smem);
   double* ws = df_smem + (kSinglePose ? (sizeof(PoseCtx) + 7) / 8 : 0) + threadIdx.x;
@@ -244,6 +255,7 @@ __global__ void __launch_bounds__(kDfThreads) deform_persistent_kernel(SkinView 
             const double i6 = dmul(c2, id);
             const double i7 = dmul(dsub(dmul(J1, J6), dmul(J0, J7)), id);
             const double i8 = dmul(dsub(dmul(J0, J4), dmul(J1, J3)), id);
+            if (kStats) ++st_i;
             step = make3(dadd(dadd(dmul(i0, g.x), dmul(i1, g.y)), dmul(i2, g.z)),
                          dadd(dadd(dmul(i3, g.x), dmul(i4, g.y)), dmul(i5, g.z)),
                          dadd(dadd(dmul(i6, g.x), dmul(i7, g.y)), dmul(i8, g.z)));
@@ -261,6 +273,7 @@ __global__ void __launch_bounds__(kDfThreads) deform_persistent_kernel(SkinView 
           mask &= mask - 1;
           cand = rigid_apply((kSinglePose ? Pbase : Pbase + pose)->bone_inv[b], xt);
           state = DF_EVAL_INIT;
+          if (kStats) ++st_s;
         } else {
           fin = true;
           state = DF_NEED;
@@ -305,7 +318,11 @@ __global__ void __launch_bounds__(kDfThreads) deform_persistent_kernel(SkinView 
     // ---- B: one skinning eval per busy lane (the hot part) --------------------------
     if (state == DF_EVAL_INIT || state == DF_EVAL_LS) {
       double Jn[9];
-      skin_eval(S, kSinglePose ? Pbase : Pbase + pose, cand, xt, ws, stride, g, gcn, Jn);
+      const int nu = skin_eval(S, kSinglePose ? Pbase : Pbase + pose, cand, xt, ws, stride, g, gcn, Jn);
+      if (kStats) {
+        ++st_e;
+        st_u += static_cast<unsigned long long>(nu);
+      }
       J0 = Jn[0], J1 = Jn[1], J2 = Jn[2], J3 = Jn[3], J4 = Jn[4], J5 = Jn[5], J6 = Jn[6], J7 = Jn[7], J8 = Jn[8];
     }
 
@@ -346,6 +363,21 @@ __global__ void __launch_bounds__(kDfThreads) deform_persistent_kernel(SkinView 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) canon += __shfl_xor_sync(0xffffffffu, canon, o);
   if (lane == 0) df_add_canonical(sink, canon);
+  if (kStats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      st_e += __shfl_xor_sync(0xffffffffu, st_e, o);
+      st_u += __shfl_xor_sync(0xffffffffu, st_u, o);
+      st_i += __shfl_xor_sync(0xffffffffu, st_i, o);
+      st_s += __shfl_xor_sync(0xffffffffu, st_s, o);
+    }
+    if (lane == 0) {
+      atomicAdd(stats + 0, st_e);
+      atomicAdd(stats + 1, st_u);
+      atomicAdd(stats + 2, st_i);
+      atomicAdd(stats + 3, st_s);
+    }
+  }
 }
 
 }  // namespace arfx

@@ -83,6 +83,10 @@ struct KernelProfiler {
 struct ModelImpl {
   int device = 0;
   KernelProfiler prof;
+  // deterministic work counters (roofline accounting): [0] evals [1] union bones
+  // [2] Newton steps [3] starts [4] exact prune tests [5] field queries
+  bool stats_on = false;
+  DevBuf<unsigned long long> stats;
   cudaStream_t stream = nullptr;
   std::vector<HostBone> bones;
   GridCfg grid{};
@@ -148,6 +152,9 @@ void field_query_batch(ModelImpl& m, const double* d_pts, int64_t n, float4* d_o
 void hash_encode_batch(ModelImpl& m, const double* d_pts, int64_t n, float* d_feats,
                        int* d_domain_err, cudaStream_t s);
 void skin_weights_batch(ModelImpl& m, const double* d_pts, int64_t n, double* d_w, cudaStream_t s);
+
+// peaks.cu
+void measure_pipe_peaks(double* fp64_tflops, double* fp32_tflops);
 
 // composite.cu
 void composite_explicit(int n_rays, const int64_t* d_off, const double* d_delta, const uint8_t* d_skip,

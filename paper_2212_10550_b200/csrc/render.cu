@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, con
                                                                 const double* __restrict__ pz,
                                                                 const int32_t* __restrict__ owner,
                                                                 float4* __restrict__ res,
-                                                                const unsigned long long* n_dev, long long cap) {
+                                                                const unsigned long long* n_dev, long long cap,
+                                                                unsigned long long* stats) {
   constexpr int IN = 2 * L;
   extern __shared__ float4 ft_smem4[];
   float* W0T = reinterpret_cast<float*>(ft_smem4);          // [IN][HID]
@@ -317,6 +318,10 @@ __global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, con
       const long long q = t0 + threadIdx.x;
       const bool ok = q < n && owner[q] >= 0;
       valid[threadIdx.x] = ok;
+      if (stats) {
+        const int c = __syncthreads_count(ok);
+        if (threadIdx.x == 0 && c) atomicAdd(stats + 5, static_cast<unsigned long long>(c));
+      }
       if (ok) {
         double u[3];
         normalize_point(F, make3(px[q], py[q], pz[q]), u);
@@ -616,17 +621,18 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   w.work.ensure(static_cast<size_t>(std::max<long long>(n_hint, 1)));
   const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
+  unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
   m.prof.begin("prune", s);
   prune_kernel<Src, Sink, single><<<grid_for(n_hint, 256, 8), 256, pose_smem, s>>>(d_poses, src, K, w.work.ptr,
-                                                                                  w.counters.ptr + 5);
+                                                                                  w.counters.ptr + 5, stats);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
   const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDfThreads * sizeof(double);
-  auto kern = deform_persistent_kernel<Src, Sink, single>;
+  auto kern = stats ? deform_persistent_kernel<Src, Sink, single, true> : deform_persistent_kernel<Src, Sink, single, false>;
   const int grid = persistent_grid(kern, smem, n_hint);
   m.prof.begin(name, s);
   kern<<<grid, kDfThreads, smem, s>>>(m.sv, d_poses, m.inv, src, K, w.work.ptr, w.counters.ptr + 5,
-                                      w.counters.ptr + 4);
+                                      w.counters.ptr + 4, stats);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
@@ -658,7 +664,7 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
     m.prof.begin("field", s);
     kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
                                          m.ws.pres.ptr, m.ws.counters.ptr + 2,
-                                         static_cast<long long>(m.ws.cap_pool));
+                                         static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
     return;
