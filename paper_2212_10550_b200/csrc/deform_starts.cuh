@@ -1,0 +1,505 @@
+// deform_starts.cuh -- correspondence search (K2) as independent Newton starts, sm_100a.
+//
+// inverse_lbs_ctx (R/articulation.hpp:94-145) runs one damped-Newton solve per surviving
+// start (bone) of a posed target x', then pushes the converged ones into InverseRoots in
+// bone order (R/articulation.hpp:66-81). The solves are independent; only the push order
+// couples them. So:
+//
+//  K2a start_mask_kernel  thread per target: surviving-start mask (f32 bounding-sphere
+//                         reject + exact FP64 capsule distance), start count, and a
+//                         warp-aggregated per-bone histogram of starts.
+//  (scan)                 exclusive prefix of the start counts -> start slot of each target;
+//                         per-bone prefix -> bone-major item offsets.
+//  K2b start_scatter      item (target, bone) written bone-major: consecutive items are
+//                         spatially adjacent targets of the SAME bone, so a warp's lanes
+//                         start in the same canonical neighbourhood -> the skinning-cell
+//                         loads coalesce and the bone transforms are warp-uniform.
+//  K2c start_newton       persistent warps over the items; per-lane state machine whose
+//                         unit of progress is one skinning eval (so lanes that converge
+//                         early take a new item instead of idling); result (root, residual
+//                         or "no root") written to the start's slot.
+//  K2d finalize           thread per target: replays InverseRoots::push over its starts in
+//                         bone order (bit-exact dedup / replacement / kMaxRoots), then the
+//                         sink: in-box roots to the root pool (render / occupancy) or all
+//                         roots to [n][8] (inverse_lbs API).
+#pragma once
+
+#include "deform.cuh"
+#include "field.cuh"
+
+namespace arfx {
+
+constexpr int kDsThreads = 128;
+constexpr int kDsItemChunk = 64;
+constexpr int kItemBoneShift = 26;  // item = target | bone << 26 (targets < 2^26)
+
+enum DsState : int { DS_NEED = 0, DS_ITER = 1, DS_EVAL_INIT = 2, DS_EVAL_LS = 3, DS_DONE = 4 };
+
+__device__ __forceinline__ unsigned ds_lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <bool kSinglePose>
+__device__ __forceinline__ const PoseCtx* ds_stage_pose(const PoseCtx* poses, double* smem) {
+  if (!kSinglePose) return poses;
+  const int words = static_cast<int>(sizeof(PoseCtx) / 8);
+  const double* g = reinterpret_cast<const double*>(poses);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) smem[i] = g[i];
+  __syncthreads();
+  return reinterpret_cast<const PoseCtx*>(smem);
+}
+
+// Surviving starts: bit b set iff cap_dist(x', b) <= cutoff_b (R/articulation.hpp:101-102).
+__device__ __forceinline__ uint32_t ds_prune(const PoseCtx* __restrict__ P, d3 xt, int& exact_tests) {
+  const float fx = static_cast<float>(xt.x), fy = static_cast<float>(xt.y), fz = static_cast<float>(xt.z);
+  uint32_t mask = 0;
+  for (int b = 0; b < P->nb; ++b) {
+    const float dx = fx - P->sph[b][0], dy = fy - P->sph[b][1], dz = fz - P->sph[b][2];
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    if (d2 > P->sph[b][3]) continue;  // provably pruned (see PoseCtx::sph)
+    ++exact_tests;
+    const d3 ca = make3(P->cap_a[b][0], P->cap_a[b][1], P->cap_a[b][2]);
+    const d3 cb = make3(P->cap_b[b][0], P->cap_b[b][1], P->cap_b[b][2]);
+    if (point_segment_distance(xt, ca, cb) > P->cutoff[b]) continue;
+    mask |= 1u << b;
+  }
+  return mask;
+}
+
+// K2a
+template <class Src, bool kSinglePose>
+__global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restrict__ poses, Src src,
+                                                         uint32_t* __restrict__ mask_out,
+                                                         uint32_t* __restrict__ count_out,
+                                                         unsigned long long* __restrict__ bone_hist,
+                                                         unsigned long long* stats) {
+  extern __shared__ double sm_smem[];
+  __shared__ unsigned long long hist[kMaxBones];
+  const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sm_smem);
+  for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long n = src.count();
+  int exact = 0;
+  for (long long base = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+       base < n; base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = base + lane;
+    uint32_t mask = 0;
+    if (s < n) {
+      int pose;
+      const d3 xt = src.point(s, pose);
+      mask = ds_prune(kSinglePose ? Pb : Pb + pose, xt, exact);
+      mask_out[s] = mask;
+      count_out[s] = static_cast<uint32_t>(__popc(mask));
+    }
+    uint32_t any = mask;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+    for (uint32_t m = any; m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
+      if (lane == 0) atomicAdd(&hist[b], static_cast<unsigned long long>(__popc(bal)));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x)
+    if (hist[i]) atomicAdd(bone_hist + i, hist[i]);
+  if (stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
+    if (lane == 0 && exact) atomicAdd(stats + 4, static_cast<unsigned long long>(exact));
+  }
+}
+
+// per-bone exclusive prefix -> item offsets (one tiny block)
+__global__ void bone_offsets_kernel(const unsigned long long* __restrict__ hist, int nb,
+                                    unsigned long long* __restrict__ cursor, unsigned long long* total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long acc = 0;
+  for (int b = 0; b < nb; ++b) {
+    cursor[b] = acc;
+    acc += hist[b];
+  }
+  *total = acc;
+}
+
+// K2b: bone-major items, warp-aggregated per bone
+template <class Src>
+__global__ void __launch_bounds__(256) start_scatter_kernel(Src src, const uint32_t* __restrict__ mask_in,
+                                                            unsigned long long* __restrict__ cursor,
+                                                            uint32_t* __restrict__ items, long long cap) {
+  const int lane = threadIdx.x & 31;
+  const long long n = src.count();
+  for (long long base = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+       base < n; base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = base + lane;
+    const uint32_t mask = s < n ? mask_in[s] : 0u;
+    uint32_t any = mask;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+    for (uint32_t m = any; m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const bool has = (mask >> b) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(cursor + b, static_cast<unsigned long long>(__popc(bal)));
+      off = __shfl_sync(0xffffffffu, off, 0);
+      const long long pos = static_cast<long long>(off) + __popc(bal & ds_lanemask_lt());
+      if (has && pos < cap) items[pos] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
+    }
+  }
+}
+
+// K2c: Newton over the items. Result per start slot: root (x,y,z) and residual, or
+// residual = -1 when the start did not converge (singular / stalled / max iterations).
+template <class Src, bool kSinglePose, bool kStats>
+__global__ void __launch_bounds__(kDsThreads) start_newton_kernel(SkinView S, const PoseCtx* __restrict__ poses,
+                                                                  InverseOpts opt, Src src,
+                                                                  const uint32_t* __restrict__ items,
+                                                                  const unsigned long long* n_items,
+                                                                  const uint32_t* __restrict__ mask_in,
+                                                                  const uint32_t* __restrict__ slot_base,
+                                                                  double* __restrict__ rx, double* __restrict__ ry,
+                                                                  double* __restrict__ rz, double* __restrict__ rr,
+                                                                  unsigned long long* cursor,
+                                                                  unsigned long long* stats, long long cap) {
+  extern __shared__ double ds_smem[];
+  const PoseCtx* Pbase = ds_stage_pose<kSinglePose>(poses, ds_smem);
+  double* ws = ds_smem + (kSinglePose ? (sizeof(PoseCtx) + 7) / 8 : 0) + threadIdx.x;
+  const int stride = blockDim.x;
+  const int lane = threadIdx.x & 31;
+  long long n = static_cast<long long>(*n_items);
+  n = n < cap ? n : cap;  // on overflow the host regrows and re-runs the frame
+  unsigned long long st_e = 0, st_u = 0, st_i = 0, st_s = 0;
+
+  int state = DS_NEED;
+  long long s = 0, slot = 0;
+  int pose = 0, it = 0, h = 0;
+  d3 xt = make3(0, 0, 0), x = xt, g = xt, step = xt, cand = xt;
+  double gn = 0.0, gcn = 0.0, damp = 1.0;
+  double J0 = 0, J1 = 0, J2 = 0, J3 = 0, J4 = 0, J5 = 0, J6 = 0, J7 = 0, J8 = 0;
+  long long q_next = 0, q_end = 0;  // warp-uniform item queue
+
+  while (true) {
+    // ---- A: bring every lane to an eval (or DONE) ----
+    while (true) {
+      bool emit = false, conv = false;
+      if (state == DS_ITER) {  // Newton step with the frozen Jacobian (R/math.hpp:141-158)
+        if (it >= opt.max_iterations) {
+          emit = true;
+        } else {
+          const double c0 = dsub(dmul(J4, J8), dmul(J5, J7));
+          const double c1 = dsub(dmul(J3, J8), dmul(J5, J6));
+          const double c2 = dsub(dmul(J3, J7), dmul(J4, J6));
+          const double det = dadd(dsub(dmul(J0, c0), dmul(J1, c1)), dmul(J2, c2));
+          if (fabs(det) < 2.2250738585072014e-308 * 64) {
+            emit = true;  // singular: the start fails (R/articulation.hpp:114-118)
+          } else {
+            if (kStats) ++st_i;
+            const double id = ddiv(1.0, det);
+            const double i0 = dmul(c0, id);
+            const double i1 = dmul(dsub(dmul(J2, J7), dmul(J1, J8)), id);
+            const double i2 = dmul(dsub(dmul(J1, J5), dmul(J2, J4)), id);
+            const double i3 = dmul(dsub(dmul(J5, J6), dmul(J3, J8)), id);
+            const double i4 = dmul(dsub(dmul(J0, J8), dmul(J2, J6)), id);
+            const double i5 = dmul(dsub(dmul(J2, J3), dmul(J0, J5)), id);
+            const double i6 = dmul(c2, id);
+            const double i7 = dmul(dsub(dmul(J1, J6), dmul(J0, J7)), id);
+            const double i8 = dmul(dsub(dmul(J0, J4), dmul(J1, J3)), id);
+            step = make3(dadd(dadd(dmul(i0, g.x), dmul(i1, g.y)), dmul(i2, g.z)),
+                         dadd(dadd(dmul(i3, g.x), dmul(i4, g.y)), dmul(i5, g.z)),
+                         dadd(dadd(dmul(i6, g.x), dmul(i7, g.y)), dmul(i8, g.z)));
+            damp = 1.0;
+            h = 0;
+            cand = sub3(x, mul3(step, damp));
+            state = DS_EVAL_LS;
+          }
+        }
+      }
+      if (emit) {  // failed start
+        rr[slot] = -1.0;
+        state = DS_NEED;
+      }
+      (void)conv;
+      const bool need = state == DS_NEED;
+      const unsigned nm = __ballot_sync(0xffffffffu, need);
+      if (nm) {
+        const int k = __popc(nm);
+        const int r = __popc(nm & ds_lanemask_lt());
+        const long long avail = q_end - q_next;
+        long long id;
+        if (avail >= k) {
+          id = q_next + r;
+          q_next += k;
+        } else {
+          long long base = 0;
+          if (lane == 0) base = static_cast<long long>(atomicAdd(cursor, static_cast<unsigned long long>(kDsItemChunk)));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          id = r < avail ? q_next + r : base + (r - avail);
+          q_next = base + (k - avail);
+          q_end = base + kDsItemChunk;
+        }
+        if (need) {
+          if (id >= n) {
+            state = DS_DONE;
+          } else {
+            const uint32_t item = items[id];
+            s = item & ((1u << kItemBoneShift) - 1u);
+            const int b = static_cast<int>(item >> kItemBoneShift);
+            slot = static_cast<long long>(slot_base[s]) + __popc(mask_in[s] & ((1u << b) - 1u));
+            if (slot >= cap) slot = cap;  // overflow: scratch slot (result arrays hold cap + 1)
+            xt = src.point(s, pose);
+            cand = rigid_apply((kSinglePose ? Pbase : Pbase + pose)->bone_inv[b], xt);
+            state = DS_EVAL_INIT;
+            if (kStats) ++st_s;
+          }
+        }
+      }
+      if (!__ballot_sync(0xffffffffu, state == DS_ITER || state == DS_NEED)) break;
+    }
+    if (__all_sync(0xffffffffu, state == DS_DONE)) break;
+
+    // ---- B: one skinning eval per busy lane ----
+    if (state == DS_EVAL_INIT || state == DS_EVAL_LS) {
+      double Jn[9];
+      const int nu = skin_eval(S, kSinglePose ? Pbase : Pbase + pose, cand, xt, ws, stride, g, gcn, Jn);
+      J0 = Jn[0], J1 = Jn[1], J2 = Jn[2], J3 = Jn[3], J4 = Jn[4], J5 = Jn[5], J6 = Jn[6], J7 = Jn[7], J8 = Jn[8];
+      if (kStats) {
+        ++st_e;
+        st_u += static_cast<unsigned long long>(nu);
+      }
+    }
+
+    // ---- C: Newton / line-search bookkeeping (R/articulation.hpp:104-142) ----
+    if (state == DS_EVAL_INIT) {
+      x = cand;
+      gn = gcn;
+      if (gn < opt.tolerance) {
+        rx[slot] = x.x, ry[slot] = x.y, rz[slot] = x.z, rr[slot] = gn;
+        state = DS_NEED;
+      } else {
+        it = 0;
+        state = DS_ITER;
+      }
+    } else if (state == DS_EVAL_LS) {
+      if (gcn < gn || h == 3) {
+        if (gcn >= gn && gn >= opt.tolerance) {
+          rr[slot] = -1.0;  // stalled
+          state = DS_NEED;
+        } else {
+          x = cand;
+          gn = gcn;
+          ++it;
+          if (gn < opt.tolerance) {
+            rx[slot] = x.x, ry[slot] = x.y, rz[slot] = x.z, rr[slot] = gn;
+            state = DS_NEED;
+          } else {
+            state = DS_ITER;
+          }
+        }
+      } else {
+        damp = dmul(damp, 0.5);
+        ++h;
+        cand = sub3(x, mul3(step, damp));
+      }
+    }
+  }
+  if (kStats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      st_e += __shfl_xor_sync(0xffffffffu, st_e, o);
+      st_u += __shfl_xor_sync(0xffffffffu, st_u, o);
+      st_i += __shfl_xor_sync(0xffffffffu, st_i, o);
+      st_s += __shfl_xor_sync(0xffffffffu, st_s, o);
+    }
+    if (lane == 0) {
+      atomicAdd(stats + 0, st_e);
+      atomicAdd(stats + 1, st_u);
+      atomicAdd(stats + 2, st_i);
+      atomicAdd(stats + 3, st_s);
+    }
+  }
+}
+
+// ---- K2d finalize: InverseRoots::push replay + sink -----------------------------
+
+struct PoolSink {  // render / occupancy: in-box roots (posed_query_ctx R/articulation.hpp:170-173)
+  uint8_t* snroot;
+  int32_t* sbase;
+  double *px, *py, *pz;
+  int32_t* powner;
+  unsigned long long* counters;  // [1] canonical, [2] pool cursor, [3] overflow
+  long long cap_pool;
+  FieldView F;
+};
+
+struct RootsSink {  // batched inverse_lbs API: every root + residual, [n][8]
+  int32_t* counts;
+  double* roots;
+  double* resid;
+};
+
+__device__ __forceinline__ void ds_gather_roots(long long s, const uint32_t* mask_in, const uint32_t* slot_base,
+                                                const double* rx, const double* ry, const double* rz,
+                                                const double* rr, double dedup, Roots& R, long long cap) {
+  R.count = 0;
+  const int c = __popc(mask_in[s]);
+  const long long b0 = slot_base[s];
+  for (int j = 0; j < c && b0 + j < cap; ++j) {
+    const double r = rr[b0 + j];
+    if (r < 0.0) continue;
+    roots_push(R, make3(rx[b0 + j], ry[b0 + j], rz[b0 + j]), r, dedup);
+  }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(256) finalize_pool_kernel(Src src, const uint32_t* __restrict__ mask_in,
+                                                            const uint32_t* __restrict__ slot_base,
+                                                            const double* __restrict__ rx,
+                                                            const double* __restrict__ ry,
+                                                            const double* __restrict__ rz,
+                                                            const double* __restrict__ rr, double dedup,
+                                                            PoolSink K, long long cap) {
+  const long long n = src.count();
+  const int lane = threadIdx.x & 31;
+  unsigned canon = 0;
+  for (long long base = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+       base < n; base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = base + lane;
+    Roots R;
+    R.count = 0;
+    uint32_t inbox = 0;
+    if (s < n) {
+      ds_gather_roots(s, mask_in, slot_base, rx, ry, rz, rr, dedup, R, cap);
+      for (int k = 0; k < R.count; ++k)
+        if (field_contains(K.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]))) inbox |= 1u << k;
+    }
+    const int need = __popc(inbox);
+    int incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    long long pbase = 0;
+    if (lane == 0 && total) pbase = static_cast<long long>(atomicAdd(K.counters + 2, static_cast<unsigned long long>(total)));
+    pbase = __shfl_sync(0xffffffffu, pbase, 0);
+    if (s < n) {
+      K.snroot[s] = static_cast<uint8_t>(need);
+      if (need == 0) {
+        K.sbase[s] = -1;
+      } else {
+        ++canon;
+        long long q = pbase + incl - need;
+        K.sbase[s] = static_cast<int32_t>(q);
+        if (q + need > K.cap_pool) {
+          atomicAdd(K.counters + 3, 1ull);
+        } else {
+          for (uint32_t m = inbox; m; m &= m - 1, ++q) {
+            const int k = __ffs(m) - 1;
+            K.px[q] = R.x[k][0];
+            K.py[q] = R.x[k][1];
+            K.pz[q] = R.x[k][2];
+            K.powner[q] = static_cast<int32_t>(s);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) canon += __shfl_xor_sync(0xffffffffu, canon, o);
+  if (lane == 0 && canon) atomicAdd(K.counters + 1, static_cast<unsigned long long>(canon));
+}
+
+template <class Src>
+__global__ void __launch_bounds__(256) finalize_roots_kernel(Src src, const uint32_t* __restrict__ mask_in,
+                                                             const uint32_t* __restrict__ slot_base,
+                                                             const double* __restrict__ rx,
+                                                             const double* __restrict__ ry,
+                                                             const double* __restrict__ rz,
+                                                             const double* __restrict__ rr, double dedup,
+                                                             RootsSink K, long long cap) {
+  const long long n = src.count();
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    Roots R;
+    ds_gather_roots(s, mask_in, slot_base, rx, ry, rz, rr, dedup, R, cap);
+    K.counts[s] = R.count;
+    for (int k = 0; k < R.count; ++k) {
+      K.roots[(s * kMaxRoots + k) * 3 + 0] = R.x[k][0];
+      K.roots[(s * kMaxRoots + k) * 3 + 1] = R.x[k][1];
+      K.roots[(s * kMaxRoots + k) * 3 + 2] = R.x[k][2];
+      K.resid[s * kMaxRoots + k] = R.r[k];
+    }
+  }
+}
+
+// ---- exclusive scan of u32 counts (in place), 3 phases --------------------------------
+
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t w = lane < nw ? warp_sums[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < nw) warp_sums[lane] = wi - w;
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  const uint32_t out = warp_sums[warp] + incl - v;
+  total = warp_sums[32];
+  __syncthreads();
+  return out;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __restrict__ a, long long n,
+                                                                  uint32_t* __restrict__ block_sums) {
+  __shared__ uint32_t ws[33];
+  const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
+  const uint32_t v = i < n ? a[i] : 0u;
+  uint32_t total;
+  const uint32_t ex = block_exclusive_scan(v, ws, total);
+  if (i < n) a[i] = ex;
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restrict__ sums, long long nb,
+                                                                unsigned long long* __restrict__ grand) {
+  __shared__ uint32_t ws[33];
+  uint32_t carry = 0;
+  for (long long b0 = 0; b0 < nb; b0 += kScanBlock) {
+    const long long i = b0 + threadIdx.x;
+    const uint32_t v = i < nb ? sums[i] : 0u;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(v, ws, total);
+    if (i < nb) sums[i] = ex + carry;
+    carry += total;
+  }
+  if (threadIdx.x == 0) *grand = carry;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, long long n,
+                                                               const uint32_t* __restrict__ sums) {
+  const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
+  if (i < n) a[i] += sums[blockIdx.x];
+}
+
+}  // namespace arfx

@@ -56,9 +56,15 @@ struct Workspace {
   DevBuf<float4> pres;                // (density, r, g, b) per pool entry
   DevBuf<int32_t> ray_first, ray_count, row_list;
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
-  DevBuf<uint2> work;                  // K2a -> K2b work list: (sample, start mask)
+  // K2 start pipeline (deform_starts.cuh)
+  size_t cap_targets = 0, cap_starts = 0;
+  DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base
+  DevBuf<unsigned long long> bone_hist;       // [0,32) per-bone start counts, [32,64) item cursors
+  DevBuf<uint32_t> items;                     // bone-major (target | bone << 26)
+  DevBuf<double> rx, ry, rz, rr;              // per start slot: root, residual (-1: no root)
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
+  void ensure_starts(size_t targets);
 };
 
 // Optional per-kernel CUDA-event timing on the launching stream (bench / roofline).

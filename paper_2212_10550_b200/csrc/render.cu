@@ -18,7 +18,7 @@
 #include <cstdio>
 
 #include "deform.cuh"
-#include "deform_persistent.cuh"
+#include "deform_starts.cuh"
 #include "field.cuh"
 #include "model.h"
 
@@ -604,36 +604,76 @@ int grid_for(long long n, int threads, int per_sm) {
 }
 
 template <class Kern>
-int persistent_grid(Kern kernel, size_t smem, long long n_hint) {
+int persistent_grid(Kern kernel, int threads, size_t smem, long long n_hint) {
   int per_sm = 0;
-  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDfThreads, smem));
+  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
   per_sm = std::max(per_sm, 1);
-  const long long want = (n_hint + kDfThreads - 1) / kDfThreads;
+  const long long want = (n_hint + threads - 1) / threads;
   return static_cast<int>(std::max(1LL, std::min(want, static_cast<long long>(sm_count()) * per_sm)));
 }
 
-// K2a prune + K2b persistent state-machine deformer (deform_persistent.cuh).
+__global__ void starts_overflow_kernel(const unsigned long long* total, unsigned long long cap,
+                                       unsigned long long* overflow) {
+  if (*total > cap) *overflow += 1;
+}
+
+template <class Src>
+void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long n, cudaStream_t s) {
+  Workspace& w = m.ws;
+  finalize_pool_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.rx.ptr, w.ry.ptr,
+                                                                w.rz.ptr, w.rr.ptr, m.inv.dedup_radius, K,
+                                                                static_cast<long long>(w.cap_starts));
+  ARFX_CUDA(cudaGetLastError());
+}
+template <class Src>
+void launch_finalize(ModelImpl& m, const Src& src, const RootsSink& K, long long n, cudaStream_t s) {
+  Workspace& w = m.ws;
+  finalize_roots_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.rx.ptr, w.ry.ptr,
+                                                                 w.rz.ptr, w.rr.ptr, m.inv.dedup_radius, K,
+                                                                 static_cast<long long>(w.cap_starts));
+  ARFX_CUDA(cudaGetLastError());
+}
+
+// K2 = K2a start masks -> scan -> K2b bone-major scatter -> K2c Newton -> K2d finalize
+// (deform_starts.cuh). Counters: [4] item cursor, [6] total starts, [7] items.
 template <class Src, class Sink>
 void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, const Sink& K, long long n_hint,
                         const char* name, cudaStream_t s) {
   Workspace& w = m.ws;
   constexpr bool single = Src::kSinglePose;
-  w.work.ensure(static_cast<size_t>(std::max<long long>(n_hint, 1)));
+  const long long n = std::max<long long>(n_hint, 1);
+  w.ensure_starts(static_cast<size_t>(n));
   const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
-  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
+  unsigned long long* C = w.counters.ptr;
   unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
+  ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.bone_hist.ptr, 0, 2 * kMaxBones * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.scount.ptr, 0, static_cast<size_t>(n) * sizeof(uint32_t), s));
   m.prof.begin("prune", s);
-  prune_kernel<Src, Sink, single><<<grid_for(n_hint, 256, 8), 256, pose_smem, s>>>(d_poses, src, K, w.work.ptr,
-                                                                                  w.counters.ptr + 5, stats);
+  start_mask_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
+                                                                            w.bone_hist.ptr, stats);
+  ARFX_CUDA(cudaGetLastError());
+  const long long nb = (n + kScanBlock - 1) / kScanBlock;
+  scan_blocks_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, n, w.scan_sums.ptr);
+  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, nb, C + 6);
+  scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, n, w.scan_sums.ptr);
+  bone_offsets_kernel<<<1, 32, 0, s>>>(w.bone_hist.ptr, m.sv.nb, w.bone_hist.ptr + kMaxBones, C + 7);
+  starts_overflow_kernel<<<1, 1, 0, s>>>(C + 7, static_cast<unsigned long long>(w.cap_starts), C + 3);
+  start_scatter_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.bone_hist.ptr + kMaxBones,
+                                                               w.items.ptr, static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
-  const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDfThreads * sizeof(double);
-  auto kern = stats ? deform_persistent_kernel<Src, Sink, single, true> : deform_persistent_kernel<Src, Sink, single, false>;
-  const int grid = persistent_grid(kern, smem, n_hint);
+  const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDsThreads * sizeof(double);
+  auto kern = stats ? start_newton_kernel<Src, single, true> : start_newton_kernel<Src, single, false>;
+  const int grid = persistent_grid(kern, kDsThreads, smem, 2 * n);
   m.prof.begin(name, s);
-  kern<<<grid, kDfThreads, smem, s>>>(m.sv, d_poses, m.inv, src, K, w.work.ptr, w.counters.ptr + 5,
-                                      w.counters.ptr + 4, stats);
+  kern<<<grid, kDsThreads, smem, s>>>(m.sv, d_poses, m.inv, src, w.items.ptr, C + 7, w.smask.ptr, w.scount.ptr,
+                                      w.rx.ptr, w.ry.ptr, w.rz.ptr, w.rr.ptr, C + 4, stats,
+                                      static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+  m.prof.begin("finalize", s);
+  launch_finalize(m, src, K, n, s);
   m.prof.end(s);
 }
 
@@ -682,6 +722,26 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
 
 }  // namespace
 
+void Workspace::ensure_starts(size_t targets) {
+  if (targets > cap_targets) {
+    smask.alloc(targets);
+    scount.alloc(targets);
+    scan_sums.alloc(targets / kScanBlock + 2);
+    cap_targets = targets;
+  }
+  if (!bone_hist.ptr) bone_hist.alloc(2 * kMaxBones);
+  // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
+  const size_t want = std::max<size_t>(targets * 5 / 2, 1 << 16);
+  if (want > cap_starts) {
+    items.alloc(want);
+    rx.alloc(want + 1);
+    ry.alloc(want + 1);
+    rz.alloc(want + 1);
+    rr.alloc(want + 1);
+    cap_starts = want;
+  }
+}
+
 void Workspace::ensure(size_t posed, size_t pix) {
   if (posed > cap_posed) {
     const size_t c = posed;
@@ -695,9 +755,8 @@ void Workspace::ensure(size_t posed, size_t pix) {
     sbase.alloc(c);
     ssel.alloc(c);
     cap_posed = c;
-    // root pool: <= 3 slots per sample in practice ~0.6; plus one partially used chunk per
-    // resident deformer warp (148 SMs x 64 warps x kDfPoolChunk)
-    const size_t pc = c + c / 2 + static_cast<size_t>(148) * 64 * kDfPoolChunk;
+    // root pool: in-box roots, ~0.6 per posed sample in practice (<= 8); overflow -> regrow
+    const size_t pc = c + c / 2 + 1024;
     px.alloc(pc);
     py.alloc(pc);
     pz.alloc(pc);
