@@ -94,18 +94,21 @@ __global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restri
       mask_out[s] = mask;
       count_out[s] = static_cast<uint32_t>(__popc(mask));
     }
-    uint32_t any = mask;
+    if (bone_hist) {  // optional per-bone start histogram
+      uint32_t any = mask;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
-    for (uint32_t m = any; m; m &= m - 1) {
-      const int b = __ffs(m) - 1;
-      const unsigned bal = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
-      if (lane == 0) atomicAdd(&hist[b], static_cast<unsigned long long>(__popc(bal)));
+      for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+      for (uint32_t m = any; m; m &= m - 1) {
+        const int b = __ffs(m) - 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
+        if (lane == 0) atomicAdd(&hist[b], static_cast<unsigned long long>(__popc(bal)));
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x)
-    if (hist[i]) atomicAdd(bone_hist + i, hist[i]);
+  if (bone_hist)
+    for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x)
+      if (hist[i]) atomicAdd(bone_hist + i, hist[i]);
   if (stats) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
@@ -149,6 +152,69 @@ __global__ void __launch_bounds__(256) start_scatter_kernel(Src src, const uint3
       const long long pos = static_cast<long long>(off) + __popc(bal & ds_lanemask_lt());
       if (has && pos < cap) items[pos] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
     }
+  }
+}
+
+// Approximate (f32) skinning cell of a point: only a sort key for locality, never used
+// in the arithmetic (skin_eval recomputes the exact cell in FP64).
+__device__ __forceinline__ int approx_skin_cell(const SkinView& S, d3 x) {
+  const float p[3] = {static_cast<float>(x.x), static_cast<float>(x.y), static_cast<float>(x.z)};
+  const int res[3] = {S.rx, S.ry, S.rz};
+  int c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float lo = static_cast<float>(S.lo[a]), e = static_cast<float>(S.e[a]);
+    float u = (p[a] - lo) / e * static_cast<float>(res[a] - 1);
+    u = fminf(fmaxf(u, 0.0f), static_cast<float>(res[a] - 2));
+    c[a] = static_cast<int>(u);
+  }
+  return (c[2] * (S.ry - 1) + c[1]) * (S.rx - 1) + c[0];
+}
+
+// K2b (counting sort by (bone, skinning cell of the start point x0 = B_b^-1 x')):
+// pass 1 -- per target, per surviving bone: key, unsorted item, key histogram.
+template <class Src, bool kSinglePose>
+__global__ void __launch_bounds__(256) start_key_kernel(SkinView S, const PoseCtx* __restrict__ poses, Src src,
+                                                        const uint32_t* __restrict__ mask_in,
+                                                        const uint32_t* __restrict__ slot_base,
+                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ unsorted,
+                                                        uint32_t* __restrict__ key_hist, long long cap) {
+  extern __shared__ double sk_smem[];
+  const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sk_smem);
+  const int ncell = (S.rx - 1) * (S.ry - 1) * (S.rz - 1);
+  const long long n = src.count();
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint32_t mask = mask_in[s];
+    if (!mask) continue;
+    int pose;
+    const d3 xt = src.point(s, pose);
+    const PoseCtx* P = kSinglePose ? Pb : Pb + pose;
+    long long slot = slot_base[s];
+    for (uint32_t m = mask; m; m &= m - 1, ++slot) {
+      const int b = __ffs(m) - 1;
+      const uint32_t key = static_cast<uint32_t>(b * ncell + approx_skin_cell(S, rigid_apply(P->bone_inv[b], xt)));
+      if (slot < cap) {
+        keys[slot] = key;
+        unsorted[slot] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
+      }
+      atomicAdd(key_hist + key, 1u);
+    }
+  }
+}
+
+// pass 2 -- place each start at its key's next position (order within a key irrelevant)
+__global__ void __launch_bounds__(256) start_place_kernel(const unsigned long long* n_starts,
+                                                          const uint32_t* __restrict__ keys,
+                                                          const uint32_t* __restrict__ unsorted,
+                                                          uint32_t* __restrict__ key_cursor,
+                                                          uint32_t* __restrict__ items, long long cap) {
+  long long n = static_cast<long long>(*n_starts);
+  n = n < cap ? n : cap;
+  for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint32_t pos = atomicAdd(key_cursor + keys[j], 1u);
+    if (pos < cap) items[pos] = unsorted[j];
   }
 }
 
@@ -470,9 +536,17 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   return out;
 }
 
-__global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __restrict__ a, long long n,
+template <class Src>
+__global__ void src_count_kernel(Src src, unsigned long long* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = static_cast<unsigned long long>(src.count());
+}
+
+// n: the live element count on the device (grid sized for the capacity; blocks past n exit)
+__global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
                                                                   uint32_t* __restrict__ block_sums) {
   __shared__ uint32_t ws[33];
+  const long long n = static_cast<long long>(*n_dev);
+  if (static_cast<long long>(blockIdx.x) * kScanBlock >= n) return;
   const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
   const uint32_t v = i < n ? a[i] : 0u;
   uint32_t total;
@@ -481,9 +555,10 @@ __global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __res
   if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restrict__ sums, long long nb,
+__global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restrict__ sums, const unsigned long long* n_dev,
                                                                 unsigned long long* __restrict__ grand) {
   __shared__ uint32_t ws[33];
+  const long long nb = (static_cast<long long>(*n_dev) + kScanBlock - 1) / kScanBlock;
   uint32_t carry = 0;
   for (long long b0 = 0; b0 < nb; b0 += kScanBlock) {
     const long long i = b0 + threadIdx.x;
@@ -496,8 +571,9 @@ __global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restr
   if (threadIdx.x == 0) *grand = carry;
 }
 
-__global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, long long n,
+__global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
                                                                const uint32_t* __restrict__ sums) {
+  const long long n = static_cast<long long>(*n_dev);
   const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
   if (i < n) a[i] += sums[blockIdx.x];
 }

@@ -60,11 +60,12 @@ struct Workspace {
   size_t cap_targets = 0, cap_starts = 0;
   DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base
   DevBuf<unsigned long long> bone_hist;       // [0,32) per-bone start counts, [32,64) item cursors
-  DevBuf<uint32_t> items;                     // bone-major (target | bone << 26)
+  DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
+  DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
   DevBuf<double> rx, ry, rz, rr;              // per start slot: root, residual (-1: no root)
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
-  void ensure_starts(size_t targets);
+  void ensure_starts(size_t targets, size_t nkeys);
 };
 
 // Optional per-kernel CUDA-event timing on the launching stream (bench / roofline).

@@ -612,6 +612,8 @@ int persistent_grid(Kern kernel, int threads, size_t smem, long long n_hint) {
   return static_cast<int>(std::max(1LL, std::min(want, static_cast<long long>(sm_count()) * per_sm)));
 }
 
+__global__ void set_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+
 __global__ void starts_overflow_kernel(const unsigned long long* total, unsigned long long cap,
                                        unsigned long long* overflow) {
   if (*total > cap) *overflow += 1;
@@ -642,32 +644,42 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   Workspace& w = m.ws;
   constexpr bool single = Src::kSinglePose;
   const long long n = std::max<long long>(n_hint, 1);
-  w.ensure_starts(static_cast<size_t>(n));
+  w.ensure_starts(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1));
   const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
   unsigned long long* C = w.counters.ptr;
   unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
+  const long long nkeys = static_cast<long long>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1);
+  const long long cap = static_cast<long long>(w.cap_starts);
   ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
-  ARFX_CUDA(cudaMemsetAsync(w.bone_hist.ptr, 0, 2 * kMaxBones * sizeof(unsigned long long), s));
-  ARFX_CUDA(cudaMemsetAsync(w.scount.ptr, 0, static_cast<size_t>(n) * sizeof(uint32_t), s));
+  ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
   m.prof.begin("prune", s);
+  src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5);
+  set_u64_kernel<<<1, 1, 0, s>>>(C + 8, static_cast<unsigned long long>(nkeys));
   start_mask_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
-                                                                            w.bone_hist.ptr, stats);
+                                                                            nullptr, stats);
   ARFX_CUDA(cudaGetLastError());
+  // start slots: exclusive scan of the per-target start counts (C6 = total starts)
   const long long nb = (n + kScanBlock - 1) / kScanBlock;
-  scan_blocks_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, n, w.scan_sums.ptr);
-  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, nb, C + 6);
-  scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, n, w.scan_sums.ptr);
-  bone_offsets_kernel<<<1, 32, 0, s>>>(w.bone_hist.ptr, m.sv.nb, w.bone_hist.ptr + kMaxBones, C + 7);
-  starts_overflow_kernel<<<1, 1, 0, s>>>(C + 7, static_cast<unsigned long long>(w.cap_starts), C + 3);
-  start_scatter_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.bone_hist.ptr + kMaxBones,
-                                                               w.items.ptr, static_cast<long long>(w.cap_starts));
+  scan_blocks_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
+  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 5, C + 6);
+  scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
+  starts_overflow_kernel<<<1, 1, 0, s>>>(C + 6, static_cast<unsigned long long>(cap), C + 3);
+  // counting sort of the starts by (bone, skinning cell of x0)
+  start_key_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(
+      m.sv, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
+  const long long nbk = (nkeys + kScanBlock - 1) / kScanBlock;
+  scan_blocks_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
+  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 8, C + 9);
+  scan_add_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
+  start_place_kernel<<<grid_for(2 * n, 256, 8), 256, 0, s>>>(C + 6, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr,
+                                                            w.items.ptr, cap);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
   const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDsThreads * sizeof(double);
   auto kern = stats ? start_newton_kernel<Src, single, true> : start_newton_kernel<Src, single, false>;
   const int grid = persistent_grid(kern, kDsThreads, smem, 2 * n);
   m.prof.begin(name, s);
-  kern<<<grid, kDsThreads, smem, s>>>(m.sv, d_poses, m.inv, src, w.items.ptr, C + 7, w.smask.ptr, w.scount.ptr,
+  kern<<<grid, kDsThreads, smem, s>>>(m.sv, d_poses, m.inv, src, w.items.ptr, C + 6, w.smask.ptr, w.scount.ptr,
                                       w.rx.ptr, w.ry.ptr, w.rz.ptr, w.rr.ptr, C + 4, stats,
                                       static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
@@ -722,18 +734,21 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
 
 }  // namespace
 
-void Workspace::ensure_starts(size_t targets) {
+void Workspace::ensure_starts(size_t targets, size_t nkeys) {
   if (targets > cap_targets) {
     smask.alloc(targets);
     scount.alloc(targets);
-    scan_sums.alloc(targets / kScanBlock + 2);
     cap_targets = targets;
   }
+  key_hist.ensure(nkeys);
+  scan_sums.ensure(std::max(targets, nkeys) / kScanBlock + 2);
   if (!bone_hist.ptr) bone_hist.alloc(2 * kMaxBones);
   // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
   const size_t want = std::max<size_t>(targets * 5 / 2, 1 << 16);
   if (want > cap_starts) {
     items.alloc(want);
+    keys.alloc(want);
+    unsorted.alloc(want);
     rx.alloc(want + 1);
     ry.alloc(want + 1);
     rz.alloc(want + 1);
@@ -769,7 +784,7 @@ void Workspace::ensure(size_t posed, size_t pix) {
     ray_count.alloc(pix);
     n_pix = pix;
   }
-  if (!counters.ptr) counters.alloc(8);
+  if (!counters.ptr) counters.alloc(16);
 }
 
 void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N,
@@ -800,7 +815,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   w.ensure(static_cast<size_t>(std::max<long long>(std::min<long long>(n_rays * std::max(N, 1), 1LL << 22),
                                                    1LL << 16)),
            static_cast<size_t>(cam.width) * cam.height);
-  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
 
   MarchArgs A{};
   A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
@@ -902,7 +917,7 @@ void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d
   Workspace& w = m.ws;
   const long long n = static_cast<long long>(g.res) * g.res * g.res;
   w.ensure(static_cast<size_t>(n), 0);
-  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   CellSrc src{g.res, g.res, g.res, {}, {}};
   occ_source_common(g, src.lo, src.cs);
   launch_deform(m, p.dev.ptr, src, n, s);
@@ -928,7 +943,7 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
   ctxs.alloc(poses.size());
   for (size_t i = 0; i < poses.size(); ++i)
     ARFX_CUDA(cudaMemcpyAsync(ctxs.ptr + i, poses[i]->dev.ptr, sizeof(PoseCtx), cudaMemcpyDeviceToDevice, s));
-  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   JitterSrc src{g.res, g.res, g.res, static_cast<int>(poses.size()), {}, {}, seed, step};
   occ_source_common(g, src.lo, src.cs);
   launch_deform(m, ctxs.ptr, src, n, s);
@@ -946,7 +961,7 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
                        int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s) {
   if (n <= 0) return;
-  if (!m.ws.counters.ptr) m.ws.counters.alloc(8);
+  if (!m.ws.counters.ptr) m.ws.counters.alloc(16);
   const AosSrc src{d_pts, n};
   const RootsSink K{d_counts, d_roots, d_res};
   launch_deform_sink(m, d_ctx, src, K, n, "inverse_lbs", s);
@@ -958,7 +973,7 @@ void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n
   if (n <= 0) return;
   Workspace& w = m.ws;
   w.ensure(static_cast<size_t>(n), 0);
-  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 8 * sizeof(unsigned long long), s));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   ListSrc src{d_pts, d_pts, d_pts, nullptr, n, n};
   // ListSrc expects SoA; user batches are AoS -> split on device
   DevBuf<double> soa;
