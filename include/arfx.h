@@ -182,6 +182,8 @@ int arfx_occ_info(arfx_occ_grid g, int res[3], double box_lo[3], double box_hi[3
 int arfx_occ_download(arfx_occ_grid g, float* values, uint8_t* mask);
 int arfx_occ_upload(arfx_occ_grid g, const float* values, const uint8_t* mask);
 int arfx_occ_rebuild_mask(arfx_occ_grid g, void* stream); /* R/occupancy.hpp:87-91 */
+/* OccupancyGrid::is_occupied (R/occupancy.hpp:81-85) over a batch of normalized points */
+int arfx_occ_is_occupied(arfx_occ_grid g, const double* pts, int64_t n, uint8_t* out);
 int arfx_build_inference_grid(arfx_model m, arfx_pose p, arfx_occ_grid g, arfx_counters* c,
                               void* stream);
 /* asynchronous variant: counters (u64 x4: posed, canonical, pool, overflow) to device memory */

@@ -107,6 +107,7 @@ _PROTOS = {
     "arfx_occ_rebuild_mask": (C.c_int, [H, P]),
     "arfx_build_inference_grid": (C.c_int, [H, H, H, C.POINTER(ArfxCounters), P]),
     "arfx_build_inference_grid_device": (C.c_int, [H, H, H, P, P]),
+    "arfx_occ_is_occupied": (C.c_int, [H, c_double_p, C.c_int64, c_uint8_p]),
     "arfx_stats_enable": (C.c_int, [H, C.c_int]),
     "arfx_stats_read": (C.c_int, [H, c_uint64_p]),
     "arfx_pipe_peaks": (C.c_int, [c_double_p, c_double_p]),

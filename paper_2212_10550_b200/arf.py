@@ -401,6 +401,13 @@ class OccupancyGrid:
     def rebuild_mask(self):
         call("arfx_occ_rebuild_mask", self._h, None)
 
+    def is_occupied(self, pts_normalized) -> np.ndarray:
+        """OccupancyGrid::is_occupied (R/occupancy.hpp:81-85), batched on the GPU."""
+        p = np.ascontiguousarray(pts_normalized, np.float64).reshape(-1, 3)
+        out = np.zeros(p.shape[0], np.uint8)
+        call("arfx_occ_is_occupied", self._h, ptr(p, C.c_double), p.shape[0], ptr(out, C.c_uint8))
+        return out.astype(bool)
+
     def occupied_fraction(self) -> float:
         m = self.mask
         return float(m.sum()) / float(m.size)

@@ -857,6 +857,22 @@ int arfx_profile_read(arfx_model mh, int max, char* names, double* ms, int64_t* 
   });
 }
 
+int arfx_occ_is_occupied(arfx_occ_grid gh, const double* pts, int64_t n, uint8_t* out) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    require(n == 0 || (pts && out), "occ_is_occupied: null argument");
+    ARFX_CUDA(cudaSetDevice(g.device));
+    if (n <= 0) return;
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), nullptr);
+    DevBuf<uint8_t> o;
+    o.alloc(static_cast<size_t>(n));
+    occ_query_batch(g, P.d.ptr, n, o.ptr, nullptr);
+    d2h(out, o.ptr, static_cast<size_t>(n), nullptr);
+    ARFX_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
 int arfx_stats_enable(arfx_model mh, int on) {
   return guard([&] {
     require(mh != nullptr, "stats_enable: null model");

@@ -74,6 +74,7 @@ struct InverseOpts {  // R/articulation.hpp:84-88
 struct OccView {
   int rx, ry, rz;
   double lo[3], hi[3], e[3];
+  double inv_e[3];  // RN(1/e): fast path of the cell decision (render.cu cell_axis_fast)
   const uint8_t* mask;
 };
 

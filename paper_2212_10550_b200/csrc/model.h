@@ -149,6 +149,7 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
                           uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
                           cudaStream_t s);
 void occ_rebuild(OccImpl& g, cudaStream_t s);
+void occ_query_batch(OccImpl& g, const double* d_pts, int64_t n, uint8_t* d_out, cudaStream_t s);
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
                        int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s);
 void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n, float* d_dens,

@@ -89,7 +89,39 @@ __device__ __forceinline__ double sample_t(double tn, double step, int i, double
   return dadd(tn, dmul(dadd(static_cast<double>(i), jitter), step));
 }
 
-// OccupancyGrid::is_occupied  R/occupancy.hpp:71-85
+// Exact cell coordinate of OccupancyGrid::cell_of along one axis (R/occupancy.hpp:73-76):
+// returns -1 when the point is outside ([u < 0 || u >= 1]), else int(u * res) clamped.
+// The reference divides (u = (x - lo) / e). Only the integer decision matters here, so
+// the quotient is first formed with the precomputed reciprocal (|q - u| <= 3 ulp) and the
+// correctly rounded division is paid only when q * res lies within 1e-12 of an integer
+// (or of the 0 / 1 bounds), where the two could round to different cells.
+__device__ __forceinline__ int cell_axis_fast(double x, double lo, double e, double inv_e, int res) {
+  const double d = dsub(x, lo);
+  const double v = dmul(dmul(d, inv_e), static_cast<double>(res));
+  const double fl = floor(v);
+  const bool safe = (v - fl) > 1e-12 && (fl + 1.0 - v) > 1e-12 && fabs(d) > 1e-290;
+  if (safe) {
+    if (v < 0.0 || v >= static_cast<double>(res)) return -1;
+    const int c = static_cast<int>(fl);
+    return c > res - 1 ? res - 1 : c;
+  }
+  const double u = ddiv(d, e);
+  if (u < 0 || u >= 1) return -1;
+  const int c = static_cast<int>(dmul(u, static_cast<double>(res)));
+  return (res - 1 < c) ? res - 1 : c;
+}
+
+__device__ __forceinline__ bool occupied_fast(const OccView& g, d3 x) {
+  const int cx = cell_axis_fast(x.x, g.lo[0], g.e[0], g.inv_e[0], g.rx);
+  if (cx < 0) return false;
+  const int cy = cell_axis_fast(x.y, g.lo[1], g.e[1], g.inv_e[1], g.ry);
+  if (cy < 0) return false;
+  const int cz = cell_axis_fast(x.z, g.lo[2], g.e[2], g.inv_e[2], g.rz);
+  if (cz < 0) return false;
+  return g.mask[(static_cast<size_t>(cz) * g.ry + cy) * g.rx + cx] != 0;
+}
+
+// OccupancyGrid::is_occupied  R/occupancy.hpp:71-85 (reference form, kept for reference)
 __device__ __forceinline__ bool occupied(const OccView& g, d3 x) {
   const double u0 = ddiv(dsub(x.x, g.lo[0]), g.e[0]);
   const double u1 = ddiv(dsub(x.y, g.lo[1]), g.e[1]);
@@ -157,7 +189,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
             if (A.has_occ) {
               const double t = sample_t(R.tn, step, i, jitter_at(A, rng, i));
               const d3 xn = rigid_apply(A.w2n, add3(R.o, mul3(R.d, t)));
-              f = occupied(A.occ, xn);
+              f = occupied_fast(A.occ, xn);
             } else {
               f = true;
             }
@@ -511,6 +543,12 @@ __global__ void occ_dilate_kernel(int rx, int ry, int rz, int axis, int r, const
 }
 
 // ---- batch query kernels (API) ----------------------------------------------
+
+__global__ void occ_query_kernel(OccView g, const double* __restrict__ pts, long long n, uint8_t* out) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = occupied_fast(g, make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2])) ? 1 : 0;
+}
 
 __global__ void inverse_lbs_kernel(SkinView S, const PoseCtx* __restrict__ P, InverseOpts opt,
                                    const double* __restrict__ pts, long long n, int32_t* counts,
@@ -883,8 +921,15 @@ OccView OccImpl::view() const {
   v.e[0] = box.hi.x - box.lo.x;
   v.e[1] = box.hi.y - box.lo.y;
   v.e[2] = box.hi.z - box.lo.z;
+  for (int a = 0; a < 3; ++a) v.inv_e[a] = 1.0 / v.e[a];
   v.mask = mask.ptr;
   return v;
+}
+
+void occ_query_batch(OccImpl& g, const double* d_pts, int64_t n, uint8_t* d_out, cudaStream_t s) {
+  if (n <= 0) return;
+  occ_query_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.view(), d_pts, n, d_out);
+  ARFX_CUDA(cudaGetLastError());
 }
 
 void occ_rebuild(OccImpl& g, cudaStream_t s) {

@@ -155,6 +155,29 @@ def test_inference_grid_mask_bit_exact(models, ref):
     del gpu_grid
 
 
+def test_is_occupied_cell_boundaries(gpu):
+    """The march's division-free cell decision == the reference's exact
+    u = (x - lo) / e, int(u * res) (R/occupancy.hpp:71-85), incl. points on cell faces."""
+    lo, hi = np.array([-1.332, -0.382, -1.332]), np.array([1.332, 2.282, 1.332])
+    g = arf.OccupancyGrid(arf.Aabb(tuple(lo), tuple(hi)), arf.OccupancyConfig(resolution=64, dilation=0))
+    rng = np.random.default_rng(11)
+    g.upload(values=None, mask=(rng.uniform(size=64 ** 3) < 0.5).astype(np.uint8))
+    e = hi - lo
+    cs = e / 64
+    k = rng.integers(-2, 67, size=(20000, 3)).astype(np.float64)
+    face = lo + k * cs                                    # exactly on (computed) cell faces
+    jit = face + rng.choice([-1, 0, 1], size=face.shape) * np.spacing(np.abs(face) + 1e-300) * rng.integers(0, 4, face.shape)
+    rnd = lo - 0.05 + (e + 0.1) * rng.uniform(size=(20000, 3))
+    pts = np.concatenate([face, jit, rnd, [hi, lo, (lo + hi) / 2]])
+    u = (pts - lo) / e                                    # IEEE division, as the reference
+    inside = np.all((u >= 0) & (u < 1), axis=1)
+    c = np.minimum((u * 64).astype(np.int64), 63)
+    mask = g.mask.reshape(64, 64, 64)
+    expect = np.zeros(len(pts), bool)
+    expect[inside] = mask[c[inside, 2], c[inside, 1], c[inside, 0]] != 0
+    assert np.array_equal(g.is_occupied(pts), expect)
+
+
 @pytest.mark.parametrize("stratified", [False, True])
 def test_render_trace_parity(models, ref, stratified):
     sk, dm, rm = models
