@@ -88,8 +88,9 @@ def _p(a, t):
 
 def build(which: str = "all") -> None:
     """make -C oracle (reference part only where /root/reference exists)."""
-    targets = {"all": ["oracle"] + (["ref"] if Path("/root/reference/proj/include/arf").is_dir() else []),
-               "oracle": ["oracle"], "ref": ["ref"]}[which]
+    have_ref = Path("/root/reference/proj/include/arf").is_dir()
+    targets = {"all": ["oracle"] + (["ref", "adapter"] if have_ref else []),
+               "oracle": ["oracle"], "ref": ["ref"], "adapter": ["adapter"]}[which]
     for t in targets:
         subprocess.run(["make", "-s", "-C", str(HERE), t], check=True)
 

@@ -542,6 +542,12 @@ def composite_backward(ray_lengths, delta, skipped, density, color, epsilon: flo
     return ds, dcs
 
 
+def shard_rows(height: int, rank: int, world: int, tile: int = 16) -> list:
+    """Rows rendered by `rank` of `world`: interleaved `tile`-row tiles (tile % world == rank),
+    the same partition libarfx applies for arfx_render_model(..., rank, world, ...)."""
+    return [y for y in range(height) if (y // tile) % world == rank]
+
+
 def device_count() -> int:
     n = C.c_int()
     call("arfx_device_count", C.byref(n))

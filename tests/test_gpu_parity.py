@@ -256,3 +256,29 @@ def test_composite_explicit(gpu, ref):
         np.testing.assert_allclose(ds[sl], rds, rtol=1e-10, atol=1e-14)
         np.testing.assert_allclose(dcs[sl], rdc, rtol=1e-10, atol=1e-14)
         off += L
+
+
+def test_sharded_render_equals_full_frame(models):
+    """Row-tile shards (multi-GPU partition) rendered separately reassemble the full frame."""
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, 9)
+    cam = fx.default_camera(sk, 72, 70)
+    occ = arf.build_model_inference_grid(dm, pose, arf.OccupancyConfig())
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=4, frame_id=2)
+    full = arf.render_model(dm, pose, cam, occ, opt)
+    parts = arf.RenderImages(cam.width, cam.height, np.full((70, 72, 3), -1, np.float32),
+                             np.full((70, 72), -1, np.float32))
+    for r in range(3):
+        arf.render_model(dm, pose, cam, occ, opt, shard=r, n_shards=3, out=parts)
+    assert np.array_equal(parts.rgb, full.rgb) and np.array_equal(parts.alpha, full.alpha)
+
+
+def test_cpp_dropin_adapter():
+    """include/arfx/arf_gpu.hpp used as a reference user would (tests/cpp/adapter_parity.cpp)."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "adapter_parity"
+    if not exe.exists():
+        pytest.skip("adapter_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
