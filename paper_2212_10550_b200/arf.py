@@ -542,6 +542,38 @@ def composite_backward(ray_lengths, delta, skipped, density, color, epsilon: flo
     return ds, dcs
 
 
+def field_query_backward(model: Model, pts, d_density, d_color) -> None:
+    """CanonicalField::query_backward (R/field.hpp:91-103) over a batch; accumulates into
+    the model's gradient buffers (Model.zero_grad / Model.grads)."""
+    p = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    dd = np.ascontiguousarray(d_density, np.float32).reshape(-1)
+    dc = np.ascontiguousarray(d_color, np.float32).reshape(-1, 3)
+    call("arfx_field_query_backward", model._h, ptr(p, C.c_double), p.shape[0], ptr(dd, C.c_float),
+         ptr(dc, C.c_float))
+
+
+def train_fwd_bwd(model: Model, pose: "SkeletonPose | PosedModelView", camera: Camera,
+                  occupancy: OccupancyGrid | None, opt: RenderOptions, px, py, d_color, d_alpha):
+    """Training forward + backward for rays through pixels (px, py) with upstream dL/dC, dL/dA
+    (composed per SPEC.md:490-494); accumulates FieldGrads into the model. Returns rgb, alpha."""
+    view = pose if isinstance(pose, PosedModelView) else PosedModelView(model, pose)
+    pxa = np.ascontiguousarray(px, np.int32)
+    pya = np.ascontiguousarray(py, np.int32)
+    n = pxa.shape[0]
+    dc = np.ascontiguousarray(d_color, np.float32).reshape(n, 3)
+    da = np.ascontiguousarray(d_alpha, np.float32).reshape(n)
+    rgb = np.zeros((n, 3), np.float32)
+    alpha = np.zeros(n, np.float32)
+    cnt = L.ArfxCounters()
+    call("arfx_train_fwd_bwd", model._h, view._h, C.byref(camera.to_c()),
+         occupancy._h if occupancy is not None else None, C.byref(opt.to_c()), n, ptr(pxa, C.c_int32),
+         ptr(pya, C.c_int32), ptr(dc, C.c_float), ptr(da, C.c_float), ptr(rgb, C.c_float), ptr(alpha, C.c_float),
+         C.byref(cnt), None)
+    model.counters.posed_queries += cnt.posed_queries
+    model.counters.canonical_queries += cnt.canonical_queries
+    return rgb, alpha
+
+
 def shard_rows(height: int, rank: int, world: int, tile: int = 16) -> list:
     """Rows rendered by `rank` of `world`: interleaved `tile`-row tiles (tile % world == rank),
     the same partition libarfx applies for arfx_render_model(..., rank, world, ...)."""

@@ -1124,26 +1124,106 @@ int arfx_composite_backward(int n_rays, const int32_t* ray_len, const double* t,
   });
 }
 
+namespace {
+void ensure_grads(ModelImpl& m, cudaStream_t s) {
+  if (!m.grid_grad.ptr) {
+    m.grid_grad.alloc(m.n_grid);
+    m.mlp_grad.alloc(m.n_mlp);
+    ARFX_CUDA(cudaMemsetAsync(m.grid_grad.ptr, 0, m.n_grid * sizeof(float), s));
+    ARFX_CUDA(cudaMemsetAsync(m.mlp_grad.ptr, 0, m.n_mlp * sizeof(float), s));
+  }
+}
+}  // namespace
+
+// CanonicalField::query_backward (R/field.hpp:91-103) over a batch; accumulates into the
+// model's gradient buffers (zero them with arfx_model_zero_grad).
 int arfx_field_query_backward(arfx_model mh, const double* pts, int64_t n, const float* d_density,
                               const float* d_color) {
   return guard([&] {
-    (void)mh;
-    (void)pts;
-    (void)n;
-    (void)d_density;
-    (void)d_color;
-    throw std::runtime_error("arfx_field_query_backward: not built yet in this revision");
+    require(mh && (n == 0 || (pts && d_density && d_color)), "field_query_backward: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n <= 0) return;
+    const cudaStream_t s = m.stream;
+    ensure_grads(m, s);
+    Workspace& w = m.ws;
+    w.ensure(static_cast<size_t>(n), 0);
+    w.ensure_train();
+    std::vector<double> sx(static_cast<size_t>(n)), sy(sx.size()), sz(sx.size());
+    for (int64_t i = 0; i < n; ++i) {
+      sx[static_cast<size_t>(i)] = pts[3 * i];
+      sy[static_cast<size_t>(i)] = pts[3 * i + 1];
+      sz[static_cast<size_t>(i)] = pts[3 * i + 2];
+      const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+      if (!(x >= m.grid.box.lo.x && x <= m.grid.box.hi.x && y >= m.grid.box.lo.y && y <= m.grid.box.hi.y &&
+            z >= m.grid.box.lo.z && z <= m.grid.box.hi.z))
+        throw std::domain_error("hash grid: point outside bounding box");
+    }
+    h2d(w.px.ptr, sx.data(), sx.size(), s);
+    h2d(w.py.ptr, sy.data(), sy.size(), s);
+    h2d(w.pz.ptr, sz.data(), sz.size(), s);
+    h2d(w.pgs.ptr, d_density, static_cast<size_t>(n), s);
+    h2d(w.pgc.ptr, d_color, static_cast<size_t>(3 * n), s);
+    ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 1, static_cast<size_t>(n), s));
+    const unsigned long long cnt = static_cast<unsigned long long>(n);
+    h2d(w.counters.ptr + 2, &cnt, 1, s);
+    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(n), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
   });
 }
 
+// Training forward + backward over n rays (composed per SPEC.md:490-494; see train.cu).
 int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
                        const arfx_render_options* opt, int64_t n_rays, const int32_t* px, const int32_t* py,
                        const float* d_color, const float* d_alpha, float* rgb, float* alpha, arfx_counters* c,
                        void* stream) {
   return guard([&] {
-    (void)mh, (void)ph, (void)cam, (void)occ, (void)opt, (void)n_rays, (void)px, (void)py;
-    (void)d_color, (void)d_alpha, (void)rgb, (void)alpha, (void)c, (void)stream;
-    throw std::runtime_error("arfx_train_fwd_bwd: not built yet in this revision");
+    require(mh && ph && opt && (n_rays == 0 || (px && py && d_color && d_alpha)), "train_fwd_bwd: null argument");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_camera(hc);
+    require(opt->samples_per_ray <= 1024, "render: libarfx supports samples_per_ray <= 1024");
+    for (int64_t r = 0; r < n_rays; ++r)
+      if (px[r] < 0 || py[r] < 0 || px[r] >= hc.width || py[r] >= hc.height)
+        throw std::invalid_argument("generate_ray: pixel outside image");
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n_rays <= 0) return;
+    const cudaStream_t s = stream_of(m, stream);
+    ensure_grads(m, s);
+    Staged<int32_t> PX, PY;
+    Staged<float> DC, DA;
+    PX.up(px, static_cast<size_t>(n_rays), s);
+    PY.up(py, static_cast<size_t>(n_rays), s);
+    DC.up(d_color, static_cast<size_t>(3 * n_rays), s);
+    DA.up(d_alpha, static_cast<size_t>(n_rays), s);
+    DevBuf<float> orgb, oalpha;
+    orgb.alloc(static_cast<size_t>(3 * n_rays));
+    oalpha.alloc(static_cast<size_t>(n_rays));
+    unsigned long long hcnt[4];
+    for (int attempt = 0;; ++attempt) {
+      train_forward(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+                    opt->seed, opt->frame_id, n_rays, PX.d.ptr, PY.d.ptr, s);
+      d2h(hcnt, m.ws.counters.ptr, 4, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hcnt, rerun);
+      if (!rerun) break;
+      if (attempt == 2) throw std::runtime_error("train_fwd_bwd: workspace overflow persisted");
+    }
+    Workspace& w = m.ws;
+    w.ensure_train();
+    ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
+    train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, DC.d.ptr, DA.d.ptr, orgb.ptr,
+                    oalpha.ptr, s);
+    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
+                        w.pgc.ptr, s);
+    if (rgb) d2h(rgb, orgb.ptr, static_cast<size_t>(3 * n_rays), s);
+    if (alpha) d2h(alpha, oalpha.ptr, static_cast<size_t>(n_rays), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    if (c) {
+      c->posed_queries = hcnt[0];
+      c->canonical_queries = hcnt[1];
+    }
   });
 }
 

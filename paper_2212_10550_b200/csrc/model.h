@@ -63,9 +63,14 @@ struct Workspace {
   DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
   DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
   DevBuf<double> rx, ry, rz, rr;              // per start slot: root, residual (-1: no root)
+  // training scratch (train.cu)
+  DevBuf<double> strans;   // transmittance before each posed sample
+  DevBuf<float> pgs, pgc;  // per pool entry: dsigma, dcolor[3]
+  DevBuf<uint8_t> pflag;   // per pool entry: query_backward needed
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
   void ensure_starts(size_t targets, size_t nkeys);
+  void ensure_train();
 };
 
 // Optional per-kernel CUDA-event timing on the launching stream (bench / roofline).
@@ -160,6 +165,16 @@ void field_query_batch(ModelImpl& m, const double* d_pts, int64_t n, float4* d_o
 void hash_encode_batch(ModelImpl& m, const double* d_pts, int64_t n, float* d_feats,
                        int* d_domain_err, cudaStream_t s);
 void skin_weights_batch(ModelImpl& m, const double* d_pts, int64_t n, double* d_w, cudaStream_t s);
+
+void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N, bool stratified,
+                   uint64_t seed, uint64_t frame, long long n_rays, const int32_t* d_px, const int32_t* d_py,
+                   cudaStream_t s);
+
+// train.cu
+void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
+                     float* d_rgb, float* d_alpha, cudaStream_t s);
+void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
+                         const float* gs, const float* gc, cudaStream_t s);
 
 // peaks.cu
 void measure_pipe_peaks(double* fp64_tflops, double* fp32_tflops);

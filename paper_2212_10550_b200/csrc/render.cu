@@ -146,6 +146,8 @@ struct MarchArgs {
   uint64_t seed, frame;
   const int32_t* rows;
   int n_rows, W;
+  const int32_t *lpx, *lpy;  // list mode (training rays): ray r = (lpx[r], lpy[r]), ids = r
+  long long n_list;
   double *sx, *sy, *sz, *sdelta;
   int32_t* sray;
   int16_t* sidx;
@@ -165,19 +167,27 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
   __shared__ int wcount[kMarchWarps];
   __shared__ long long wbase[kMarchWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long n_rays = static_cast<long long>(A.n_rows) * A.W;
+  const long long n_rays = A.lpx ? A.n_list : static_cast<long long>(A.n_rows) * A.W;
   const int K = (A.N + 31) >> 5;
   for (long long g0 = static_cast<long long>(blockIdx.x) * kMarchWarps; g0 < n_rays;
        g0 += static_cast<long long>(gridDim.x) * kMarchWarps) {
     const long long r = g0 + warp;
     int count = 0;
-    int pix = -1;
+    int pix = -1, rid = -1;  // pix keys the RNG stream (R/render.hpp:201); rid indexes outputs
     RayGeom R{};
     double step = 0.0;
     Pcg32 rng{0, 0};
     if (r < n_rays) {
-      const int py = A.rows[r / A.W], px = static_cast<int>(r % A.W);
+      int px, py;
+      if (A.lpx) {
+        px = A.lpx[r];
+        py = A.lpy[r];
+      } else {
+        py = A.rows[r / A.W];
+        px = static_cast<int>(r % A.W);
+      }
       pix = py * A.W + px;
+      rid = A.lpx ? static_cast<int>(r) : pix;
       R = make_ray(A.cam, A.w2n, A.nlo, A.nhi, px, py);
       if (R.valid && A.N > 0) {
         step = ddiv(dsub(R.tf, R.tn), static_cast<double>(A.N));
@@ -215,8 +225,8 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
     if (r < n_rays) {
       const long long first = wbase[warp];
       if (lane == 0) {
-        A.ray_first[pix] = static_cast<int32_t>(first < A.cap ? first : A.cap);
-        A.ray_count[pix] = (first + count <= A.cap) ? count : 0;
+        A.ray_first[rid] = static_cast<int32_t>(first < A.cap ? first : A.cap);
+        A.ray_count[rid] = (first + count <= A.cap) ? count : 0;
       }
       if (count) {
         long long run = first;
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
               A.sy[pos] = xn.y;
               A.sz[pos] = xn.z;
               A.sdelta[pos] = delta;
-              A.sray[pos] = pix;
+              A.sray[pos] = rid;
               A.sidx[pos] = static_cast<int16_t>(i);
             }
           }
@@ -907,6 +917,68 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   if (d_counters)
     ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToDevice, s));
+}
+
+// Training forward (K1 in ray-list mode, K2, K3) for n_rays pixels (d_px, d_py on device);
+// the composite forward+backward and the field backward follow in train.cu.
+void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N, bool stratified,
+                   uint64_t seed, uint64_t frame, long long n_rays, const int32_t* d_px, const int32_t* d_py,
+                   cudaStream_t s) {
+  Workspace& w = m.ws;
+  w.ensure(static_cast<size_t>(std::max<long long>(std::min<long long>(n_rays * std::max(N, 1), 1LL << 22), 1LL << 16)),
+           static_cast<size_t>(std::max<long long>(n_rays, 1)));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
+  MarchArgs A{};
+  A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
+  for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
+  for (int k = 0; k < 12; ++k) A.w2n[k] = p.host.w2n[k];
+  A.nlo[0] = m.norm.lo.x;
+  A.nlo[1] = m.norm.lo.y;
+  A.nlo[2] = m.norm.lo.z;
+  A.nhi[0] = m.norm.hi.x;
+  A.nhi[1] = m.norm.hi.y;
+  A.nhi[2] = m.norm.hi.z;
+  A.has_occ = occ != nullptr;
+  if (occ) A.occ = occ->view();
+  A.N = N;
+  A.stratified = stratified;
+  A.seed = seed;
+  A.frame = frame;
+  A.W = cam.width;
+  A.lpx = d_px;
+  A.lpy = d_py;
+  A.n_list = n_rays;
+  A.sx = w.sx.ptr;
+  A.sy = w.sy.ptr;
+  A.sz = w.sz.ptr;
+  A.sdelta = w.sdelta.ptr;
+  A.sray = w.sray.ptr;
+  A.sidx = w.sidx.ptr;
+  A.ray_first = w.ray_first.ptr;
+  A.ray_count = w.ray_count.ptr;
+  A.counters = w.counters.ptr;
+  A.cap = static_cast<long long>(w.cap_posed);
+  if (n_rays > 0) {
+    const long long groups = (n_rays + kMarchWarps - 1) / kMarchWarps;
+    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 8));
+    m.prof.begin("march", s);
+    march_kernel<<<grid, kMarchWarps * 32, 0, s>>>(A);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+  }
+  ListSrc src{w.sx.ptr, w.sy.ptr, w.sz.ptr, w.counters.ptr, 0, static_cast<long long>(w.cap_posed)};
+  launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s);
+  launch_field_pool(m, s, static_cast<long long>(w.cap_pool));
+  finalize_counters_kernel<<<1, 1, 0, s>>>(w.counters.ptr, static_cast<long long>(w.cap_posed));
+}
+
+void Workspace::ensure_train() {
+  if (strans.n < cap_posed) strans.alloc(cap_posed);
+  if (pgs.n < cap_pool) {
+    pgs.alloc(cap_pool);
+    pgc.alloc(3 * cap_pool);
+    pflag.alloc(cap_pool);
+  }
 }
 
 OccView OccImpl::view() const {
