@@ -59,24 +59,23 @@ class ClockSampler:
         self._t = None
 
     def start(self):
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([s.strip() for s in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        try:  # nvidia-smi's own sampling loop (every 50 ms) for the whole timed region
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._p = None
+        time.sleep(0.3)  # first sample lands before the timed region starts
 
     def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        time.sleep(0.1)
+        if getattr(self, "_p", None) is not None:
+            self._p.terminate()
+            try:
+                out, _ = self._p.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.rows = [[s.strip() for s in ln.split(",")] for ln in out.splitlines() if ln.strip()]
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         reasons = set()
@@ -273,6 +272,9 @@ def run_ours(args):
         line["pipe_peaks_tflops"] = {"fp64_addmul": p64.value, "fp32_addmul": p32.value}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
+        if world == 1 and not args.no_extra:
+            line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
+                                     "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline)}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -368,6 +370,120 @@ def run_e2e(args, model, poses, cam, opt, occ, rank, world, views):
             "d2h_bytes_per_step": rows * W_IMG * 16 + 32, "steps": K}
 
 
+def bench_microbench(steps: int, with_cpu: bool):
+    """BASELINE configs[1]: Fast-SNARF correspondence search, 1 M posed points x 9 starts
+    (9-bone default figure, 32^3 skinning grid, PoseContext with cutoff_factor 1e30)."""
+    import torch
+    from paper_2212_10550_b200 import arf, fixtures as fx
+    from paper_2212_10550_b200._lib import check, lib
+    L = lib()
+    sk9 = fx.default_figure_skeleton(9)
+    tiny = arf.HashGridConfig(levels=2, features_per_level=2, table_size_log2=10, base_resolution=4, max_resolution=8)
+    model = arf.build_model(sk9, tiny, arf.MlpConfig(4, 16, 1, 4), (32, 32, 32), 1)
+    pose = fx.microbench_pose(sk9)
+    n = 1_000_000
+    pts = fx.microbench_points(sk9, pose, n)
+    h = C.c_void_p()
+    pre = arf.rigid()
+    check(L.arfx_pose_create_context(model._h, arf.ptr(pose.bone_transforms, C.c_double), arf.ptr(pre, C.c_double),
+                                     1e30, C.byref(h)))
+    stream = torch.cuda.current_stream()
+    d_pts = torch.from_numpy(pts).cuda()
+    d_cnt = torch.zeros(n, dtype=torch.int32, device="cuda")
+    d_roots = torch.zeros(n * 8 * 3, dtype=torch.float64, device="cuda")
+    d_res = torch.zeros(n * 8, dtype=torch.float64, device="cuda")
+    sp = C.c_void_p(stream.cuda_stream)
+
+    def run():
+        check(L.arfx_inverse_lbs_device(model._h, h, C.c_void_p(d_pts.data_ptr()), n, C.c_void_p(d_cnt.data_ptr()),
+                                        C.c_void_p(d_roots.data_ptr()), C.c_void_p(d_res.data_ptr()), sp))
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    roots = d_cnt.cpu().numpy()
+    out = {"workload": "BASELINE configs[1]: 1M posed points x 9 starts, 32^3 skinning grid (9-bone figure)",
+           "points_per_s": n / (ms * 1e-3), "starts_per_s": 9 * n / (ms * 1e-3), "ms_per_call": ms,
+           "mean_roots_per_point": float(roots.mean())}
+    if with_cpu:
+        try:
+            from oracle.oracle_ctypes import Checker
+            ref = Checker("ref")
+            rm = ref.build_model(sk9, tiny, arf.MlpConfig(4, 16, 1, 4), (32, 32, 32), 1)
+            k = 200_000
+            t0 = time.perf_counter()
+            rc, _, _ = ref.inverse_lbs(rm, pose.bone_transforms, pre, 1e30, pts[:k])
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"points_per_s": k / dt, "cores": ref.thread_count(), "kind": "reference",
+                                   "sample": f"first {k} of the 1M points, arf::inverse_lbs_ctx via parallel_for"}
+            out["roots_match_reference_on_sample"] = bool(np.array_equal(rc, roots[:k]))
+        except Exception as e:
+            out["cpu_baseline"] = {"unavailable": str(e)}
+    L.arfx_pose_destroy(h)
+    return out
+
+
+def bench_train(model, steps: int, with_cpu: bool):
+    """BASELINE configs[2]: one training step = 4096 rays fwd+bwd through deformer / hash grid /
+    MLP / compositing (stratified, training grid after one update over 8 poses), through the
+    public host API (pixels + upstream gradients in, rgb/alpha out, grads on the device)."""
+    import torch
+    from paper_2212_10550_b200 import arf, fixtures as fx
+    sk = fx.smpl24()
+    cam = fx.default_camera(sk, W_IMG, H_IMG)
+    poses = [fx.random_pose(sk, 100 + i) for i in range(8)]
+    grid = arf.OccupancyGrid(model.normalized_box, fx.config1_occupancy())
+    arf.update_training_grid(model, grid, poses, 0.95, 7, 0)
+    rng = fx.keyed_rng(9, 1)
+    n = 4096
+    px = np.empty(n, np.int32)
+    py = np.empty(n, np.int32)
+    for k in range(n):
+        px[k] = rng.next_below(W_IMG)
+        py[k] = rng.next_below(H_IMG)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=3, frame_id=0)
+    dC = np.ones((n, 3), np.float32)
+    dA = np.ones(n, np.float32)
+    view = arf.PosedModelView(model, poses[0])
+    for i in range(2):
+        model.zero_grad()
+        arf.train_fwd_bwd(model, view, cam, grid, opt, px, py, dC, dA)
+    torch.cuda.synchronize()
+    c0 = model.counters.posed_queries
+    t0 = time.perf_counter()
+    for i in range(steps):
+        view.update(poses[i % 8])
+        model.zero_grad()
+        arf.train_fwd_bwd(model, view, cam, grid, opt, px, py, dC, dA)
+    dt = time.perf_counter() - t0
+    posed = model.counters.posed_queries - c0
+    out = {"workload": "BASELINE configs[2]: 4096-ray training step (fwd+bwd, zero-grad included; no optimizer, "
+                       "as in the reference composition)", "iters_per_s": steps / dt, "ms_per_iter": 1000 * dt / steps,
+           "posed_samples_per_iter": posed / steps}
+    if with_cpu:
+        try:
+            from oracle.oracle_ctypes import Checker
+            ref = Checker("ref")
+            rm = ref.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+            rg = ref.occ_empty(rm.norm_lo[:], rm.norm_hi[:], fx.config1_occupancy())
+            ref.update_training_grid(rm, [p.bone_transforms for p in poses], [p.global_transform for p in poses],
+                                     0.95, 7, 0, rg)
+            t0 = time.perf_counter()
+            ref.train_fwd_bwd(rm, poses[0].bone_transforms, poses[0].global_transform, cam, rg, opt, px, py, dC, dA)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"iters_per_s": 1.0 / dt, "cores": 1, "kind": "reference",
+                                   "sample": "1 step of the reference pieces composed serially (oracle/ref_driver.cpp)"}
+        except Exception as e:
+            out["cpu_baseline"] = {"unavailable": str(e)}
+    return out
+
+
 def cpu_baseline():
     try:
         secs, posed, threads = reference_frames(2)
@@ -382,10 +498,11 @@ def cpu_baseline():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100, help="timed frames (default: the 100-frame animation)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

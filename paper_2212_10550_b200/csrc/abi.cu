@@ -216,6 +216,7 @@ OccImpl& occ_ref(arfx_occ_grid g) {
 void check_overflow_and_grow(ModelImpl& m, const unsigned long long* c, bool& rerun) {
   rerun = false;
   Workspace& w = m.ws;
+  if (c[6] > w.cap_starts) w.learned_starts = static_cast<size_t>(c[6] + c[6] / 4 + 1024);
   if (c[0] > w.cap_posed || c[3] > 0 || c[2] > w.cap_pool) {
     const size_t need = static_cast<size_t>(std::max<unsigned long long>(c[0], w.cap_posed));
     w.cap_posed = 0;  // force reallocation
@@ -657,8 +658,8 @@ int arfx_build_inference_grid(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, arf
     const cudaStream_t s = stream_of(m, stream);
     for (int attempt = 0; attempt < 3; ++attempt) {
       inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
-      unsigned long long hc[4];
-      d2h(hc, m.ws.counters.ptr, 4, s);
+      unsigned long long hc[8];
+      d2h(hc, m.ws.counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -705,8 +706,8 @@ int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses
       if (attempt)
         ARFX_CUDA(cudaMemcpyAsync(g.values.ptr, saved.ptr, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
       training_grid_update(m, ps, decay, seed, step, g, nullptr, s);
-      unsigned long long hc[4];
-      d2h(hc, m.ws.counters.ptr, 4, s);
+      unsigned long long hc[8];
+      d2h(hc, m.ws.counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -755,8 +756,8 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
       render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
                    opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, t_rb->rgb.ptr,
                    t_rb->alpha.ptr, nullptr, s);
-      unsigned long long hcnt[4];
-      d2h(hcnt, m.ws.counters.ptr, 4, s);
+      unsigned long long hcnt[8];
+      d2h(hcnt, m.ws.counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hcnt, rerun);
@@ -1033,8 +1034,8 @@ int arfx_posed_query(arfx_model mh, arfx_pose ph, const double* pts, int64_t n, 
     dh.alloc(static_cast<size_t>(n));
     for (int attempt = 0; attempt < 3; ++attempt) {
       posed_query_batch(m, ph->impl, P.d.ptr, n, dd.ptr, dcl.ptr, dcan.ptr, dh.ptr, nullptr, m.stream);
-      unsigned long long hc[4];
-      d2h(hc, m.ws.counters.ptr, 4, m.stream);
+      unsigned long long hc[8];
+      d2h(hc, m.ws.counters.ptr, 8, m.stream);
       ARFX_CUDA(cudaStreamSynchronize(m.stream));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -1199,11 +1200,11 @@ int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx
     DevBuf<float> orgb, oalpha;
     orgb.alloc(static_cast<size_t>(3 * n_rays));
     oalpha.alloc(static_cast<size_t>(n_rays));
-    unsigned long long hcnt[4];
+    unsigned long long hcnt[8];
     for (int attempt = 0;; ++attempt) {
       train_forward(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
                     opt->seed, opt->frame_id, n_rays, PX.d.ptr, PY.d.ptr, s);
-      d2h(hcnt, m.ws.counters.ptr, 4, s);
+      d2h(hcnt, m.ws.counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hcnt, rerun);

@@ -69,7 +69,8 @@ struct Workspace {
   DevBuf<uint8_t> pflag;   // per pool entry: query_backward needed
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
-  void ensure_starts(size_t targets, size_t nkeys);
+  size_t learned_starts = 0;  // raised when a frame overflowed the start slots
+  void ensure_starts(size_t targets, size_t nkeys, size_t min_starts = 0);
   void ensure_train();
 };
 

@@ -692,7 +692,11 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   Workspace& w = m.ws;
   constexpr bool single = Src::kSinglePose;
   const long long n = std::max<long long>(n_hint, 1);
-  w.ensure_starts(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1));
+  // the batched inverse_lbs API runs asynchronously and cannot re-run: size its start slots
+  // for the worst case (every bone survives pruning); render/occupancy learn from overflow
+  const size_t worst = std::is_same<Sink, RootsSink>::value ? static_cast<size_t>(n) * m.sv.nb : 0;
+  w.ensure_starts(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1),
+                  worst);
   const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
   unsigned long long* C = w.counters.ptr;
   unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
@@ -782,7 +786,7 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
 
 }  // namespace
 
-void Workspace::ensure_starts(size_t targets, size_t nkeys) {
+void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
   if (targets > cap_targets) {
     smask.alloc(targets);
     scount.alloc(targets);
@@ -792,7 +796,7 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys) {
   scan_sums.ensure(std::max(targets, nkeys) / kScanBlock + 2);
   if (!bone_hist.ptr) bone_hist.alloc(2 * kMaxBones);
   // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
-  const size_t want = std::max<size_t>(targets * 5 / 2, 1 << 16);
+  const size_t want = std::max<size_t>({targets * 5 / 2, static_cast<size_t>(1) << 16, min_starts, learned_starts});
   if (want > cap_starts) {
     items.alloc(want);
     keys.alloc(want);

@@ -62,6 +62,25 @@ def keyed_rng(seed: int, a: int, b: int = 0, c: int = 0) -> Pcg32:  # R/rng.hpp:
     return Pcg32(mix_key(seed, a, b), mix_key(c, a ^ 0x5851F42D4C957F2D, seed))
 
 
+def pcg_stream_u32(rng: Pcg32, count: int) -> np.ndarray:
+    """The next `count` outputs of `rng` (vectorised; identical to calling next_u32 in a
+    loop). State k = A_k*s0 + inc*S_k (mod 2^64), A_k = mult^k, S_k = sum_{j<k} mult^j."""
+    with np.errstate(over="ignore"):
+        mult = np.full(count, PCG_MULT, np.uint64)
+        mult[0] = 1
+        A = np.cumprod(mult, dtype=np.uint64)              # mult^k, wraps mod 2^64
+        S = np.concatenate([np.zeros(1, np.uint64), np.cumsum(A[:-1], dtype=np.uint64)])
+        old = A * np.uint64(rng.state) + S * np.uint64(rng.inc)
+        xs = (((old >> np.uint64(18)) ^ old) >> np.uint64(27)) & np.uint64(0xFFFFFFFF)
+        rot = old >> np.uint64(59)
+        out = ((xs >> rot) | (xs << ((np.uint64(32) - rot) & np.uint64(31)))) & np.uint64(0xFFFFFFFF)
+    # advance the Python generator past the consumed draws
+    st = rng.state
+    a_n, s_n = int(A[-1]) * PCG_MULT % (1 << 64), (int(S[-1]) + int(A[-1])) % (1 << 64)
+    rng.state = (a_n * st + s_n * rng.inc) % (1 << 64)
+    return out.astype(np.uint64)
+
+
 # ---- rotation helpers (R/math.hpp:160-173, :210-212) -------------------------
 
 def axis_angle(a, angle: float) -> np.ndarray:
@@ -223,21 +242,15 @@ def microbench_points(skel9: Skeleton, pose: SkeletonPose, n: int, seed: int = 5
     around the POSED segment B_i(head) + (B_i(tail) - B_i(head)) * u."""
     rng = keyed_rng(seed, stream)
     nb = skel9.bone_count()
-    heads, tails = [], []
-    for i, b in enumerate(skel9.bones):
-        T = pose.bone_transforms[i]
-        heads.append(_apply(T, b.head))
-        tails.append(_apply(T, b.tail))
-    out = np.empty((n, 3), np.float64)
-    for k in range(n):
-        seg = rng.next_below(nb)
-        u = rng.next_double()
-        jx = rng.uniform(-0.06, 0.06)
-        jy = rng.uniform(-0.06, 0.06)
-        jz = rng.uniform(-0.06, 0.06)
-        a, b = heads[seg], tails[seg]
-        out[k] = (a[0] + (b[0] - a[0]) * u + jx, a[1] + (b[1] - a[1]) * u + jy, a[2] + (b[2] - a[2]) * u + jz)
-    return out
+    heads = np.array([_apply(pose.bone_transforms[i], b.head) for i, b in enumerate(skel9.bones)])
+    tails = np.array([_apply(pose.bone_transforms[i], b.tail) for i, b in enumerate(skel9.bones)])
+    d = pcg_stream_u32(rng, 5 * n).reshape(n, 5)
+    seg = ((d[:, 0] * np.uint64(nb)) >> np.uint64(32)).astype(np.int64)      # next_below
+    u = d[:, 1].astype(np.float64) * 2.0 ** -32                              # next_double
+    span = 0.06 - (-0.06)
+    j = -0.06 + span * (d[:, 2:5].astype(np.float64) * 2.0 ** -32)           # uniform(-.06, .06)
+    a, b = heads[seg], tails[seg]
+    return a + (b - a) * u[:, None] + j
 
 
 def _apply(T, x):

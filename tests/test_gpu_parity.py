@@ -126,6 +126,22 @@ def test_inverse_lbs_roots_bit_exact(models, ref):
     assert (cnt > 0).mean() > 0.5
 
 
+def test_microbench_roots_bit_exact(gpu, ref):
+    """BASELINE configs[1] shape: 9-bone figure, 32^3 grid, cutoff 1e30 (every bone is a start)."""
+    sk9 = fx.default_figure_skeleton(9)
+    tiny = arf.HashGridConfig(levels=2, features_per_level=2, table_size_log2=10, base_resolution=4, max_resolution=8)
+    dm = gpu.build_model(sk9, tiny, arf.MlpConfig(4, 16, 1, 4), (32, 32, 32), 1)
+    rm = ref.build_model(sk9, tiny, arf.MlpConfig(4, 16, 1, 4), (32, 32, 32), 1)
+    pose = fx.microbench_pose(sk9)
+    pts = fx.microbench_points(sk9, pose, 30000)
+    cnt, roots, res = dm.inverse_lbs(pose, pts, arf.rigid(), 1e30)
+    rcnt, rroots, rres = ref.inverse_lbs(rm, pose.bone_transforms, arf.rigid(), 1e30, pts)
+    assert np.array_equal(cnt, rcnt)
+    k = np.arange(8)[None, :] < cnt[:, None]
+    assert np.array_equal(roots[k].view(np.uint64), rroots[k].view(np.uint64))
+    assert np.array_equal(res[k].view(np.uint64), rres[k].view(np.uint64))
+
+
 def test_posed_query(models, ref):
     sk, dm, rm = models
     pose = fx.random_pose(sk, 5)

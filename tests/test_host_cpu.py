@@ -96,6 +96,14 @@ def test_no_cpu_fallback_without_gpu():
         arf.composite([1], [0.1], [0], np.ones(1, np.float32), np.ones((1, 3), np.float32), 1e-3)
 
 
+def test_vectorised_pcg_stream():
+    import numpy as np
+    r1, r2 = fx.keyed_rng(5, 5), fx.keyed_rng(5, 5)
+    v = fx.pcg_stream_u32(r1, 5000)
+    w = np.array([r2.next_u32() for _ in range(5000)], np.uint64)
+    assert np.array_equal(v, w) and r1.state == r2.state and r1.next_u32() == r2.next_u32()
+
+
 def test_fixture_pcg_matches_reference_stream(oracle):
     """Python keyed_rng restatement == the C one (used for poses / microbench points)."""
     # oracle hashes: identical builds from the same seed => same PCG stream
