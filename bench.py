@@ -183,6 +183,7 @@ def run_ours(args):
     L = lib()
 
     # size the workspace through the synchronous API once (overflow-checked)
+    model.set_mlp_mode(args.mlp)
     arf.render_model(model, views[0], cam, occ, opt, rank, world)
 
     def frame(i, slot):
@@ -192,6 +193,17 @@ def run_ours(args):
         check(L.arfx_render_model_device(model._h, v._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
                                          C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
                                          C.c_void_p(d_cnt[slot, 1].data_ptr()), sp))
+
+    def timed_frames(k0, n):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        torch.cuda.synchronize()
+        for k in range(n):
+            flush.zero_()
+            evs[k][0].record(stream)
+            frame(k0 + k, k0 + k)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        return float(sum(a.elapsed_time(b) for a, b in evs))
 
     for i in range(Wm):
         frame(i, i)
@@ -245,6 +257,18 @@ def run_ours(args):
     # e2e through the host-buffer public API
     e2e = run_e2e(args, model, poses, cam, opt, occ, rank, world, views)
 
+    # the same frames with the other render decoder (exact f32 SIMT MLP vs tcgen05)
+    other = "exact" if args.mlp == "tcgen05" else "tcgen05"
+    model.set_mlp_mode(other)
+    for i in range(2):
+        frame(i, i)
+    ms_other = timed_frames(Wm, K)
+    if world > 1:
+        t2 = torch.tensor([ms_other], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        ms_other = float(t2[0])
+    model.set_mlp_mode(args.mlp)
+
     line = None
     if rank == 0:
         peaks, peak_kind = measured_peaks()
@@ -259,7 +283,9 @@ def run_ours(args):
                 "kernels_ms_per_frame": {k: v[0] / K for k, v in prof.items()},
                 "clocks": clk, "e2e": e2e,
                 "gpu_launches": int(sum(v[1] for v in prof.values())),
-                "peaks_kind": peak_kind}
+                "peaks_kind": peak_kind,
+                "render_decoder": args.mlp,
+                "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}
         rays_rank = sum(1 for y in range(H_IMG) if (y // 16) % world == rank) * W_IMG
         dom, per_kernel = roofline(prof, stats, K, rays_rank, opt.samples_per_ray, posed, peaks, peak_kind,
                                    (p64.value, p32.value))
@@ -268,6 +294,7 @@ def run_ours(args):
         line["work_counts"] = {"evals": int(stats[0]), "union_bone_visits": int(stats[1]),
                                "newton_steps": int(stats[2]), "starts": int(stats[3]),
                                "exact_prune_tests": int(stats[4]), "field_queries": int(stats[5]),
+                               "field_queries_tcgen05": int(stats[6]),
                                "frames": K}
         line["pipe_peaks_tflops"] = {"fp64_addmul": p64.value, "fp32_addmul": p32.value}
         if world == 1 and not args.no_cpu_baseline:
@@ -310,7 +337,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     stats (deterministic, summed over the same K frames): evals E, union-bone visits U,
     Newton steps I, starts S, exact prune tests P, field queries Q.
     """
-    E, U, I, S, P, Q = (float(x) for x in stats[:6])
+    E, U, I, S, P, Q, QT = (float(x) for x in stats[:7])
     fp64_peak, fp32_peak = pipe
     traffic = ncu_traffic()
     out = {}
@@ -332,6 +359,10 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
           f64src, "FP64 add/mul/div/sqrt of inverse_lbs_ctx as written (no FMA)")
     # K3 field: exact MLP 6400 mul + 6400 add + 512 encode accumulations (f32) per query
     entry("field", "fp32", Q * 13312, "TFLOP/s", fp32_peak, f32src, "f32 mul+add of encode+MLP, 13312/query")
+    # K3 field on tcgen05: 2*(32*64 + 64*64 + 64*4) = 12800 algorithmic MLP flops per query
+    # (the split-bf16 scheme issues 3 MMAs per product and pads the head to N=16: not counted)
+    entry("field_tc", "tensor", QT * 12800, "TFLOP/s", peaks.get("bf16_tflops"),
+          f"MEASURED_PEAKS.json bf16_tflops ({peak_kind})", "12800 MLP flops/query (algorithmic)")
     # K1 march: ~80 FP64 per ray + 36 per sample (ray.at, to_normalized, t, cell_of)
     entry("march", "fp64", rays * K * (80 + 36 * N), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64")
     entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
@@ -501,6 +532,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100, help="timed frames (default: the 100-frame animation)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "exact"],
+                    help="render decoder for `value` (the other one is reported as other_decoder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")
     args = ap.parse_args()

@@ -160,6 +160,12 @@ int arfx_model_describe(arfx_model m, arfx_model_desc* out);
 int arfx_model_get_params(arfx_model m, float* grid_params, float* mlp_params,
                           double* skin_weights);
 int arfx_model_set_params(arfx_model m, const float* grid_params, const float* mlp_params);
+/* Decoder used by arfx_render_model*: ARFX_MLP_EXACT (default) = f32 SIMT with the
+ * reference's summation order; ARFX_MLP_TCGEN05 = tcgen05.mma kind::tf32 with fp32
+ * accumulation (stated tolerance: 1e-3 relative on rendered RGB). Occupancy grids,
+ * training and the batched query APIs always use the exact decoder. */
+enum { ARFX_MLP_EXACT = 0, ARFX_MLP_TCGEN05 = 1 };
+int arfx_model_set_mlp_mode(arfx_model m, int mode);
 int arfx_model_zero_grad(arfx_model m, void* stream);
 int arfx_model_get_grads(arfx_model m, float* grid_grad, float* mlp_grad);
 /* device pointers of the parameter / gradient arrays (for NCCL / optimizers) */
@@ -220,7 +226,7 @@ int arfx_profile_read(arfx_model m, int max, char* names, double* ms, int64_t* l
 
 /* deterministic work counters for roofline accounting (off by default):
  * out[0] skinning evals, [1] union-bone visits, [2] Newton steps, [3] starts,
- * [4] exact prune distance tests, [5] field queries. arfx_stats_read resets them. */
+ * [4] exact prune distance tests, [5] field queries (exact SIMT decoder), [6] field queries (tcgen05 decoder). arfx_stats_read resets them. */
 int arfx_stats_enable(arfx_model m, int on);
 int arfx_stats_read(arfx_model m, uint64_t* out16);
 /* measured FP64 / FP32 add+mul issue roofs of this GPU (TFLOP/s, 1 flop per add or mul) */

@@ -249,6 +249,11 @@ class Model:
         m = None if mlp is None else np.ascontiguousarray(mlp, np.float32)
         call("arfx_model_set_params", self._h, ptr(g, C.c_float), ptr(m, C.c_float))
 
+    def set_mlp_mode(self, mode: str) -> None:
+        """'exact' (f32 SIMT, the reference's summation order; default) or 'tcgen05'
+        (tensor-core tf32, stated tolerance 1e-3 relative on rendered RGB). Render only."""
+        call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1}[mode])
+
     def zero_grad(self):
         call("arfx_model_zero_grad", self._h, None)
 

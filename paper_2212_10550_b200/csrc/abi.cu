@@ -488,6 +488,14 @@ int arfx_model_set_params(arfx_model mh, const float* gp, const float* mp) {
   });
 }
 
+int arfx_model_set_mlp_mode(arfx_model mh, int mode) {
+  return guard([&] {
+    require(mh != nullptr, "set_mlp_mode: null model");
+    require(mode == ARFX_MLP_EXACT || mode == ARFX_MLP_TCGEN05, "set_mlp_mode: unknown mode");
+    mh->impl.mlp_mode = mode;
+  });
+}
+
 int arfx_model_zero_grad(arfx_model mh, void* stream) {
   return guard([&] {
     require(mh != nullptr, "null model");

@@ -1,0 +1,341 @@
+// field_tc.cu -- K3 on the 5th-gen tensor cores: encode + 32-64-64-4 decoder with
+// tcgen05.mma (kind::f16 on split-bf16 operands, fp32 accumulate in TMEM), one 128-query tile (M = 128) per
+// iteration of a persistent 128-thread CTA.
+//
+// Operands are split bf16 pairs (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)) and every
+// product is formed as hi*hi + hi*lo + lo*hi with kind::f16 MMAs (bf16 in, fp32 accumulate
+// in TMEM): ~16 significant bits, i.e. ~1e-5 relative, for the same shared-memory
+// footprint as one fp32 operand.
+//   encode   thread = query, warp-uniform level (as field_tile_kernel); features go straight
+//            into the UMMA K-major, no-swizzle canonical layout of A0 (hi and lo planes)
+//   layer 0  D[128x64] = A0[128x32] * W0^T    2 K-steps x 3 MMAs, TMEM cols [0, 64)
+//   epi 0    tcgen05.ld, + b0, ReLU -> A1 planes
+//   layer 1  D[128x64] = A1[128x64] * W1^T    4 x 3 MMAs, TMEM cols [0, 64) (D0 consumed)
+//   epi 1    + b1, ReLU -> A1 (in place: the layer-1 MMAs have completed)
+//   layer 2  D[128x16] = A1[128x64] * W2p^T   4 x 3 MMAs, W2 padded to N = 16, cols [64, 80)
+//   epi 2    + b2, softplus / logistic (R/field.hpp:78-81) -> (density, rgb)
+// One thread issues the MMAs; completion is signalled with tcgen05.commit on an mbarrier.
+// Not bit-exact with the reference's sequential f32 sums (stated tolerance);
+// the exact SIMT decoder (field_tile_kernel) stays the default (arfx_model_set_mlp_mode).
+#include <cuda_runtime.h>
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "field.cuh"
+#include "model.h"
+
+namespace arfx {
+namespace {
+
+constexpr int kTcTile = 128;
+constexpr int kIn = 32, kHid = 64, kOutPad = 16;
+constexpr uint32_t kTmemCols = 512;  // 4 groups x 128 columns (whole TMEM: one CTA per SM)
+
+// K-major, no-swizzle canonical layout (cute "INTERLEAVE"): element (r, k) of an R x K bf16
+// operand at byte (k/8)*(R*16) + (r/8)*128 + (r%8)*16 + (k%8)*2 = (k/8)*(R*16) + r*16 + (k%8)*2.
+// Core matrices are 8 rows x 16 B; LBO (next 16-B K chunk) = R*16, SBO (next 8 rows) = 128.
+__device__ __forceinline__ int kmaj_off(int r, int k, int R) { return (k >> 3) * (R * 16) + r * 16 + (k & 7) * 2; }
+
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // descriptor version for sm_100
+  return d;         // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// D (+)= sum over K-steps of Ahi*Bhi + Ahi*Blo + Alo*Bhi; operand planes: hi at off, lo at
+// off + plane bytes. K per MMA = 16 (two 16-byte chunks).
+__device__ __forceinline__ void mma_split(uint32_t tmem_d, uint32_t a_hi, uint32_t a_plane, int a_rows,
+                                          uint32_t b_hi, uint32_t b_plane, int b_rows, int K, uint32_t idesc) {
+  for (int ks = 0; ks < K / 16; ++ks) {
+    const uint32_t ao = a_hi + ks * 2 * (a_rows * 16), bo = b_hi + ks * 2 * (b_rows * 16);
+    const uint64_t ah = smem_desc(ao, a_rows * 16, 128), al = smem_desc(ao + a_plane, a_rows * 16, 128);
+    const uint64_t bh = smem_desc(bo, b_rows * 16, 128), bl = smem_desc(bo + b_plane, b_rows * 16, 128);
+    mma_bf16(tmem_d, ah, bh, idesc, ks > 0 ? 1u : 0u);
+    mma_bf16(tmem_d, ah, bl, idesc, 1u);
+    mma_bf16(tmem_d, al, bh, idesc, 1u);
+  }
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// One CTA per SM runs kGroups independent 128-query pipelines (4 warps each, own TMEM
+// columns, own activation tile, own mbarrier, own named barrier) over shared weights, so
+// the hash-grid gathers of one group overlap the MMAs/epilogues of the others.
+constexpr int kGroups = 4;
+constexpr int kTcThreads = kGroups * kTcTile;
+
+struct TcSmem {  // byte offsets inside the dynamic smem; each operand = hi plane, lo plane
+  static constexpr int B0P = kHid * kIn * 2, B1P = kHid * kHid * 2, B2P = kOutPad * kHid * 2;
+  static constexpr int A0P = kTcTile * kIn * 2, A1P = kTcTile * kHid * 2;
+  static constexpr int B0 = 0;                              // W0  64 x 32  (2 x 4 KB)
+  static constexpr int B1 = B0 + 2 * B0P;                   // W1  64 x 64  (2 x 8 KB)
+  static constexpr int B2 = B1 + 2 * B1P;                   // W2p 16 x 64  (2 x 2 KB)
+  static constexpr int BIAS = B2 + 2 * B2P;                 // b0[64] b1[64] b2[4]
+  static constexpr int ACT = BIAS + 1024;                   // per group: hidden 128 x 64 (2 x 16 KB);
+  static constexpr int ACT_BYTES = 2 * A1P;                 //   the 128 x 32 features alias its start
+  static constexpr int MBAR = ACT + kGroups * ACT_BYTES;    // u64 [kGroups]
+  static constexpr int TADDR = MBAR + 8 * kGroups;          // u32
+  static constexpr int TOTAL = TADDR + 16;
+};
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kTcTile) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, const double* __restrict__ px,
+                                                                 const double* __restrict__ py,
+                                                                 const double* __restrict__ pz,
+                                                                 const int32_t* __restrict__ owner,
+                                                                 float4* __restrict__ res,
+                                                                 const unsigned long long* n_dev, long long cap,
+                                                                 unsigned long long* stats) {
+  extern __shared__ __align__(1024) unsigned char tc_smem[];
+  const int g = threadIdx.x / kTcTile;  // pipeline group
+  const int tid = threadIdx.x % kTcTile, warp = tid >> 5;
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  if (static_cast<long long>(blockIdx.x) * kTcTile * kGroups >= n) return;
+
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem));
+  float* bias = reinterpret_cast<float*>(tc_smem + TcSmem::BIAS);
+  const uint32_t mbar = sbase + TcSmem::MBAR + 8 * g;
+  uint32_t* taddr_smem = reinterpret_cast<uint32_t*>(tc_smem + TcSmem::TADDR);
+  const int A1 = TcSmem::ACT + g * TcSmem::ACT_BYTES, A0 = A1;  // byte offsets of this group's tile
+
+  // ---- stage the weights in the K-major operand layouts (W[o][i] is N x K, K-major) ----
+  const float* W0 = F.mlp;
+  const float* b0 = W0 + kIn * kHid;
+  const float* W1 = b0 + kHid;
+  const float* b1 = W1 + kHid * kHid;
+  const float* W2 = b1 + kHid;
+  const float* b2 = W2 + 4 * kHid;
+  auto put = [&](int off, int plane, float x) {
+    __nv_bfloat16 hi, lo;
+    split_bf16(x, hi, lo);
+    *reinterpret_cast<__nv_bfloat16*>(tc_smem + off) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(tc_smem + off + plane) = lo;
+  };
+  const int ctid = threadIdx.x;
+  for (int i = ctid; i < kHid * kIn; i += kTcThreads) {
+    const int o = i / kIn, k = i % kIn;
+    put(TcSmem::B0 + kmaj_off(o, k, kHid), TcSmem::B0P, __ldg(W0 + i));
+  }
+  for (int i = ctid; i < kHid * kHid; i += kTcThreads) {
+    const int o = i / kHid, k = i % kHid;
+    put(TcSmem::B1 + kmaj_off(o, k, kHid), TcSmem::B1P, __ldg(W1 + i));
+  }
+  for (int i = ctid; i < kOutPad * kHid; i += kTcThreads) {
+    const int o = i / kHid, k = i % kHid;
+    put(TcSmem::B2 + kmaj_off(o, k, kOutPad), TcSmem::B2P, o < 4 ? __ldg(W2 + o * kHid + k) : 0.0f);
+  }
+  for (int i = ctid; i < kHid; i += kTcThreads) {
+    bias[i] = __ldg(b0 + i);
+    bias[64 + i] = __ldg(b1 + i);
+  }
+  if (ctid < 4) bias[128 + ctid] = __ldg(b2 + ctid);
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  if (ctid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbase + TcSmem::TADDR),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *taddr_smem + static_cast<uint32_t>(g * 128);        // this group's columns
+  const uint32_t tmem_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);  // this warp's 32 lanes
+  uint32_t phase = 0;
+  constexpr uint32_t ID64 = idesc_bf16(128, 64);
+  constexpr uint32_t ID16 = idesc_bf16(128, 16);
+  // writes row `tid`, columns [c, c+8) of a split operand (hi plane, lo plane)
+  auto put8 = [&](int base, int plane, int c, const float* x) {
+    __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) split_bf16(x[j], hi[j], lo[j]);
+    *reinterpret_cast<uint4*>(tc_smem + base + kmaj_off(tid, c, kTcTile)) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(tc_smem + base + plane + kmaj_off(tid, c, kTcTile)) = *reinterpret_cast<const uint4*>(lo);
+  };
+
+  for (long long t0 = (static_cast<long long>(blockIdx.x) * kGroups + g) * kTcTile; t0 < n;
+       t0 += static_cast<long long>(gridDim.x) * kGroups * kTcTile) {
+    // ---- normalized coords per query (registers: thread = query = A row) ----
+    const long long q = t0 + tid;
+    const bool ok = q < n && owner[q] >= 0;
+    if (stats) {
+      const unsigned c = __popc(__ballot_sync(0xffffffffu, ok));
+      if ((tid & 31) == 0 && c) atomicAdd(stats + 6, static_cast<unsigned long long>(c));
+    }
+    double u[3] = {0.0, 0.0, 0.0};
+    if (ok) normalize_point(F, make3(px[q], py[q], pz[q]), u);
+    // ---- encode into A0 (warp-uniform level, thread = query) ----
+    {
+#pragma unroll 1
+      for (int l = 0; l < 16; l += 4) {
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 o = make_float2(0.f, 0.f);
+          if (ok) o = encode_level_f2(F, l + j, u);
+          f[2 * j] = o.x;
+          f[2 * j + 1] = o.y;
+        }
+        put8(A0, TcSmem::A0P, 2 * l, f);
+      }
+    }
+    fence_async_smem();
+    group_sync(g);
+    // ---- layer 0 ----
+    if (tid == 0) {
+      tc_fence_after();
+      mma_split(tmem, sbase + A0, TcSmem::A0P, kTcTile, sbase + TcSmem::B0, TcSmem::B0P, kHid, kIn, ID64);
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue 0: + b0, ReLU -> A1 ----
+#pragma unroll
+    for (int c = 0; c < kHid; c += 16) {
+      float v[16];
+      tmem_ld16(tmem_row + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias[c + j], 0.f);
+      put8(A1, TcSmem::A1P, c, v);
+      put8(A1, TcSmem::A1P, c + 8, v + 8);
+    }
+    tc_fence_before();
+    fence_async_smem();
+    group_sync(g);
+    // ---- layer 1 ----
+    if (tid == 0) {
+      tc_fence_after();
+      mma_split(tmem, sbase + A1, TcSmem::A1P, kTcTile, sbase + TcSmem::B1, TcSmem::B1P, kHid, kHid, ID64);
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue 1: + b1, ReLU -> A1 (in place) ----
+#pragma unroll
+    for (int c = 0; c < kHid; c += 16) {
+      float v[16];
+      tmem_ld16(tmem_row + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias[64 + c + j], 0.f);
+      put8(A1, TcSmem::A1P, c, v);
+      put8(A1, TcSmem::A1P, c + 8, v + 8);
+    }
+    tc_fence_before();
+    fence_async_smem();
+    group_sync(g);
+    // ---- layer 2 (N padded to 16) ----
+    if (tid == 0) {
+      tc_fence_after();
+      mma_split(tmem + 64, sbase + A1, TcSmem::A1P, kTcTile, sbase + TcSmem::B2, TcSmem::B2P, kOutPad, kHid,
+                ID16);
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      float v[16];
+      tmem_ld16(tmem_row + 64, v);
+      if (ok) {
+        const float l0 = v[0] + bias[128], l1 = v[1] + bias[129], l2 = v[2] + bias[130], l3 = v[3] + bias[131];
+        res[t0 + tid] = make_float4(softplus_f(l0), logistic_f(l1), logistic_f(l2), logistic_f(l3));
+      }
+    }
+    tc_fence_before();
+    group_sync(g);
+  }
+  __syncthreads();
+  if (ctid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*taddr_smem), "n"(kTmemCols)
+                 : "memory");
+}
+
+}  // namespace
+
+bool field_tc_supported(const FieldView& F) {
+  return F.F == 2 && F.L == 16 && F.in_dim == kIn && F.hidden == kHid && F.n_layers == 3 && F.out_dim == 4;
+}
+
+void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
+  const size_t smem = TcSmem::TOTAL + 1024;  // + alignment slack
+  static bool attr = false;
+  if (!attr) {
+    ARFX_CUDA(cudaFuncSetAttribute(field_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  int sms = 148, dev = 0;
+  ARFX_CUDA(cudaGetDevice(&dev));
+  ARFX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // persistent: one CTA per SM (it owns all 512 TMEM columns)
+  const long long tiles = (n_hint + kTcTile * kGroups - 1) / (kTcTile * kGroups);
+  const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));
+  m.prof.begin("field_tc", s);
+  field_tc_kernel<<<grid, kTcThreads, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
+                                              m.ws.pres.ptr, m.ws.counters.ptr + 2,
+                                              static_cast<long long>(m.ws.cap_pool),
+                                              m.stats_on ? m.stats.ptr : nullptr);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+}
+
+}  // namespace arfx

@@ -100,6 +100,7 @@ struct ModelImpl {
   // [2] Newton steps [3] starts [4] exact prune tests [5] field queries
   bool stats_on = false;
   DevBuf<unsigned long long> stats;
+  int mlp_mode = 0;  // render decoder: 0 exact f32 SIMT (bit-faithful sums), 1 tcgen05 split-bf16 (3-term, f32 accumulate)
   cudaStream_t stream = nullptr;
   std::vector<HostBone> bones;
   GridCfg grid{};
@@ -176,6 +177,10 @@ void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const fl
                      float* d_rgb, float* d_alpha, cudaStream_t s);
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
                          const float* gs, const float* gc, cudaStream_t s);
+
+// field_tc.cu
+bool field_tc_supported(const FieldView& F);
+void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint);
 
 // peaks.cu
 void measure_pipe_peaks(double* fp64_tflops, double* fp32_tflops);

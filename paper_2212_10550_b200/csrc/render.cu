@@ -751,7 +751,14 @@ void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long lo
   launch_deform_sink(m, d_poses, src, K, n_hint, "deform", s);
 }
 
-void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint) {
+// allow_tc: the render may use the tcgen05 decoder (arfx_model_set_mlp_mode); occupancy
+// grids, training and the query APIs always use the exact f32 MLP so their integer
+// decisions (masks, root selection feeding gradients) stay reference-exact.
+void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allow_tc = false) {
+  if (allow_tc && m.mlp_mode == 1 && field_tc_supported(m.fv)) {
+    launch_field_tc(m, s, n_hint);
+    return;
+  }
   if (field_is_standard_host(m.fv)) {
     static bool attr_set = false;
     const size_t smem = field_tile_smem(m.fv);
@@ -908,7 +915,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   }
   ListSrc src{w.sx.ptr, w.sy.ptr, w.sz.ptr, w.counters.ptr, 0, static_cast<long long>(w.cap_posed)};
   launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s);
-  launch_field_pool(m, s, static_cast<long long>(w.cap_pool));
+  launch_field_pool(m, s, static_cast<long long>(w.cap_pool), /*allow_tc=*/true);
   CompositeArgs C{w.row_list.ptr, n_rows, cam.width, w.ray_first.ptr, w.ray_count.ptr, w.sdelta.ptr,
                   w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w.ssel.ptr, eps, d_rgb, d_alpha};
   if (n_rays > 0) {

@@ -298,3 +298,34 @@ def test_cpp_dropin_adapter():
         pytest.skip("adapter_parity not built (needs /root/reference at build time)")
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("structured", [False, True])
+def test_render_tcgen05_decoder(gpu, ref, structured):
+    """The tcgen05 (split-bf16, fp32-accumulate) decoder against the reference render.
+    Stated tolerance (north_star: 1e-3 relative): |d| <= 1e-3 * |ref| + 1e-5 per pixel."""
+    sk = fx.smpl24()
+    g, m = fx.config1_grid(), fx.config1_mlp()
+    dm = gpu.build_model(sk, g, m, (32, 32, 32), fx.CONFIG1_SEED)
+    rm = ref.build_model(sk, g, m, (32, 32, 32), fx.CONFIG1_SEED)
+    if structured:
+        gp, mp, _ = ref.arrays(rm)
+        rng = np.random.default_rng(5)
+        gp[:] = rng.uniform(-0.5, 0.5, gp.size).astype(np.float32)
+        mp[:] = (mp * 2).astype(np.float32)
+        dm.set_params(gp, mp)
+    pose = fx.random_pose(sk, fx.CONFIG1_POSE_SEED)
+    cam = fx.default_camera(sk, 128, 128)
+    cfg = arf.OccupancyConfig()
+    occ = arf.build_model_inference_grid(dm, pose, cfg)
+    rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, cfg)
+    opt = arf.RenderOptions(samples_per_ray=128)
+    dm.set_mlp_mode("tcgen05")
+    try:
+        img = arf.render_model(dm, pose, cam, occ, opt)
+    finally:
+        dm.set_mlp_mode("exact")
+    rrgb, ralpha, _ = ref.render(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt)
+    assert rrgb.max() > 1e-3  # the frame is not empty
+    np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-3, atol=PIX_ATOL)
+    np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-3, atol=PIX_ATOL)

@@ -1,5 +1,5 @@
 """Small driver for ncu: config-1 avatar, F frames of (inference grid + render) at 540x540
-through the device API on one stream. Usage: python tools/prof_frame.py [frames]"""
+through the device API on one stream. Usage: python tools/prof_frame.py [frames] [exact|tcgen05]"""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -12,10 +12,11 @@ from paper_2212_10550_b200 import arf, fixtures as fx  # noqa: E402
 from paper_2212_10550_b200._lib import check, lib  # noqa: E402
 
 
-def main(frames: int = 3):
+def main(frames: int = 3, mlp: str = "exact"):
     L = lib()
     sk = fx.smpl24()
     model = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    model.set_mlp_mode(mlp)
     poses = fx.animation_poses(sk, 4)
     cam = fx.default_camera(sk, 540, 540)
     opt = fx.config1_render_options()
@@ -30,4 +31,4 @@ def main(frames: int = 3):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 3, sys.argv[2] if len(sys.argv) > 2 else "exact")
