@@ -28,7 +28,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xptxas", "-O3",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-O2",
     "-I", str(CSRC), "-I", str(ROOT / "include"),
-]
+] + os.environ.get("ARFX_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DARFX_DS_MIN_BLOCKS=6)
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              "-I", str(CSRC), "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include"]

@@ -104,13 +104,16 @@ __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __res
     }
     const double va[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
     const double vb[8] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x, b3.y};
+    // The reference skips corners with wt == 0 (R/skinning.hpp:45); adding the
+    // product instead is bit-identical: wt * v = +-0 for finite v, acc starts at +0 and
+    // x + (+-0) == x, (+0) + (-0) == +0 -- so the data-dependent branch (and its DSETP/FSEL
+    // per corner per bone) is dropped.
     double acc = 0.0, acc2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (wt[k] != 0.0) {
-        acc = dadd(acc, dmul(wt[k], va[k]));
-        acc2 = dadd(acc2, dmul(wt[k], vb[k]));
-      }
+    for (int k = 0; k < 8; ++k) {
+      acc = dadd(acc, dmul(wt[k], va[k]));
+      acc2 = dadd(acc2, dmul(wt[k], vb[k]));
+    }
     ws[j * stride] = acc;
     sum = dadd(sum, acc);
     if (two) {

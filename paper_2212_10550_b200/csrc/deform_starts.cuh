@@ -30,6 +30,10 @@
 namespace arfx {
 
 constexpr int kDsThreads = 128;
+#ifndef ARFX_DS_MIN_BLOCKS
+#define ARFX_DS_MIN_BLOCKS 5
+#endif
+constexpr int kDsMinBlocks = ARFX_DS_MIN_BLOCKS;  // 5 x 128 threads: <= 102 registers
 constexpr int kDsItemChunk = 64;
 constexpr int kItemBoneShift = 26;  // item = target | bone << 26 (targets < 2^26)
 
@@ -221,14 +225,13 @@ __global__ void __launch_bounds__(256) start_place_kernel(const unsigned long lo
 // K2c: Newton over the items. Result per start slot: root (x,y,z) and residual, or
 // residual = -1 when the start did not converge (singular / stalled / max iterations).
 template <class Src, bool kSinglePose, bool kStats>
-__global__ void __launch_bounds__(kDsThreads) start_newton_kernel(SkinView S, const PoseCtx* __restrict__ poses,
+__global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(SkinView S, const PoseCtx* __restrict__ poses,
                                                                   InverseOpts opt, Src src,
                                                                   const uint32_t* __restrict__ items,
                                                                   const unsigned long long* n_items,
                                                                   const uint32_t* __restrict__ mask_in,
                                                                   const uint32_t* __restrict__ slot_base,
-                                                                  double* __restrict__ rx, double* __restrict__ ry,
-                                                                  double* __restrict__ rz, double* __restrict__ rr,
+                                                                  double4* __restrict__ res,
                                                                   unsigned long long* cursor,
                                                                   unsigned long long* stats, long long cap) {
   extern __shared__ double ds_smem[];
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kDsThreads) start_newton_kernel(SkinView S, co
         }
       }
       if (emit) {  // failed start
-        rr[slot] = -1.0;
+        res[slot] = make_double4(0.0, 0.0, 0.0, -1.0);
         state = DS_NEED;
       }
       (void)conv;
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(kDsThreads) start_newton_kernel(SkinView S, co
       x = cand;
       gn = gcn;
       if (gn < opt.tolerance) {
-        rx[slot] = x.x, ry[slot] = x.y, rz[slot] = x.z, rr[slot] = gn;
+        res[slot] = make_double4(x.x, x.y, x.z, gn);
         state = DS_NEED;
       } else {
         it = 0;
@@ -352,14 +355,14 @@ __global__ void __launch_bounds__(kDsThreads) start_newton_kernel(SkinView S, co
     } else if (state == DS_EVAL_LS) {
       if (gcn < gn || h == 3) {
         if (gcn >= gn && gn >= opt.tolerance) {
-          rr[slot] = -1.0;  // stalled
+          res[slot] = make_double4(0.0, 0.0, 0.0, -1.0);  // stalled
           state = DS_NEED;
         } else {
           x = cand;
           gn = gcn;
           ++it;
           if (gn < opt.tolerance) {
-            rx[slot] = x.x, ry[slot] = x.y, rz[slot] = x.z, rr[slot] = gn;
+            res[slot] = make_double4(x.x, x.y, x.z, gn);
             state = DS_NEED;
           } else {
             state = DS_ITER;
@@ -408,25 +411,21 @@ struct RootsSink {  // batched inverse_lbs API: every root + residual, [n][8]
 };
 
 __device__ __forceinline__ void ds_gather_roots(long long s, const uint32_t* mask_in, const uint32_t* slot_base,
-                                                const double* rx, const double* ry, const double* rz,
-                                                const double* rr, double dedup, Roots& R, long long cap) {
+                                                const double4* res, double dedup, Roots& R, long long cap) {
   R.count = 0;
   const int c = __popc(mask_in[s]);
   const long long b0 = slot_base[s];
   for (int j = 0; j < c && b0 + j < cap; ++j) {
-    const double r = rr[b0 + j];
-    if (r < 0.0) continue;
-    roots_push(R, make3(rx[b0 + j], ry[b0 + j], rz[b0 + j]), r, dedup);
+    const double4 v = res[b0 + j];
+    if (v.w < 0.0) continue;
+    roots_push(R, make3(v.x, v.y, v.z), v.w, dedup);
   }
 }
 
 template <class Src>
 __global__ void __launch_bounds__(256) finalize_pool_kernel(Src src, const uint32_t* __restrict__ mask_in,
                                                             const uint32_t* __restrict__ slot_base,
-                                                            const double* __restrict__ rx,
-                                                            const double* __restrict__ ry,
-                                                            const double* __restrict__ rz,
-                                                            const double* __restrict__ rr, double dedup,
+                                                            const double4* __restrict__ res, double dedup,
                                                             PoolSink K, long long cap) {
   const long long n = src.count();
   const int lane = threadIdx.x & 31;
@@ -438,7 +437,7 @@ __global__ void __launch_bounds__(256) finalize_pool_kernel(Src src, const uint3
     R.count = 0;
     uint32_t inbox = 0;
     if (s < n) {
-      ds_gather_roots(s, mask_in, slot_base, rx, ry, rz, rr, dedup, R, cap);
+      ds_gather_roots(s, mask_in, slot_base, res, dedup, R, cap);
       for (int k = 0; k < R.count; ++k)
         if (field_contains(K.F, make3(R.x[k][0], R.x[k][1], R.x[k][2]))) inbox |= 1u << k;
     }
@@ -483,16 +482,13 @@ __global__ void __launch_bounds__(256) finalize_pool_kernel(Src src, const uint3
 template <class Src>
 __global__ void __launch_bounds__(256) finalize_roots_kernel(Src src, const uint32_t* __restrict__ mask_in,
                                                              const uint32_t* __restrict__ slot_base,
-                                                             const double* __restrict__ rx,
-                                                             const double* __restrict__ ry,
-                                                             const double* __restrict__ rz,
-                                                             const double* __restrict__ rr, double dedup,
+                                                             const double4* __restrict__ res, double dedup,
                                                              RootsSink K, long long cap) {
   const long long n = src.count();
   for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
        s += static_cast<long long>(gridDim.x) * blockDim.x) {
     Roots R;
-    ds_gather_roots(s, mask_in, slot_base, rx, ry, rz, rr, dedup, R, cap);
+    ds_gather_roots(s, mask_in, slot_base, res, dedup, R, cap);
     K.counts[s] = R.count;
     for (int k = 0; k < R.count; ++k) {
       K.roots[(s * kMaxRoots + k) * 3 + 0] = R.x[k][0];

@@ -10,6 +10,7 @@
 //  * per-cell packed table for the deformer (see SkinView in arfx_internal.h).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <numeric>
 
@@ -185,9 +186,11 @@ void build_cell_table(ModelImpl& m) {
   ARFX_CUDA(cudaStreamSynchronize(m.stream));
   std::vector<uint32_t> off(h.size());
   uint64_t acc = 0;
+  m.max_union = 1;
   for (size_t i = 0; i < h.size(); ++i) {
     off[i] = static_cast<uint32_t>(acc);
     acc += h[i];
+    m.max_union = std::max(m.max_union, static_cast<int>(h[i]));
   }
   m.cell_vals.alloc(static_cast<size_t>(acc) * 8 + 8);
   ARFX_CUDA(cudaMemcpyAsync(m.cell_off.ptr, off.data(), off.size() * sizeof(uint32_t),

@@ -62,7 +62,7 @@ struct Workspace {
   DevBuf<unsigned long long> bone_hist;       // [0,32) per-bone start counts, [32,64) item cursors
   DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
   DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
-  DevBuf<double> rx, ry, rz, rr;              // per start slot: root, residual (-1: no root)
+  DevBuf<double4> res4;                        // per start slot: root xyz, residual (-1: no root)
   // training scratch (train.cu)
   DevBuf<double> strans;   // transmittance before each posed sample
   DevBuf<float> pgs, pgc;  // per pool entry: dsigma, dcolor[3]
@@ -115,6 +115,7 @@ struct ModelImpl {
   DevBuf<double> skin;
   DevBuf<uint32_t> cell_mask, cell_off;
   DevBuf<double> cell_vals;
+  int max_union = 1;  // widest per-cell bone union (sizes the Newton kernel's scratch)
   FieldView fv{};
   SkinView sv{};
   Workspace ws;

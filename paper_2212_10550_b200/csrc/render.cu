@@ -670,16 +670,16 @@ __global__ void starts_overflow_kernel(const unsigned long long* total, unsigned
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long n, cudaStream_t s) {
   Workspace& w = m.ws;
-  finalize_pool_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.rx.ptr, w.ry.ptr,
-                                                                w.rz.ptr, w.rr.ptr, m.inv.dedup_radius, K,
+  finalize_pool_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
+                                                                m.inv.dedup_radius, K,
                                                                 static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
 }
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const RootsSink& K, long long n, cudaStream_t s) {
   Workspace& w = m.ws;
-  finalize_roots_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.rx.ptr, w.ry.ptr,
-                                                                 w.rz.ptr, w.rr.ptr, m.inv.dedup_radius, K,
+  finalize_roots_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
+                                                                 m.inv.dedup_radius, K,
                                                                  static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
 }
@@ -727,12 +727,13 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
                                                             w.items.ptr, cap);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
-  const size_t smem = pose_smem + static_cast<size_t>(m.sv.nb) * kDsThreads * sizeof(double);
+  // per-thread union-bone scratch: the widest cell union (build_cell_table), not n_bones
+  const size_t smem = pose_smem + static_cast<size_t>(m.max_union) * kDsThreads * sizeof(double);
   auto kern = stats ? start_newton_kernel<Src, single, true> : start_newton_kernel<Src, single, false>;
   const int grid = persistent_grid(kern, kDsThreads, smem, 2 * n);
   m.prof.begin(name, s);
   kern<<<grid, kDsThreads, smem, s>>>(m.sv, d_poses, m.inv, src, w.items.ptr, C + 6, w.smask.ptr, w.scount.ptr,
-                                      w.rx.ptr, w.ry.ptr, w.rz.ptr, w.rr.ptr, C + 4, stats,
+                                      w.res4.ptr, C + 4, stats,
                                       static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
@@ -808,10 +809,7 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
     items.alloc(want);
     keys.alloc(want);
     unsorted.alloc(want);
-    rx.alloc(want + 1);
-    ry.alloc(want + 1);
-    rz.alloc(want + 1);
-    rr.alloc(want + 1);
+    res4.alloc(want + 1);
     cap_starts = want;
   }
 }

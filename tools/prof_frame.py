@@ -23,10 +23,14 @@ def main(frames: int = 3, mlp: str = "exact"):
     occ = arf.OccupancyGrid(model.normalized_box, fx.config1_occupancy())
     views = [arf.PosedModelView(model, p) for p in poses]
     out = arf.RenderImages(540, 540, np.zeros((540, 540, 3), np.float32), np.zeros((540, 540), np.float32))
+    stats = np.zeros(16, np.uint64)
+    check(L.arfx_stats_enable(model._h, 1))
     for f in range(frames):
         v = views[f % len(views)]
         check(L.arfx_build_inference_grid(model._h, v._h, occ._h, None, None))
         arf.render_model(model, v, cam, occ, opt, out=out)
+    check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
+    print("per-frame stats E U I S P Q QT:", (stats[:7] / frames).astype(np.int64).tolist())
     print("frames", frames, "posed", model.counters.posed_queries, "alpha sum", float(out.alpha.sum()))
 
 
