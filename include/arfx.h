@@ -24,6 +24,9 @@
  *   arfx_composite(_backward)   <- arf::composite / composite_backward R/render.hpp:98-157
  *   arfx_field_query_backward   <- CanonicalField::query_backward     R/field.hpp:91-103
  *   arfx_train_fwd_bwd          <- composed training step
+ *   arfx_losses / arfx_train_step(_device)  <- SPEC.md:454-489 losses fused into the step
+ *   arfx_adam_step              <- SPEC.md:508-509 optimizer (flat vector, shardable)
+ *   arfx_figure_*               <- R/scene.hpp analytic ground truth (SPEC.md scenegen)
  *
  * Error convention (the reference throws; R/math.hpp:12-18): every function
  * returns an int status, 0 = ok, and sets a thread-local message readable via
@@ -266,6 +269,80 @@ int arfx_train_fwd_bwd(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_o
                        const arfx_render_options* opt, int64_t n_rays, const int32_t* px,
                        const int32_t* py, const float* d_color, const float* d_alpha, float* rgb,
                        float* alpha, arfx_counters* c, void* stream);
+
+/* ---- training: losses, fused step, optimizer -- */
+
+typedef struct arfx_loss_config { /* LossWeights SPEC.md:446-449; defaults :510 */
+  double w_rgb, w_alpha, w_hard, w_density; /* 1, 0.1, 0.1, 0.1 */
+  double huber_delta;                       /* 0.1 */
+} arfx_loss_config;
+
+typedef struct arfx_adam_config {
+  double lr_grid, lr_mlp; /* 1e-2, 1e-3 */
+  double beta1, beta2;    /* 0.9, 0.99 */
+  double eps;             /* 1e-15 */
+  int64_t total_steps;    /* cosine decay horizon T (<= 0: constant lr) */
+  double final_lr_factor; /* lr(T) / lr(0) */
+} arfx_adam_config;
+
+/* Per-ray losses on rendered (rgb, alpha) vs targets: loss4 = (L_rgb, L_alpha, L_hard,
+ * weighted total) as batch means, and the f32 upstream gradients dL/dC [n][3], dL/dA [n]
+ * (any output may be NULL). Host buffers. */
+int arfx_losses(int64_t n, const float* rgb, const float* alpha, const float* gt_rgb, const float* gt_alpha,
+                const arfx_loss_config* cfg, double* loss4, float* d_rgb, float* d_alpha);
+/* Fused training step over n rays: forward (as arfx_train_fwd_bwd), the losses evaluated
+ * per ray inside the composite kernel against gt_rgb/gt_alpha, their gradient fed straight
+ * into the composite reverse pass, field backward -> accumulated into the model's
+ * gradients. loss4 as arfx_losses. Host buffers (synchronous). */
+int arfx_train_step(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                    const arfx_render_options* opt, int64_t n_rays, const int32_t* px, const int32_t* py,
+                    const float* gt_rgb, const float* gt_alpha, const arfx_loss_config* cfg, double* loss4,
+                    float* rgb, float* alpha, arfx_counters* c, void* stream);
+/* The same on device arrays (d_loss4: 4 doubles on the device; d_rgb/d_alpha may be NULL).
+ * Enqueued on `stream`; the host waits only for the workspace-overflow check. */
+int arfx_train_step_device(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                           const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                           const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
+                           const arfx_loss_config* cfg, double* d_loss4, float* d_rgb, float* d_alpha,
+                           void* stream);
+/* Adam over flat parameter indices [begin, end) (multiples of 4; end = -1: all), step >= 1,
+ * gradients zeroed in the same pass. Asynchronous on stream. */
+int arfx_adam_step(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
+                   void* stream);
+/* Flat device vectors [grid | pad | mlp | pad] of n_flat floats: params, grads, Adam m, v
+ * (allocated on first use); mlp_offset = index of the first MLP parameter. */
+int arfx_model_flat(arfx_model m, float** params, float** grads, float** adam_m, float** adam_v,
+                    int64_t* n_flat, int64_t* mlp_offset);
+/* Host copies of the flat Adam moments (n_flat floats each; checkpoint / resume). */
+int arfx_model_get_adam(arfx_model m, float* adam_m, float* adam_v);
+int arfx_model_set_adam(arfx_model m, const float* adam_m, const float* adam_v);
+
+/* ---- analytic ground truth (SPEC.md scenegen; R/scene.hpp) -------------------------- */
+
+typedef struct arfx_figure { /* arf::CapsuleFigure  R/scene.hpp:13-27 */
+  arfx_skeleton skeleton;
+  double color[ARFX_MAX_BONES][3];
+  double amplitude[ARFX_MAX_BONES];
+  double softness;
+} arfx_figure;
+
+/* bones12 == NULL: analytic_query in canonical space (R/scene.hpp:31-50); else the posed
+ * field PosedFigure(fig, pose).query (R/scene.hpp:56-97). density[n], color[n][3]. */
+int arfx_figure_query(const arfx_figure* fig, const double* bones12, const double* pts, int64_t n,
+                      double* density, double* color);
+/* Ground-truth frame: render_image (R/render.hpp:178-218) of PosedFigure::query (matter iff
+ * density > 0), to_norm = global^-1, box = the model's normalized box, no occupancy; plus
+ * the exact silhouette PosedFigure::ray_hits (R/scene.hpp:123-130) per pixel. Host buffers
+ * rgb[H][W][3], alpha[H][W], mask[H][W] (any may be NULL). */
+int arfx_figure_render(const arfx_figure* fig, const double* bones12, const double* global12,
+                       const double box_lo[3], const double box_hi[3], const arfx_camera* cam,
+                       const arfx_render_options* opt, float* rgb, float* alpha, uint8_t* mask, void* stream);
+/* The same for n rays given by device pixel lists; device outputs; asynchronous on stream. */
+int arfx_figure_render_rays_device(const arfx_figure* fig, const double* bones12, const double* global12,
+                                   const double box_lo[3], const double box_hi[3], const arfx_camera* cam,
+                                   const arfx_render_options* opt, int64_t n, const int32_t* d_px,
+                                   const int32_t* d_py, float* d_rgb, float* d_alpha, uint8_t* d_mask,
+                                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -1404,3 +1404,214 @@ int arfo_train_fwd_bwd(const ao_model* m, const double* bones12, const double* g
   scratch_free(&s);
   return 0;
 }
+
+/* ---- analytic ground truth: CapsuleFigure / PosedFigure (R/scene.hpp:10-130) ---------- */
+
+typedef struct {
+  int nb;
+  v3 a[AO_MAX_BONES], b[AO_MAX_BONES];
+} figpose_t;
+
+static int figure_prepare(const ao_figure* f, const double* bones12, figpose_t* P) { /* :19-26, :61-75 */
+  int e;
+  if ((e = validate_skeleton(&f->skel))) return e;
+  for (int i = 0; i < f->skel.n_bones; ++i)
+    if (!(f->amplitude[i] > 0)) return fail(1, "figure: amplitudes must be positive");
+  if (!(f->softness > 0)) return fail(1, "figure: softness must be positive");
+  P->nb = f->skel.n_bones;
+  for (int i = 0; i < P->nb; ++i) {
+    const v3 h = vload(f->skel.head[i]), t = vload(f->skel.tail[i]);
+    P->a[i] = bones12 ? rapply(bones12 + 12 * i, h) : h;
+    P->b[i] = bones12 ? rapply(bones12 + 12 * i, t) : t;
+  }
+  return 0;
+}
+
+static double smoothstep01(double t) { /* R/math.hpp:25-35 */
+  t = t < 0.0 ? 0.0 : (1.0 < t ? 1.0 : t);
+  return t * t * (3.0 - 2.0 * t);
+}
+
+/* PosedFigure::query :79-97 (analytic_query :31-50 with rest segments) */
+static double figure_query(const ao_figure* f, const figpose_t* P, v3 x, v3* color) {
+  double total = 0.0;
+  v3 acc = V(0, 0, 0);
+  *color = V(0, 0, 0);
+  for (int i = 0; i < P->nb; ++i) {
+    const double d = point_segment_distance(x, P->a[i], P->b[i]);
+    if (d >= f->skel.radius[i]) continue;
+    const double s = smoothstep01((f->skel.radius[i] - d) / f->softness);
+    if (s <= 0.0) continue;
+    const double dens = f->amplitude[i] * s;
+    total += dens;
+    acc = vadd(acc, vmul(vload(f->color[i]), dens));
+  }
+  if (total > 0.0) {
+    *color = V(acc.x / total, acc.y / total, acc.z / total);
+    return total;
+  }
+  return 0.0;
+}
+
+static double ray_segment_distance(v3 o, v3 d, v3 a, v3 b) { /* :103-117 */
+  const v3 ab = vsub(b, a);
+  double best = 1.7976931348623157e308;
+  for (int i = 0; i <= 64; ++i) {
+    const double u = (double)i / 64;
+    const v3 p = vadd(a, vmul(ab, u));
+    const double t = dmax_(0.0, vdot(vsub(p, o), d));
+    best = dmin_(best, vnorm(vsub(p, vadd(o, vmul(d, t)))));
+  }
+  return best;
+}
+
+int arfo_figure_query(const ao_figure* f, const double* bones12, const double* pts, int64_t n, double* dens,
+                      double* col) {
+  figpose_t P;
+  int e;
+  if ((e = figure_prepare(f, bones12, &P))) return e;
+  for (int64_t i = 0; i < n; ++i) {
+    v3 c;
+    dens[i] = figure_query(f, &P, vload(pts + 3 * i), &c);
+    vstore(col + 3 * i, c);
+  }
+  return 0;
+}
+
+/* render_image :178-218 over PosedFigure::query (matter iff density > 0), to_norm = G^-1,
+ * no occupancy; mask = PosedFigure::ray_hits :123-130 (the dataset's exact alpha) */
+int arfo_figure_render(const ao_figure* f, const double* bones12, const double* global12, const double lo[3],
+                       const double hi[3], const ao_camera* cam, const ao_render_opts* o, float* rgb, float* alpha,
+                       uint8_t* mask) {
+  figpose_t P;
+  int e;
+  if ((e = figure_prepare(f, bones12, &P))) return e;
+  double w2n[12];
+  rinverse(global12, w2n);
+  const int N = o->samples_per_ray;
+  double* t = (double*)malloc(sizeof(double) * (size_t)(N + 1));
+  if (!t) return fail(5, "oracle: out of memory");
+  for (int py = 0; py < cam->height; ++py)
+    for (int px = 0; px < cam->width; ++px) {
+      const size_t pix = (size_t)py * cam->width + px;
+      ray_t ray = generate_ray(cam, px, py);
+      if (mask) {
+        int hit = 0;
+        for (int i = 0; i < P.nb && !hit; ++i)
+          hit = ray_segment_distance(ray.o, ray.d, P.a[i], P.b[i]) < f->skel.radius[i];
+        mask[pix] = (uint8_t)hit;
+      }
+      double cr = 0, cg = 0, cb = 0, a = 0;
+      const v3 on = rapply(w2n, ray.o);
+      const v3 dn = vsub(rapply(w2n, ray_at(&ray, 1.0)), on);
+      double tn, tf;
+      if (ray_box(on, dn, lo, hi, &tn, &tf) && tn < tf && N > 0) {
+        pcg rng = keyed_rng(o->seed, o->frame_id, (uint64_t)pix, 0);
+        const double step = (tf - tn) / N;
+        for (int i = 0; i < N; ++i) t[i] = tn + (i + (o->stratified ? pcg_double(&rng) : 0.5)) * step;
+        double T = 1.0;
+        for (int i = 0; i < N; ++i) {
+          if (o->epsilon_terminate > 0 && T <= o->epsilon_terminate) break;
+          v3 c;
+          const double sigma = figure_query(f, &P, ray_at(&ray, t[i]), &c);
+          if (sigma <= 0.0) continue;
+          const double delta = (i + 1 < N) ? t[i + 1] - t[i] : tf - t[i];
+          const double al = -expm1(-sigma * delta);
+          const double w = al * T;
+          cr += c.x * w;
+          cg += c.y * w;
+          cb += c.z * w;
+          a += w;
+          T *= 1.0 - al;
+        }
+      }
+      if (rgb) {
+        rgb[3 * pix] = (float)cr;
+        rgb[3 * pix + 1] = (float)cg;
+        rgb[3 * pix + 2] = (float)cb;
+      }
+      if (alpha) alpha[pix] = (float)a;
+    }
+  free(t);
+  return 0;
+}
+
+/* ---- training losses + optimizer (no reference code exists) ---------- */
+
+/* Eq. 9-11 per ray on the f32 rendered values, in double; gradients of the weighted batch
+ * mean rounded to f32 (hard subgradient at 0/1 = one-sided limit inside). */
+int arfo_losses(int64_t n, const float* rgb, const float* alpha, const float* gt_rgb, const float* gt_alpha,
+                const ao_loss_cfg* c, double* loss4, float* d_rgb, float* d_alpha) {
+  if (!(c->huber_delta > 0)) return fail(1, "loss: huber_delta must be positive");
+  const double inv_n = n > 0 ? 1.0 / (double)n : 0.0;
+  double sr = 0, sa = 0, sh = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const double ex = (double)rgb[3 * r] - (double)gt_rgb[3 * r];
+    const double ey = (double)rgb[3 * r + 1] - (double)gt_rgb[3 * r + 1];
+    const double ez = (double)rgb[3 * r + 2] - (double)gt_rgb[3 * r + 2];
+    const double rn = sqrt(ex * ex + ey * ey + ez * ez);
+    const double d = c->huber_delta;
+    double lr, gs;
+    if (rn <= d) {
+      lr = 0.5 * (rn * rn);
+      gs = 1.0;
+    } else {
+      lr = d * (rn - 0.5 * d);
+      gs = d / rn;
+    }
+    const double crgb = c->w_rgb * inv_n;
+    if (d_rgb) {
+      d_rgb[3 * r] = (float)(crgb * (ex * gs));
+      d_rgb[3 * r + 1] = (float)(crgb * (ey * gs));
+      d_rgb[3 * r + 2] = (float)(crgb * (ez * gs));
+    }
+    const double A = (double)alpha[r];
+    const double ea = A - (double)gt_alpha[r];
+    const double la = fabs(ea);
+    const double s1 = ea > 0.0 ? 1.0 : (ea < 0.0 ? -1.0 : 0.0);
+    const double p = exp(-fabs(A)), q = exp(-fabs(A - 1.0));
+    const double sum = p + q;
+    const double lh = -log(sum) + log1p(exp(-1.0));
+    const double sp = A < 0.0 ? -1.0 : 1.0, sq = A > 1.0 ? 1.0 : -1.0;
+    const double dh = (sp * p + sq * q) / sum;
+    if (d_alpha) d_alpha[r] = (float)((c->w_alpha * s1 + c->w_hard * dh) * inv_n);
+    sr += lr;
+    sa += la;
+    sh += lh;
+  }
+  if (loss4) {
+    loss4[0] = sr * inv_n;
+    loss4[1] = sa * inv_n;
+    loss4[2] = sh * inv_n;
+    loss4[3] = c->w_rgb * loss4[0] + c->w_alpha * loss4[1] + c->w_hard * loss4[2];
+  }
+  return 0;
+}
+
+static double cosine_lr(double lr0, const ao_adam_cfg* c, int64_t step) {
+  if (c->total_steps <= 0) return lr0;
+  const double t = (double)(step < c->total_steps ? step : c->total_steps) / (double)c->total_steps;
+  const double f = c->final_lr_factor;
+  return lr0 * (f + (1.0 - f) * 0.5 * (1.0 + cos(3.14159265358979323846 * t)));
+}
+
+int arfo_adam(int64_t n, float* p, float* g, float* m, float* v, const ao_adam_cfg* c, int64_t step,
+              int64_t mlp_offset) {
+  if (step < 1) return fail(1, "adam: step must be >= 1");
+  const float b1 = (float)c->beta1, omb1 = (float)(1.0 - c->beta1);
+  const float b2 = (float)c->beta2, omb2 = (float)(1.0 - c->beta2);
+  const float c1 = (float)(1.0 / (1.0 - pow(c->beta1, (double)step)));
+  const float c2 = (float)(1.0 / (1.0 - pow(c->beta2, (double)step)));
+  const float eps = (float)c->eps;
+  const float lrg = (float)cosine_lr(c->lr_grid, c, step), lrm = (float)cosine_lr(c->lr_mlp, c, step);
+  for (int64_t i = 0; i < n; ++i) {
+    const float gg = g[i];
+    const float lr = i >= mlp_offset ? lrm : lrg;
+    m[i] = b1 * m[i] + omb1 * gg;
+    v[i] = b2 * v[i] + omb2 * (gg * gg);
+    const float den = sqrtf(v[i] * c2) + eps;
+    p[i] = p[i] - (lr * (m[i] * c1)) / den;
+    g[i] = 0.0f;
+  }
+  return 0;
+}

@@ -111,6 +111,13 @@ typedef struct {
   double* s_delta;    /* [cap] */
 } ao_render_trace;
 
+typedef struct { /* arf::CapsuleFigure, R/scene.hpp:13-27 */
+  ao_skeleton skel;
+  double color[AO_MAX_BONES][3];
+  double amplitude[AO_MAX_BONES];
+  double softness;
+} ao_figure;
+
 #define AO_API_DECLARE(P)                                                                        \
   const char* P##last_error(void);                                                               \
   int P##model_sizes(const ao_skeleton* s, const ao_grid_cfg* g, const ao_mlp_cfg* m,            \
@@ -159,10 +166,31 @@ typedef struct {
                        const ao_camera* cam, const ao_occ_grid* occ, const ao_render_opts* o,    \
                        int64_t n_rays, const int32_t* px, const int32_t* py,                     \
                        const float* d_color, const float* d_alpha, float* rgb, float* alpha,     \
-                       float* grid_grad, float* mlp_grad, uint64_t* counters);
+                       float* grid_grad, float* mlp_grad, uint64_t* counters);                   \
+  int P##figure_query(const ao_figure* f, const double* bones12, const double* pts, int64_t n,   \
+                      double* dens, double* col);                                                \
+  int P##figure_render(const ao_figure* f, const double* bones12, const double* global12,        \
+                       const double lo[3], const double hi[3], const ao_camera* cam,             \
+                       const ao_render_opts* o, float* rgb, float* alpha, uint8_t* mask);
 
 AO_API_DECLARE(arfo_)
 AO_API_DECLARE(arfr_)
+
+/* Training pieces with no reference implementation (SPEC.md:454-530 only; SURVEY.md §8f
+ * row 1): restated here from the SPEC text, oracle-only (no arfr_ counterpart). */
+typedef struct {
+  double w_rgb, w_alpha, w_hard, w_density, huber_delta;
+} ao_loss_cfg;
+typedef struct {
+  double lr_grid, lr_mlp, beta1, beta2, eps;
+  int64_t total_steps;
+  double final_lr_factor;
+} ao_adam_cfg;
+int arfo_losses(int64_t n, const float* rgb, const float* alpha, const float* gt_rgb, const float* gt_alpha,
+                const ao_loss_cfg* c, double* loss4, float* d_rgb, float* d_alpha);
+/* one Adam step over a flat vector; lr_of(i) = i >= mlp_offset ? lr_mlp_t : lr_grid_t */
+int arfo_adam(int64_t n, float* p, float* g, float* m, float* v, const ao_adam_cfg* c, int64_t step,
+              int64_t mlp_offset);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,21 @@ class Skel(C.Structure):
                 ("tail", (C.c_double * 3) * MAXB), ("radius", C.c_double * MAXB)]
 
 
+class Figure(C.Structure):
+    _fields_ = [("skel", Skel), ("color", (C.c_double * 3) * MAXB), ("amplitude", C.c_double * MAXB),
+                ("softness", C.c_double)]
+
+
+class LossCfg(C.Structure):
+    _fields_ = [("w_rgb", C.c_double), ("w_alpha", C.c_double), ("w_hard", C.c_double), ("w_density", C.c_double),
+                ("huber_delta", C.c_double)]
+
+
+class AdamCfg(C.Structure):
+    _fields_ = [("lr_grid", C.c_double), ("lr_mlp", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("total_steps", C.c_int64), ("final_lr_factor", C.c_double)]
+
+
 class GridCfg(C.Structure):
     _fields_ = [("levels", C.c_int), ("features_per_level", C.c_int), ("table_size_log2", C.c_int),
                 ("base_resolution", C.c_int), ("max_resolution", C.c_int), ("box_lo", C.c_double * 3),
@@ -301,6 +316,68 @@ class Checker:
     @staticmethod
     def occ_arrays(g):
         return g._arrays
+
+    def figure(self, fig) -> Figure:
+        f = Figure()
+        f.skel = self.skel(fig.skeleton)
+        col = np.asarray(fig.colors, np.float64).reshape(-1, 3)
+        amp = np.asarray(fig.amplitudes, np.float64).reshape(-1)
+        for i in range(col.shape[0]):
+            for c in range(3):
+                f.color[i][c] = float(col[i, c])
+            f.amplitude[i] = float(amp[i])
+        f.softness = float(fig.softness)
+        return f
+
+    def figure_query(self, fig, pts, bones12=None):
+        p = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+        dens = np.zeros(p.shape[0], np.float64)
+        col = np.zeros((p.shape[0], 3), np.float64)
+        b = None if bones12 is None else np.ascontiguousarray(bones12, np.float64)
+        self.check(self.f("figure_query")(C.byref(self.figure(fig)), _p(b, C.c_double), _p(p, C.c_double),
+                                          C.c_int64(p.shape[0]), _p(dens, C.c_double), _p(col, C.c_double)))
+        return dens, col
+
+    def figure_render(self, fig, bones12, global12, lo, hi, cam, opts):
+        W, H = cam.width, cam.height
+        rgb = np.zeros((H, W, 3), np.float32)
+        alpha = np.zeros((H, W), np.float32)
+        mask = np.zeros((H, W), np.uint8)
+        b = np.ascontiguousarray(bones12, np.float64)
+        g = np.ascontiguousarray(global12, np.float64)
+        lo = np.ascontiguousarray(lo, np.float64)
+        hi = np.ascontiguousarray(hi, np.float64)
+        self.check(self.f("figure_render")(C.byref(self.figure(fig)), _p(b, C.c_double), _p(g, C.c_double),
+                                           _p(lo, C.c_double), _p(hi, C.c_double), C.byref(self.cam(cam)),
+                                           C.byref(self.opts(opts)), _p(rgb, C.c_float), _p(alpha, C.c_float),
+                                           _p(mask, C.c_uint8)))
+        return rgb, alpha, mask
+
+    # ---- training pieces with no reference code: oracle restatement only
+    def losses(self, rgb, alpha, gt_rgb, gt_alpha, cfg):
+        assert self.kind == "oracle", "losses exist only in the C restatement (the reference has none)"
+        r = np.ascontiguousarray(rgb, np.float32).reshape(-1, 3)
+        n = r.shape[0]
+        a = np.ascontiguousarray(alpha, np.float32).reshape(n)
+        gr = np.ascontiguousarray(gt_rgb, np.float32).reshape(n, 3)
+        ga = np.ascontiguousarray(gt_alpha, np.float32).reshape(n)
+        l4 = np.zeros(4, np.float64)
+        dr = np.zeros((n, 3), np.float32)
+        da = np.zeros(n, np.float32)
+        c = LossCfg(cfg.w_rgb, cfg.w_alpha, cfg.w_hard, cfg.w_density, cfg.huber_delta)
+        self.check(self.f("losses")(C.c_int64(n), _p(r, C.c_float), _p(a, C.c_float), _p(gr, C.c_float),
+                                    _p(ga, C.c_float), C.byref(c), _p(l4, C.c_double), _p(dr, C.c_float),
+                                    _p(da, C.c_float)))
+        return l4, dr, da
+
+    def adam(self, p, g, m, v, cfg, step, mlp_offset):
+        """In place on float32 numpy arrays (one Adam step, grads zeroed)."""
+        assert self.kind == "oracle"
+        for a in (p, g, m, v):
+            assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+        c = AdamCfg(cfg.lr_grid, cfg.lr_mlp, cfg.beta1, cfg.beta2, cfg.eps, int(cfg.total_steps), cfg.final_lr_factor)
+        self.check(self.f("adam")(C.c_int64(p.size), _p(p, C.c_float), _p(g, C.c_float), _p(m, C.c_float),
+                                  _p(v, C.c_float), C.byref(c), C.c_int64(step), C.c_int64(mlp_offset)))
 
     def render(self, M, bones12, global12, cam, occ, opts):
         W, H = cam.width, cam.height

@@ -655,3 +655,70 @@ int arfr_bench_frames(const ao_model* m, int n_frames, const double* bones12,
 int arfr_thread_count(void) { return arf::thread_count(); }
 
 }  // extern "C"
+
+namespace {
+arf::CapsuleFigure figure_of(const ao_figure* f) {
+  arf::CapsuleFigure fig;
+  fig.skeleton = skeleton(&f->skel);
+  for (int i = 0; i < f->skel.n_bones; ++i) {
+    fig.colors.push_back(v3(f->color[i]));
+    fig.amplitudes.push_back(f->amplitude[i]);
+  }
+  fig.softness = f->softness;
+  return fig;
+}
+}  // namespace
+
+extern "C" {
+
+// analytic_query (R/scene.hpp:31-50) / PosedFigure::query (:79-97)
+int arfr_figure_query(const ao_figure* f, const double* bones12, const double* pts, int64_t n, double* dens,
+                      double* col) {
+  return guard([&] {
+    const arf::CapsuleFigure fig = figure_of(f);
+    fig.validate();
+    if (bones12) {
+      const arf::PosedFigure pf(fig, pose_of(f->skel.n_bones, bones12, bones12));
+      for (int64_t i = 0; i < n; ++i) {
+        const auto r = pf.query(v3(pts + 3 * i));
+        dens[i] = r.density;
+        put3(col + 3 * i, r.color);
+      }
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const auto r = arf::analytic_query(v3(pts + 3 * i), fig);
+        dens[i] = r.density;
+        put3(col + 3 * i, r.color);
+      }
+    }
+  });
+}
+
+// The dataset frame: render_image (R/render.hpp:178-218) of PosedFigure::query through
+// G^-1 into the given normalized box, no occupancy; mask = PosedFigure::ray_hits.
+int arfr_figure_render(const ao_figure* f, const double* bones12, const double* global12, const double lo[3],
+                       const double hi[3], const ao_camera* cam, const ao_render_opts* o, float* rgb, float* alpha,
+                       uint8_t* mask) {
+  return guard([&] {
+    const arf::CapsuleFigure fig = figure_of(f);
+    const arf::SkeletonPose pose = pose_of(f->skel.n_bones, bones12, global12);
+    const arf::PosedFigure pf(fig, pose);
+    const arf::Rigidd ginv = pose.global_transform.inverse();
+    const arf::Camera C = camera(cam);
+    const arf::RenderImages img = arf::render_image<double>(
+        C, box(lo, hi),
+        [&](const arf::Vec3d& x, arf::RadianceSample<double>& out) {
+          out = pf.query(x);
+          return out.density > 0.0;
+        },
+        [&](const arf::Vec3d& x) { return ginv.apply(x); }, nullptr, render_opts(o));
+    if (rgb) std::copy(img.rgb.begin(), img.rgb.end(), rgb);
+    if (alpha) std::copy(img.alpha.begin(), img.alpha.end(), alpha);
+    if (mask)
+      for (int py = 0; py < C.height; ++py)
+        for (int px = 0; px < C.width; ++px)
+          mask[static_cast<size_t>(py) * C.width + px] = pf.ray_hits(arf::generate_ray(C, px, py)) ? 1 : 0;
+  });
+}
+
+}  // extern "C"

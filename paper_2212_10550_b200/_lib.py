@@ -69,6 +69,21 @@ class ArfxModelDesc(C.Structure):
                 ("n_mlp_params", C.c_size_t), ("n_skin_weights", C.c_size_t)]
 
 
+class ArfxLossConfig(C.Structure):
+    _fields_ = [("w_rgb", C.c_double), ("w_alpha", C.c_double), ("w_hard", C.c_double), ("w_density", C.c_double),
+                ("huber_delta", C.c_double)]
+
+
+class ArfxAdamConfig(C.Structure):
+    _fields_ = [("lr_grid", C.c_double), ("lr_mlp", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("total_steps", C.c_int64), ("final_lr_factor", C.c_double)]
+
+
+class ArfxFigure(C.Structure):
+    _fields_ = [("skeleton", ArfxSkeleton), ("color", (C.c_double * 3) * MAX_BONES),
+                ("amplitude", C.c_double * MAX_BONES), ("softness", C.c_double)]
+
+
 H = C.c_void_p  # opaque handles
 P = C.c_void_p  # raw pointers / streams
 
@@ -139,6 +154,26 @@ _PROTOS = {
     "arfx_train_fwd_bwd": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int64,
                                      c_int32_p, c_int32_p, c_float_p, c_float_p, c_float_p, c_float_p,
                                      C.POINTER(ArfxCounters), P]),
+    "arfx_losses": (C.c_int, [C.c_int64, c_float_p, c_float_p, c_float_p, c_float_p, C.POINTER(ArfxLossConfig),
+                              c_double_p, c_float_p, c_float_p]),
+    "arfx_train_step": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int64,
+                                  c_int32_p, c_int32_p, c_float_p, c_float_p, C.POINTER(ArfxLossConfig), c_double_p,
+                                  c_float_p, c_float_p, C.POINTER(ArfxCounters), P]),
+    "arfx_train_step_device": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int64,
+                                         P, P, P, P, C.POINTER(ArfxLossConfig), P, P, P, P]),
+    "arfx_adam_step": (C.c_int, [H, C.POINTER(ArfxAdamConfig), C.c_int64, C.c_int64, C.c_int64, P]),
+    "arfx_model_flat": (C.c_int, [H, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "arfx_model_get_adam": (C.c_int, [H, c_float_p, c_float_p]),
+    "arfx_model_set_adam": (C.c_int, [H, c_float_p, c_float_p]),
+    "arfx_figure_query": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, C.c_int64, c_double_p,
+                                    c_double_p]),
+    "arfx_figure_render": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, c_double_p, c_double_p,
+                                     C.POINTER(ArfxCamera), C.POINTER(ArfxRenderOptions), c_float_p, c_float_p,
+                                     c_uint8_p, P]),
+    "arfx_figure_render_rays_device": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, c_double_p,
+                                                 c_double_p, C.POINTER(ArfxCamera), C.POINTER(ArfxRenderOptions),
+                                                 C.c_int64, P, P, P, P, P, P]),
 }
 
 STATUS_NAMES = {1: "invalid_argument", 2: "DataError", 3: "NumericError", 4: "domain_error",

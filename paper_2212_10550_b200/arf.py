@@ -251,7 +251,8 @@ class Model:
 
     def set_mlp_mode(self, mode: str) -> None:
         """'exact' (f32 SIMT, the reference's summation order; default) or 'tcgen05'
-        (tensor-core tf32, stated tolerance 1e-3 relative on rendered RGB). Render only."""
+        (tensor cores, split-bf16 operands with f32 accumulation; stated tolerance 1e-3
+        relative on rendered RGB). Render only."""
         call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1}[mode])
 
     def zero_grad(self):
@@ -267,6 +268,31 @@ class Model:
         ps = [C.c_void_p() for _ in range(4)]
         call("arfx_model_device_arrays", self._h, *[C.byref(p) for p in ps])
         return [p.value for p in ps]
+
+    def flat(self) -> dict:
+        """Flat device vectors [grid | pad | mlp | pad]: pointers to params, grads, Adam m, v,
+        their length n_flat and the MLP offset (arfx_model_flat)."""
+        ps = [C.c_void_p() for _ in range(4)]
+        n, off = C.c_int64(), C.c_int64()
+        call("arfx_model_flat", self._h, *[C.byref(p) for p in ps], C.byref(n), C.byref(off))
+        return {"params": ps[0].value, "grads": ps[1].value, "adam_m": ps[2].value, "adam_v": ps[3].value,
+                "n_flat": n.value, "mlp_offset": off.value}
+
+    def adam_step(self, cfg: "AdamConfig", step: int, begin: int = 0, end: int = -1, stream=None) -> None:
+        """One Adam step (zero-grad fused) over flat indices [begin, end) (arfx_adam_step)."""
+        call("arfx_adam_step", self._h, C.byref(cfg.to_c()), step, begin, end, stream)
+
+    def adam_state(self):
+        n = self.flat()["n_flat"]
+        m = np.zeros(n, np.float32)
+        v = np.zeros(n, np.float32)
+        call("arfx_model_get_adam", self._h, ptr(m, C.c_float), ptr(v, C.c_float))
+        return m, v
+
+    def set_adam_state(self, m, v) -> None:
+        m = np.ascontiguousarray(m, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        call("arfx_model_set_adam", self._h, ptr(m, C.c_float), ptr(v, C.c_float))
 
     def close(self):
         if self._h:
@@ -577,6 +603,128 @@ def train_fwd_bwd(model: Model, pose: "SkeletonPose | PosedModelView", camera: C
     model.counters.posed_queries += cnt.posed_queries
     model.counters.canonical_queries += cnt.canonical_queries
     return rgb, alpha
+
+
+# ----------------------------------------------------------------------------- training
+
+
+@dataclass
+class LossConfig:  # LossWeights SPEC.md:446-449, defaults
+    w_rgb: float = 1.0
+    w_alpha: float = 0.1
+    w_hard: float = 0.1
+    w_density: float = 0.1
+    huber_delta: float = 0.1
+
+    def to_c(self) -> L.ArfxLossConfig:
+        return L.ArfxLossConfig(self.w_rgb, self.w_alpha, self.w_hard, self.w_density, self.huber_delta)
+
+
+@dataclass
+class AdamConfig:  # SPEC.md:508-509 (betas / eps: the encoding system's practice)
+    lr_grid: float = 1e-2
+    lr_mlp: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.99
+    eps: float = 1e-15
+    total_steps: int = 0        # cosine horizon; <= 0: constant lr
+    final_lr_factor: float = 0.0
+
+    def to_c(self) -> L.ArfxAdamConfig:
+        return L.ArfxAdamConfig(self.lr_grid, self.lr_mlp, self.beta1, self.beta2, self.eps, int(self.total_steps),
+                                self.final_lr_factor)
+
+
+def losses(rgb, alpha, gt_rgb, gt_alpha, cfg: LossConfig):
+    """SPEC.md:454-477 losses on rendered values: returns (loss4, d_rgb, d_alpha) with
+    loss4 = (L_rgb, L_alpha, L_hard, weighted total) and f32 gradients of the total."""
+    r = np.ascontiguousarray(rgb, np.float32).reshape(-1, 3)
+    n = r.shape[0]
+    a = np.ascontiguousarray(alpha, np.float32).reshape(n)
+    gr = np.ascontiguousarray(gt_rgb, np.float32).reshape(n, 3)
+    ga = np.ascontiguousarray(gt_alpha, np.float32).reshape(n)
+    l4 = np.zeros(4, np.float64)
+    dr = np.zeros((n, 3), np.float32)
+    da = np.zeros(n, np.float32)
+    call("arfx_losses", n, ptr(r, C.c_float), ptr(a, C.c_float), ptr(gr, C.c_float), ptr(ga, C.c_float),
+         C.byref(cfg.to_c()), ptr(l4, C.c_double), ptr(dr, C.c_float), ptr(da, C.c_float))
+    return l4, dr, da
+
+
+def train_step(model: Model, pose: "SkeletonPose | PosedModelView", camera: Camera, occupancy: "OccupancyGrid | None",
+               opt: RenderOptions, px, py, gt_rgb, gt_alpha, cfg: LossConfig):
+    """Fused training forward + losses + backward (arfx_train_step): accumulates gradients
+    into the model; returns (loss4, rgb, alpha)."""
+    view = pose if isinstance(pose, PosedModelView) else PosedModelView(model, pose)
+    pxa = np.ascontiguousarray(px, np.int32)
+    pya = np.ascontiguousarray(py, np.int32)
+    n = pxa.shape[0]
+    gr = np.ascontiguousarray(gt_rgb, np.float32).reshape(n, 3)
+    ga = np.ascontiguousarray(gt_alpha, np.float32).reshape(n)
+    l4 = np.zeros(4, np.float64)
+    rgb = np.zeros((n, 3), np.float32)
+    alpha = np.zeros(n, np.float32)
+    cnt = L.ArfxCounters()
+    call("arfx_train_step", model._h, view._h, C.byref(camera.to_c()),
+         occupancy._h if occupancy is not None else None, C.byref(opt.to_c()), n, ptr(pxa, C.c_int32),
+         ptr(pya, C.c_int32), ptr(gr, C.c_float), ptr(ga, C.c_float), C.byref(cfg.to_c()), ptr(l4, C.c_double),
+         ptr(rgb, C.c_float), ptr(alpha, C.c_float), C.byref(cnt), None)
+    model.counters.posed_queries += cnt.posed_queries
+    model.counters.canonical_queries += cnt.canonical_queries
+    return l4, rgb, alpha
+
+
+# ----------------------------------------------------------------------------- analytic ground truth
+
+
+@dataclass
+class CapsuleFigure:  # R/scene.hpp:13-27
+    skeleton: Skeleton
+    colors: np.ndarray       # (n_bones, 3)
+    amplitudes: np.ndarray   # (n_bones,)
+    softness: float = 0.01
+
+    def to_c(self) -> L.ArfxFigure:
+        f = L.ArfxFigure()
+        f.skeleton = self.skeleton.to_c()
+        col = np.asarray(self.colors, np.float64).reshape(-1, 3)
+        amp = np.asarray(self.amplitudes, np.float64).reshape(-1)
+        if col.shape[0] != self.skeleton.bone_count() or amp.shape[0] != self.skeleton.bone_count():
+            raise L.InvalidArgument(1, "figure: per-bone color/amplitude required")
+        for i in range(col.shape[0]):
+            for c in range(3):
+                f.color[i][c] = float(col[i, c])
+            f.amplitude[i] = float(amp[i])
+        f.softness = float(self.softness)
+        return f
+
+
+def figure_query(fig: CapsuleFigure, pts, pose: SkeletonPose | None = None):
+    """analytic_query (R/scene.hpp:31-50) or, with a pose, PosedFigure::query (:79-97)."""
+    p = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    n = p.shape[0]
+    dens = np.zeros(n, np.float64)
+    col = np.zeros((n, 3), np.float64)
+    bt = None if pose is None else np.ascontiguousarray(pose.bone_transforms, np.float64)
+    call("arfx_figure_query", C.byref(fig.to_c()), ptr(bt, C.c_double), ptr(p, C.c_double), n,
+         ptr(dens, C.c_double), ptr(col, C.c_double))
+    return dens, col
+
+
+def figure_render(fig: CapsuleFigure, pose: SkeletonPose, normalized_box: Aabb, camera: Camera,
+                  opt: RenderOptions):
+    """Ground-truth frame of the posed analytic figure: render_image (R/render.hpp:178-218)
+    through normalized space (G^-1) into `normalized_box`, no occupancy; plus the exact
+    silhouette mask PosedFigure::ray_hits (R/scene.hpp:123-130). Returns (RenderImages, mask)."""
+    W, Hh = camera.width, camera.height
+    out = RenderImages(W, Hh, np.zeros((Hh, W, 3), np.float32), np.zeros((Hh, W), np.float32))
+    mask = np.zeros((Hh, W), np.uint8)
+    lo = np.asarray(normalized_box.lo, np.float64)
+    hi = np.asarray(normalized_box.hi, np.float64)
+    call("arfx_figure_render", C.byref(fig.to_c()), ptr(pose.bone_transforms, C.c_double),
+         ptr(pose.global_transform, C.c_double), ptr(lo, C.c_double), ptr(hi, C.c_double), C.byref(camera.to_c()),
+         C.byref(opt.to_c()), ptr(out.rgb, C.c_float), ptr(out.alpha, C.c_float), ptr(mask, C.c_uint8), None)
+    return out, mask
 
 
 def shard_rows(height: int, rank: int, world: int, tile: int = 16) -> list:

@@ -195,10 +195,24 @@ void setup_model(ModelImpl& m, const std::vector<HostBone>& bones, GridCfg grid,
 void alloc_model(ModelImpl& m) {
   ARFX_CUDA(cudaGetDevice(&m.device));
   if (!m.stream) ARFX_CUDA(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
-  m.grid_params.alloc(m.n_grid);
-  m.mlp_params.alloc((m.n_mlp + 3) / 4 * 4);  // float4-padded for the smem staging
-  ARFX_CUDA(cudaMemset(m.mlp_params.ptr, 0, m.mlp_params.n * sizeof(float)));
+  // [grid | pad to 256 B | mlp (float4-padded for the smem staging) | pad to 1024 floats]
+  m.mlp_off = (m.n_grid + 63) / 64 * 64;
+  m.n_flat = (m.mlp_off + (m.n_mlp + 3) / 4 * 4 + 1023) / 1024 * 1024;
+  m.flat_params.alloc(m.n_flat);
+  ARFX_CUDA(cudaMemset(m.flat_params.ptr, 0, m.n_flat * sizeof(float)));
+  m.grid_params.view(m.flat_params.ptr, m.n_grid);
+  m.mlp_params.view(m.flat_params.ptr + m.mlp_off, (m.n_mlp + 3) / 4 * 4);
   m.skin.alloc(m.n_skin);
+}
+
+// FieldGrads (R/field.hpp:19-36) as one flat zeroed vector laid out like the parameters
+void ensure_grad_store(ModelImpl& m, cudaStream_t s) {
+  if (m.flat_grads.ptr) return;
+  m.flat_grads.alloc(m.n_flat);
+  ARFX_CUDA(cudaMemsetAsync(m.flat_grads.ptr, 0, m.n_flat * sizeof(float), s));
+  ARFX_CUDA(cudaStreamSynchronize(s));
+  m.grid_grad.view(m.flat_grads.ptr, m.n_grid);
+  m.mlp_grad.view(m.flat_grads.ptr + m.mlp_off, m.n_mlp);
 }
 
 void make_pose_host(ModelImpl& m, const double* bones12, const double* global12, PoseCtx& ctx) {
@@ -279,6 +293,55 @@ void ray_offsets(int n_rays, const int32_t* ray_len, std::vector<int64_t>& off) 
     require(ray_len[r] >= 0, "composite: negative ray length");
     off[static_cast<size_t>(r) + 1] = off[static_cast<size_t>(r)] + ray_len[r];
   }
+}
+}  // namespace
+}  // namespace arfx
+
+namespace arfx {
+namespace {
+// CapsuleFigure::validate (R/scene.hpp:19-26) + PosedFigure ctor (:61-75)
+FigureView figure_view_of(const arfx_figure* fig, const double* bones12) {
+  require(fig != nullptr, "figure: null");
+  const std::vector<HostBone> bones = bones_of(&fig->skeleton);
+  validate_skeleton(bones);
+  for (int i = 0; i < fig->skeleton.n_bones; ++i)
+    if (!(fig->amplitude[i] > 0)) throw std::invalid_argument("figure: amplitudes must be positive");
+  if (!(fig->softness > 0)) throw std::invalid_argument("figure: softness must be positive");
+  FigureView F{};
+  F.nb = fig->skeleton.n_bones;
+  F.soft = fig->softness;
+  for (int i = 0; i < F.nb; ++i) {
+    const HostBone& b = bones[static_cast<size_t>(i)];
+    HV a = b.head, t = b.tail;
+    if (bones12) {
+      a = rigid_apply(bones12 + 12 * i, b.head);
+      t = rigid_apply(bones12 + 12 * i, b.tail);
+    }
+    F.a[i][0] = a.x, F.a[i][1] = a.y, F.a[i][2] = a.z;
+    F.b[i][0] = t.x, F.b[i][1] = t.y, F.b[i][2] = t.z;
+    F.radius[i] = b.radius;
+    F.amp[i] = fig->amplitude[i];
+    for (int c = 0; c < 3; ++c) F.col[i][c] = fig->color[i][c];
+  }
+  return F;
+}
+
+struct FigureFrame {
+  FigureView F;
+  HostCamera cam;
+  double w2n[12];
+};
+
+FigureFrame figure_frame(const arfx_figure* fig, const double* bones12, const double* global12,
+                         const double* lo, const double* hi, const arfx_camera* cam, const arfx_render_options* opt) {
+  require(bones12 && global12 && lo && hi && opt, "figure_render: null argument");
+  FigureFrame f;
+  f.F = figure_view_of(fig, bones12);
+  f.cam = camera_of(cam);
+  validate_camera(f.cam);
+  require(opt->samples_per_ray >= 0, "figure_render: negative samples_per_ray");
+  rigid_inverse(global12, f.w2n);
+  return f;
 }
 }  // namespace
 }  // namespace arfx
@@ -501,11 +564,9 @@ int arfx_model_zero_grad(arfx_model mh, void* stream) {
     require(mh != nullptr, "null model");
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
-    m.grid_grad.ensure(m.n_grid);
-    m.mlp_grad.ensure(m.n_mlp);
+    ensure_grad_store(m, m.stream);
     const cudaStream_t s = stream_of(m, stream);
-    ARFX_CUDA(cudaMemsetAsync(m.grid_grad.ptr, 0, m.n_grid * sizeof(float), s));
-    ARFX_CUDA(cudaMemsetAsync(m.mlp_grad.ptr, 0, m.n_mlp * sizeof(float), s));
+    ARFX_CUDA(cudaMemsetAsync(m.flat_grads.ptr, 0, m.n_flat * sizeof(float), s));
   });
 }
 
@@ -526,8 +587,7 @@ int arfx_model_device_arrays(arfx_model mh, float** gp, float** mp, float** gg, 
     require(mh != nullptr, "null model");
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
-    m.grid_grad.ensure(m.n_grid);
-    m.mlp_grad.ensure(m.n_mlp);
+    ensure_grad_store(m, m.stream);
     if (gp) *gp = m.grid_params.ptr;
     if (mp) *mp = m.mlp_params.ptr;
     if (gg) *gg = m.grid_grad.ptr;
@@ -1134,14 +1194,7 @@ int arfx_composite_backward(int n_rays, const int32_t* ray_len, const double* t,
 }
 
 namespace {
-void ensure_grads(ModelImpl& m, cudaStream_t s) {
-  if (!m.grid_grad.ptr) {
-    m.grid_grad.alloc(m.n_grid);
-    m.mlp_grad.alloc(m.n_mlp);
-    ARFX_CUDA(cudaMemsetAsync(m.grid_grad.ptr, 0, m.n_grid * sizeof(float), s));
-    ARFX_CUDA(cudaMemsetAsync(m.mlp_grad.ptr, 0, m.n_mlp * sizeof(float), s));
-  }
-}
+void ensure_grads(ModelImpl& m, cudaStream_t s) { ensure_grad_store(m, s); }
 }  // namespace
 
 // CanonicalField::query_backward (R/field.hpp:91-103) over a batch; accumulates into the
@@ -1181,24 +1234,95 @@ int arfx_field_query_backward(arfx_model mh, const double* pts, int64_t n, const
   });
 }
 
+}  // extern "C"
+
+namespace arfx {
+namespace {
+__global__ void pixel_check_kernel(long long n, const int32_t* px, const int32_t* py, int W, int H,
+                                   unsigned long long* bad) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    if (px[i] < 0 || py[i] < 0 || px[i] >= W || py[i] >= H) atomicAdd(bad, 1ull);
+}
+
+void validate_train(arfx_model mh, arfx_pose ph, const arfx_render_options* opt, const HostCamera& hc) {
+  require(mh && ph && opt, "train: null argument");
+  validate_camera(hc);
+  require(opt->samples_per_ray <= 1024, "render: libarfx supports samples_per_ray <= 1024");
+}
+
+// One training forward + backward over n rays on device arrays (train.cu): ray-list march,
+// deformer, field forward (re-run on workspace overflow), composite + reverse pass with
+// given upstream gradients (d_dC/d_dA) or the fused losses (lt), field backward into the
+// model's flat gradient vector. Returns the posed/canonical counters.
+void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, const arfx_render_options* opt,
+               long long n_rays, const int32_t* d_px, const int32_t* d_py, const float* d_dC, const float* d_dA,
+               const LossTargets* lt, float* d_rgb, float* d_alpha, cudaStream_t s, unsigned long long* hcnt) {
+  ensure_grad_store(m, s);
+  DevBuf<unsigned long long> bad;
+  bad.alloc(1);
+  ARFX_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(unsigned long long), s));
+  pixel_check_kernel<<<static_cast<unsigned>(std::min<long long>((n_rays + 255) / 256, 1024)), 256, 0, s>>>(
+      n_rays, d_px, d_py, hc.width, hc.height, bad.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  for (int attempt = 0;; ++attempt) {
+    train_forward(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0, opt->seed, opt->frame_id, n_rays, d_px,
+                  d_py, s);
+    unsigned long long nbad = 0;
+    d2h(hcnt, m.ws.counters.ptr, 8, s);
+    d2h(&nbad, bad.ptr, 1, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    if (nbad) throw std::invalid_argument("generate_ray: pixel outside image");
+    bool rerun;
+    check_overflow_and_grow(m, hcnt, rerun);
+    if (!rerun) break;
+    if (attempt == 2) throw std::runtime_error("train: workspace overflow persisted");
+  }
+  Workspace& w = m.ws;
+  w.ensure_train();
+  ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
+  train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
+  field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
+                      s);
+}
+
+LossTargets loss_targets(const arfx_loss_config* cfg, const float* gt_rgb, const float* gt_alpha, double* terms) {
+  require(cfg != nullptr, "loss: null config");
+  require(cfg->w_rgb >= 0 && cfg->w_alpha >= 0 && cfg->w_hard >= 0 && cfg->w_density >= 0,
+          "loss: weights must be non-negative");
+  require(cfg->huber_delta > 0, "loss: huber_delta must be positive");
+  return LossTargets{gt_rgb, gt_alpha, cfg->w_rgb, cfg->w_alpha, cfg->w_hard, cfg->w_density, cfg->huber_delta, terms};
+}
+
+AdamCfg adam_of(const arfx_adam_config* c) {
+  require(c != nullptr, "adam: null config");
+  require(c->lr_grid >= 0 && c->lr_mlp >= 0, "adam: learning rates must be non-negative");
+  require(c->beta1 >= 0 && c->beta1 < 1 && c->beta2 >= 0 && c->beta2 < 1, "adam: betas must be in [0, 1)");
+  require(c->eps > 0, "adam: eps must be positive");
+  return AdamCfg{c->lr_grid, c->lr_mlp, c->beta1, c->beta2, c->eps, static_cast<long long>(c->total_steps),
+                 c->final_lr_factor};
+}
+}  // namespace
+}  // namespace arfx
+
+extern "C" {
+
 // Training forward + backward over n rays (composed per SPEC.md:490-494; see train.cu).
 int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
                        const arfx_render_options* opt, int64_t n_rays, const int32_t* px, const int32_t* py,
                        const float* d_color, const float* d_alpha, float* rgb, float* alpha, arfx_counters* c,
                        void* stream) {
   return guard([&] {
-    require(mh && ph && opt && (n_rays == 0 || (px && py && d_color && d_alpha)), "train_fwd_bwd: null argument");
-    ModelImpl& m = mh->impl;
     const HostCamera hc = camera_of(cam);
-    validate_camera(hc);
-    require(opt->samples_per_ray <= 1024, "render: libarfx supports samples_per_ray <= 1024");
+    validate_train(mh, ph, opt, hc);
+    require(n_rays == 0 || (px && py && d_color && d_alpha), "train_fwd_bwd: null argument");
     for (int64_t r = 0; r < n_rays; ++r)
       if (px[r] < 0 || py[r] < 0 || px[r] >= hc.width || py[r] >= hc.height)
         throw std::invalid_argument("generate_ray: pixel outside image");
+    ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
     if (n_rays <= 0) return;
     const cudaStream_t s = stream_of(m, stream);
-    ensure_grads(m, s);
     Staged<int32_t> PX, PY;
     Staged<float> DC, DA;
     PX.up(px, static_cast<size_t>(n_rays), s);
@@ -1209,23 +1333,8 @@ int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx
     orgb.alloc(static_cast<size_t>(3 * n_rays));
     oalpha.alloc(static_cast<size_t>(n_rays));
     unsigned long long hcnt[8];
-    for (int attempt = 0;; ++attempt) {
-      train_forward(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
-                    opt->seed, opt->frame_id, n_rays, PX.d.ptr, PY.d.ptr, s);
-      d2h(hcnt, m.ws.counters.ptr, 8, s);
-      ARFX_CUDA(cudaStreamSynchronize(s));
-      bool rerun;
-      check_overflow_and_grow(m, hcnt, rerun);
-      if (!rerun) break;
-      if (attempt == 2) throw std::runtime_error("train_fwd_bwd: workspace overflow persisted");
-    }
-    Workspace& w = m.ws;
-    w.ensure_train();
-    ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
-    train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, DC.d.ptr, DA.d.ptr, orgb.ptr,
-                    oalpha.ptr, s);
-    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
-                        w.pgc.ptr, s);
+    run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, PX.d.ptr, PY.d.ptr, DC.d.ptr, DA.d.ptr,
+              nullptr, orgb.ptr, oalpha.ptr, s, hcnt);
     if (rgb) d2h(rgb, orgb.ptr, static_cast<size_t>(3 * n_rays), s);
     if (alpha) d2h(alpha, oalpha.ptr, static_cast<size_t>(n_rays), s);
     ARFX_CUDA(cudaStreamSynchronize(s));
@@ -1233,6 +1342,236 @@ int arfx_train_fwd_bwd(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx
       c->posed_queries = hcnt[0];
       c->canonical_queries = hcnt[1];
     }
+  });
+}
+
+int arfx_losses(int64_t n, const float* rgb, const float* alpha, const float* gt_rgb, const float* gt_alpha,
+                const arfx_loss_config* cfg, double* loss4, float* d_rgb, float* d_alpha) {
+  return guard([&] {
+    require(n == 0 || (rgb && alpha && gt_rgb && gt_alpha), "losses: null argument");
+    LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    require_device();
+    const cudaStream_t s = cudaStreamPerThread;
+    DevBuf<double> T, L4;
+    L4.alloc(4);
+    if (n <= 0) {
+      if (loss4) std::fill(loss4, loss4 + 4, 0.0);
+      return;
+    }
+    Staged<float> R, A, GR, GA;
+    R.up(rgb, static_cast<size_t>(3 * n), s);
+    A.up(alpha, static_cast<size_t>(n), s);
+    GR.up(gt_rgb, static_cast<size_t>(3 * n), s);
+    GA.up(gt_alpha, static_cast<size_t>(n), s);
+    T.alloc(static_cast<size_t>(3 * n));
+    DevBuf<float> dR, dA;
+    dR.alloc(static_cast<size_t>(3 * n));
+    dA.alloc(static_cast<size_t>(n));
+    lt.gt_rgb = GR.d.ptr;
+    lt.gt_alpha = GA.d.ptr;
+    lt.ray_terms = T.ptr;
+    ray_losses(n, R.d.ptr, A.d.ptr, lt, dR.ptr, dA.ptr, s);
+    loss_reduce(T.ptr, n, lt, L4.ptr, s);
+    if (loss4) d2h(loss4, L4.ptr, 4, s);
+    if (d_rgb) d2h(d_rgb, dR.ptr, static_cast<size_t>(3 * n), s);
+    if (d_alpha) d2h(d_alpha, dA.ptr, static_cast<size_t>(n), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_train_step(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                    const arfx_render_options* opt, int64_t n_rays, const int32_t* px, const int32_t* py,
+                    const float* gt_rgb, const float* gt_alpha, const arfx_loss_config* cfg, double* loss4,
+                    float* rgb, float* alpha, arfx_counters* c, void* stream) {
+  return guard([&] {
+    const HostCamera hc = camera_of(cam);
+    validate_train(mh, ph, opt, hc);
+    require(n_rays == 0 || (px && py && gt_rgb && gt_alpha), "train_step: null argument");
+    LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n_rays <= 0) return;
+    const cudaStream_t s = stream_of(m, stream);
+    Staged<int32_t> PX, PY;
+    Staged<float> GR, GA;
+    PX.up(px, static_cast<size_t>(n_rays), s);
+    PY.up(py, static_cast<size_t>(n_rays), s);
+    GR.up(gt_rgb, static_cast<size_t>(3 * n_rays), s);
+    GA.up(gt_alpha, static_cast<size_t>(n_rays), s);
+    DevBuf<float> orgb, oalpha;
+    DevBuf<double> T, L4;
+    orgb.alloc(static_cast<size_t>(3 * n_rays));
+    oalpha.alloc(static_cast<size_t>(n_rays));
+    T.alloc(static_cast<size_t>(3 * n_rays));
+    L4.alloc(4);
+    lt.gt_rgb = GR.d.ptr;
+    lt.gt_alpha = GA.d.ptr;
+    lt.ray_terms = T.ptr;
+    unsigned long long hcnt[8];
+    run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, PX.d.ptr, PY.d.ptr, nullptr, nullptr, &lt,
+              orgb.ptr, oalpha.ptr, s, hcnt);
+    loss_reduce(T.ptr, n_rays, lt, L4.ptr, s);
+    if (loss4) d2h(loss4, L4.ptr, 4, s);
+    if (rgb) d2h(rgb, orgb.ptr, static_cast<size_t>(3 * n_rays), s);
+    if (alpha) d2h(alpha, oalpha.ptr, static_cast<size_t>(n_rays), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    if (c) {
+      c->posed_queries = hcnt[0];
+      c->canonical_queries = hcnt[1];
+    }
+  });
+}
+
+int arfx_train_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                           const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                           const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
+                           const arfx_loss_config* cfg, double* d_loss4, float* d_rgb, float* d_alpha,
+                           void* stream) {
+  return guard([&] {
+    const HostCamera hc = camera_of(cam);
+    validate_train(mh, ph, opt, hc);
+    require(n_rays == 0 || (d_px && d_py && d_gt_rgb && d_gt_alpha && d_loss4), "train_step: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n_rays <= 0) return;
+    const cudaStream_t s = stream_of(m, stream);
+    Workspace& w = m.ws;
+    w.train_terms.ensure(static_cast<size_t>(3 * n_rays));
+    w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
+    w.train_alpha.ensure(static_cast<size_t>(n_rays));
+    LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
+    unsigned long long hcnt[8];
+    run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, d_px, d_py, nullptr, nullptr, &lt,
+              d_rgb ? d_rgb : w.train_rgb.ptr, d_alpha ? d_alpha : w.train_alpha.ptr, s, hcnt);
+    loss_reduce(w.train_terms.ptr, n_rays, lt, d_loss4, s);
+  });
+}
+
+int arfx_adam_step(arfx_model mh, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
+                   void* stream) {
+  return guard([&] {
+    require(mh != nullptr, "adam: null model");
+    const AdamCfg c = adam_of(cfg);
+    require(step >= 1, "adam: step must be >= 1");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (end < 0) end = static_cast<int64_t>(m.n_flat);
+    require(begin >= 0 && begin <= end && end <= static_cast<int64_t>(m.n_flat) && begin % 4 == 0 && end % 4 == 0,
+            "adam: range must be a multiple-of-4 slice of the flat vector");
+    const cudaStream_t s = stream_of(m, stream);
+    ensure_grad_store(m, s);
+    adam_step(m, c, step, begin, end, s);
+  });
+}
+
+int arfx_model_flat(arfx_model mh, float** params, float** grads, float** am, float** av, int64_t* n_flat,
+                    int64_t* mlp_offset) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    ensure_grad_store(m, m.stream);
+    if ((am || av) && !m.adam_m.ptr) {
+      m.adam_m.alloc(m.n_flat);
+      m.adam_v.alloc(m.n_flat);
+      ARFX_CUDA(cudaMemsetAsync(m.adam_m.ptr, 0, m.n_flat * sizeof(float), m.stream));
+      ARFX_CUDA(cudaMemsetAsync(m.adam_v.ptr, 0, m.n_flat * sizeof(float), m.stream));
+      ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    }
+    if (params) *params = m.flat_params.ptr;
+    if (grads) *grads = m.flat_grads.ptr;
+    if (am) *am = m.adam_m.ptr;
+    if (av) *av = m.adam_v.ptr;
+    if (n_flat) *n_flat = static_cast<int64_t>(m.n_flat);
+    if (mlp_offset) *mlp_offset = static_cast<int64_t>(m.mlp_off);
+  });
+}
+
+int arfx_model_get_adam(arfx_model mh, float* am, float* av) {
+  return guard([&] {
+    require(mh != nullptr, "null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (!m.adam_m.ptr) {
+      if (am) std::fill(am, am + m.n_flat, 0.0f);
+      if (av) std::fill(av, av + m.n_flat, 0.0f);
+      return;
+    }
+    if (am) d2h(am, m.adam_m.ptr, m.n_flat, m.stream);
+    if (av) d2h(av, m.adam_v.ptr, m.n_flat, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_model_set_adam(arfx_model mh, const float* am, const float* av) {
+  return guard([&] {
+    require(mh && am && av, "set_adam: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (!m.adam_m.ptr) {
+      m.adam_m.alloc(m.n_flat);
+      m.adam_v.alloc(m.n_flat);
+    }
+    h2d(m.adam_m.ptr, am, m.n_flat, m.stream);
+    h2d(m.adam_v.ptr, av, m.n_flat, m.stream);
+    ARFX_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+int arfx_figure_query(const arfx_figure* fig, const double* bones12, const double* pts, int64_t n,
+                      double* density, double* color) {
+  return guard([&] {
+    const FigureView F = figure_view_of(fig, bones12);
+    require(n == 0 || (pts && density && color), "figure_query: null argument");
+    require_device();
+    if (n <= 0) return;
+    const cudaStream_t s = cudaStreamPerThread;
+    Staged<double> P;
+    P.up(pts, static_cast<size_t>(3 * n), s);
+    DevBuf<double> D, Cc;
+    D.alloc(static_cast<size_t>(n));
+    Cc.alloc(static_cast<size_t>(3 * n));
+    figure_query_batch(F, P.d.ptr, n, D.ptr, Cc.ptr, s);
+    d2h(density, D.ptr, static_cast<size_t>(n), s);
+    d2h(color, Cc.ptr, static_cast<size_t>(3 * n), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_figure_render(const arfx_figure* fig, const double* bones12, const double* global12,
+                       const double box_lo[3], const double box_hi[3], const arfx_camera* cam,
+                       const arfx_render_options* opt, float* rgb, float* alpha, uint8_t* mask, void* stream) {
+  return guard([&] {
+    const FigureFrame f = figure_frame(fig, bones12, global12, box_lo, box_hi, cam, opt);
+    require_device();
+    const cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+    const long long n = static_cast<long long>(f.cam.width) * f.cam.height;
+    DevBuf<float> R, A;
+    DevBuf<uint8_t> M;
+    R.alloc(static_cast<size_t>(3 * n));
+    A.alloc(static_cast<size_t>(n));
+    M.alloc(static_cast<size_t>(n));
+    figure_render(f.F, f.cam, f.w2n, box_lo, box_hi, opt->samples_per_ray, opt->stratified != 0,
+                  opt->epsilon_terminate, opt->seed, opt->frame_id, n, nullptr, nullptr, R.ptr, A.ptr, M.ptr, s);
+    if (rgb) d2h(rgb, R.ptr, static_cast<size_t>(3 * n), s);
+    if (alpha) d2h(alpha, A.ptr, static_cast<size_t>(n), s);
+    if (mask) d2h(mask, M.ptr, static_cast<size_t>(n), s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int arfx_figure_render_rays_device(const arfx_figure* fig, const double* bones12, const double* global12,
+                                   const double box_lo[3], const double box_hi[3], const arfx_camera* cam,
+                                   const arfx_render_options* opt, int64_t n, const int32_t* d_px,
+                                   const int32_t* d_py, float* d_rgb, float* d_alpha, uint8_t* d_mask,
+                                   void* stream) {
+  return guard([&] {
+    const FigureFrame f = figure_frame(fig, bones12, global12, box_lo, box_hi, cam, opt);
+    require(n == 0 || (d_px && d_py && d_rgb && d_alpha), "figure_render_rays: null argument");
+    require_device();
+    const cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+    figure_render(f.F, f.cam, f.w2n, box_lo, box_hi, opt->samples_per_ray, opt->stratified != 0,
+                  opt->epsilon_terminate, opt->seed, opt->frame_id, n, d_px, d_py, d_rgb, d_alpha, d_mask, s);
   });
 }
 

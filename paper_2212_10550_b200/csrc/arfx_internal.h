@@ -84,4 +84,15 @@ struct CameraView {  // R/camera.hpp:9-13
   double ext[12];
 };
 
+// arf::CapsuleFigure (R/scene.hpp:13-27) posed by PosedFigure (R/scene.hpp:56-75): per bone
+// the (posed or canonical) segment, radius, color, amplitude; the analytic ground truth.
+struct FigureView {
+  int nb;
+  int pad_;
+  double a[kMaxBones][3], b[kMaxBones][3];
+  double radius[kMaxBones], amp[kMaxBones];
+  double col[kMaxBones][3];
+  double soft;
+};
+
 }  // namespace arfx

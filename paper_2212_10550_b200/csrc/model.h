@@ -19,14 +19,22 @@ template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t n = 0;
+  bool owned = true;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && owned) cudaFree(ptr);
     ptr = nullptr;
     n = 0;
+    owned = true;
+  }
+  void view(T* p, size_t count) {  // non-owning window into another buffer
+    release();
+    ptr = p;
+    n = count;
+    owned = false;
   }
   void ensure(size_t count) {  // grow-only, contents not preserved
     if (count <= n) return;
@@ -55,6 +63,8 @@ struct Workspace {
   DevBuf<int32_t> powner;             // owning sample (-1: value precomputed by deformer)
   DevBuf<float4> pres;                // (density, r, g, b) per pool entry
   DevBuf<int32_t> ray_first, ray_count, row_list;
+  DevBuf<double> train_terms;          // fused-loss per-ray terms
+  DevBuf<float> train_rgb, train_alpha;  // training outputs when the caller passes none
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
@@ -111,6 +121,11 @@ struct ModelImpl {
   HostBox skin_box{}, canon{}, norm{};
   InverseOpts inv{20, 1e-5, 1e-3};
   size_t n_grid = 0, n_mlp = 0, n_skin = 0;
+  // Flat parameter / gradient / Adam-moment vectors [grid | pad | mlp | pad] (n_flat floats):
+  // one buffer each so data-parallel training reduce-scatters / all-gathers them in one call;
+  // grid_* and mlp_* are non-owning views into them.
+  DevBuf<float> flat_params, flat_grads, adam_m, adam_v;
+  size_t n_flat = 0, mlp_off = 0;
   DevBuf<float> grid_params, mlp_params, grid_grad, mlp_grad;
   DevBuf<double> skin;
   DevBuf<uint32_t> cell_mask, cell_off;
@@ -174,8 +189,26 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
                    cudaStream_t s);
 
 // train.cu
+// fused-loss targets for train_composite (losses.cuh); device arrays
+struct LossTargets {
+  const float* gt_rgb;    // [n][3]
+  const float* gt_alpha;  // [n]
+  double w_rgb, w_alpha, w_hard, w_density, huber_delta;
+  double* ray_terms;      // [n][3] out
+};
+void loss_reduce(const double* d_terms, long long n, const LossTargets& lt, double* d_out4, cudaStream_t s);
+void ray_losses(long long n, const float* d_rgb, const float* d_alpha, const LossTargets& lt, float* d_grad_rgb,
+                float* d_grad_alpha, cudaStream_t s);
+// optim.cu: Adam over the flat parameter vector
+struct AdamCfg {
+  double lr_grid, lr_mlp, beta1, beta2, eps;
+  long long total_steps;
+  double final_lr_factor;
+};
+double cosine_lr(double lr0, const AdamCfg& c, long long step);
+void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s);
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
-                     float* d_rgb, float* d_alpha, cudaStream_t s);
+                     float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt = nullptr);
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
                          const float* gs, const float* gc, cudaStream_t s);
 
@@ -194,5 +227,13 @@ void composite_backward_explicit(int n_rays, const int64_t* d_off, const double*
                                  const uint8_t* d_skip, const float* d_dens, const float* d_col,
                                  double eps, const double* d_dC3, const double* d_dA, double* d_trans,
                                  double* d_sigma, double* d_c3, cudaStream_t s);
+
+// scene.cu: analytic ground truth (R/scene.hpp)
+void figure_query_batch(const FigureView& F, const double* d_pts, long long n, double* d_dens, double* d_col,
+                        cudaStream_t s);
+void figure_render(const FigureView& F, const HostCamera& cam, const double* w2n12, const double* nlo,
+                   const double* nhi, int N, bool stratified, double eps, uint64_t seed, uint64_t frame, long long n,
+                   const int32_t* d_px, const int32_t* d_py, float* d_rgb, float* d_alpha, uint8_t* d_mask,
+                   cudaStream_t s);
 
 }  // namespace arfx

@@ -1,0 +1,95 @@
+// optim.cu -- Adam over the flat [grid | mlp] parameter vector, with the zero-grad fused
+// (adaptive moments, lr 1e-2 grid / 1e-3 MLP, cosine decay; beta1 0.9,
+// beta2 0.99, eps 1e-15 follow the cited encoding system's practice -- the paper names no
+// optimizer). One pass, HBM-bound: reads p, g, m, v and writes p, m, v, g = 0 (32 B per
+// parameter), float4-vectorised. f32 arithmetic, no FMA (--fmad=false), fixed op order:
+//   m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g g
+//   p = p - lr_t * (m c1) / (sqrt(v c2) + eps),   c1 = 1/(1 - b1^t), c2 = 1/(1 - b2^t)
+// so oracle/arf_oracle.c arfo_adam reproduces it bit for bit. [begin, end) selects a shard
+// of the flat vector (data-parallel training: reduce-scatter -> sharded Adam -> all-gather).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "model.h"
+
+namespace arfx {
+namespace {
+
+struct AdamScalars {
+  float b1, omb1, b2, omb2, c1, c2, eps, lr_grid, lr_mlp;
+  long long mlp_off;
+};
+
+__device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, float lr, const AdamScalars& k) {
+  const float gg = g;
+  m = __fadd_rn(__fmul_rn(k.b1, m), __fmul_rn(k.omb1, gg));
+  v = __fadd_rn(__fmul_rn(k.b2, v), __fmul_rn(k.omb2, __fmul_rn(gg, gg)));
+  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, k.c2)), k.eps);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, __fmul_rn(m, k.c1)), den));
+  g = 0.0f;
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ g,
+                                                   float* __restrict__ m, float* __restrict__ v, long long b4,
+                                                   long long e4, AdamScalars k) {
+  for (long long i = b4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < e4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 P = reinterpret_cast<float4*>(p)[i], G = reinterpret_cast<float4*>(g)[i];
+    float4 M = reinterpret_cast<float4*>(m)[i], V = reinterpret_cast<float4*>(v)[i];
+    const float lr = (4 * i >= k.mlp_off) ? k.lr_mlp : k.lr_grid;  // mlp_off % 64 == 0
+    adam1(P.x, G.x, M.x, V.x, lr, k);
+    adam1(P.y, G.y, M.y, V.y, lr, k);
+    adam1(P.z, G.z, M.z, V.z, lr, k);
+    adam1(P.w, G.w, M.w, V.w, lr, k);
+    reinterpret_cast<float4*>(p)[i] = P;
+    reinterpret_cast<float4*>(g)[i] = G;
+    reinterpret_cast<float4*>(m)[i] = M;
+    reinterpret_cast<float4*>(v)[i] = V;
+  }
+}
+
+}  // namespace
+
+// lr_t = lr0 (f + (1 - f) (1 + cos(pi min(t, T) / T)) / 2), t = step (1-based); T <= 0: constant
+double cosine_lr(double lr0, const AdamCfg& c, long long step) {
+  if (c.total_steps <= 0) return lr0;
+  const double t = static_cast<double>(std::min(step, c.total_steps)) / static_cast<double>(c.total_steps);
+  const double f = c.final_lr_factor;
+  return lr0 * (f + (1.0 - f) * 0.5 * (1.0 + std::cos(3.14159265358979323846 * t)));
+}
+
+void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s) {
+  const size_t n = m.n_flat;
+  if (!m.adam_m.ptr) {
+    m.adam_m.alloc(n);
+    m.adam_v.alloc(n);
+    ARFX_CUDA(cudaMemsetAsync(m.adam_m.ptr, 0, n * sizeof(float), s));
+    ARFX_CUDA(cudaMemsetAsync(m.adam_v.ptr, 0, n * sizeof(float), s));
+  }
+  AdamScalars k;
+  k.b1 = static_cast<float>(c.beta1);
+  k.omb1 = static_cast<float>(1.0 - c.beta1);
+  k.b2 = static_cast<float>(c.beta2);
+  k.omb2 = static_cast<float>(1.0 - c.beta2);
+  k.c1 = static_cast<float>(1.0 / (1.0 - std::pow(c.beta1, static_cast<double>(step))));
+  k.c2 = static_cast<float>(1.0 / (1.0 - std::pow(c.beta2, static_cast<double>(step))));
+  k.eps = static_cast<float>(c.eps);
+  k.lr_grid = static_cast<float>(cosine_lr(c.lr_grid, c, step));
+  k.lr_mlp = static_cast<float>(cosine_lr(c.lr_mlp, c, step));
+  k.mlp_off = static_cast<long long>(m.mlp_off);
+  const long long b4 = begin / 4, e4 = end / 4;
+  if (e4 <= b4) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long blocks = std::min<long long>((e4 - b4 + 255) / 256, static_cast<long long>(sms) * 8);
+  m.prof.begin("adam", s);
+  adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr,
+                                                              m.adam_v.ptr, b4, e4, k);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
+}
+
+}  // namespace arfx

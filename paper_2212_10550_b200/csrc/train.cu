@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "field.cuh"
+#include "losses.cuh"
 #include "model.h"
 
 namespace arfx {
@@ -58,6 +59,12 @@ struct TrainCompositeArgs {
   double* strans;  // scratch: transmittance before each posed sample
   const float* dC;
   const float* dA;
+  // fused losses: when gt_rgb != null, dC / dA come from ray_loss instead
+  const float* gt_rgb;
+  const float* gt_alpha;
+  LossCfg loss;
+  double inv_n;
+  double* ray_terms;  // [n_rays][3] unweighted per-ray loss terms
   float *rgb, *alpha;
   float* pgs;      // per pool entry: dsigma (f32, as passed to query_backward)
   float* pgc;      // per pool entry: dcolor[3]
@@ -90,12 +97,24 @@ __global__ void train_composite_kernel(TrainCompositeArgs A) {
       if (A.eps > 0 && T <= A.eps) m = A.sidx[s] + 1;
     }
     if (cnt == 0) m = 0;
-    A.rgb[3 * r + 0] = static_cast<float>(cr);
-    A.rgb[3 * r + 1] = static_cast<float>(cg);
-    A.rgb[3 * r + 2] = static_cast<float>(cb);
-    A.alpha[r] = static_cast<float>(acc);
+    const float fr = static_cast<float>(cr), fg = static_cast<float>(cg), fb = static_cast<float>(cb);
+    const float fa = static_cast<float>(acc);
+    A.rgb[3 * r + 0] = fr;
+    A.rgb[3 * r + 1] = fg;
+    A.rgb[3 * r + 2] = fb;
+    A.alpha[r] = fa;
+    // ---- upstream: given, or the fused loss gradient of this ray ----
+    double dcx, dcy, dcz, da;
+    if (A.gt_rgb) {
+      const RayLoss L = ray_loss(fr, fg, fb, fa, A.gt_rgb + 3 * r, A.gt_alpha[r], A.loss, A.inv_n);
+      A.ray_terms[3 * r + 0] = L.rgb;
+      A.ray_terms[3 * r + 1] = L.alpha;
+      A.ray_terms[3 * r + 2] = L.hard;
+      dcx = L.dC[0], dcy = L.dC[1], dcz = L.dC[2], da = L.dA;
+    } else {
+      dcx = A.dC[3 * r + 0], dcy = A.dC[3 * r + 1], dcz = A.dC[3 * r + 2], da = A.dA[r];
+    }
     // ---- backward (composite_backward R/render.hpp:125-157), reverse over i < m ----
-    const double dcx = A.dC[3 * r + 0], dcy = A.dC[3 * r + 1], dcz = A.dC[3 * r + 2], da = A.dA[r];
     double chx = 0.0, chy = 0.0, chz = 0.0, ahat = 0.0;
     for (int j = cnt - 1; j >= 0; --j) {
       const long long s = first + j;
@@ -306,15 +325,89 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
 }
 
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
-                     float* d_rgb, float* d_alpha, cudaStream_t s) {
+                     float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt) {
   Workspace& w = m.ws;
   TrainCompositeArgs A{n_rays, N, eps, w.ray_first.ptr, w.ray_count.ptr, w.sidx.ptr, w.sdelta.ptr, w.snroot.ptr,
-                       w.sbase.ptr, w.pres.ptr, w.strans.ptr, d_dC, d_dA, d_rgb, d_alpha, w.pgs.ptr, w.pgc.ptr,
-                       w.pflag.ptr};
+                       w.sbase.ptr, w.pres.ptr, w.strans.ptr, d_dC, d_dA, nullptr, nullptr, LossCfg{}, 0.0, nullptr,
+                       d_rgb, d_alpha, w.pgs.ptr, w.pgc.ptr, w.pflag.ptr};
+  if (lt) {
+    A.gt_rgb = lt->gt_rgb;
+    A.gt_alpha = lt->gt_alpha;
+    A.loss = LossCfg{lt->w_rgb, lt->w_alpha, lt->w_hard, lt->w_density, lt->huber_delta};
+    A.inv_n = 1.0 / static_cast<double>(n_rays);
+    A.ray_terms = lt->ray_terms;
+  }
   m.prof.begin("train_composite", s);
   train_composite_kernel<<<static_cast<unsigned>(std::max<long long>(1, (n_rays + 127) / 128)), 128, 0, s>>>(A);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
+}
+
+namespace {
+// loss4 = (L_rgb, L_alpha, L_hard, w_rgb L_rgb + w_alpha L_alpha + w_hard L_hard): batch means of
+// the per-ray terms; one block, fixed strided order + fixed tree -> deterministic
+__global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restrict__ t, long long n, LossCfg L,
+                                                          double* __restrict__ out4) {
+  __shared__ double sh[3][256];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 256) {
+    a += t[3 * i + 0];
+    b += t[3 * i + 1];
+    c += t[3 * i + 2];
+  }
+  sh[0][threadIdx.x] = a;
+  sh[1][threadIdx.x] = b;
+  sh[2][threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int k = 0; k < 3; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double inv = n > 0 ? 1.0 / static_cast<double>(n) : 0.0;
+    const double lr = sh[0][0] * inv, la = sh[1][0] * inv, lh = sh[2][0] * inv;
+    out4[0] = lr;
+    out4[1] = la;
+    out4[2] = lh;
+    out4[3] = L.w_rgb * lr + L.w_alpha * la + L.w_hard * lh;
+  }
+}
+
+__global__ void ray_loss_kernel(long long n, const float* __restrict__ rgb, const float* __restrict__ alpha,
+                                const float* __restrict__ gt_rgb, const float* __restrict__ gt_alpha, LossCfg L,
+                                double* __restrict__ terms, float* __restrict__ d_rgb, float* __restrict__ d_alpha) {
+  const double inv_n = 1.0 / static_cast<double>(n);
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const RayLoss o = ray_loss(rgb[3 * r], rgb[3 * r + 1], rgb[3 * r + 2], alpha[r], gt_rgb + 3 * r, gt_alpha[r], L,
+                               inv_n);
+    terms[3 * r + 0] = o.rgb;
+    terms[3 * r + 1] = o.alpha;
+    terms[3 * r + 2] = o.hard;
+    if (d_rgb) {
+      d_rgb[3 * r + 0] = o.dC[0];
+      d_rgb[3 * r + 1] = o.dC[1];
+      d_rgb[3 * r + 2] = o.dC[2];
+    }
+    if (d_alpha) d_alpha[r] = o.dA;
+  }
+}
+}  // namespace
+
+void loss_reduce(const double* d_terms, long long n, const LossTargets& lt, double* d_out4, cudaStream_t s) {
+  loss_reduce_kernel<<<1, 256, 0, s>>>(d_terms, n, LossCfg{lt.w_rgb, lt.w_alpha, lt.w_hard, lt.w_density,
+                                                           lt.huber_delta}, d_out4);
+  ARFX_CUDA(cudaGetLastError());
+}
+
+void ray_losses(long long n, const float* d_rgb, const float* d_alpha, const LossTargets& lt, float* d_grad_rgb,
+                float* d_grad_alpha, cudaStream_t s) {
+  if (n <= 0) return;
+  ray_loss_kernel<<<static_cast<unsigned>(std::min<long long>((n + 127) / 128, 4096)), 128, 0, s>>>(
+      n, d_rgb, d_alpha, lt.gt_rgb, lt.gt_alpha,
+      LossCfg{lt.w_rgb, lt.w_alpha, lt.w_hard, lt.w_density, lt.huber_delta}, lt.ray_terms, d_grad_rgb, d_grad_alpha);
+  ARFX_CUDA(cudaGetLastError());
 }
 
 }  // namespace arfx

@@ -161,6 +161,24 @@ def default_figure_skeleton(n_bones: int = 10) -> Skeleton:
     return Skeleton([Bone(p, h, t, r) for (p, h, t, r) in spec[:n_bones]])
 
 
+def default_figure():
+    """The reference's default_figure() (R/scene.hpp:129-154): 10 colored capsules,
+    amplitude 80, softness 0.012."""
+    from .arf import CapsuleFigure
+    colors = [(0.90, 0.10, 0.10), (0.95, 0.85, 0.10), (0.10, 0.80, 0.15), (0.10, 0.25, 0.90), (0.10, 0.85, 0.80),
+              (0.85, 0.15, 0.85), (0.95, 0.55, 0.10), (0.55, 0.10, 0.85), (0.10, 0.55, 0.45), (0.60, 0.80, 0.10)]
+    return CapsuleFigure(default_figure_skeleton(), np.array(colors), np.full(10, 80.0), 0.012)
+
+
+def figure_for(skel: Skeleton, seed: int = 77, amplitude: float = 80.0, softness: float = 0.012):
+    """A CapsuleFigure over any skeleton (e.g. smpl24): per-bone colors U(0.1, 0.95)^3 from
+    keyed_rng(seed, 3), drawn r, g, b per bone in bone order."""
+    from .arf import CapsuleFigure
+    rng = keyed_rng(seed, 3)
+    cols = np.array([[rng.uniform(0.1, 0.95) for _ in range(3)] for _ in range(skel.bone_count())])
+    return CapsuleFigure(skel, cols, np.full(skel.bone_count(), amplitude), softness)
+
+
 # ---- poses / cameras ----------------------------------------------------------
 
 def random_pose(skel: Skeleton, seed: int, stream: int = 7, max_angle: float = 0.5, yaw: float = 0.3) -> SkeletonPose:

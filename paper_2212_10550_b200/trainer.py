@@ -1,0 +1,194 @@
+"""Training loop host side (SPEC.md:440-530 train_step).
+
+The reference code base stops at the differentiable pieces (composite_backward,
+query_backward); the SPEC's trainer is built here over the libarfx training ABI:
+
+  per step t (all on the device, one host sync for the workspace-overflow check):
+    rays     B / world rays per rank: frame f and pixels from keyed_rng(seed, 0x7a11, t, rank)
+             (draw order: frame, then px, py per ray), ground truth gathered from the
+             device-resident dataset frames (analytic figure, arfx_figure_render)
+    step     arfx_train_step_device: forward, losses fused into the composite kernel,
+             backward -> the model's flat gradient vector
+    sync     world > 1: reduce-scatter(AVG) of the flat gradients over NCCL, Adam on this
+             rank's shard, all-gather of the parameter shards (FlatDataParallel)
+    optim    arfx_adam_step (zero-grad fused), cosine lr
+    occ      every k steps: update_training_grid over the dataset poses (R/occupancy.hpp:155-171),
+             identical on every rank (same keys, same parameters)
+
+torch is plumbing only: device tensors for the dataset / ray lists and torch.distributed
+for the collectives. Every compute step is a libarfx kernel.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from . import arf
+from . import fixtures as fx
+
+
+def device_view(ptr: int, n: int, dtype="float32"):
+    """Zero-copy torch view of n elements of libarfx device memory (__cuda_array_interface__)."""
+    import torch
+
+    class _CAI:
+        pass
+
+    o = _CAI()
+    o.__cuda_array_interface__ = {"shape": (int(n),), "typestr": np.dtype(dtype).str, "data": (int(ptr), False),
+                                  "version": 3, "strides": None}
+    return torch.as_tensor(o, device="cuda")
+
+
+@dataclass
+class TrainConfig:  # TrainConfig SPEC.md:450-453
+    iterations: int = 200
+    rays_per_batch: int = 4096           # global batch (split over ranks)
+    samples_per_ray: int = 128
+    occupancy_interval: int = 16         # k
+    seed: int = 1234
+    loss: arf.LossConfig = field(default_factory=arf.LossConfig)
+    adam: arf.AdamConfig = field(default_factory=arf.AdamConfig)
+    occupancy: arf.OccupancyConfig = field(default_factory=arf.OccupancyConfig)
+    gt_oversample: int = 4               # SPEC scenegen: ground truth at 4x the training N
+
+
+class FlatDataParallel:
+    """Gradient / parameter synchronisation of the flat [grid | mlp] vectors over a process
+    group: reduce-scatter(AVG) grads -> `optimizer(begin, end)` on this rank's shard ->
+    all-gather params, then the other shards' gradients are cleared (the optimizer zeroes
+    its own). With world == 1 it is just optimizer(0, n). Backends without reduce-scatter
+    (gloo, used by the CPU tests) fall back to all-reduce + slicing, same result."""
+
+    def __init__(self, params, grads, n_flat: int, rank: int = 0, world: int = 1, group=None):
+        self.params, self.grads, self.n = params, grads, int(n_flat)
+        self.rank, self.world, self.group = rank, world, group
+        if self.n % (4 * world):
+            raise ValueError("flat vector length must split into multiple-of-4 shards")
+        self.chunk = self.n // world
+
+    def shard(self, rank: int | None = None):
+        r = self.rank if rank is None else rank
+        return r * self.chunk, (r + 1) * self.chunk
+
+    def step(self, optimizer) -> None:
+        b, e = self.shard()
+        if self.world > 1:
+            import torch.distributed as dist
+            backend = dist.get_backend(self.group)
+            if backend == "nccl":
+                dist.reduce_scatter_tensor(self.grads[b:e], self.grads, op=dist.ReduceOp.AVG, group=self.group)
+            else:
+                dist.all_reduce(self.grads, op=dist.ReduceOp.SUM, group=self.group)
+                self.grads.div_(self.world)
+        optimizer(b, e)
+        if self.world > 1:
+            import torch.distributed as dist
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(self.params, self.params[b:e], group=self.group)
+            else:
+                parts = [self.params[r * self.chunk:(r + 1) * self.chunk].clone() for r in range(self.world)]
+                dist.all_gather(parts, self.params[b:e].clone(), group=self.group)
+                for r, p in enumerate(parts):
+                    self.params[r * self.chunk:(r + 1) * self.chunk].copy_(p)
+            if b > 0:
+                self.grads[:b].zero_()
+            if e < self.n:
+                self.grads[e:].zero_()
+
+
+def ray_batch(seed: int, step: int, rank: int, n: int, n_frames: int, width: int, height: int):
+    """This rank's rays of step `step`: (frame, px[n], py[n]); keyed_rng(seed, 0x7a11, step, rank),
+    draws: frame = next_below(n_frames), then per ray px = next_below(W), py = next_below(H)."""
+    rng = fx.keyed_rng(seed, 0x7A11, step, rank)
+    f = rng.next_below(n_frames)
+    u = fx.pcg_stream_u32(rng, 2 * n).reshape(n, 2)
+    px = ((u[:, 0] * np.uint64(width)) >> np.uint64(32)).astype(np.int32)
+    py = ((u[:, 1] * np.uint64(height)) >> np.uint64(32)).astype(np.int32)
+    return f, px, py
+
+
+class Trainer:
+    """SPEC train_step loop on one GPU per rank (world from torch.distributed when initialised)."""
+
+    def __init__(self, model: arf.Model, figure: arf.CapsuleFigure, poses, camera: arf.Camera, cfg: TrainConfig,
+                 rank: int = 0, world: int = 1, group=None):
+        import torch
+        self.torch = torch
+        self.model, self.figure, self.poses, self.camera, self.cfg = model, figure, list(poses), camera, cfg
+        self.rank, self.world = rank, world
+        if cfg.rays_per_batch % world:
+            raise ValueError("rays_per_batch must divide by the number of ranks")
+        self.n_local = cfg.rays_per_batch // world
+        self.views = [arf.PosedModelView(model, p) for p in self.poses]
+        # ---- dataset: ground-truth frames of the analytic figure (device resident)
+        W, H = camera.width, camera.height
+        gt_opt = arf.RenderOptions(samples_per_ray=cfg.gt_oversample * cfg.samples_per_ray)
+        rgbs, masks = [], []
+        for p in self.poses:
+            img, mask = arf.figure_render(figure, p, model.normalized_box, camera, gt_opt)
+            rgbs.append(img.rgb)
+            masks.append(mask.astype(np.float32))
+        self.gt_rgb = torch.from_numpy(np.stack(rgbs)).cuda().reshape(len(self.poses), H * W, 3)
+        self.gt_alpha = torch.from_numpy(np.stack(masks)).cuda().reshape(len(self.poses), H * W)
+        # ---- optimizer state + data-parallel sync over the flat vectors
+        fl = model.flat()
+        self.n_flat = fl["n_flat"]
+        self.params = device_view(fl["params"], self.n_flat)
+        self.grads = device_view(fl["grads"], self.n_flat)
+        self.dp = FlatDataParallel(self.params, self.grads, self.n_flat, rank, world, group)
+        self.stream = torch.cuda.current_stream()
+        self.loss4 = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.px = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
+        self.py = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
+        self.b_rgb = torch.zeros((self.n_local, 3), dtype=torch.float32, device="cuda")
+        self.b_alpha = torch.zeros(self.n_local, dtype=torch.float32, device="cuda")
+        # ---- occupancy: built from the untrained model at step 0
+        self.grid = arf.OccupancyGrid(model.normalized_box, cfg.occupancy)
+        arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
+        self.step_id = 0
+        self.history = []
+
+    def _opt(self, frame: int) -> arf.RenderOptions:
+        return arf.RenderOptions(samples_per_ray=self.cfg.samples_per_ray, stratified=True, seed=self.cfg.seed,
+                                 frame_id=self.step_id * 1024 + frame)
+
+    def step(self) -> np.ndarray:
+        torch = self.torch
+        cfg, W = self.cfg, self.camera.width
+        f, px, py = ray_batch(cfg.seed, self.step_id, self.rank, self.n_local, len(self.poses), W, self.camera.height)
+        self.px.copy_(torch.from_numpy(px), non_blocking=False)
+        self.py.copy_(torch.from_numpy(py), non_blocking=False)
+        idx = (self.py.long() * W + self.px.long())
+        self.b_rgb.copy_(self.gt_rgb[f].index_select(0, idx))
+        self.b_alpha.copy_(self.gt_alpha[f].index_select(0, idx))
+        sp = C.c_void_p(self.stream.cuda_stream)
+        L.call("arfx_train_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()), self.grid._h,
+               C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
+               C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
+               C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
+               None, None, sp)
+        t = self.step_id + 1
+        self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
+        if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
+            arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t)
+        self.step_id = t
+        loss = self.loss4.cpu().numpy().copy()
+        if not np.all(np.isfinite(loss)):
+            raise L.NumericError(3, f"train_step: non-finite loss at step {t}: {loss.tolist()}")
+        self.history.append(loss)
+        return loss
+
+    def train(self, iterations: int | None = None):
+        for _ in range(iterations or self.cfg.iterations):
+            self.step()
+        return np.array(self.history)
+
+
+def psnr(img, ref) -> float:
+    """PSNR = 10 log10(1 / MSE) for [0,1] images, capped at 99 dB."""
+    mse = float(np.mean((np.asarray(img, np.float64) - np.asarray(ref, np.float64)) ** 2))
+    return 99.0 if mse == 0 else min(99.0, 10.0 * np.log10(1.0 / mse))

@@ -1,0 +1,137 @@
+"""GPU: analytic ground truth (R/scene.hpp) against the reference, and the SPEC training
+pieces (losses, fused step, Adam, trainer) against the oracle restatement."""
+import numpy as np
+import pytest
+
+from paper_2212_10550_b200 import arf, fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+
+def test_figure_query_bit_exact(gpu, ref):
+    fig = fx.default_figure()
+    rng = np.random.default_rng(0)
+    pts = rng.uniform([-0.7, 0.0, -0.2], [0.7, 1.8, 0.2], size=(20000, 3))
+    pose = fx.random_pose(fig.skeleton, 3, max_angle=0.4)
+    for p in (None, pose):
+        d, c = arf.figure_query(fig, pts, p)
+        rd, rc = ref.figure_query(fig, pts, None if p is None else p.bone_transforms)
+        assert np.array_equal(d.view(np.uint64), rd.view(np.uint64))
+        assert np.array_equal(c.view(np.uint64), rc.view(np.uint64))
+
+
+@pytest.mark.parametrize("stratified", [False, True])
+def test_figure_render_vs_reference(gpu, ref, stratified):
+    fig = fx.figure_for(fx.smpl24())
+    sk = fig.skeleton
+    pose = fx.random_pose(sk, 42)
+    cam = fx.default_camera(sk, 72, 64)
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (16, 16, 16), 1)
+    box = m.normalized_box
+    opt = arf.RenderOptions(samples_per_ray=256, stratified=stratified, seed=5, frame_id=1)
+    img, mask = arf.figure_render(fig, pose, box, cam, opt)
+    rrgb, ralpha, rmask = ref.figure_render(fig, pose.bone_transforms, pose.global_transform, box.lo, box.hi, cam, opt)
+    assert np.array_equal(mask, rmask)
+    assert mask.sum() > 100
+    # sample positions and per-sample fields are bit-exact; composite's expm1 (CUDA vs glibc, <= 1 ulp)
+    np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-6, atol=1e-7)
+
+
+def test_losses_vs_oracle(gpu, oracle):
+    rng = np.random.default_rng(2)
+    n = 5000
+    rgb = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    alpha = rng.uniform(0, 1, n).astype(np.float32)
+    alpha[:4] = [0.0, 1.0, 0.5, 0.25]
+    gt = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    gt[:50] = rgb[:50]  # r = 0 and small-residual rays
+    gta = (rng.uniform(0, 1, n) > 0.5).astype(np.float32)
+    gta[:4] = [0.0, 1.0, 0.5, 0.25]
+    cfg = arf.LossConfig()
+    l4, dr, da = arf.losses(rgb, alpha, gt, gta, cfg)
+    ol4, odr, oda = oracle.losses(rgb, alpha, gt, gta, cfg)
+    # double arithmetic with CUDA exp/log vs glibc (<= 1 ulp in double) -> f32 gradients equal or 1 ulp apart
+    np.testing.assert_allclose(l4, ol4, rtol=1e-12)
+    assert np.all(np.abs(dr.view(np.int32) - odr.view(np.int32)) <= 1)
+    assert np.all(np.abs(da.view(np.int32) - oda.view(np.int32)) <= 1)
+
+
+def test_adam_bit_exact(gpu, oracle):
+    import torch
+    from paper_2212_10550_b200.trainer import device_view
+    m = arf.build_model(fx.default_figure_skeleton(), arf.HashGridConfig(levels=4, table_size_log2=12),
+                        arf.MlpConfig(8, 16, 2, 4), (8, 8, 8), 3)
+    fl = m.flat()
+    n = fl["n_flat"]
+    rng = np.random.default_rng(4)
+    p, g = device_view(fl["params"], n), device_view(fl["grads"], n)
+    hp = rng.normal(size=n).astype(np.float32)
+    p.copy_(torch.from_numpy(hp))
+    cfg = arf.AdamConfig(total_steps=50, final_lr_factor=0.1)
+    op, om, ov = hp.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    for step in range(1, 4):
+        hg = rng.normal(size=n).astype(np.float32)
+        g.copy_(torch.from_numpy(hg))
+        m.adam_step(cfg, step)
+        torch.cuda.synchronize()
+        og = hg.copy()
+        oracle.adam(op, og, om, ov, cfg, step, fl["mlp_offset"])
+    dm, dv = m.adam_state()
+    assert np.array_equal(p.cpu().numpy(), op)
+    assert np.array_equal(dm, om) and np.array_equal(dv, ov)
+    assert np.all(g.cpu().numpy() == 0)
+
+
+def test_fused_train_step_matches_composed(gpu, oracle):
+    """arfx_train_step (losses inside the composite kernel) == train_fwd_bwd fed with the
+    oracle's loss gradients of the same rendered rays."""
+    sk = fx.default_figure_skeleton()
+    fig = fx.default_figure()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (24, 24, 24), 11)
+    pose = fx.random_pose(sk, 8, max_angle=0.3)
+    cam = fx.default_camera(sk, 96, 96)
+    occ = arf.OccupancyGrid(m.normalized_box, arf.OccupancyConfig())
+    arf.update_training_grid(m, occ, [pose], 0.95, 3, 0)
+    gt_img, mask = arf.figure_render(fig, pose, m.normalized_box, cam, arf.RenderOptions(samples_per_ray=512))
+    rng = np.random.default_rng(5)
+    n = 2048
+    px = rng.integers(0, 96, n).astype(np.int32)
+    py = rng.integers(0, 96, n).astype(np.int32)
+    gt_rgb = gt_img.rgb[py, px]
+    gt_a = mask[py, px].astype(np.float32)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=9, frame_id=4)
+    cfg = arf.LossConfig()
+    m.zero_grad()
+    l4, rgb, alpha = arf.train_step(m, pose, cam, occ, opt, px, py, gt_rgb, gt_a, cfg)
+    g1, w1 = m.grads()
+    ol4, odr, oda = oracle.losses(rgb, alpha, gt_rgb, gt_a, cfg)
+    np.testing.assert_allclose(l4, ol4, rtol=1e-12)
+    m.zero_grad()
+    rgb2, alpha2 = arf.train_fwd_bwd(m, pose, cam, occ, opt, px, py, odr, oda)
+    g2, w2 = m.grads()
+    assert np.array_equal(rgb, rgb2) and np.array_equal(alpha, alpha2)
+    assert np.abs(w1).max() > 0
+    # same per-sample upstream (up to 1-ulp exp/log differences); f32 atomics reorder the sums
+    np.testing.assert_allclose(w1, w2, rtol=1e-4, atol=1e-6 * np.abs(w2).max())
+    np.testing.assert_allclose(g1, g2, rtol=1e-4, atol=1e-6 * np.abs(g2).max())
+
+
+def test_trainer_reduces_loss(gpu):
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig, psnr
+    sk = fx.default_figure_skeleton()
+    fig = fx.default_figure()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (24, 24, 24), 12)
+    poses = [fx.random_pose(sk, 200 + i, max_angle=0.3) for i in range(4)]
+    cam = fx.default_camera(sk, 64, 64)
+    cfg = TrainConfig(iterations=150, rays_per_batch=2048, samples_per_ray=96,
+                      adam=arf.AdamConfig(total_steps=150))
+    tr = Trainer(m, fig, poses, cam, cfg)
+    h = tr.train()
+    assert h.shape == (150, 4) and np.all(np.isfinite(h))
+    assert h[-20:, 3].mean() < 0.5 * h[:10, 3].mean(), (h[:10, 3].mean(), h[-20:, 3].mean())
+    # the trained model renders closer to the ground truth than the untrained one did
+    occ = arf.build_model_inference_grid(m, poses[0], arf.OccupancyConfig())
+    img = arf.render_model(m, poses[0], cam, occ, arf.RenderOptions(samples_per_ray=96))
+    gt = tr.gt_rgb[0].cpu().numpy().reshape(64, 64, 3)
+    assert psnr(img.rgb, gt) > 15.0, psnr(img.rgb, gt)
