@@ -301,7 +301,14 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline()
         if world == 1 and not args.no_extra:
             line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
-                                     "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline)}
+                                     "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline),
+                                     "train_step_full": bench_train_full(30)}
+    if world > 1 and args.dp_train:
+        # config 5 (data-parallel training over NCCL); opt-in: the only multi-rank path that
+        # cannot be exercised on this single-GPU development pool
+        dp = bench_train_full(20, rank, world, None)
+        if rank == 0:
+            line["extra_configs"] = {"train_step_dp": dp}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -515,6 +522,50 @@ def bench_train(model, steps: int, with_cpu: bool):
     return out
 
 
+def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
+    """SPEC train_step at config 3 (config 5 when world > 1: 4096 rays per rank, weak scaling):
+    rays + ground truth gathered on the device, forward + fused losses + backward
+    (arfx_train_step_device), reduce-scatter / sharded Adam / all-gather of the flat vectors over
+    NCCL (world > 1), Adam with fused zero-grad, occupancy update every 16 steps. Ground truth:
+    8 frames of the analytic smpl24 figure rendered at 4x N by arfx_figure_render. Device-timed
+    with CUDA events on the step stream; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2212_10550_b200 import arf, fixtures as fx
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig
+    sk = fx.smpl24()
+    model = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    cam = fx.default_camera(sk, W_IMG, H_IMG)
+    poses = [fx.random_pose(sk, 100 + i) for i in range(8)]
+    cfg = TrainConfig(iterations=steps, rays_per_batch=4096 * world, samples_per_ray=128, occupancy_interval=16,
+                      seed=9, adam=arf.AdamConfig(total_steps=1000))
+    tr = Trainer(model, fx.figure_for(sk), poses, cam, cfg, rank, world, group)
+    for _ in range(3):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0 = model.counters.posed_queries
+    e0.record()
+    for _ in range(steps):
+        tr.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        ms = float(t[0])
+    h = np.array(tr.history)
+    return {"workload": f"SPEC train_step, config {'5' if world > 1 else '3'}: 4096 rays/rank x {world} rank(s), "
+                        "fwd + fused losses + bwd + Adam (+ occupancy update every 16 steps)"
+                        + (", grads reduce-scatter + params all-gather over NCCL" if world > 1 else ""),
+            "iters_per_s": steps / (ms / 1000.0), "ms_per_iter": ms / steps, "rays_per_s": 4096 * world * steps /
+            (ms / 1000.0), "n_flat_params": tr.n_flat, "loss_first": h[0].tolist(), "loss_last": h[-1].tolist(),
+            "posed_samples_per_iter_rank0": (model.counters.posed_queries - c0) / steps}
+
+
 def cpu_baseline():
     try:
         secs, posed, threads = reference_frames(2)
@@ -535,6 +586,8 @@ def main():
     ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "exact"],
                     help="render decoder for `value` (the other one is reported as other_decoder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dp-train", action="store_true",
+                    help="N > 1: also time the data-parallel SPEC train step (config 5) over NCCL")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
