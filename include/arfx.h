@@ -25,6 +25,7 @@
  *   arfx_field_query_backward   <- CanonicalField::query_backward     R/field.hpp:91-103
  *   arfx_train_fwd_bwd          <- composed training step
  *   arfx_losses / arfx_train_step(_device)  <- SPEC.md:454-489 losses fused into the step
+ *   arfx_density_step(_device)  <- SPEC.md:478-484 L_density occupancy regulariser
  *   arfx_adam_step              <- SPEC.md:508-509 optimizer (flat vector, shardable)
  *   arfx_figure_*               <- R/scene.hpp analytic ground truth (SPEC.md scenegen)
  *
@@ -305,6 +306,14 @@ int arfx_train_step_device(arfx_model m, arfx_pose p, const arfx_camera* cam, ar
                            const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
                            const arfx_loss_config* cfg, double* d_loss4, float* d_rgb, float* d_alpha,
                            void* stream);
+/* L_density (Eq. 12): n points uniform in the normalized box, point i
+ * drawn from keyed_rng(seed, 0xde45, step, i) (x, y, z); those in EMPTY cells of `occ`
+ * are posed-queried (R/articulation.hpp:163-181); loss2 = (L_density = mean |sigma| over
+ * them, n_empty); w_density * dL/dtheta accumulated into the model's gradients. */
+int arfx_density_step(arfx_model m, arfx_pose p, arfx_occ_grid occ, int64_t n_points, uint64_t seed,
+                      uint64_t step, const arfx_loss_config* cfg, double* loss2, void* stream);
+int arfx_density_step_device(arfx_model m, arfx_pose p, arfx_occ_grid occ, int64_t n_points, uint64_t seed,
+                             uint64_t step, const arfx_loss_config* cfg, double* d_loss2, void* stream);
 /* Adam over flat parameter indices [begin, end) (multiples of 4; end = -1: all), step >= 1,
  * gradients zeroed in the same pass. Asynchronous on stream. */
 int arfx_adam_step(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,

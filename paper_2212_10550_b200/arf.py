@@ -674,6 +674,32 @@ def train_step(model: Model, pose: "SkeletonPose | PosedModelView", camera: Came
     return l4, rgb, alpha
 
 
+def density_step(model: Model, pose: "SkeletonPose | PosedModelView", occupancy: "OccupancyGrid", n_points: int,
+                 seed: int, step: int, cfg: LossConfig):
+    """L_density (SPEC.md:478-484): returns (L_density, n_empty); w_density * gradient is
+    accumulated into the model (arfx_density_step)."""
+    view = pose if isinstance(pose, PosedModelView) else PosedModelView(model, pose)
+    out = np.zeros(2, np.float64)
+    call("arfx_density_step", model._h, view._h, occupancy._h, n_points, seed & (2**64 - 1), step & (2**64 - 1),
+         C.byref(cfg.to_c()), ptr(out, C.c_double), None)
+    return float(out[0]), int(out[1])
+
+
+def density_points(occupancy_box: Aabb, n: int, seed: int, step: int) -> np.ndarray:
+    """The L_density sample points (host restatement of density_points_kernel, for tests):
+    point i = lo + e * (u0, u1, u2), u from keyed_rng(seed, 0xde45, step, i)."""
+    from .fixtures import keyed_rng
+    lo = np.asarray(occupancy_box.lo, np.float64)
+    e = np.asarray(occupancy_box.hi, np.float64) - lo
+    out = np.empty((n, 3), np.float64)
+    for i in range(n):
+        r = keyed_rng(seed, 0xDE45, step, i)
+        u = (r.next_double(), r.next_double(), r.next_double())
+        for a in range(3):
+            out[i, a] = lo[a] + e[a] * u[a]
+    return out
+
+
 # ----------------------------------------------------------------------------- analytic ground truth
 
 

@@ -1447,6 +1447,58 @@ int arfx_train_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, 
   });
 }
 
+namespace {
+void run_density(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step, double w,
+                 double* d_out2, cudaStream_t s) {
+  ensure_grad_store(m, s);
+  for (int attempt = 0;; ++attempt) {
+    density_forward(m, p, g, n, seed, step, s);
+    unsigned long long hc[8];
+    d2h(hc, m.ws.counters.ptr, 8, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    bool rerun;
+    check_overflow_and_grow(m, hc, rerun);
+    if (!rerun) break;
+    if (attempt == 2) throw std::runtime_error("density_step: workspace overflow persisted");
+  }
+  density_backward(m, n, w, d_out2, s);
+}
+}  // namespace
+
+int arfx_density_step(arfx_model mh, arfx_pose ph, arfx_occ_grid occ, int64_t n_points, uint64_t seed,
+                      uint64_t step, const arfx_loss_config* cfg, double* loss2, void* stream) {
+  return guard([&] {
+    require(mh && ph && occ, "density_step: null argument");
+    const LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n_points <= 0) {
+      if (loss2) loss2[0] = loss2[1] = 0.0;
+      return;
+    }
+    const cudaStream_t s = stream_of(m, stream);
+    DevBuf<double> out;
+    out.alloc(2);
+    run_density(m, ph->impl, occ->impl, n_points, seed, step, lt.w_density, out.ptr, s);
+    double h[2];
+    d2h(h, out.ptr, 2, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    if (loss2) loss2[0] = h[0], loss2[1] = h[1];
+  });
+}
+
+int arfx_density_step_device(arfx_model mh, arfx_pose ph, arfx_occ_grid occ, int64_t n_points, uint64_t seed,
+                             uint64_t step, const arfx_loss_config* cfg, double* d_loss2, void* stream) {
+  return guard([&] {
+    require(mh && ph && occ && d_loss2, "density_step: null argument");
+    const LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (n_points <= 0) return;
+    run_density(m, ph->impl, occ->impl, n_points, seed, step, lt.w_density, d_loss2, stream_of(m, stream));
+  });
+}
+
 int arfx_adam_step(arfx_model mh, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
                    void* stream) {
   return guard([&] {

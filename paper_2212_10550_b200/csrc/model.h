@@ -64,6 +64,9 @@ struct Workspace {
   DevBuf<float4> pres;                // (density, r, g, b) per pool entry
   DevBuf<int32_t> ray_first, ray_count, row_list;
   DevBuf<double> train_terms;          // fused-loss per-ray terms
+  DevBuf<double> dens_pts;             // L_density points (SoA)
+  DevBuf<uint8_t> dens_empty;          // point lies in an empty occupancy cell
+  DevBuf<float> dens_scale;            // w_density / n_empty
   DevBuf<float> train_rgb, train_alpha;  // training outputs when the caller passes none
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
   // K2 start pipeline (deform_starts.cuh)
@@ -199,6 +202,10 @@ struct LossTargets {
 void loss_reduce(const double* d_terms, long long n, const LossTargets& lt, double* d_out4, cudaStream_t s);
 void ray_losses(long long n, const float* d_rgb, const float* d_alpha, const LossTargets& lt, float* d_grad_rgb,
                 float* d_grad_alpha, cudaStream_t s);
+// L_density (render.cu): forward (points + posed query), backward (loss + K8)
+void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step,
+                     cudaStream_t s);
+void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s);
 // optim.cu: Adam over the flat parameter vector
 struct AdamCfg {
   double lr_grid, lr_mlp, beta1, beta2, eps;

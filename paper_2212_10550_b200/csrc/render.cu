@@ -1149,4 +1149,116 @@ KernelProfiler::~KernelProfiler() {
   for (cudaEvent_t e : free_events) cudaEventDestroy(e);
 }
 
+// ---- L_density: occupancy-based regulariser (Eq. 12) ----------
+// n points uniform in the normalized box, point i from keyed_rng(seed, 0xde45, step, i)
+// (x, y, z draws); points in EMPTY cells of the occupancy grid are posed-queried (K2 + exact
+// K3) and L_density = mean |sigma| over them (0 when none). Its gradient
+// w_density * sign(sigma) / n_empty lands on the selected root's pool entry, and K8 runs
+// query_backward there -- the same path as the photometric step.
+namespace {
+__global__ void density_points_kernel(OccView g, long long n, uint64_t seed, uint64_t step, double* __restrict__ x,
+                                      double* __restrict__ y, double* __restrict__ z, uint8_t* __restrict__ empty) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    Pcg32 r = keyed_rng(seed, 0xDE45ull, step, static_cast<uint64_t>(i));
+    const double u0 = pcg_double(r), u1 = pcg_double(r), u2 = pcg_double(r);
+    const d3 p = make3(dadd(g.lo[0], dmul(g.e[0], u0)), dadd(g.lo[1], dmul(g.e[1], u1)),
+                       dadd(g.lo[2], dmul(g.e[2], u2)));
+    x[i] = p.x;
+    y[i] = p.y;
+    z[i] = p.z;
+    empty[i] = occupied(g, p) ? 0 : 1;
+  }
+}
+
+// one block, fixed order: out2 = (mean sigma over empty points with a root... / n_empty, n_empty),
+// scale = w / n_empty for the flag pass
+__global__ void __launch_bounds__(256) density_reduce_kernel(long long n, const uint8_t* __restrict__ empty,
+                                                             const uint8_t* __restrict__ snroot,
+                                                             const int32_t* __restrict__ sbase,
+                                                             const float4* __restrict__ pres, double w,
+                                                             double* __restrict__ out2, float* __restrict__ scale) {
+  __shared__ double ss[256];
+  __shared__ unsigned long long sc[256];
+  double a = 0.0;
+  unsigned long long c = 0;
+  for (long long i = threadIdx.x; i < n; i += 256) {
+    if (!empty[i]) continue;
+    ++c;
+    float4 v;
+    if (select_root(snroot, sbase, pres, i, v) >= 0) a += fabs(static_cast<double>(v.x));
+  }
+  ss[threadIdx.x] = a;
+  sc[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      ss[threadIdx.x] += ss[threadIdx.x + o];
+      sc[threadIdx.x] += sc[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double ne = static_cast<double>(sc[0]);
+    out2[0] = sc[0] ? ss[0] / ne : 0.0;
+    out2[1] = ne;
+    *scale = sc[0] ? static_cast<float>(w / ne) : 0.0f;
+  }
+}
+
+__global__ void density_flag_kernel(long long n, const uint8_t* __restrict__ empty, const uint8_t* __restrict__ snroot,
+                                    const int32_t* __restrict__ sbase, const float4* __restrict__ pres,
+                                    const float* __restrict__ scale, float* __restrict__ pgs, float* __restrict__ pgc,
+                                    uint8_t* __restrict__ pflag) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!empty[i]) continue;
+    float4 v;
+    const int sel = select_root(snroot, sbase, pres, i, v);
+    if (sel < 0) continue;
+    const long long p = sbase[i] + sel;
+    // d|sigma|/dsigma = sign(sigma); sigma = softplus > 0 except underflow
+    pgs[p] = v.x > 0.0f ? *scale : (v.x < 0.0f ? -*scale : 0.0f);
+    pgc[3 * p + 0] = pgc[3 * p + 1] = pgc[3 * p + 2] = 0.0f;
+    pflag[p] = 1;
+  }
+}
+}  // namespace
+
+// Forward half: points, occupancy test, posed query into the workspace pool. Returns with
+// the counters on the device (the caller checks overflow and re-runs).
+void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step,
+                     cudaStream_t s) {
+  Workspace& w = m.ws;
+  w.ensure(static_cast<size_t>(n), 0);
+  w.dens_pts.ensure(static_cast<size_t>(3 * n));
+  w.dens_empty.ensure(static_cast<size_t>(n));
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
+  double* x = w.dens_pts.ptr;
+  density_points_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.view(), n, seed, step, x, x + n, x + 2 * n,
+                                                             w.dens_empty.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  // every point is queried (the occupancy test only decides which ones enter the loss): the
+  // empty-cell fraction is ~90 %, and querying all keeps the pipeline branch-free
+  ListSrc src{x, x + n, x + 2 * n, nullptr, n, n};
+  launch_deform(m, p.dev.ptr, src, n, s);
+  launch_field_pool(m, s, n);
+}
+
+// Backward half: loss reduction and gradient flags, then K8 into the model's gradients.
+void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s) {
+  Workspace& w = m.ws;
+  w.ensure_train();
+  w.dens_scale.ensure(1);
+  ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
+  density_reduce_kernel<<<1, 256, 0, s>>>(n, w.dens_empty.ptr, w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w_density,
+                                          d_out2, w.dens_scale.ptr);
+  density_flag_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.dens_empty.ptr, w.snroot.ptr, w.sbase.ptr,
+                                                          w.pres.ptr, w.dens_scale.ptr, w.pgs.ptr, w.pgc.ptr,
+                                                          w.pflag.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
+                      s);
+}
+
 }  // namespace arfx

@@ -3,12 +3,13 @@
 The reference code base stops at the differentiable pieces (composite_backward,
 query_backward); the SPEC's trainer is built here over the libarfx training ABI:
 
-  per step t (all on the device, one host sync for the workspace-overflow check):
+  per step t (all on the device; the host syncs only for the workspace-overflow checks):
     rays     B / world rays per rank: frame f and pixels from keyed_rng(seed, 0x7a11, t, rank)
              (draw order: frame, then px, py per ray), ground truth gathered from the
              device-resident dataset frames (analytic figure, arfx_figure_render)
     step     arfx_train_step_device: forward, losses fused into the composite kernel,
              backward -> the model's flat gradient vector
+    density  arfx_density_step_device: L_density over 4096 uniform points (w_density > 0)
     sync     world > 1: reduce-scatter(AVG) of the flat gradients over NCCL, Adam on this
              rank's shard, all-gather of the parameter shards (FlatDataParallel)
     optim    arfx_adam_step (zero-grad fused), cosine lr
@@ -54,6 +55,7 @@ class TrainConfig:  # TrainConfig SPEC.md:450-453
     adam: arf.AdamConfig = field(default_factory=arf.AdamConfig)
     occupancy: arf.OccupancyConfig = field(default_factory=arf.OccupancyConfig)
     gt_oversample: int = 4               # SPEC scenegen: ground truth at 4x the training N
+    density_points: int = 4096           # L_density point budget per step
 
 
 class FlatDataParallel:
@@ -142,6 +144,7 @@ class Trainer:
         self.dp = FlatDataParallel(self.params, self.grads, self.n_flat, rank, world, group)
         self.stream = torch.cuda.current_stream()
         self.loss4 = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.loss_d = torch.zeros(2, dtype=torch.float64, device="cuda")
         self.px = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
         self.py = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
         self.b_rgb = torch.zeros((self.n_local, 3), dtype=torch.float32, device="cuda")
@@ -171,12 +174,19 @@ class Trainer:
                C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
                C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
                None, None, sp)
+        if cfg.loss.w_density > 0 and cfg.density_points > 0:  # L_density
+            L.call("arfx_density_step_device", self.model._h, self.views[f]._h, self.grid._h, cfg.density_points,
+                   (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id, C.byref(cfg.loss.to_c()),
+                   C.c_void_p(self.loss_d.data_ptr()), sp)
         t = self.step_id + 1
         self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
         if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
             arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t)
         self.step_id = t
-        loss = self.loss4.cpu().numpy().copy()
+        l4 = self.loss4.cpu().numpy()
+        ld = float(self.loss_d[0].cpu()) if cfg.loss.w_density > 0 else 0.0
+        # (L_rgb, L_alpha, L_hard, L_density, total)
+        loss = np.array([l4[0], l4[1], l4[2], ld, l4[3] + cfg.loss.w_density * ld])
         if not np.all(np.isfinite(loss)):
             raise L.NumericError(3, f"train_step: non-finite loss at step {t}: {loss.tolist()}")
         self.history.append(loss)

@@ -128,10 +128,49 @@ def test_trainer_reduces_loss(gpu):
                       adam=arf.AdamConfig(total_steps=150))
     tr = Trainer(m, fig, poses, cam, cfg)
     h = tr.train()
-    assert h.shape == (150, 4) and np.all(np.isfinite(h))
-    assert h[-20:, 3].mean() < 0.5 * h[:10, 3].mean(), (h[:10, 3].mean(), h[-20:, 3].mean())
+    assert h.shape == (150, 5) and np.all(np.isfinite(h))
+    assert h[-20:, 4].mean() < 0.5 * h[:10, 4].mean(), (h[:10, 4].mean(), h[-20:, 4].mean())
     # the trained model renders closer to the ground truth than the untrained one did
     occ = arf.build_model_inference_grid(m, poses[0], arf.OccupancyConfig())
     img = arf.render_model(m, poses[0], cam, occ, arf.RenderOptions(samples_per_ray=96))
     gt = tr.gt_rgb[0].cpu().numpy().reshape(64, 64, 3)
     assert psnr(img.rgb, gt) > 15.0, psnr(img.rgb, gt)
+
+
+def test_density_step_vs_reference(gpu, ref):
+    """L_density: the GPU's empty-cell selection, loss and gradient against the reference's
+    posed_query + query_backward on the same points (restated on the host)."""
+    sk = fx.default_figure_skeleton()
+    g, mc = arf.HashGridConfig(levels=16, table_size_log2=14, base_resolution=4, max_resolution=96), \
+        arf.MlpConfig(32, 64, 2, 4)
+    dm = arf.build_model(sk, g, mc, (16, 16, 16), 21)
+    rm = ref.build_model(sk, g, mc, (16, 16, 16), 21)
+    pose = fx.random_pose(sk, 6, max_angle=0.3)
+    cfg_o = arf.OccupancyConfig()
+    occ = arf.build_model_inference_grid(dm, pose, cfg_o)
+    # the inference grid marks every cell holding a root occupied; clear every other z-slab
+    # so empty cells with roots (the regulariser's targets) exist
+    vals, mask = occ.download()
+    mask = mask.reshape(64, 64, 64).copy()
+    mask[::2] = 0
+    occ.upload(vals, mask.reshape(-1))
+    n, seed, step = 3000, 17, 5
+    cfg = arf.LossConfig(w_density=0.25)
+    dm.zero_grad()
+    ld, n_empty = arf.density_step(dm, pose, occ, n, seed, step, cfg)
+    gg, gm = dm.grads()
+    pts = arf.density_points(dm.normalized_box, n, seed, step)
+    lo = np.array(dm.normalized_box.lo)
+    e = np.array(dm.normalized_box.hi) - lo
+    u = (pts - lo) / e
+    c = np.minimum((u * 64).astype(np.int64), 63)
+    empty = mask[c[:, 2], c[:, 1], c[:, 0]] == 0
+    assert n_empty == int(empty.sum()) and 0 < n_empty < n
+    dens, col, canon, has = ref.posed_query(rm, pose.bone_transforms, pose.global_transform, pts)
+    sel = empty & (has != 0)
+    np.testing.assert_allclose(ld, float(np.abs(dens[sel].astype(np.float64)).sum() / n_empty), rtol=1e-5)
+    rg, rw = ref.field_query_backward(rm, canon[sel], np.full(sel.sum(), cfg.w_density / n_empty, np.float32),
+                                      np.zeros((sel.sum(), 3), np.float32))
+    assert np.abs(rw).max() > 0
+    np.testing.assert_allclose(gm, rw, rtol=1e-4, atol=1e-6 * np.abs(rw).max())
+    np.testing.assert_allclose(gg, rg, rtol=1e-4, atol=1e-6 * np.abs(rg).max())

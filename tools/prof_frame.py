@@ -1,5 +1,5 @@
 """Small driver for ncu: config-1 avatar, F frames of (inference grid + render) at 540x540
-through the device API on one stream. Usage: python tools/prof_frame.py [frames] [exact|tcgen05]"""
+through the device API on one stream. Usage: python tools/prof_frame.py [frames] [exact|tcgen05] [stats]"""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -24,13 +24,15 @@ def main(frames: int = 3, mlp: str = "exact"):
     views = [arf.PosedModelView(model, p) for p in poses]
     out = arf.RenderImages(540, 540, np.zeros((540, 540, 3), np.float32), np.zeros((540, 540), np.float32))
     stats = np.zeros(16, np.uint64)
-    check(L.arfx_stats_enable(model._h, 1))
+    with_stats = len(sys.argv) > 3 and sys.argv[3] == "stats"
+    check(L.arfx_stats_enable(model._h, 1 if with_stats else 0))
     for f in range(frames):
         v = views[f % len(views)]
         check(L.arfx_build_inference_grid(model._h, v._h, occ._h, None, None))
         arf.render_model(model, v, cam, occ, opt, out=out)
-    check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
-    print("per-frame stats E U I S P Q QT:", (stats[:7] / frames).astype(np.int64).tolist())
+    if with_stats:
+        check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
+        print("per-frame stats E U I S P Q QT:", (stats[:7] / frames).astype(np.int64).tolist())
     print("frames", frames, "posed", model.counters.posed_queries, "alpha sum", float(out.alpha.sum()))
 
 
