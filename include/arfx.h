@@ -28,6 +28,7 @@
  *   arfx_density_step(_device)  <- SPEC.md:478-484 L_density occupancy regulariser
  *   arfx_adam_step              <- SPEC.md:508-509 optimizer (flat vector, shardable)
  *   arfx_figure_*               <- R/scene.hpp analytic ground truth (SPEC.md scenegen)
+ *   arfx_checkpoint_save/load   <- SPEC.md checkpoint file (versioned, bitwise round trip)
  *
  * Error convention (the reference throws; R/math.hpp:12-18): every function
  * returns an int status, 0 = ok, and sets a thread-local message readable via
@@ -187,6 +188,9 @@ int arfx_pose_destroy(arfx_pose p);
 int arfx_occ_create(const double box_lo[3], const double box_hi[3], const arfx_occ_config* cfg,
                     arfx_occ_grid* out); /* OccupancyGrid::empty  R/occupancy.hpp:59-69 */
 int arfx_occ_destroy(arfx_occ_grid g);
+/* an OccupancyGrid from its stored members (density threshold, not alpha; checkpoint restore) */
+int arfx_occ_create_raw(const double box_lo[3], const double box_hi[3], int resolution, double density_threshold,
+                        int dilation, arfx_occ_grid* out);
 int arfx_occ_info(arfx_occ_grid g, int res[3], double box_lo[3], double box_hi[3],
                   double* density_threshold, int* dilation);
 int arfx_occ_download(arfx_occ_grid g, float* values, uint8_t* mask);
@@ -325,6 +329,21 @@ int arfx_model_flat(arfx_model m, float** params, float** grads, float** adam_m,
 /* Host copies of the flat Adam moments (n_flat floats each; checkpoint / resume). */
 int arfx_model_get_adam(arfx_model m, float* adam_m, float* adam_v);
 int arfx_model_set_adam(arfx_model m, const float* adam_m, const float* adam_v);
+
+/* ---- checkpoint / wire format --- */
+
+/* Versioned little-endian binary: magic "ARFXCKPT", u32 version (1), then the model
+ * description (skeleton, grid / MLP configs, skinning resolution + boxes, canonical and
+ * normalized boxes, inverse-LBS options), the parameter arrays in the reference layouts
+ * (grid [L][2^T][F] f32, MLP W/b f32, skinning [z][y][x][bone] f64), optionally the
+ * occupancy grid (resolution, box, density threshold, dilation, values f32, mask u8) and
+ * the optimizer state (step, Adam m / v over the flat vector), then an FNV-1a 64 checksum
+ * of everything before it. Round trips are bitwise. */
+int arfx_checkpoint_save(const char* path, arfx_model m, arfx_occ_grid occ /* may be NULL */, int64_t step,
+                         int with_optimizer);
+/* Creates a model (and the occupancy grid when present and occ_out != NULL); restores the
+ * Adam moments when present. Errors: 2 (DataError) for a malformed / corrupt file. */
+int arfx_checkpoint_load(const char* path, arfx_model* m_out, arfx_occ_grid* occ_out, int64_t* step_out);
 
 /* ---- analytic ground truth (SPEC.md scenegen; R/scene.hpp) -------------------------- */
 

@@ -170,6 +170,9 @@ _PROTOS = {
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "arfx_model_get_adam": (C.c_int, [H, c_float_p, c_float_p]),
     "arfx_model_set_adam": (C.c_int, [H, c_float_p, c_float_p]),
+    "arfx_occ_create_raw": (C.c_int, [c_double_p, c_double_p, C.c_int, C.c_double, C.c_int, C.POINTER(H)]),
+    "arfx_checkpoint_save": (C.c_int, [C.c_char_p, H, H, C.c_int64, C.c_int]),
+    "arfx_checkpoint_load": (C.c_int, [C.c_char_p, C.POINTER(H), C.POINTER(H), C.POINTER(C.c_int64)]),
     "arfx_figure_query": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, C.c_int64, c_double_p,
                                     c_double_p]),
     "arfx_figure_render": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, c_double_p, c_double_p,

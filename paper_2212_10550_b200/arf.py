@@ -394,14 +394,27 @@ class OccupancyGrid:
         h = C.c_void_p()
         call("arfx_occ_create", ptr(lo, C.c_double), ptr(hi, C.c_double), C.byref(cfg.to_c()), C.byref(h))
         self._h = h
+        self._describe()
+
+    def _describe(self):
         res = np.zeros(3, np.int32)
+        lo = np.zeros(3, np.float64)
+        hi = np.zeros(3, np.float64)
         thr = C.c_double()
         dil = C.c_int32()
-        call("arfx_occ_info", self._h, ptr(res, C.c_int32), None, None, C.byref(thr), C.byref(dil))
+        call("arfx_occ_info", self._h, ptr(res, C.c_int32), ptr(lo, C.c_double), ptr(hi, C.c_double), C.byref(thr),
+             C.byref(dil))
         self.resolution = tuple(int(r) for r in res)
-        self.box = box
+        self.box = Aabb(tuple(lo.tolist()), tuple(hi.tolist()))
         self.density_threshold = thr.value
         self.dilation = dil.value
+
+    @staticmethod
+    def _from_handle(h) -> "OccupancyGrid":
+        g = OccupancyGrid.__new__(OccupancyGrid)
+        g._h = h if isinstance(h, C.c_void_p) else C.c_void_p(h)
+        g._describe()
+        return g
 
     @staticmethod
     def empty(box: Aabb, cfg: OccupancyConfig) -> "OccupancyGrid":
@@ -698,6 +711,26 @@ def density_points(occupancy_box: Aabb, n: int, seed: int, step: int) -> np.ndar
         for a in range(3):
             out[i, a] = lo[a] + e[a] * u[a]
     return out
+
+
+# ----------------------------------------------------------------------------- checkpoint
+
+
+def save_checkpoint(path, model: Model, occupancy: "OccupancyGrid | None" = None, step: int = 0,
+                    with_optimizer: bool = False) -> None:
+    """SPEC checkpoint file (arfx_checkpoint_save): configs, grid, MLP, skinning, optional
+    occupancy grid and Adam state; bitwise round trip."""
+    call("arfx_checkpoint_save", str(path).encode(), model._h, occupancy._h if occupancy is not None else None,
+         int(step), 1 if with_optimizer else 0)
+
+
+def load_checkpoint(path):
+    """-> (Model, OccupancyGrid | None, step)."""
+    mh, oh, st = C.c_void_p(), C.c_void_p(), C.c_int64()
+    call("arfx_checkpoint_load", str(path).encode(), C.byref(mh), C.byref(oh), C.byref(st))
+    model = Model(mh)
+    occ = OccupancyGrid._from_handle(oh) if oh.value else None
+    return model, occ, st.value
 
 
 # ----------------------------------------------------------------------------- analytic ground truth

@@ -59,6 +59,11 @@ int guard(F&& f) {
   }
 }
 
+}  // namespace
+// lets host-only translation units (checkpoint.cpp) report through arfx_last_error()
+void set_error_message(const std::string& m) { g_err = m; }
+namespace {
+
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
@@ -656,6 +661,31 @@ int arfx_occ_create(const double lo[3], const double hi[3], const arfx_occ_confi
     o.box = HostBox{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
     o.dilation = cfg->dilation;
     o.threshold = occupancy_threshold(o.box, o.res, cfg->alpha_threshold);
+    const size_t n = static_cast<size_t>(o.res) * o.res * o.res;
+    o.values.alloc(n);
+    o.mask.alloc(n);
+    ARFX_CUDA(cudaMemset(o.values.ptr, 0, n * sizeof(float)));
+    ARFX_CUDA(cudaMemset(o.mask.ptr, 0, n));
+    *out = g.release();
+  });
+}
+
+// arf::OccupancyGrid members as stored (R/occupancy.hpp:37-48): checkpoint restore
+int arfx_occ_create_raw(const double lo[3], const double hi[3], int resolution, double density_threshold,
+                        int dilation, arfx_occ_grid* out) {
+  return guard([&] {
+    require(lo && hi && out, "occ_create_raw: null argument");
+    require(resolution >= 1 && resolution <= 1024, "occupancy: resolution out of range");
+    require(dilation >= 0, "occupancy: negative dilation");
+    require(std::isfinite(density_threshold), "occupancy: non-finite threshold");
+    require_device();
+    auto g = std::make_unique<arfx_occ_s>();
+    OccImpl& o = g->impl;
+    ARFX_CUDA(cudaGetDevice(&o.device));
+    o.res = resolution;
+    o.box = HostBox{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+    o.dilation = dilation;
+    o.threshold = density_threshold;
     const size_t n = static_cast<size_t>(o.res) * o.res * o.res;
     o.values.alloc(n);
     o.mask.alloc(n);

@@ -81,4 +81,6 @@ void validate_camera(const HostCamera& c);  // R/camera.hpp:15-22
 double occupancy_threshold(const HostBox& box, int res, double alpha_threshold);
 void validate_occ_cfg(int resolution, double alpha_threshold, int dilation, double decay, int interval);
 
+void set_error_message(const std::string& m);  // abi.cu: the thread-local arfx_last_error()
+
 }  // namespace arfx

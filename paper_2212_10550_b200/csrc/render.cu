@@ -507,24 +507,6 @@ __global__ void occ_query_kernel(OccView g, const double* __restrict__ pts, long
     out[i] = occupied_fast(g, make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2])) ? 1 : 0;
 }
 
-__global__ void inverse_lbs_kernel(SkinView S, const PoseCtx* __restrict__ P, InverseOpts opt,
-                                   const double* __restrict__ pts, long long n, int32_t* counts,
-                                   double* roots, double* resid) {
-  extern __shared__ double ws_smem[];
-  double* ws = ws_smem + threadIdx.x;
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    Roots R;
-    inverse_lbs(S, P, opt, make3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]), ws, blockDim.x, R);
-    counts[i] = R.count;
-    for (int k = 0; k < R.count; ++k) {
-      roots[(i * kMaxRoots + k) * 3 + 0] = R.x[k][0];
-      roots[(i * kMaxRoots + k) * 3 + 1] = R.x[k][1];
-      roots[(i * kMaxRoots + k) * 3 + 2] = R.x[k][2];
-      resid[i * kMaxRoots + k] = R.r[k];
-    }
-  }
-}
 
 __global__ void posed_out_kernel(long long n, const uint8_t* __restrict__ snroot,
                                  const int32_t* __restrict__ sbase, const float4* __restrict__ pres,

@@ -174,3 +174,33 @@ def test_density_step_vs_reference(gpu, ref):
     assert np.abs(rw).max() > 0
     np.testing.assert_allclose(gm, rw, rtol=1e-4, atol=1e-6 * np.abs(rw).max())
     np.testing.assert_allclose(gg, rg, rtol=1e-4, atol=1e-6 * np.abs(rg).max())
+
+
+def test_checkpoint_bitwise_round_trip(gpu, tmp_path):
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig
+    sk = fx.default_figure_skeleton()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (20, 20, 20), 13)
+    poses = [fx.random_pose(sk, 300 + i, max_angle=0.3) for i in range(2)]
+    cam = fx.default_camera(sk, 48, 48)
+    tr = Trainer(m, fx.default_figure(), poses, cam, TrainConfig(iterations=5, rays_per_batch=1024,
+                                                                 samples_per_ray=64))
+    tr.train()
+    path = tmp_path / "avatar.ckpt"
+    arf.save_checkpoint(path, m, tr.grid, step=tr.step_id, with_optimizer=True)
+    m2, occ2, step = arf.load_checkpoint(path)
+    assert step == 5 and occ2 is not None
+    for a, b in zip(m.params(), m2.params()):
+        assert np.array_equal(a, b)
+    for a, b in zip(m.adam_state(), m2.adam_state()):
+        assert np.array_equal(a, b)
+    for a, b in zip(tr.grid.download(), occ2.download()):
+        assert np.array_equal(a, b)
+    assert occ2.density_threshold == tr.grid.density_threshold and occ2.dilation == tr.grid.dilation
+    opt = arf.RenderOptions(samples_per_ray=64)
+    i1 = arf.render_model(m, poses[0], cam, tr.grid, opt)
+    i2 = arf.render_model(m2, poses[0], cam, occ2, opt)
+    assert np.array_equal(i1.rgb, i2.rgb) and np.array_equal(i1.alpha, i2.alpha)
+    # a second save of the restored model is byte-identical
+    path2 = tmp_path / "again.ckpt"
+    arf.save_checkpoint(path2, m2, occ2, step=step, with_optimizer=True)
+    assert path.read_bytes() == path2.read_bytes()

@@ -114,3 +114,19 @@ def test_fixture_pcg_matches_reference_stream(oracle):
     r = fx.keyed_rng(77, 0x6a1d, 17)
     expect = np.array([r.uniform(-1e-4, 1e-4) for _ in range(gp.size)], np.float64).astype(np.float32)
     assert np.array_equal(gp.view(np.uint32), expect.view(np.uint32))
+
+
+def test_checkpoint_rejects_malformed_files(tmp_path):
+    """Checkpoint parsing (checkpoint.cpp) fails with DataError before touching a device."""
+    from paper_2212_10550_b200 import DataError, InvalidArgument
+    from paper_2212_10550_b200 import arf as A
+    bad = tmp_path / "bad.ckpt"
+    bad.write_bytes(b"not a checkpoint at all, definitely not")
+    with pytest.raises(DataError):
+        A.load_checkpoint(bad)
+    # right magic, wrong checksum
+    bad.write_bytes(b"ARFXCKPT" + b"\x01\x00\x00\x00" + b"\x00" * 40)
+    with pytest.raises(DataError, match="checksum"):
+        A.load_checkpoint(bad)
+    with pytest.raises(InvalidArgument):
+        A.load_checkpoint(tmp_path / "missing.ckpt")
