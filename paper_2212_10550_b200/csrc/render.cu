@@ -58,6 +58,17 @@ __device__ __forceinline__ int cell_axis_fast(double x, double lo, double e, dou
   return (res - 1 < c) ? res - 1 : c;
 }
 
+// Cell-space coordinate v ~ (x - lo) / e * res evaluated by a cheaper formula (error
+// <= ~1e-13): returns the cell, -1 outside, or -2 when v lies within 1e-12 of an integer
+// (cell edge or box bound), where only the reference's own arithmetic may decide.
+__device__ __forceinline__ int cell_from_v(double v, int res) {
+  const double fl = floor(v);
+  const double fr = dsub(v, fl);  // exact
+  if (!(fr > 1e-12 && fr < 1.0 - 1e-12)) return -2;
+  if (fl < 0.0 || fl >= static_cast<double>(res)) return -1;
+  return static_cast<int>(fl);
+}
+
 __device__ __forceinline__ bool occupied_fast(const OccView& g, d3 x) {
   const int cx = cell_axis_fast(x.x, g.lo[0], g.e[0], g.inv_e[0], g.rx);
   if (cx < 0) return false;
@@ -109,21 +120,35 @@ __device__ __forceinline__ double jitter_at(const MarchArgs& A, Pcg32 base, int 
   return pcg_double(base);
 }
 
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __longlong_as_double(__shfl_sync(0xffffffffu, __double_as_longlong(v), src));
+}
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  return static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<long long>(v), src));
+}
+
+// K1. Block = 256 rays per iteration. Lane l of warp w sets up ray (w, l) once (make_ray:
+// ~100 FP64 incl. 4 divisions and a sqrt); the warp then walks its 32 rays, broadcasting
+// each ray's geometry by shuffle and testing its N samples 32 at a time (ballots kept in
+// dynamic smem). One block-wide exclusive scan of the 256 ray counts and one atomic place
+// the block's samples; the second pass recomputes t / x only for occupied samples.
 __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
-  __shared__ unsigned bal[kMarchWarps][kMaxN / 32];
-  __shared__ int wcount[kMarchWarps];
-  __shared__ long long wbase[kMarchWarps];
+  extern __shared__ unsigned march_bal[];  // [256 rays][K]
+  __shared__ int wsum[kMarchWarps];
+  __shared__ long long bbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_rays = A.lpx ? A.n_list : static_cast<long long>(A.n_rows) * A.W;
   const int K = (A.N + 31) >> 5;
-  for (long long g0 = static_cast<long long>(blockIdx.x) * kMarchWarps; g0 < n_rays;
-       g0 += static_cast<long long>(gridDim.x) * kMarchWarps) {
-    const long long r = g0 + warp;
-    int count = 0;
+  constexpr int kRays = kMarchWarps * 32;
+  for (long long g0 = static_cast<long long>(blockIdx.x) * kRays; g0 < n_rays;
+       g0 += static_cast<long long>(gridDim.x) * kRays) {
+    // ---- this lane's ray
+    const long long r = g0 + threadIdx.x;
     int pix = -1, rid = -1;  // pix keys the RNG stream (R/render.hpp:201); rid indexes outputs
     RayGeom R{};
     double step = 0.0;
     Pcg32 rng{0, 0};
+    d3 cP = make3(0.0, 0.0, 0.0), cQ = cP;
     if (r < n_rays) {
       int px, py;
       if (A.lpx) {
@@ -136,68 +161,113 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
       pix = py * A.W + px;
       rid = A.lpx ? static_cast<int>(r) : pix;
       R = make_ray(A.cam, A.w2n, A.nlo, A.nhi, px, py);
-      if (R.valid && A.N > 0) {
+      R.valid = R.valid && A.N > 0;
+      if (R.valid) {
         step = ddiv(dsub(R.tf, R.tn), static_cast<double>(A.N));
         if (A.stratified) rng = keyed_rng(A.seed, A.frame, static_cast<uint64_t>(pix));
-        for (int k = 0; k < K; ++k) {
-          const int i = k * 32 + lane;
-          bool f = false;
-          if (i < A.N) {
-            if (A.has_occ) {
-              const double t = sample_t(R.tn, step, i, jitter_at(A, rng, i));
-              const d3 xn = rigid_apply(A.w2n, add3(R.o, mul3(R.d, t)));
-              f = occupied_fast(A.occ, xn);
-            } else {
-              f = true;
-            }
-          }
-          const unsigned b = __ballot_sync(0xffffffffu, f);
-          if (lane == 0) bal[warp][k] = b;
-          count += __popc(b);
-        }
+        // cell-space ray: v(t) = P + Q t ~ (G^-1 (o + d t) - lo) / e * res (fast path only)
+        const d3 on = rigid_apply(A.w2n, R.o);
+        const d3 dn = matvec(A.w2n, R.d);
+        const double sx = A.occ.inv_e[0] * A.occ.rx, sy = A.occ.inv_e[1] * A.occ.ry, sz = A.occ.inv_e[2] * A.occ.rz;
+        cP = make3((on.x - A.occ.lo[0]) * sx, (on.y - A.occ.lo[1]) * sy, (on.z - A.occ.lo[2]) * sz);
+        cQ = make3(dn.x * sx, dn.y * sy, dn.z * sz);
       }
     }
-    if (lane == 0) wcount[warp] = count;
+    // ---- pass 1: occupancy ballots, ray by ray (warp-uniform loop)
+    int my_count = 0;
+    const unsigned vmask = __ballot_sync(0xffffffffu, R.valid);
+    for (int j = 0; j < 32; ++j) {
+      if (!((vmask >> j) & 1u)) continue;
+      const double Px = shfl_d(cP.x, j), Py = shfl_d(cP.y, j), Pz = shfl_d(cP.z, j);
+      const double Qx = shfl_d(cQ.x, j), Qy = shfl_d(cQ.y, j), Qz = shfl_d(cQ.z, j);
+      const double tn = shfl_d(R.tn, j), st = shfl_d(step, j);
+      const Pcg32 rg{shfl_u64(rng.state, j), shfl_u64(rng.inc, j)};
+      const int pj = __shfl_sync(0xffffffffu, pix, j);
+      unsigned* bal = march_bal + (warp * 32 + j) * K;
+      int count = 0;
+      for (int k = 0; k < K; ++k) {
+        const int i = k * 32 + lane;
+        bool f = false;
+        if (i < A.N) {
+          if (A.has_occ) {
+            // t exactly as the reference; the cell decision from v = P + Q t (one FMA per
+            // axis), exact reference arithmetic only within 1e-12 of a cell edge
+            const double t = sample_t(tn, st, i, jitter_at(A, rg, i));
+            const int cx = cell_from_v(__fma_rn(Qx, t, Px), A.occ.rx);
+            const int cy = cell_from_v(__fma_rn(Qy, t, Py), A.occ.ry);
+            const int cz = cell_from_v(__fma_rn(Qz, t, Pz), A.occ.rz);
+            if (cx == -2 || cy == -2 || cz == -2) {
+              const RayGeom Rj = make_ray(A.cam, A.w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
+              f = occupied(A.occ, rigid_apply(A.w2n, add3(Rj.o, mul3(Rj.d, t))));
+            } else if (cx >= 0 && cy >= 0 && cz >= 0) {
+              f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
+            }
+          } else {
+            f = true;
+          }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) bal[k] = b;
+        count += __popc(b);
+      }
+      if (lane == j) my_count = count;
+    }
+    // ---- block exclusive scan of the 256 ray counts, one atomic per block
+    int incl = my_count;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (threadIdx.x == 0) {
       long long tot = 0;
       for (int w = 0; w < kMarchWarps; ++w) {
-        wbase[w] = tot;
-        tot += wcount[w];
+        const int c = wsum[w];
+        wsum[w] = static_cast<int>(tot);
+        tot += c;
       }
-      const long long base = tot ? static_cast<long long>(atomicAdd(A.counters, static_cast<unsigned long long>(tot))) : 0;
-      for (int w = 0; w < kMarchWarps; ++w) wbase[w] += base;
+      bbase = tot ? static_cast<long long>(atomicAdd(A.counters, static_cast<unsigned long long>(tot))) : 0;
     }
     __syncthreads();
+    const long long first = bbase + wsum[warp] + (incl - my_count);
     if (r < n_rays) {
-      const long long first = wbase[warp];
-      if (lane == 0) {
-        A.ray_first[rid] = static_cast<int32_t>(first < A.cap ? first : A.cap);
-        A.ray_count[rid] = (first + count <= A.cap) ? count : 0;
-      }
-      if (count) {
-        long long run = first;
-        for (int k = 0; k < K; ++k) {
-          const unsigned b = bal[warp][k];
-          if ((b >> lane) & 1u) {
-            const long long pos = run + __popc(b & lanemask_lt());
-            if (pos < A.cap) {
-              const int i = k * 32 + lane;
-              const double t = sample_t(R.tn, step, i, jitter_at(A, rng, i));
-              double delta;
-              if (i + 1 < A.N) delta = dsub(sample_t(R.tn, step, i + 1, jitter_at(A, rng, i + 1)), t);
-              else delta = dsub(R.tf, t);
-              const d3 xn = rigid_apply(A.w2n, add3(R.o, mul3(R.d, t)));
-              A.sx[pos] = xn.x;
-              A.sy[pos] = xn.y;
-              A.sz[pos] = xn.z;
-              A.sdelta[pos] = delta;
-              A.sray[pos] = rid;
-              A.sidx[pos] = static_cast<int16_t>(i);
-            }
+      A.ray_first[rid] = static_cast<int32_t>(first < A.cap ? first : A.cap);
+      A.ray_count[rid] = (first + my_count <= A.cap) ? my_count : 0;
+    }
+    // ---- pass 2: write the occupied samples of each ray
+    const unsigned cmask = __ballot_sync(0xffffffffu, my_count > 0);
+    for (int j = 0; j < 32; ++j) {
+      if (!((cmask >> j) & 1u)) continue;
+      const d3 o = make3(shfl_d(R.o.x, j), shfl_d(R.o.y, j), shfl_d(R.o.z, j));
+      const d3 d = make3(shfl_d(R.d.x, j), shfl_d(R.d.y, j), shfl_d(R.d.z, j));
+      const double tn = shfl_d(R.tn, j), tf = shfl_d(R.tf, j), st = shfl_d(step, j);
+      const Pcg32 rg{shfl_u64(rng.state, j), shfl_u64(rng.inc, j)};
+      const long long f0 = static_cast<long long>(shfl_u64(static_cast<uint64_t>(first), j));
+      const int rj = __shfl_sync(0xffffffffu, rid, j);
+      const unsigned* bal = march_bal + (warp * 32 + j) * K;
+      long long run = f0;
+      for (int k = 0; k < K; ++k) {
+        const unsigned b = bal[k];
+        if ((b >> lane) & 1u) {
+          const long long pos = run + __popc(b & lanemask_lt());
+          if (pos < A.cap) {
+            const int i = k * 32 + lane;
+            const double t = sample_t(tn, st, i, jitter_at(A, rg, i));
+            double delta;
+            if (i + 1 < A.N) delta = dsub(sample_t(tn, st, i + 1, jitter_at(A, rg, i + 1)), t);
+            else delta = dsub(tf, t);
+            const d3 xn = rigid_apply(A.w2n, add3(o, mul3(d, t)));
+            A.sx[pos] = xn.x;
+            A.sy[pos] = xn.y;
+            A.sz[pos] = xn.z;
+            A.sdelta[pos] = delta;
+            A.sray[pos] = rj;
+            A.sidx[pos] = static_cast<int16_t>(i);
           }
-          run += __popc(b);
         }
+        run += __popc(b);
       }
     }
     __syncthreads();
@@ -833,10 +903,11 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   A.counters = w.counters.ptr;
   A.cap = static_cast<long long>(w.cap_posed);
   if (n_rays > 0) {
-    const long long groups = (n_rays + kMarchWarps - 1) / kMarchWarps;
-    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 8));
+    const long long groups = (n_rays + kMarchWarps * 32 - 1) / (kMarchWarps * 32);
+    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
+    const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
     m.prof.begin("march", s);
-    march_kernel<<<grid, kMarchWarps * 32, 0, s>>>(A);
+    march_kernel<<<grid, kMarchWarps * 32, smem, s>>>(A);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
   }
@@ -897,10 +968,11 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   A.counters = w.counters.ptr;
   A.cap = static_cast<long long>(w.cap_posed);
   if (n_rays > 0) {
-    const long long groups = (n_rays + kMarchWarps - 1) / kMarchWarps;
-    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 8));
+    const long long groups = (n_rays + kMarchWarps * 32 - 1) / (kMarchWarps * 32);
+    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
+    const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
     m.prof.begin("march", s);
-    march_kernel<<<grid, kMarchWarps * 32, 0, s>>>(A);
+    march_kernel<<<grid, kMarchWarps * 32, smem, s>>>(A);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
   }
