@@ -37,7 +37,7 @@ constexpr int kDsMinBlocks = ARFX_DS_MIN_BLOCKS;  // 5 x 128 threads: <= 102 reg
 constexpr int kDsItemChunk = 64;
 constexpr int kItemBoneShift = 26;  // item = target | bone << 26 (targets < 2^26)
 
-enum DsState : int { DS_NEED = 0, DS_ITER = 1, DS_EVAL_INIT = 2, DS_EVAL_LS = 3, DS_DONE = 4 };
+enum DsState : int { DS_NEED = 0, DS_EVAL_INIT = 2, DS_EVAL_LS = 3, DS_DONE = 4 };
 
 __device__ __forceinline__ unsigned ds_lanemask_lt() {
   unsigned m;
@@ -246,52 +246,16 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
   int state = DS_NEED;
   long long s = 0, slot = 0;
   int pose = 0, it = 0, h = 0;
-  d3 xt = make3(0, 0, 0), x = xt, g = xt, step = xt, cand = xt;
-  double gn = 0.0, gcn = 0.0, damp = 1.0;
-  double J0 = 0, J1 = 0, J2 = 0, J3 = 0, J4 = 0, J5 = 0, J6 = 0, J7 = 0, J8 = 0;
+  // loop-carried per-lane state only: the Newton step is taken eagerly right after the eval
+  // that accepted x, so g and J (12 doubles) live within one trip; for DS_EVAL_INIT, x holds
+  // the start point x0 until its eval completes
+  d3 xt = make3(0, 0, 0), x = xt, step = xt;
+  double gn = 0.0, damp = 1.0;
   long long q_next = 0, q_end = 0;  // warp-uniform item queue
 
   while (true) {
-    // ---- A: bring every lane to an eval (or DONE) ----
-    while (true) {
-      bool emit = false, conv = false;
-      if (state == DS_ITER) {  // Newton step with the frozen Jacobian (R/math.hpp:141-158)
-        if (it >= opt.max_iterations) {
-          emit = true;
-        } else {
-          const double c0 = dsub(dmul(J4, J8), dmul(J5, J7));
-          const double c1 = dsub(dmul(J3, J8), dmul(J5, J6));
-          const double c2 = dsub(dmul(J3, J7), dmul(J4, J6));
-          const double det = dadd(dsub(dmul(J0, c0), dmul(J1, c1)), dmul(J2, c2));
-          if (fabs(det) < 2.2250738585072014e-308 * 64) {
-            emit = true;  // singular: the start fails (R/articulation.hpp:114-118)
-          } else {
-            if (kStats) ++st_i;
-            const double id = ddiv(1.0, det);
-            const double i0 = dmul(c0, id);
-            const double i1 = dmul(dsub(dmul(J2, J7), dmul(J1, J8)), id);
-            const double i2 = dmul(dsub(dmul(J1, J5), dmul(J2, J4)), id);
-            const double i3 = dmul(dsub(dmul(J5, J6), dmul(J3, J8)), id);
-            const double i4 = dmul(dsub(dmul(J0, J8), dmul(J2, J6)), id);
-            const double i5 = dmul(dsub(dmul(J2, J3), dmul(J0, J5)), id);
-            const double i6 = dmul(c2, id);
-            const double i7 = dmul(dsub(dmul(J1, J6), dmul(J0, J7)), id);
-            const double i8 = dmul(dsub(dmul(J0, J4), dmul(J1, J3)), id);
-            step = make3(dadd(dadd(dmul(i0, g.x), dmul(i1, g.y)), dmul(i2, g.z)),
-                         dadd(dadd(dmul(i3, g.x), dmul(i4, g.y)), dmul(i5, g.z)),
-                         dadd(dadd(dmul(i6, g.x), dmul(i7, g.y)), dmul(i8, g.z)));
-            damp = 1.0;
-            h = 0;
-            cand = sub3(x, mul3(step, damp));
-            state = DS_EVAL_LS;
-          }
-        }
-      }
-      if (emit) {  // failed start
-        res[slot] = make_double4(0.0, 0.0, 0.0, -1.0);
-        state = DS_NEED;
-      }
-      (void)conv;
+    // ---- A: refill finished lanes from the warp's item queue ----
+    {
       const bool need = state == DS_NEED;
       const unsigned nm = __ballot_sync(0xffffffffu, need);
       if (nm) {
@@ -320,40 +284,37 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
             slot = static_cast<long long>(slot_base[s]) + __popc(mask_in[s] & ((1u << b) - 1u));
             if (slot >= cap) slot = cap;  // overflow: scratch slot (result arrays hold cap + 1)
             xt = src.point(s, pose);
-            cand = rigid_apply((kSinglePose ? Pbase : Pbase + pose)->bone_inv[b], xt);
+            x = rigid_apply((kSinglePose ? Pbase : Pbase + pose)->bone_inv[b], xt);  // x0
             state = DS_EVAL_INIT;
             if (kStats) ++st_s;
           }
         }
       }
-      if (!__ballot_sync(0xffffffffu, state == DS_ITER || state == DS_NEED)) break;
     }
     if (__all_sync(0xffffffffu, state == DS_DONE)) break;
 
     // ---- B: one skinning eval per busy lane ----
     if (state == DS_EVAL_INIT || state == DS_EVAL_LS) {
-      double Jn[9];
+      const d3 cand = state == DS_EVAL_INIT ? x : sub3(x, mul3(step, damp));
+      d3 g;
+      double gcn, Jn[9];
       const int nu = skin_eval(S, kSinglePose ? Pbase : Pbase + pose, cand, xt, ws, stride, g, gcn, Jn);
-      J0 = Jn[0], J1 = Jn[1], J2 = Jn[2], J3 = Jn[3], J4 = Jn[4], J5 = Jn[5], J6 = Jn[6], J7 = Jn[7], J8 = Jn[8];
       if (kStats) {
         ++st_e;
         st_u += static_cast<unsigned long long>(nu);
       }
-    }
-
-    // ---- C: Newton / line-search bookkeeping (R/articulation.hpp:104-142) ----
-    if (state == DS_EVAL_INIT) {
-      x = cand;
-      gn = gcn;
-      if (gn < opt.tolerance) {
-        res[slot] = make_double4(x.x, x.y, x.z, gn);
-        state = DS_NEED;
-      } else {
-        it = 0;
-        state = DS_ITER;
-      }
-    } else if (state == DS_EVAL_LS) {
-      if (gcn < gn || h == 3) {
+      // ---- C: Newton / line-search bookkeeping (R/articulation.hpp:104-142) ----
+      bool iterate = false;
+      if (state == DS_EVAL_INIT) {
+        gn = gcn;
+        if (gn < opt.tolerance) {
+          res[slot] = make_double4(x.x, x.y, x.z, gn);
+          state = DS_NEED;
+        } else {
+          it = 0;
+          iterate = true;
+        }
+      } else if (gcn < gn || h == 3) {
         if (gcn >= gn && gn >= opt.tolerance) {
           res[slot] = make_double4(0.0, 0.0, 0.0, -1.0);  // stalled
           state = DS_NEED;
@@ -365,13 +326,48 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
             res[slot] = make_double4(x.x, x.y, x.z, gn);
             state = DS_NEED;
           } else {
-            state = DS_ITER;
+            iterate = true;
           }
         }
       } else {
         damp = dmul(damp, 0.5);
         ++h;
-        cand = sub3(x, mul3(step, damp));
+      }
+      if (iterate) {  // Newton step with the Jacobian of the accepted eval (R/math.hpp:141-158)
+        bool fail = it >= opt.max_iterations;
+        if (!fail) {
+          const double J0 = Jn[0], J1 = Jn[1], J2 = Jn[2], J3 = Jn[3], J4 = Jn[4], J5 = Jn[5], J6 = Jn[6],
+                       J7 = Jn[7], J8 = Jn[8];
+          const double c0 = dsub(dmul(J4, J8), dmul(J5, J7));
+          const double c1 = dsub(dmul(J3, J8), dmul(J5, J6));
+          const double c2 = dsub(dmul(J3, J7), dmul(J4, J6));
+          const double det = dadd(dsub(dmul(J0, c0), dmul(J1, c1)), dmul(J2, c2));
+          if (fabs(det) < 2.2250738585072014e-308 * 64) {
+            fail = true;  // singular: the start fails (R/articulation.hpp:114-118)
+          } else {
+            if (kStats) ++st_i;
+            const double id = ddiv(1.0, det);
+            const double i0 = dmul(c0, id);
+            const double i1 = dmul(dsub(dmul(J2, J7), dmul(J1, J8)), id);
+            const double i2 = dmul(dsub(dmul(J1, J5), dmul(J2, J4)), id);
+            const double i3 = dmul(dsub(dmul(J5, J6), dmul(J3, J8)), id);
+            const double i4 = dmul(dsub(dmul(J0, J8), dmul(J2, J6)), id);
+            const double i5 = dmul(dsub(dmul(J2, J3), dmul(J0, J5)), id);
+            const double i6 = dmul(c2, id);
+            const double i7 = dmul(dsub(dmul(J1, J6), dmul(J0, J7)), id);
+            const double i8 = dmul(dsub(dmul(J0, J4), dmul(J1, J3)), id);
+            step = make3(dadd(dadd(dmul(i0, g.x), dmul(i1, g.y)), dmul(i2, g.z)),
+                         dadd(dadd(dmul(i3, g.x), dmul(i4, g.y)), dmul(i5, g.z)),
+                         dadd(dadd(dmul(i6, g.x), dmul(i7, g.y)), dmul(i8, g.z)));
+            damp = 1.0;
+            h = 0;
+            state = DS_EVAL_LS;
+          }
+        }
+        if (fail) {
+          res[slot] = make_double4(0.0, 0.0, 0.0, -1.0);
+          state = DS_NEED;
+        }
       }
     }
   }
