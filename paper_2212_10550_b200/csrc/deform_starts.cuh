@@ -252,6 +252,10 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
   d3 xt = make3(0, 0, 0), x = xt, step = xt;
   double gn = 0.0, damp = 1.0;
   long long q_next = 0, q_end = 0;  // warp-uniform item queue
+  // refill granularity: up to kDsItemChunk items per atomic, smaller when the launch has few
+  // items per warp (occupancy grids) so the work spreads over all warps instead of a few
+  const long long n_warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const long long chunk = max(1LL, min(static_cast<long long>(kDsItemChunk), n / (8 * n_warps)));
 
   while (true) {
     // ---- A: refill finished lanes from the warp's item queue ----
@@ -268,11 +272,12 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
           q_next += k;
         } else {
           long long base = 0;
-          if (lane == 0) base = static_cast<long long>(atomicAdd(cursor, static_cast<unsigned long long>(kDsItemChunk)));
+          const long long take = max(chunk, static_cast<long long>(k) - avail);  // >= the lanes still short
+          if (lane == 0) base = static_cast<long long>(atomicAdd(cursor, static_cast<unsigned long long>(take)));
           base = __shfl_sync(0xffffffffu, base, 0);
           id = r < avail ? q_next + r : base + (r - avail);
           q_next = base + (k - avail);
-          q_end = base + kDsItemChunk;
+          q_end = base + take;
         }
         if (need) {
           if (id >= n) {
