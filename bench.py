@@ -360,6 +360,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
                      "traffic": traffic.get(name), "peak_source": peak_src, "work": note}
 
     f64src = "fp64 add/mul issue roof measured by bench.py (arfx_pipe_peaks; not in MEASURED_PEAKS.json)"
+    hbm = peaks.get("hbm_gbs")
     f32src = "fp32 add/mul issue roof measured by bench.py (arfx_pipe_peaks)"
     # K2b deformer: 41/eval + 60/union bone + 66/Newton step + 18/start + 7/rejected line-search candidate
     entry("deform", "fp64", 41 * E + 60 * U + 66 * I + 18 * S + 7 * max(E - S - I, 0.0), "TFLOP/s", fp64_peak,
@@ -370,10 +371,14 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     # (the split-bf16 scheme issues 3 MMAs per product and pads the head to N=16: not counted)
     entry("field_tc", "tensor", QT * 12800, "TFLOP/s", peaks.get("bf16_tflops"),
           f"MEASURED_PEAKS.json bf16_tflops ({peak_kind})", "12800 MLP flops/query (algorithmic)")
+    # K3 encode stage of the tcgen05 decoder: 16 levels x 8 corners x 8 B gathered (f32 table)
+    # + 128 B of split-bf16 features written per query; the table is L2-resident (64 MiB)
+    entry("encode_tc", "l2/l1 gathers", QT * (1024 + 128), "GB/s", hbm,
+          f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); gathers are L2-resident, so frac is vs HBM for scale only",
+          "1024 B gathered + 128 B written per query")
     # K1 march: ~80 FP64 per ray + 36 per sample (ray.at, to_normalized, t, cell_of)
     entry("march", "fp64", rays * K * (80 + 36 * N), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64")
     entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
-    hbm = peaks.get("hbm_gbs")
     # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
     entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")

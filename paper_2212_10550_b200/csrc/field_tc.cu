@@ -126,8 +126,9 @@ struct TcSmem {  // byte offsets inside the dynamic smem; each operand = hi plan
   static constexpr int BIAS = B2 + 2 * B2P;                 // b0[64] b1[64] b2[4]
   static constexpr int ACT = BIAS + 1024;                   // per group: hidden 128 x 64 (2 x 16 KB);
   static constexpr int ACT_BYTES = 2 * A1P;                 //   the 128 x 32 features alias its start
-  static constexpr int MBAR = ACT + kGroups * ACT_BYTES;    // u64 [kGroups]
-  static constexpr int TADDR = MBAR + 8 * kGroups;          // u32
+  static constexpr int MBAR = ACT + kGroups * ACT_BYTES;    // u64 [kGroups]: MMA completion
+  static constexpr int LBAR = MBAR + 8 * kGroups;           // u64 [kGroups]: feature-tile load
+  static constexpr int TADDR = LBAR + 8 * kGroups;          // u32
   static constexpr int TOTAL = TADDR + 16;
 };
 
@@ -135,13 +136,56 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kTcTile) : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, const double* __restrict__ px,
-                                                                 const double* __restrict__ py,
-                                                                 const double* __restrict__ pz,
+// Encode stage: thread = query, all 16 levels (warp-uniform level), features split into
+// bf16 hi/lo and stored straight in the UMMA K-major A0 layout of the query's 128-row tile
+// (16 KB per tile in global memory): a warp's 32 consecutive rows are 512 contiguous bytes
+// per 16-B chunk, so the stores coalesce. It runs at much higher occupancy than the fused
+// encode+MMA kernel could (smem-bound there), which is what hides the hash-table gathers;
+// the MMA stage then only streams tiles. (A thread per (query, 4-level chunk) split was
+// measured slower: 4x the FP64 normalisation for no extra gather parallelism.)
+constexpr int kEncThreads = 256;
+#ifndef ARFX_ENC_MIN_BLOCKS
+#define ARFX_ENC_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kEncThreads, ARFX_ENC_MIN_BLOCKS)
+    encode_tiles_kernel(FieldView F, const double* __restrict__ px, const double* __restrict__ py,
+                        const double* __restrict__ pz, const int32_t* __restrict__ owner,
+                        const unsigned long long* n_dev, long long cap, unsigned char* __restrict__ tiles,
+                        unsigned long long* stats) {
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const bool ok = owner[q] >= 0;
+    if (stats) {
+      const unsigned c = __popc(__ballot_sync(__activemask(), ok));
+      if ((threadIdx.x & 31) == 0 && c) atomicAdd(stats + 6, static_cast<unsigned long long>(c));
+    }
+    if (!ok) continue;  // row left as is: rows are independent in the MMAs, its result is dropped
+    double u[3];
+    normalize_point(F, make3(px[q], py[q], pz[q]), u);
+    unsigned char* tile = tiles + (q / kTcTile) * (2 * TcSmem::A0P);
+    const int r = static_cast<int>(q % kTcTile);
+#pragma unroll 1
+    for (int l = 0; l < 16; l += 4) {
+      __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 o = encode_level_f2(F, l + j, u);
+        split_bf16(o.x, hi[2 * j], lo[2 * j]);
+        split_bf16(o.y, hi[2 * j + 1], lo[2 * j + 1]);
+      }
+      *reinterpret_cast<uint4*>(tile + kmaj_off(r, 2 * l, kTcTile)) = *reinterpret_cast<const uint4*>(hi);
+      *reinterpret_cast<uint4*>(tile + TcSmem::A0P + kmaj_off(r, 2 * l, kTcTile)) =
+          *reinterpret_cast<const uint4*>(lo);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, const unsigned char* __restrict__ tiles,
                                                                  const int32_t* __restrict__ owner,
                                                                  float4* __restrict__ res,
-                                                                 const unsigned long long* n_dev, long long cap,
-                                                                 unsigned long long* stats) {
+                                                                 const unsigned long long* n_dev, long long cap) {
   extern __shared__ __align__(1024) unsigned char tc_smem[];
   const int g = threadIdx.x / kTcTile;  // pipeline group
   const int tid = threadIdx.x % kTcTile, warp = tid >> 5;
@@ -152,6 +196,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem));
   float* bias = reinterpret_cast<float*>(tc_smem + TcSmem::BIAS);
   const uint32_t mbar = sbase + TcSmem::MBAR + 8 * g;
+  const uint32_t lbar = sbase + TcSmem::LBAR + 8 * g;
   uint32_t* taddr_smem = reinterpret_cast<uint32_t*>(tc_smem + TcSmem::TADDR);
   const int A1 = TcSmem::ACT + g * TcSmem::ACT_BYTES, A0 = A1;  // byte offsets of this group's tile
 
@@ -186,7 +231,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
     bias[64 + i] = __ldg(b1 + i);
   }
   if (ctid < 4) bias[128 + ctid] = __ldg(b2 + ctid);
-  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lbar) : "memory");
+  }
   if (ctid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbase + TcSmem::TADDR),
                  "n"(kTmemCols)
@@ -199,7 +247,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
   tc_fence_after();
   const uint32_t tmem = *taddr_smem + static_cast<uint32_t>(g * 128);        // this group's columns
   const uint32_t tmem_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);  // this warp's 32 lanes
-  uint32_t phase = 0;
+  uint32_t phase = 0, lphase = 0;
   constexpr uint32_t ID64 = idesc_bf16(128, 64);
   constexpr uint32_t ID16 = idesc_bf16(128, 16);
   // writes row `tid`, columns [c, c+8) of a split operand (hi plane, lo plane)
@@ -213,32 +261,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 
   for (long long t0 = (static_cast<long long>(blockIdx.x) * kGroups + g) * kTcTile; t0 < n;
        t0 += static_cast<long long>(gridDim.x) * kGroups * kTcTile) {
-    // ---- normalized coords per query (registers: thread = query = A row) ----
+    // ---- feature tile (16 KB, hi + lo planes) from the encode stage: one bulk copy ----
     const long long q = t0 + tid;
     const bool ok = q < n && owner[q] >= 0;
-    if (stats) {
-      const unsigned c = __popc(__ballot_sync(0xffffffffu, ok));
-      if ((tid & 31) == 0 && c) atomicAdd(stats + 6, static_cast<unsigned long long>(c));
+    if (tid == 0) {
+      constexpr uint32_t kBytes = 2 * TcSmem::A0P;
+      const unsigned char* src = tiles + (t0 / kTcTile) * kBytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lbar), "n"(kBytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sbase + A0),
+          "l"(src), "n"(kBytes), "r"(lbar)
+          : "memory");
     }
-    double u[3] = {0.0, 0.0, 0.0};
-    if (ok) normalize_point(F, make3(px[q], py[q], pz[q]), u);
-    // ---- encode into A0 (warp-uniform level, thread = query) ----
-    {
-#pragma unroll 1
-      for (int l = 0; l < 16; l += 4) {
-        float f[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 o = make_float2(0.f, 0.f);
-          if (ok) o = encode_level_f2(F, l + j, u);
-          f[2 * j] = o.x;
-          f[2 * j + 1] = o.y;
-        }
-        put8(A0, TcSmem::A0P, 2 * l, f);
-      }
-    }
-    fence_async_smem();
-    group_sync(g);
+    mbar_wait(lbar, lphase);
+    lphase ^= 1;
     // ---- layer 0 ----
     if (tid == 0) {
       tc_fence_after();
@@ -329,11 +365,19 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   // persistent: one CTA per SM (it owns all 512 TMEM columns)
   const long long tiles = (n_hint + kTcTile * kGroups - 1) / (kTcTile * kGroups);
   const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));
+  const size_t tile_bytes = static_cast<size_t>(2 * TcSmem::A0P);
+  m.ws.tc_tiles.ensure(static_cast<size_t>((m.ws.cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
+  m.prof.begin("encode_tc", s);
+  encode_tiles_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n_hint + 255) / 256,
+                                                                                       static_cast<long long>(sms) * 16))),
+                        kEncThreads, 0, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
+                                     m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool), m.ws.tc_tiles.ptr,
+                                     m.stats_on ? m.stats.ptr : nullptr);
+  ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
   m.prof.begin("field_tc", s);
-  field_tc_kernel<<<grid, kTcThreads, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
-                                              m.ws.pres.ptr, m.ws.counters.ptr + 2,
-                                              static_cast<long long>(m.ws.cap_pool),
-                                              m.stats_on ? m.stats.ptr : nullptr);
+  field_tc_kernel<<<grid, kTcThreads, smem, s>>>(m.fv, m.ws.tc_tiles.ptr, m.ws.powner.ptr, m.ws.pres.ptr,
+                                              m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool));
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }

@@ -64,6 +64,7 @@ struct Workspace {
   DevBuf<float4> pres;                // (density, r, g, b) per pool entry
   DevBuf<int32_t> ray_first, ray_count, row_list;
   DevBuf<double> train_terms;          // fused-loss per-ray terms
+  DevBuf<unsigned char> tc_tiles;      // tcgen05 decoder: split-bf16 feature tiles (16 KB / 128 queries)
   DevBuf<double> dens_pts;             // L_density points (SoA)
   DevBuf<uint8_t> dens_empty;          // point lies in an empty occupancy cell
   DevBuf<float> dens_scale;            // w_density / n_empty
