@@ -491,11 +491,13 @@ __global__ void __launch_bounds__(256) finalize_roots_kernel(Src src, const uint
     Roots R;
     ds_gather_roots(s, mask_in, slot_base, res, dedup, R, cap);
     K.counts[s] = R.count;
-    for (int k = 0; k < R.count; ++k) {
-      K.roots[(s * kMaxRoots + k) * 3 + 0] = R.x[k][0];
-      K.roots[(s * kMaxRoots + k) * 3 + 1] = R.x[k][1];
-      K.roots[(s * kMaxRoots + k) * 3 + 2] = R.x[k][2];
-      K.resid[s * kMaxRoots + k] = R.r[k];
+    // unused slots are zero, as the reference's value-initialised InverseRoots arrays
+    for (int k = 0; k < kMaxRoots; ++k) {
+      const bool u = k < R.count;
+      K.roots[(s * kMaxRoots + k) * 3 + 0] = u ? R.x[k][0] : 0.0;
+      K.roots[(s * kMaxRoots + k) * 3 + 1] = u ? R.x[k][1] : 0.0;
+      K.roots[(s * kMaxRoots + k) * 3 + 2] = u ? R.x[k][2] : 0.0;
+      K.resid[s * kMaxRoots + k] = u ? R.r[k] : 0.0;
     }
   }
 }
