@@ -30,6 +30,9 @@
 namespace arfx {
 
 constexpr int kDsThreads = 128;
+#ifndef ARFX_NEWTON_POSE_SMEM
+#define ARFX_NEWTON_POSE_SMEM 1
+#endif
 #ifndef ARFX_DS_MIN_BLOCKS
 #define ARFX_DS_MIN_BLOCKS 5
 #endif
@@ -235,8 +238,16 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
                                                                   unsigned long long* cursor,
                                                                   unsigned long long* stats, long long cap) {
   extern __shared__ double ds_smem[];
+#if ARFX_NEWTON_POSE_SMEM
   const PoseCtx* Pbase = ds_stage_pose<kSinglePose>(poses, ds_smem);
   double* ws = ds_smem + (kSinglePose ? (sizeof(PoseCtx) + 7) / 8 : 0) + threadIdx.x;
+#else
+  // the PoseContext is read through L1 (one cached copy per SM) instead of a per-block smem
+  // copy: smem per block is only the union-bone scratch, which leaves L1 more room for the
+  // skinning cell table gathers
+  const PoseCtx* Pbase = poses;
+  double* ws = ds_smem + threadIdx.x;
+#endif
   const int stride = blockDim.x;
   const int lane = threadIdx.x & 31;
   long long n = static_cast<long long>(*n_items);

@@ -727,7 +727,8 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
   // per-thread union-bone scratch: the widest cell union (build_cell_table), not n_bones
-  const size_t smem = pose_smem + static_cast<size_t>(m.max_union) * kDsThreads * sizeof(double);
+  const size_t smem = (ARFX_NEWTON_POSE_SMEM ? pose_smem : 0) +
+                      static_cast<size_t>(m.max_union) * kDsThreads * sizeof(double);
   auto kern = stats ? start_newton_kernel<Src, single, true> : start_newton_kernel<Src, single, false>;
   const int grid = persistent_grid(kern, kDsThreads, smem, 2 * n);
   m.prof.begin(name, s);
