@@ -81,6 +81,8 @@ struct Workspace {
   DevBuf<double> strans;   // transmittance before each posed sample
   DevBuf<float> pgs, pgc;  // per pool entry: dsigma, dcolor[3]
   DevBuf<uint8_t> pflag;   // per pool entry: query_backward needed
+  DevBuf<float> bwd_rec;   // K8a -> K8b: per flagged query, MLP layer inputs and deltas
+  DevBuf<unsigned long long> bwd_n;
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
   size_t learned_starts = 0;  // raised when a frame overflowed the start slots

@@ -28,7 +28,6 @@ namespace arfx {
 namespace {
 
 constexpr int kMarchWarps = 8;
-constexpr int kMaxN = 1024;  // samples per ray handled by the march kernel
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

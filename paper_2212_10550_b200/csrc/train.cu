@@ -150,64 +150,73 @@ __global__ void train_composite_kernel(TrainCompositeArgs A) {
 constexpr int kFbThreads = 64;
 constexpr int kIn = 32, kHid = 64, kOut = 4;
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
-// K8. Activations per thread live in smem as [k][thread] (conflict-free):
-//   X[32] input features, H1[64], H2[64], D[64] (gradient scratch).
-__global__ void __launch_bounds__(kFbThreads) field_backward_kernel(FieldView F, const double* __restrict__ px,
-                                                                    const double* __restrict__ py,
-                                                                    const double* __restrict__ pz,
-                                                                    const uint8_t* __restrict__ pflag,
-                                                                    const float* __restrict__ pgs,
-                                                                    const float* __restrict__ pgc,
-                                                                    const unsigned long long* n_dev, long long cap,
-                                                                    float* __restrict__ grid_grad,
-                                                                    float* __restrict__ mlp_grad) {
+// K8a: one thread per flagged pool entry (query): exact forward recompute (encode + MLP
+// in the reference's summation order, activations in smem as [k][thread], conflict-free),
+// then the per-query half of DecoderMlp::backward (R/mlp.hpp:116-154): logit deltas, the
+// dprev chains through ReLU masks, the hash-grid scatter (R/hash_grid.hpp:155-169, f32
+// atomics). The operands of the weight gradients (inputs and deltas of each layer) go to a
+// compacted per-query record; K8b reduces them over queries.
+constexpr int kBwdRec = kIn + kHid + kHid + kOut + kHid + kHid;  // X, H1, H2, u2, dh2, dh1 = 292 floats
+constexpr int kRecX = 0, kRecH1 = kIn, kRecH2 = kIn + kHid, kRecU2 = kIn + 2 * kHid, kRecD2 = kRecU2 + kOut,
+              kRecD1 = kRecD2 + kHid;
+
+__global__ void __launch_bounds__(kFbThreads) field_bwd_query_kernel(FieldView F, const double* __restrict__ px,
+                                                                     const double* __restrict__ py,
+                                                                     const double* __restrict__ pz,
+                                                                     const uint8_t* __restrict__ pflag,
+                                                                     const float* __restrict__ pgs,
+                                                                     const float* __restrict__ pgc,
+                                                                     const unsigned long long* n_dev, long long cap,
+                                                                     float* __restrict__ grid_grad,
+                                                                     float* __restrict__ rec, long long rec_cap,
+                                                                     unsigned long long* n_rec) {
   extern __shared__ float fb_smem[];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
   float* X = fb_smem;                    // [kIn][kFbThreads]
   float* H1 = X + kIn * kFbThreads;      // [kHid][kFbThreads]
   float* H2 = H1 + kHid * kFbThreads;    // [kHid][kFbThreads]
   float* D = H2 + kHid * kFbThreads;     // [kHid][kFbThreads]
-  const float* W = F.mlp;
-  const float* W0 = W;
+  const float* W0 = F.mlp;
   const float* B0 = W0 + kIn * kHid;
   const float* W1 = B0 + kHid;
   const float* B1 = W1 + kHid * kHid;
   const float* W2 = B1 + kHid;
   const float* B2 = W2 + kOut * kHid;
-  float* gW0 = mlp_grad;
-  float* gB0 = gW0 + kIn * kHid;
-  float* gW1 = gB0 + kHid;
-  float* gB1 = gW1 + kHid * kHid;
-  float* gW2 = gB1 + kHid;
-  float* gB2 = gW2 + kOut * kHid;
   long long n = static_cast<long long>(*n_dev);
   n = n < cap ? n : cap;
   for (long long base = static_cast<long long>(blockIdx.x) * kFbThreads; base < n;
        base += static_cast<long long>(gridDim.x) * kFbThreads) {
     const long long q = base + t;
     const bool act = q < n && pflag[q] != 0;
-    const d3 x = act ? make3(px[q], py[q], pz[q]) : make3(0, 0, 0);
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (!am) continue;  // warp-uniform: the whole warp skips unflagged stretches of the pool
+    long long slot = 0;
+    if (lane == 0) slot = static_cast<long long>(atomicAdd(n_rec, static_cast<unsigned long long>(__popc(am))));
+    slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(am & ((1u << lane) - 1u));
+    if (!act) continue;
+    float* R = rec + (slot < rec_cap ? slot : rec_cap) * kBwdRec;  // rec holds rec_cap + 1 records
+    const d3 x = make3(px[q], py[q], pz[q]);
     // ---- forward recompute (CanonicalField::query_backward re-runs the forward) ----
     float feats[kIn];
-    if (act) hash_encode_f2(F, x, feats);
-    else
-      for (int i = 0; i < kIn; ++i) feats[i] = 0.0f;
-    for (int i = 0; i < kIn; ++i) X[i * kFbThreads + t] = feats[i];
+    hash_encode_f2(F, x, feats);
+    for (int i = 0; i < kIn; ++i) {
+      X[i * kFbThreads + t] = feats[i];
+      R[kRecX + i] = feats[i];
+    }
     for (int o = 0; o < kHid; ++o) {
       float a = B0[o];
       for (int i = 0; i < kIn; ++i) a = fadd(a, fmul(__ldg(W0 + o * kIn + i), feats[i]));
-      H1[o * kFbThreads + t] = (a < 0.0f) ? 0.0f : a;
+      const float h = (a < 0.0f) ? 0.0f : a;
+      H1[o * kFbThreads + t] = h;
+      R[kRecH1 + o] = h;
     }
     for (int o = 0; o < kHid; ++o) {
       float a = B1[o];
       for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(__ldg(W1 + o * kHid + i), H1[i * kFbThreads + t]));
-      H2[o * kFbThreads + t] = (a < 0.0f) ? 0.0f : a;
+      const float h = (a < 0.0f) ? 0.0f : a;
+      H2[o * kFbThreads + t] = h;
+      R[kRecH2 + o] = h;
     }
     float lg[kOut];
     for (int o = 0; o < kOut; ++o) {
@@ -216,82 +225,103 @@ __global__ void __launch_bounds__(kFbThreads) field_backward_kernel(FieldView F,
       lg[o] = a;
     }
     // ---- d logits (R/field.hpp:95-99) ----
-    float u2[kOut] = {0.f, 0.f, 0.f, 0.f};
-    if (act) {
-      u2[0] = fmul(pgs[q], logistic_f(lg[0]));
-      for (int c = 0; c < 3; ++c) {
-        const float v = logistic_f(lg[1 + c]);
-        u2[1 + c] = fmul(fmul(pgc[3 * q + c], v), __fsub_rn(1.0f, v));
-      }
+    float u2[kOut];
+    u2[0] = fmul(pgs[q], logistic_f(lg[0]));
+    for (int c = 0; c < 3; ++c) {
+      const float v = logistic_f(lg[1 + c]);
+      u2[1 + c] = fmul(fmul(pgc[3 * q + c], v), __fsub_rn(1.0f, v));
     }
-    // ---- output layer backward: gb2 += u; gW2 += u*h2; dprev = sum_o u*W2 (u != 0) ----
+    for (int o = 0; o < kOut; ++o) R[kRecU2 + o] = u2[o];
+    // ---- dprev through the output layer (u != 0 only), ReLU mask of hidden layer 2 ----
     for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = 0.0f;
     for (int o = 0; o < kOut; ++o) {
       const float u = u2[o];
-      const float sb = warp_sum(u);
-      if ((t & 31) == 0 && sb != 0.0f) atomicAdd(gB2 + o, sb);
-      for (int i = 0; i < kHid; ++i) {
-        const float g = warp_sum(fmul(u, H2[i * kFbThreads + t]));
-        if ((t & 31) == 0 && g != 0.0f) atomicAdd(gW2 + o * kHid + i, g);
-      }
       if (u != 0.0f)
         for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = fadd(D[i * kFbThreads + t], fmul(u, __ldg(W2 + o * kHid + i)));
     }
-    // ReLU mask on hidden layer 2 (post == 0), then the gradient w.r.t. h2 lives in H2
     for (int i = 0; i < kHid; ++i) {
-      const float d = D[i * kFbThreads + t];
-      H2[i * kFbThreads + t] = (H2[i * kFbThreads + t] == 0.0f) ? 0.0f : d;
+      const float d = (H2[i * kFbThreads + t] == 0.0f) ? 0.0f : D[i * kFbThreads + t];
+      H2[i * kFbThreads + t] = d;  // H2 now holds d h2
+      R[kRecD2 + i] = d;
     }
-    // ---- hidden layer 1 backward (input = h1) ----
+    // ---- hidden layer 1 ----
     for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = 0.0f;
     for (int o = 0; o < kHid; ++o) {
       const float u = H2[o * kFbThreads + t];
-      const float sb = warp_sum(u);
-      if ((t & 31) == 0 && sb != 0.0f) atomicAdd(gB1 + o, sb);
-      if (__any_sync(0xffffffffu, u != 0.0f)) {
-        for (int i = 0; i < kHid; ++i) {
-          const float g = warp_sum(fmul(u, H1[i * kFbThreads + t]));
-          if ((t & 31) == 0 && g != 0.0f) atomicAdd(gW1 + o * kHid + i, g);
-        }
-      }
       if (u != 0.0f)
         for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = fadd(D[i * kFbThreads + t], fmul(u, __ldg(W1 + o * kHid + i)));
     }
     for (int i = 0; i < kHid; ++i) {
-      const float d = D[i * kFbThreads + t];
-      H1[i * kFbThreads + t] = (H1[i * kFbThreads + t] == 0.0f) ? 0.0f : d;
+      const float d = (H1[i * kFbThreads + t] == 0.0f) ? 0.0f : D[i * kFbThreads + t];
+      H1[i * kFbThreads + t] = d;  // H1 now holds d h1
+      R[kRecD1 + i] = d;
     }
-    // ---- first layer backward (input = features) -> d features ----
+    // ---- first layer -> d features ----
     float din[kIn];
     for (int i = 0; i < kIn; ++i) din[i] = 0.0f;
     for (int o = 0; o < kHid; ++o) {
       const float u = H1[o * kFbThreads + t];
-      const float sb = warp_sum(u);
-      if ((t & 31) == 0 && sb != 0.0f) atomicAdd(gB0 + o, sb);
-      if (__any_sync(0xffffffffu, u != 0.0f)) {
-        for (int i = 0; i < kIn; ++i) {
-          const float g = warp_sum(fmul(u, X[i * kFbThreads + t]));
-          if ((t & 31) == 0 && g != 0.0f) atomicAdd(gW0 + o * kIn + i, g);
-        }
-      }
       if (u != 0.0f)
         for (int i = 0; i < kIn; ++i) din[i] = fadd(din[i], fmul(u, __ldg(W0 + o * kIn + i)));
     }
     // ---- encode backward (R/hash_grid.hpp:155-169) ----
-    if (act) {
-      double u[3];
-      normalize_point(F, x, u);
-      for (int l = 0; l < F.L; ++l) {
-        LevelCorners lc;
-        level_corners(F, l, u, lc);
-        float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
-        for (int k = 0; k < 8; ++k) {
-          const float w = lc.w[k];
-          if (w == 0.0f) continue;
-          atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 0, fmul(w, din[2 * l + 0]));
-          atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 1, fmul(w, din[2 * l + 1]));
-        }
+    double uu[3];
+    normalize_point(F, x, uu);
+    for (int l = 0; l < F.L; ++l) {
+      LevelCorners lc;
+      level_corners(F, l, uu, lc);
+      float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
+      for (int k = 0; k < 8; ++k) {
+        const float w = lc.w[k];
+        if (w == 0.0f) continue;
+        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 0, fmul(w, din[2 * l + 0]));
+        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 1, fmul(w, din[2 * l + 1]));
       }
+    }
+  }
+}
+
+// K8b: MLP weight / bias gradients, gW[o][i] = sum_q delta[q][o] * in[q][i] and gb[o] =
+// sum_q delta[q][o], over the K8a records: a block stages kWq records in smem (row-major,
+// so threads walking i read consecutive words) and each thread owns a strided set of the
+// 6,532 parameters; one f32 atomic per parameter per block.
+constexpr int kWq = 32;
+constexpr int kWThreads = 256;
+__global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const float* __restrict__ rec,
+                                                                      const unsigned long long* n_rec,
+                                                                      long long rec_cap,
+                                                                      float* __restrict__ mlp_grad) {
+  __shared__ float S[kWq][kBwdRec + 1];
+  long long n = static_cast<long long>(*n_rec);
+  n = n < rec_cap ? n : rec_cap;
+  constexpr int kW0 = kHid * kIn, kB0 = kW0 + kHid, kW1 = kB0 + kHid * kHid, kB1 = kW1 + kHid,
+                kW2 = kB1 + kOut * kHid, kB2 = kW2 + kOut;
+  for (long long c0 = static_cast<long long>(blockIdx.x) * kWq; c0 < n; c0 += static_cast<long long>(gridDim.x) * kWq) {
+    const int nq = static_cast<int>(n - c0 < kWq ? n - c0 : kWq);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nq * kBwdRec; e += kWThreads) S[e / kBwdRec][e % kBwdRec] = rec[c0 * kBwdRec + e];
+    __syncthreads();
+    for (int p = threadIdx.x; p < kB2; p += kWThreads) {
+      int dOff, iOff, o, i;  // delta offset / input offset (-1: bias)
+      if (p < kW0) {
+        o = p / kIn, i = p % kIn, dOff = kRecD1, iOff = kRecX;
+      } else if (p < kB0) {
+        o = p - kW0, i = 0, dOff = kRecD1, iOff = -1;
+      } else if (p < kW1) {
+        o = (p - kB0) / kHid, i = (p - kB0) % kHid, dOff = kRecD2, iOff = kRecH1;
+      } else if (p < kB1) {
+        o = p - kW1, i = 0, dOff = kRecD2, iOff = -1;
+      } else if (p < kW2) {
+        o = (p - kB1) / kHid, i = (p - kB1) % kHid, dOff = kRecU2, iOff = kRecH2;
+      } else {
+        o = p - kW2, i = 0, dOff = kRecU2, iOff = -1;
+      }
+      float acc = 0.0f;
+      if (iOff >= 0)
+        for (int qq = 0; qq < nq; ++qq) acc = fadd(acc, fmul(S[qq][dOff + o], S[qq][iOff + i]));
+      else
+        for (int qq = 0; qq < nq; ++qq) acc = fadd(acc, S[qq][dOff + o]);
+      if (acc != 0.0f) atomicAdd(mlp_grad + p, acc);
     }
   }
 }
@@ -312,14 +342,23 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   const size_t smem = static_cast<size_t>(kIn + 3 * kHid) * kFbThreads * sizeof(float);
   static bool attr = false;
   if (!attr) {
-    ARFX_CUDA(cudaFuncSetAttribute(field_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ARFX_CUDA(cudaFuncSetAttribute(field_bwd_query_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     attr = true;
   }
+  Workspace& w = m.ws;
+  const long long rec_cap = cap;
+  w.bwd_rec.ensure(static_cast<size_t>(rec_cap + 1) * kBwdRec);
+  w.bwd_n.ensure(1);
+  ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
   const long long blocks = std::min<long long>((cap + kFbThreads - 1) / kFbThreads, static_cast<long long>(sms()) * 8);
   m.prof.begin("field_backward", s);
-  field_backward_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), kFbThreads, smem, s>>>(
-      m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, flag, gs, gc, d_n, cap, m.grid_grad.ptr, m.mlp_grad.ptr);
+  field_bwd_query_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), kFbThreads, smem, s>>>(
+      m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, flag, gs, gc, d_n, cap, m.grid_grad.ptr, w.bwd_rec.ptr, rec_cap,
+      w.bwd_n.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  field_bwd_weights_kernel<<<static_cast<unsigned>(sms() * 4), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
+                                                                                m.mlp_grad.ptr);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
