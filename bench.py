@@ -552,10 +552,10 @@ def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
         dist.barrier(group)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0 = model.counters.posed_queries
-    e0.record()
+    e0.record(tr.stream)  # the trainer's stream carries every step
     for _ in range(steps):
         tr.step()
-    e1.record()
+    e1.record(tr.stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:

@@ -304,7 +304,9 @@ int arfx_train_step(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_
                     const float* gt_rgb, const float* gt_alpha, const arfx_loss_config* cfg, double* loss4,
                     float* rgb, float* alpha, arfx_counters* c, void* stream);
 /* The same on device arrays (d_loss4: 4 doubles on the device; d_rgb/d_alpha may be NULL).
- * Enqueued on `stream`; the host waits only for the workspace-overflow check. */
+ * Fully asynchronous on `stream` (n_rays * samples_per_ray <= 2^22): workspace capacity is
+ * reserved for the worst case instead of checked on the host; pixel coordinates are not
+ * range-checked (an out-of-image pixel yields its ray, no out-of-bounds access). */
 int arfx_train_step_device(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
                            const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
                            const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,

@@ -1287,8 +1287,25 @@ void validate_train(arfx_model mh, arfx_pose ph, const arfx_render_options* opt,
 // model's flat gradient vector. Returns the posed/canonical counters.
 void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, const arfx_render_options* opt,
                long long n_rays, const int32_t* d_px, const int32_t* d_py, const float* d_dC, const float* d_dA,
-               const LossTargets* lt, float* d_rgb, float* d_alpha, cudaStream_t s, unsigned long long* hcnt) {
+               const LossTargets* lt, float* d_rgb, float* d_alpha, cudaStream_t s, unsigned long long* hcnt,
+               bool host_sync = true) {
   ensure_grad_store(m, s);
+  const long long posed_max = n_rays * std::max(opt->samples_per_ray, 1);
+  if (!host_sync && posed_max <= (1LL << 22)) {
+    // no host round trip: capacities for the worst case (every sample occupied, every root
+    // and start kept), so nothing can overflow; pixels are not range-checked here (an
+    // out-of-image pixel only yields a ray through it, no out-of-bounds access)
+    m.ws.reserve_worst(static_cast<size_t>(posed_max), static_cast<size_t>(m.sv.nb));
+    train_forward(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0, opt->seed, opt->frame_id, n_rays, d_px,
+                  d_py, s);
+    Workspace& w = m.ws;
+    w.ensure_train();
+    ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
+    train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
+    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
+                        w.pgc.ptr, s);
+    return;
+  }
   DevBuf<unsigned long long> bad;
   bad.alloc(1);
   ARFX_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(unsigned long long), s));
@@ -1472,15 +1489,21 @@ int arfx_train_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, 
     LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
     unsigned long long hcnt[8];
     run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, d_px, d_py, nullptr, nullptr, &lt,
-              d_rgb ? d_rgb : w.train_rgb.ptr, d_alpha ? d_alpha : w.train_alpha.ptr, s, hcnt);
+              d_rgb ? d_rgb : w.train_rgb.ptr, d_alpha ? d_alpha : w.train_alpha.ptr, s, hcnt, /*host_sync=*/false);
     loss_reduce(w.train_terms.ptr, n_rays, lt, d_loss4, s);
   });
 }
 
 namespace {
 void run_density(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step, double w,
-                 double* d_out2, cudaStream_t s) {
+                 double* d_out2, cudaStream_t s, bool host_sync = true) {
   ensure_grad_store(m, s);
+  if (!host_sync && n <= (1LL << 22)) {  // worst-case capacities: no overflow check needed
+    m.ws.reserve_worst(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb));
+    density_forward(m, p, g, n, seed, step, s);
+    density_backward(m, n, w, d_out2, s);
+    return;
+  }
   for (int attempt = 0;; ++attempt) {
     density_forward(m, p, g, n, seed, step, s);
     unsigned long long hc[8];
@@ -1525,7 +1548,8 @@ int arfx_density_step_device(arfx_model mh, arfx_pose ph, arfx_occ_grid occ, int
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
     if (n_points <= 0) return;
-    run_density(m, ph->impl, occ->impl, n_points, seed, step, lt.w_density, d_loss2, stream_of(m, stream));
+    run_density(m, ph->impl, occ->impl, n_points, seed, step, lt.w_density, d_loss2, stream_of(m, stream),
+                /*host_sync=*/false);
   });
 }
 

@@ -82,9 +82,11 @@ struct Workspace {
   DevBuf<float> pgs, pgc;  // per pool entry: dsigma, dcolor[3]
   DevBuf<uint8_t> pflag;   // per pool entry: query_backward needed
   DevBuf<float> bwd_rec;   // K8a -> K8b: per flagged query, MLP layer inputs and deltas
+  DevBuf<int32_t> bwd_list;  // flagged pool entries, compacted
   DevBuf<unsigned long long> bwd_n;
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
+  void reserve_worst(size_t targets, size_t n_bones);
   size_t learned_starts = 0;  // raised when a frame overflowed the start slots
   void ensure_starts(size_t targets, size_t nkeys, size_t min_starts = 0);
   void ensure_train();

@@ -111,6 +111,7 @@ struct MarchArgs {
   int32_t *ray_first, *ray_count;
   unsigned long long* counters;
   long long cap;
+  int rpw;  // rays per warp (1..32): small ray lists (training) spread over more warps
 };
 
 __device__ __forceinline__ double jitter_at(const MarchArgs& A, Pcg32 base, int i) {
@@ -138,11 +139,11 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_rays = A.lpx ? A.n_list : static_cast<long long>(A.n_rows) * A.W;
   const int K = (A.N + 31) >> 5;
-  constexpr int kRays = kMarchWarps * 32;
+  const int kRays = kMarchWarps * A.rpw;
   for (long long g0 = static_cast<long long>(blockIdx.x) * kRays; g0 < n_rays;
        g0 += static_cast<long long>(gridDim.x) * kRays) {
-    // ---- this lane's ray
-    const long long r = g0 + threadIdx.x;
+    // ---- this lane's ray (lanes >= rpw hold none)
+    const long long r = lane < A.rpw ? g0 + warp * A.rpw + lane : n_rays;
     int pix = -1, rid = -1;  // pix keys the RNG stream (R/render.hpp:201); rid indexes outputs
     RayGeom R{};
     double step = 0.0;
@@ -813,6 +814,22 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
   }
 }
 
+// Worst-case reservation for a call that must not synchronise with the host: `targets`
+// posed points can produce at most kMaxRoots pool entries and n_bones starts each.
+void Workspace::reserve_worst(size_t targets, size_t n_bones) {
+  ensure(std::max(targets, cap_posed), 0);
+  const size_t pool = targets * kMaxRoots + 1024;
+  if (pool > cap_pool) {
+    px.alloc(pool);
+    py.alloc(pool);
+    pz.alloc(pool);
+    powner.alloc(pool);
+    pres.alloc(pool);
+    cap_pool = pool;
+  }
+  learned_starts = std::max(learned_starts, targets * n_bones + 1024);
+}
+
 void Workspace::ensure(size_t posed, size_t pix) {
   if (posed > cap_posed) {
     const size_t c = posed;
@@ -903,7 +920,9 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   A.counters = w.counters.ptr;
   A.cap = static_cast<long long>(w.cap_posed);
   if (n_rays > 0) {
-    const long long groups = (n_rays + kMarchWarps * 32 - 1) / (kMarchWarps * 32);
+    A.rpw = static_cast<int>(std::min<long long>(
+        32, std::max<long long>(1, (n_rays + sm_count() * 4LL * kMarchWarps - 1) / (sm_count() * 4LL * kMarchWarps))));
+    const long long groups = (n_rays + kMarchWarps * A.rpw - 1) / (kMarchWarps * A.rpw);
     const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
     const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
     m.prof.begin("march", s);
@@ -968,7 +987,9 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   A.counters = w.counters.ptr;
   A.cap = static_cast<long long>(w.cap_posed);
   if (n_rays > 0) {
-    const long long groups = (n_rays + kMarchWarps * 32 - 1) / (kMarchWarps * 32);
+    A.rpw = static_cast<int>(std::min<long long>(
+        32, std::max<long long>(1, (n_rays + sm_count() * 4LL * kMarchWarps - 1) / (sm_count() * 4LL * kMarchWarps))));
+    const long long groups = (n_rays + kMarchWarps * A.rpw - 1) / (kMarchWarps * A.rpw);
     const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
     const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
     m.prof.begin("march", s);

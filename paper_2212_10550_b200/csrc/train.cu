@@ -147,137 +147,209 @@ __global__ void train_composite_kernel(TrainCompositeArgs A) {
   }
 }
 
-constexpr int kFbThreads = 64;
 constexpr int kIn = 32, kHid = 64, kOut = 4;
 
 
-// K8a: one thread per flagged pool entry (query): exact forward recompute (encode + MLP
-// in the reference's summation order, activations in smem as [k][thread], conflict-free),
-// then the per-query half of DecoderMlp::backward (R/mlp.hpp:116-154): logit deltas, the
-// dprev chains through ReLU masks, the hash-grid scatter (R/hash_grid.hpp:155-169, f32
-// atomics). The operands of the weight gradients (inputs and deltas of each layer) go to a
-// compacted per-query record; K8b reduces them over queries.
+// K8a: one 64-thread team per flagged pool entry (query), 4 teams per block, the decoder
+// weights staged once per block in smem (rows padded: conflict-free both for row-wise
+// forward dots and column-wise backward dots). Thread l < 16 encodes level l; thread o
+// computes hidden unit o of each layer with its inputs in the reference's order, so the
+// forward recompute is bit-identical to K3's; the backward dprev chains (R/mlp.hpp:116-154,
+// u != 0 only, ReLU mask where post == 0) run one output per thread in the reference's
+// o-order; thread l < 16 scatters level l of the encode backward (R/hash_grid.hpp:155-169,
+// f32 atomics). The layer inputs and deltas go to a per-query record for K8b.
 constexpr int kBwdRec = kIn + kHid + kHid + kOut + kHid + kHid;  // X, H1, H2, u2, dh2, dh1 = 292 floats
 constexpr int kRecX = 0, kRecH1 = kIn, kRecH2 = kIn + kHid, kRecU2 = kIn + 2 * kHid, kRecD2 = kRecU2 + kOut,
               kRecD1 = kRecD2 + kHid;
+constexpr int kTeam = 64, kTeams = 4, kTeamThreads = kTeam * kTeams;
+constexpr int kTeamSmem = kBwdRec + kOut + kIn;  // record + logits + d features
+constexpr int kW0s = kIn + 1, kW1s = kHid + 1;  // padded row strides
 
-__global__ void __launch_bounds__(kFbThreads) field_bwd_query_kernel(FieldView F, const double* __restrict__ px,
-                                                                     const double* __restrict__ py,
-                                                                     const double* __restrict__ pz,
-                                                                     const uint8_t* __restrict__ pflag,
-                                                                     const float* __restrict__ pgs,
-                                                                     const float* __restrict__ pgc,
-                                                                     const unsigned long long* n_dev, long long cap,
-                                                                     float* __restrict__ grid_grad,
-                                                                     float* __restrict__ rec, long long rec_cap,
-                                                                     unsigned long long* n_rec) {
-  extern __shared__ float fb_smem[];
-  const int t = threadIdx.x, lane = t & 31;
-  float* X = fb_smem;                    // [kIn][kFbThreads]
-  float* H1 = X + kIn * kFbThreads;      // [kHid][kFbThreads]
-  float* H2 = H1 + kHid * kFbThreads;    // [kHid][kFbThreads]
-  float* D = H2 + kHid * kFbThreads;     // [kHid][kFbThreads]
-  const float* W0 = F.mlp;
-  const float* B0 = W0 + kIn * kHid;
-  const float* W1 = B0 + kHid;
-  const float* B1 = W1 + kHid * kHid;
-  const float* W2 = B1 + kHid;
-  const float* B2 = W2 + kOut * kHid;
+__global__ void flag_list_kernel(const uint8_t* __restrict__ pflag, const unsigned long long* n_dev, long long cap,
+                                 int32_t* __restrict__ list, unsigned long long* n_list) {
   long long n = static_cast<long long>(*n_dev);
   n = n < cap ? n : cap;
-  for (long long base = static_cast<long long>(blockIdx.x) * kFbThreads; base < n;
-       base += static_cast<long long>(gridDim.x) * kFbThreads) {
-    const long long q = base + t;
-    const bool act = q < n && pflag[q] != 0;
-    const unsigned am = __ballot_sync(0xffffffffu, act);
-    if (!am) continue;  // warp-uniform: the whole warp skips unflagged stretches of the pool
-    long long slot = 0;
-    if (lane == 0) slot = static_cast<long long>(atomicAdd(n_rec, static_cast<unsigned long long>(__popc(am))));
-    slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(am & ((1u << lane) - 1u));
-    if (!act) continue;
-    float* R = rec + (slot < rec_cap ? slot : rec_cap) * kBwdRec;  // rec holds rec_cap + 1 records
-    const d3 x = make3(px[q], py[q], pz[q]);
-    // ---- forward recompute (CanonicalField::query_backward re-runs the forward) ----
-    float feats[kIn];
-    hash_encode_f2(F, x, feats);
-    for (int i = 0; i < kIn; ++i) {
-      X[i * kFbThreads + t] = feats[i];
-      R[kRecX + i] = feats[i];
+  const int lane = threadIdx.x & 31;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < n;
+       base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long q = base + threadIdx.x;
+    const bool f = q < n && pflag[q] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (!m) continue;
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(n_list, static_cast<unsigned long long>(__popc(m)));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (f) list[b + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(q);
+  }
+}
+
+__device__ __forceinline__ void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kTeam) : "memory");
+}
+
+// A team carries kTQ queries at once: the 64 threads cover 16 levels x 4 queries in the
+// encode phases, and each hidden-unit thread runs kTQ independent dot-product chains (one
+// weight load serves all of them), so no phase leaves most of the team idle at a barrier.
+constexpr int kTQ = 4;
+
+__global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView F, const double* __restrict__ px,
+                                                                      const double* __restrict__ py,
+                                                                      const double* __restrict__ pz,
+                                                                      const int32_t* __restrict__ list,
+                                                                      const unsigned long long* n_list,
+                                                                      const float* __restrict__ pgs,
+                                                                      const float* __restrict__ pgc,
+                                                                      float* __restrict__ grid_grad,
+                                                                      float* __restrict__ rec) {
+  extern __shared__ float bw_smem[];
+  float* W0p = bw_smem;                    // [64][33]
+  float* W1p = W0p + kHid * kW0s;          // [64][65]
+  float* W2p = W1p + kHid * kW1s;          // [4][65]
+  float* Bs = W2p + kOut * kW1s;           // b0[64] b1[64] b2[4]
+  float* TS = Bs + 2 * kHid + kOut;        // [kTeams][kTQ][kTeamSmem]
+  const float* W = F.mlp;
+  for (int e = threadIdx.x; e < kHid * kIn; e += kTeamThreads) W0p[(e / kIn) * kW0s + e % kIn] = __ldg(W + e);
+  const float* W1g = W + kIn * kHid + kHid;
+  for (int e = threadIdx.x; e < kHid * kHid; e += kTeamThreads) W1p[(e / kHid) * kW1s + e % kHid] = __ldg(W1g + e);
+  const float* W2g = W1g + kHid * kHid + kHid;
+  for (int e = threadIdx.x; e < kOut * kHid; e += kTeamThreads) W2p[(e / kHid) * kW1s + e % kHid] = __ldg(W2g + e);
+  for (int e = threadIdx.x; e < kHid; e += kTeamThreads) {
+    Bs[e] = __ldg(W + kIn * kHid + e);
+    Bs[kHid + e] = __ldg(W1g + kHid * kHid + e);
+  }
+  if (threadIdx.x < kOut) Bs[2 * kHid + threadIdx.x] = __ldg(W2g + kOut * kHid + threadIdx.x);
+  __syncthreads();
+  const int team = threadIdx.x / kTeam, t = threadIdx.x % kTeam;
+  float* S0 = TS + team * kTQ * kTeamSmem;
+  auto S = [&](int j) { return S0 + j * kTeamSmem; };
+  const long long n = static_cast<long long>(*n_list);
+  const int ej = t >> 4, el = t & 15;  // encode phases: query ej, level el
+  for (long long k0 = (static_cast<long long>(blockIdx.x) * kTeams + team) * kTQ; k0 < n;
+       k0 += static_cast<long long>(gridDim.x) * kTeams * kTQ) {
+    const int nq = static_cast<int>(n - k0 < kTQ ? n - k0 : kTQ);
+    // ---- encode (thread = (query ej, level el)) ----
+    double u[3] = {0.0, 0.0, 0.0};
+    long long qe = -1;
+    if (ej < nq) {
+      qe = list[k0 + ej];
+      normalize_point(F, make3(px[qe], py[qe], pz[qe]), u);
+      const float2 o = encode_level_f2(F, el, u);
+      S(ej)[kRecX + 2 * el] = o.x;
+      S(ej)[kRecX + 2 * el + 1] = o.y;
     }
-    for (int o = 0; o < kHid; ++o) {
-      float a = B0[o];
-      for (int i = 0; i < kIn; ++i) a = fadd(a, fmul(__ldg(W0 + o * kIn + i), feats[i]));
-      const float h = (a < 0.0f) ? 0.0f : a;
-      H1[o * kFbThreads + t] = h;
-      R[kRecH1 + o] = h;
+    team_sync(team);
+    {  // hidden layer 1 (R/mlp.hpp:100-104 order), kTQ chains
+      float a[kTQ];
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) a[j] = Bs[t];
+      for (int i = 0; i < kIn; ++i) {
+        const float w = W0p[t * kW0s + i];
+#pragma unroll
+        for (int j = 0; j < kTQ; ++j) a[j] = fadd(a[j], fmul(w, S(j)[kRecX + i]));
+      }
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) S(j)[kRecH1 + t] = (a[j] < 0.0f) ? 0.0f : a[j];
     }
-    for (int o = 0; o < kHid; ++o) {
-      float a = B1[o];
-      for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(__ldg(W1 + o * kHid + i), H1[i * kFbThreads + t]));
-      const float h = (a < 0.0f) ? 0.0f : a;
-      H2[o * kFbThreads + t] = h;
-      R[kRecH2 + o] = h;
+    team_sync(team);
+    {
+      float a[kTQ];
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) a[j] = Bs[kHid + t];
+      for (int i = 0; i < kHid; ++i) {
+        const float w = W1p[t * kW1s + i];
+#pragma unroll
+        for (int j = 0; j < kTQ; ++j) a[j] = fadd(a[j], fmul(w, S(j)[kRecH1 + i]));
+      }
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) S(j)[kRecH2 + t] = (a[j] < 0.0f) ? 0.0f : a[j];
     }
-    float lg[kOut];
-    for (int o = 0; o < kOut; ++o) {
-      float a = B2[o];
-      for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(__ldg(W2 + o * kHid + i), H2[i * kFbThreads + t]));
-      lg[o] = a;
-    }
-    // ---- d logits (R/field.hpp:95-99) ----
-    float u2[kOut];
-    u2[0] = fmul(pgs[q], logistic_f(lg[0]));
-    for (int c = 0; c < 3; ++c) {
-      const float v = logistic_f(lg[1 + c]);
-      u2[1 + c] = fmul(fmul(pgc[3 * q + c], v), __fsub_rn(1.0f, v));
-    }
-    for (int o = 0; o < kOut; ++o) R[kRecU2 + o] = u2[o];
-    // ---- dprev through the output layer (u != 0 only), ReLU mask of hidden layer 2 ----
-    for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = 0.0f;
-    for (int o = 0; o < kOut; ++o) {
-      const float u = u2[o];
-      if (u != 0.0f)
-        for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = fadd(D[i * kFbThreads + t], fmul(u, __ldg(W2 + o * kHid + i)));
-    }
-    for (int i = 0; i < kHid; ++i) {
-      const float d = (H2[i * kFbThreads + t] == 0.0f) ? 0.0f : D[i * kFbThreads + t];
-      H2[i * kFbThreads + t] = d;  // H2 now holds d h2
-      R[kRecD2 + i] = d;
-    }
-    // ---- hidden layer 1 ----
-    for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = 0.0f;
-    for (int o = 0; o < kHid; ++o) {
-      const float u = H2[o * kFbThreads + t];
-      if (u != 0.0f)
-        for (int i = 0; i < kHid; ++i) D[i * kFbThreads + t] = fadd(D[i * kFbThreads + t], fmul(u, __ldg(W1 + o * kHid + i)));
-    }
-    for (int i = 0; i < kHid; ++i) {
-      const float d = (H1[i * kFbThreads + t] == 0.0f) ? 0.0f : D[i * kFbThreads + t];
-      H1[i * kFbThreads + t] = d;  // H1 now holds d h1
-      R[kRecD1 + i] = d;
-    }
-    // ---- first layer -> d features ----
-    float din[kIn];
-    for (int i = 0; i < kIn; ++i) din[i] = 0.0f;
-    for (int o = 0; o < kHid; ++o) {
-      const float u = H1[o * kFbThreads + t];
-      if (u != 0.0f)
-        for (int i = 0; i < kIn; ++i) din[i] = fadd(din[i], fmul(u, __ldg(W0 + o * kIn + i)));
-    }
-    // ---- encode backward (R/hash_grid.hpp:155-169) ----
-    double uu[3];
-    normalize_point(F, x, uu);
-    for (int l = 0; l < F.L; ++l) {
-      LevelCorners lc;
-      level_corners(F, l, uu, lc);
-      float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
-      for (int k = 0; k < 8; ++k) {
-        const float w = lc.w[k];
-        if (w == 0.0f) continue;
-        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 0, fmul(w, din[2 * l + 0]));
-        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[k]) + 1, fmul(w, din[2 * l + 1]));
+    team_sync(team);
+    if (t < kTQ * kOut) {  // logits + d logits (R/field.hpp:95-99), thread = (query, output)
+      const int j = t / kOut, o = t % kOut;
+      if (j < nq) {
+        const long long q = list[k0 + j];
+        float a = Bs[2 * kHid + o];
+        for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(W2p[o * kW1s + i], S(j)[kRecH2 + i]));
+        float uo;
+        if (o == 0) {
+          uo = fmul(pgs[q], logistic_f(a));
+        } else {
+          const float v = logistic_f(a);
+          uo = fmul(fmul(pgc[3 * q + o - 1], v), __fsub_rn(1.0f, v));
+        }
+        S(j)[kRecU2 + o] = uo;
+        S(j)[kBwdRec + o] = a;
+      } else {
+        S(j)[kRecU2 + o] = 0.0f;
       }
     }
+    team_sync(team);
+    {  // dprev through the output layer (u != 0 only), ReLU mask of hidden layer 2
+      float d[kTQ];
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) d[j] = 0.0f;
+      for (int o = 0; o < kOut; ++o) {
+        const float w = W2p[o * kW1s + t];
+#pragma unroll
+        for (int j = 0; j < kTQ; ++j) {
+          const float uo = S(j)[kRecU2 + o];
+          if (uo != 0.0f) d[j] = fadd(d[j], fmul(uo, w));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) S(j)[kRecD2 + t] = (S(j)[kRecH2 + t] == 0.0f) ? 0.0f : d[j];
+    }
+    team_sync(team);
+    {
+      float d[kTQ];
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) d[j] = 0.0f;
+      for (int o = 0; o < kHid; ++o) {
+        const float w = W1p[o * kW1s + t];
+#pragma unroll
+        for (int j = 0; j < kTQ; ++j) {
+          const float uo = S(j)[kRecD2 + o];
+          if (uo != 0.0f) d[j] = fadd(d[j], fmul(uo, w));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kTQ; ++j) S(j)[kRecD1 + t] = (S(j)[kRecH1 + t] == 0.0f) ? 0.0f : d[j];
+    }
+    team_sync(team);
+    {  // d features: thread = (query pair, input i), kTQ / 2 chains each
+      const int i = t & (kIn - 1), jb = (t >> 5) * (kTQ / 2);
+      float d[kTQ / 2];
+#pragma unroll
+      for (int j = 0; j < kTQ / 2; ++j) d[j] = 0.0f;
+      for (int o = 0; o < kHid; ++o) {
+        const float w = W0p[o * kW0s + i];
+#pragma unroll
+        for (int j = 0; j < kTQ / 2; ++j) {
+          const float uo = S(jb + j)[kRecD1 + o];
+          if (uo != 0.0f) d[j] = fadd(d[j], fmul(uo, w));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kTQ / 2; ++j) S(jb + j)[kBwdRec + kOut + i] = d[j];
+    }
+    team_sync(team);
+    if (ej < nq) {  // encode backward (R/hash_grid.hpp:155-169): query ej, level el
+      LevelCorners lc;
+      level_corners(F, el, u, lc);
+      float* gt = grid_grad + static_cast<size_t>(el) * F.T * 2;
+      const float d0 = S(ej)[kBwdRec + kOut + 2 * el], d1 = S(ej)[kBwdRec + kOut + 2 * el + 1];
+      for (int c = 0; c < 8; ++c) {
+        const float w = lc.w[c];
+        if (w == 0.0f) continue;
+        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[c]) + 0, fmul(w, d0));
+        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[c]) + 1, fmul(w, d1));
+      }
+    }
+    for (int j = 0; j < nq; ++j) {
+      float* R = rec + (k0 + j) * kBwdRec;
+      for (int e = t; e < kBwdRec; e += kTeam) R[e] = S(j)[e];
+    }
+    team_sync(team);
   }
 }
 
@@ -296,34 +368,43 @@ __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const floa
   n = n < rec_cap ? n : rec_cap;
   constexpr int kW0 = kHid * kIn, kB0 = kW0 + kHid, kW1 = kB0 + kHid * kHid, kB1 = kW1 + kHid,
                 kW2 = kB1 + kOut * kHid, kB2 = kW2 + kOut;
+  constexpr int kPer = (kB2 + kWThreads - 1) / kWThreads;  // parameters per thread (26)
+  // parameter p = threadIdx.x + j * kWThreads: its delta / input offsets in the record
+  int dOff[kPer], iOff[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int p = threadIdx.x + j * kWThreads;
+    int d = -1, in = -1;
+    if (p < kW0) d = kRecD1 + p / kIn, in = kRecX + p % kIn;
+    else if (p < kB0) d = kRecD1 + (p - kW0);
+    else if (p < kW1) d = kRecD2 + (p - kB0) / kHid, in = kRecH1 + (p - kB0) % kHid;
+    else if (p < kB1) d = kRecD2 + (p - kW1);
+    else if (p < kW2) d = kRecU2 + (p - kB1) / kHid, in = kRecH2 + (p - kB1) % kHid;
+    else if (p < kB2) d = kRecU2 + (p - kW2);
+    dOff[j] = d;
+    iOff[j] = in;
+  }
+  float acc[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) acc[j] = 0.0f;
   for (long long c0 = static_cast<long long>(blockIdx.x) * kWq; c0 < n; c0 += static_cast<long long>(gridDim.x) * kWq) {
     const int nq = static_cast<int>(n - c0 < kWq ? n - c0 : kWq);
     __syncthreads();
     for (int e = threadIdx.x; e < nq * kBwdRec; e += kWThreads) S[e / kBwdRec][e % kBwdRec] = rec[c0 * kBwdRec + e];
     __syncthreads();
-    for (int p = threadIdx.x; p < kB2; p += kWThreads) {
-      int dOff, iOff, o, i;  // delta offset / input offset (-1: bias)
-      if (p < kW0) {
-        o = p / kIn, i = p % kIn, dOff = kRecD1, iOff = kRecX;
-      } else if (p < kB0) {
-        o = p - kW0, i = 0, dOff = kRecD1, iOff = -1;
-      } else if (p < kW1) {
-        o = (p - kB0) / kHid, i = (p - kB0) % kHid, dOff = kRecD2, iOff = kRecH1;
-      } else if (p < kB1) {
-        o = p - kW1, i = 0, dOff = kRecD2, iOff = -1;
-      } else if (p < kW2) {
-        o = (p - kB1) / kHid, i = (p - kB1) % kHid, dOff = kRecU2, iOff = kRecH2;
-      } else {
-        o = p - kW2, i = 0, dOff = kRecU2, iOff = -1;
+    for (int qq = 0; qq < nq; ++qq) {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        if (dOff[j] < 0) continue;
+        const float dv = S[qq][dOff[j]];
+        acc[j] = fadd(acc[j], iOff[j] >= 0 ? fmul(dv, S[qq][iOff[j]]) : dv);
       }
-      float acc = 0.0f;
-      if (iOff >= 0)
-        for (int qq = 0; qq < nq; ++qq) acc = fadd(acc, fmul(S[qq][dOff + o], S[qq][iOff + i]));
-      else
-        for (int qq = 0; qq < nq; ++qq) acc = fadd(acc, S[qq][dOff + o]);
-      if (acc != 0.0f) atomicAdd(mlp_grad + p, acc);
     }
   }
+  // one atomic per parameter per block (the grid is a few blocks per SM)
+#pragma unroll
+  for (int j = 0; j < kPer; ++j)
+    if (dOff[j] >= 0 && acc[j] != 0.0f) atomicAdd(mlp_grad + threadIdx.x + j * kWThreads, acc[j]);
 }
 
 int sms() {
@@ -339,26 +420,29 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
                          const float* gs, const float* gc, cudaStream_t s) {
   if (!(m.fv.F == 2 && m.fv.in_dim == kIn && m.fv.hidden == kHid && m.fv.n_layers == 3 && m.fv.out_dim == kOut))
     throw std::invalid_argument("train path: libarfx implements the 32-64-64-4 decoder (levels*F == 32)");
-  const size_t smem = static_cast<size_t>(kIn + 3 * kHid) * kFbThreads * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    ARFX_CUDA(cudaFuncSetAttribute(field_bwd_query_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    attr = true;
-  }
   Workspace& w = m.ws;
   const long long rec_cap = cap;
   w.bwd_rec.ensure(static_cast<size_t>(rec_cap + 1) * kBwdRec);
+  w.bwd_list.ensure(static_cast<size_t>(rec_cap + 1));
   w.bwd_n.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
-  const long long blocks = std::min<long long>((cap + kFbThreads - 1) / kFbThreads, static_cast<long long>(sms()) * 8);
   m.prof.begin("field_backward", s);
-  field_bwd_query_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), kFbThreads, smem, s>>>(
-      m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, flag, gs, gc, d_n, cap, m.grid_grad.ptr, w.bwd_rec.ptr, rec_cap,
-      w.bwd_n.ptr);
+  flag_list_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((cap + 255) / 256,
+                                                                                       static_cast<long long>(sms()) * 8))),
+                     256, 0, s>>>(flag, d_n, cap, w.bwd_list.ptr, w.bwd_n.ptr);
+  const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
+                            static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
+  static bool team_attr = false;
+  if (!team_attr) {
+    ARFX_CUDA(cudaFuncSetAttribute(field_bwd_team_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(team_smem)));
+    team_attr = true;
+  }
+  field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
+      m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
   ARFX_CUDA(cudaGetLastError());
-  field_bwd_weights_kernel<<<static_cast<unsigned>(sms() * 4), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
-                                                                                m.mlp_grad.ptr);
+  field_bwd_weights_kernel<<<static_cast<unsigned>(sms()), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
+                                                                            m.mlp_grad.ptr);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }

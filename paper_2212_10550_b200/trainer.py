@@ -3,7 +3,8 @@
 The reference code base stops at the differentiable pieces (composite_backward,
 query_backward); the SPEC's trainer is built here over the libarfx training ABI:
 
-  per step t (all on the device; the host syncs only for the workspace-overflow checks):
+  per step t (all enqueued on the device without host synchronisation; the occupancy update
+  every k steps is the sync point, where the losses are also checked for finiteness):
     rays     B / world rays per rank: frame f and pixels from keyed_rng(seed, 0x7a11, t, rank)
              (draw order: frame, then px, py per ray), ground truth gathered from the
              device-resident dataset frames (analytic figure, arfx_figure_render)
@@ -142,7 +143,10 @@ class Trainer:
         self.params = device_view(fl["params"], self.n_flat)
         self.grads = device_view(fl["grads"], self.n_flat)
         self.dp = FlatDataParallel(self.params, self.grads, self.n_flat, rank, world, group)
-        self.stream = torch.cuda.current_stream()
+        # one non-default stream carries every step: libarfx launches, torch copies/gathers and
+        # the NCCL collectives are then ordered without host synchronisation
+        self.stream = torch.cuda.Stream()
+        self.stream.wait_stream(torch.cuda.current_stream())
         self.loss4 = torch.zeros(4, dtype=torch.float64, device="cuda")
         self.loss_d = torch.zeros(2, dtype=torch.float64, device="cuda")
         self.px = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
@@ -153,21 +157,38 @@ class Trainer:
         self.grid = arf.OccupancyGrid(model.normalized_box, cfg.occupancy)
         arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
         self.step_id = 0
-        self.history = []
+        self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
+        self._checked = 0     # steps whose loss has been checked for finiteness
+        # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
+        self._h_pix = [torch.zeros((2, self.n_local), dtype=torch.int32).pin_memory() for _ in range(2)]
+        self._h_evt = [torch.cuda.Event(), torch.cuda.Event()]
 
     def _opt(self, frame: int) -> arf.RenderOptions:
         return arf.RenderOptions(samples_per_ray=self.cfg.samples_per_ray, stratified=True, seed=self.cfg.seed,
                                  frame_id=self.step_id * 1024 + frame)
 
-    def step(self) -> np.ndarray:
+    def step(self):
+        """One SPEC train step, enqueued without host synchronisation (except the occupancy
+        update every k steps, which is also where the loss is checked for finiteness).
+        Returns the step's loss as a device tensor (L_rgb, L_alpha, L_hard, L_density, total)."""
+        with self.torch.cuda.stream(self.stream):
+            return self._step()
+
+    def _step(self):
         torch = self.torch
         cfg, W = self.cfg, self.camera.width
         f, px, py = ray_batch(cfg.seed, self.step_id, self.rank, self.n_local, len(self.poses), W, self.camera.height)
-        self.px.copy_(torch.from_numpy(px), non_blocking=False)
-        self.py.copy_(torch.from_numpy(py), non_blocking=False)
+        slot = self.step_id & 1
+        self._h_evt[slot].synchronize()  # the copy that last used this staging slot has run
+        hp = self._h_pix[slot]
+        hp[0].numpy()[:] = px
+        hp[1].numpy()[:] = py
+        self.px.copy_(hp[0], non_blocking=True)
+        self.py.copy_(hp[1], non_blocking=True)
+        self._h_evt[slot].record(self.stream)
         idx = (self.py.long() * W + self.px.long())
-        self.b_rgb.copy_(self.gt_rgb[f].index_select(0, idx))
-        self.b_alpha.copy_(self.gt_alpha[f].index_select(0, idx))
+        torch.index_select(self.gt_rgb[f], 0, idx, out=self.b_rgb)
+        torch.index_select(self.gt_alpha[f], 0, idx, out=self.b_alpha)
         sp = C.c_void_p(self.stream.cuda_stream)
         L.call("arfx_train_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()), self.grid._h,
                C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
@@ -178,24 +199,44 @@ class Trainer:
             L.call("arfx_density_step_device", self.model._h, self.views[f]._h, self.grid._h, cfg.density_points,
                    (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id, C.byref(cfg.loss.to_c()),
                    C.c_void_p(self.loss_d.data_ptr()), sp)
+        else:
+            self.loss_d.zero_()
         t = self.step_id + 1
         self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
-        if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
-            arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t)
+        loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
+                            self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
+        self._hist.append(loss)
         self.step_id = t
-        l4 = self.loss4.cpu().numpy()
-        ld = float(self.loss_d[0].cpu()) if cfg.loss.w_density > 0 else 0.0
-        # (L_rgb, L_alpha, L_hard, L_density, total)
-        loss = np.array([l4[0], l4[1], l4[2], ld, l4[3] + cfg.loss.w_density * ld])
-        if not np.all(np.isfinite(loss)):
-            raise L.NumericError(3, f"train_step: non-finite loss at step {t}: {loss.tolist()}")
-        self.history.append(loss)
+        if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
+            self.stream.synchronize()  # the host-buffer API below runs on the library's stream
+            arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t)
+            self._check()
         return loss
+
+    def _check(self):
+        if self._checked < len(self._hist):
+            h = torch_stack_cpu(self.torch, self._hist[self._checked:])
+            bad = ~np.all(np.isfinite(h), axis=1)
+            if bad.any():
+                k = self._checked + int(np.argmax(bad)) + 1
+                raise L.NumericError(3, f"train_step: non-finite loss at step {k}: {h[np.argmax(bad)].tolist()}")
+            self._checked = len(self._hist)
+
+    @property
+    def history(self) -> np.ndarray:
+        """Per-step losses (synchronises): rows (L_rgb, L_alpha, L_hard, L_density, total)."""
+        self.stream.synchronize()
+        self._check()
+        return torch_stack_cpu(self.torch, self._hist) if self._hist else np.zeros((0, 5))
 
     def train(self, iterations: int | None = None):
         for _ in range(iterations or self.cfg.iterations):
             self.step()
-        return np.array(self.history)
+        return self.history
+
+
+def torch_stack_cpu(torch, ts) -> np.ndarray:
+    return torch.stack(ts).cpu().numpy()
 
 
 def psnr(img, ref) -> float:
