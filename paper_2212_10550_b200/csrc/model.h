@@ -83,6 +83,7 @@ struct Workspace {
   DevBuf<uint8_t> pflag;   // per pool entry: query_backward needed
   DevBuf<float> bwd_rec;   // K8a -> K8b: per flagged query, MLP layer inputs and deltas
   DevBuf<int32_t> bwd_list;  // flagged pool entries, compacted
+  DevBuf<float> bwd_partial;  // K8b per-block MLP gradient rows
   DevBuf<unsigned long long> bwd_n;
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);

@@ -162,7 +162,9 @@ constexpr int kBwdRec = kIn + kHid + kHid + kOut + kHid + kHid;  // X, H1, H2, u
 constexpr int kRecX = 0, kRecH1 = kIn, kRecH2 = kIn + kHid, kRecU2 = kIn + 2 * kHid, kRecD2 = kRecU2 + kOut,
               kRecD1 = kRecD2 + kHid;
 constexpr int kTeam = 64, kTeams = 4, kTeamThreads = kTeam * kTeams;
-constexpr int kTeamSmem = kBwdRec + kOut + kIn;  // record + logits + d features
+constexpr int kRecDin = kBwdRec;                  // + d features (32) for the scatter kernel
+constexpr int kRecStride = kBwdRec + kIn;         // floats per query record in global memory
+constexpr int kTeamSmem = kRecStride + kOut;      // record + d features + logits
 constexpr int kW0s = kIn + 1, kW1s = kHid + 1;  // padded row strides
 
 __global__ void flag_list_kernel(const uint8_t* __restrict__ pflag, const unsigned long long* n_dev, long long cap,
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
           uo = fmul(fmul(pgc[3 * q + o - 1], v), __fsub_rn(1.0f, v));
         }
         S(j)[kRecU2 + o] = uo;
-        S(j)[kBwdRec + o] = a;
+        S(j)[kRecStride + o] = a;
       } else {
         S(j)[kRecU2 + o] = 0.0f;
       }
@@ -330,46 +332,89 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
         }
       }
 #pragma unroll
-      for (int j = 0; j < kTQ / 2; ++j) S(jb + j)[kBwdRec + kOut + i] = d[j];
+      for (int j = 0; j < kTQ / 2; ++j) S(jb + j)[kRecDin + i] = d[j];
     }
     team_sync(team);
-    if (ej < nq) {  // encode backward (R/hash_grid.hpp:155-169): query ej, level el
-      LevelCorners lc;
-      level_corners(F, el, u, lc);
-      float* gt = grid_grad + static_cast<size_t>(el) * F.T * 2;
-      const float d0 = S(ej)[kBwdRec + kOut + 2 * el], d1 = S(ej)[kBwdRec + kOut + 2 * el + 1];
-      for (int c = 0; c < 8; ++c) {
-        const float w = lc.w[c];
-        if (w == 0.0f) continue;
-        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[c]) + 0, fmul(w, d0));
-        atomicAdd(gt + 2 * static_cast<size_t>(lc.idx[c]) + 1, fmul(w, d1));
-      }
-    }
     for (int j = 0; j < nq; ++j) {
-      float* R = rec + (k0 + j) * kBwdRec;
-      for (int e = t; e < kBwdRec; e += kTeam) R[e] = S(j)[e];
+      float* R = rec + (k0 + j) * kRecStride;
+      for (int e = t; e < kRecStride; e += kTeam) R[e] = S(j)[e];
     }
     team_sync(team);
   }
 }
 
+// K8c: hash-grid scatter-add of the encode backward (R/hash_grid.hpp:155-169), warp-
+// aggregated: a warp takes one level for 32 consecutive queries of the compacted list
+// (spatially coherent: the pool follows ray order); lanes whose corner hits the same table
+// row are grouped with __match_any_sync and summed by shuffles, and one lane per distinct
+// row issues the atomics -- coarse (dense) levels collapse many contributions per row.
+__global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const double* __restrict__ px,
+                                                           const double* __restrict__ py,
+                                                           const double* __restrict__ pz,
+                                                           const int32_t* __restrict__ list,
+                                                           const unsigned long long* n_list,
+                                                           const float* __restrict__ rec,
+                                                           float* __restrict__ grid_grad) {
+  const long long n = static_cast<long long>(*n_list);
+  const int lane = threadIdx.x & 31;
+  const long long chunks = (n + 31) / 32;
+  const long long total = chunks * F.L;
+  for (long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gw < total;
+       gw += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int l = static_cast<int>(gw % F.L);
+    const long long k = (gw / F.L) * 32 + lane;
+    const bool act = k < n;
+    LevelCorners lc;
+    float d0 = 0.0f, d1 = 0.0f;
+    if (act) {
+      const long long q = list[k];
+      double u[3];
+      normalize_point(F, make3(px[q], py[q], pz[q]), u);
+      level_corners(F, l, u, lc);
+      d0 = rec[k * kRecStride + kRecDin + 2 * l];
+      d1 = rec[k * kRecStride + kRecDin + 2 * l + 1];
+    }
+    float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      const bool has = act && lc.w[c] != 0.0f;
+      const uint32_t key = has ? lc.idx[c] : 0xffffffffu;
+      const float v0 = has ? fmul(lc.w[c], d0) : 0.0f, v1 = has ? fmul(lc.w[c], d1) : 0.0f;
+      const unsigned g = __match_any_sync(0xffffffffu, key);
+      float s0 = 0.0f, s1 = 0.0f;
+      for (unsigned mm = g; mm; mm &= mm - 1) {
+        const int src = __ffs(mm) - 1;
+        s0 = fadd(s0, __shfl_sync(g, v0, src));
+        s1 = fadd(s1, __shfl_sync(g, v1, src));
+      }
+      if (has && lane == __ffs(g) - 1) {
+        atomicAdd(gt + 2 * static_cast<size_t>(key) + 0, s0);
+        atomicAdd(gt + 2 * static_cast<size_t>(key) + 1, s1);
+      }
+    }
+  }
+}
+
 // K8b: MLP weight / bias gradients, gW[o][i] = sum_q delta[q][o] * in[q][i] and gb[o] =
-// sum_q delta[q][o], over the K8a records: a block stages kWq records in smem (row-major,
-// so threads walking i read consecutive words) and each thread owns a strided set of the
-// 6,532 parameters; one f32 atomic per parameter per block.
+// sum_q delta[q][o], over the K8a records: a block stages kWq records at a time in smem
+// (row-major: threads walking i read consecutive words); each thread owns ~26 of the 6,532
+// parameters and accumulates them in registers over all of the block's chunks, then
+// writes one partial row; K8d sums the partial rows in block order (deterministic, no
+// atomics).
 constexpr int kWq = 32;
 constexpr int kWThreads = 256;
+constexpr int kNParams = kHid * kIn + kHid + kHid * kHid + kHid + kOut * kHid + kOut;  // 6,532
 __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const float* __restrict__ rec,
                                                                       const unsigned long long* n_rec,
                                                                       long long rec_cap,
-                                                                      float* __restrict__ mlp_grad) {
-  __shared__ float S[kWq][kBwdRec + 1];
+                                                                      float* __restrict__ partial) {
+  __shared__ float S[kWq][kRecStride + 1];
   long long n = static_cast<long long>(*n_rec);
   n = n < rec_cap ? n : rec_cap;
   constexpr int kW0 = kHid * kIn, kB0 = kW0 + kHid, kW1 = kB0 + kHid * kHid, kB1 = kW1 + kHid,
                 kW2 = kB1 + kOut * kHid, kB2 = kW2 + kOut;
+  static_assert(kB2 == kNParams, "parameter count");
   constexpr int kPer = (kB2 + kWThreads - 1) / kWThreads;  // parameters per thread (26)
-  // parameter p = threadIdx.x + j * kWThreads: its delta / input offsets in the record
   int dOff[kPer], iOff[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
@@ -390,7 +435,8 @@ __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const floa
   for (long long c0 = static_cast<long long>(blockIdx.x) * kWq; c0 < n; c0 += static_cast<long long>(gridDim.x) * kWq) {
     const int nq = static_cast<int>(n - c0 < kWq ? n - c0 : kWq);
     __syncthreads();
-    for (int e = threadIdx.x; e < nq * kBwdRec; e += kWThreads) S[e / kBwdRec][e % kBwdRec] = rec[c0 * kBwdRec + e];
+    const float* src = rec + c0 * kRecStride;
+    for (int e = threadIdx.x; e < nq * kRecStride; e += kWThreads) S[e / kRecStride][e % kRecStride] = src[e];
     __syncthreads();
     for (int qq = 0; qq < nq; ++qq) {
 #pragma unroll
@@ -401,10 +447,30 @@ __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const floa
       }
     }
   }
-  // one atomic per parameter per block (the grid is a few blocks per SM)
+  float* row = partial + static_cast<size_t>(blockIdx.x) * kNParams;
 #pragma unroll
   for (int j = 0; j < kPer; ++j)
-    if (dOff[j] >= 0 && acc[j] != 0.0f) atomicAdd(mlp_grad + threadIdx.x + j * kWThreads, acc[j]);
+    if (dOff[j] >= 0) row[threadIdx.x + j * kWThreads] = acc[j];
+}
+
+// K8d: mlp_grad[p] += sum over blocks of partial[b][p]: a block takes 32 parameters, its 8
+// warps sum interleaved row subsets (coalesced 128-B rows), then a fixed-order combine --
+// deterministic, no atomics
+__global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __restrict__ partial, int n_blocks,
+                                                             float* __restrict__ mlp_grad) {
+  __shared__ float part[8][32];
+  const int pi = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + pi;
+  float a = 0.0f;
+  if (p < kNParams)
+    for (int b = wp; b < n_blocks; b += 8) a = fadd(a, partial[static_cast<size_t>(b) * kNParams + p]);
+  part[wp][pi] = a;
+  __syncthreads();
+  if (wp == 0 && p < kNParams) {
+    float t = part[0][pi];
+    for (int k = 1; k < 8; ++k) t = fadd(t, part[k][pi]);
+    mlp_grad[p] = fadd(mlp_grad[p], t);
+  }
 }
 
 int sms() {
@@ -422,7 +488,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
     throw std::invalid_argument("train path: libarfx implements the 32-64-64-4 decoder (levels*F == 32)");
   Workspace& w = m.ws;
   const long long rec_cap = cap;
-  w.bwd_rec.ensure(static_cast<size_t>(rec_cap + 1) * kBwdRec);
+  w.bwd_rec.ensure(static_cast<size_t>(rec_cap + 1) * kRecStride);
   w.bwd_list.ensure(static_cast<size_t>(rec_cap + 1));
   w.bwd_n.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
@@ -441,8 +507,14 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
   ARFX_CUDA(cudaGetLastError());
-  field_bwd_weights_kernel<<<static_cast<unsigned>(sms()), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
-                                                                            m.mlp_grad.ptr);
+  grid_scatter_kernel<<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(m.fv, w.px.ptr, w.py.ptr, w.pz.ptr,
+                                                                     w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr,
+                                                                     m.grid_grad.ptr);
+  const int wblocks = sms() * 4;
+  w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
+  field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
+                                                                              w.bwd_partial.ptr);
+  weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, s>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
