@@ -254,6 +254,9 @@ def run_ours(args):
     total_ms, posed_all = float(t[0]), float(t[1])
     fps = K / (total_ms / 1000.0)
 
+    # kernel launches per frame, counted by the CUDA profiler (kineto) on 2 untimed frames
+    launches_per_frame = count_launches(lambda i: frame(Wm + i, Wm + K), 2)
+
     # e2e through the host-buffer public API
     e2e = run_e2e(args, model, poses, cam, opt, occ, rank, world, views)
 
@@ -282,7 +285,8 @@ def run_ours(args):
                 "rays_per_s": npix * K / (total_ms / 1000.0),
                 "kernels_ms_per_frame": {k: v[0] / K for k, v in prof.items()},
                 "clocks": clk, "e2e": e2e,
-                "gpu_launches": int(sum(v[1] for v in prof.values())),
+                "gpu_launches": launches_per_frame * K if launches_per_frame else int(sum(v[1] for v in prof.values())),
+                "gpu_launches_per_frame": launches_per_frame,
                 "peaks_kind": peak_kind,
                 "render_decoder": args.mlp,
                 "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}
@@ -315,6 +319,25 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def count_launches(fn, n):
+    """Kernel launches per call of fn(i), counted with torch.profiler (CUPTI activity) over n calls;
+    only libarfx kernels run inside fn. None when the profiler is unavailable."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for i in range(n):
+                fn(i)
+            torch.cuda.synchronize()
+        k = sum(1 for e in prof.events() if getattr(e, "device_type", None) is not None
+                and str(e.device_type).endswith("CUDA") and "memset" not in e.name.lower()
+                and "memcpy" not in e.name.lower())
+        return int(round(k / n))
+    except Exception:
+        return None
 
 
 def read_profile(model, L):

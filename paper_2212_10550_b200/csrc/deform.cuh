@@ -180,79 +180,7 @@ __device__ __forceinline__ void skin_weights_dense(const SkinView& S, d3 x, doub
   }
 }
 
-// One start of inverse_lbs_ctx (R/articulation.hpp:103-142). Returns true when the
-// start converged; x / gn hold the root and its residual.
-__device__ __forceinline__ bool newton_start(const SkinView& S, const PoseCtx* __restrict__ P,
-                                             const InverseOpts& opt, int b, d3 xt, double* ws,
-                                             int stride, d3& x, double& gn) {
-  x = rigid_apply(P->bone_inv[b], xt);
-  d3 g;
-  double J[9];
-  skin_eval(S, P, x, xt, ws, stride, g, gn, J);
-  bool converged = gn < opt.tolerance;
-  for (int it = 0; it < opt.max_iterations && !converged; ++it) {
-    // Mat3::inverse  R/math.hpp:141-158 (singular -> abandon start, :114-118)
-    const double* m = J;
-    const double c0 = dsub(dmul(m[4], m[8]), dmul(m[5], m[7]));
-    const double c1 = dsub(dmul(m[3], m[8]), dmul(m[5], m[6]));
-    const double c2 = dsub(dmul(m[3], m[7]), dmul(m[4], m[6]));
-    const double det = dadd(dsub(dmul(m[0], c0), dmul(m[1], c1)), dmul(m[2], c2));
-    if (fabs(det) < 2.2250738585072014e-308 * 64) break;
-    const double id = ddiv(1.0, det);
-    double inv[9];
-    inv[0] = dmul(c0, id);
-    inv[1] = dmul(dsub(dmul(m[2], m[7]), dmul(m[1], m[8])), id);
-    inv[2] = dmul(dsub(dmul(m[1], m[5]), dmul(m[2], m[4])), id);
-    inv[3] = dmul(dsub(dmul(m[5], m[6]), dmul(m[3], m[8])), id);
-    inv[4] = dmul(dsub(dmul(m[0], m[8]), dmul(m[2], m[6])), id);
-    inv[5] = dmul(dsub(dmul(m[2], m[3]), dmul(m[0], m[5])), id);
-    inv[6] = dmul(c2, id);
-    inv[7] = dmul(dsub(dmul(m[1], m[6]), dmul(m[0], m[7])), id);
-    inv[8] = dmul(dsub(dmul(m[0], m[4]), dmul(m[1], m[3])), id);
-    const d3 step = matvec(inv, g);
-    double damp = 1.0;
-    d3 xn = x, gnx = g;
-    double gnn = gn;
-    double Jn[9];
-    for (int h = 0; h < 4; ++h) {
-      const d3 cand = sub3(x, mul3(step, damp));
-      d3 gc;
-      double gcn, Jc[9];
-      skin_eval(S, P, cand, xt, ws, stride, gc, gcn, Jc);
-      if (gcn < gn || h == 3) {
-        xn = cand;
-        gnx = gc;
-        gnn = gcn;
-#pragma unroll
-        for (int e = 0; e < 9; ++e) Jn[e] = Jc[e];
-        break;
-      }
-      damp = dmul(damp, 0.5);
-    }
-    if (gnn >= gn && gn >= opt.tolerance) break;  // stalled
-    x = xn;
-    g = gnx;
-    gn = gnn;
-#pragma unroll
-    for (int e = 0; e < 9; ++e) J[e] = Jn[e];
-    converged = gn < opt.tolerance;
-  }
-  return converged;
-}
-
-// inverse_lbs_ctx  R/articulation.hpp:94-145
-__device__ __forceinline__ void inverse_lbs(const SkinView& S, const PoseCtx* __restrict__ P,
-                                            const InverseOpts& opt, d3 xt, double* ws, int stride,
-                                            Roots& R) {
-  R.count = 0;
-  for (int b = 0; b < P->nb; ++b) {
-    const d3 ca = make3(P->cap_a[b][0], P->cap_a[b][1], P->cap_a[b][2]);
-    const d3 cb = make3(P->cap_b[b][0], P->cap_b[b][1], P->cap_b[b][2]);
-    if (point_segment_distance(xt, ca, cb) > P->cutoff[b]) continue;
-    d3 x;
-    double gn;
-    if (newton_start(S, P, opt, b, xt, ws, stride, x, gn)) roots_push(R, x, gn, opt.dedup_radius);
-  }
-}
+// The per-start Newton iteration itself (inverse_lbs_ctx's loop body) lives in the start
+// pipeline's state machine, deform_starts.cuh start_newton_kernel.
 
 }  // namespace arfx

@@ -80,13 +80,9 @@ template <class Src, bool kSinglePose>
 __global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restrict__ poses, Src src,
                                                          uint32_t* __restrict__ mask_out,
                                                          uint32_t* __restrict__ count_out,
-                                                         unsigned long long* __restrict__ bone_hist,
                                                          unsigned long long* stats) {
   extern __shared__ double sm_smem[];
-  __shared__ unsigned long long hist[kMaxBones];
   const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sm_smem);
-  for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long n = src.count();
   int exact = 0;
@@ -101,64 +97,11 @@ __global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restri
       mask_out[s] = mask;
       count_out[s] = static_cast<uint32_t>(__popc(mask));
     }
-    if (bone_hist) {  // optional per-bone start histogram
-      uint32_t any = mask;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
-      for (uint32_t m = any; m; m &= m - 1) {
-        const int b = __ffs(m) - 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
-        if (lane == 0) atomicAdd(&hist[b], static_cast<unsigned long long>(__popc(bal)));
-      }
-    }
   }
-  __syncthreads();
-  if (bone_hist)
-    for (int i = threadIdx.x; i < kMaxBones; i += blockDim.x)
-      if (hist[i]) atomicAdd(bone_hist + i, hist[i]);
   if (stats) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
     if (lane == 0 && exact) atomicAdd(stats + 4, static_cast<unsigned long long>(exact));
-  }
-}
-
-// per-bone exclusive prefix -> item offsets (one tiny block)
-__global__ void bone_offsets_kernel(const unsigned long long* __restrict__ hist, int nb,
-                                    unsigned long long* __restrict__ cursor, unsigned long long* total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  unsigned long long acc = 0;
-  for (int b = 0; b < nb; ++b) {
-    cursor[b] = acc;
-    acc += hist[b];
-  }
-  *total = acc;
-}
-
-// K2b: bone-major items, warp-aggregated per bone
-template <class Src>
-__global__ void __launch_bounds__(256) start_scatter_kernel(Src src, const uint32_t* __restrict__ mask_in,
-                                                            unsigned long long* __restrict__ cursor,
-                                                            uint32_t* __restrict__ items, long long cap) {
-  const int lane = threadIdx.x & 31;
-  const long long n = src.count();
-  for (long long base = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
-       base < n; base += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long s = base + lane;
-    const uint32_t mask = s < n ? mask_in[s] : 0u;
-    uint32_t any = mask;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
-    for (uint32_t m = any; m; m &= m - 1) {
-      const int b = __ffs(m) - 1;
-      const bool has = (mask >> b) & 1u;
-      const unsigned bal = __ballot_sync(0xffffffffu, has);
-      unsigned long long off = 0;
-      if (lane == 0) off = atomicAdd(cursor + b, static_cast<unsigned long long>(__popc(bal)));
-      off = __shfl_sync(0xffffffffu, off, 0);
-      const long long pos = static_cast<long long>(off) + __popc(bal & ds_lanemask_lt());
-      if (has && pos < cap) items[pos] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
-    }
   }
 }
 

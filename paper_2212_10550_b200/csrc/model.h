@@ -73,7 +73,6 @@ struct Workspace {
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
   DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base
-  DevBuf<unsigned long long> bone_hist;       // [0,32) per-bone start counts, [32,64) item cursors
   DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
   DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
   DevBuf<double4> res4;                        // per start slot: root xyz, residual (-1: no root)

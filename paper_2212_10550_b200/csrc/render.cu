@@ -707,7 +707,7 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5);
   set_u64_kernel<<<1, 1, 0, s>>>(C + 8, static_cast<unsigned long long>(nkeys));
   start_mask_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
-                                                                            nullptr, stats);
+                                                                            stats);
   ARFX_CUDA(cudaGetLastError());
   // start slots: exclusive scan of the per-target start counts (C6 = total starts)
   const long long nb = (n + kScanBlock - 1) / kScanBlock;
@@ -802,7 +802,6 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
   }
   key_hist.ensure(nkeys);
   scan_sums.ensure(std::max(targets, nkeys) / kScanBlock + 2);
-  if (!bone_hist.ptr) bone_hist.alloc(2 * kMaxBones);
   // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
   const size_t want = std::max<size_t>({targets * 5 / 2, static_cast<size_t>(1) << 16, min_starts, learned_starts});
   if (want > cap_starts) {
