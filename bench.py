@@ -611,7 +611,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100, help="timed frames (default: the 100-frame animation)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "exact"],
+    ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "tcgen05_fp16", "exact"],
                     help="render decoder for `value` (the other one is reported as other_decoder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dp-train", action="store_true",

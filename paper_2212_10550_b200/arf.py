@@ -252,8 +252,9 @@ class Model:
     def set_mlp_mode(self, mode: str) -> None:
         """'exact' (f32 SIMT, the reference's summation order; default) or 'tcgen05'
         (tensor cores, split-bf16 operands with f32 accumulation; stated tolerance 1e-3
-        relative on rendered RGB). Render only."""
-        call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1}[mode])
+        relative on rendered RGB); 'tcgen05_fp16' additionally gathers the hash table in fp16.
+        Render only."""
+        call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1, "tcgen05_fp16": 2}[mode])
 
     def zero_grad(self):
         call("arfx_model_zero_grad", self._h, None)

@@ -559,7 +559,8 @@ int arfx_model_set_params(arfx_model mh, const float* gp, const float* mp) {
 int arfx_model_set_mlp_mode(arfx_model mh, int mode) {
   return guard([&] {
     require(mh != nullptr, "set_mlp_mode: null model");
-    require(mode == ARFX_MLP_EXACT || mode == ARFX_MLP_TCGEN05, "set_mlp_mode: unknown mode");
+    require(mode == ARFX_MLP_EXACT || mode == ARFX_MLP_TCGEN05 || mode == ARFX_MLP_TCGEN05_FP16,
+            "set_mlp_mode: unknown mode");
     mh->impl.mlp_mode = mode;
   });
 }

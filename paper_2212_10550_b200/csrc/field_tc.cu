@@ -147,11 +147,37 @@ constexpr int kEncThreads = 256;
 #ifndef ARFX_ENC_MIN_BLOCKS
 #define ARFX_ENC_MIN_BLOCKS 4
 #endif
+// fp16 gathers (mode 2): the level's float2 row is read as half2 (4 B instead of 8 B),
+// widened to f32, and accumulated exactly like encode_level_f2
+__device__ __forceinline__ float2 encode_level_h2(const FieldView& F, const __half2* __restrict__ table, int l,
+                                                  const double u[3]) {
+  LevelCorners lc;
+  level_corners(F, l, u, lc);
+  const __half2* t = table + static_cast<size_t>(l) * F.T;
+  float2 row[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) row[k] = __half22float2(__ldg(t + lc.idx[k]));
+  float o0 = 0.0f, o1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o0 = fadd(o0, fmul(lc.w[k], row[k].x));
+    o1 = fadd(o1, fmul(lc.w[k], row[k].y));
+  }
+  return make_float2(o0, o1);
+}
+
+__global__ void to_half2_kernel(const float2* __restrict__ src, __half2* __restrict__ dst, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __float22half2_rn(src[i]);
+}
+
+template <bool kHalf>
 __global__ void __launch_bounds__(kEncThreads, ARFX_ENC_MIN_BLOCKS)
-    encode_tiles_kernel(FieldView F, const double* __restrict__ px, const double* __restrict__ py,
-                        const double* __restrict__ pz, const int32_t* __restrict__ owner,
-                        const unsigned long long* n_dev, long long cap, unsigned char* __restrict__ tiles,
-                        unsigned long long* stats) {
+    encode_tiles_kernel(FieldView F, const __half2* __restrict__ table_h2, const double* __restrict__ px,
+                        const double* __restrict__ py, const double* __restrict__ pz,
+                        const int32_t* __restrict__ owner, const unsigned long long* n_dev, long long cap,
+                        unsigned char* __restrict__ tiles, unsigned long long* stats) {
   long long n = static_cast<long long>(*n_dev);
   n = n < cap ? n : cap;
   for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
@@ -171,7 +197,7 @@ __global__ void __launch_bounds__(kEncThreads, ARFX_ENC_MIN_BLOCKS)
       __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 o = encode_level_f2(F, l + j, u);
+        const float2 o = kHalf ? encode_level_h2(F, table_h2, l + j, u) : encode_level_f2(F, l + j, u);
         split_bf16(o.x, hi[2 * j], lo[2 * j]);
         split_bf16(o.y, hi[2 * j + 1], lo[2 * j + 1]);
       }
@@ -367,10 +393,20 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));
   const size_t tile_bytes = static_cast<size_t>(2 * TcSmem::A0P);
   m.ws.tc_tiles.ensure(static_cast<size_t>((m.ws.cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
+  const bool half = m.mlp_mode == 2;
+  if (half) {  // refresh the fp16 copy of the table (params may have changed since the last render)
+    const long long nrow = static_cast<long long>(m.n_grid / 2);
+    m.grid_h2.ensure(static_cast<size_t>(nrow));
+    m.prof.begin("table_fp16", s);
+    to_half2_kernel<<<static_cast<unsigned>(std::min<long long>((nrow + 255) / 256, static_cast<long long>(sms) * 8)), 256,
+                      0, s>>>(reinterpret_cast<const float2*>(m.grid_params.ptr), m.grid_h2.ptr, nrow);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+  }
   m.prof.begin("encode_tc", s);
-  encode_tiles_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n_hint + 255) / 256,
+  (half ? encode_tiles_kernel<true> : encode_tiles_kernel<false>)<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n_hint + 255) / 256,
                                                                                        static_cast<long long>(sms) * 16))),
-                        kEncThreads, 0, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
+                        kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
                                      m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool), m.ws.tc_tiles.ptr,
                                      m.stats_on ? m.stats.ptr : nullptr);
   ARFX_CUDA(cudaGetLastError());

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include <cstdint>
 #include <string>
@@ -118,7 +119,9 @@ struct ModelImpl {
   // [2] Newton steps [3] starts [4] exact prune tests [5] field queries
   bool stats_on = false;
   DevBuf<unsigned long long> stats;
-  int mlp_mode = 0;  // render decoder: 0 exact f32 SIMT (bit-faithful sums), 1 tcgen05 split-bf16 (3-term, f32 accumulate)
+  int mlp_mode = 0;  // render decoder: 0 exact f32 SIMT (bit-faithful sums), 1 tcgen05 split-bf16 (3-term,
+                     // f32 accumulate), 2 = 1 with fp16 hash-table gathers
+  DevBuf<__half2> grid_h2;  // fp16 copy of the hash table (mode 2), refreshed per render
   cudaStream_t stream = nullptr;
   std::vector<HostBone> bones;
   GridCfg grid{};

@@ -300,8 +300,9 @@ def test_cpp_dropin_adapter():
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("mode", ["tcgen05", "tcgen05_fp16"])
 @pytest.mark.parametrize("structured", [False, True])
-def test_render_tcgen05_decoder(gpu, ref, structured):
+def test_render_tcgen05_decoder(gpu, ref, structured, mode):
     """The tcgen05 (split-bf16, fp32-accumulate) decoder against the reference render.
     Stated tolerance (north_star: 1e-3 relative): |d| <= 1e-3 * |ref| + 1e-5 per pixel."""
     sk = fx.smpl24()
@@ -320,7 +321,7 @@ def test_render_tcgen05_decoder(gpu, ref, structured):
     occ = arf.build_model_inference_grid(dm, pose, cfg)
     rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, cfg)
     opt = arf.RenderOptions(samples_per_ray=128)
-    dm.set_mlp_mode("tcgen05")
+    dm.set_mlp_mode(mode)
     try:
         img = arf.render_model(dm, pose, cam, occ, opt)
     finally:
