@@ -186,10 +186,25 @@ def run_ours(args):
     model.set_mlp_mode(args.mlp)
     arf.render_model(model, views[0], cam, occ, opt, rank, world)
 
+    # multi-GPU: each rank builds one z-slab of the per-pose occupancy grid, the slabs are
+    # all-gathered over NCCL (1 MiB of f32 values) and every rank re-thresholds / dilates
+    shard_grid = world > 1 and not args.no_shard_grid and occ_cfg.resolution % world == 0
+    if shard_grid:
+        from paper_2212_10550_b200.trainer import device_view
+        occ_vals = device_view(occ.device_arrays()[0], occ.cell_count())
+        slab = occ.cell_count() // world
+        my_slab = occ_vals[rank * slab:(rank + 1) * slab]
+
     def frame(i, slot):
         v = views[i % N_FRAMES]
-        check(L.arfx_build_inference_grid_device(model._h, v._h, occ._h,
-                                                 C.c_void_p(d_cnt[slot, 0].data_ptr()), sp))
+        if shard_grid:
+            check(L.arfx_build_inference_grid_shard_device(model._h, v._h, occ._h, rank, world,
+                                                           C.c_void_p(d_cnt[slot, 0].data_ptr()), sp))
+            dist.all_gather_into_tensor(occ_vals, my_slab)
+            check(L.arfx_occ_rebuild_mask_async(occ._h, sp))
+        else:
+            check(L.arfx_build_inference_grid_device(model._h, v._h, occ._h,
+                                                     C.c_void_p(d_cnt[slot, 0].data_ptr()), sp))
         check(L.arfx_render_model_device(model._h, v._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
                                          C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
                                          C.c_void_p(d_cnt[slot, 1].data_ptr()), sp))
@@ -280,7 +295,9 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f64+f32",
                 "data": "synthetic (random-init avatar, synthetic animation poses)",
                 "config": {"workload": WORKLOAD, "l2": "flushed between timed frames (256 MB write)",
-                           "parallelism": f"rays sharded over {world} GPU(s), 16-row interleaved tiles"},
+                           "parallelism": f"rays sharded over {world} GPU(s), 16-row interleaved tiles"
+                           + (", occupancy grid z-slab sharded + NCCL all-gather" if shard_grid else
+                              (", occupancy grid built redundantly per rank" if world > 1 else ""))},
                 "posed_samples_per_s": posed_all / (total_ms / 1000.0),
                 "rays_per_s": npix * K / (total_ms / 1000.0),
                 "kernels_ms_per_frame": {k: v[0] / K for k, v in prof.items()},
@@ -614,6 +631,8 @@ def main():
     ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "tcgen05_fp16", "exact"],
                     help="render decoder for `value` (the other one is reported as other_decoder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shard-grid", action="store_true",
+                    help="N > 1: build the occupancy grid redundantly on every rank instead of z-slab shards")
     ap.add_argument("--dp-train", action="store_true",
                     help="N > 1: also time the data-parallel SPEC train step (config 5) over NCCL")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")

@@ -205,6 +205,16 @@ int arfx_build_inference_grid(arfx_model m, arfx_pose p, arfx_occ_grid g, arfx_c
 /* asynchronous variant: counters (u64 x4: posed, canonical, pool, overflow) to device memory */
 int arfx_build_inference_grid_device(arfx_model m, arfx_pose p, arfx_occ_grid g,
                                      uint64_t* d_counters, void* stream);
+/* Multi-GPU: the inference grid's cell values for z-slab `shard` of
+ * `n_shards` only (slices [res*shard/n, res*(shard+1)/n)); all-gather the values across ranks
+ * (arfx_occ_device_arrays: z-major, so slabs are contiguous) and then rebuild the mask with
+ * arfx_occ_rebuild_mask_async. Per-cell values are bit-identical to the full build. */
+int arfx_build_inference_grid_shard_device(arfx_model m, arfx_pose p, arfx_occ_grid g, int shard, int n_shards,
+                                           uint64_t* d_counters, void* stream);
+/* device pointers of the occupancy values [z][y][x] f32 and mask u8 */
+int arfx_occ_device_arrays(arfx_occ_grid g, float** values, uint8_t** mask);
+/* threshold + dilation of the current values, asynchronous on stream */
+int arfx_occ_rebuild_mask_async(arfx_occ_grid g, void* stream);
 int arfx_update_training_grid(arfx_model m, const arfx_pose* poses, int n_poses, double decay,
                               uint64_t seed, uint64_t step, arfx_occ_grid g, arfx_counters* c,
                               void* stream);

@@ -410,6 +410,12 @@ class OccupancyGrid:
         self.density_threshold = thr.value
         self.dilation = dil.value
 
+    def device_arrays(self):
+        """(values f32 [z][y][x], mask u8) device pointers."""
+        v, m = C.c_void_p(), C.c_void_p()
+        call("arfx_occ_device_arrays", self._h, C.byref(v), C.byref(m))
+        return v.value, m.value
+
     @staticmethod
     def _from_handle(h) -> "OccupancyGrid":
         g = OccupancyGrid.__new__(OccupancyGrid)
@@ -499,6 +505,13 @@ def build_model_inference_grid(model: Model, pose: SkeletonPose, cfg: OccupancyC
     model.counters.posed_queries += cnt.posed_queries
     model.counters.canonical_queries += cnt.canonical_queries
     return g
+
+
+def build_inference_grid_shard(model: Model, view: "PosedModelView", grid: OccupancyGrid, shard: int,
+                               n_shards: int, stream=None) -> None:
+    """Cell values of z-slab `shard` of `n_shards` (multi-GPU: all-gather the values, then
+    grid.rebuild_mask()); asynchronous on `stream` (NULL: the library stream)."""
+    call("arfx_build_inference_grid_shard_device", model._h, view._h, grid._h, shard, n_shards, None, stream)
 
 
 def update_training_grid(model: Model, grid: OccupancyGrid, poses: Sequence[SkeletonPose], decay: float,

@@ -784,6 +784,34 @@ int arfx_build_inference_grid_device(arfx_model mh, arfx_pose ph, arfx_occ_grid 
   });
 }
 
+int arfx_build_inference_grid_shard_device(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, int shard,
+                                           int n_shards, uint64_t* d_counters, void* stream) {
+  return guard([&] {
+    require(mh && ph, "build_inference_grid_shard: null argument");
+    require(n_shards >= 1 && shard >= 0 && shard < n_shards, "build_inference_grid_shard: bad shard");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    inference_grid_shard(m, ph->impl, occ_ref(gh), shard, n_shards, reinterpret_cast<unsigned long long*>(d_counters),
+                         stream_of(m, stream));
+  });
+}
+
+int arfx_occ_device_arrays(arfx_occ_grid gh, float** values, uint8_t** mask) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    if (values) *values = g.values.ptr;
+    if (mask) *mask = g.mask.ptr;
+  });
+}
+
+int arfx_occ_rebuild_mask_async(arfx_occ_grid gh, void* stream) {
+  return guard([&] {
+    OccImpl& g = occ_ref(gh);
+    ARFX_CUDA(cudaSetDevice(g.device));
+    occ_rebuild(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses, double decay,
                               uint64_t seed, uint64_t step, arfx_occ_grid gh, arfx_counters* c, void* stream) {
   return guard([&] {

@@ -179,6 +179,8 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
                   cudaStream_t s);
 void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d_counters,
                     cudaStream_t s);
+void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int n_shards,
+                          unsigned long long* d_counters, cudaStream_t s);
 void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,
                           uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
                           cudaStream_t s);

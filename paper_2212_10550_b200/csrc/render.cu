@@ -304,13 +304,14 @@ struct AosSrc {  // user batch of xyz triples (inverse_lbs API / microbench)
 
 struct CellSrc {  // cell centres of an occupancy grid  R/occupancy.hpp:53-58, :141-144
   static constexpr bool kSinglePose = true;
-  int rx, ry, rz;
+  int rx, ry, rz;       // rz: z-slices of this (possibly sharded) range
   double lo[3], cs[3];
+  int z0 = 0;           // first z-slice (multi-GPU z-slab shard)
   __device__ long long count() const { return static_cast<long long>(rx) * ry * rz; }
   __device__ d3 point(long long i, int& pose) const {
     pose = 0;
     const int ix = static_cast<int>(i % rx), iy = static_cast<int>((i / rx) % ry),
-              iz = static_cast<int>(i / (static_cast<long long>(rx) * ry));
+              iz = z0 + static_cast<int>(i / (static_cast<long long>(rx) * ry));
     return make3(dadd(lo[0], dmul(dadd(static_cast<double>(ix), 0.5), cs[0])),
                  dadd(lo[1], dmul(dadd(static_cast<double>(iy), 0.5), cs[1])),
                  dadd(lo[2], dmul(dadd(static_cast<double>(iz), 0.5), cs[2])));
@@ -1075,6 +1076,34 @@ void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d
   ARFX_CUDA(cudaGetLastError());
   occ_rebuild(g, s);
   m.prof.end(s);
+  if (d_counters)
+    ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, s));
+}
+
+// z-slab shard of the inference grid (multi-GPU): cell values for slices
+// [z0, z1) only; the caller all-gathers the values (z-major layout: slabs are contiguous)
+// and rebuilds the mask (threshold + dilation) on the full grid. Bit-identical per cell.
+void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int n_shards,
+                          unsigned long long* d_counters, cudaStream_t s) {
+  Workspace& w = m.ws;
+  const int z0 = static_cast<int>(static_cast<long long>(g.res) * shard / n_shards);
+  const int z1 = static_cast<int>(static_cast<long long>(g.res) * (shard + 1) / n_shards);
+  const long long plane = static_cast<long long>(g.res) * g.res;
+  const long long n = plane * (z1 - z0);
+  w.ensure(static_cast<size_t>(std::max<long long>(n, 1)), 0);
+  ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
+  if (n > 0) {
+    CellSrc src{g.res, g.res, z1 - z0, {}, {}, z0};
+    occ_source_common(g, src.lo, src.cs);
+    launch_deform(m, p.dev.ptr, src, n, s);
+    launch_field_pool(m, s, n);
+    m.prof.begin("occ_values+mask", s);
+    occ_values_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.snroot.ptr, w.sbase.ptr, w.pres.ptr,
+                                                         g.values.ptr + plane * z0, 1.0f, 0);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+  }
   if (d_counters)
     ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToDevice, s));

@@ -330,3 +330,28 @@ def test_render_tcgen05_decoder(gpu, ref, structured, mode):
     assert rrgb.max() > 1e-3  # the frame is not empty
     np.testing.assert_allclose(img.rgb, rrgb, rtol=1e-3, atol=PIX_ATOL)
     np.testing.assert_allclose(img.alpha, ralpha, rtol=1e-3, atol=PIX_ATOL)
+
+
+@pytest.mark.parametrize("n_shards", [2, 4, 8])
+def test_inference_grid_z_slab_shards(gpu, n_shards):
+    """Multi-GPU occupancy: the z-slab shards, written into one grid and re-thresholded,
+    equal the single-GPU build bit for bit (values and mask)."""
+    import ctypes as C
+    from paper_2212_10550_b200._lib import call
+    sk = fx.smpl24()
+    m = gpu.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    pose = fx.random_pose(sk, fx.CONFIG1_POSE_SEED)
+    view = arf.PosedModelView(m, pose)
+    full = arf.build_model_inference_grid(m, pose, arf.OccupancyConfig(), view)
+    part = arf.OccupancyGrid(m.normalized_box, arf.OccupancyConfig())
+    import torch
+    st = torch.cuda.Stream()  # one stream orders the shard builds and the mask rebuild
+    sp = C.c_void_p(st.cuda_stream)
+    for s in range(n_shards):
+        arf.build_inference_grid_shard(m, view, part, s, n_shards, sp)
+    call("arfx_occ_rebuild_mask_async", part._h, sp)
+    st.synchronize()
+    fv, fm = full.download()
+    pv, pm = part.download()
+    assert np.array_equal(fv.view(np.uint32), pv.view(np.uint32))
+    assert np.array_equal(fm, pm) and fm.sum() > 0
