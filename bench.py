@@ -154,7 +154,7 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_dist_paths:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2212_10550_b200 import arf, fixtures as fx
     from paper_2212_10550_b200._lib import ArfxCounters, call, check, lib
@@ -188,7 +188,7 @@ def run_ours(args):
 
     # multi-GPU: each rank builds one z-slab of the per-pose occupancy grid, the slabs are
     # all-gathered over NCCL (1 MiB of f32 values) and every rank re-thresholds / dilates
-    shard_grid = world > 1 and not args.no_shard_grid and occ_cfg.resolution % world == 0
+    shard_grid = (world > 1 or args.force_dist_paths) and not args.no_shard_grid and occ_cfg.resolution % world == 0
     if shard_grid:
         from paper_2212_10550_b200.trainer import device_view
         occ_vals = device_view(occ.device_arrays()[0], occ.cell_count())
@@ -324,13 +324,13 @@ def run_ours(args):
             line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
                                      "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline),
                                      "train_step_full": bench_train_full(30)}
-    if world > 1 and args.dp_train:
-        # config 5 (data-parallel training over NCCL); opt-in: the only multi-rank path that
-        # cannot be exercised on this single-GPU development pool
+    if (world > 1 or args.force_dist_paths) and not args.no_dp_train:
+        # config 5: data-parallel SPEC training over NCCL (reduce-scatter grads, sharded Adam,
+        # all-gather params); also run at N = 1 under torchrun with --force-dist-paths
         dp = bench_train_full(20, rank, world, None)
         if rank == 0:
             line["extra_configs"] = {"train_step_dp": dp}
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
@@ -631,10 +631,12 @@ def main():
     ap.add_argument("--mlp", default="tcgen05", choices=["tcgen05", "tcgen05_fp16", "exact"],
                     help="render decoder for `value` (the other one is reported as other_decoder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist-paths", action="store_true",
+                    help="exercise the multi-GPU code paths (grid all-gather, DP train) at N = 1 under torchrun")
     ap.add_argument("--no-shard-grid", action="store_true",
                     help="N > 1: build the occupancy grid redundantly on every rank instead of z-slab shards")
-    ap.add_argument("--dp-train", action="store_true",
-                    help="N > 1: also time the data-parallel SPEC train step (config 5) over NCCL")
+    ap.add_argument("--no-dp-train", action="store_true",
+                    help="N > 1: skip the data-parallel SPEC train step side measurement (config 5)")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
