@@ -7,7 +7,7 @@ import json
 import sys
 
 GROUPS = {"deform": ["start_newton_kernel"], "prune": ["start_mask_kernel", "start_key_kernel", "start_place_kernel"],
-          "finalize": ["finalize_pool_kernel"], "field": ["field_tile_kernel"], "field_tc": ["field_tc_kernel"],
+          "finalize": ["finalize_pool_kernel"], "field": ["field_tile_kernel"], "field_tc": ["field_tc_kernel"], "encode_tc": ["encode_tiles_kernel"],
           "march": ["march_kernel"], "composite": ["composite_kernel"]}
 
 
