@@ -20,17 +20,21 @@ def main(src, dst):
     d = json.load(open(src))
     out = {}
     for name, kernels in GROUPS.items():
-        per_src = {}
+        # per source kind (CellSrc: occupancy grid, ListSrc: render): mean per launch of each
+        # kernel of the group, summed over the group's kernels; then averaged over the kinds
+        per = {}
         for k, v in d.items():
             if "dram__bytes_read.sum" not in v:
                 continue
             for kern in kernels:
                 if kern in k:
-                    srckind = "CellSrc" if "CellSrc" in k else "ListSrc"
-                    per_src[srckind] = per_src.get(srckind, 0.0) + mb(v["dram__bytes_read.sum"]) + mb(
-                        v["dram__bytes_write.sum"])
-        if per_src:
-            out[name] = sum(per_src.values()) / len(per_src)
+                    kind = "CellSrc" if "CellSrc" in k else "ListSrc"
+                    per.setdefault((kind, kern), []).append(mb(v["dram__bytes_read.sum"]) + mb(v["dram__bytes_write.sum"]))
+        kinds = {}
+        for (kind, kern), xs in per.items():
+            kinds[kind] = kinds.get(kind, 0.0) + sum(xs) / len(xs)
+        if kinds:
+            out[name] = sum(kinds.values()) / len(kinds)
     out["_note"] = ("DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum), ncu --set full "
                     "--clock-control none, cold serialized replay; from " + src)
     json.dump(out, open(dst, "w"), indent=1)
