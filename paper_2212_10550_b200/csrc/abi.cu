@@ -885,20 +885,34 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
                    t_rb->alpha.ptr, nullptr, s);
       unsigned long long hcnt[8];
       d2h(hcnt, m.ws.counters.ptr, 8, s);
+      // this shard's row tiles (other shards' rows are left untouched), enqueued behind the
+      // counters so one synchronisation covers both; on overflow the frame re-runs and
+      // copies again. Full tiles of a shard are one strided 2-D copy per image.
+      const int W = hc.width, H = hc.height, T = 16;
+      const int full_tiles = H / T;  // tiles 0..full_tiles-1 have T rows
+      const int first = shard;        // tiles of this shard: first, first + nshards, ...
+      const int n_full = first < full_tiles ? (full_tiles - 1 - first) / nshards + 1 : 0;
+      if (n_full > 0) {
+        const size_t off = static_cast<size_t>(first) * T * W;
+        const size_t pitch3 = static_cast<size_t>(nshards) * T * W * 3 * sizeof(float);
+        const size_t pitch1 = static_cast<size_t>(nshards) * T * W * sizeof(float);
+        ARFX_CUDA(cudaMemcpy2DAsync(rgb + off * 3, pitch3, t_rb->rgb.ptr + off * 3, pitch3,
+                                    static_cast<size_t>(T) * W * 3 * sizeof(float), static_cast<size_t>(n_full),
+                                    cudaMemcpyDeviceToHost, s));
+        ARFX_CUDA(cudaMemcpy2DAsync(alpha + off, pitch1, t_rb->alpha.ptr + off, pitch1,
+                                    static_cast<size_t>(T) * W * sizeof(float), static_cast<size_t>(n_full),
+                                    cudaMemcpyDeviceToHost, s));
+      }
+      if (H % T && full_tiles % nshards == shard) {  // the partial last tile
+        const size_t off = static_cast<size_t>(full_tiles) * T * W;
+        const size_t rows = static_cast<size_t>(H % T);
+        d2h(rgb + off * 3, t_rb->rgb.ptr + off * 3, rows * W * 3, s);
+        d2h(alpha + off, t_rb->alpha.ptr + off, rows * W, s);
+      }
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hcnt, rerun);
       if (rerun) continue;
-      // copy this shard's row tiles (other shards' rows are left untouched)
-      const int W = hc.width;
-      for (int y0 = 0; y0 < hc.height; y0 += 16) {
-        if ((y0 / 16) % nshards != shard) continue;
-        const int rows = std::min(16, hc.height - y0);
-        const size_t off = static_cast<size_t>(y0) * W;
-        d2h(rgb + off * 3, t_rb->rgb.ptr + off * 3, static_cast<size_t>(rows) * W * 3, s);
-        d2h(alpha + off, t_rb->alpha.ptr + off, static_cast<size_t>(rows) * W, s);
-      }
-      ARFX_CUDA(cudaStreamSynchronize(s));
       if (c) {
         c->posed_queries = hcnt[0];
         c->canonical_queries = hcnt[1];
