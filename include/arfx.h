@@ -200,6 +200,10 @@ int arfx_occ_upload(arfx_occ_grid g, const float* values, const uint8_t* mask);
 int arfx_occ_rebuild_mask(arfx_occ_grid g, void* stream); /* R/occupancy.hpp:87-91 */
 /* OccupancyGrid::is_occupied (R/occupancy.hpp:81-85) over a batch of normalized points */
 int arfx_occ_is_occupied(arfx_occ_grid g, const double* pts, int64_t n, uint8_t* out);
+/* build_model_inference_grid (R/model.hpp:138-148). With c != NULL it synchronises and
+ * reports the query counters; with c == NULL it reserves worst-case workspace and returns
+ * without a host round trip (the grid is complete for later work on the same stream; the
+ * host-buffer accessors arfx_occ_download / arfx_render_model synchronise). */
 int arfx_build_inference_grid(arfx_model m, arfx_pose p, arfx_occ_grid g, arfx_counters* c,
                               void* stream);
 /* asynchronous variant: counters (u64 x4: posed, canonical, pool, overflow) to device memory */

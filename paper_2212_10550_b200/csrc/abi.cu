@@ -734,6 +734,7 @@ int arfx_occ_upload(arfx_occ_grid gh, const float* values, const uint8_t* mask) 
   return guard([&] {
     OccImpl& g = occ_ref(gh);
     ARFX_CUDA(cudaSetDevice(g.device));
+    ARFX_CUDA(cudaDeviceSynchronize());  // order after asynchronous builds on model streams
     const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
     if (values) ARFX_CUDA(cudaMemcpy(g.values.ptr, values, n * sizeof(float), cudaMemcpyHostToDevice));
     if (mask) ARFX_CUDA(cudaMemcpy(g.mask.ptr, mask, n, cudaMemcpyHostToDevice));
@@ -744,6 +745,7 @@ int arfx_occ_rebuild_mask(arfx_occ_grid gh, void* stream) {
   return guard([&] {
     OccImpl& g = occ_ref(gh);
     ARFX_CUDA(cudaSetDevice(g.device));
+    if (!stream) ARFX_CUDA(cudaDeviceSynchronize());  // legacy stream: order after model streams
     occ_rebuild(g, static_cast<cudaStream_t>(stream));
     ARFX_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   });
@@ -755,6 +757,15 @@ int arfx_build_inference_grid(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, arf
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
     const cudaStream_t s = stream_of(m, stream);
+    if (!c) {
+      // no counters requested: reserve the worst case (every cell keeps 8 roots / starts on
+      // every bone) so nothing can overflow, and return without a host round trip; the grid
+      // is complete for any later work on the same stream
+      const OccImpl& g = occ_ref(gh);
+      m.ws.reserve_worst(static_cast<size_t>(g.res) * g.res * g.res, static_cast<size_t>(m.sv.nb));
+      inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
+      return;
+    }
     for (int attempt = 0; attempt < 3; ++attempt) {
       inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
       unsigned long long hc[8];
@@ -1005,6 +1016,7 @@ int arfx_occ_is_occupied(arfx_occ_grid gh, const double* pts, int64_t n, uint8_t
     require(n == 0 || (pts && out), "occ_is_occupied: null argument");
     ARFX_CUDA(cudaSetDevice(g.device));
     if (n <= 0) return;
+    ARFX_CUDA(cudaDeviceSynchronize());  // a grid built asynchronously on a model stream
     Staged<double> P;
     P.up(pts, static_cast<size_t>(3 * n), nullptr);
     DevBuf<uint8_t> o;
