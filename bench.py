@@ -195,7 +195,7 @@ def run_ours(args):
         slab = occ.cell_count() // world
         my_slab = occ_vals[rank * slab:(rank + 1) * slab]
 
-    def frame(i, slot):
+    def frame_direct(i, slot):
         v = views[i % N_FRAMES]
         if shard_grid:
             check(L.arfx_build_inference_grid_shard_device(model._h, v._h, occ._h, rank, world,
@@ -208,6 +208,38 @@ def run_ours(args):
         check(L.arfx_render_model_device(model._h, v._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
                                          C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
                                          C.c_void_p(d_cnt[slot, 1].data_ptr()), sp))
+
+    # CUDA-graph frames: the frame's ~40 launches captured once for one pose handle; each frame
+    # copies its (device-resident) pose context into that handle and replays (kernels read the
+    # pose from device memory). With grid shards the NCCL all-gather sits between two graphs.
+    gview = arf.PosedModelView(model, poses[0])
+    g_cnt = torch.zeros((2, 4), dtype=torch.int64, device="cuda")
+
+    def make_graphs():
+        hs = []
+        if args.no_graph:
+            return hs
+        for pmask in ([2, 4 | 8] if shard_grid else [1 | 8]):
+            h = C.c_void_p()
+            check(L.arfx_frame_graph_create(model._h, gview._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
+                                            pmask, C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
+                                            C.c_void_p(g_cnt.data_ptr()), sp, C.byref(h)))
+            hs.append(h)
+        return hs
+
+    graphs = make_graphs()
+
+    def frame_graph(i, slot):
+        # `graphs` is looked up at call time (re-captured for the other decoder below)
+        check(L.arfx_pose_copy(gview._h, views[i % N_FRAMES]._h, sp))
+        check(L.arfx_frame_graph_launch(graphs[0], sp))
+        if shard_grid:
+            dist.all_gather_into_tensor(occ_vals, my_slab)
+            check(L.arfx_frame_graph_launch(graphs[1], sp))
+        d_cnt[slot].copy_(g_cnt)
+
+    def frame(i, slot):
+        return frame_graph(i, slot) if graphs else frame_direct(i, slot)
 
     def timed_frames(k0, n):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
@@ -223,8 +255,6 @@ def run_ours(args):
     for i in range(Wm):
         frame(i, i)
     torch.cuda.synchronize()
-    check(L.arfx_profile_enable(model._h, 1))
-    _ = read_profile(model, L)  # reset
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else local)
@@ -241,12 +271,20 @@ def run_ours(args):
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
+    # per-kernel device times (libarfx events around each launch) on an untimed direct pass
+    # over the same frames
+    check(L.arfx_profile_enable(model._h, 1))
+    _ = read_profile(model, L)  # reset
+    for k in range(K):
+        flush.zero_()
+        frame_direct(Wm + k, Wm + K + 1)
+    torch.cuda.synchronize()
     prof = read_profile(model, L)
     check(L.arfx_profile_enable(model._h, 0))
     # deterministic work counts of the same K frames (re-run untimed with counters on)
     check(L.arfx_stats_enable(model._h, 1))
     for k in range(K):
-        frame(Wm + k, Wm + K)
+        frame_direct(Wm + k, Wm + K)
     torch.cuda.synchronize()
     stats = np.zeros(16, np.uint64)
     check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
@@ -275,12 +313,18 @@ def run_ours(args):
     # e2e through the host-buffer public API
     e2e = run_e2e(args, model, poses, cam, opt, occ, rank, world, views)
 
-    # the same frames with the other render decoder (exact f32 SIMT MLP vs tcgen05)
-    other = "exact" if args.mlp == "tcgen05" else "tcgen05"
+    # the same frames with the other render decoder (exact f32 SIMT MLP vs tcgen05); the
+    # decoder is part of the captured graph, so the graphs are re-captured for it
+    other = "exact" if args.mlp != "exact" else "tcgen05"
     model.set_mlp_mode(other)
+    main_graphs = graphs
+    graphs = make_graphs()
     for i in range(2):
         frame(i, i)
     ms_other = timed_frames(Wm, K)
+    for h in graphs:
+        check(L.arfx_frame_graph_destroy(h))
+    graphs = main_graphs
     if world > 1:
         t2 = torch.tensor([ms_other], dtype=torch.float64, device="cuda")
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -306,6 +350,7 @@ def run_ours(args):
                 "gpu_launches_per_frame": launches_per_frame,
                 "peaks_kind": peak_kind,
                 "render_decoder": args.mlp,
+                "frame_launch": "cuda_graph (pose copied into the captured handle per frame)" if graphs else "direct",
                 "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}
         rays_rank = sum(1 for y in range(H_IMG) if (y // 16) % world == rank) * W_IMG
         dom, per_kernel = roofline(prof, stats, K, rays_rank, opt.samples_per_ray, posed, peaks, peak_kind,
@@ -633,6 +678,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist-paths", action="store_true",
                     help="exercise the multi-GPU code paths (grid all-gather, DP train) at N = 1 under torchrun")
+    ap.add_argument("--no-graph", action="store_true", help="launch each frame's kernels directly (no CUDA graph)")
     ap.add_argument("--no-shard-grid", action="store_true",
                     help="N > 1: build the occupancy grid redundantly on every rank instead of z-slab shards")
     ap.add_argument("--no-dp-train", action="store_true",

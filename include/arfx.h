@@ -136,6 +136,7 @@ typedef struct { /* everything arf::Model<float> holds besides the big arrays */
 typedef struct arfx_model_s* arfx_model;      /* device-resident arf::Model<float> */
 typedef struct arfx_pose_s* arfx_pose;        /* device-resident PosedModelView   */
 typedef struct arfx_occ_s* arfx_occ_grid;     /* device-resident OccupancyGrid    */
+typedef struct arfx_frame_graph_s* arfx_frame_graph; /* a captured frame (CUDA graph)   */
 
 /* ---- library / errors ------------------------------------------------ */
 const char* arfx_last_error(void);
@@ -347,6 +348,22 @@ int arfx_model_flat(arfx_model m, float** params, float** grads, float** adam_m,
 /* Host copies of the flat Adam moments (n_flat floats each; checkpoint / resume). */
 int arfx_model_get_adam(arfx_model m, float* adam_m, float* adam_v);
 int arfx_model_set_adam(arfx_model m, const float* adam_m, const float* adam_v);
+
+/* ---- CUDA-graph frames ---------------------------------------------------------------- */
+
+enum { ARFX_GRAPH_GRID = 1, ARFX_GRAPH_GRID_SHARD = 2, ARFX_GRAPH_MASK = 4, ARFX_GRAPH_RENDER = 8 };
+/* Captures the chosen parts of one frame for pose handle p as a CUDA graph: the inference
+ * grid (GRID) or its z-slab shard (GRID_SHARD), the mask rebuild (MASK), the render into
+ * device buffers (RENDER; d_counters [2][4] may be NULL). Every kernel reads the pose from
+ * its device PoseContext, so after updating the handle in place (arfx_pose_update,
+ * arfx_pose_copy) a replay renders the new pose. `stream` must be non-NULL (capture). */
+int arfx_frame_graph_create(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                            const arfx_render_options* opt, int shard, int n_shards, int parts, float* d_rgb,
+                            float* d_alpha, uint64_t* d_counters, void* stream, arfx_frame_graph* out);
+int arfx_frame_graph_launch(arfx_frame_graph g, void* stream);
+int arfx_frame_graph_destroy(arfx_frame_graph g);
+/* dst <- src (same model): host and device PoseContext, asynchronous on stream */
+int arfx_pose_copy(arfx_pose dst, arfx_pose src, void* stream);
 
 /* ---- checkpoint / wire format --- */
 

@@ -176,6 +176,11 @@ _PROTOS = {
     "arfx_occ_create_raw": (C.c_int, [c_double_p, c_double_p, C.c_int, C.c_double, C.c_int, C.POINTER(H)]),
     "arfx_checkpoint_save": (C.c_int, [C.c_char_p, H, H, C.c_int64, C.c_int]),
     "arfx_checkpoint_load": (C.c_int, [C.c_char_p, C.POINTER(H), C.POINTER(H), C.POINTER(C.c_int64)]),
+    "arfx_pose_copy": (C.c_int, [H, H, P]),
+    "arfx_frame_graph_create": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int,
+                                          C.c_int, C.c_int, P, P, P, P, C.POINTER(H)]),
+    "arfx_frame_graph_launch": (C.c_int, [H, P]),
+    "arfx_frame_graph_destroy": (C.c_int, [H]),
     "arfx_figure_query": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, C.c_int64, c_double_p,
                                     c_double_p]),
     "arfx_figure_render": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, c_double_p, c_double_p,

@@ -23,6 +23,15 @@ struct arfx_pose_s {
 struct arfx_occ_s {
   arfx::OccImpl impl;
 };
+struct arfx_frame_graph_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int device = 0;
+  ~arfx_frame_graph_s() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
 
 namespace arfx {
 
@@ -874,6 +883,101 @@ int arfx_render_model_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam
                  opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha,
                  reinterpret_cast<unsigned long long*>(d_counters), stream_of(m, stream));
   });
+}
+
+// ---- CUDA-graph frames -------------------------------------------------------------------
+// The pose is read by every kernel from its device PoseContext, so a graph captured for a
+// pose handle replays correctly after the handle is updated in place (arfx_pose_update /
+// arfx_pose_copy). The workspace is sized by an uncaptured warm-up run of the same parts.
+
+int arfx_pose_copy(arfx_pose dst, arfx_pose src, void* stream) {
+  return guard([&] {
+    require(dst && src, "pose_copy: null pose");
+    require(dst->impl.model == src->impl.model, "pose_copy: poses of different models");
+    ModelImpl& m = *dst->impl.model;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    dst->impl.host = src->impl.host;
+    ARFX_CUDA(cudaMemcpyAsync(dst->impl.dev.ptr, src->impl.dev.ptr, sizeof(PoseCtx), cudaMemcpyDeviceToDevice,
+                              stream_of(m, stream)));
+  });
+}
+
+int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                            const arfx_render_options* opt, int shard, int nshards, int parts, float* d_rgb,
+                            float* d_alpha, uint64_t* d_counters, void* stream, arfx_frame_graph* out) {
+  return guard([&] {
+    require(mh && ph && out, "frame_graph_create: null argument");
+    require(parts > 0 && (parts & ~(ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK | ARFX_GRAPH_RENDER)) == 0,
+            "frame_graph_create: bad parts");
+    require(!((parts & ARFX_GRAPH_GRID) && (parts & ARFX_GRAPH_GRID_SHARD)), "frame_graph_create: grid or shard");
+    require(!(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK)) || occ,
+            "frame_graph_create: the grid parts need an occupancy grid");
+    require(!(parts & ARFX_GRAPH_RENDER) || (d_rgb && d_alpha && opt), "frame_graph_create: render outputs");
+    ModelImpl& m = mh->impl;
+    HostCamera hc{};
+    if (parts & ARFX_GRAPH_RENDER) {
+      hc = camera_of(cam);
+      validate_render(hc, opt, shard, nshards);
+    }
+    require(nshards >= 1 && shard >= 0 && shard < nshards, "frame_graph_create: bad shard");
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    require(s != nullptr, "frame_graph_create: needs a non-NULL stream");
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counters);
+    auto enqueue = [&] {
+      if (parts & ARFX_GRAPH_GRID) inference_grid(m, ph->impl, occ->impl, cnt, s);
+      if (parts & ARFX_GRAPH_GRID_SHARD) inference_grid_shard(m, ph->impl, occ->impl, shard, nshards, cnt, s);
+      if (parts & ARFX_GRAPH_MASK) occ_rebuild(occ->impl, s);
+      if (parts & ARFX_GRAPH_RENDER)
+        render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+                     opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha,
+                     cnt ? cnt + 4 : nullptr, s);
+    };
+    // warm-up (uncaptured): sizes the workspace for the worst case of the grid parts and
+    // sets kernel attributes; the render workspace grows from its counters if needed
+    if (occ && (parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD)))
+      m.ws.reserve_worst(static_cast<size_t>(occ->impl.res) * occ->impl.res * occ->impl.res,
+                         static_cast<size_t>(m.sv.nb));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      enqueue();
+      unsigned long long hcnt[8];
+      d2h(hcnt, m.ws.counters.ptr, 8, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hcnt, rerun);
+      if (!rerun) break;
+    }
+    const bool prof = m.prof.on;
+    m.prof.on = false;  // no event records inside the graph
+    auto g = std::make_unique<arfx_frame_graph_s>();
+    g->device = m.device;
+    ARFX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(s, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      m.prof.on = prof;
+      throw;
+    }
+    ARFX_CUDA(cudaStreamEndCapture(s, &g->graph));
+    m.prof.on = prof;
+    ARFX_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+    *out = g.release();
+  });
+}
+
+int arfx_frame_graph_launch(arfx_frame_graph g, void* stream) {
+  return guard([&] {
+    require(g && g->exec, "frame_graph_launch: null graph");
+    ARFX_CUDA(cudaSetDevice(g->device));
+    ARFX_CUDA(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int arfx_frame_graph_destroy(arfx_frame_graph g) {
+  return guard([&] { delete g; });
 }
 
 int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,

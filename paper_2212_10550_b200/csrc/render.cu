@@ -95,7 +95,7 @@ __device__ __forceinline__ bool occupied(const OccView& g, d3 x) {
 
 struct MarchArgs {
   CameraView cam;
-  double w2n[12];
+  const PoseCtx* pose;  // world -> normalized rigid read from device memory (graph-replayable)
   double nlo[3], nhi[3];
   OccView occ;
   int has_occ;
@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
   extern __shared__ unsigned march_bal[];  // [256 rays][K]
   __shared__ int wsum[kMarchWarps];
   __shared__ long long bbase;
+  __shared__ double w2n[12];
+  if (threadIdx.x < 12) w2n[threadIdx.x] = A.pose->w2n[threadIdx.x];
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_rays = A.lpx ? A.n_list : static_cast<long long>(A.n_rows) * A.W;
   const int K = (A.N + 31) >> 5;
@@ -160,14 +163,14 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
       }
       pix = py * A.W + px;
       rid = A.lpx ? static_cast<int>(r) : pix;
-      R = make_ray(A.cam, A.w2n, A.nlo, A.nhi, px, py);
+      R = make_ray(A.cam, w2n, A.nlo, A.nhi, px, py);
       R.valid = R.valid && A.N > 0;
       if (R.valid) {
         step = ddiv(dsub(R.tf, R.tn), static_cast<double>(A.N));
         if (A.stratified) rng = keyed_rng(A.seed, A.frame, static_cast<uint64_t>(pix));
         // cell-space ray: v(t) = P + Q t ~ (G^-1 (o + d t) - lo) / e * res (fast path only)
-        const d3 on = rigid_apply(A.w2n, R.o);
-        const d3 dn = matvec(A.w2n, R.d);
+        const d3 on = rigid_apply(w2n, R.o);
+        const d3 dn = matvec(w2n, R.d);
         const double sx = A.occ.inv_e[0] * A.occ.rx, sy = A.occ.inv_e[1] * A.occ.ry, sz = A.occ.inv_e[2] * A.occ.rz;
         cP = make3((on.x - A.occ.lo[0]) * sx, (on.y - A.occ.lo[1]) * sy, (on.z - A.occ.lo[2]) * sz);
         cQ = make3(dn.x * sx, dn.y * sy, dn.z * sz);
@@ -197,8 +200,8 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
             const int cy = cell_from_v(__fma_rn(Qy, t, Py), A.occ.ry);
             const int cz = cell_from_v(__fma_rn(Qz, t, Pz), A.occ.rz);
             if (cx == -2 || cy == -2 || cz == -2) {
-              const RayGeom Rj = make_ray(A.cam, A.w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
-              f = occupied(A.occ, rigid_apply(A.w2n, add3(Rj.o, mul3(Rj.d, t))));
+              const RayGeom Rj = make_ray(A.cam, w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
+              f = occupied(A.occ, rigid_apply(w2n, add3(Rj.o, mul3(Rj.d, t))));
             } else if (cx >= 0 && cy >= 0 && cz >= 0) {
               f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
             }
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
             double delta;
             if (i + 1 < A.N) delta = dsub(sample_t(tn, st, i + 1, jitter_at(A, rg, i + 1)), t);
             else delta = dsub(tf, t);
-            const d3 xn = rigid_apply(A.w2n, add3(o, mul3(d, t)));
+            const d3 xn = rigid_apply(w2n, add3(o, mul3(d, t)));
             A.sx[pos] = xn.x;
             A.sy[pos] = xn.y;
             A.sz[pos] = xn.z;
@@ -893,7 +896,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   MarchArgs A{};
   A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
   for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
-  for (int k = 0; k < 12; ++k) A.w2n[k] = p.host.w2n[k];
+  A.pose = p.dev.ptr;
   A.nlo[0] = m.norm.lo.x;
   A.nlo[1] = m.norm.lo.y;
   A.nlo[2] = m.norm.lo.z;
@@ -959,7 +962,7 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   MarchArgs A{};
   A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
   for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
-  for (int k = 0; k < 12; ++k) A.w2n[k] = p.host.w2n[k];
+  A.pose = p.dev.ptr;
   A.nlo[0] = m.norm.lo.x;
   A.nlo[1] = m.norm.lo.y;
   A.nlo[2] = m.norm.lo.z;

@@ -355,3 +355,38 @@ def test_inference_grid_z_slab_shards(gpu, n_shards):
     pv, pm = part.download()
     assert np.array_equal(fv.view(np.uint32), pv.view(np.uint32))
     assert np.array_equal(fm, pm) and fm.sum() > 0
+
+
+def test_frame_graph_replays_updated_poses(gpu):
+    """A frame captured as a CUDA graph (grid + render) replays new poses copied into the
+    same handle: images and masks equal the direct (uncaptured) calls bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_2212_10550_b200._lib import call
+    sk = fx.smpl24()
+    m = gpu.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = [fx.random_pose(sk, 1000 + i) for i in range(3)]
+    views = [arf.PosedModelView(m, p) for p in poses]
+    gview = arf.PosedModelView(m, poses[0])
+    cam = fx.default_camera(sk, 96, 96)
+    opt = arf.RenderOptions()
+    occ = arf.OccupancyGrid(m.normalized_box, arf.OccupancyConfig())
+    st = torch.cuda.Stream()
+    sp = C.c_void_p(st.cuda_stream)
+    rgb = torch.zeros(96 * 96 * 3, device="cuda")
+    alpha = torch.zeros(96 * 96, device="cuda")
+    g = C.c_void_p()
+    call("arfx_frame_graph_create", m._h, gview._h, C.byref(cam.to_c()), occ._h, C.byref(opt.to_c()), 0, 1,
+         1 | 8, C.c_void_p(rgb.data_ptr()), C.c_void_p(alpha.data_ptr()), None, sp, C.byref(g))
+    try:
+        for p, v in zip(poses, views):
+            call("arfx_pose_copy", gview._h, v._h, sp)
+            call("arfx_frame_graph_launch", g, sp)
+            st.synchronize()
+            ref_occ = arf.build_model_inference_grid(m, p, arf.OccupancyConfig())
+            ref_img = arf.render_model(m, p, cam, ref_occ, opt)
+            assert np.array_equal(occ.mask, ref_occ.mask)
+            assert np.array_equal(rgb.cpu().numpy().reshape(96, 96, 3), ref_img.rgb)
+            assert np.array_equal(alpha.cpu().numpy().reshape(96, 96), ref_img.alpha)
+    finally:
+        call("arfx_frame_graph_destroy", g)
