@@ -29,7 +29,10 @@
 
 namespace arfx {
 
-constexpr int kDsThreads = 128;
+#ifndef ARFX_DS_THREADS
+#define ARFX_DS_THREADS 128
+#endif
+constexpr int kDsThreads = ARFX_DS_THREADS;
 #ifndef ARFX_NEWTON_POSE_SMEM
 #define ARFX_NEWTON_POSE_SMEM 1
 #endif
