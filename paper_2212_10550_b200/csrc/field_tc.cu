@@ -380,11 +380,7 @@ bool field_tc_supported(const FieldView& F) {
 
 void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   const size_t smem = TcSmem::TOTAL + 1024;  // + alignment slack
-  static bool attr = false;
-  if (!attr) {
-    ARFX_CUDA(cudaFuncSetAttribute(field_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(field_tc_kernel), smem);
   int sms = 148, dev = 0;
   ARFX_CUDA(cudaGetDevice(&dev));
   ARFX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -212,6 +212,10 @@ struct LossTargets {
 void loss_reduce(const double* d_terms, long long n, const LossTargets& lt, double* d_out4, cudaStream_t s);
 void ray_losses(long long n, const float* d_rgb, const float* d_alpha, const LossTargets& lt, float* d_grad_rgb,
                 float* d_grad_alpha, cudaStream_t s);
+// Raises `kernel`'s dynamic shared-memory limit on the current device to at least `bytes`
+// (per device and kernel, thread-safe; a no-op when already high enough).
+void ensure_dyn_smem(const void* kernel, size_t bytes);
+
 // L_density (render.cu): forward (points + posed query), backward (loss + K8)
 void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step,
                      cudaStream_t s);

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdio>
 
 #include "deform.cuh"
@@ -765,13 +767,9 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     return;
   }
   if (field_is_standard_host(m.fv)) {
-    static bool attr_set = false;
     const size_t smem = field_tile_smem(m.fv);
     auto kern = field_tile_kernel<16, 64>;
-    if (!attr_set) {
-      ARFX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      attr_set = true;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     int per_sm = 0;
     ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFieldTile, smem));
     const long long tiles = (n_hint + kFieldTile - 1) / kFieldTile;
@@ -1253,6 +1251,18 @@ KernelProfiler::~KernelProfiler() {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : free_events) cudaEventDestroy(e);
+}
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  ARFX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = done[{kernel, dev}];
+  if (bytes <= cur) return;
+  ARFX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  cur = bytes;
 }
 
 // ---- L_density: occupancy-based regulariser (Eq. 12) ----------

@@ -498,12 +498,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
                      256, 0, s>>>(flag, d_n, cap, w.bwd_list.ptr, w.bwd_n.ptr);
   const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
-  static bool team_attr = false;
-  if (!team_attr) {
-    ARFX_CUDA(cudaFuncSetAttribute(field_bwd_team_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(team_smem)));
-    team_attr = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
   ARFX_CUDA(cudaGetLastError());
