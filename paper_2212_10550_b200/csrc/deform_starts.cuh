@@ -371,12 +371,21 @@ struct RootsSink {  // batched inverse_lbs API: every root + residual, [n][8]
 __device__ __forceinline__ void ds_gather_roots(long long s, const uint32_t* mask_in, const uint32_t* slot_base,
                                                 const double4* res, double dedup, Roots& R, long long cap) {
   R.count = 0;
-  const int c = __popc(mask_in[s]);
   const long long b0 = slot_base[s];
-  for (int j = 0; j < c && b0 + j < cap; ++j) {
-    const double4 v = res[b0 + j];
-    if (v.w < 0.0) continue;
-    roots_push(R, make3(v.x, v.y, v.z), v.w, dedup);
+  const int c = static_cast<int>(min(static_cast<long long>(__popc(mask_in[s])), cap - b0));
+  // the first four start results are loaded before any push (independent loads in flight;
+  // most targets have <= 4 starts), the rest one at a time; pushes stay in bone order
+  double4 v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (j < c) v[j] = res[b0 + j];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (j < c && v[j].w >= 0.0) roots_push(R, make3(v[j].x, v[j].y, v[j].z), v[j].w, dedup);
+  for (int j = 4; j < c; ++j) {
+    const double4 w = res[b0 + j];
+    if (w.w < 0.0) continue;
+    roots_push(R, make3(w.x, w.y, w.z), w.w, dedup);
   }
 }
 
