@@ -357,6 +357,8 @@ def run_ours(args):
                                    (p64.value, p32.value))
         line["roofline"] = dom
         line["roofline_kernels"] = per_kernel
+        if os.environ.get("ARFX_ROOFLINE_MD"):
+            Path(os.environ["ARFX_ROOFLINE_MD"]).write_text(roofline_table(per_kernel))
         line["work_counts"] = {"evals": int(stats[0]), "union_bone_visits": int(stats[1]),
                                "newton_steps": int(stats[2]), "starts": int(stats[3]),
                                "exact_prune_tests": int(stats[4]), "field_queries": int(stats[5]),
@@ -467,8 +469,25 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
     entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")
+    # K2d finalize: per start its 32-B result read, per pool entry its 36-B canonical root +
+    # owner + result slot written, per target 9 B of mask / count / base (HBM)
+    n_targets = posed + 64 ** 3 * K  # render samples + occupancy cells
+    entry("finalize", "hbm", 32.0 * S + 36.0 * (Q + QT) + 9.0 * n_targets, "GB/s", hbm,
+          f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "32 B/start + 36 B/pool entry + 9 B/target")
     dom = max(out.values(), key=lambda e: e["ms_per_launch"] * e["launches"]) if out else None
     return dom, out
+
+
+def roofline_table(per_kernel) -> str:
+    """Markdown table of every kernel group's roofline fraction (profiles/roofline_r1.md)."""
+    rows = ["| kernel | bound | achieved | peak | unit | frac | ms/launch | launches | DRAM bytes/launch (ncu) |",
+            "|---|---|---|---|---|---|---|---|---|"]
+    for k, e in sorted(per_kernel.items(), key=lambda kv: -kv[1]["ms_per_launch"] * kv[1]["launches"]):
+        tr = e.get("traffic")
+        rows.append(f"| {k} | {e['bound']} | {e['achieved']:.3g} | {e['peak']:.4g} | {e['unit']} | "
+                    f"{(e['frac'] or 0):.3f} | {e['ms_per_launch']:.4f} | {e['launches']} | "
+                    f"{'-' if tr is None else f'{tr / 1e6:.1f} MB'} |")
+    return "\n".join(rows) + "\n"
 
 
 def run_e2e(args, model, poses, cam, opt, occ, rank, world, views):
