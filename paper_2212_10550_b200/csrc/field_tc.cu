@@ -125,7 +125,8 @@ struct TcSmem {  // byte offsets inside the dynamic smem; each operand = hi plan
   static constexpr int B2 = B1 + 2 * B1P;                   // W2p 16 x 64  (2 x 2 KB)
   static constexpr int BIAS = B2 + 2 * B2P;                 // b0[64] b1[64] b2[4]
   static constexpr int ACT = BIAS + 1024;                   // per group: hidden 128 x 64 (2 x 16 KB);
-  static constexpr int ACT_BYTES = 2 * A1P;                 //   the 128 x 32 features alias its start
+  static constexpr int ACT_BYTES = 2 * A0P + 2 * A1P;       //   + its own feature tile (2 x 8 KB), so the
+                                                            //   next tile's bulk copy overlaps this one
   static constexpr int MBAR = ACT + kGroups * ACT_BYTES;    // u64 [kGroups]: MMA completion
   static constexpr int LBAR = MBAR + 8 * kGroups;           // u64 [kGroups]: feature-tile load
   static constexpr int TADDR = LBAR + 8 * kGroups;          // u32
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
   const uint32_t mbar = sbase + TcSmem::MBAR + 8 * g;
   const uint32_t lbar = sbase + TcSmem::LBAR + 8 * g;
   uint32_t* taddr_smem = reinterpret_cast<uint32_t*>(tc_smem + TcSmem::TADDR);
-  const int A1 = TcSmem::ACT + g * TcSmem::ACT_BYTES, A0 = A1;  // byte offsets of this group's tile
+  const int A0 = TcSmem::ACT + g * TcSmem::ACT_BYTES, A1 = A0 + 2 * TcSmem::A0P;  // this group's tiles
 
   // ---- stage the weights in the K-major operand layouts (W[o][i] is N x K, K-major) ----
   const float* W0 = F.mlp;
@@ -285,21 +286,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
     *reinterpret_cast<uint4*>(tc_smem + base + plane + kmaj_off(tid, c, kTcTile)) = *reinterpret_cast<const uint4*>(lo);
   };
 
-  for (long long t0 = (static_cast<long long>(blockIdx.x) * kGroups + g) * kTcTile; t0 < n;
-       t0 += static_cast<long long>(gridDim.x) * kGroups * kTcTile) {
-    // ---- feature tile (16 KB, hi + lo planes) from the encode stage: one bulk copy ----
+  constexpr uint32_t kTileBytes = 2 * TcSmem::A0P;
+  auto load_tile = [&](long long t) {  // one bulk copy of a 16-KB feature tile into A0
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lbar), "n"(kTileBytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sbase + A0),
+        "l"(tiles + (t / kTcTile) * kTileBytes), "n"(kTileBytes), "r"(lbar)
+        : "memory");
+  };
+  const long long stride = static_cast<long long>(gridDim.x) * kGroups * kTcTile;
+  const long long first = (static_cast<long long>(blockIdx.x) * kGroups + g) * kTcTile;
+  if (tid == 0 && first < n) load_tile(first);
+  for (long long t0 = first; t0 < n; t0 += stride) {
     const long long q = t0 + tid;
     const bool ok = q < n && owner[q] >= 0;
-    if (tid == 0) {
-      constexpr uint32_t kBytes = 2 * TcSmem::A0P;
-      const unsigned char* src = tiles + (t0 / kTcTile) * kBytes;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lbar), "n"(kBytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sbase + A0),
-          "l"(src), "n"(kBytes), "r"(lbar)
-          : "memory");
-    }
-    mbar_wait(lbar, lphase);
+    mbar_wait(lbar, lphase);  // this tile's features have landed in A0
     lphase ^= 1;
     // ---- layer 0 ----
     if (tid == 0) {
@@ -310,6 +311,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
     mbar_wait(mbar, phase);
     phase ^= 1;
     tc_fence_after();
+    // A0 is free again: the next tile's copy overlaps the rest of this one
+    if (tid == 0 && t0 + stride < n) load_tile(t0 + stride);
     // ---- epilogue 0: + b0, ReLU -> A1 ----
 #pragma unroll
     for (int c = 0; c < kHid; c += 16) {
