@@ -1,22 +1,30 @@
-// field_tc.cu -- K3 on the 5th-gen tensor cores: encode + 32-64-64-4 decoder with
-// tcgen05.mma (kind::f16 on split-bf16 operands, fp32 accumulate in TMEM), one 128-query tile (M = 128) per
-// iteration of a persistent 128-thread CTA.
+// field_tc.cu -- K3 on the 5th-gen tensor cores, in two stages:
+//
+//   encode_tiles_kernel  thread = query, 16 hash-grid levels (warp-uniform level, exact f64
+//                        corner weights as field_tile_kernel); the 32 features are split into
+//                        bf16 hi / lo planes and written straight into the UMMA K-major,
+//                        no-swizzle canonical layout of their 128-query tile in global memory
+//                        (coalesced 512-B stores). High occupancy: this stage is the gathers.
+//   field_tc_kernel      the 32-64-64-4 decoder: one persistent 512-thread CTA per SM runs 4
+//                        independent 128-query pipelines (own TMEM columns, mbarriers, named
+//                        barrier) over weights staged once in smem. Per tile:
+//     load     one cp.async.bulk of the 16-KB feature tile into the group's A0 buffer (the
+//              next tile's copy is issued as soon as layer 0 has consumed A0)
+//     layer 0  D[128x64] = A0[128x32] * W0^T    2 K-steps x 3 MMAs, TMEM cols [0, 64)
+//     epi 0    tcgen05.ld, + b0, ReLU -> A1 planes
+//     layer 1  D[128x64] = A1[128x64] * W1^T    4 x 3 MMAs, TMEM cols [0, 64) (D0 consumed)
+//     epi 1    + b1, ReLU -> A1 (in place: the layer-1 MMAs have completed)
+//     layer 2  D[128x16] = A1[128x64] * W2p^T   4 x 3 MMAs, W2 padded to N = 16, cols [64, 80)
+//     epi 2    + b2, softplus / logistic (R/field.hpp:78-81) -> (density, rgb)
+//   One thread issues the MMAs (tcgen05.mma kind::f16); completion is signalled with
+//   tcgen05.commit on an mbarrier.
 //
 // Operands are split bf16 pairs (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)) and every
-// product is formed as hi*hi + hi*lo + lo*hi with kind::f16 MMAs (bf16 in, fp32 accumulate
-// in TMEM): ~16 significant bits, i.e. ~1e-5 relative, for the same shared-memory
-// footprint as one fp32 operand.
-//   encode   thread = query, warp-uniform level (as field_tile_kernel); features go straight
-//            into the UMMA K-major, no-swizzle canonical layout of A0 (hi and lo planes)
-//   layer 0  D[128x64] = A0[128x32] * W0^T    2 K-steps x 3 MMAs, TMEM cols [0, 64)
-//   epi 0    tcgen05.ld, + b0, ReLU -> A1 planes
-//   layer 1  D[128x64] = A1[128x64] * W1^T    4 x 3 MMAs, TMEM cols [0, 64) (D0 consumed)
-//   epi 1    + b1, ReLU -> A1 (in place: the layer-1 MMAs have completed)
-//   layer 2  D[128x16] = A1[128x64] * W2p^T   4 x 3 MMAs, W2 padded to N = 16, cols [64, 80)
-//   epi 2    + b2, softplus / logistic (R/field.hpp:78-81) -> (density, rgb)
-// One thread issues the MMAs; completion is signalled with tcgen05.commit on an mbarrier.
+// product is formed as hi*hi + hi*lo + lo*hi (bf16 in, fp32 accumulate in TMEM): ~16
+// significant bits, ~1e-5 relative, for the same smem footprint as one fp32 operand.
 // Not bit-exact with the reference's sequential f32 sums (stated tolerance);
 // the exact SIMT decoder (field_tile_kernel) stays the default (arfx_model_set_mlp_mode).
+// ARFX_MLP_TCGEN05_FP16 feeds the encode stage from an fp16 copy of the table.
 #include <cuda_runtime.h>
 
 #include <cuda_bf16.h>
