@@ -6,18 +6,16 @@
 // couples them. So:
 //
 //  K2a start_mask_kernel  thread per target: surviving-start mask (f32 bounding-sphere
-//                         reject + exact FP64 capsule distance), start count, and a
-//                         warp-aggregated per-bone histogram of starts.
-//  (scan)                 exclusive prefix of the start counts -> start slot of each target;
-//                         per-bone prefix -> bone-major item offsets.
-//  K2b start_scatter      item (target, bone) written bone-major: consecutive items are
-//                         spatially adjacent targets of the SAME bone, so a warp's lanes
-//                         start in the same canonical neighbourhood -> the skinning-cell
-//                         loads coalesce and the bone transforms are warp-uniform.
+//                         reject + exact FP64 capsule distance) and start count.
+//  (scan)                 exclusive prefix of the start counts -> start slot of each target.
+//  K2b start_key/place    counting sort of the (target, bone) items by (bone, skinning cell
+//                         of x0 = B_b^-1 x'): a warp's lanes start in the same cell rows, so
+//                         the cell-table gathers broadcast in L1.
 //  K2c start_newton       persistent warps over the items; per-lane state machine whose
-//                         unit of progress is one skinning eval (so lanes that converge
-//                         early take a new item instead of idling); result (root, residual
-//                         or "no root") written to the start's slot.
+//                         unit of progress is one skinning eval (lanes that converge early
+//                         take a new item instead of idling); the Newton step is taken right
+//                         after the eval that accepted x; result (root, residual or "no
+//                         root") written as one double4 to the start's slot.
 //  K2d finalize           thread per target: replays InverseRoots::push over its starts in
 //                         bone order (bit-exact dedup / replacement / kMaxRoots), then the
 //                         sink: in-box roots to the root pool (render / occupancy) or all

@@ -1,17 +1,21 @@
-// render.cu -- the per-frame hot path on sm_100a (exact SIMT path).
+// render.cu -- the per-frame hot path on sm_100a.
 //
 //   K1 march_kernel     generate_ray + to_normalized + ray_box + sample_points +
 //                       is_occupied (R/camera.hpp:61-70, R/render.hpp:15-37, :67-86,
-//                       R/occupancy.hpp:71-85), one warp per ray, ballot/popc
-//                       compaction of the occupied samples, one atomic per 8 rays.
-//   K2 deform_kernel    inverse_lbs_ctx + in-box filter of posed_query_ctx
-//                       (R/articulation.hpp:94-145, :163-181), FP64 exact; appends
-//                       the in-box roots of each posed sample to a compact root pool.
-//   K3 field_kernel     CanonicalField::query over the root pool (R/field.hpp:75-82).
+//                       R/occupancy.hpp:71-85): lane per ray for the ray setup, then warp
+//                       ballots over 32 samples at a time with an affine cell-space line
+//                       (exact reference arithmetic within 1e-12 of a cell edge); one
+//                       block-wide scan + atomic per block; exact recompute of occupied samples.
+//   K2 deformer         inverse_lbs_ctx + in-box filter of posed_query_ctx
+//                       (R/articulation.hpp:94-145, :163-181), FP64 exact, as the start
+//                       pipeline of deform_starts.cuh (prune, sort, Newton, finalize).
+//   K3 field            CanonicalField::query over the root pool (R/field.hpp:75-82): exact
+//                       field_tile_kernel, or the tcgen05 decoder (field_tc.cu) for renders.
 //   K4 composite_kernel max-density root selection (R/articulation.hpp:174) then
 //                       composite (R/render.hpp:98-119), one thread per ray.
-//   K5 occupancy        build_inference_grid / update_training_grid / rebuild_mask /
-//                       dilated_mask (R/occupancy.hpp:87-171) reuse K2 + K3.
+//   K5 occupancy        build_inference_grid (full or z-slab shard) / update_training_grid /
+//                       rebuild_mask / dilated_mask (R/occupancy.hpp:87-171) reuse K2 + K3.
+//   L_density           density_points / reduce / flag kernels + K2/K3/K8.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -6,18 +6,19 @@
 // then CanonicalField::query_backward (R/field.hpp:91-103) at every accumulated
 // non-skipped sample's selected canonical root, accumulated into FieldGrads.
 //
-//   K1..K3 as in render (march in ray-list mode, deformer, field forward over the pool)
-//   K7 train_composite_kernel  thread per ray: selection + composite forward (rgb, alpha,
-//                              terminated_at) + exact reverse pass; dsigma / dc land on the
-//                              selected root's pool entry (R/render.hpp:148-162)
-//   K8 field_backward_kernel   thread per flagged pool entry: exact forward recompute
-//                              (encode + MLP, activations in smem), reference-order MLP
-//                              backward per query (R/mlp.hpp:116-154); weight gradients
-//                              warp-reduced then one atomic per weight per warp; the
-//                              encode backward scatters w*up into the grid gradient with
-//                              f32 atomics (R/hash_grid.hpp:155-169).
-// Gradient sums are therefore order-different from the reference's serial per-thread
-// buffers (SPEC.md:426 allows reassociation); everything upstream is bit-exact.
+//   K1..K3 as in render (march in ray-list mode, deformer, exact field over the pool)
+//   K7  train_composite_kernel  thread per ray: selection + composite forward (rgb, alpha,
+//                               terminated_at), the SPEC losses and their gradient when
+//                               targets are given (losses.cuh), then the exact reverse
+//                               pass; dsigma / dc land on the selected root's pool entry
+//   K8a flag_list + field_bwd_team_kernel  64-thread team per 4 flagged queries: forward
+//                               recompute (bit-identical to K3), dprev chains in the
+//                               reference's order, per-query records of layer inputs/deltas
+//   K8c grid_scatter_kernel     warp-aggregated hash-grid scatter-add (R/hash_grid.hpp:155-169)
+//   K8b/K8d field_bwd_weights + weights_reduce  MLP weight gradients over the records,
+//                               register-accumulated per CTA, fixed-order row reduction
+// Gradient sums are order-different from the reference's serial per-thread buffers
+// (SPEC.md:426 allows reassociation); everything upstream is bit-exact.
 #include <cuda_runtime.h>
 
 #include <algorithm>
