@@ -701,6 +701,9 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   Workspace& w = m.ws;
   constexpr bool single = Src::kSinglePose;
   const long long n = std::max<long long>(n_hint, 1);
+  // items pack (target, bone) as target | bone << kItemBoneShift
+  if (n >= (1LL << kItemBoneShift))
+    throw std::invalid_argument("deformer: more than 2^26 posed points in one call (split the batch / frame)");
   // the batched inverse_lbs API runs asynchronously and cannot re-run: size its start slots
   // for the worst case (every bone survives pruning); render/occupancy learn from overflow
   const size_t worst = std::is_same<Sink, RootsSink>::value ? static_cast<size_t>(n) * m.sv.nb : 0;
