@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, con
                                                                 const int32_t* __restrict__ owner,
                                                                 float4* __restrict__ res,
                                                                 const unsigned long long* n_dev, long long cap,
-                                                                unsigned long long* stats) {
+                                                                unsigned long long* stats, long long team_max) {
   constexpr int IN = 2 * L;
   extern __shared__ float4 ft_smem4[];
   float* W0T = reinterpret_cast<float*>(ft_smem4);          // [IN][HID]
@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, con
   int* valid = reinterpret_cast<int*>(U + 3 * kFieldTile);
   long long n = static_cast<long long>(*n_dev);
   n = n < cap ? n : cap;
+  if (n <= team_max) return;  // small batch: field_team_kernel has it
   if (static_cast<long long>(blockIdx.x) * kFieldTile >= n) return;
   for (int i = threadIdx.x; i < IN * HID; i += kFieldTile) {  // W0 transposed
     const int o = i / IN, k = i % IN;
@@ -419,6 +420,99 @@ __global__ void __launch_bounds__(kFieldTile) field_tile_kernel(FieldView F, con
       res[t0 + threadIdx.x] = make_float4(softplus_f(logits[0]), logistic_f(logits[1]), logistic_f(logits[2]),
                                           logistic_f(logits[3]));
     }
+  }
+}
+
+// Small batches (occupancy grids: ~10^4 queries; training: ~10^4-10^5): the tile kernel's
+// thread-per-query MLP is a 13k-op serial chain per thread, so a few thousand queries leave
+// the GPU idle. Here a 64-thread team carries 4 queries: thread (query, level) encodes,
+// thread o computes hidden unit o of each layer (its sum in the reference's input order, so
+// the outputs are bit-identical to field_tile_kernel's), 4 chains per weight load.
+constexpr int kFtTeam = 64, kFtTeams = 4, kFtQ = 4;
+__global__ void __launch_bounds__(kFtTeam * kFtTeams) field_team_kernel(FieldView F, const double* __restrict__ px,
+                                                                        const double* __restrict__ py,
+                                                                        const double* __restrict__ pz,
+                                                                        const int32_t* __restrict__ owner,
+                                                                        float4* __restrict__ res,
+                                                                        const unsigned long long* n_dev, long long cap,
+                                                                        unsigned long long* stats, long long team_max) {
+  constexpr int IN = 32, HID = 64, W0S = IN + 1, W1S = HID + 1;
+  __shared__ float W0p[HID * W0S], W1p[HID * W1S], W2p[4 * W1S], Bs[2 * HID + 4];
+  __shared__ float X[kFtTeams][kFtQ][IN], H1[kFtTeams][kFtQ][HID], H2[kFtTeams][kFtQ][HID];
+  __shared__ int OK[kFtTeams][kFtQ];
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  if (n > team_max) return;  // large batch: field_tile_kernel has it
+  const float* W = F.mlp;
+  const float* W1g = W + IN * HID + HID;
+  const float* W2g = W1g + HID * HID + HID;
+  for (int e = threadIdx.x; e < HID * IN; e += blockDim.x) W0p[(e / IN) * W0S + e % IN] = __ldg(W + e);
+  for (int e = threadIdx.x; e < HID * HID; e += blockDim.x) W1p[(e / HID) * W1S + e % HID] = __ldg(W1g + e);
+  for (int e = threadIdx.x; e < 4 * HID; e += blockDim.x) W2p[(e / HID) * W1S + e % HID] = __ldg(W2g + e);
+  for (int e = threadIdx.x; e < HID; e += blockDim.x) {
+    Bs[e] = __ldg(W + IN * HID + e);
+    Bs[HID + e] = __ldg(W1g + HID * HID + e);
+  }
+  if (threadIdx.x < 4) Bs[2 * HID + threadIdx.x] = __ldg(W2g + 4 * HID + threadIdx.x);
+  __syncthreads();
+  const int team = threadIdx.x / kFtTeam, t = threadIdx.x % kFtTeam;
+  const int ej = t >> 4, el = t & 15;
+  for (long long k0 = (static_cast<long long>(blockIdx.x) * kFtTeams + team) * kFtQ; k0 < n;
+       k0 += static_cast<long long>(gridDim.x) * kFtTeams * kFtQ) {
+    {
+      const long long q = k0 + ej;
+      const bool ok = q < n && owner[q] >= 0;
+      if (el == 0) OK[team][ej] = ok;
+      if (ok) {
+        double u[3];
+        normalize_point(F, make3(px[q], py[q], pz[q]), u);
+        const float2 o = encode_level_f2(F, el, u);
+        X[team][ej][2 * el] = o.x;
+        X[team][ej][2 * el + 1] = o.y;
+      }
+      if (stats && el == 0 && ok) atomicAdd(stats + 5, 1ull);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kFtTeam) : "memory");
+    {
+      float a[kFtQ];
+#pragma unroll
+      for (int j = 0; j < kFtQ; ++j) a[j] = Bs[t];
+      for (int i = 0; i < IN; ++i) {
+        const float w = W0p[t * W0S + i];
+#pragma unroll
+        for (int j = 0; j < kFtQ; ++j) a[j] = fadd(a[j], fmul(w, X[team][j][i]));
+      }
+#pragma unroll
+      for (int j = 0; j < kFtQ; ++j) H1[team][j][t] = (a[j] < 0.0f) ? 0.0f : a[j];
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kFtTeam) : "memory");
+    {
+      float a[kFtQ];
+#pragma unroll
+      for (int j = 0; j < kFtQ; ++j) a[j] = Bs[HID + t];
+      for (int i = 0; i < HID; ++i) {
+        const float w = W1p[t * W1S + i];
+#pragma unroll
+        for (int j = 0; j < kFtQ; ++j) a[j] = fadd(a[j], fmul(w, H1[team][j][i]));
+      }
+#pragma unroll
+      for (int j = 0; j < kFtQ; ++j) H2[team][j][t] = (a[j] < 0.0f) ? 0.0f : a[j];
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kFtTeam) : "memory");
+    if (t < kFtQ) {  // thread j: the 4 logits of query j (R/field.hpp:78-81)
+      const int j = t;
+      if (OK[team][j]) {
+        float lg[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          float a = Bs[2 * HID + o];
+          for (int i = 0; i < HID; ++i) a = fadd(a, fmul(W2p[o * W1S + i], H2[team][j][i]));
+          lg[o] = a;
+        }
+        res[k0 + j] = make_float4(softplus_f(lg[0]), logistic_f(lg[1]), logistic_f(lg[2]), logistic_f(lg[3]));
+      }
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kFtTeam) : "memory");
   }
 }
 
@@ -782,10 +876,17 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     const long long tiles = (n_hint + kFieldTile - 1) / kFieldTile;
     const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sm_count()) *
                                                                         std::max(per_sm, 1))));
+    // the query count is only known on the device: both kernels are launched and exactly one
+    // of them runs, by the count (teams below kTeamMax queries, tiles above)
+    constexpr long long kTeamMax = 65536;
     m.prof.begin("field", s);
+    field_team_kernel<<<static_cast<unsigned>(sm_count() * 8), kFtTeam * kFtTeams, 0, s>>>(
+        m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr, m.ws.pres.ptr, m.ws.counters.ptr + 2,
+        static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax);
     kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
                                          m.ws.pres.ptr, m.ws.counters.ptr + 2,
-                                         static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr);
+                                         static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr,
+                                         kTeamMax);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
     return;
