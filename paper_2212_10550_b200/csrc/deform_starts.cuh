@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(256) start_key_kernel(SkinView S, const PoseCt
         keys[slot] = key;
         unsorted[slot] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
       }
-      atomicAdd(key_hist + key, 1u);
+      // warp-aggregated histogram: neighbouring targets' starts often share a key
+      const unsigned act = __activemask();
+      const unsigned grp = __match_any_sync(act, key);
+      if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(grp) - 1)) atomicAdd(key_hist + key, static_cast<uint32_t>(__popc(grp)));
     }
   }
 }
@@ -162,10 +165,21 @@ __global__ void __launch_bounds__(256) start_place_kernel(const unsigned long lo
                                                           uint32_t* __restrict__ items, long long cap) {
   long long n = static_cast<long long>(*n_starts);
   n = n < cap ? n : cap;
-  for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-       j += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const uint32_t pos = atomicAdd(key_cursor + keys[j], 1u);
-    if (pos < cap) items[pos] = unsorted[j];
+  const unsigned lane = threadIdx.x & 31;
+  for (long long j0 = static_cast<long long>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); j0 < n;
+       j0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long j = j0 + lane;
+    const bool act = j < n;
+    const uint32_t key = act ? keys[j] : 0xffffffffu;
+    // warp-aggregated: starts of neighbouring targets often share (bone, cell); one atomic
+    // per distinct key in the warp, ranks within the group by lane order
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(grp) - 1;
+    uint32_t base = 0;
+    if (act && static_cast<int>(lane) == leader) base = atomicAdd(key_cursor + key, static_cast<uint32_t>(__popc(grp)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const uint32_t pos = base + __popc(grp & ((1u << lane) - 1u));
+    if (act && pos < cap) items[pos] = unsorted[j];
   }
 }
 
