@@ -174,6 +174,18 @@ int arfx_model_set_params(arfx_model m, const float* grid_params, const float* m
  * occupancy grids, training and the query APIs always use the exact decoder. */
 enum { ARFX_MLP_EXACT = 0, ARFX_MLP_TCGEN05 = 1, ARFX_MLP_TCGEN05_FP16 = 2 };
 int arfx_model_set_mlp_mode(arfx_model m, int mode);
+/* Deterministic gradients (default off): the field backward visits the flagged queries in
+ * owner order (rays front to back / points) instead of atomic-compaction order, so the f32
+ * MLP weight-gradient sums are fixed, and the hash-grid scatter sums fixed-point int64
+ * contributions (each rounded to a multiple of 2^-46) instead of f32 atomics. Repeated
+ * train/density steps on the same inputs then give bit-identical gradients, Adam states
+ * and parameters. The grid sums stay in an accumulator until consumed: arfx_adam_step over
+ * the whole flat vector folds them in during its sweep, arfx_model_get_grads flushes them;
+ * code that reads the gradient arrays directly (arfx_model_device_arrays / arfx_model_flat,
+ * e.g. a data-parallel reduce-scatter) calls arfx_model_flush_grads first (async on
+ * `stream`). arfx_model_zero_grad discards pending sums. */
+int arfx_model_set_deterministic(arfx_model m, int on);
+int arfx_model_flush_grads(arfx_model m, void* stream);
 int arfx_model_zero_grad(arfx_model m, void* stream);
 int arfx_model_get_grads(arfx_model m, float* grid_grad, float* mlp_grad);
 /* device pointers of the parameter / gradient arrays (for NCCL / optimizers) */

@@ -256,6 +256,17 @@ class Model:
         Render only."""
         call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1, "tcgen05_fp16": 2}[mode])
 
+    def set_deterministic(self, on: bool = True) -> None:
+        """Bit-reproducible gradients (arfx_model_set_deterministic): owner-ordered backward
+        lists and fixed-point int64 hash-grid sums, so repeated train / density steps on the
+        same inputs give identical gradients, Adam states and parameters."""
+        call("arfx_model_set_deterministic", self._h, 1 if on else 0)
+
+    def flush_grads(self, stream=None) -> None:
+        """Deterministic mode: fold pending hash-grid sums into the gradient array (needed
+        before reading it through device pointers, e.g. a data-parallel reduce-scatter)."""
+        call("arfx_model_flush_grads", self._h, stream)
+
     def zero_grad(self):
         call("arfx_model_zero_grad", self._h, None)
 

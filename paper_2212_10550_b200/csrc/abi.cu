@@ -574,6 +574,20 @@ int arfx_model_set_mlp_mode(arfx_model mh, int mode) {
   });
 }
 
+int arfx_model_set_deterministic(arfx_model mh, int on) {
+  return guard([&] {
+    require(mh != nullptr, "set_deterministic: null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (!on && m.acc_pending) {
+      ARFX_CUDA(cudaDeviceSynchronize());
+      flush_grad_acc(m, m.stream);
+      ARFX_CUDA(cudaStreamSynchronize(m.stream));
+    }
+    m.det = on != 0;
+  });
+}
+
 int arfx_model_zero_grad(arfx_model mh, void* stream) {
   return guard([&] {
     require(mh != nullptr, "null model");
@@ -582,6 +596,19 @@ int arfx_model_zero_grad(arfx_model mh, void* stream) {
     ensure_grad_store(m, m.stream);
     const cudaStream_t s = stream_of(m, stream);
     ARFX_CUDA(cudaMemsetAsync(m.flat_grads.ptr, 0, m.n_flat * sizeof(float), s));
+    if (m.acc_pending) {  // pending deterministic-mode sums are discarded too
+      ARFX_CUDA(cudaMemsetAsync(m.grid_acc.ptr, 0, m.grid_acc.n * sizeof(long long), s));
+      m.acc_pending = false;
+    }
+  });
+}
+
+int arfx_model_flush_grads(arfx_model mh, void* stream) {
+  return guard([&] {
+    require(mh != nullptr, "flush_grads: null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    flush_grad_acc(m, stream_of(m, stream));
   });
 }
 
@@ -591,6 +618,10 @@ int arfx_model_get_grads(arfx_model mh, float* gg, float* mg) {
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
     require(m.grid_grad.ptr != nullptr, "no gradients accumulated yet (call arfx_model_zero_grad)");
+    if (m.acc_pending) {
+      ARFX_CUDA(cudaDeviceSynchronize());  // the backward may have run on a caller stream
+      flush_grad_acc(m, m.stream);
+    }
     if (gg) d2h(gg, m.grid_grad.ptr, m.n_grid, m.stream);
     if (mg) d2h(mg, m.mlp_grad.ptr, m.n_mlp, m.stream);
     ARFX_CUDA(cudaStreamSynchronize(m.stream));
@@ -1418,7 +1449,8 @@ int arfx_field_query_backward(arfx_model mh, const double* pts, int64_t n, const
     ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 1, static_cast<size_t>(n), s));
     const unsigned long long cnt = static_cast<unsigned long long>(n);
     h2d(w.counters.ptr + 2, &cnt, 1, s);
-    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(n), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr, s);
+    const BwdOwners own{static_cast<long long>(n), nullptr, nullptr, true};
+    field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(n), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr, s, &own);
     ARFX_CUDA(cudaStreamSynchronize(s));
   });
 }
@@ -1461,8 +1493,9 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
     w.ensure_train();
     ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
     train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
+    const BwdOwners own{n_rays, w.ray_first.ptr, w.ray_count.ptr, false};
     field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
-                        w.pgc.ptr, s);
+                        w.pgc.ptr, s, &own);
     return;
   }
   DevBuf<unsigned long long> bad;
@@ -1488,8 +1521,9 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
   w.ensure_train();
   ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
   train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
+  const BwdOwners own{n_rays, w.ray_first.ptr, w.ray_count.ptr, false};
   field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
-                      s);
+                      s, &own);
 }
 
 LossTargets loss_targets(const arfx_loss_config* cfg, const float* gt_rgb, const float* gt_alpha, double* terms) {

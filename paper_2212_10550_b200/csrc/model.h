@@ -84,6 +84,7 @@ struct Workspace {
   DevBuf<float> bwd_rec;   // K8a -> K8b: per flagged query, MLP layer inputs and deltas
   DevBuf<int32_t> bwd_list;  // flagged pool entries, compacted
   DevBuf<float> bwd_partial;  // K8b per-block MLP gradient rows
+  DevBuf<uint32_t> bwd_own;   // deterministic mode: per-owner flagged count -> list offset
   DevBuf<unsigned long long> bwd_n;
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
   void ensure(size_t posed, size_t pix);
@@ -122,6 +123,12 @@ struct ModelImpl {
   int mlp_mode = 0;  // render decoder: 0 exact f32 SIMT (bit-faithful sums), 1 tcgen05 split-bf16 (3-term,
                      // f32 accumulate), 2 = 1 with fp16 hash-table gathers
   DevBuf<__half2> grid_h2;  // fp16 copy of the hash table (mode 2), refreshed per render
+  // deterministic gradients (arfx_model_set_deterministic): K8b/K8c sum fixed-point int64
+  // contributions (exact, order-independent); grid_acc is the hash-grid accumulator, kept
+  // all-zero between steps (the drain pass takes and clears every touched row)
+  bool det = false;
+  DevBuf<long long> grid_acc;  // fixed-point hash-grid gradient, one per grid_grad element
+  bool acc_pending = false;    // grid_acc holds sums not yet folded into grid_grad
   cudaStream_t stream = nullptr;
   std::vector<HostBone> bones;
   GridCfg grid{};
@@ -230,8 +237,16 @@ double cosine_lr(double lr0, const AdamCfg& c, long long step);
 void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s);
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
                      float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt = nullptr);
+// Owner order of the flagged pool entries (deterministic mode): targets [first[o],
+// first[o]+count[o]) per owner o (nullptr: target o), or the pool entries themselves.
+struct BwdOwners {
+  long long n_owner;
+  const int32_t *first, *count;
+  bool pool_is_target;
+};
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
-                         const float* gs, const float* gc, cudaStream_t s);
+                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own);
+void flush_grad_acc(ModelImpl& m, cudaStream_t s);  // deterministic mode: grid_acc -> grid_grad
 
 // field_tc.cu
 bool field_tc_supported(const FieldView& F);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "fixed.cuh"
 #include "model.h"
 
 namespace arfx {
@@ -31,12 +32,28 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
   g = 0.0f;
 }
 
+// acc (deterministic mode, pending hash-grid sums): the first n4_acc float4s of the
+// gradient also take acc's fixed-point sums, which are cleared -- the same f32 expression
+// as flush_grad_acc (train.cu), so folding here or flushing first gives equal bits.
+template <bool Acc>
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ g,
                                                    float* __restrict__ m, float* __restrict__ v, long long b4,
-                                                   long long e4, AdamScalars k) {
+                                                   long long e4, AdamScalars k, longlong2* __restrict__ acc,
+                                                   long long n4_acc) {
   for (long long i = b4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < e4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float4 P = reinterpret_cast<float4*>(p)[i], G = reinterpret_cast<float4*>(g)[i];
+    if (Acc && i < n4_acc) {
+      const longlong2 a = acc[2 * i], b = acc[2 * i + 1];
+      if ((a.x | a.y | b.x | b.y) != 0) {
+        if (a.x) G.x = __fadd_rn(G.x, fix_to_f32(a.x));
+        if (a.y) G.y = __fadd_rn(G.y, fix_to_f32(a.y));
+        if (b.x) G.z = __fadd_rn(G.z, fix_to_f32(b.x));
+        if (b.y) G.w = __fadd_rn(G.w, fix_to_f32(b.y));
+        acc[2 * i] = make_longlong2(0, 0);
+        acc[2 * i + 1] = make_longlong2(0, 0);
+      }
+    }
     float4 M = reinterpret_cast<float4*>(m)[i], V = reinterpret_cast<float4*>(v)[i];
     const float lr = (4 * i >= k.mlp_off) ? k.lr_mlp : k.lr_grid;  // mlp_off % 64 == 0
     adam1(P.x, G.x, M.x, V.x, lr, k);
@@ -86,8 +103,17 @@ void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long blocks = std::min<long long>((e4 - b4 + 255) / 256, static_cast<long long>(sms) * 8);
   m.prof.begin("adam", s);
-  adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr,
-                                                              m.adam_v.ptr, b4, e4, k);
+  if (m.acc_pending && !(begin == 0 && end >= static_cast<long long>(m.grid_acc.n)))
+    flush_grad_acc(m, s);  // a shard cannot consume the whole accumulator
+  if (m.acc_pending) {
+    adam_kernel<true><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr, m.adam_v.ptr, b4, e4, k,
+        reinterpret_cast<longlong2*>(m.grid_acc.ptr), static_cast<long long>(m.grid_acc.n / 4));
+    m.acc_pending = false;
+  } else {
+    adam_kernel<false><<<static_cast<unsigned>(blocks), 256, 0, s>>>(m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr,
+                                                                     m.adam_v.ptr, b4, e4, k, nullptr, 0);
+  }
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }

@@ -1481,8 +1481,9 @@ void density_backward(ModelImpl& m, long long n, double w_density, double* d_out
                                                           w.pres.ptr, w.dens_scale.ptr, w.pgs.ptr, w.pgc.ptr,
                                                           w.pflag.ptr);
   ARFX_CUDA(cudaGetLastError());
+  const BwdOwners own{n, nullptr, nullptr, false};  // owner = density point = target
   field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
-                      s);
+                      s, &own);
 }
 
 }  // namespace arfx

@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "field.cuh"
+#include "fixed.cuh"
 #include "losses.cuh"
 #include "model.h"
 
@@ -167,6 +168,7 @@ constexpr int kRecDin = kBwdRec;                  // + d features (32) for the s
 constexpr int kRecStride = kBwdRec + kIn;         // floats per query record in global memory
 constexpr int kTeamSmem = kRecStride + kOut;      // record + d features + logits
 constexpr int kW0s = kIn + 1, kW1s = kHid + 1;  // padded row strides
+
 
 __global__ void flag_list_kernel(const uint8_t* __restrict__ pflag, const unsigned long long* n_dev, long long cap,
                                  int32_t* __restrict__ list, unsigned long long* n_list) {
@@ -349,13 +351,15 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
 // (spatially coherent: the pool follows ray order); lanes whose corner hits the same table
 // row are grouped with __match_any_sync and summed by shuffles, and one lane per distinct
 // row issues the atomics -- coarse (dense) levels collapse many contributions per row.
+template <bool Det>
 __global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const double* __restrict__ px,
                                                            const double* __restrict__ py,
                                                            const double* __restrict__ pz,
                                                            const int32_t* __restrict__ list,
                                                            const unsigned long long* n_list,
                                                            const float* __restrict__ rec,
-                                                           float* __restrict__ grid_grad) {
+                                                           float* __restrict__ grid_grad,
+                                                           long long* __restrict__ grid_acc) {
   const long long n = static_cast<long long>(*n_list);
   const int lane = threadIdx.x & 31;
   const long long chunks = (n + 31) / 32;
@@ -382,6 +386,23 @@ __global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const do
       const uint32_t key = has ? lc.idx[c] : 0xffffffffu;
       const float v0 = has ? fmul(lc.w[c], d0) : 0.0f, v1 = has ? fmul(lc.w[c], d1) : 0.0f;
       const unsigned g = __match_any_sync(0xffffffffu, key);
+      if (Det) {
+        // fixed point: exact integer sums, independent of which lanes / warps meet a row
+        const long long i0 = f32_to_fix(v0), i1 = f32_to_fix(v1);
+        long long a0 = 0, a1 = 0;
+        for (unsigned mm = g; mm; mm &= mm - 1) {
+          const int src = __ffs(mm) - 1;
+          a0 += __shfl_sync(g, i0, src);
+          a1 += __shfl_sync(g, i1, src);
+        }
+        if (has && lane == __ffs(g) - 1) {
+          unsigned long long* ga =
+              reinterpret_cast<unsigned long long*>(grid_acc + 2 * (static_cast<size_t>(l) * F.T + key));
+          atomicAdd(ga + 0, static_cast<unsigned long long>(a0));
+          atomicAdd(ga + 1, static_cast<unsigned long long>(a1));
+        }
+        continue;
+      }
       float s0 = 0.0f, s1 = 0.0f;
       for (unsigned mm = g; mm; mm &= mm - 1) {
         const int src = __ffs(mm) - 1;
@@ -394,6 +415,103 @@ __global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const do
       }
     }
   }
+}
+
+
+// Deterministic mode: the hash-grid gradient stays in grid_acc (exact int64 sums, one per
+// grid_grad element) until a consumer needs it -- Adam folds it in during its own sweep
+// (optim.cu); anything else calls flush_grad_acc, this sweep: grad += acc * 2^-46 and
+// acc = 0 wherever acc != 0 (same f32 expression as Adam's, so both give equal bits).
+__global__ void __launch_bounds__(256) grid_flush_kernel(long long n2, longlong2* __restrict__ acc,
+                                                         float2* __restrict__ grad) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n2;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const longlong2 a = acc[i];
+    if ((a.x | a.y) == 0) continue;
+    acc[i] = make_longlong2(0, 0);
+    float2 g = grad[i];
+    if (a.x) g.x = fadd(g.x, fix_to_f32(a.x));
+    if (a.y) g.y = fadd(g.y, fix_to_f32(a.y));
+    grad[i] = g;
+  }
+}
+
+// Deterministic K8 list: flagged pool entries in owner order (training: rays in batch
+// order, each ray's samples front to back; L_density: points; query_backward: the pool
+// itself), so the K8a records and K8b's per-CTA chunks -- hence the f32 weight-gradient
+// sums -- are the same on every run. Count (warp per owner) -> one-block scan -> write.
+struct OwnerRanges {
+  long long n_owner;
+  const int32_t *first, *count;  // target range per owner; nullptr: owner o = target o
+  bool pool_is_target;           // the pool entries are the targets (no root lists)
+};
+
+__device__ __forceinline__ long long owner_candidate(const OwnerRanges& O, const uint8_t* snroot,
+                                                     const int32_t* sbase, const uint8_t* pflag, long long t) {
+  if (O.pool_is_target) return pflag[t] ? t : -1;
+  const int nr = snroot[t];
+  if (nr == 0) return -1;
+  const long long b = sbase[t];
+  for (int k = 0; k < nr; ++k)
+    if (pflag[b + k]) return b + k;  // at most one root per target is flagged (the selected one)
+  return -1;
+}
+
+template <bool Write>
+__global__ void __launch_bounds__(256) owner_list_kernel(OwnerRanges O, const uint8_t* __restrict__ snroot,
+                                                         const int32_t* __restrict__ sbase,
+                                                         const uint8_t* __restrict__ pflag,
+                                                         uint32_t* __restrict__ cnt_or_off,
+                                                         int32_t* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  for (long long o = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; o < O.n_owner;
+       o += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const long long t0 = O.first ? O.first[o] : o;
+    const int nt = O.count ? O.count[o] : 1;
+    uint32_t run = Write ? cnt_or_off[o] : 0u;
+    for (int j0 = 0; j0 < nt; j0 += 32) {
+      const long long q = j0 + lane < nt ? owner_candidate(O, snroot, sbase, pflag, t0 + j0 + lane) : -1;
+      const unsigned b = __ballot_sync(0xffffffffu, q >= 0);
+      if (Write && q >= 0) list[run + __popc(b & ((1u << lane) - 1u))] = static_cast<int32_t>(q);
+      run += __popc(b);
+    }
+    if (!Write && lane == 0) cnt_or_off[o] = run;
+  }
+}
+
+__global__ void __launch_bounds__(1024) owner_scan_kernel(uint32_t* __restrict__ a, long long n,
+                                                          unsigned long long* __restrict__ total) {
+  __shared__ uint32_t ws[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (long long b0 = 0; b0 < n; b0 += 1024) {
+    const long long i = b0 + threadIdx.x;
+    const uint32_t v = i < n ? a[i] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = ws[lane];
+      uint32_t xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += t;
+      }
+      ws[lane] = xi - x;
+      if (lane == 31) ws[32] = xi;
+    }
+    __syncthreads();
+    if (i < n) a[i] = carry + ws[warp] + incl - v;
+    carry += ws[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
 }
 
 // K8b: MLP weight / bias gradients, gW[o][i] = sum_q delta[q][o] * in[q][i] and gb[o] =
@@ -484,7 +602,7 @@ int sms() {
 }  // namespace
 
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
-                         const float* gs, const float* gc, cudaStream_t s) {
+                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own) {
   if (!(m.fv.F == 2 && m.fv.in_dim == kIn && m.fv.hidden == kHid && m.fv.n_layers == 3 && m.fv.out_dim == kOut))
     throw std::invalid_argument("train path: libarfx implements the 32-64-64-4 decoder (levels*F == 32)");
   Workspace& w = m.ws;
@@ -494,25 +612,55 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   w.bwd_n.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
   m.prof.begin("field_backward", s);
-  flag_list_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((cap + 255) / 256,
-                                                                                       static_cast<long long>(sms()) * 8))),
-                     256, 0, s>>>(flag, d_n, cap, w.bwd_list.ptr, w.bwd_n.ptr);
+  if (m.det && own) {
+    w.bwd_own.ensure(static_cast<size_t>(std::max<long long>(own->n_owner, 1)));
+    OwnerRanges O{own->n_owner, own->first, own->count, own->pool_is_target};
+    const unsigned ob = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((own->n_owner + 7) / 8,
+                                                                                         sms() * 16LL)));
+    owner_list_kernel<false><<<ob, 256, 0, s>>>(O, w.snroot.ptr, w.sbase.ptr, flag, w.bwd_own.ptr, nullptr);
+    owner_scan_kernel<<<1, 1024, 0, s>>>(w.bwd_own.ptr, own->n_owner, w.bwd_n.ptr);
+    owner_list_kernel<true><<<ob, 256, 0, s>>>(O, w.snroot.ptr, w.sbase.ptr, flag, w.bwd_own.ptr, w.bwd_list.ptr);
+  } else {
+    flag_list_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((cap + 255) / 256,
+                                                                                         static_cast<long long>(sms()) * 8))),
+                       256, 0, s>>>(flag, d_n, cap, w.bwd_list.ptr, w.bwd_n.ptr);
+  }
   const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
   ARFX_CUDA(cudaGetLastError());
-  grid_scatter_kernel<<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(m.fv, w.px.ptr, w.py.ptr, w.pz.ptr,
-                                                                     w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr,
-                                                                     m.grid_grad.ptr);
   const int wblocks = sms() * 4;
+  if (m.det) {
+    const size_t n_acc = static_cast<size_t>(m.fv.L) * m.fv.T * 2;  // == n_grid
+    if (m.grid_acc.n < n_acc) {  // zeroed once; consumers leave it all-zero
+      m.grid_acc.alloc(n_acc);
+      ARFX_CUDA(cudaMemsetAsync(m.grid_acc.ptr, 0, n_acc * sizeof(long long), s));
+    }
+    grid_scatter_kernel<true><<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(
+        m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr,
+        m.grid_acc.ptr);
+    m.acc_pending = true;
+  } else {
+    grid_scatter_kernel<false><<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(
+        m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr, nullptr);
+  }
   w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
   field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
                                                                               w.bwd_partial.ptr);
   weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, s>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
+}
+
+void flush_grad_acc(ModelImpl& m, cudaStream_t s) {
+  if (!m.acc_pending) return;
+  const long long n2 = static_cast<long long>(m.grid_acc.n / 2);
+  grid_flush_kernel<<<static_cast<unsigned>(std::min<long long>((n2 + 255) / 256, sms() * 16LL)), 256, 0, s>>>(
+      n2, reinterpret_cast<longlong2*>(m.grid_acc.ptr), reinterpret_cast<float2*>(m.grid_grad.ptr));
+  ARFX_CUDA(cudaGetLastError());
+  m.acc_pending = false;
 }
 
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,

@@ -57,6 +57,7 @@ class TrainConfig:  # TrainConfig SPEC.md:450-453
     occupancy: arf.OccupancyConfig = field(default_factory=arf.OccupancyConfig)
     gt_oversample: int = 4               # SPEC scenegen: ground truth at 4x the training N
     density_points: int = 4096           # L_density point budget per step
+    deterministic: bool = False          # bit-reproducible gradients (Model.set_deterministic)
 
 
 class FlatDataParallel:
@@ -127,6 +128,7 @@ class Trainer:
             raise ValueError("rays_per_batch must divide by the number of ranks")
         self.n_local = cfg.rays_per_batch // world
         self.views = [arf.PosedModelView(model, p) for p in self.poses]
+        model.set_deterministic(cfg.deterministic)
         # ---- dataset: ground-truth frames of the analytic figure (device resident)
         W, H = camera.width, camera.height
         gt_opt = arf.RenderOptions(samples_per_ray=cfg.gt_oversample * cfg.samples_per_ray)
@@ -202,6 +204,8 @@ class Trainer:
         else:
             self.loss_d.zero_()
         t = self.step_id + 1
+        if cfg.deterministic and self.world > 1:
+            self.model.flush_grads(sp)  # the reduce-scatter reads the gradient array directly
         self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
         loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
                             self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
@@ -228,6 +232,26 @@ class Trainer:
         self.stream.synchronize()
         self._check()
         return torch_stack_cpu(self.torch, self._hist) if self._hist else np.zeros((0, 5))
+
+    def save(self, path) -> None:
+        """Checkpoint (model, Adam moments, occupancy grid, step) for an exact resume."""
+        self.stream.synchronize()
+        arf.save_checkpoint(path, self.model, self.grid, step=self.step_id, with_optimizer=True)
+
+    def restore(self, path) -> None:
+        """Resume from `save`: parameters, Adam moments, occupancy grid and step counter are
+        replaced, so the following steps draw the same ray batches (keyed by step) as an
+        uninterrupted run -- with TrainConfig.deterministic the continuation is bit-identical."""
+        self.stream.synchronize()
+        m2, occ, step = arf.load_checkpoint(path)
+        if occ is None:
+            raise ValueError("restore: checkpoint has no occupancy grid")
+        g, w, _ = m2.params()
+        self.model.set_params(g, w)
+        self.model.set_adam_state(*m2.adam_state())
+        m2.close()
+        self.grid = occ
+        self.step_id = int(step)
 
     def train(self, iterations: int | None = None):
         for _ in range(iterations or self.cfg.iterations):

@@ -239,3 +239,102 @@ def test_density_loss_descends_alone(gpu):
     h = tr.train()
     assert h[0, 3] > 0.01, h[0]
     assert h[-5:, 3].mean() < 0.5 * h[:5, 3].mean(), (h[:5, 3], h[-5:, 3])
+
+
+def _det_trainer(seed_model=21, iterations=24):
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig
+    sk = fx.default_figure_skeleton()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (20, 20, 20), seed_model)
+    poses = [fx.random_pose(sk, 400 + i, max_angle=0.3) for i in range(3)]
+    cam = fx.default_camera(sk, 48, 48)
+    cfg = TrainConfig(iterations=iterations, rays_per_batch=1024, samples_per_ray=64, occupancy_interval=8,
+                      deterministic=True, adam=arf.AdamConfig(total_steps=iterations))
+    return Trainer(m, fx.default_figure(), poses, cam, cfg)
+
+
+def test_deterministic_gradients(gpu):
+    """Model.set_deterministic: the same fused train step twice gives bit-identical grid and
+    MLP gradients (fixed-point int64 sums), within f32-reassociation distance of the default
+    f32-atomic gradients."""
+    sk = fx.default_figure_skeleton()
+    fig = fx.default_figure()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (24, 24, 24), 11)
+    pose = fx.random_pose(sk, 8, max_angle=0.3)
+    cam = fx.default_camera(sk, 96, 96)
+    occ = arf.OccupancyGrid(m.normalized_box, arf.OccupancyConfig())
+    arf.update_training_grid(m, occ, [pose], 0.95, 3, 0)
+    gt_img, mask = arf.figure_render(fig, pose, m.normalized_box, cam, arf.RenderOptions(samples_per_ray=256))
+    rng = np.random.default_rng(6)
+    n = 4096
+    px = rng.integers(0, 96, n).astype(np.int32)
+    py = rng.integers(0, 96, n).astype(np.int32)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=9, frame_id=4)
+    args = (m, pose, cam, occ, opt, px, py, gt_img.rgb[py, px], mask[py, px].astype(np.float32), arf.LossConfig())
+    m.zero_grad()
+    arf.train_step(*args)
+    g0, w0 = m.grads()
+    m.set_deterministic(True)
+    runs = []
+    for _ in range(3):
+        m.zero_grad()
+        arf.train_step(*args)
+        runs.append(m.grads())
+    for g, w in runs[1:]:
+        assert np.array_equal(g, runs[0][0]) and np.array_equal(w, runs[0][1])
+    g1, w1 = runs[0]
+    assert np.abs(g1).max() > 0 and np.abs(w1).max() > 0
+    np.testing.assert_allclose(w1, w0, rtol=1e-4, atol=1e-6 * np.abs(w0).max())
+    np.testing.assert_allclose(g1, g0, rtol=1e-4, atol=1e-6 * np.abs(g0).max())
+    # Adam folding the pending grid sums during its sweep == flushing them first
+    n = m.flat()["n_flat"]
+    p0 = m.params()
+    a0 = m.adam_state()
+    m.zero_grad()
+    arf.train_step(*args)
+    m.adam_step(arf.AdamConfig(), 1, 0, n)
+    pa = m.params()
+    m.set_params(p0[0], p0[1])
+    m.set_adam_state(*a0)
+    m.zero_grad()
+    arf.train_step(*args)
+    m.flush_grads()
+    m.adam_step(arf.AdamConfig(), 1, 0, n)
+    pb = m.params()
+    assert not np.array_equal(pa[0], p0[0])
+    assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
+    m.set_params(p0[0], p0[1])
+    # the density step's backward goes through the same reductions
+    m.zero_grad()
+    d1 = arf.density_step(m, pose, occ, 4096, 5, 1, arf.LossConfig())
+    gd1 = m.grads()
+    m.zero_grad()
+    d2 = arf.density_step(m, pose, occ, 4096, 5, 1, arf.LossConfig())
+    gd2 = m.grads()
+    assert np.array_equal(np.asarray(d1), np.asarray(d2))
+    assert np.array_equal(gd1[0], gd2[0]) and np.array_equal(gd1[1], gd2[1])
+
+
+def test_deterministic_training_and_exact_resume(gpu, tmp_path):
+    """TrainConfig.deterministic: two runs from the same seed give bit-identical loss
+    histories, parameters and Adam moments (occupancy refreshes every 8 steps included); a
+    run saved at step 12 and restored into a fresh trainer continues bit-identically."""
+    a = _det_trainer()
+    ha = a.train()
+    b = _det_trainer()
+    hb = b.train()
+    assert np.array_equal(ha, hb)
+    for x, y in zip(a.model.params(), b.model.params()):
+        assert np.array_equal(x, y)
+    for x, y in zip(a.model.adam_state(), b.model.adam_state()):
+        assert np.array_equal(x, y)
+    c = _det_trainer()
+    c.train(12)
+    c.save(tmp_path / "half.ckpt")
+    d = _det_trainer(seed_model=99)   # different init: everything must come from the checkpoint
+    d.restore(tmp_path / "half.ckpt")
+    hd = d.train(12)
+    assert np.array_equal(hd, ha[12:])
+    for x, y in zip(a.model.params(), d.model.params()):
+        assert np.array_equal(x, y)
+    for x, y in zip(a.grid.download(), d.grid.download()):
+        assert np.array_equal(x, y)
