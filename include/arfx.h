@@ -349,6 +349,15 @@ int arfx_density_step(arfx_model m, arfx_pose p, arfx_occ_grid occ, int64_t n_po
                       uint64_t step, const arfx_loss_config* cfg, double* loss2, void* stream);
 int arfx_density_step_device(arfx_model m, arfx_pose p, arfx_occ_grid occ, int64_t n_points, uint64_t seed,
                              uint64_t step, const arfx_loss_config* cfg, double* d_loss2, void* stream);
+/* arfx_train_step_device + arfx_density_step_device in one call (same results): the
+ * L_density forward runs on a library-owned side stream with its own workspace,
+ * concurrently with the train step; its backward joins on `stream` after the train
+ * backward. n_points <= 0 skips the density step. */
+int arfx_train_density_step_device(arfx_model m, arfx_pose pose, const arfx_camera* cam, arfx_occ_grid occ,
+                                   const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                                   const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
+                                   const arfx_loss_config* cfg, double* d_loss4, int64_t n_points,
+                                   uint64_t seed, uint64_t step, double* d_loss2, void* stream);
 /* Adam over flat parameter indices [begin, end) (multiples of 4; end = -1: all), step >= 1,
  * gradients zeroed in the same pass. Asynchronous on stream. */
 int arfx_adam_step(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,

@@ -170,6 +170,9 @@ _PROTOS = {
                                     c_double_p, P]),
     "arfx_density_step_device": (C.c_int, [H, H, H, C.c_int64, C.c_uint64, C.c_uint64,
                                            C.POINTER(ArfxLossConfig), P, P]),
+    "arfx_train_density_step_device": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions),
+                                                 C.c_int64, P, P, P, P, C.POINTER(ArfxLossConfig), P, C.c_int64,
+                                                 C.c_uint64, C.c_uint64, P, P]),
     "arfx_adam_step": (C.c_int, [H, C.POINTER(ArfxAdamConfig), C.c_int64, C.c_int64, C.c_int64, P]),
     "arfx_model_flat": (C.c_int, [H, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P),
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -243,7 +243,7 @@ OccImpl& occ_ref(arfx_occ_grid g) {
 
 void check_overflow_and_grow(ModelImpl& m, const unsigned long long* c, bool& rerun) {
   rerun = false;
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   if (c[6] > w.cap_starts) w.learned_starts = static_cast<size_t>(c[6] + c[6] / 4 + 1024);
   if (c[0] > w.cap_posed || c[3] > 0 || c[2] > w.cap_pool) {
     const size_t need = static_cast<size_t>(std::max<unsigned long long>(c[0], w.cap_posed));
@@ -269,6 +269,12 @@ ModelImpl::~ModelImpl() {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
+  if (side) {
+    cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
 }
 
 void ModelImpl::refresh_views() { fill_field_view(*this); }
@@ -802,14 +808,14 @@ int arfx_build_inference_grid(arfx_model mh, arfx_pose ph, arfx_occ_grid gh, arf
       // every bone) so nothing can overflow, and return without a host round trip; the grid
       // is complete for any later work on the same stream
       const OccImpl& g = occ_ref(gh);
-      m.ws.reserve_worst(static_cast<size_t>(g.res) * g.res * g.res, static_cast<size_t>(m.sv.nb));
+      m.ws().reserve_worst(static_cast<size_t>(g.res) * g.res * g.res, static_cast<size_t>(m.sv.nb));
       inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
       return;
     }
     for (int attempt = 0; attempt < 3; ++attempt) {
       inference_grid(m, ph->impl, occ_ref(gh), nullptr, s);
       unsigned long long hc[8];
-      d2h(hc, m.ws.counters.ptr, 8, s);
+      d2h(hc, m.ws().counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -885,7 +891,7 @@ int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses
         ARFX_CUDA(cudaMemcpyAsync(g.values.ptr, saved.ptr, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
       training_grid_update(m, ps, decay, seed, step, g, nullptr, s);
       unsigned long long hc[8];
-      d2h(hc, m.ws.counters.ptr, 8, s);
+      d2h(hc, m.ws().counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -967,12 +973,12 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
     // warm-up (uncaptured): sizes the workspace for the worst case of the grid parts and
     // sets kernel attributes; the render workspace grows from its counters if needed
     if (occ && (parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD)))
-      m.ws.reserve_worst(static_cast<size_t>(occ->impl.res) * occ->impl.res * occ->impl.res,
+      m.ws().reserve_worst(static_cast<size_t>(occ->impl.res) * occ->impl.res * occ->impl.res,
                          static_cast<size_t>(m.sv.nb));
     for (int attempt = 0; attempt < 3; ++attempt) {
       enqueue();
       unsigned long long hcnt[8];
-      d2h(hcnt, m.ws.counters.ptr, 8, s);
+      d2h(hcnt, m.ws().counters.ptr, 8, s);
       ARFX_CUDA(cudaStreamSynchronize(s));
       bool rerun;
       check_overflow_and_grow(m, hcnt, rerun);
@@ -1030,7 +1036,7 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
                    opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, t_rb->rgb.ptr,
                    t_rb->alpha.ptr, nullptr, s);
       unsigned long long hcnt[8];
-      d2h(hcnt, m.ws.counters.ptr, 8, s);
+      d2h(hcnt, m.ws().counters.ptr, 8, s);
       // this shard's row tiles (other shards' rows are left untouched), enqueued behind the
       // counters so one synchronisation covers both; on overflow the frame re-runs and
       // copies again. Full tiles of a shard are one strided 2-D copy per image.
@@ -1076,7 +1082,7 @@ int arfx_render_trace(arfx_model mh, int64_t capacity, int64_t* n_samples, int32
     require(mh && n_samples, "render_trace: null argument");
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
-    Workspace& w = m.ws;
+    Workspace& w = m.ws();
     ARFX_CUDA(cudaStreamSynchronize(m.stream));
     ARFX_CUDA(cudaDeviceSynchronize());
     unsigned long long hc[4];
@@ -1323,7 +1329,7 @@ int arfx_posed_query(arfx_model mh, arfx_pose ph, const double* pts, int64_t n, 
     for (int attempt = 0; attempt < 3; ++attempt) {
       posed_query_batch(m, ph->impl, P.d.ptr, n, dd.ptr, dcl.ptr, dcan.ptr, dh.ptr, nullptr, m.stream);
       unsigned long long hc[8];
-      d2h(hc, m.ws.counters.ptr, 8, m.stream);
+      d2h(hc, m.ws().counters.ptr, 8, m.stream);
       ARFX_CUDA(cudaStreamSynchronize(m.stream));
       bool rerun;
       check_overflow_and_grow(m, hc, rerun);
@@ -1428,7 +1434,7 @@ int arfx_field_query_backward(arfx_model mh, const double* pts, int64_t n, const
     if (n <= 0) return;
     const cudaStream_t s = m.stream;
     ensure_grads(m, s);
-    Workspace& w = m.ws;
+    Workspace& w = m.ws();
     w.ensure(static_cast<size_t>(n), 0);
     w.ensure_train();
     std::vector<double> sx(static_cast<size_t>(n)), sy(sx.size()), sz(sx.size());
@@ -1486,10 +1492,10 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
     // no host round trip: capacities for the worst case (every sample occupied, every root
     // and start kept), so nothing can overflow; pixels are not range-checked here (an
     // out-of-image pixel only yields a ray through it, no out-of-bounds access)
-    m.ws.reserve_worst(static_cast<size_t>(posed_max), static_cast<size_t>(m.sv.nb));
+    m.ws().reserve_worst(static_cast<size_t>(posed_max), static_cast<size_t>(m.sv.nb));
     train_forward(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0, opt->seed, opt->frame_id, n_rays, d_px,
                   d_py, s);
-    Workspace& w = m.ws;
+    Workspace& w = m.ws();
     w.ensure_train();
     ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
     train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
@@ -1508,7 +1514,7 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
     train_forward(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0, opt->seed, opt->frame_id, n_rays, d_px,
                   d_py, s);
     unsigned long long nbad = 0;
-    d2h(hcnt, m.ws.counters.ptr, 8, s);
+    d2h(hcnt, m.ws().counters.ptr, 8, s);
     d2h(&nbad, bad.ptr, 1, s);
     ARFX_CUDA(cudaStreamSynchronize(s));
     if (nbad) throw std::invalid_argument("generate_ray: pixel outside image");
@@ -1517,7 +1523,7 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
     if (!rerun) break;
     if (attempt == 2) throw std::runtime_error("train: workspace overflow persisted");
   }
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   w.ensure_train();
   ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
   train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
@@ -1675,7 +1681,7 @@ int arfx_train_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, 
     ARFX_CUDA(cudaSetDevice(m.device));
     if (n_rays <= 0) return;
     const cudaStream_t s = stream_of(m, stream);
-    Workspace& w = m.ws;
+    Workspace& w = m.ws();
     w.train_terms.ensure(static_cast<size_t>(3 * n_rays));
     w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
     w.train_alpha.ensure(static_cast<size_t>(n_rays));
@@ -1692,7 +1698,7 @@ void run_density(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t se
                  double* d_out2, cudaStream_t s, bool host_sync = true) {
   ensure_grad_store(m, s);
   if (!host_sync && n <= (1LL << 22)) {  // worst-case capacities: no overflow check needed
-    m.ws.reserve_worst(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb));
+    m.ws().reserve_worst(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb));
     density_forward(m, p, g, n, seed, step, s);
     density_backward(m, n, w, d_out2, s);
     return;
@@ -1700,7 +1706,7 @@ void run_density(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t se
   for (int attempt = 0;; ++attempt) {
     density_forward(m, p, g, n, seed, step, s);
     unsigned long long hc[8];
-    d2h(hc, m.ws.counters.ptr, 8, s);
+    d2h(hc, m.ws().counters.ptr, 8, s);
     ARFX_CUDA(cudaStreamSynchronize(s));
     bool rerun;
     check_overflow_and_grow(m, hc, rerun);
@@ -1743,6 +1749,60 @@ int arfx_density_step_device(arfx_model mh, arfx_pose ph, arfx_occ_grid occ, int
     if (n_points <= 0) return;
     run_density(m, ph->impl, occ->impl, n_points, seed, step, lt.w_density, d_loss2, stream_of(m, stream),
                 /*host_sync=*/false);
+  });
+}
+
+// Train step + L_density step in one call: the density forward (points, deformer, field
+// on the side workspace) runs on the model's side stream concurrently with the train
+// step's forward and backward, and its backward joins after the train backward on
+// `stream` (gradient accumulation stays ordered). Same results as arfx_train_step_device
+// followed by arfx_density_step_device.
+int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                                   const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                                   const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
+                                   const arfx_loss_config* cfg, double* d_loss4, int64_t n_points, uint64_t dseed,
+                                   uint64_t dstep, double* d_loss2, void* stream) {
+  return guard([&] {
+    const HostCamera hc = camera_of(cam);
+    validate_train(mh, ph, opt, hc);
+    require(n_rays == 0 || (d_px && d_py && d_gt_rgb && d_gt_alpha && d_loss4), "train_step: null argument");
+    require(n_points <= 0 || (occ && d_loss2), "density_step: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    const LossTargets dl = loss_targets(cfg, nullptr, nullptr, nullptr);
+    ensure_grad_store(m, s);
+    const bool dens = n_points > 0;
+    if (dens) {
+      require(n_points <= (1LL << 22), "density_step: at most 2^22 points per call");
+      if (!m.side) {
+        ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+        ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
+        ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
+      }
+      WorkspaceScope side(m, m.ws_side);
+      m.ws().reserve_worst(static_cast<size_t>(n_points), static_cast<size_t>(m.sv.nb));
+      ARFX_CUDA(cudaEventRecord(m.ev_fork, s));
+      ARFX_CUDA(cudaStreamWaitEvent(m.side, m.ev_fork, 0));
+      density_forward(m, ph->impl, occ->impl, n_points, dseed, dstep, m.side);
+      ARFX_CUDA(cudaEventRecord(m.ev_join, m.side));
+    }
+    if (n_rays > 0) {
+      Workspace& w = m.ws();
+      w.train_terms.ensure(static_cast<size_t>(3 * n_rays));
+      w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
+      w.train_alpha.ensure(static_cast<size_t>(n_rays));
+      LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
+      unsigned long long hcnt[8];
+      run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, d_px, d_py, nullptr, nullptr, &lt,
+                w.train_rgb.ptr, w.train_alpha.ptr, s, hcnt, /*host_sync=*/false);
+      loss_reduce(w.train_terms.ptr, n_rays, lt, d_loss4, s);
+    }
+    if (dens) {
+      ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_join, 0));
+      WorkspaceScope side(m, m.ws_side);
+      density_backward(m, n_points, dl.w_density, d_loss2, s);
+    }
   });
 }
 

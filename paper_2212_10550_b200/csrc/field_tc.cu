@@ -399,7 +399,7 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   const long long tiles = (n_hint + kTcTile * kGroups - 1) / (kTcTile * kGroups);
   const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));
   const size_t tile_bytes = static_cast<size_t>(2 * TcSmem::A0P);
-  m.ws.tc_tiles.ensure(static_cast<size_t>((m.ws.cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
+  m.ws().tc_tiles.ensure(static_cast<size_t>((m.ws().cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
   const bool half = m.mlp_mode == 2;
   if (half) {  // refresh the fp16 copy of the table (params may have changed since the last render)
     const long long nrow = static_cast<long long>(m.n_grid / 2);
@@ -413,14 +413,14 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   m.prof.begin("encode_tc", s);
   (half ? encode_tiles_kernel<true> : encode_tiles_kernel<false>)<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n_hint + 255) / 256,
                                                                                        static_cast<long long>(sms) * 16))),
-                        kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
-                                     m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool), m.ws.tc_tiles.ptr,
+                        kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,
+                                     m.ws().counters.ptr + 2, static_cast<long long>(m.ws().cap_pool), m.ws().tc_tiles.ptr,
                                      m.stats_on ? m.stats.ptr : nullptr);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
   m.prof.begin("field_tc", s);
-  field_tc_kernel<<<grid, kTcThreads, smem, s>>>(m.fv, m.ws.tc_tiles.ptr, m.ws.powner.ptr, m.ws.pres.ptr,
-                                              m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool));
+  field_tc_kernel<<<grid, kTcThreads, smem, s>>>(m.fv, m.ws().tc_tiles.ptr, m.ws().powner.ptr, m.ws().pres.ptr,
+                                              m.ws().counters.ptr + 2, static_cast<long long>(m.ws().cap_pool));
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }

@@ -151,7 +151,13 @@ struct ModelImpl {
   int max_union = 1;  // widest per-cell bone union (sizes the Newton kernel's scratch)
   FieldView fv{};
   SkinView sv{};
-  Workspace ws;
+  // Workspaces: ws() is the one the launch helpers use; a second one lets the L_density
+  // forward run on the side stream concurrently with the train step (WorkspaceScope).
+  Workspace ws_main, ws_side;
+  Workspace* ws_cur = &ws_main;
+  Workspace& ws() { return *ws_cur; }
+  cudaStream_t side = nullptr;  // lazily created non-blocking stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<uint8_t> overflow_note;
   ~ModelImpl();
   void refresh_views();
@@ -237,6 +243,17 @@ double cosine_lr(double lr0, const AdamCfg& c, long long step);
 void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s);
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
                      float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt = nullptr);
+// Points the launch helpers at another workspace for a scope (host-side; the kernels
+// enqueued inside capture that workspace's buffers).
+struct WorkspaceScope {
+  ModelImpl& m;
+  Workspace* prev;
+  WorkspaceScope(ModelImpl& mm, Workspace& w) : m(mm), prev(mm.ws_cur) { m.ws_cur = &w; }
+  ~WorkspaceScope() { m.ws_cur = prev; }
+  WorkspaceScope(const WorkspaceScope&) = delete;
+  WorkspaceScope& operator=(const WorkspaceScope&) = delete;
+};
+
 // Owner order of the flagged pool entries (deterministic mode): targets [first[o],
 // first[o]+count[o]) per owner o (nullptr: target o), or the pool entries themselves.
 struct BwdOwners {

@@ -772,7 +772,7 @@ __global__ void starts_overflow_kernel(const unsigned long long* total, unsigned
 
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long n, cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   finalize_pool_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
                                                                 m.inv.dedup_radius, K,
                                                                 static_cast<long long>(w.cap_starts));
@@ -780,7 +780,7 @@ void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long 
 }
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const RootsSink& K, long long n, cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   finalize_roots_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
                                                                  m.inv.dedup_radius, K,
                                                                  static_cast<long long>(w.cap_starts));
@@ -792,7 +792,7 @@ void launch_finalize(ModelImpl& m, const Src& src, const RootsSink& K, long long
 template <class Src, class Sink>
 void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, const Sink& K, long long n_hint,
                         const char* name, cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   constexpr bool single = Src::kSinglePose;
   const long long n = std::max<long long>(n_hint, 1);
   // items pack (target, bone) as target | bone << kItemBoneShift
@@ -853,7 +853,7 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
 template <class Src>
 void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long long n_hint,
                    cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   PoolSink K{w.snroot.ptr, w.sbase.ptr, w.px.ptr, w.py.ptr, w.pz.ptr, w.powner.ptr,
              w.counters.ptr, static_cast<long long>(w.cap_pool), m.fv};
   launch_deform_sink(m, d_poses, src, K, n_hint, "deform", s);
@@ -881,11 +881,11 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     constexpr long long kTeamMax = 65536;
     m.prof.begin("field", s);
     field_team_kernel<<<static_cast<unsigned>(sm_count() * 8), kFtTeam * kFtTeams, 0, s>>>(
-        m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr, m.ws.pres.ptr, m.ws.counters.ptr + 2,
-        static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax);
-    kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr,
-                                         m.ws.pres.ptr, m.ws.counters.ptr + 2,
-                                         static_cast<long long>(m.ws.cap_pool), m.stats_on ? m.stats.ptr : nullptr,
+        m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr, m.ws().pres.ptr, m.ws().counters.ptr + 2,
+        static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax);
+    kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,
+                                         m.ws().pres.ptr, m.ws().counters.ptr + 2,
+                                         static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr,
                                          kTeamMax);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
@@ -896,8 +896,8 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
   const int in_smem = wbytes <= 48 * 1024 ? 1 : 0;
   m.prof.begin("field", s);
   field_pool_kernel<<<grid_for(n_hint, threads, 16), threads, in_smem ? wbytes : 0, s>>>(
-      m.fv, m.ws.px.ptr, m.ws.py.ptr, m.ws.pz.ptr, m.ws.powner.ptr, m.ws.pres.ptr,
-      m.ws.counters.ptr + 2, static_cast<long long>(m.ws.cap_pool), in_smem);
+      m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr, m.ws().pres.ptr,
+      m.ws().counters.ptr + 2, static_cast<long long>(m.ws().cap_pool), in_smem);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
@@ -973,7 +973,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
                   bool stratified, double eps, uint64_t seed, uint64_t frame, int shard,
                   int nshards, float* d_rgb, float* d_alpha, unsigned long long* d_counters,
                   cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   // rows of this shard: interleaved 16-row tiles
   if (w.last_shard != shard || w.last_nshards != nshards || w.last_rows != cam.height ||
       w.last_w != cam.width) {
@@ -1061,7 +1061,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
 void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ, int N, bool stratified,
                    uint64_t seed, uint64_t frame, long long n_rays, const int32_t* d_px, const int32_t* d_py,
                    cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   w.ensure(static_cast<size_t>(std::max<long long>(std::min<long long>(n_rays * std::max(N, 1), 1LL << 22), 1LL << 16)),
            static_cast<size_t>(std::max<long long>(n_rays, 1)));
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
@@ -1171,7 +1171,7 @@ static void occ_source_common(OccImpl& g, double lo[3], double cs[3]) {
 
 void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d_counters,
                     cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   const long long n = static_cast<long long>(g.res) * g.res * g.res;
   w.ensure(static_cast<size_t>(n), 0);
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
@@ -1195,7 +1195,7 @@ void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d
 // and rebuilds the mask (threshold + dilation) on the full grid. Bit-identical per cell.
 void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int n_shards,
                           unsigned long long* d_counters, cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   const int z0 = static_cast<int>(static_cast<long long>(g.res) * shard / n_shards);
   const int z1 = static_cast<int>(static_cast<long long>(g.res) * (shard + 1) / n_shards);
   const long long plane = static_cast<long long>(g.res) * g.res;
@@ -1221,7 +1221,7 @@ void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int 
 void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,
                           uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
                           cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   const long long n = static_cast<long long>(g.res) * g.res * g.res;
   w.ensure(static_cast<size_t>(n), 0);
   DevBuf<PoseCtx> ctxs;
@@ -1246,7 +1246,7 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
                        int32_t* d_counts, double* d_roots, double* d_res, cudaStream_t s) {
   if (n <= 0) return;
-  if (!m.ws.counters.ptr) m.ws.counters.alloc(16);
+  if (!m.ws().counters.ptr) m.ws().counters.alloc(16);
   const AosSrc src{d_pts, n};
   const RootsSink K{d_counts, d_roots, d_res};
   launch_deform_sink(m, d_ctx, src, K, n, "inverse_lbs", s);
@@ -1256,7 +1256,7 @@ void posed_query_batch(ModelImpl& m, PoseImpl& p, const double* d_pts, int64_t n
                        float* d_col, double* d_canon, uint8_t* d_has, unsigned long long* d_counters,
                        cudaStream_t s) {
   if (n <= 0) return;
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   w.ensure(static_cast<size_t>(n), 0);
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   ListSrc src{d_pts, d_pts, d_pts, nullptr, n, n};
@@ -1453,7 +1453,7 @@ __global__ void density_flag_kernel(long long n, const uint8_t* __restrict__ emp
 // the counters on the device (the caller checks overflow and re-runs).
 void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step,
                      cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   w.ensure(static_cast<size_t>(n), 0);
   w.dens_pts.ensure(static_cast<size_t>(3 * n));
   w.dens_empty.ensure(static_cast<size_t>(n));
@@ -1471,7 +1471,7 @@ void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_
 
 // Backward half: loss reduction and gradient flags, then K8 into the model's gradients.
 void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   w.ensure_train();
   w.dens_scale.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));

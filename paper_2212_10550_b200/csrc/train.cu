@@ -605,7 +605,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
                          const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own) {
   if (!(m.fv.F == 2 && m.fv.in_dim == kIn && m.fv.hidden == kHid && m.fv.n_layers == 3 && m.fv.out_dim == kOut))
     throw std::invalid_argument("train path: libarfx implements the 32-64-64-4 decoder (levels*F == 32)");
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   const long long rec_cap = cap;
   w.bwd_rec.ensure(static_cast<size_t>(rec_cap + 1) * kRecStride);
   w.bwd_list.ensure(static_cast<size_t>(rec_cap + 1));
@@ -665,7 +665,7 @@ void flush_grad_acc(ModelImpl& m, cudaStream_t s) {
 
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
                      float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt) {
-  Workspace& w = m.ws;
+  Workspace& w = m.ws();
   TrainCompositeArgs A{n_rays, N, eps, w.ray_first.ptr, w.ray_count.ptr, w.sidx.ptr, w.sdelta.ptr, w.snroot.ptr,
                        w.sbase.ptr, w.pres.ptr, w.strans.ptr, d_dC, d_dA, nullptr, nullptr, LossCfg{}, 0.0, nullptr,
                        d_rgb, d_alpha, w.pgs.ptr, w.pgc.ptr, w.pflag.ptr};

@@ -159,6 +159,7 @@ class Trainer:
         self.grid = arf.OccupancyGrid(model.normalized_box, cfg.occupancy)
         arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
         self.step_id = 0
+        self.fused_density = True  # arfx_train_density_step_device (False: the two calls in sequence)
         self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
         self._checked = 0     # steps whose loss has been checked for finiteness
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
@@ -192,16 +193,26 @@ class Trainer:
         torch.index_select(self.gt_rgb[f], 0, idx, out=self.b_rgb)
         torch.index_select(self.gt_alpha[f], 0, idx, out=self.b_alpha)
         sp = C.c_void_p(self.stream.cuda_stream)
-        L.call("arfx_train_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()), self.grid._h,
-               C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
-               C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
-               C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
-               None, None, sp)
-        if cfg.loss.w_density > 0 and cfg.density_points > 0:  # L_density
-            L.call("arfx_density_step_device", self.model._h, self.views[f]._h, self.grid._h, cfg.density_points,
-                   (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id, C.byref(cfg.loss.to_c()),
+        dens = cfg.loss.w_density > 0 and cfg.density_points > 0  # L_density
+        if dens and self.fused_density:
+            # one call: the density forward overlaps the train step on a side stream
+            L.call("arfx_train_density_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
+                   self.grid._h, C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
+                   C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
+                   C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
+                   cfg.density_points, (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id,
                    C.c_void_p(self.loss_d.data_ptr()), sp)
         else:
+            L.call("arfx_train_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
+                   self.grid._h, C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
+                   C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
+                   C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
+                   None, None, sp)
+            if dens:
+                L.call("arfx_density_step_device", self.model._h, self.views[f]._h, self.grid._h, cfg.density_points,
+                       (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id, C.byref(cfg.loss.to_c()),
+                       C.c_void_p(self.loss_d.data_ptr()), sp)
+        if not dens:
             self.loss_d.zero_()
         t = self.step_id + 1
         if cfg.deterministic and self.world > 1:

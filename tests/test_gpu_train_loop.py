@@ -338,3 +338,42 @@ def test_deterministic_training_and_exact_resume(gpu, tmp_path):
         assert np.array_equal(x, y)
     for x, y in zip(a.grid.download(), d.grid.download()):
         assert np.array_equal(x, y)
+
+
+def _dens_trainer(fused: bool):
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig
+    fig = fx.default_figure()
+    sk = fig.skeleton
+    poses = [arf.pose_from_joint_rotations(sk, fx.bend_pose_rotations(10, 0.0, 0.0)),
+             fx.random_pose(sk, 17, max_angle=0.3)]
+    cam = fx.default_camera(sk, 48, 48)
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (24, 24, 24), 9)
+    g, mp, _ = m.params()
+    mp[-4] = 2.0
+    m.set_params(g, mp)
+    cfg = TrainConfig(iterations=10, rays_per_batch=1024, samples_per_ray=64, seed=5, occupancy_interval=0,
+                      density_points=8192, deterministic=True,
+                      loss=arf.LossConfig(w_density=1.0), adam=arf.AdamConfig(total_steps=10))
+    tr = Trainer(m, fig, poses, cam, cfg)
+    tr.fused_density = fused
+    vals, mask = tr.grid.download()
+    mask = mask.reshape(64, 64, 64).copy()
+    mask[:, :, ::2] = 0  # empty cells with roots: L_density has work
+    tr.grid.upload(vals, mask.reshape(-1))
+    return tr
+
+
+def test_fused_density_step_matches_sequential(gpu):
+    """arfx_train_density_step_device (density forward on the side stream, overlapping the
+    train step) == arfx_train_step_device then arfx_density_step_device, bit for bit in
+    deterministic mode (losses, parameters, Adam moments over 10 steps)."""
+    a = _dens_trainer(True)
+    ha = a.train()
+    b = _dens_trainer(False)
+    hb = b.train()
+    assert np.all(ha[:, 3] > 0) and np.all(ha[:, 0] > 0)
+    assert np.array_equal(ha, hb)
+    for x, y in zip(a.model.params(), b.model.params()):
+        assert np.array_equal(x, y)
+    for x, y in zip(a.model.adam_state(), b.model.adam_state()):
+        assert np.array_equal(x, y)
