@@ -7,7 +7,7 @@
 // non-skipped sample's selected canonical root, accumulated into FieldGrads.
 //
 //   K1..K3 as in render (march in ray-list mode, deformer, exact field over the pool)
-//   K7  train_composite_kernel  thread per ray: selection + composite forward (rgb, alpha,
+//   K7  train_composite_warp_kernel  warp per ray: selection + composite forward (rgb, alpha,
 //                               terminated_at), the SPEC losses and their gradient when
 //                               targets are given (losses.cuh), then the exact reverse
 //                               pass; dsigma / dc land on the selected root's pool entry
@@ -73,78 +73,124 @@ struct TrainCompositeArgs {
   uint8_t* pflag;  // per pool entry: needs query_backward
 };
 
-__global__ void train_composite_kernel(TrainCompositeArgs A) {
-  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < A.n_rays;
-       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+// K7, warp per ray: lanes take 32 consecutive samples at a time and do the independent
+// per-sample work in parallel (root selection, alpha = -expm1(-sigma delta), the gradient
+// outputs); only the reference's sequential recurrences -- T, C, A forward and the suffix
+// C^, A^ backward -- walk the samples one by one, every lane running the same chain on
+// values broadcast by shuffle. Same operations in the same order as the per-sample loop
+// of R/render.hpp:98-157, so bit-identical; a 4,096-ray batch fills 4,096 warps instead
+// of 32 blocks of threads.
+__device__ __forceinline__ double shfl_dd(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+__global__ void __launch_bounds__(128) train_composite_warp_kernel(TrainCompositeArgs A) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < A.n_rays;
+       r += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
     const int first = A.ray_first[r], cnt = A.ray_count[r];
     // ---- forward (composite R/render.hpp:98-119) ----
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, acc = 0.0;
-    int m = A.N;  // terminated_at (index into the full N-sample list)
+    int m = A.N;  // terminated_at
     if (A.eps > 0 && T <= A.eps) m = 0;
-    for (int j = 0; j < cnt && m == A.N; ++j) {
+    for (int c0 = 0; c0 < cnt && m == A.N; c0 += 32) {
+      const int j = c0 + lane;
       const long long s = first + j;
-      A.strans[s] = T;
-      float4 v;
-      const int sel = select_root_t(A.snroot, A.sbase, A.pres, s, v);
-      if (sel < 0) continue;
-      const double sigma = static_cast<double>(v.x);
-      if (sigma <= 0.0) continue;
-      const double alpha = -expm1(-__dmul_rn(sigma, A.sdelta[s]));
-      const double w = __dmul_rn(alpha, T);
-      cr = __dadd_rn(cr, __dmul_rn(static_cast<double>(v.y), w));
-      cg = __dadd_rn(cg, __dmul_rn(static_cast<double>(v.z), w));
-      cb = __dadd_rn(cb, __dmul_rn(static_cast<double>(v.w), w));
-      acc = __dadd_rn(acc, w);
-      T = __dmul_rn(T, __dsub_rn(1.0, alpha));
-      if (A.eps > 0 && T <= A.eps) m = A.sidx[s] + 1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      double alpha = 0.0;
+      bool contrib = false;
+      int sid = 0;
+      if (j < cnt) {
+        const int sel = select_root_t(A.snroot, A.sbase, A.pres, s, v);
+        contrib = sel >= 0 && static_cast<double>(v.x) > 0.0;
+        if (contrib) alpha = -expm1(-__dmul_rn(static_cast<double>(v.x), A.sdelta[s]));
+        sid = A.sidx[s];
+      }
+      const unsigned cmask = __ballot_sync(0xffffffffu, contrib);
+      const int kn = min(32, cnt - c0);
+      double myT = 0.0;
+      int k = 0;
+      for (; k < kn; ++k) {  // uniform across the warp
+        if (lane == k) myT = T;
+        if (!((cmask >> k) & 1u)) continue;
+        const double a = shfl_dd(alpha, k);
+        const double w = __dmul_rn(a, T);
+        cr = __dadd_rn(cr, __dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.y, k)), w));
+        cg = __dadd_rn(cg, __dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.z, k)), w));
+        cb = __dadd_rn(cb, __dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.w, k)), w));
+        acc = __dadd_rn(acc, w);
+        T = __dmul_rn(T, __dsub_rn(1.0, a));
+        if (A.eps > 0 && T <= A.eps) {
+          m = __shfl_sync(0xffffffffu, sid, k) + 1;
+          ++k;
+          break;
+        }
+      }
+      if (lane < k) A.strans[s] = myT;  // samples the forward visited
     }
     if (cnt == 0) m = 0;
     const float fr = static_cast<float>(cr), fg = static_cast<float>(cg), fb = static_cast<float>(cb);
     const float fa = static_cast<float>(acc);
-    A.rgb[3 * r + 0] = fr;
-    A.rgb[3 * r + 1] = fg;
-    A.rgb[3 * r + 2] = fb;
-    A.alpha[r] = fa;
-    // ---- upstream: given, or the fused loss gradient of this ray ----
+    // ---- upstream: given, or the fused loss gradient of this ray (uniform in the warp) ----
     double dcx, dcy, dcz, da;
     if (A.gt_rgb) {
       const RayLoss L = ray_loss(fr, fg, fb, fa, A.gt_rgb + 3 * r, A.gt_alpha[r], A.loss, A.inv_n);
-      A.ray_terms[3 * r + 0] = L.rgb;
-      A.ray_terms[3 * r + 1] = L.alpha;
-      A.ray_terms[3 * r + 2] = L.hard;
+      if (lane == 0) {
+        A.ray_terms[3 * r + 0] = L.rgb;
+        A.ray_terms[3 * r + 1] = L.alpha;
+        A.ray_terms[3 * r + 2] = L.hard;
+      }
       dcx = L.dC[0], dcy = L.dC[1], dcz = L.dC[2], da = L.dA;
     } else {
       dcx = A.dC[3 * r + 0], dcy = A.dC[3 * r + 1], dcz = A.dC[3 * r + 2], da = A.dA[r];
     }
+    if (lane == 0) {
+      A.rgb[3 * r + 0] = fr;
+      A.rgb[3 * r + 1] = fg;
+      A.rgb[3 * r + 2] = fb;
+      A.alpha[r] = fa;
+    }
     // ---- backward (composite_backward R/render.hpp:125-157), reverse over i < m ----
     double chx = 0.0, chy = 0.0, chz = 0.0, ahat = 0.0;
-    for (int j = cnt - 1; j >= 0; --j) {
+    for (int c0 = ((cnt - 1) / 32) * 32; cnt > 0 && c0 >= 0; c0 -= 32) {
+      const int j = c0 + lane;
       const long long s = first + j;
-      if (A.sidx[s] >= m) continue;
-      float4 v;
-      const int sel = select_root_t(A.snroot, A.sbase, A.pres, s, v);
-      if (sel < 0) continue;  // skipped (no root)
-      const double sigma = static_cast<double>(v.x);
-      const double alpha = sigma <= 0.0 ? 0.0 : -expm1(-__dmul_rn(sigma, A.sdelta[s]));
-      const double cx = static_cast<double>(v.y), cy = static_cast<double>(v.z), cz = static_cast<double>(v.w);
-      const double dCda = __dadd_rn(__dadd_rn(__dmul_rn(dcx, __dsub_rn(cx, chx)), __dmul_rn(dcy, __dsub_rn(cy, chy))),
-                                    __dmul_rn(dcz, __dsub_rn(cz, chz)));
-      const double dAda = __dsub_rn(1.0, ahat);
-      const double trans = A.strans[s];
-      const double dat = __dmul_rn(trans, __dadd_rn(dCda, __dmul_rn(da, dAda)));
-      const double om = __dsub_rn(1.0, alpha);
-      const double ds = __dmul_rn(__dmul_rn(dat, A.sdelta[s]), om);
-      const double at = __dmul_rn(alpha, trans);
-      const long long p = A.sbase[s] + sel;
-      A.pgs[p] = static_cast<float>(ds);
-      A.pgc[3 * p + 0] = static_cast<float>(__dmul_rn(dcx, at));
-      A.pgc[3 * p + 1] = static_cast<float>(__dmul_rn(dcy, at));
-      A.pgc[3 * p + 2] = static_cast<float>(__dmul_rn(dcz, at));
-      A.pflag[p] = 1;
-      chx = __dadd_rn(__dmul_rn(cx, alpha), __dmul_rn(chx, om));
-      chy = __dadd_rn(__dmul_rn(cy, alpha), __dmul_rn(chy, om));
-      chz = __dadd_rn(__dmul_rn(cz, alpha), __dmul_rn(chz, om));
-      ahat = __dadd_rn(alpha, __dmul_rn(ahat, om));
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      int sel = -1;
+      double alpha = 0.0;
+      if (j < cnt && A.sidx[s] < m) {
+        sel = select_root_t(A.snroot, A.sbase, A.pres, s, v);
+        if (sel >= 0 && static_cast<double>(v.x) > 0.0)
+          alpha = -expm1(-__dmul_rn(static_cast<double>(v.x), A.sdelta[s]));
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, sel >= 0);
+      if (!vmask) continue;
+      double mx = 0.0, my = 0.0, mz = 0.0, ma = 0.0;  // C^, A^ seen by this lane's sample
+      for (int k = 31 - __clz(vmask); k >= 0; --k) {  // uniform, reverse sample order
+        if (!((vmask >> k) & 1u)) continue;
+        if (lane == k) mx = chx, my = chy, mz = chz, ma = ahat;
+        const double a = shfl_dd(alpha, k);
+        const double om = __dsub_rn(1.0, a);
+        chx = __dadd_rn(__dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.y, k)), a), __dmul_rn(chx, om));
+        chy = __dadd_rn(__dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.z, k)), a), __dmul_rn(chy, om));
+        chz = __dadd_rn(__dmul_rn(static_cast<double>(__shfl_sync(0xffffffffu, v.w, k)), a), __dmul_rn(chz, om));
+        ahat = __dadd_rn(a, __dmul_rn(ahat, om));
+      }
+      if (sel >= 0) {
+        const double cx = static_cast<double>(v.y), cy = static_cast<double>(v.z), cz = static_cast<double>(v.w);
+        const double dCda = __dadd_rn(__dadd_rn(__dmul_rn(dcx, __dsub_rn(cx, mx)), __dmul_rn(dcy, __dsub_rn(cy, my))),
+                                      __dmul_rn(dcz, __dsub_rn(cz, mz)));
+        const double dAda = __dsub_rn(1.0, ma);
+        const double trans = A.strans[s];
+        const double dat = __dmul_rn(trans, __dadd_rn(dCda, __dmul_rn(da, dAda)));
+        const double om = __dsub_rn(1.0, alpha);
+        const double ds = __dmul_rn(__dmul_rn(dat, A.sdelta[s]), om);
+        const double at = __dmul_rn(alpha, trans);
+        const long long p = A.sbase[s] + sel;
+        A.pgs[p] = static_cast<float>(ds);
+        A.pgc[3 * p + 0] = static_cast<float>(__dmul_rn(dcx, at));
+        A.pgc[3 * p + 1] = static_cast<float>(__dmul_rn(dcy, at));
+        A.pgc[3 * p + 2] = static_cast<float>(__dmul_rn(dcz, at));
+        A.pflag[p] = 1;
+      }
     }
   }
 }
@@ -677,7 +723,7 @@ void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const fl
     A.ray_terms = lt->ray_terms;
   }
   m.prof.begin("train_composite", s);
-  train_composite_kernel<<<static_cast<unsigned>(std::max<long long>(1, (n_rays + 127) / 128)), 128, 0, s>>>(A);
+  train_composite_warp_kernel<<<static_cast<unsigned>(std::max<long long>(1, (n_rays + 3) / 4)), 128, 0, s>>>(A);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
