@@ -309,6 +309,11 @@ int arfx_train_fwd_bwd(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_o
 typedef struct arfx_loss_config { /* LossWeights SPEC.md:446-449; defaults :510 */
   double w_rgb, w_alpha, w_hard, w_density; /* 1, 0.1, 0.1, 0.1 */
   double huber_delta;                       /* 0.1 */
+  /* 0 (default): gt_rgb / gt_alpha hold one target per ray. > 0 (device train steps only):
+   * they hold whole ground-truth frames [gt_height][gt_width] (row-major, rgb interleaved)
+   * and ray r reads the target at its pixel (py[r], px[r]) inside the composite kernel
+   * (a pixel outside the frame reads target 0). */
+  int64_t gt_width, gt_height;
 } arfx_loss_config;
 
 typedef struct arfx_adam_config {

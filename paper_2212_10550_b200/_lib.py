@@ -71,7 +71,7 @@ class ArfxModelDesc(C.Structure):
 
 class ArfxLossConfig(C.Structure):
     _fields_ = [("w_rgb", C.c_double), ("w_alpha", C.c_double), ("w_hard", C.c_double), ("w_density", C.c_double),
-                ("huber_delta", C.c_double)]
+                ("huber_delta", C.c_double), ("gt_width", C.c_int64), ("gt_height", C.c_int64)]
 
 
 class ArfxAdamConfig(C.Structure):

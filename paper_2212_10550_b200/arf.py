@@ -654,8 +654,11 @@ class LossConfig:  # LossWeights SPEC.md:446-449, defaults
     w_density: float = 0.1
     huber_delta: float = 0.1
 
-    def to_c(self) -> L.ArfxLossConfig:
-        return L.ArfxLossConfig(self.w_rgb, self.w_alpha, self.w_hard, self.w_density, self.huber_delta)
+    def to_c(self, gt_frame: "tuple[int, int] | None" = None) -> L.ArfxLossConfig:
+        """gt_frame = (width, height): the device train steps read targets from whole frames
+        at each ray's pixel (arfx_loss_config.gt_width / gt_height)."""
+        w, h = gt_frame if gt_frame is not None else (0, 0)
+        return L.ArfxLossConfig(self.w_rgb, self.w_alpha, self.w_hard, self.w_density, self.huber_delta, w, h)
 
 
 @dataclass

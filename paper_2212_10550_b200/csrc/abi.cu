@@ -1537,7 +1537,11 @@ LossTargets loss_targets(const arfx_loss_config* cfg, const float* gt_rgb, const
   require(cfg->w_rgb >= 0 && cfg->w_alpha >= 0 && cfg->w_hard >= 0 && cfg->w_density >= 0,
           "loss: weights must be non-negative");
   require(cfg->huber_delta > 0, "loss: huber_delta must be positive");
-  return LossTargets{gt_rgb, gt_alpha, cfg->w_rgb, cfg->w_alpha, cfg->w_hard, cfg->w_density, cfg->huber_delta, terms};
+  require(cfg->gt_width >= 0 && cfg->gt_height >= 0, "loss: negative ground-truth frame size");
+  LossTargets lt{gt_rgb, gt_alpha, cfg->w_rgb, cfg->w_alpha, cfg->w_hard, cfg->w_density, cfg->huber_delta, terms};
+  lt.gt_w = cfg->gt_width;
+  lt.gt_h = cfg->gt_height;
+  return lt;
 }
 
 AdamCfg adam_of(const arfx_adam_config* c) {
@@ -1596,6 +1600,7 @@ int arfx_losses(int64_t n, const float* rgb, const float* alpha, const float* gt
   return guard([&] {
     require(n == 0 || (rgb && alpha && gt_rgb && gt_alpha), "losses: null argument");
     LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    require(lt.gt_w == 0, "loss: frame targets (gt_width > 0) are for the device train steps only");
     require_device();
     const cudaStream_t s = cudaStreamPerThread;
     DevBuf<double> T, L4;
@@ -1634,6 +1639,7 @@ int arfx_train_step(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_oc
     validate_train(mh, ph, opt, hc);
     require(n_rays == 0 || (px && py && gt_rgb && gt_alpha), "train_step: null argument");
     LossTargets lt = loss_targets(cfg, nullptr, nullptr, nullptr);
+    require(lt.gt_w == 0, "loss: frame targets (gt_width > 0) are for the device train steps only");
     ModelImpl& m = mh->impl;
     ARFX_CUDA(cudaSetDevice(m.device));
     if (n_rays <= 0) return;
@@ -1686,6 +1692,8 @@ int arfx_train_step_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, 
     w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
     w.train_alpha.ensure(static_cast<size_t>(n_rays));
     LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
+    lt.px = d_px;
+    lt.py = d_py;
     unsigned long long hcnt[8];
     run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, d_px, d_py, nullptr, nullptr, &lt,
               d_rgb ? d_rgb : w.train_rgb.ptr, d_alpha ? d_alpha : w.train_alpha.ptr, s, hcnt, /*host_sync=*/false);
@@ -1793,6 +1801,8 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
       w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
       w.train_alpha.ensure(static_cast<size_t>(n_rays));
       LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
+      lt.px = d_px;
+      lt.py = d_py;
       unsigned long long hcnt[8];
       run_train(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, n_rays, d_px, d_py, nullptr, nullptr, &lt,
                 w.train_rgb.ptr, w.train_alpha.ptr, s, hcnt, /*host_sync=*/false);

@@ -217,10 +217,12 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
 // train.cu
 // fused-loss targets for train_composite (losses.cuh); device arrays
 struct LossTargets {
-  const float* gt_rgb;    // [n][3]
-  const float* gt_alpha;  // [n]
+  const float* gt_rgb;    // [n][3], or a [gt_h][gt_w][3] frame when gt_w > 0
+  const float* gt_alpha;  // [n], or [gt_h][gt_w]
   double w_rgb, w_alpha, w_hard, w_density, huber_delta;
   double* ray_terms;      // [n][3] out
+  long long gt_w = 0, gt_h = 0;
+  const int32_t *px = nullptr, *py = nullptr;  // ray pixels (frame targets)
 };
 void loss_reduce(const double* d_terms, long long n, const LossTargets& lt, double* d_out4, cudaStream_t s);
 void ray_losses(long long n, const float* d_rgb, const float* d_alpha, const LossTargets& lt, float* d_grad_rgb,

@@ -64,6 +64,8 @@ struct TrainCompositeArgs {
   // fused losses: when gt_rgb != null, dC / dA come from ray_loss instead
   const float* gt_rgb;
   const float* gt_alpha;
+  const int32_t *gpx, *gpy;  // gt_w > 0: targets are frames read at the ray's pixel
+  long long gt_w, gt_h;
   LossCfg loss;
   double inv_n;
   double* ray_terms;  // [n_rays][3] unweighted per-ray loss terms
@@ -132,7 +134,18 @@ __global__ void __launch_bounds__(128) train_composite_warp_kernel(TrainComposit
     // ---- upstream: given, or the fused loss gradient of this ray (uniform in the warp) ----
     double dcx, dcy, dcz, da;
     if (A.gt_rgb) {
-      const RayLoss L = ray_loss(fr, fg, fb, fa, A.gt_rgb + 3 * r, A.gt_alpha[r], A.loss, A.inv_n);
+      const float zero3[3] = {0.0f, 0.0f, 0.0f};
+      const float* grgb = A.gt_rgb + 3 * r;
+      float galpha = 0.0f;
+      if (A.gt_w > 0) {
+        const long long x = A.gpx[r], y = A.gpy[r];
+        const bool in = x >= 0 && y >= 0 && x < A.gt_w && y < A.gt_h;
+        grgb = in ? A.gt_rgb + 3 * (y * A.gt_w + x) : zero3;
+        galpha = in ? A.gt_alpha[y * A.gt_w + x] : 0.0f;
+      } else {
+        galpha = A.gt_alpha[r];
+      }
+      const RayLoss L = ray_loss(fr, fg, fb, fa, grgb, galpha, A.loss, A.inv_n);
       if (lane == 0) {
         A.ray_terms[3 * r + 0] = L.rgb;
         A.ray_terms[3 * r + 1] = L.alpha;
@@ -455,10 +468,8 @@ __global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const do
         s0 = fadd(s0, __shfl_sync(g, v0, src));
         s1 = fadd(s1, __shfl_sync(g, v1, src));
       }
-      if (has && lane == __ffs(g) - 1) {
-        atomicAdd(gt + 2 * static_cast<size_t>(key) + 0, s0);
-        atomicAdd(gt + 2 * static_cast<size_t>(key) + 1, s1);
-      }
+      // one 8-byte vector atomic per row (sm_90+), both features
+      if (has && lane == __ffs(g) - 1) atomicAdd(reinterpret_cast<float2*>(gt) + key, make_float2(s0, s1));
     }
   }
 }
@@ -713,11 +724,16 @@ void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const fl
                      float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt) {
   Workspace& w = m.ws();
   TrainCompositeArgs A{n_rays, N, eps, w.ray_first.ptr, w.ray_count.ptr, w.sidx.ptr, w.sdelta.ptr, w.snroot.ptr,
-                       w.sbase.ptr, w.pres.ptr, w.strans.ptr, d_dC, d_dA, nullptr, nullptr, LossCfg{}, 0.0, nullptr,
+                       w.sbase.ptr, w.pres.ptr, w.strans.ptr, d_dC, d_dA, nullptr, nullptr, nullptr, nullptr, 0, 0,
+                       LossCfg{}, 0.0, nullptr,
                        d_rgb, d_alpha, w.pgs.ptr, w.pgc.ptr, w.pflag.ptr};
   if (lt) {
     A.gt_rgb = lt->gt_rgb;
     A.gt_alpha = lt->gt_alpha;
+    A.gpx = lt->px;
+    A.gpy = lt->py;
+    A.gt_w = lt->gt_w;
+    A.gt_h = lt->gt_h;
     A.loss = LossCfg{lt->w_rgb, lt->w_alpha, lt->w_hard, lt->w_density, lt->huber_delta};
     A.inv_n = 1.0 / static_cast<double>(n_rays);
     A.ray_terms = lt->ray_terms;

@@ -153,8 +153,6 @@ class Trainer:
         self.loss_d = torch.zeros(2, dtype=torch.float64, device="cuda")
         self.px = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
         self.py = torch.zeros(self.n_local, dtype=torch.int32, device="cuda")
-        self.b_rgb = torch.zeros((self.n_local, 3), dtype=torch.float32, device="cuda")
-        self.b_alpha = torch.zeros(self.n_local, dtype=torch.float32, device="cuda")
         # ---- occupancy: built from the untrained model at step 0
         self.grid = arf.OccupancyGrid(model.normalized_box, cfg.occupancy)
         arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
@@ -189,24 +187,23 @@ class Trainer:
         self.px.copy_(hp[0], non_blocking=True)
         self.py.copy_(hp[1], non_blocking=True)
         self._h_evt[slot].record(self.stream)
-        idx = (self.py.long() * W + self.px.long())
-        torch.index_select(self.gt_rgb[f], 0, idx, out=self.b_rgb)
-        torch.index_select(self.gt_alpha[f], 0, idx, out=self.b_alpha)
+        # targets: the composite kernel reads frame f's ground truth at each ray's pixel
+        g_rgb = C.c_void_p(self.gt_rgb[f].data_ptr())
+        g_alpha = C.c_void_p(self.gt_alpha[f].data_ptr())
+        lc = cfg.loss.to_c((W, self.camera.height))
         sp = C.c_void_p(self.stream.cuda_stream)
         dens = cfg.loss.w_density > 0 and cfg.density_points > 0  # L_density
         if dens and self.fused_density:
             # one call: the density forward overlaps the train step on a side stream
             L.call("arfx_train_density_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
                    self.grid._h, C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
-                   C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
-                   C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
+                   C.c_void_p(self.py.data_ptr()), g_rgb, g_alpha, C.byref(lc), C.c_void_p(self.loss4.data_ptr()),
                    cfg.density_points, (cfg.seed * 4 + self.rank) & (2**64 - 1), self.step_id,
                    C.c_void_p(self.loss_d.data_ptr()), sp)
         else:
             L.call("arfx_train_step_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
                    self.grid._h, C.byref(self._opt(f).to_c()), self.n_local, C.c_void_p(self.px.data_ptr()),
-                   C.c_void_p(self.py.data_ptr()), C.c_void_p(self.b_rgb.data_ptr()),
-                   C.c_void_p(self.b_alpha.data_ptr()), C.byref(cfg.loss.to_c()), C.c_void_p(self.loss4.data_ptr()),
+                   C.c_void_p(self.py.data_ptr()), g_rgb, g_alpha, C.byref(lc), C.c_void_p(self.loss4.data_ptr()),
                    None, None, sp)
             if dens:
                 L.call("arfx_density_step_device", self.model._h, self.views[f]._h, self.grid._h, cfg.density_points,

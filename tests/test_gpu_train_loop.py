@@ -377,3 +377,48 @@ def test_fused_density_step_matches_sequential(gpu):
         assert np.array_equal(x, y)
     for x, y in zip(a.model.adam_state(), b.model.adam_state()):
         assert np.array_equal(x, y)
+
+
+def test_frame_targets_match_per_ray_targets(gpu):
+    """arfx_loss_config.gt_width/height: the composite kernel reading whole ground-truth
+    frames at each ray's pixel == per-ray target arrays (bitwise losses and gradients;
+    pixels outside the frame read target 0)."""
+    import ctypes as C
+    import torch
+    from paper_2212_10550_b200 import _lib as L
+    sk = fx.default_figure_skeleton()
+    fig = fx.default_figure()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (24, 24, 24), 11)
+    m.set_deterministic(True)
+    pose = fx.random_pose(sk, 8, max_angle=0.3)
+    W, H = 80, 64
+    cam = fx.default_camera(sk, W, H)
+    occ = arf.OccupancyGrid(m.normalized_box, arf.OccupancyConfig())
+    arf.update_training_grid(m, occ, [pose], 0.95, 3, 0)
+    gt_img, mask = arf.figure_render(fig, pose, m.normalized_box, cam, arf.RenderOptions(samples_per_ray=256))
+    rng = np.random.default_rng(7)
+    n = 2048
+    px = rng.integers(0, W, n).astype(np.int32)
+    py = rng.integers(0, H, n).astype(np.int32)
+    px[:8] = W + 3  # outside the frame: a valid ray, target 0
+    inside = (px < W) & (py < H)
+    ray_rgb = np.where(inside[:, None], gt_img.rgb[np.minimum(py, H - 1), np.minimum(px, W - 1)], 0).astype(np.float32)
+    ray_a = np.where(inside, mask[np.minimum(py, H - 1), np.minimum(px, W - 1)], 0).astype(np.float32)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    t_px, t_py = dev(px), dev(py)
+    f_rgb, f_a = dev(gt_img.rgb.astype(np.float32)), dev(mask.astype(np.float32))
+    r_rgb, r_a = dev(ray_rgb), dev(ray_a)
+    opt = arf.RenderOptions(samples_per_ray=96, stratified=True, seed=3, frame_id=2)
+    view = arf.PosedModelView(m, pose)
+    out = []
+    for rgb_p, a_p, lc in ((r_rgb, r_a, arf.LossConfig().to_c()), (f_rgb, f_a, arf.LossConfig().to_c((W, H)))):
+        loss4 = torch.zeros(4, dtype=torch.float64, device="cuda")
+        m.zero_grad()
+        L.call("arfx_train_step_device", m._h, view._h, C.byref(cam.to_c()), occ._h, C.byref(opt.to_c()), n,
+               C.c_void_p(t_px.data_ptr()), C.c_void_p(t_py.data_ptr()), C.c_void_p(rgb_p.data_ptr()),
+               C.c_void_p(a_p.data_ptr()), C.byref(lc), C.c_void_p(loss4.data_ptr()), None, None, None)
+        torch.cuda.synchronize()
+        out.append((loss4.cpu().numpy(), *m.grads()))
+    assert out[0][0][0] > 0
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
