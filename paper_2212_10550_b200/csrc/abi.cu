@@ -275,6 +275,12 @@ ModelImpl::~ModelImpl() {
   }
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
+  }
+  if (ev_aux_fork) cudaEventDestroy(ev_aux_fork);
+  if (ev_aux_join) cudaEventDestroy(ev_aux_join);
 }
 
 void ModelImpl::refresh_views() { fill_field_view(*this); }

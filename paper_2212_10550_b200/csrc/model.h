@@ -158,6 +158,8 @@ struct ModelImpl {
   Workspace& ws() { return *ws_cur; }
   cudaStream_t side = nullptr;  // lazily created non-blocking stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t aux = nullptr;   // K8b/K8d next to K8c (field_backward_pool)
+  cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
   std::vector<uint8_t> overflow_note;
   ~ModelImpl();
   void refresh_views();

@@ -688,7 +688,23 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
   ARFX_CUDA(cudaGetLastError());
+  // K8b + K8d (MLP weights, smem/FP32) run on the aux stream beside K8c (hash-grid
+  // scatter, L2 atomics); both only read the K8a records. The join keeps the next
+  // gradient writer on `s` ordered after K8d's non-atomic mlp_grad update.
   const int wblocks = sms() * 4;
+  if (!m.aux) {
+    ARFX_CUDA(cudaStreamCreateWithFlags(&m.aux, cudaStreamNonBlocking));
+    ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_aux_fork, cudaEventDisableTiming));
+    ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_aux_join, cudaEventDisableTiming));
+  }
+  w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
+  ARFX_CUDA(cudaEventRecord(m.ev_aux_fork, s));
+  ARFX_CUDA(cudaStreamWaitEvent(m.aux, m.ev_aux_fork, 0));
+  field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, m.aux>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
+                                                                                  w.bwd_partial.ptr);
+  weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, m.aux>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  ARFX_CUDA(cudaEventRecord(m.ev_aux_join, m.aux));
   if (m.det) {
     const size_t n_acc = static_cast<size_t>(m.fv.L) * m.fv.T * 2;  // == n_grid
     if (m.grid_acc.n < n_acc) {  // zeroed once; consumers leave it all-zero
@@ -703,10 +719,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
     grid_scatter_kernel<false><<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(
         m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr, nullptr);
   }
-  w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
-  field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, s>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
-                                                                              w.bwd_partial.ptr);
-  weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, s>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
+  ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_aux_join, 0));
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
 }
