@@ -186,6 +186,13 @@ int arfx_model_set_mlp_mode(arfx_model m, int mode);
  * `stream`). arfx_model_zero_grad discards pending sums. */
 int arfx_model_set_deterministic(arfx_model m, int on);
 int arfx_model_flush_grads(arfx_model m, void* stream);
+/* Optimizer on its own stream: every kernel of this model that reads the parameters or
+ * writes the gradients (field forward / backward, gradient flush) first waits on `event`
+ * (a cudaEvent_t the caller records after each optimizer step; NULL clears). The trainer
+ * uses it to run Adam of step t concurrently with the march and deformer of step t+1,
+ * which read neither. Host-buffer APIs do not wait on it: synchronise the optimizer's
+ * stream before them. */
+int arfx_model_set_param_fence(arfx_model m, void* event);
 int arfx_model_zero_grad(arfx_model m, void* stream);
 int arfx_model_get_grads(arfx_model m, float* grid_grad, float* mlp_grad);
 /* device pointers of the parameter / gradient arrays (for NCCL / optimizers) */

@@ -111,6 +111,7 @@ _PROTOS = {
     "arfx_model_set_mlp_mode": (C.c_int, [H, C.c_int]),
     "arfx_model_set_deterministic": (C.c_int, [H, C.c_int]),
     "arfx_model_flush_grads": (C.c_int, [H, C.c_void_p]),
+    "arfx_model_set_param_fence": (C.c_int, [H, C.c_void_p]),
     "arfx_model_zero_grad": (C.c_int, [H, P]),
     "arfx_model_get_grads": (C.c_int, [H, c_float_p, c_float_p]),
     "arfx_model_device_arrays": (C.c_int, [H, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]),

@@ -267,6 +267,11 @@ class Model:
         before reading it through device pointers, e.g. a data-parallel reduce-scatter)."""
         call("arfx_model_flush_grads", self._h, stream)
 
+    def set_param_fence(self, event) -> None:
+        """cudaEvent_t handle (e.g. torch.cuda.Event().cuda_event) that parameter-reading /
+        gradient-writing kernels wait on; None clears (arfx_model_set_param_fence)."""
+        call("arfx_model_set_param_fence", self._h, event)
+
     def zero_grad(self):
         call("arfx_model_zero_grad", self._h, None)
 

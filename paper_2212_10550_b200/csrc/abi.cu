@@ -615,6 +615,13 @@ int arfx_model_zero_grad(arfx_model mh, void* stream) {
   });
 }
 
+int arfx_model_set_param_fence(arfx_model mh, void* event) {
+  return guard([&] {
+    require(mh != nullptr, "set_param_fence: null model");
+    mh->impl.param_fence = static_cast<cudaEvent_t>(event);
+  });
+}
+
 int arfx_model_flush_grads(arfx_model mh, void* stream) {
   return guard([&] {
     require(mh != nullptr, "flush_grads: null model");

@@ -159,6 +159,12 @@ struct ModelImpl {
   cudaStream_t side = nullptr;  // lazily created non-blocking stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t aux = nullptr;   // K8b/K8d next to K8c (field_backward_pool)
+  // arfx_model_set_param_fence: kernels that read the parameters or write the gradients
+  // wait for this event first (an optimizer running on another stream)
+  cudaEvent_t param_fence = nullptr;
+  void wait_params(cudaStream_t s) const {
+    if (param_fence) ARFX_CUDA(cudaStreamWaitEvent(s, param_fence, 0));
+  }
   cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
   std::vector<uint8_t> overflow_note;
   ~ModelImpl();

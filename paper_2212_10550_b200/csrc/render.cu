@@ -863,6 +863,7 @@ void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long lo
 // grids, training and the query APIs always use the exact f32 MLP so their integer
 // decisions (masks, root selection feeding gradients) stay reference-exact.
 void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allow_tc = false) {
+  m.wait_params(s);
   if (allow_tc && m.mlp_mode >= 1 && field_tc_supported(m.fv)) {
     launch_field_tc(m, s, n_hint);
     return;

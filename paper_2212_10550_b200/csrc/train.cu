@@ -668,6 +668,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   w.bwd_list.ensure(static_cast<size_t>(rec_cap + 1));
   w.bwd_n.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
+  m.wait_params(s);
   m.prof.begin("field_backward", s);
   if (m.det && own) {
     w.bwd_own.ensure(static_cast<size_t>(std::max<long long>(own->n_owner, 1)));
@@ -726,6 +727,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
 
 void flush_grad_acc(ModelImpl& m, cudaStream_t s) {
   if (!m.acc_pending) return;
+  m.wait_params(s);
   const long long n2 = static_cast<long long>(m.grid_acc.n / 2);
   grid_flush_kernel<<<static_cast<unsigned>(std::min<long long>((n2 + 255) / 256, sms() * 16LL)), 256, 0, s>>>(
       n2, reinterpret_cast<longlong2*>(m.grid_acc.ptr), reinterpret_cast<float2*>(m.grid_grad.ptr));

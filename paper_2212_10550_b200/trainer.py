@@ -158,6 +158,10 @@ class Trainer:
         arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
         self.step_id = 0
         self.fused_density = True  # arfx_train_density_step_device (False: the two calls in sequence)
+        # single rank: Adam on its own stream behind a parameter fence (overlaps the next step)
+        self.adam_stream = torch.cuda.Stream() if world == 1 else None
+        self.ev_params = torch.cuda.Event()
+        self._fence_set = False
         self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
         self._checked = 0     # steps whose loss has been checked for finiteness
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
@@ -214,16 +218,45 @@ class Trainer:
         t = self.step_id + 1
         if cfg.deterministic and self.world > 1:
             self.model.flush_grads(sp)  # the reduce-scatter reads the gradient array directly
-        self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
+        if self.adam_stream is not None:
+            # Adam of step t on its own stream, fenced: the next step's march and deformer
+            # (which read neither parameters nor gradients) run beside it, its field kernels
+            # wait on ev_params (arfx_model_set_param_fence)
+            self.adam_stream.wait_stream(self.stream)
+            self.model.adam_step(cfg.adam, t, 0, self.n_flat, C.c_void_p(self.adam_stream.cuda_stream))
+            self.ev_params.record(self.adam_stream)
+            if not self._fence_set:
+                self.model.set_param_fence(self.ev_params.cuda_event)
+                self._fence_set = True
+        else:
+            self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
         loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
                             self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
         self._hist.append(loss)
         self.step_id = t
         if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
-            self.stream.synchronize()  # the host-buffer API below runs on the library's stream
+            self._sync()  # the host-buffer API below runs on the library's stream
             arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t)
             self._check()
         return loss
+
+    def _sync(self):
+        self.stream.synchronize()
+        if self.adam_stream is not None:
+            self.adam_stream.synchronize()
+
+    def close(self):
+        """Detach the parameter fence (the model outlives the trainer)."""
+        self._sync()
+        if self._fence_set:
+            self.model.set_param_fence(None)
+            self._fence_set = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _check(self):
         if self._checked < len(self._hist):
@@ -237,20 +270,20 @@ class Trainer:
     @property
     def history(self) -> np.ndarray:
         """Per-step losses (synchronises): rows (L_rgb, L_alpha, L_hard, L_density, total)."""
-        self.stream.synchronize()
+        self._sync()
         self._check()
         return torch_stack_cpu(self.torch, self._hist) if self._hist else np.zeros((0, 5))
 
     def save(self, path) -> None:
         """Checkpoint (model, Adam moments, occupancy grid, step) for an exact resume."""
-        self.stream.synchronize()
+        self._sync()
         arf.save_checkpoint(path, self.model, self.grid, step=self.step_id, with_optimizer=True)
 
     def restore(self, path) -> None:
         """Resume from `save`: parameters, Adam moments, occupancy grid and step counter are
         replaced, so the following steps draw the same ray batches (keyed by step) as an
         uninterrupted run -- with TrainConfig.deterministic the continuation is bit-identical."""
-        self.stream.synchronize()
+        self._sync()
         m2, occ, step = arf.load_checkpoint(path)
         if occ is None:
             raise ValueError("restore: checkpoint has no occupancy grid")
