@@ -71,6 +71,7 @@ struct Workspace {
   DevBuf<float> dens_scale;            // w_density / n_empty
   DevBuf<float> train_rgb, train_alpha;  // training outputs when the caller passes none
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
+  DevBuf<int> occ_box;                  // occupied-cell bounding box (march empty-space skip)
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
   DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base

@@ -118,7 +118,74 @@ struct MarchArgs {
   unsigned long long* counters;
   long long cap;
   int rpw;  // rays per warp (1..32): small ray lists (training) spread over more warps
+  const int* occ_box;  // occupied-cell bounding box (-x0, -y0, -z0, x1, y1, z1) or nullptr
 };
+
+// Bounding box of the occupied cells, for the march's empty-space skip: stored as
+// (-x0, -y0, -z0, x1, y1, z1) so one atomicMax per entry reduces it; the buffer is preset
+// to 0x80808080 (a large negative int) by a memset, so an all-empty mask leaves x1 < x0.
+__global__ void __launch_bounds__(256) occ_bbox_kernel(OccView g, int* __restrict__ box) {
+  int b[6] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+  const long long n = static_cast<long long>(g.rx) * g.ry * g.rz;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!g.mask[i]) continue;
+    const int x = static_cast<int>(i % g.rx), y = static_cast<int>((i / g.rx) % g.ry),
+              z = static_cast<int>(i / (static_cast<long long>(g.rx) * g.ry));
+    b[0] = max(b[0], -x), b[1] = max(b[1], -y), b[2] = max(b[2], -z);
+    b[3] = max(b[3], x), b[4] = max(b[4], y), b[5] = max(b[5], z);
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b[k] = max(b[k], __shfl_xor_sync(0xffffffffu, b[k], o));
+  }
+  if ((threadIdx.x & 31) == 0 && b[3] >= 0)
+    for (int k = 0; k < 6; ++k) atomicMax(box + k, b[k]);
+}
+
+// Conservative sample-index range [i0, i1] of a ray that can reach an occupied cell: the
+// cell-space line v = P + Q t against the occupied box grown by one cell per side, then
+// one sample of slack each way (t_i = t_n + (i + j) step, j in [0, 1)). Samples outside
+// cannot fall in an occupied cell -- the exact per-sample decision is untouched inside.
+__device__ __forceinline__ void occ_index_range(const int* box, d3 P, d3 Q, double tn, double step, int N, int& i0,
+                                                int& i1) {
+  if (!(step > 0.0)) {  // degenerate segment: every sample at t_n, no skipping
+    i0 = 0, i1 = N - 1;
+    return;
+  }
+  double lo_t = -1e300, hi_t = 1e300;
+  const double p[3] = {P.x, P.y, P.z}, q[3] = {Q.x, Q.y, Q.z};
+  bool empty = box[3] < -box[0];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double lo = static_cast<double>(-box[a] - 1), hi = static_cast<double>(box[3 + a] + 2);
+    if (fabs(q[a]) < 1e-300) {
+      if (p[a] < lo || p[a] > hi) empty = true;
+    } else {
+      const double t1 = (lo - p[a]) / q[a], t2 = (hi - p[a]) / q[a];
+      lo_t = fmax(lo_t, fmin(t1, t2));
+      hi_t = fmin(hi_t, fmax(t1, t2));
+    }
+  }
+  if (empty || !(lo_t <= hi_t)) {
+    i0 = 1, i1 = 0;
+    return;
+  }
+  const double a0 = floor((lo_t - tn) / step) - 1.0, a1 = ceil((hi_t - tn) / step) + 1.0;
+  i0 = a0 < 0.0 ? 0 : (a0 > static_cast<double>(N) ? N : static_cast<int>(a0));
+  i1 = a1 < 0.0 ? -1 : (a1 > static_cast<double>(N - 1) ? N - 1 : static_cast<int>(a1));
+}
+
+const int* launch_occ_bbox(Workspace& w, const OccView& g, cudaStream_t s) {
+  w.occ_box.ensure(6);
+  ARFX_CUDA(cudaMemsetAsync(w.occ_box.ptr, 0x80, 6 * sizeof(int), s));
+  const long long n = static_cast<long long>(g.rx) * g.ry * g.rz;
+  occ_bbox_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 1184))), 256, 0,
+                    s>>>(g, w.occ_box.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  return w.occ_box.ptr;
+}
 
 __device__ __forceinline__ double jitter_at(const MarchArgs& A, Pcg32 base, int i) {
   if (!A.stratified) return 0.5;
@@ -138,12 +205,14 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
 // each ray's geometry by shuffle and testing its N samples 32 at a time (ballots kept in
 // dynamic smem). One block-wide exclusive scan of the 256 ray counts and one atomic place
 // the block's samples; the second pass recomputes t / x only for occupied samples.
-__global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
+__global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A) {
   extern __shared__ unsigned march_bal[];  // [256 rays][K]
   __shared__ int wsum[kMarchWarps];
   __shared__ long long bbase;
   __shared__ double w2n[12];
+  __shared__ int obox[6];
   if (threadIdx.x < 12) w2n[threadIdx.x] = A.pose->w2n[threadIdx.x];
+  if (threadIdx.x < 6) obox[threadIdx.x] = A.occ_box ? A.occ_box[threadIdx.x] : 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_rays = A.lpx ? A.n_list : static_cast<long long>(A.n_rows) * A.W;
@@ -158,6 +227,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
     double step = 0.0;
     Pcg32 rng{0, 0};
     d3 cP = make3(0.0, 0.0, 0.0), cQ = cP;
+    int r_i0 = 0, r_i1 = A.N - 1;  // samples that can reach an occupied cell
     if (r < n_rays) {
       int px, py;
       if (A.lpx) {
@@ -180,46 +250,92 @@ __global__ void __launch_bounds__(kMarchWarps * 32) march_kernel(MarchArgs A) {
         const double sx = A.occ.inv_e[0] * A.occ.rx, sy = A.occ.inv_e[1] * A.occ.ry, sz = A.occ.inv_e[2] * A.occ.rz;
         cP = make3((on.x - A.occ.lo[0]) * sx, (on.y - A.occ.lo[1]) * sy, (on.z - A.occ.lo[2]) * sz);
         cQ = make3(dn.x * sx, dn.y * sy, dn.z * sz);
+        if (A.has_occ && A.occ_box) occ_index_range(obox, cP, cQ, R.tn, step, A.N, r_i0, r_i1);
       }
     }
-    // ---- pass 1: occupancy ballots, ray by ray (warp-uniform loop)
     int my_count = 0;
-    const unsigned vmask = __ballot_sync(0xffffffffu, R.valid);
-    for (int j = 0; j < 32; ++j) {
-      if (!((vmask >> j) & 1u)) continue;
-      const double Px = shfl_d(cP.x, j), Py = shfl_d(cP.y, j), Pz = shfl_d(cP.z, j);
-      const double Qx = shfl_d(cQ.x, j), Qy = shfl_d(cQ.y, j), Qz = shfl_d(cQ.z, j);
-      const double tn = shfl_d(R.tn, j), st = shfl_d(step, j);
-      const Pcg32 rg{shfl_u64(rng.state, j), shfl_u64(rng.inc, j)};
-      const int pj = __shfl_sync(0xffffffffu, pix, j);
-      unsigned* bal = march_bal + (warp * 32 + j) * K;
-      int count = 0;
-      for (int k = 0; k < K; ++k) {
-        const int i = k * 32 + lane;
-        bool f = false;
-        if (i < A.N) {
-          if (A.has_occ) {
-            // t exactly as the reference; the cell decision from v = P + Q t (one FMA per
-            // axis), exact reference arithmetic only within 1e-12 of a cell edge
-            const double t = sample_t(tn, st, i, jitter_at(A, rg, i));
-            const int cx = cell_from_v(__fma_rn(Qx, t, Px), A.occ.rx);
-            const int cy = cell_from_v(__fma_rn(Qy, t, Py), A.occ.ry);
-            const int cz = cell_from_v(__fma_rn(Qz, t, Pz), A.occ.rz);
-            if (cx == -2 || cy == -2 || cz == -2) {
-              const RayGeom Rj = make_ray(A.cam, w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
-              f = occupied(A.occ, rigid_apply(w2n, add3(Rj.o, mul3(Rj.d, t))));
-            } else if (cx >= 0 && cy >= 0 && cz >= 0) {
+    if (A.rpw == 32) {
+      // ---- pass 1, thread per ray (full warps): each lane walks its own ray's samples
+      // (stratified jitter drawn sequentially from the ray's stream: draw i == jitter_at(i)),
+      // only over [r_i0, r_i1], the samples that can reach the occupied box
+      if (R.valid) {
+        unsigned* bal = march_bal + (warp * 32 + lane) * K;
+        for (int k = 0; k < K; ++k) bal[k] = 0u;
+        if (!A.has_occ) {
+          for (int k = 0; k < K; ++k) bal[k] = (A.N - 32 * k >= 32) ? 0xffffffffu : ((1u << (A.N - 32 * k)) - 1u);
+          my_count = A.N;
+        } else {
+          Pcg32 g = rng;
+          if (A.stratified && r_i0 > 0) pcg_advance(g, static_cast<uint64_t>(r_i0));
+          unsigned word = 0u;
+          int wk = r_i0 >> 5;
+          for (int i = r_i0; i <= r_i1; ++i) {
+            const double t = sample_t(R.tn, step, i, A.stratified ? pcg_double(g) : 0.5);
+            const int cx = cell_from_v(__fma_rn(cQ.x, t, cP.x), A.occ.rx);
+            const int cy = cell_from_v(__fma_rn(cQ.y, t, cP.y), A.occ.ry);
+            const int cz = cell_from_v(__fma_rn(cQ.z, t, cP.z), A.occ.rz);
+            bool f = false;
+            if (cx == -2 || cy == -2 || cz == -2)
+              f = occupied(A.occ, rigid_apply(w2n, add3(R.o, mul3(R.d, t))));
+            else if (cx >= 0 && cy >= 0 && cz >= 0)
               f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
+            if ((i >> 5) != wk) {
+              bal[wk] = word;
+              word = 0u;
+              wk = i >> 5;
             }
-          } else {
-            f = true;
+            if (f) {
+              word |= 1u << (i & 31);
+              ++my_count;
+            }
           }
+          if (r_i0 <= r_i1) bal[wk] = word;
         }
-        const unsigned b = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) bal[k] = b;
-        count += __popc(b);
       }
-      if (lane == j) my_count = count;
+    } else {
+      // ---- pass 1, warp per ray (small batches, rays per warp < 32): lanes over samples
+      const unsigned vmask = __ballot_sync(0xffffffffu, R.valid);
+      for (int j = 0; j < 32; ++j) {
+        if (!((vmask >> j) & 1u)) continue;
+        const double Px = shfl_d(cP.x, j), Py = shfl_d(cP.y, j), Pz = shfl_d(cP.z, j);
+        const double Qx = shfl_d(cQ.x, j), Qy = shfl_d(cQ.y, j), Qz = shfl_d(cQ.z, j);
+        const double tn = shfl_d(R.tn, j), st = shfl_d(step, j);
+        const Pcg32 rg{shfl_u64(rng.state, j), shfl_u64(rng.inc, j)};
+        const int pj = __shfl_sync(0xffffffffu, pix, j);
+        const int ri0 = __shfl_sync(0xffffffffu, r_i0, j), ri1 = __shfl_sync(0xffffffffu, r_i1, j);
+        unsigned* bal = march_bal + (warp * 32 + j) * K;
+        int count = 0;
+        for (int k = 0; k < K; ++k) {
+          const int i = k * 32 + lane;
+          if (k * 32 > ri1 || k * 32 + 31 < ri0) {  // whole chunk outside the occupied box
+            if (lane == 0) bal[k] = 0u;
+            continue;
+          }
+          bool f = false;
+          if (i < A.N && i >= ri0 && i <= ri1) {
+            if (A.has_occ) {
+              // t exactly as the reference; the cell decision from v = P + Q t (one FMA per
+              // axis), exact reference arithmetic only within 1e-12 of a cell edge
+              const double t = sample_t(tn, st, i, jitter_at(A, rg, i));
+              const int cx = cell_from_v(__fma_rn(Qx, t, Px), A.occ.rx);
+              const int cy = cell_from_v(__fma_rn(Qy, t, Py), A.occ.ry);
+              const int cz = cell_from_v(__fma_rn(Qz, t, Pz), A.occ.rz);
+              if (cx == -2 || cy == -2 || cz == -2) {
+                const RayGeom Rj = make_ray(A.cam, w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
+                f = occupied(A.occ, rigid_apply(w2n, add3(Rj.o, mul3(Rj.d, t))));
+              } else if (cx >= 0 && cy >= 0 && cz >= 0) {
+                f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
+              }
+            } else {
+              f = true;
+            }
+          }
+          const unsigned b = __ballot_sync(0xffffffffu, f);
+          if (lane == 0) bal[k] = b;
+          count += __popc(b);
+        }
+        if (lane == j) my_count = count;
+      }
     }
     // ---- block exclusive scan of the 256 ray counts, one atomic per block
     int incl = my_count;
@@ -1011,7 +1127,10 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   A.nhi[1] = m.norm.hi.y;
   A.nhi[2] = m.norm.hi.z;
   A.has_occ = occ != nullptr;
-  if (occ) A.occ = occ->view();
+  if (occ) {
+    A.occ = occ->view();
+    A.occ_box = launch_occ_bbox(w, A.occ, s);
+  }
   A.N = N;
   A.stratified = stratified;
   A.seed = seed;
@@ -1077,7 +1196,10 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   A.nhi[1] = m.norm.hi.y;
   A.nhi[2] = m.norm.hi.z;
   A.has_occ = occ != nullptr;
-  if (occ) A.occ = occ->view();
+  if (occ) {
+    A.occ = occ->view();
+    A.occ_box = launch_occ_bbox(w, A.occ, s);
+  }
   A.N = N;
   A.stratified = stratified;
   A.seed = seed;

@@ -390,3 +390,28 @@ def test_frame_graph_replays_updated_poses(gpu):
             assert np.array_equal(alpha.cpu().numpy().reshape(96, 96), ref_img.alpha)
     finally:
         call("arfx_frame_graph_destroy", g)
+
+
+@pytest.mark.parametrize("stratified", [False, True])
+def test_thread_per_ray_march_matches_warp_march(gpu, stratified):
+    """K1 has two pass-1 forms: thread per ray for full-warp launches (>= ~150 k rays, the
+    animation frames) and warp per ray for smaller batches (verified sample for sample
+    against the reference above). A 480x420 frame takes the first; each of its two
+    16-row-tile shards (~100 k rays) takes the second: images and posed-sample counts must
+    be identical."""
+    sk = fx.smpl24()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    pose = fx.animation_poses(sk, 2)[1]
+    cam = fx.default_camera(sk, 480, 420)
+    occ = arf.build_model_inference_grid(m, pose, fx.config1_occupancy())
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=stratified, seed=3, frame_id=5)
+    p0 = m.counters.posed_queries
+    full = arf.render_model(m, pose, cam, occ, opt)
+    p1 = m.counters.posed_queries
+    halves = arf.RenderImages(480, 420, np.zeros((420, 480, 3), np.float32), np.zeros((420, 480), np.float32))
+    for shard in range(2):
+        arf.render_model(m, pose, cam, occ, opt, shard, 2, out=halves)
+    p2 = m.counters.posed_queries
+    assert p1 - p0 == p2 - p1 > 100000
+    assert np.array_equal(full.rgb, halves.rgb) and np.array_equal(full.alpha, halves.alpha)
+    assert (full.alpha > 0).sum() > 5000
