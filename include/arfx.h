@@ -204,6 +204,10 @@ int arfx_pose_create(arfx_model m, const double* bone_transforms12, const double
                      arfx_pose* out);
 int arfx_pose_update(arfx_pose p, const double* bone_transforms12, const double* global12,
                      void* stream);
+/* arfx_pose_update without the stream synchronisation: the PoseContext is staged in a
+ * pinned ring and copied on `stream` (kernels enqueued earlier still see the old pose);
+ * the host arrays may be reused on return. */
+int arfx_pose_update_async(arfx_pose p, const double* bones12, const double* global12, void* stream);
 int arfx_pose_destroy(arfx_pose p);
 
 /* ---- occupancy grid ---------------------------------------------------- */
@@ -256,6 +260,16 @@ int arfx_render_model_device(arfx_model m, arfx_pose p, const arfx_camera* cam,
                              arfx_occ_grid occ, const arfx_render_options* opt, int row_shard,
                              int n_shards, float* d_rgb, float* d_alpha, uint64_t* d_counters,
                              void* stream);
+/* arfx_render_model with host buffers but no host round trip (pipelines frames): the frame
+ * renders on `stream` into one of two library-owned device image slots and this shard's
+ * rows, plus counters4 = (posed, canonical, pool, overflow), are copied to the host buffers
+ * on a library copy stream while the next frame renders. The host buffers (pinned for
+ * overlap) are valid after arfx_render_wait. counters4[3] != 0: the workspace overflowed,
+ * re-render that frame with arfx_render_model (which grows it). */
+int arfx_render_model_async(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
+                            const arfx_render_options* opt, int shard, int n_shards, float* rgb, float* alpha,
+                            uint64_t* counters4, void* stream);
+int arfx_render_wait(arfx_model m);
 /* Trace of the last render on this model (posed-sample list), for parity tests:
  * per posed sample: pixel, sample index, has_root, density, rgb, canonical root. */
 int arfx_render_trace(arfx_model m, int64_t capacity, int64_t* n_samples, int32_t* s_ray,

@@ -117,6 +117,11 @@ _PROTOS = {
     "arfx_model_device_arrays": (C.c_int, [H, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
     "arfx_pose_create": (C.c_int, [H, c_double_p, c_double_p, C.POINTER(H)]),
     "arfx_pose_update": (C.c_int, [H, c_double_p, c_double_p, P]),
+    "arfx_pose_update_async": (C.c_int, [H, c_double_p, c_double_p, P]),
+    "arfx_render_model_async": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int,
+                                          C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                          C.POINTER(C.c_uint64), P]),
+    "arfx_render_wait": (C.c_int, [H]),
     "arfx_pose_destroy": (C.c_int, [H]),
     "arfx_occ_create": (C.c_int, [c_double_p, c_double_p, C.POINTER(ArfxOccConfig), C.POINTER(H)]),
     "arfx_occ_destroy": (C.c_int, [H]),

@@ -385,10 +385,11 @@ class PosedModelView:
              ptr(pose.global_transform, C.c_double), C.byref(h))
         self._h = h
 
-    def update(self, pose: SkeletonPose, stream=None):
+    def update(self, pose: SkeletonPose, stream=None, sync: bool = True):
+        """sync=False: arfx_pose_update_async (staged copy on `stream`, no synchronisation)."""
         self.pose = pose
-        call("arfx_pose_update", self._h, ptr(pose.bone_transforms, C.c_double),
-             ptr(pose.global_transform, C.c_double), stream)
+        call("arfx_pose_update" if sync else "arfx_pose_update_async", self._h,
+             ptr(pose.bone_transforms, C.c_double), ptr(pose.global_transform, C.c_double), stream)
 
     def close(self):
         if self._h:
@@ -555,6 +556,25 @@ def render_model(model: Model, pose: "SkeletonPose | PosedModelView", camera: Ca
     model.counters.posed_queries += cnt.posed_queries
     model.counters.canonical_queries += cnt.canonical_queries
     return out
+
+
+def render_model_async(model: Model, pose: "PosedModelView", camera: Camera, occupancy: "OccupancyGrid | None",
+                       opt: RenderOptions, out: RenderImages, counters: np.ndarray, shard: int = 0,
+                       n_shards: int = 1, stream=None) -> None:
+    """arfx_render_model_async: enqueue the frame; `out` (pinned numpy arrays for overlap) and
+    `counters` (uint64[4]: posed, canonical, pool, overflow) are filled once render_wait
+    returns. A frame with counters[3] != 0 overflowed the workspace: re-render it with
+    render_model."""
+    assert counters.dtype == np.uint64 and counters.size >= 4 and counters.flags.c_contiguous
+    call("arfx_render_model_async", model._h, pose._h, C.byref(camera.to_c()),
+         occupancy._h if occupancy is not None else None, C.byref(opt.to_c()), shard, n_shards,
+         ptr(out.rgb, C.c_float), ptr(out.alpha, C.c_float),
+         counters.ctypes.data_as(C.POINTER(C.c_uint64)), stream)
+
+
+def render_wait(model: Model) -> None:
+    """Wait for every render_model_async copy of this model (host buffers valid after)."""
+    call("arfx_render_wait", model._h)
 
 
 @dataclass

@@ -281,9 +281,26 @@ ModelImpl::~ModelImpl() {
   }
   if (ev_aux_fork) cudaEventDestroy(ev_aux_fork);
   if (ev_aux_join) cudaEventDestroy(ev_aux_join);
+  if (copy_stream) {
+    cudaStreamSynchronize(copy_stream);
+    cudaStreamDestroy(copy_stream);
+  }
+  for (auto& a : async_slot) {
+    if (a.rendered) cudaEventDestroy(a.rendered);
+    if (a.copied) cudaEventDestroy(a.copied);
+  }
 }
 
 void ModelImpl::refresh_views() { fill_field_view(*this); }
+
+PoseImpl::~PoseImpl() {
+  for (auto& e : ring_ev)
+    if (e) {
+      cudaEventSynchronize(e);
+      cudaEventDestroy(e);
+    }
+  if (ring) cudaFreeHost(ring);
+}
 
 }  // namespace arfx
 
@@ -704,6 +721,28 @@ int arfx_pose_update(arfx_pose ph, const double* bones12, const double* global12
   });
 }
 
+int arfx_pose_update_async(arfx_pose ph, const double* bones12, const double* global12, void* stream) {
+  return guard([&] {
+    require(ph != nullptr, "pose_update: null pose");
+    PoseImpl& p = ph->impl;
+    ModelImpl& m = *p.model;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    make_pose_host(m, bones12, global12, p.host);
+    if (!p.ring) {
+      ARFX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p.ring), PoseImpl::kRing * sizeof(PoseCtx),
+                              cudaHostAllocDefault));
+      for (auto& e : p.ring_ev) ARFX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int k = p.ring_next;
+    p.ring_next = (k + 1) % PoseImpl::kRing;
+    ARFX_CUDA(cudaEventSynchronize(p.ring_ev[k]));  // this staging slot's last copy has run
+    p.ring[k] = p.host;
+    ARFX_CUDA(cudaMemcpyAsync(p.dev.ptr, p.ring + k, sizeof(PoseCtx), cudaMemcpyHostToDevice, s));
+    ARFX_CUDA(cudaEventRecord(p.ring_ev[k], s));
+  });
+}
+
 int arfx_pose_destroy(arfx_pose p) {
   return guard([&] { delete p; });
 }
@@ -1085,6 +1124,80 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
       return;
     }
     throw std::runtime_error("render_model: workspace overflow persisted");
+  });
+}
+
+// Host-buffer render without a host round trip: the frame renders into one of two device
+// image slots on `stream`; the slot's D2H copies (this shard's row tiles, counters) run on
+// the model's copy stream while the next frame renders. A slot is re-used only after its
+// previous copies completed (device-side wait).
+int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                            const arfx_render_options* opt, int shard, int nshards, float* rgb, float* alpha,
+                            uint64_t* counters4, void* stream) {
+  return guard([&] {
+    require(mh && ph && rgb && alpha, "render_model_async: null argument");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    if (!m.copy_stream) {
+      ARFX_CUDA(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
+      for (auto& a : m.async_slot) {
+        ARFX_CUDA(cudaEventCreateWithFlags(&a.rendered, cudaEventDisableTiming));
+        ARFX_CUDA(cudaEventCreateWithFlags(&a.copied, cudaEventDisableTiming));
+      }
+    }
+    ModelImpl::AsyncSlot& a = m.async_slot[m.async_next];
+    m.async_next ^= 1;
+    const size_t npix = static_cast<size_t>(hc.width) * hc.height;
+    if (a.rgb.n < npix * 3) {
+      ARFX_CUDA(cudaDeviceSynchronize());  // growing a slot: nothing in flight may use it
+      a.rgb.ensure(npix * 3);
+      a.alpha.ensure(npix);
+      a.counters.ensure(4);
+    }
+    ARFX_CUDA(cudaStreamWaitEvent(s, a.copied, 0));  // the slot's previous copies are done
+    render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+                 opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, a.rgb.ptr, a.alpha.ptr,
+                 a.counters.ptr, s);
+    ARFX_CUDA(cudaEventRecord(a.rendered, s));
+    const cudaStream_t c = m.copy_stream;
+    ARFX_CUDA(cudaStreamWaitEvent(c, a.rendered, 0));
+    const int W = hc.width, H = hc.height, T = 16;
+    const int full_tiles = H / T;
+    const int n_full = shard < full_tiles ? (full_tiles - 1 - shard) / nshards + 1 : 0;
+    if (n_full > 0) {
+      const size_t off = static_cast<size_t>(shard) * T * W;
+      const size_t pitch3 = static_cast<size_t>(nshards) * T * W * 3 * sizeof(float);
+      const size_t pitch1 = static_cast<size_t>(nshards) * T * W * sizeof(float);
+      ARFX_CUDA(cudaMemcpy2DAsync(rgb + off * 3, pitch3, a.rgb.ptr + off * 3, pitch3,
+                                  static_cast<size_t>(T) * W * 3 * sizeof(float), static_cast<size_t>(n_full),
+                                  cudaMemcpyDeviceToHost, c));
+      ARFX_CUDA(cudaMemcpy2DAsync(alpha + off, pitch1, a.alpha.ptr + off, pitch1,
+                                  static_cast<size_t>(T) * W * sizeof(float), static_cast<size_t>(n_full),
+                                  cudaMemcpyDeviceToHost, c));
+    }
+    if (H % T && full_tiles % nshards == shard) {
+      const size_t off = static_cast<size_t>(full_tiles) * T * W;
+      const size_t rows = static_cast<size_t>(H % T);
+      ARFX_CUDA(cudaMemcpyAsync(rgb + off * 3, a.rgb.ptr + off * 3, rows * W * 3 * sizeof(float),
+                                cudaMemcpyDeviceToHost, c));
+      ARFX_CUDA(cudaMemcpyAsync(alpha + off, a.alpha.ptr + off, rows * W * sizeof(float), cudaMemcpyDeviceToHost,
+                                c));
+    }
+    if (counters4)
+      ARFX_CUDA(cudaMemcpyAsync(counters4, a.counters.ptr, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c));
+    ARFX_CUDA(cudaEventRecord(a.copied, c));
+  });
+}
+
+int arfx_render_wait(arfx_model mh) {
+  return guard([&] {
+    require(mh != nullptr, "render_wait: null model");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (m.copy_stream) ARFX_CUDA(cudaStreamSynchronize(m.copy_stream));
   });
 }
 

@@ -160,6 +160,15 @@ struct ModelImpl {
   cudaStream_t side = nullptr;  // lazily created non-blocking stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t aux = nullptr;   // K8b/K8d next to K8c (field_backward_pool)
+  // arfx_render_model_async: two device image slots; their D2H copies run on copy_stream
+  // while the next frame renders
+  struct AsyncSlot {
+    DevBuf<float> rgb, alpha;
+    DevBuf<unsigned long long> counters;
+    cudaEvent_t rendered = nullptr, copied = nullptr;
+  } async_slot[2];
+  int async_next = 0;
+  cudaStream_t copy_stream = nullptr;
   // arfx_model_set_param_fence: kernels that read the parameters or write the gradients
   // wait for this event first (an optimizer running on another stream)
   cudaEvent_t param_fence = nullptr;
@@ -176,6 +185,12 @@ struct PoseImpl {
   ModelImpl* model = nullptr;
   PoseCtx host{};
   DevBuf<PoseCtx> dev;
+  // arfx_pose_update_async: pinned staging ring (the H2D copy never waits on the stream)
+  static constexpr int kRing = 4;
+  PoseCtx* ring = nullptr;
+  cudaEvent_t ring_ev[kRing] = {};
+  int ring_next = 0;
+  ~PoseImpl();
 };
 
 struct OccImpl {

@@ -415,3 +415,34 @@ def test_thread_per_ray_march_matches_warp_march(gpu, stratified):
     assert p1 - p0 == p2 - p1 > 100000
     assert np.array_equal(full.rgb, halves.rgb) and np.array_equal(full.alpha, halves.alpha)
     assert (full.alpha > 0).sum() > 5000
+
+
+def test_async_host_render_pipeline_matches_sync(gpu):
+    """arfx_pose_update_async + async inference grid + arfx_render_model_async over several
+    frames (copies of frame k overlap frame k+1) give exactly the synchronous renders."""
+    import torch
+    from paper_2212_10550_b200._lib import check, lib
+    sk = fx.smpl24()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = fx.animation_poses(sk, 3)
+    cam = fx.default_camera(sk, 200, 180)
+    opt = fx.config1_render_options()
+    cfg = fx.config1_occupancy()
+    ref = []
+    for p in poses:
+        occ = arf.build_model_inference_grid(m, p, cfg)
+        ref.append(arf.render_model(m, p, cam, occ, opt))
+    L = lib()
+    occ = arf.OccupancyGrid(m.normalized_box, cfg)
+    view = arf.PosedModelView(m, poses[0])
+    pin = lambda shape: torch.zeros(shape, dtype=torch.float32).pin_memory().numpy()  # noqa: E731
+    outs = [arf.RenderImages(200, 180, pin((180, 200, 3)), pin((180, 200))) for _ in poses]
+    cnts = [np.zeros(4, np.uint64) for _ in poses]
+    for p, o, c in zip(poses, outs, cnts):
+        view.update(p, sync=False)
+        check(L.arfx_build_inference_grid(m._h, view._h, occ._h, None, None))
+        arf.render_model_async(m, view, cam, occ, opt, o, c)
+    arf.render_wait(m)
+    for r, o, c in zip(ref, outs, cnts):
+        assert c[3] == 0 and c[0] > 0
+        assert np.array_equal(r.rgb, o.rgb) and np.array_equal(r.alpha, o.alpha)
