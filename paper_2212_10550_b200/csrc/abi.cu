@@ -1627,7 +1627,7 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
     train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
     const BwdOwners own{n_rays, w.ray_first.ptr, w.ray_count.ptr, false};
     field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
-                        w.pgc.ptr, s, &own);
+                        w.pgc.ptr, s, &own, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
     return;
   }
   DevBuf<unsigned long long> bad;
@@ -1655,7 +1655,7 @@ void run_train(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, co
   train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, d_dC, d_dA, d_rgb, d_alpha, s, lt);
   const BwdOwners own{n_rays, w.ray_first.ptr, w.ray_count.ptr, false};
   field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
-                      s, &own);
+                      s, &own, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
 }
 
 LossTargets loss_targets(const arfx_loss_config* cfg, const float* gt_rgb, const float* gt_alpha, double* terms) {

@@ -72,6 +72,7 @@ struct Workspace {
   DevBuf<float> train_rgb, train_alpha;  // training outputs when the caller passes none
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
   DevBuf<int> occ_box;                  // occupied-cell bounding box (march empty-space skip)
+  DevBuf<float> fwd_act;  // training forwards: per pool entry X | H1 | H2 | logits (K8a reuses them)
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
   DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base
@@ -287,8 +288,16 @@ struct BwdOwners {
   const int32_t *first, *count;
   bool pool_is_target;
 };
+// Saved decoder activations (training forwards through the team decoder, pool <= 65536
+// queries): per pool entry X[32] | H1[64] | H2[64] | logits[4], bit-identical to a recompute.
+constexpr int kActStride = 164;
+#ifndef ARFX_SAVE_ACT
+#define ARFX_SAVE_ACT 1  // 0: K8a always recomputes the forward (reference build for tests)
+#endif
+constexpr long long kTeamMaxQueries = 65536;
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
-                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own);
+                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own,
+                         const float* act = nullptr);
 void flush_grad_acc(ModelImpl& m, cudaStream_t s);  // deterministic mode: grid_acc -> grid_grad
 
 // field_tc.cu

@@ -551,7 +551,8 @@ __global__ void __launch_bounds__(kFtTeam * kFtTeams) field_team_kernel(FieldVie
                                                                         const int32_t* __restrict__ owner,
                                                                         float4* __restrict__ res,
                                                                         const unsigned long long* n_dev, long long cap,
-                                                                        unsigned long long* stats, long long team_max) {
+                                                                        unsigned long long* stats, long long team_max,
+                                                                        float* __restrict__ act) {
   constexpr int IN = 32, HID = 64, W0S = IN + 1, W1S = HID + 1;
   __shared__ float W0p[HID * W0S], W1p[HID * W1S], W2p[4 * W1S], Bs[2 * HID + 4];
   __shared__ float X[kFtTeams][kFtQ][IN], H1[kFtTeams][kFtQ][HID], H2[kFtTeams][kFtQ][HID];
@@ -626,6 +627,20 @@ __global__ void __launch_bounds__(kFtTeam * kFtTeams) field_team_kernel(FieldVie
           lg[o] = a;
         }
         res[k0 + j] = make_float4(softplus_f(lg[0]), logistic_f(lg[1]), logistic_f(lg[2]), logistic_f(lg[3]));
+        if (act) {
+#pragma unroll
+          for (int o = 0; o < 4; ++o) act[(k0 + j) * kActStride + 160 + o] = lg[o];
+        }
+      }
+    }
+    if (act) {  // training: keep X | H1 | H2 for the field backward (K8a)
+#pragma unroll
+      for (int j = 0; j < kFtQ; ++j) {
+        if (!OK[team][j]) continue;
+        float* A = act + (k0 + j) * kActStride;
+        if (t < IN) A[t] = X[team][j][t];
+        A[IN + t] = H1[team][j][t];
+        A[IN + HID + t] = H2[team][j][t];
       }
     }
     asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(kFtTeam) : "memory");
@@ -978,7 +993,8 @@ void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long lo
 // allow_tc: the render may use the tcgen05 decoder (arfx_model_set_mlp_mode); occupancy
 // grids, training and the query APIs always use the exact f32 MLP so their integer
 // decisions (masks, root selection feeding gradients) stay reference-exact.
-void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allow_tc = false) {
+void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allow_tc = false,
+                       float* act = nullptr) {
   m.wait_params(s);
   if (allow_tc && m.mlp_mode >= 1 && field_tc_supported(m.fv)) {
     launch_field_tc(m, s, n_hint);
@@ -995,11 +1011,11 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
                                                                         std::max(per_sm, 1))));
     // the query count is only known on the device: both kernels are launched and exactly one
     // of them runs, by the count (teams below kTeamMax queries, tiles above)
-    constexpr long long kTeamMax = 65536;
+    constexpr long long kTeamMax = kTeamMaxQueries;
     m.prof.begin("field", s);
     field_team_kernel<<<static_cast<unsigned>(sm_count() * 8), kFtTeam * kFtTeams, 0, s>>>(
         m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr, m.ws().pres.ptr, m.ws().counters.ptr + 2,
-        static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax);
+        static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax, act);
     kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,
                                          m.ws().pres.ptr, m.ws().counters.ptr + 2,
                                          static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr,
@@ -1231,7 +1247,8 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   }
   ListSrc src{w.sx.ptr, w.sy.ptr, w.sz.ptr, w.counters.ptr, 0, static_cast<long long>(w.cap_posed)};
   launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s);
-  launch_field_pool(m, s, static_cast<long long>(w.cap_pool));
+  w.fwd_act.ensure(static_cast<size_t>(kTeamMaxQueries) * kActStride);
+  launch_field_pool(m, s, static_cast<long long>(w.cap_pool), false, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
   finalize_counters_kernel<<<1, 1, 0, s>>>(w.counters.ptr, static_cast<long long>(w.cap_posed));
 }
 
@@ -1589,7 +1606,8 @@ void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_
   // empty-cell fraction is ~90 %, and querying all keeps the pipeline branch-free
   ListSrc src{x, x + n, x + 2 * n, nullptr, n, n};
   launch_deform(m, p.dev.ptr, src, n, s);
-  launch_field_pool(m, s, n);
+  w.fwd_act.ensure(static_cast<size_t>(kTeamMaxQueries) * kActStride);
+  launch_field_pool(m, s, n, false, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
 }
 
 // Backward half: loss reduction and gradient flags, then K8 into the model's gradients.
@@ -1606,7 +1624,7 @@ void density_backward(ModelImpl& m, long long n, double w_density, double* d_out
   ARFX_CUDA(cudaGetLastError());
   const BwdOwners own{n, nullptr, nullptr, false};  // owner = density point = target
   field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
-                      s, &own);
+                      s, &own, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
 }
 
 }  // namespace arfx

@@ -264,7 +264,9 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
                                                                       const float* __restrict__ pgs,
                                                                       const float* __restrict__ pgc,
                                                                       float* __restrict__ grid_grad,
-                                                                      float* __restrict__ rec) {
+                                                                      float* __restrict__ rec,
+                                                                      const float* __restrict__ act,
+                                                                      const unsigned long long* pool_n) {
   extern __shared__ float bw_smem[];
   float* W0p = bw_smem;                    // [64][33]
   float* W1p = W0p + kHid * kW0s;          // [64][65]
@@ -287,10 +289,22 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
   float* S0 = TS + team * kTQ * kTeamSmem;
   auto S = [&](int j) { return S0 + j * kTeamSmem; };
   const long long n = static_cast<long long>(*n_list);
+  // the forward's saved activations are valid when it ran the team decoder (pool <= 64 Ki)
+  const bool use_act = act != nullptr && static_cast<long long>(*pool_n) <= kTeamMaxQueries;
   const int ej = t >> 4, el = t & 15;  // encode phases: query ej, level el
   for (long long k0 = (static_cast<long long>(blockIdx.x) * kTeams + team) * kTQ; k0 < n;
        k0 += static_cast<long long>(gridDim.x) * kTeams * kTQ) {
     const int nq = static_cast<int>(n - k0 < kTQ ? n - k0 : kTQ);
+    if (use_act) {  // X | H1 | H2 | logits as the forward computed them (bit-identical)
+      for (int j = 0; j < nq; ++j) {
+        const float* A = act + static_cast<long long>(list[k0 + j]) * kActStride;
+        if (t < kIn) S(j)[kRecX + t] = A[t];
+        S(j)[kRecH1 + t] = A[kIn + t];
+        S(j)[kRecH2 + t] = A[kIn + kHid + t];
+        if (t < kOut) S(j)[kRecStride + t] = A[kIn + 2 * kHid + t];
+      }
+      team_sync(team);
+    } else {
     // ---- encode (thread = (query ej, level el)) ----
     double u[3] = {0.0, 0.0, 0.0};
     long long qe = -1;
@@ -328,12 +342,18 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
       for (int j = 0; j < kTQ; ++j) S(j)[kRecH2 + t] = (a[j] < 0.0f) ? 0.0f : a[j];
     }
     team_sync(team);
+    }  // recompute
     if (t < kTQ * kOut) {  // logits + d logits (R/field.hpp:95-99), thread = (query, output)
       const int j = t / kOut, o = t % kOut;
       if (j < nq) {
         const long long q = list[k0 + j];
-        float a = Bs[2 * kHid + o];
-        for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(W2p[o * kW1s + i], S(j)[kRecH2 + i]));
+        float a;
+        if (use_act) {
+          a = S(j)[kRecStride + o];
+        } else {
+          a = Bs[2 * kHid + o];
+          for (int i = 0; i < kHid; ++i) a = fadd(a, fmul(W2p[o * kW1s + i], S(j)[kRecH2 + i]));
+        }
         float uo;
         if (o == 0) {
           uo = fmul(pgs[q], logistic_f(a));
@@ -659,7 +679,7 @@ int sms() {
 }  // namespace
 
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
-                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own) {
+                         const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own, const float* act) {
   if (!(m.fv.F == 2 && m.fv.in_dim == kIn && m.fv.hidden == kHid && m.fv.n_layers == 3 && m.fv.out_dim == kOut))
     throw std::invalid_argument("train path: libarfx implements the 32-64-64-4 decoder (levels*F == 32)");
   Workspace& w = m.ws();
@@ -687,7 +707,8 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
-      m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr);
+      m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr, act,
+      d_n);
   ARFX_CUDA(cudaGetLastError());
   // K8b + K8d (MLP weights, smem/FP32) run on the aux stream beside K8c (hash-grid
   // scatter, L2 atomics); both only read the K8a records. The join keeps the next
