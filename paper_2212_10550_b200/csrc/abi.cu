@@ -179,6 +179,7 @@ void fill_field_view(ModelImpl& m) {
   s.weights = m.skin.ptr;
   s.cell_mask = m.cell_mask.ptr;
   s.cell_off = m.cell_off.ptr;
+  s.cell_mo = m.cell_mo.ptr;
   s.cell_vals = m.cell_vals.ptr;
 }
 

@@ -10,6 +10,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <vector_types.h>  // uint2 (host compilers too)
+
 namespace arfx {
 
 constexpr int kMaxBones = 32;   // R/articulation.hpp:10
@@ -45,6 +47,7 @@ struct SkinView {
   const uint32_t* cell_mask; // [(rz-1)(ry-1)(rx-1)]
   const uint32_t* cell_off;  // offset into cell_vals in units of 8 doubles
   const double* cell_vals;
+  const uint2* cell_mo;      // (cell_mask, cell_off) pairs: one load per eval
 };
 
 // PoseContext (R/articulation.hpp:17-42) + world->normalized rigid (R/model.hpp:85-98).

@@ -85,8 +85,9 @@ __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __res
     wt[k] = dmul(dmul(wx, wy), wz);
   }
   const int cell = (c[2] * (S.ry - 1) + c[1]) * (S.rx - 1) + c[0];
-  const uint32_t mask = __ldg(S.cell_mask + cell);
-  const double* vals = S.cell_vals + static_cast<size_t>(__ldg(S.cell_off + cell)) * 8;
+  const uint2 mo = __ldg(S.cell_mo + cell);
+  const uint32_t mask = mo.x;
+  const double* vals = S.cell_vals + static_cast<size_t>(mo.y) * 8;
   // pass 1: raw interpolated weights per union bone, and their sum (bone order); two
   // bones per trip so 8 independent 16-byte loads are in flight before the math
   double sum = 0.0;

@@ -169,6 +169,13 @@ void build_skinning_grid_dev(ModelImpl& m, double blend_factor) {
   ARFX_CUDA(cudaGetLastError());
 }
 
+__global__ void cell_pack_kernel(const uint32_t* __restrict__ mask, const uint32_t* __restrict__ off, int64_t nc,
+                                 uint2* __restrict__ mo) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nc;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    mo[i] = make_uint2(mask[i], off[i]);
+}
+
 void build_cell_table(ModelImpl& m) {
   const int rx = m.skin_res[0], ry = m.skin_res[1], rz = m.skin_res[2];
   const int nb = static_cast<int>(m.bones.size());
@@ -198,6 +205,11 @@ void build_cell_table(ModelImpl& m) {
   cell_fill_kernel<<<blocks_for(nc, 128), 128, 0, m.stream>>>(m.skin.ptr, rx, ry, rz, nb,
                                                               m.cell_mask.ptr, m.cell_off.ptr,
                                                               m.cell_vals.ptr);
+  ARFX_CUDA(cudaGetLastError());
+  // (union mask, value offset) pairs: one 8-byte load per skinning eval instead of two
+  // dependent ones
+  m.cell_mo.alloc(static_cast<size_t>(nc));
+  cell_pack_kernel<<<blocks_for(nc, 128), 128, 0, m.stream>>>(m.cell_mask.ptr, m.cell_off.ptr, nc, m.cell_mo.ptr);
   ARFX_CUDA(cudaGetLastError());
   ARFX_CUDA(cudaStreamSynchronize(m.stream));
 }

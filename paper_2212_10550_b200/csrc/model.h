@@ -149,6 +149,7 @@ struct ModelImpl {
   DevBuf<float> grid_params, mlp_params, grid_grad, mlp_grad;
   DevBuf<double> skin;
   DevBuf<uint32_t> cell_mask, cell_off;
+  DevBuf<uint2> cell_mo;  // (cell_mask, cell_off) interleaved for the Newton kernel
   DevBuf<double> cell_vals;
   int max_union = 1;  // widest per-cell bone union (sizes the Newton kernel's scratch)
   FieldView fv{};
