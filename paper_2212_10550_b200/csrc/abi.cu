@@ -1920,6 +1920,7 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
       ARFX_CUDA(cudaEventRecord(m.ev_fork, s));
       ARFX_CUDA(cudaStreamWaitEvent(m.side, m.ev_fork, 0));
       density_forward(m, ph->impl, occ->impl, n_points, dseed, dstep, m.side);
+      density_flags(m, n_points, dl.w_density, d_loss2, m.side);
       ARFX_CUDA(cudaEventRecord(m.ev_join, m.side));
     }
     if (n_rays > 0) {
@@ -1938,7 +1939,7 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
     if (dens) {
       ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_join, 0));
       WorkspaceScope side(m, m.ws_side);
-      density_backward(m, n_points, dl.w_density, d_loss2, s);
+      density_backward_field(m, n_points, s);
     }
   });
 }

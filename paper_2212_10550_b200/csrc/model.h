@@ -261,6 +261,8 @@ void ensure_dyn_smem(const void* kernel, size_t bytes);
 void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_t seed, uint64_t step,
                      cudaStream_t s);
 void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s);
+void density_flags(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s);
+void density_backward_field(ModelImpl& m, long long n, cudaStream_t s);
 // optim.cu: Adam over the flat parameter vector
 struct AdamCfg {
   double lr_grid, lr_mlp, beta1, beta2, eps;

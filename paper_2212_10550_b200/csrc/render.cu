@@ -1214,7 +1214,7 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
   A.has_occ = occ != nullptr;
   if (occ) {
     A.occ = occ->view();
-    A.occ_box = launch_occ_bbox(w, A.occ, s);
+    // (no occupied-box range here: random training rays gain nothing from it)
   }
   A.N = N;
   A.stratified = stratified;
@@ -1537,16 +1537,16 @@ __global__ void density_points_kernel(OccView g, long long n, uint64_t seed, uin
 
 // one block, fixed order: out2 = (mean sigma over empty points with a root... / n_empty, n_empty),
 // scale = w / n_empty for the flag pass
-__global__ void __launch_bounds__(256) density_reduce_kernel(long long n, const uint8_t* __restrict__ empty,
+__global__ void __launch_bounds__(1024) density_reduce_kernel(long long n, const uint8_t* __restrict__ empty,
                                                              const uint8_t* __restrict__ snroot,
                                                              const int32_t* __restrict__ sbase,
                                                              const float4* __restrict__ pres, double w,
                                                              double* __restrict__ out2, float* __restrict__ scale) {
-  __shared__ double ss[256];
-  __shared__ unsigned long long sc[256];
+  __shared__ double ss[1024];
+  __shared__ unsigned long long sc[1024];
   double a = 0.0;
   unsigned long long c = 0;
-  for (long long i = threadIdx.x; i < n; i += 256) {
+  for (long long i = threadIdx.x; i < n; i += 1024) {
     if (!empty[i]) continue;
     ++c;
     float4 v;
@@ -1555,7 +1555,7 @@ __global__ void __launch_bounds__(256) density_reduce_kernel(long long n, const 
   ss[threadIdx.x] = a;
   sc[threadIdx.x] = c;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
+  for (int o = 512; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
       ss[threadIdx.x] += ss[threadIdx.x + o];
       sc[threadIdx.x] += sc[threadIdx.x + o];
@@ -1610,21 +1610,32 @@ void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_
   launch_field_pool(m, s, n, false, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
 }
 
-// Backward half: loss reduction and gradient flags, then K8 into the model's gradients.
-void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s) {
+// Backward half, part 1: loss reduction and gradient flags (reads only the density
+// forward's workspace; may run on the forward's stream).
+void density_flags(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s) {
   Workspace& w = m.ws();
   w.ensure_train();
   w.dens_scale.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
-  density_reduce_kernel<<<1, 256, 0, s>>>(n, w.dens_empty.ptr, w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w_density,
-                                          d_out2, w.dens_scale.ptr);
+  density_reduce_kernel<<<1, 1024, 0, s>>>(n, w.dens_empty.ptr, w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w_density,
+                                           d_out2, w.dens_scale.ptr);
   density_flag_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.dens_empty.ptr, w.snroot.ptr, w.sbase.ptr,
                                                           w.pres.ptr, w.dens_scale.ptr, w.pgs.ptr, w.pgc.ptr,
                                                           w.pflag.ptr);
   ARFX_CUDA(cudaGetLastError());
+}
+
+// Part 2: K8 into the model's gradients (ordered after every other gradient writer).
+void density_backward_field(ModelImpl& m, long long n, cudaStream_t s) {
+  Workspace& w = m.ws();
   const BwdOwners own{n, nullptr, nullptr, false};  // owner = density point = target
   field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr, w.pgc.ptr,
                       s, &own, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
+}
+
+void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s) {
+  density_flags(m, n, w_density, d_out2, s);
+  density_backward_field(m, n, s);
 }
 
 }  // namespace arfx
