@@ -514,8 +514,12 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
 }
 
 template <class Src>
-__global__ void src_count_kernel(Src src, unsigned long long* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *out = static_cast<unsigned long long>(src.count());
+__global__ void src_count_kernel(Src src, unsigned long long* out, unsigned long long* out2 = nullptr,
+                                 unsigned long long v2 = 0) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    *out = static_cast<unsigned long long>(src.count());
+    if (out2) *out2 = v2;  // a second constant counter in the same launch
+  }
 }
 
 // n: the live element count on the device (grid sized for the capacity; blocks past n exit)
@@ -532,8 +536,11 @@ __global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __res
   if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
 }
 
+// overflow (optional): counted when the grand total exceeds cap
 __global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restrict__ sums, const unsigned long long* n_dev,
-                                                                unsigned long long* __restrict__ grand) {
+                                                                unsigned long long* __restrict__ grand,
+                                                                unsigned long long cap = 0,
+                                                                unsigned long long* overflow = nullptr) {
   __shared__ uint32_t ws[33];
   const long long nb = (static_cast<long long>(*n_dev) + kScanBlock - 1) / kScanBlock;
   uint32_t carry = 0;
@@ -545,7 +552,10 @@ __global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restr
     if (i < nb) sums[i] = ex + carry;
     carry += total;
   }
-  if (threadIdx.x == 0) *grand = carry;
+  if (threadIdx.x == 0) {
+    *grand = carry;
+    if (overflow && carry > cap) *overflow += 1;
+  }
 }
 
 __global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,

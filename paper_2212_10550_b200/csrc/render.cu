@@ -894,12 +894,6 @@ int persistent_grid(Kern kernel, int threads, size_t smem, long long n_hint) {
   return static_cast<int>(std::max(1LL, std::min(want, static_cast<long long>(sm_count()) * per_sm)));
 }
 
-__global__ void set_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
-
-__global__ void starts_overflow_kernel(const unsigned long long* total, unsigned long long cap,
-                                       unsigned long long* overflow) {
-  if (*total > cap) *overflow += 1;
-}
 
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long n, cudaStream_t s) {
@@ -942,17 +936,16 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
   ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
   m.prof.begin("prune", s);
-  src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5);
-  set_u64_kernel<<<1, 1, 0, s>>>(C + 8, static_cast<unsigned long long>(nkeys));
+  src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5, C + 8, static_cast<unsigned long long>(nkeys));
   start_mask_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
                                                                             stats);
   ARFX_CUDA(cudaGetLastError());
   // start slots: exclusive scan of the per-target start counts (C6 = total starts)
   const long long nb = (n + kScanBlock - 1) / kScanBlock;
   scan_blocks_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
-  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 5, C + 6);
+  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 5, C + 6, static_cast<unsigned long long>(cap),
+                                            C + 3);  // C3 += 1 when the starts exceed the slots
   scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
-  starts_overflow_kernel<<<1, 1, 0, s>>>(C + 6, static_cast<unsigned long long>(cap), C + 3);
   // counting sort of the starts by (bone, skinning cell of x0)
   start_key_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(
       m.sv, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
