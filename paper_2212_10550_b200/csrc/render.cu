@@ -777,30 +777,26 @@ __global__ void occ_values_kernel(long long n, const uint8_t* __restrict__ snroo
   }
 }
 
-__global__ void occ_threshold_kernel(long long n, const float* __restrict__ values, float thr,
-                                     uint8_t* __restrict__ mask) {
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    mask[i] = values[i] >= thr ? 1 : 0;
-}
-
-// one separable pass of dilated_mask  R/occupancy.hpp:101-119
-__global__ void occ_dilate_kernel(int rx, int ry, int rz, int axis, int r, const uint8_t* __restrict__ src,
-                                  uint8_t* __restrict__ dst) {
+// rebuild_mask + dilated_mask (R/occupancy.hpp:87-91, :101-125) in one pass: a cell is
+// set iff any cell of its clipped (2r+1)^3 box has values >= thr -- the separable x, y, z
+// box dilation of the thresholded mask, evaluated directly (warps walk x-rows, so the
+// neighbouring values come from L1)
+__global__ void __launch_bounds__(256) occ_rebuild_kernel(int rx, int ry, int rz, int r, const float* __restrict__ values,
+                                                          float thr, uint8_t* __restrict__ mask) {
   const long long n = static_cast<long long>(rx) * ry * rz;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int idx3[3] = {static_cast<int>(i % rx), static_cast<int>((i / rx) % ry),
-                         static_cast<int>(i / (static_cast<long long>(rx) * ry))};
-    const int nn[3] = {rx, ry, rz};
-    const long long stride[3] = {1, rx, static_cast<long long>(rx) * ry};
-    uint8_t v = 0;
-    for (int d = -r; d <= r && !v; ++d) {
-      const int j = idx3[axis] + d;
-      if (j < 0 || j >= nn[axis]) continue;
-      v = src[i + static_cast<long long>(d) * stride[axis]];
-    }
-    dst[i] = v;
+    const int x = static_cast<int>(i % rx), y = static_cast<int>((i / rx) % ry),
+              z = static_cast<int>(i / (static_cast<long long>(rx) * ry));
+    const int x0 = max(x - r, 0), x1 = min(x + r, rx - 1), y0 = max(y - r, 0), y1 = min(y + r, ry - 1),
+              z0 = max(z - r, 0), z1 = min(z + r, rz - 1);
+    bool v = false;
+    for (int zz = z0; zz <= z1 && !v; ++zz)
+      for (int yy = y0; yy <= y1 && !v; ++yy) {
+        const float* row = values + (static_cast<long long>(zz) * ry + yy) * rx;
+        for (int xx = x0; xx <= x1; ++xx) v = v || (__ldg(row + xx) >= thr);
+      }
+    mask[i] = v ? 1 : 0;
   }
 }
 
@@ -1279,17 +1275,9 @@ void occ_query_batch(OccImpl& g, const double* d_pts, int64_t n, uint8_t* d_out,
 
 void occ_rebuild(OccImpl& g, cudaStream_t s) {
   const long long n = static_cast<long long>(g.res) * g.res * g.res;
-  occ_threshold_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, g.values.ptr, static_cast<float>(g.threshold),
-                                                          g.mask.ptr);
+  occ_rebuild_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, std::max(g.dilation, 0), g.values.ptr,
+                                                        static_cast<float>(g.threshold), g.mask.ptr);
   ARFX_CUDA(cudaGetLastError());
-  if (g.dilation > 0) {
-    g.tmp.ensure(static_cast<size_t>(n));
-    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 0, g.dilation, g.mask.ptr, g.tmp.ptr);
-    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 1, g.dilation, g.tmp.ptr, g.mask.ptr);
-    occ_dilate_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(g.res, g.res, g.res, 2, g.dilation, g.mask.ptr, g.tmp.ptr);
-    ARFX_CUDA(cudaMemcpyAsync(g.mask.ptr, g.tmp.ptr, static_cast<size_t>(n), cudaMemcpyDeviceToDevice, s));
-    ARFX_CUDA(cudaGetLastError());
-  }
 }
 
 static void occ_source_common(OccImpl& g, double lo[3], double cs[3]) {
