@@ -202,7 +202,7 @@ struct OccImpl {
   double threshold = 0.0;
   int dilation = 1;
   DevBuf<float> values;
-  DevBuf<uint8_t> mask, tmp;
+  DevBuf<uint8_t> mask;
   OccView view() const;
 };
 
