@@ -729,22 +729,39 @@ __global__ void composite_kernel(CompositeArgs A) {
     const int first = A.ray_first[pix], cnt = A.ray_count[pix];
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, acc = 0.0;
     bool done = A.eps > 0 && T <= A.eps;
-    for (int j = 0; j < cnt; ++j) {
-      const long long s = first + j;
-      float4 v;
-      const int sel = select_root(A.snroot, A.sbase, A.pres, s, v);
-      A.ssel[s] = static_cast<int8_t>(sel);
-      if (done || sel < 0) continue;
-      const double sigma = static_cast<double>(v.x);
-      if (sigma <= 0.0) continue;
-      const double alpha = -expm1(-dmul(sigma, A.sdelta[s]));
-      const double w = dmul(alpha, T);
-      cr = dadd(cr, dmul(static_cast<double>(v.y), w));
-      cg = dadd(cg, dmul(static_cast<double>(v.z), w));
-      cb = dadd(cb, dmul(static_cast<double>(v.w), w));
-      acc = dadd(acc, w);
-      T = dmul(T, dsub(1.0, alpha));
-      if (A.eps > 0 && T <= A.eps) done = true;
+    // 4 samples at a time: their root selections (dependent snroot -> sbase -> pres loads)
+    // and deltas are independent of the compositing chain, so they are fetched together
+    // first; the chain then runs over them in order, exactly as the per-sample loop
+    for (int j0 = 0; j0 < cnt; j0 += 4) {
+      float4 vv[4];
+      int ss[4];
+      double dd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ss[u] = -1;
+        dd[u] = 0.0;
+        vv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j0 + u < cnt) {
+          const long long s = first + j0 + u;
+          ss[u] = select_root(A.snroot, A.sbase, A.pres, s, vv[u]);
+          A.ssel[s] = static_cast<int8_t>(ss[u]);
+          if (!done && ss[u] >= 0) dd[u] = A.sdelta[s];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u >= cnt || done || ss[u] < 0) continue;
+        const double sigma = static_cast<double>(vv[u].x);
+        if (sigma <= 0.0) continue;
+        const double alpha = -expm1(-dmul(sigma, dd[u]));
+        const double w = dmul(alpha, T);
+        cr = dadd(cr, dmul(static_cast<double>(vv[u].y), w));
+        cg = dadd(cg, dmul(static_cast<double>(vv[u].z), w));
+        cb = dadd(cb, dmul(static_cast<double>(vv[u].w), w));
+        acc = dadd(acc, w);
+        T = dmul(T, dsub(1.0, alpha));
+        if (A.eps > 0 && T <= A.eps) done = true;
+      }
     }
     A.rgb[3 * pix + 0] = static_cast<float>(cr);
     A.rgb[3 * pix + 1] = static_cast<float>(cg);
