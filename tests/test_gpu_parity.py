@@ -446,3 +446,45 @@ def test_async_host_render_pipeline_matches_sync(gpu):
     for r, o, c in zip(ref, outs, cnts):
         assert c[3] == 0 and c[0] > 0
         assert np.array_equal(r.rgb, o.rgb) and np.array_equal(r.alpha, o.alpha)
+
+
+def test_randomized_poses_bit_exact(models, ref):
+    """Differential sweep over random poses (seeded hypothesis: bend up to 1 rad, any yaw,
+    body points with 0 / 2 / 15 cm jitter, skinning-lattice nodes, far-outside points):
+    skinning weights, all roots + residuals and posed-query roots / has_root bit-exact vs
+    the reference on the smpl24 config-1 avatar."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+    sk, dm, rm = models
+    lo, hi = np.array(rm.canon_lo[:]), np.array(rm.canon_hi[:])
+    nlo, nhi = np.array(rm.norm_lo[:]), np.array(rm.norm_hi[:])
+
+    @hyp.settings(max_examples=8, deadline=None, derandomize=True)
+    @hyp.given(seed=st.integers(0, 2**31 - 1), angle=st.floats(0.0, 1.0), yaw=st.floats(-3.1, 3.1),
+               jitter=st.sampled_from([0.0, 0.02, 0.15]))
+    def check(seed, angle, yaw, jitter):
+        rng = np.random.default_rng(seed)
+        pose = fx.random_pose(sk, seed % 100000, max_angle=angle, yaw=yaw)
+        T = pose.bone_transforms
+        body = []
+        for i, b in enumerate(sk.bones):
+            a, e = fx._apply(T[i], b.head), fx._apply(T[i], b.tail)
+            for u in rng.uniform(0, 1, 12):
+                body.append([a[k] + (e[k] - a[k]) * u + rng.uniform(-jitter, jitter) for k in range(3)])
+        nodes = lo + (hi - lo) * (rng.integers(0, 32, (64, 3)) / 31.0)
+        far = lo + (hi - lo) * rng.uniform(-0.5, 1.5, (64, 3))
+        pts = np.concatenate([np.array(body), nodes, far])
+        assert np.array_equal(dm.skinning_weights(pts).view(np.uint64), ref.skinning_weights(rm, pts).view(np.uint64))
+        cnt, roots, res = dm.inverse_lbs(pose, pts, arf.rigid(), 3.0)
+        rcnt, rroots, rres = ref.inverse_lbs(rm, T, arf.rigid(), 3.0, pts)
+        assert np.array_equal(cnt, rcnt)
+        for i in range(len(pts)):
+            k = cnt[i]
+            assert np.array_equal(roots[i, :k].view(np.uint64), rroots[i, :k].view(np.uint64))
+            assert np.array_equal(res[i, :k].view(np.uint64), rres[i, :k].view(np.uint64))
+        q = nlo + (nhi - nlo) * rng.uniform(0.2, 0.8, (2000, 3))
+        d, c, x, h = dm.posed_query(pose, q)
+        rd, rc, rx, rh = ref.posed_query(rm, T, pose.global_transform, q)
+        assert np.array_equal(h, rh) and np.array_equal(x.view(np.uint64), rx.view(np.uint64))
+
+    check()

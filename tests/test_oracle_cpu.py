@@ -329,3 +329,46 @@ def test_figure_render_oracle_vs_ref(oracle, ref, stratified):
     inter = np.logical_and(alpha > 0.5, mask > 0).sum()
     union = np.logical_or(alpha > 0.5, mask > 0).sum()
     assert inter / union > 0.9
+
+
+# ---------------------------------------------------------------- randomized differential
+
+def _lattice_points(lo, hi, res, rng, n):
+    """Points exactly on skinning-lattice nodes / cell faces (zero trilinear weights and
+    clamped cells: the reference's skip branches)."""
+    k = rng.integers(0, res, (n, 3)).astype(np.float64)
+    return lo + (hi - lo) * (k / (res - 1))
+
+
+def test_randomized_poses_match_reference(pair, oracle, ref):
+    """Differential sweep (hypothesis-style, seeded): random poses (bend up to 1 rad, random
+    yaw), points on the posed body with jitter, on lattice nodes and far outside the box --
+    skinning weights, hash encodings, all roots + residuals and posed queries bit-identical
+    between the oracle restatement and the reference."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+    sk, g, m, O, R = pair
+    lo, hi = np.array(O.canon_lo[:]), np.array(O.canon_hi[:])
+    nlo, nhi = np.array(O.norm_lo[:]), np.array(O.norm_hi[:])
+
+    @hyp.settings(max_examples=12, deadline=None, derandomize=True)
+    @hyp.given(seed=st.integers(0, 2**31 - 1), angle=st.floats(0.0, 1.0), yaw=st.floats(-3.1, 3.1),
+               jitter=st.sampled_from([0.0, 0.02, 0.15]))
+    def check(seed, angle, yaw, jitter):
+        rng = np.random.default_rng(seed)
+        pose = fx.random_pose(sk, seed % 100000, max_angle=angle, yaw=yaw)
+        pts = np.concatenate([_body_points(sk, pose, 4, jitter, seed % 1000),
+                              _lattice_points(lo, hi, 12, rng, 16),
+                              lo + (hi - lo) * rng.uniform(-0.5, 1.5, (16, 3))])
+        assert np.array_equal(bits(oracle.skinning_weights(O, pts)), bits(ref.skinning_weights(R, pts)))
+        inside = np.all((pts >= lo) & (pts <= hi), axis=1)
+        assert np.array_equal(bits(oracle.hash_encode(O, pts[inside])), bits(ref.hash_encode(R, pts[inside])))
+        for a, b in zip(oracle.inverse_lbs(O, pose.bone_transforms, arf.rigid(), 3.0, pts),
+                        ref.inverse_lbs(R, pose.bone_transforms, arf.rigid(), 3.0, pts)):
+            assert np.array_equal(np.ascontiguousarray(a).view(np.uint8), np.ascontiguousarray(b).view(np.uint8))
+        q = nlo + (nhi - nlo) * rng.uniform(0.2, 0.8, (64, 3))
+        for a, b in zip(oracle.posed_query(O, pose.bone_transforms, pose.global_transform, q),
+                        ref.posed_query(R, pose.bone_transforms, pose.global_transform, q)):
+            assert np.array_equal(np.ascontiguousarray(a).view(np.uint8), np.ascontiguousarray(b).view(np.uint8))
+
+    check()
