@@ -488,3 +488,35 @@ def test_randomized_poses_bit_exact(models, ref):
         assert np.array_equal(h, rh) and np.array_equal(x.view(np.uint64), rx.view(np.uint64))
 
     check()
+
+
+def test_randomized_cameras_march_parity(models, ref):
+    """Seeded hypothesis sweep over camera placement (orbit angle, elevation, distance down
+    to inside the normalized box), samples per ray (incl. non-multiples of 32) and
+    stratification: the posed-sample set (pixel, index) and deltas are bit-exact vs the
+    reference -- exercises the occupied-box sample range and grazing rays."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+    sk, dm, rm = models
+    pose = fx.random_pose(sk, 31)
+    cfg = arf.OccupancyConfig()
+    occ = arf.build_model_inference_grid(dm, pose, cfg)
+    rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, cfg)
+    centre = np.array([0.0, 0.9, 0.0])
+
+    @hyp.settings(max_examples=6, deadline=None, derandomize=True)
+    @hyp.given(theta=st.floats(0.0, 6.28), elev=st.floats(-1.2, 1.2), dist=st.floats(0.3, 4.0),
+               N=st.sampled_from([1, 33, 100, 128, 257]), strat=st.booleans())
+    def check(theta, elev, dist, N, strat):
+        eye = centre + dist * np.array([np.cos(elev) * np.sin(theta), np.sin(elev), -np.cos(elev) * np.cos(theta)])
+        cam = arf.Camera.look_at(eye, centre, np.array([0.0, 1.0, 0.0]), 60.0, 40, 36)
+        opt = arf.RenderOptions(samples_per_ray=N, stratified=strat, seed=5, frame_id=2)
+        arf.render_model(dm, pose, cam, occ, opt)
+        tr = arf.render_trace(dm)
+        _, _, _, rtr = ref.render_trace(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt)
+        assert len(tr.ray) == rtr["n_samples"]
+        order = np.lexsort((tr.index, tr.ray))
+        assert np.array_equal(tr.ray[order], rtr["s_ray"]) and np.array_equal(tr.index[order], rtr["s_index"])
+        assert np.array_equal(tr.delta[order].view(np.uint64), rtr["s_delta"].view(np.uint64))
+
+    check()
