@@ -1019,7 +1019,14 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     // of them runs, by the count (teams below kTeamMax queries, tiles above)
     constexpr long long kTeamMax = kTeamMaxQueries;
     m.prof.begin("field", s);
-    field_team_kernel<<<static_cast<unsigned>(sm_count() * 8), kFtTeam * kFtTeams, 0, s>>>(
+    // persistent: exactly the resident blocks (static smem allows ~6 per SM), so no block
+    // waits for a second wave with a full share of the work
+    static int team_per_sm = 0;
+    if (!team_per_sm) {
+      ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&team_per_sm, field_team_kernel, kFtTeam * kFtTeams, 0));
+      team_per_sm = std::max(team_per_sm, 1);
+    }
+    field_team_kernel<<<static_cast<unsigned>(sm_count() * team_per_sm), kFtTeam * kFtTeams, 0, s>>>(
         m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr, m.ws().pres.ptr, m.ws().counters.ptr + 2,
         static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax, act);
     kern<<<grid, kFieldTile, smem, s>>>(m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,

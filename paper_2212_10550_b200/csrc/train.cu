@@ -706,7 +706,9 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
-  field_bwd_team_kernel<<<static_cast<unsigned>(sms() * 4), kTeamThreads, team_smem, s>>>(
+  int bwd_per_sm = 0;  // persistent: exactly the resident blocks (one wave)
+  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bwd_per_sm, field_bwd_team_kernel, kTeamThreads, team_smem));
+  field_bwd_team_kernel<<<static_cast<unsigned>(sms() * std::max(bwd_per_sm, 1)), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr, act,
       d_n);
   ARFX_CUDA(cudaGetLastError());
