@@ -411,9 +411,8 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
     m.prof.end(s);
   }
   m.prof.begin("encode_tc", s);
-  (half ? encode_tiles_kernel<true> : encode_tiles_kernel<false>)<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n_hint + 255) / 256,
-                                                                                       static_cast<long long>(sms) * 16))),
-                        kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,
+  auto enc = half ? encode_tiles_kernel<true> : encode_tiles_kernel<false>;
+  enc<<<resident_grid(enc, kEncThreads, 0, n_hint), kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,
                                      m.ws().counters.ptr + 2, static_cast<long long>(m.ws().cap_pool), m.ws().tc_tiles.ptr,
                                      m.stats_on ? m.stats.ptr : nullptr);
   ARFX_CUDA(cudaGetLastError());

@@ -327,4 +327,18 @@ void figure_render(const FigureView& F, const HostCamera& cam, const double* w2n
                    const int32_t* d_px, const int32_t* d_py, float* d_rgb, float* d_alpha, uint8_t* d_mask,
                    cudaStream_t s);
 
+
+// Grid of a grid-stride kernel: at most one wave of resident blocks (occupancy API), so
+// the static partition of the items never leaves a fractional last wave running alone.
+template <class Kern>
+int resident_grid(Kern kernel, int threads, size_t smem, long long n_items) {
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  const long long want = (n_items + threads - 1) / threads;
+  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
 }  // namespace arfx

@@ -101,7 +101,7 @@ void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long blocks = std::min<long long>((e4 - b4 + 255) / 256, static_cast<long long>(sms) * 8);
+  const long long blocks = resident_grid(adam_kernel<false>, 256, 0, e4 - b4);  // one wave
   m.prof.begin("adam", s);
   if (m.acc_pending && !(begin == 0 && end >= static_cast<long long>(m.grid_acc.n)))
     flush_grad_acc(m, s);  // a shard cannot consume the whole accumulator

@@ -911,7 +911,7 @@ int persistent_grid(Kern kernel, int threads, size_t smem, long long n_hint) {
 template <class Src>
 void launch_finalize(ModelImpl& m, const Src& src, const PoolSink& K, long long n, cudaStream_t s) {
   Workspace& w = m.ws();
-  finalize_pool_kernel<Src><<<grid_for(n, 256, 8), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
+  finalize_pool_kernel<Src><<<resident_grid(finalize_pool_kernel<Src>, 256, 0, n), 256, 0, s>>>(src, w.smask.ptr, w.scount.ptr, w.res4.ptr,
                                                                 m.inv.dedup_radius, K,
                                                                 static_cast<long long>(w.cap_starts));
   ARFX_CUDA(cudaGetLastError());
@@ -950,7 +950,8 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
   m.prof.begin("prune", s);
   src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5, C + 8, static_cast<unsigned long long>(nkeys));
-  start_mask_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
+  start_mask_kernel<Src, single><<<resident_grid(start_mask_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
+                                   s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
                                                                             stats);
   ARFX_CUDA(cudaGetLastError());
   // start slots: exclusive scan of the per-target start counts (C6 = total starts)
@@ -960,7 +961,8 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
                                             C + 3);  // C3 += 1 when the starts exceed the slots
   scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
   // counting sort of the starts by (bone, skinning cell of x0)
-  start_key_kernel<Src, single><<<grid_for(n, 256, 8), 256, pose_smem, s>>>(
+  start_key_kernel<Src, single><<<resident_grid(start_key_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
+                                  s>>>(
       m.sv, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
   const long long nbk = (nkeys + kScanBlock - 1) / kScanBlock;
   scan_blocks_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
@@ -1195,7 +1197,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
                   w.snroot.ptr, w.sbase.ptr, w.pres.ptr, w.ssel.ptr, eps, d_rgb, d_alpha};
   if (n_rays > 0) {
     m.prof.begin("composite", s);
-    composite_kernel<<<grid_for(n_rays, 128, 16), 128, 0, s>>>(C);
+    composite_kernel<<<resident_grid(composite_kernel, 128, 0, n_rays), 128, 0, s>>>(C);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
   }

@@ -735,12 +735,12 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
       m.grid_acc.alloc(n_acc);
       ARFX_CUDA(cudaMemsetAsync(m.grid_acc.ptr, 0, n_acc * sizeof(long long), s));
     }
-    grid_scatter_kernel<true><<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(
+    grid_scatter_kernel<true><<<resident_grid(grid_scatter_kernel<true>, 256, 0, 1LL << 40), 256, 0, s>>>(
         m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr,
         m.grid_acc.ptr);
     m.acc_pending = true;
   } else {
-    grid_scatter_kernel<false><<<static_cast<unsigned>(sms() * 8), 256, 0, s>>>(
+    grid_scatter_kernel<false><<<resident_grid(grid_scatter_kernel<false>, 256, 0, 1LL << 40), 256, 0, s>>>(
         m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr, nullptr);
   }
   ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_aux_join, 0));
