@@ -15,6 +15,7 @@ python tools/ncu_summary.py /tmp/frame.ncu-rep gpurun_out/ncu_frame.json > /dev/
 python tools/ncu_table.py gpurun_out/ncu_frame_kernels.md /tmp/frame.ncu-rep || exit 6
 python tools/ncu_traffic.py gpurun_out/ncu_frame.json gpurun_out/ncu_traffic.json || exit 7
 python tools/prof_train.py 2 > /dev/null || exit 8
-ncu --set full --clock-control none -o /tmp/train python tools/prof_train.py 2 > gpurun_out/rp_ncu3.log 2>&1 || exit 9
+ncu --set full --clock-control none -k regex:"newton|field_team|field_bwd|grid_scatter|composite|adam|march|weights|finalize|owner|density" \
+  -c 40 -o /tmp/train python tools/prof_train.py 2 > gpurun_out/rp_ncu3.log 2>&1 || exit 9
 python tools/ncu_table.py gpurun_out/ncu_train_kernels.md /tmp/train.ncu-rep || exit 10
 echo done
