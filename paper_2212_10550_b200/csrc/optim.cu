@@ -98,9 +98,6 @@ void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, 
   k.mlp_off = static_cast<long long>(m.mlp_off);
   const long long b4 = begin / 4, e4 = end / 4;
   if (e4 <= b4) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long blocks = resident_grid(adam_kernel<false>, 256, 0, e4 - b4);  // one wave
   m.prof.begin("adam", s);
   if (m.acc_pending && !(begin == 0 && end >= static_cast<long long>(m.grid_acc.n)))
