@@ -384,6 +384,20 @@ int arfx_train_density_step_device(arfx_model m, arfx_pose pose, const arfx_came
                                    const int32_t* d_py, const float* d_gt_rgb, const float* d_gt_alpha,
                                    const arfx_loss_config* cfg, double* d_loss4, int64_t n_points,
                                    uint64_t seed, uint64_t step, double* d_loss2, void* stream);
+/* The same step split in two, for pipelining across steps: arfx_train_forward_device runs
+ * the march, deformer and field forward of n rays into train slot 0 or 1 (its field kernels
+ * wait on the parameter fence, nothing else reads parameters or gradients);
+ * arfx_train_backward_device then runs that slot's composite + fused losses + field
+ * backward (+ the L_density step when n_points > 0), accumulating into the gradients. The
+ * caller orders them (events): backward(slot) after forward(slot), and a slot's next
+ * forward after its previous backward. Capacities are reserved for the worst case. */
+int arfx_train_forward_device(arfx_model m, arfx_pose pose, const arfx_camera* cam, arfx_occ_grid occ,
+                              const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                              const int32_t* d_py, int slot, void* stream);
+int arfx_train_backward_device(arfx_model m, arfx_pose pose, arfx_occ_grid occ, const arfx_render_options* opt,
+                               int64_t n_rays, const int32_t* d_px, const int32_t* d_py, const float* d_gt_rgb,
+                               const float* d_gt_alpha, const arfx_loss_config* cfg, double* d_loss4, int slot,
+                               int64_t n_points, uint64_t seed, uint64_t step, double* d_loss2, void* stream);
 /* Adam over flat parameter indices [begin, end) (multiples of 4; end = -1: all), step >= 1,
  * gradients zeroed in the same pass. Asynchronous on stream. */
 int arfx_adam_step(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,

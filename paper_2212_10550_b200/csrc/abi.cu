@@ -1944,6 +1944,91 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
   });
 }
 
+// Split train step for software pipelining across steps (the trainer runs the forward of
+// step t+1 -- march, deformer, field -- while step t's backward runs): slot 0 / 1 selects
+// one of two train workspaces. The forward needs no gradients; its field kernels wait on
+// the parameter fence (arfx_model_set_param_fence). The backward = composite + fused losses
+// + field backward of that slot (+ the L_density step as in arfx_train_density_step_device).
+namespace {
+Workspace& train_slot(ModelImpl& m, int slot) { return slot ? m.ws_alt : m.ws_main; }
+}  // namespace
+
+int arfx_train_forward_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                              const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
+                              const int32_t* d_py, int slot, void* stream) {
+  return guard([&] {
+    const HostCamera hc = camera_of(cam);
+    validate_train(mh, ph, opt, hc);
+    require(slot == 0 || slot == 1, "train_forward: slot must be 0 or 1");
+    require(n_rays == 0 || (d_px && d_py), "train_forward: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const long long posed_max = n_rays * std::max(opt->samples_per_ray, 1);
+    require(posed_max <= (1LL << 22), "train_forward: at most 2^22 ray samples per step");
+    if (n_rays <= 0) return;
+    WorkspaceScope scope(m, train_slot(m, slot));
+    m.ws().reserve_worst(static_cast<size_t>(posed_max), static_cast<size_t>(m.sv.nb));
+    train_forward(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0, opt->seed,
+                  opt->frame_id, n_rays, d_px, d_py, stream_of(m, stream));
+  });
+}
+
+int arfx_train_backward_device(arfx_model mh, arfx_pose ph, arfx_occ_grid occ, const arfx_render_options* opt,
+                               int64_t n_rays, const int32_t* d_px, const int32_t* d_py, const float* d_gt_rgb,
+                               const float* d_gt_alpha, const arfx_loss_config* cfg, double* d_loss4, int slot,
+                               int64_t n_points, uint64_t dseed, uint64_t dstep, double* d_loss2, void* stream) {
+  return guard([&] {
+    require(mh && ph && opt, "train_backward: null argument");
+    require(slot == 0 || slot == 1, "train_backward: slot must be 0 or 1");
+    require(n_rays == 0 || (d_px && d_py && d_gt_rgb && d_gt_alpha && d_loss4), "train_backward: null argument");
+    require(n_points <= 0 || (occ && d_loss2), "density_step: null argument");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    const LossTargets dl = loss_targets(cfg, nullptr, nullptr, nullptr);
+    ensure_grad_store(m, s);
+    const bool dens = n_points > 0;
+    if (dens) {
+      require(n_points <= (1LL << 22), "density_step: at most 2^22 points per call");
+      if (!m.side) {
+        ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+        ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
+        ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
+      }
+      WorkspaceScope side(m, m.ws_side);
+      m.ws().reserve_worst(static_cast<size_t>(n_points), static_cast<size_t>(m.sv.nb));
+      ARFX_CUDA(cudaEventRecord(m.ev_fork, s));
+      ARFX_CUDA(cudaStreamWaitEvent(m.side, m.ev_fork, 0));
+      density_forward(m, ph->impl, occ->impl, n_points, dseed, dstep, m.side);
+      density_flags(m, n_points, dl.w_density, d_loss2, m.side);
+      ARFX_CUDA(cudaEventRecord(m.ev_join, m.side));
+    }
+    if (n_rays > 0) {
+      WorkspaceScope scope(m, train_slot(m, slot));
+      Workspace& w = m.ws();
+      w.ensure_train();
+      w.train_terms.ensure(static_cast<size_t>(3 * n_rays));
+      w.train_rgb.ensure(static_cast<size_t>(3 * n_rays));
+      w.train_alpha.ensure(static_cast<size_t>(n_rays));
+      LossTargets lt = loss_targets(cfg, d_gt_rgb, d_gt_alpha, w.train_terms.ptr);
+      lt.px = d_px;
+      lt.py = d_py;
+      ARFX_CUDA(cudaMemsetAsync(w.pflag.ptr, 0, w.cap_pool, s));
+      train_composite(m, n_rays, opt->samples_per_ray, opt->epsilon_terminate, nullptr, nullptr, w.train_rgb.ptr,
+                      w.train_alpha.ptr, s, &lt);
+      const BwdOwners own{n_rays, w.ray_first.ptr, w.ray_count.ptr, false};
+      field_backward_pool(m, w.counters.ptr + 2, static_cast<long long>(w.cap_pool), w.pflag.ptr, w.pgs.ptr,
+                          w.pgc.ptr, s, &own, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
+      loss_reduce(w.train_terms.ptr, n_rays, lt, d_loss4, s);
+    }
+    if (dens) {
+      ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_join, 0));
+      WorkspaceScope side(m, m.ws_side);
+      density_backward_field(m, n_points, s);
+    }
+  });
+}
+
 int arfx_adam_step(arfx_model mh, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
                    void* stream) {
   return guard([&] {

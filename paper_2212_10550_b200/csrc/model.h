@@ -156,7 +156,7 @@ struct ModelImpl {
   SkinView sv{};
   // Workspaces: ws() is the one the launch helpers use; a second one lets the L_density
   // forward run on the side stream concurrently with the train step (WorkspaceScope).
-  Workspace ws_main, ws_side;
+  Workspace ws_main, ws_side, ws_alt;  // ws_alt: second train slot (pipelined forward/backward)
   Workspace* ws_cur = &ws_main;
   Workspace& ws() { return *ws_cur; }
   cudaStream_t side = nullptr;  // lazily created non-blocking stream

@@ -162,22 +162,96 @@ class Trainer:
         self.adam_stream = torch.cuda.Stream() if world == 1 else None
         self.ev_params = torch.cuda.Event()
         self._fence_set = False
+        # single rank: step t+1's forward (march, deformer, field) is enqueued on fstream into
+        # the other train slot right after step t's backward, so the two overlap on the GPU
+        self.pipelined = world == 1
+        self.fstream = torch.cuda.Stream()
+        self.pxs = [torch.zeros(self.n_local, dtype=torch.int32, device="cuda") for _ in range(2)]
+        self.pys = [torch.zeros(self.n_local, dtype=torch.int32, device="cuda") for _ in range(2)]
+        self.ev_fwd = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ev_bwd = [torch.cuda.Event(), torch.cuda.Event()]
+        self._pending = [None, None]  # per slot: (step, frame) of the enqueued forward
         self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
         self._checked = 0     # steps whose loss has been checked for finiteness
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
         self._h_pix = [torch.zeros((2, self.n_local), dtype=torch.int32).pin_memory() for _ in range(2)]
         self._h_evt = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def _opt(self, frame: int) -> arf.RenderOptions:
+    def _opt(self, frame: int, step: int | None = None) -> arf.RenderOptions:
+        st = self.step_id if step is None else step
         return arf.RenderOptions(samples_per_ray=self.cfg.samples_per_ray, stratified=True, seed=self.cfg.seed,
-                                 frame_id=self.step_id * 1024 + frame)
+                                 frame_id=st * 1024 + frame)
 
     def step(self):
         """One SPEC train step, enqueued without host synchronisation (except the occupancy
         update every k steps, which is also where the loss is checked for finiteness).
         Returns the step's loss as a device tensor (L_rgb, L_alpha, L_hard, L_density, total)."""
         with self.torch.cuda.stream(self.stream):
+            if self.pipelined and self.fused_density:
+                return self._step_pipelined()
             return self._step()
+
+    def _forward(self, step: int):
+        """Enqueue step `step`'s forward on fstream into train slot step & 1."""
+        torch = self.torch
+        cfg, W = self.cfg, self.camera.width
+        k = step & 1
+        fs = self.fstream
+        fs.wait_event(self.ev_bwd[k])  # the previous backward that used this slot has run
+        f, px, py = ray_batch(cfg.seed, step, self.rank, self.n_local, len(self.poses), W, self.camera.height)
+        self._h_evt[k].synchronize()
+        hp = self._h_pix[k]
+        hp[0].numpy()[:] = px
+        hp[1].numpy()[:] = py
+        with torch.cuda.stream(fs):
+            self.pxs[k].copy_(hp[0], non_blocking=True)
+            self.pys[k].copy_(hp[1], non_blocking=True)
+        self._h_evt[k].record(fs)
+        L.call("arfx_train_forward_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
+               self.grid._h, C.byref(self._opt(f, step).to_c()), self.n_local, C.c_void_p(self.pxs[k].data_ptr()),
+               C.c_void_p(self.pys[k].data_ptr()), k, C.c_void_p(fs.cuda_stream))
+        self.ev_fwd[k].record(fs)
+        self._pending[k] = (step, f)
+
+    def _step_pipelined(self):
+        torch = self.torch
+        cfg, W = self.cfg, self.camera.width
+        t = self.step_id
+        k = t & 1
+        if self._pending[k] is None or self._pending[k][0] != t:
+            self._forward(t)  # first step (or after restore / an occupancy update)
+        f = self._pending[k][1]
+        self._pending[k] = None
+        self.stream.wait_event(self.ev_fwd[k])
+        dens = cfg.loss.w_density > 0 and cfg.density_points > 0
+        lc = cfg.loss.to_c((W, self.camera.height))
+        sp = C.c_void_p(self.stream.cuda_stream)
+        L.call("arfx_train_backward_device", self.model._h, self.views[f]._h, self.grid._h,
+               C.byref(self._opt(f, t).to_c()), self.n_local, C.c_void_p(self.pxs[k].data_ptr()),
+               C.c_void_p(self.pys[k].data_ptr()), C.c_void_p(self.gt_rgb[f].data_ptr()),
+               C.c_void_p(self.gt_alpha[f].data_ptr()), C.byref(lc), C.c_void_p(self.loss4.data_ptr()), k,
+               cfg.density_points if dens else 0, (cfg.seed * 4 + self.rank) & (2**64 - 1), t,
+               C.c_void_p(self.loss_d.data_ptr()), sp)
+        self.ev_bwd[k].record(self.stream)
+        if not dens:
+            self.loss_d.zero_()
+        t1 = t + 1
+        self.adam_stream.wait_stream(self.stream)
+        self.model.adam_step(cfg.adam, t1, 0, self.n_flat, C.c_void_p(self.adam_stream.cuda_stream))
+        self.ev_params.record(self.adam_stream)
+        if not self._fence_set:
+            self.model.set_param_fence(self.ev_params.cuda_event)
+            self._fence_set = True
+        loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
+                            self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
+        self._hist.append(loss)
+        self.step_id = t1
+        if cfg.occupancy_interval > 0 and t1 % cfg.occupancy_interval == 0:
+            self._sync()
+            arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t1)
+            self._check()
+        self._forward(t1)  # overlaps this step's backward (its field waits for this Adam)
+        return loss
 
     def _step(self):
         torch = self.torch
@@ -242,6 +316,7 @@ class Trainer:
 
     def _sync(self):
         self.stream.synchronize()
+        self.fstream.synchronize()
         if self.adam_stream is not None:
             self.adam_stream.synchronize()
 
@@ -293,6 +368,7 @@ class Trainer:
         m2.close()
         self.grid = occ
         self.step_id = int(step)
+        self._pending = [None, None]  # forwards enqueued for the old state are discarded
 
     def train(self, iterations: int | None = None):
         for _ in range(iterations or self.cfg.iterations):
