@@ -674,7 +674,9 @@ def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
     cfg = TrainConfig(iterations=steps, rays_per_batch=4096 * world, samples_per_ray=128, occupancy_interval=16,
                       seed=9, adam=arf.AdamConfig(total_steps=1000))
     tr = Trainer(model, fx.figure_for(sk), poses, cam, cfg, rank, world, group)
-    for _ in range(3):
+    # warm-up through the first occupancy update too (its one-time workspace sizing is not
+    # a per-step cost)
+    for _ in range(cfg.occupancy_interval + 3):
         tr.step()
     torch.cuda.synchronize()
     if world > 1:

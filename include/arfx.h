@@ -391,6 +391,10 @@ int arfx_train_density_step_device(arfx_model m, arfx_pose pose, const arfx_came
  * backward (+ the L_density step when n_points > 0), accumulating into the gradients. The
  * caller orders them (events): backward(slot) after forward(slot), and a slot's next
  * forward after its previous backward. Capacities are reserved for the worst case. */
+/* The trainer's ray batch of one step on the device: ray i's pixel from draws 1 + 2i, 2 + 2i
+ * of keyed_rng(seed, 0x7a11, step, rank) (draw 0, the frame index, is the caller's). */
+int arfx_train_rays_device(uint64_t seed, uint64_t step, uint64_t rank, int64_t n, int width, int height,
+                           int32_t* d_px, int32_t* d_py, void* stream);
 int arfx_train_forward_device(arfx_model m, arfx_pose pose, const arfx_camera* cam, arfx_occ_grid occ,
                               const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,
                               const int32_t* d_py, int slot, void* stream);

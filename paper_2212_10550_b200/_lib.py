@@ -179,6 +179,8 @@ _PROTOS = {
     "arfx_train_density_step_device": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions),
                                                  C.c_int64, P, P, P, P, C.POINTER(ArfxLossConfig), P, C.c_int64,
                                                  C.c_uint64, C.c_uint64, P, P]),
+    "arfx_train_rays_device": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int, C.c_int, P, P,
+                                         P]),
     "arfx_train_forward_device": (C.c_int, [H, H, C.POINTER(ArfxCamera), H, C.POINTER(ArfxRenderOptions), C.c_int64,
                                             P, P, C.c_int, P]),
     "arfx_train_backward_device": (C.c_int, [H, H, H, C.POINTER(ArfxRenderOptions), C.c_int64, P, P, P, P,

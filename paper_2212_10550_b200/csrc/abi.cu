@@ -936,8 +936,8 @@ int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses
     }
     OccImpl& g = occ_ref(gh);
     const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
-    DevBuf<float> saved;  // values are updated in place: keep a copy for overflow reruns
-    saved.alloc(n);
+    DevBuf<float>& saved = g.saved;  // values are updated in place: keep a copy for overflow reruns
+    saved.ensure(n);
     ARFX_CUDA(cudaMemcpyAsync(saved.ptr, g.values.ptr, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
     for (int attempt = 0; attempt < 3; ++attempt) {
       if (attempt)
@@ -1952,6 +1952,15 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
 namespace {
 Workspace& train_slot(ModelImpl& m, int slot) { return slot ? m.ws_alt : m.ws_main; }
 }  // namespace
+
+int arfx_train_rays_device(uint64_t seed, uint64_t step, uint64_t rank, int64_t n, int width, int height,
+                           int32_t* d_px, int32_t* d_py, void* stream) {
+  return guard([&] {
+    require(n <= 0 || (d_px && d_py), "train_rays: null argument");
+    require(width > 0 && height > 0, "train_rays: empty image");
+    launch_train_rays(seed, step, rank, n, width, height, d_px, d_py, static_cast<cudaStream_t>(stream));
+  });
+}
 
 int arfx_train_forward_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
                               const arfx_render_options* opt, int64_t n_rays, const int32_t* d_px,

@@ -392,9 +392,7 @@ bool field_tc_supported(const FieldView& F) {
 void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   const size_t smem = TcSmem::TOTAL + 1024;  // + alignment slack
   ensure_dyn_smem(reinterpret_cast<const void*>(field_tc_kernel), smem);
-  int sms = 148, dev = 0;
-  ARFX_CUDA(cudaGetDevice(&dev));
-  ARFX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int sms = device_sm_count();
   // persistent: one CTA per SM (it owns all 512 TMEM columns)
   const long long tiles = (n_hint + kTcTile * kGroups - 1) / (kTcTile * kGroups);
   const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));

@@ -150,6 +150,7 @@ struct ModelImpl {
   DevBuf<double> skin;
   DevBuf<uint32_t> cell_mask, cell_off;
   DevBuf<uint2> cell_mo;  // (cell_mask, cell_off) interleaved for the Newton kernel
+  DevBuf<PoseCtx> grid_ctxs;  // update_training_grid: the pose list on the device
   DevBuf<double> cell_vals;
   int max_union = 1;  // widest per-cell bone union (sizes the Newton kernel's scratch)
   FieldView fv{};
@@ -197,6 +198,7 @@ struct PoseImpl {
 
 struct OccImpl {
   int device = 0;
+  DevBuf<float> saved;  // update_training_grid: values before the update (overflow rerun)
   int res = 64;
   HostBox box{};
   double threshold = 0.0;
@@ -263,6 +265,8 @@ void density_forward(ModelImpl& m, PoseImpl& p, OccImpl& g, long long n, uint64_
 void density_backward(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s);
 void density_flags(ModelImpl& m, long long n, double w_density, double* d_out2, cudaStream_t s);
 void density_backward_field(ModelImpl& m, long long n, cudaStream_t s);
+void launch_train_rays(uint64_t seed, uint64_t step, uint64_t rank, long long n, int W, int H, int32_t* px, int32_t* py,
+                       cudaStream_t s);
 // optim.cu: Adam over the flat parameter vector
 struct AdamCfg {
   double lr_grid, lr_mlp, beta1, beta2, eps;
@@ -328,16 +332,18 @@ void figure_render(const FigureView& F, const HostCamera& cam, const double* w2n
                    cudaStream_t s);
 
 
-// Grid of a grid-stride kernel: at most one wave of resident blocks (occupancy API), so
-// the static partition of the items never leaves a fractional last wave running alone.
+// Resident blocks per SM of a kernel at a launch shape (cudaOccupancy..., cached per device:
+// the launch helpers run on every step, the occupancy calculation is host work).
+int blocks_per_sm(const void* kernel, int threads, size_t smem);
+int device_sm_count();
+
+// Grid of a grid-stride kernel: at most one wave of resident blocks, so the static partition
+// of the items never leaves a fractional last wave running alone.
 template <class Kern>
 int resident_grid(Kern kernel, int threads, size_t smem, long long n_items) {
-  int dev = 0, sms = 148, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), threads, smem);
   const long long want = (n_items + threads - 1) / threads;
-  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  const long long cap = static_cast<long long>(device_sm_count()) * per_sm;
   return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
 }
 

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <cstdio>
 
@@ -882,14 +883,7 @@ __global__ void skin_weights_kernel(SkinView S, const double* __restrict__ pts, 
 }
 
 int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  return device_sm_count();
 }
 
 int grid_for(long long n, int threads, int per_sm) {
@@ -900,9 +894,7 @@ int grid_for(long long n, int threads, int per_sm) {
 
 template <class Kern>
 int persistent_grid(Kern kernel, int threads, size_t smem, long long n_hint) {
-  int per_sm = 0;
-  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
-  per_sm = std::max(per_sm, 1);
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), threads, smem);
   const long long want = (n_hint + threads - 1) / threads;
   return static_cast<int>(std::max(1LL, std::min(want, static_cast<long long>(sm_count()) * per_sm)));
 }
@@ -1012,8 +1004,7 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     const size_t smem = field_tile_smem(m.fv);
     auto kern = field_tile_kernel<16, 64>;
     ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
-    int per_sm = 0;
-    ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFieldTile, smem));
+    const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kFieldTile, smem);
     const long long tiles = (n_hint + kFieldTile - 1) / kFieldTile;
     const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sm_count()) *
                                                                         std::max(per_sm, 1))));
@@ -1023,11 +1014,7 @@ void launch_field_pool(ModelImpl& m, cudaStream_t s, long long n_hint, bool allo
     m.prof.begin("field", s);
     // persistent: exactly the resident blocks (static smem allows ~6 per SM), so no block
     // waits for a second wave with a full share of the work
-    static int team_per_sm = 0;
-    if (!team_per_sm) {
-      ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&team_per_sm, field_team_kernel, kFtTeam * kFtTeams, 0));
-      team_per_sm = std::max(team_per_sm, 1);
-    }
+    const int team_per_sm = blocks_per_sm(reinterpret_cast<const void*>(field_team_kernel), kFtTeam * kFtTeams, 0);
     field_team_kernel<<<static_cast<unsigned>(sm_count() * team_per_sm), kFtTeam * kFtTeams, 0, s>>>(
         m.fv, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr, m.ws().pres.ptr, m.ws().counters.ptr + 2,
         static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr, kTeamMax, act);
@@ -1371,8 +1358,8 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
   Workspace& w = m.ws();
   const long long n = static_cast<long long>(g.res) * g.res * g.res;
   w.ensure(static_cast<size_t>(n), 0);
-  DevBuf<PoseCtx> ctxs;
-  ctxs.alloc(poses.size());
+  DevBuf<PoseCtx>& ctxs = m.grid_ctxs;  // persistent: no allocation (device sync) per update
+  ctxs.ensure(poses.size());
   for (size_t i = 0; i < poses.size(); ++i)
     ARFX_CUDA(cudaMemcpyAsync(ctxs.ptr + i, poses[i]->dev.ptr, sizeof(PoseCtx), cudaMemcpyDeviceToDevice, s));
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
@@ -1387,7 +1374,7 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
   if (d_counters)
     ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToDevice, s));
-  ARFX_CUDA(cudaStreamSynchronize(s));  // ctxs is released on return
+  ARFX_CUDA(cudaStreamSynchronize(s));
 }
 
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,
@@ -1508,6 +1495,35 @@ KernelProfiler::~KernelProfiler() {
   for (cudaEvent_t e : free_events) cudaEventDestroy(e);
 }
 
+int blocks_per_sm(const void* kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  ARFX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(kernel, dev, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  per_sm = per_sm > 0 ? per_sm : 1;
+  cache.emplace(key, per_sm);
+  return per_sm;
+}
+
+int device_sm_count() {
+  static int n[64] = {};
+  int dev = 0;
+  ARFX_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
+  }
+  return n[dev];
+}
+
 void ensure_dyn_smem(const void* kernel, size_t bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> done;
@@ -1518,6 +1534,28 @@ void ensure_dyn_smem(const void* kernel, size_t bytes) {
   if (bytes <= cur) return;
   ARFX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   cur = bytes;
+}
+
+// Training ray pixels of one step (the trainer's ray_batch on the device): draw 0 of
+// keyed_rng(seed, 0x7a11, step, rank) picks the frame (host side); ray i takes draws 1 + 2i
+// (px = next_below(W)) and 2 + 2i (py = next_below(H)) -- bit-identical to the host stream.
+__global__ void train_rays_kernel(uint64_t seed, uint64_t step, uint64_t rank, long long n, uint32_t W, uint32_t H,
+                                  int32_t* __restrict__ px, int32_t* __restrict__ py) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    Pcg32 g = keyed_rng(seed, 0x7a11u, step, rank);
+    pcg_advance(g, static_cast<uint64_t>(1 + 2 * i));
+    px[i] = static_cast<int32_t>(pcg_below(g, W));
+    py[i] = static_cast<int32_t>(pcg_below(g, H));
+  }
+}
+
+void launch_train_rays(uint64_t seed, uint64_t step, uint64_t rank, long long n, int W, int H, int32_t* px, int32_t* py,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  train_rays_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(seed, step, rank, n, static_cast<uint32_t>(W),
+                                                        static_cast<uint32_t>(H), px, py);
+  ARFX_CUDA(cudaGetLastError());
 }
 
 // ---- L_density: occupancy-based regulariser (Eq. 12) ----------

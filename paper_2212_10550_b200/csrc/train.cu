@@ -669,12 +669,7 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __rest
   }
 }
 
-int sms() {
-  int dev = 0, n = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
-}
+int sms() { return device_sm_count(); }
 
 }  // namespace
 
@@ -706,8 +701,8 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
-  int bwd_per_sm = 0;  // persistent: exactly the resident blocks (one wave)
-  ARFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bwd_per_sm, field_bwd_team_kernel, kTeamThreads, team_smem));
+  const int bwd_per_sm =  // persistent: exactly the resident blocks (one wave)
+      blocks_per_sm(reinterpret_cast<const void*>(field_bwd_team_kernel), kTeamThreads, team_smem);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * std::max(bwd_per_sm, 1)), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr, act,
       d_n);

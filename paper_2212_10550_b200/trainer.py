@@ -171,6 +171,14 @@ class Trainer:
         self.ev_fwd = [torch.cuda.Event(), torch.cuda.Event()]
         self.ev_bwd = [torch.cuda.Event(), torch.cuda.Event()]
         self._pending = [None, None]  # per slot: (step, frame) of the enqueued forward
+        # per-step host work kept small: ctypes structs built once, ray pixels drawn on the
+        # device, losses written by the library straight into preallocated history rows
+        self._cam_c = camera.to_c()
+        self._opt_c = self._opt(0, 0).to_c()
+        self._lc = cfg.loss.to_c((camera.width, camera.height))
+        self._adam_c = cfg.adam.to_c()
+        self._hrows = None
+        self._hrow_next = 0
         self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
         self._checked = 0     # steps whose loss has been checked for finiteness
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
@@ -185,37 +193,44 @@ class Trainer:
     def step(self):
         """One SPEC train step, enqueued without host synchronisation (except the occupancy
         update every k steps, which is also where the loss is checked for finiteness).
-        Returns the step's loss as a device tensor (L_rgb, L_alpha, L_hard, L_density, total)."""
+        Returns the step's loss row as a device tensor (L_rgb, L_alpha, L_hard, their weighted
+        sum, L_density, n_empty); `history` gives (L_rgb, L_alpha, L_hard, L_density, total)."""
+        if self.pipelined and self.fused_density:
+            return self._step_pipelined()  # launches only on its own streams
         with self.torch.cuda.stream(self.stream):
-            if self.pipelined and self.fused_density:
-                return self._step_pipelined()
             return self._step()
 
     def _forward(self, step: int):
         """Enqueue step `step`'s forward on fstream into train slot step & 1."""
-        torch = self.torch
-        cfg, W = self.cfg, self.camera.width
+        cfg = self.cfg
         k = step & 1
         fs = self.fstream
         fs.wait_event(self.ev_bwd[k])  # the previous backward that used this slot has run
-        f, px, py = ray_batch(cfg.seed, step, self.rank, self.n_local, len(self.poses), W, self.camera.height)
-        self._h_evt[k].synchronize()
-        hp = self._h_pix[k]
-        hp[0].numpy()[:] = px
-        hp[1].numpy()[:] = py
-        with torch.cuda.stream(fs):
-            self.pxs[k].copy_(hp[0], non_blocking=True)
-            self.pys[k].copy_(hp[1], non_blocking=True)
-        self._h_evt[k].record(fs)
-        L.call("arfx_train_forward_device", self.model._h, self.views[f]._h, C.byref(self.camera.to_c()),
-               self.grid._h, C.byref(self._opt(f, step).to_c()), self.n_local, C.c_void_p(self.pxs[k].data_ptr()),
-               C.c_void_p(self.pys[k].data_ptr()), k, C.c_void_p(fs.cuda_stream))
+        f = fx.keyed_rng(cfg.seed, 0x7A11, step, self.rank).next_below(len(self.poses))  # ray_batch draw 0
+        fsp = C.c_void_p(fs.cuda_stream)
+        L.call("arfx_train_rays_device", cfg.seed, step, self.rank, self.n_local, self.camera.width,
+               self.camera.height, C.c_void_p(self.pxs[k].data_ptr()), C.c_void_p(self.pys[k].data_ptr()), fsp)
+        self._opt_c.frame_id = step * 1024 + f
+        L.call("arfx_train_forward_device", self.model._h, self.views[f]._h, C.byref(self._cam_c), self.grid._h,
+               C.byref(self._opt_c), self.n_local, C.c_void_p(self.pxs[k].data_ptr()),
+               C.c_void_p(self.pys[k].data_ptr()), k, fsp)
         self.ev_fwd[k].record(fs)
         self._pending[k] = (step, f)
 
-    def _step_pipelined(self):
+    def _history_row(self):
+        """A zeroed device row (L_rgb, L_alpha, L_hard, total_without_density, L_density,
+        n_empty) for this step's losses; blocks of 1024 rows, never moved (views stay valid)."""
         torch = self.torch
-        cfg, W = self.cfg, self.camera.width
+        if self._hrows is None or self._hrow_next == self._hrows.shape[0]:
+            with torch.cuda.stream(self.stream):  # zeroed in order before the library writes rows
+                self._hrows = torch.zeros((1024, 6), dtype=torch.float64, device="cuda")
+            self._hrow_next = 0
+        r = self._hrows[self._hrow_next]
+        self._hrow_next += 1
+        return r
+
+    def _step_pipelined(self):
+        cfg = self.cfg
         t = self.step_id
         k = t & 1
         if self._pending[k] is None or self._pending[k][0] != t:
@@ -224,34 +239,31 @@ class Trainer:
         self._pending[k] = None
         self.stream.wait_event(self.ev_fwd[k])
         dens = cfg.loss.w_density > 0 and cfg.density_points > 0
-        lc = cfg.loss.to_c((W, self.camera.height))
+        row = self._history_row()
         sp = C.c_void_p(self.stream.cuda_stream)
-        L.call("arfx_train_backward_device", self.model._h, self.views[f]._h, self.grid._h,
-               C.byref(self._opt(f, t).to_c()), self.n_local, C.c_void_p(self.pxs[k].data_ptr()),
-               C.c_void_p(self.pys[k].data_ptr()), C.c_void_p(self.gt_rgb[f].data_ptr()),
-               C.c_void_p(self.gt_alpha[f].data_ptr()), C.byref(lc), C.c_void_p(self.loss4.data_ptr()), k,
-               cfg.density_points if dens else 0, (cfg.seed * 4 + self.rank) & (2**64 - 1), t,
-               C.c_void_p(self.loss_d.data_ptr()), sp)
+        self._opt_c.frame_id = t * 1024 + f
+        L.call("arfx_train_backward_device", self.model._h, self.views[f]._h, self.grid._h, C.byref(self._opt_c),
+               self.n_local, C.c_void_p(self.pxs[k].data_ptr()), C.c_void_p(self.pys[k].data_ptr()),
+               C.c_void_p(self.gt_rgb[f].data_ptr()), C.c_void_p(self.gt_alpha[f].data_ptr()), C.byref(self._lc),
+               C.c_void_p(row.data_ptr()), k, cfg.density_points if dens else 0,
+               (cfg.seed * 4 + self.rank) & (2**64 - 1), t, C.c_void_p(row.data_ptr() + 4 * 8), sp)
         self.ev_bwd[k].record(self.stream)
-        if not dens:
-            self.loss_d.zero_()
         t1 = t + 1
-        self.adam_stream.wait_stream(self.stream)
-        self.model.adam_step(cfg.adam, t1, 0, self.n_flat, C.c_void_p(self.adam_stream.cuda_stream))
+        self.adam_stream.wait_event(self.ev_bwd[k])  # this step's gradients are complete
+        L.call("arfx_adam_step", self.model._h, C.byref(self._adam_c), t1, 0, self.n_flat,
+               C.c_void_p(self.adam_stream.cuda_stream))
         self.ev_params.record(self.adam_stream)
         if not self._fence_set:
             self.model.set_param_fence(self.ev_params.cuda_event)
             self._fence_set = True
-        loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
-                            self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
-        self._hist.append(loss)
+        self._hist.append(row)
         self.step_id = t1
         if cfg.occupancy_interval > 0 and t1 % cfg.occupancy_interval == 0:
             self._sync()
             arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t1)
             self._check()
         self._forward(t1)  # overlaps this step's backward (its field waits for this Adam)
-        return loss
+        return row
 
     def _step(self):
         torch = self.torch
@@ -304,8 +316,9 @@ class Trainer:
                 self._fence_set = True
         else:
             self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
-        loss = torch.stack([self.loss4[0], self.loss4[1], self.loss4[2], self.loss_d[0],
-                            self.loss4[3] + cfg.loss.w_density * self.loss_d[0]])
+        loss = self._history_row()
+        loss[0:4].copy_(self.loss4)
+        loss[4:6].copy_(self.loss_d)
         self._hist.append(loss)
         self.step_id = t
         if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
@@ -335,7 +348,7 @@ class Trainer:
 
     def _check(self):
         if self._checked < len(self._hist):
-            h = torch_stack_cpu(self.torch, self._hist[self._checked:])
+            h = self._rows_cpu(self._hist[self._checked:])
             bad = ~np.all(np.isfinite(h), axis=1)
             if bad.any():
                 k = self._checked + int(np.argmax(bad)) + 1
@@ -347,7 +360,13 @@ class Trainer:
         """Per-step losses (synchronises): rows (L_rgb, L_alpha, L_hard, L_density, total)."""
         self._sync()
         self._check()
-        return torch_stack_cpu(self.torch, self._hist) if self._hist else np.zeros((0, 5))
+        return self._rows_cpu(self._hist) if self._hist else np.zeros((0, 5))
+
+    def _rows_cpu(self, rows) -> np.ndarray:
+        """Stored rows (L_rgb, L_alpha, L_hard, weighted sum of those, L_density, n_empty) ->
+        (L_rgb, L_alpha, L_hard, L_density, total)."""
+        r = torch_stack_cpu(self.torch, rows)
+        return np.stack([r[:, 0], r[:, 1], r[:, 2], r[:, 4], r[:, 3] + self.cfg.loss.w_density * r[:, 4]], axis=1)
 
     def save(self, path) -> None:
         """Checkpoint (model, Adam moments, occupancy grid, step) for an exact resume."""
