@@ -130,3 +130,21 @@ def test_checkpoint_rejects_malformed_files(tmp_path):
         A.load_checkpoint(bad)
     with pytest.raises(InvalidArgument):
         A.load_checkpoint(tmp_path / "missing.ckpt")
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/arfx.h is the drop-in boundary for C / cgo / FFI callers: it must compile as
+    strict C99 (no C++ types in the signatures) and as C++."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    inc = Path(__file__).resolve().parent.parent / "include"
+    src = tmp_path / "use.c"
+    src.write_text('#include "arfx.h"\nint main(void) { arfx_loss_config c = {1, 0.1, 0.1, 0.1, 0.1, 0, 0};\n'
+                   '  (void)c; return (int)sizeof(arfx_render_options) == 0; }\n')
+    for cc, flags in (("gcc", ["-std=c99", "-pedantic", "-Wall", "-Werror"]), ("g++", ["-std=c++17", "-Wall", "-x", "c++"])):
+        if shutil.which(cc) is None:
+            continue
+        r = subprocess.run([cc, *flags, "-I", str(inc), "-c", str(src), "-o", str(tmp_path / f"{cc}.o")],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
