@@ -533,13 +533,70 @@ def run_e2e(args, model, poses, cam, opt, occ, rank, world, views):
     dt = time.perf_counter() - t0
     if int(cnts[:, 3].sum()):
         raise RuntimeError("e2e: workspace overflow in the pipelined frames")
+    # the same loop through the public frame-graph API: two captured frames (grid + render)
+    # with their own pose handles and device outputs, replayed alternately after an async
+    # pose upload; each replay's RGB/alpha/counters go to pinned host memory on a copy
+    # stream while the other graph replays
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    gviews = [arf.PosedModelView(model, poses[0]), arf.PosedModelView(model, poses[1])]
+    d_out = [(torch.zeros(W_IMG * H_IMG * 3, dtype=torch.float32, device="cuda"),
+              torch.zeros(W_IMG * H_IMG, dtype=torch.float32, device="cuda"),
+              torch.zeros(4, dtype=torch.int64, device="cuda")) for _ in range(2)]
+    h_out = [(torch.zeros(W_IMG * H_IMG * 3, dtype=torch.float32).pin_memory(),
+              torch.zeros(W_IMG * H_IMG, dtype=torch.float32).pin_memory(),
+              torch.zeros(4, dtype=torch.int64).pin_memory()) for _ in range(2)]
+    h_cnt = torch.zeros((K, 4), dtype=torch.int64).pin_memory()
+    ccam, copt = cam.to_c(), opt.to_c()
+    graphs = []
+    for i in range(2):
+        h = C.c_void_p()
+        check(L.arfx_frame_graph_create(model._h, gviews[i]._h, C.byref(ccam), occ._h, C.byref(copt), rank, world, 1 | 8,
+                                        C.c_void_p(d_out[i][0].data_ptr()), C.c_void_p(d_out[i][1].data_ptr()),
+                                        C.c_void_p(d_out[i][2].data_ptr()), sp, C.byref(h)))
+        graphs.append(h)
+    cs = torch.cuda.Stream()
+    ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
+    cur = torch.cuda.current_stream()
+
+    def graph_frame(k, pose, cnt_row):
+        i = k & 1
+        cur.wait_event(ev_copied[i])  # this slot's previous outputs have reached the host
+        gviews[i].update(pose, stream=sp, sync=False)
+        check(L.arfx_frame_graph_launch(graphs[i], sp))
+        ev_done[i].record(cur)
+        cs.wait_event(ev_done[i])
+        with torch.cuda.stream(cs):
+            h_out[i][0].copy_(d_out[i][0], non_blocking=True)
+            h_out[i][1].copy_(d_out[i][1], non_blocking=True)
+            cnt_row.copy_(d_out[i][2], non_blocking=True)
+        ev_copied[i].record(cs)
+
+    for k in range(2):
+        graph_frame(k, poses[k], h_cnt[k])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(K):
+        graph_frame(k, poses[(args.warmup + k) % N_FRAMES], h_cnt[k])
+    cs.synchronize()
+    torch.cuda.synchronize()
+    dt_graph = time.perf_counter() - t0
+    for h in graphs:
+        check(L.arfx_frame_graph_destroy(h))
+    if int(h_cnt[:, 3].sum()):
+        raise RuntimeError("e2e: workspace overflow in the graph frames")
     rows = sum(1 for y in range(H_IMG) if (y // 16) % world == rank)
     pose_ctx_bytes = 8 + 32 * (12 + 12 + 3 + 3 + 1) * 8 + 12 * 8 + 32 * 16  # sizeof(PoseCtx), kMaxBones 32
-    return {"value": K / dt, "unit": UNIT, "h2d_bytes_per_step": pose_ctx_bytes,
+    async_value = K / dt
+    graph_value = K / dt_graph
+    best_graph = graph_value > async_value
+    return {"value": max(async_value, graph_value), "unit": UNIT, "h2d_bytes_per_step": pose_ctx_bytes,
             "d2h_bytes_per_step": rows * W_IMG * 16 + 32, "steps": K,
-            "api": "arfx_pose_update_async + arfx_build_inference_grid + arfx_render_model_async (host buffers, "
-                   "D2H overlapping the next frame), one arfx_render_wait",
-            "sync_api_value": K / dt_sync}
+            "api": ("arfx_pose_update_async + arfx_frame_graph_launch (two captured grid + render frames, "
+                    "alternating) + D2H of RGB/alpha/counters to pinned host on a copy stream" if best_graph else
+                    "arfx_pose_update_async + arfx_build_inference_grid + arfx_render_model_async (host buffers, "
+                    "D2H overlapping the next frame), one arfx_render_wait"),
+            "async_api_value": async_value, "graph_api_value": graph_value, "sync_api_value": K / dt_sync}
 
 
 def bench_microbench(steps: int, with_cpu: bool):
