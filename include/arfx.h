@@ -406,6 +406,12 @@ int arfx_train_backward_device(arfx_model m, arfx_pose pose, arfx_occ_grid occ, 
  * gradients zeroed in the same pass. Asynchronous on stream. */
 int arfx_adam_step(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
                    void* stream);
+/* arfx_adam_step behind a non-finite-loss guard: d_loss = the step's n_loss
+ * loss values (device); if any is non-finite, or *d_bad (device int, sticky) is already set,
+ * the step changes nothing and *d_bad = 1. The caller reads *d_bad when convenient and aborts
+ * with the model still at its last finite state. */
+int arfx_adam_step_guarded(arfx_model m, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
+                           const double* d_loss, int n_loss, int* d_bad, void* stream);
 /* Flat device vectors [grid | pad | mlp | pad] of n_flat floats: params, grads, Adam m, v
  * (allocated on first use); mlp_offset = index of the first MLP parameter. */
 int arfx_model_flat(arfx_model m, float** params, float** grads, float** adam_m, float** adam_v,
@@ -419,9 +425,15 @@ int arfx_model_set_adam(arfx_model m, const float* adam_m, const float* adam_v);
 enum { ARFX_GRAPH_GRID = 1, ARFX_GRAPH_GRID_SHARD = 2, ARFX_GRAPH_MASK = 4, ARFX_GRAPH_RENDER = 8 };
 /* Captures the chosen parts of one frame for pose handle p as a CUDA graph: the inference
  * grid (GRID) or its z-slab shard (GRID_SHARD), the mask rebuild (MASK), the render into
- * device buffers (RENDER; d_counters [2][4] may be NULL). Every kernel reads the pose from
- * its device PoseContext, so after updating the handle in place (arfx_pose_update,
- * arfx_pose_copy) a replay renders the new pose. `stream` must be non-NULL (capture). */
+ * device buffers (RENDER). d_counters [2][4] (grid, render: posed, canonical, pool, overflow)
+ * is required for the GRID / GRID_SHARD / RENDER parts: a replay cannot grow the workspace,
+ * so a frame that overflowed it sets d_counters[3] / d_counters[4 + 3] != 0 and must be
+ * re-rendered through the synchronous API. Every kernel reads the pose from its device
+ * PoseContext, so after updating the handle in place (arfx_pose_update, arfx_pose_copy) a
+ * replay renders the new pose. `stream` must be non-NULL (capture). The graph holds raw
+ * pointers into the model's workspace: any later workspace growth (a larger render, another
+ * camera or shard, an overflow regrow) invalidates it, and arfx_frame_graph_launch then
+ * returns 1 (invalid_argument) instead of replaying -- destroy and re-create the graph. */
 int arfx_frame_graph_create(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
                             const arfx_render_options* opt, int shard, int n_shards, int parts, float* d_rgb,
                             float* d_alpha, uint64_t* d_counters, void* stream, arfx_frame_graph* out);

@@ -485,19 +485,46 @@ class Checker:
                                            _p(gg, C.c_float), _p(mg, C.c_float), _p(cnt, C.c_uint64)))
         return rgb, alpha, gg, mg, cnt
 
-    def bench_frames(self, M, poses, cam, occ_cfg, opts):
-        """reference-only: time n x (inference grid + render) with its own thread pool."""
+    def bench_frames(self, M, poses, cam, occ_cfg, opts, keep_last: bool = False):
+        """reference-only: time n x (inference grid + render) with its own thread pool.
+        keep_last: also return the last frame's (rgb, alpha, occupancy mask)."""
         assert self.kind == "ref"
         n = len(poses)
         b = np.ascontiguousarray(np.stack([p.bone_transforms for p in poses]), np.float64)
         g = np.ascontiguousarray(np.stack([p.global_transform for p in poses]), np.float64)
         secs = np.zeros(n)
         posed = np.zeros(n, np.uint64)
+        last = None
+        if keep_last:
+            res = occ_cfg.resolution
+            last = (np.zeros((cam.height, cam.width, 3), np.float32), np.zeros((cam.height, cam.width), np.float32),
+                    np.zeros(res ** 3, np.uint8))
         self.check(self.f("bench_frames")(C.byref(M), n, _p(b, C.c_double), _p(g, C.c_double),
                                           C.byref(self.cam(cam)), C.byref(self.occcfg(occ_cfg)),
                                           C.byref(self.opts(opts)), _p(secs, C.c_double), _p(posed, C.c_uint64),
-                                          None, None))
-        return secs, posed
+                                          *((None, None, None) if last is None else
+                                            (_p(last[0], C.c_float), _p(last[1], C.c_float),
+                                             _p(last[2], C.c_uint8)))))
+        return (secs, posed, last) if keep_last else (secs, posed)
+
+    def random_pose(self, sk, seed, stream=7, max_angle=0.5, yaw=0.3):
+        """reference-only: (bones12[n,12], global12[12]) of the fixture pose built by the reference
+        (ref_driver.cpp arfr_random_pose; fixtures.random_pose restates it)."""
+        assert self.kind == "ref"
+        nb = len(sk.bones)
+        b = np.zeros((nb, 12), np.float64)
+        g = np.zeros(12, np.float64)
+        self.check(self.f("random_pose")(C.byref(self.skel(sk)), C.c_uint64(seed), C.c_uint64(stream),
+                                         C.c_double(max_angle), C.c_double(yaw), _p(b, C.c_double),
+                                         _p(g, C.c_double)))
+        return b, g
+
+    def default_camera(self, sk, w, h) -> Cam:
+        """reference-only: arf::default_camera (R/scene.hpp:190-197)."""
+        assert self.kind == "ref"
+        c = Cam()
+        self.check(self.f("default_camera")(C.byref(self.skel(sk)), int(w), int(h), C.byref(c)))
+        return c
 
     def thread_count(self):
         return int(self.f("thread_count")())

@@ -629,7 +629,7 @@ int arfr_train_fwd_bwd(const ao_model* m, const double* bones12, const double* g
 int arfr_bench_frames(const ao_model* m, int n_frames, const double* bones12,
                       const double* global12, const ao_camera* cam, const ao_occ_cfg* oc,
                       const ao_render_opts* o, double* seconds, uint64_t* posed_per_frame,
-                      float* rgb_last, float* alpha_last) {
+                      float* rgb_last, float* alpha_last, uint8_t* mask_last) {
   return guard([&] {
     const arf::Model<float> M = to_model(m);
     const int nb = m->skel.n_bones;
@@ -647,12 +647,53 @@ int arfr_bench_frames(const ao_model* m, int n_frames, const double* bones12,
       if (f == n_frames - 1 && rgb_last) {
         std::copy(img.rgb.begin(), img.rgb.end(), rgb_last);
         std::copy(img.alpha.begin(), img.alpha.end(), alpha_last);
+        if (mask_last) std::copy(occ.mask.begin(), occ.mask.end(), mask_last);
       }
     }
   });
 }
 
 int arfr_thread_count(void) { return arf::thread_count(); }
+
+// bench.py --impl reference builds its workload through the reference alone (no product
+// code on that arm). random_pose: keyed_rng(seed, stream) (R/rng.hpp:61-63); per non-root
+// joint draw axis x, y, z ~ U(-1,1), then angle ~ U(-a,a) (one statement per draw, SURVEY.md
+// §8d), axis normalised, Mat3d::axis_angle (R/math.hpp:170-178); global yaw_about the root
+// head (R/scene.hpp:169-171); pose_from_joint_rotations (R/skeleton.hpp:93-110).
+int arfr_random_pose(const ao_skeleton* s, uint64_t seed, uint64_t stream, double max_angle, double yaw,
+                     double* bones12, double* global12) {
+  return guard([&] {
+    const arf::Skeleton sk = skeleton(s);
+    arf::Pcg32 rng = arf::keyed_rng(seed, stream);
+    std::vector<arf::Mat3d> rots(static_cast<std::size_t>(s->n_bones), arf::Mat3d::identity());
+    for (int i = 1; i < s->n_bones; ++i) {
+      const double ax = rng.uniform(-1.0, 1.0);
+      const double ay = rng.uniform(-1.0, 1.0);
+      const double az = rng.uniform(-1.0, 1.0);
+      const double ang = rng.uniform(-max_angle, max_angle);
+      const double n = std::sqrt(ax * ax + ay * ay + az * az);
+      rots[static_cast<std::size_t>(i)] = arf::Mat3d::axis_angle({ax / n, ay / n, az / n}, ang);
+    }
+    const arf::Rigidd g = arf::yaw_about(sk.bones[0].head, yaw);
+    const arf::SkeletonPose p = arf::pose_from_joint_rotations(sk, rots, g);
+    for (int i = 0; i < s->n_bones; ++i) put_rigid(bones12 + 12 * i, p.bone_transforms[static_cast<std::size_t>(i)]);
+    put_rigid(global12, p.global_transform);
+  });
+}
+
+// arf::default_camera (R/scene.hpp:190-197)
+int arfr_default_camera(const ao_skeleton* s, int w, int h, ao_camera* cam) {
+  return guard([&] {
+    const arf::Camera c = arf::default_camera(skeleton(s), w, h);
+    cam->fx = c.fx;
+    cam->fy = c.fy;
+    cam->cx = c.cx;
+    cam->cy = c.cy;
+    cam->width = c.width;
+    cam->height = c.height;
+    put_rigid(cam->extrinsic, c.extrinsic);
+  });
+}
 
 }  // extern "C"
 

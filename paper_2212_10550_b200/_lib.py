@@ -187,6 +187,8 @@ _PROTOS = {
                                              C.POINTER(ArfxLossConfig), P, C.c_int, C.c_int64, C.c_uint64, C.c_uint64,
                                              P, P]),
     "arfx_adam_step": (C.c_int, [H, C.POINTER(ArfxAdamConfig), C.c_int64, C.c_int64, C.c_int64, P]),
+    "arfx_adam_step_guarded": (C.c_int, [H, C.POINTER(ArfxAdamConfig), C.c_int64, C.c_int64, C.c_int64, P, C.c_int,
+                                         P, P]),
     "arfx_model_flat": (C.c_int, [H, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P),
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "arfx_model_get_adam": (C.c_int, [H, c_float_p, c_float_p]),

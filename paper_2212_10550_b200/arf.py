@@ -295,9 +295,17 @@ class Model:
         return {"params": ps[0].value, "grads": ps[1].value, "adam_m": ps[2].value, "adam_v": ps[3].value,
                 "n_flat": n.value, "mlp_offset": off.value}
 
-    def adam_step(self, cfg: "AdamConfig", step: int, begin: int = 0, end: int = -1, stream=None) -> None:
-        """One Adam step (zero-grad fused) over flat indices [begin, end) (arfx_adam_step)."""
-        call("arfx_adam_step", self._h, C.byref(cfg.to_c()), step, begin, end, stream)
+    def adam_step(self, cfg: "AdamConfig", step: int, begin: int = 0, end: int = -1, stream=None,
+                  guard=None) -> None:
+        """One Adam step (zero-grad fused) over flat indices [begin, end) (arfx_adam_step).
+        guard = (loss row device pointer, n values, device int flag pointer): the step is
+        skipped on the device if the loss is non-finite (arfx_adam_step_guarded)."""
+        if guard is None:
+            call("arfx_adam_step", self._h, C.byref(cfg.to_c()), step, begin, end, stream)
+        else:
+            d_loss, n, d_bad = guard
+            call("arfx_adam_step_guarded", self._h, C.byref(cfg.to_c()), step, begin, end, d_loss, n, d_bad,
+                 stream)
 
     def adam_state(self):
         n = self.flat()["n_flat"]

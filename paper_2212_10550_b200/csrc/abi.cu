@@ -27,6 +27,8 @@ struct arfx_frame_graph_s {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int device = 0;
+  const arfx::Workspace* ws = nullptr;  // the workspace the kernels were captured on
+  unsigned long long ws_gen = 0;        // its generation at capture
   ~arfx_frame_graph_s() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -311,7 +313,15 @@ struct RenderBuffers {
   DevBuf<float> rgb, alpha;
   DevBuf<unsigned long long> counters;
 };
-thread_local std::unique_ptr<RenderBuffers> t_rb;
+// the synchronous render's device staging, per (host thread, device): a thread may drive
+// models on several GPUs
+thread_local std::unique_ptr<RenderBuffers> t_rb_dev[64];
+RenderBuffers& render_buffers(int device) {
+  require(device >= 0 && device < 64, "render: device ordinal out of range");
+  auto& rb = t_rb_dev[device];
+  if (!rb) rb = std::make_unique<RenderBuffers>();
+  return *rb;
+}
 
 void validate_render(const HostCamera& cam, const arfx_render_options* opt, int shard, int nshards) {
   validate_camera(cam);
@@ -1003,6 +1013,8 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
     require(!(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK)) || occ,
             "frame_graph_create: the grid parts need an occupancy grid");
     require(!(parts & ARFX_GRAPH_RENDER) || (d_rgb && d_alpha && opt), "frame_graph_create: render outputs");
+    require(d_counters != nullptr || !(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_RENDER)),
+            "frame_graph_create: d_counters is required (a replay reports workspace overflow in d_counters[4 + 3])");
     ModelImpl& m = mh->impl;
     HostCamera hc{};
     if (parts & ARFX_GRAPH_RENDER) {
@@ -1054,6 +1066,8 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
     ARFX_CUDA(cudaStreamEndCapture(s, &g->graph));
     m.prof.on = prof;
     ARFX_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+    g->ws = &m.ws();
+    g->ws_gen = m.ws().gen;
     *out = g.release();
   });
 }
@@ -1061,6 +1075,10 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
 int arfx_frame_graph_launch(arfx_frame_graph g, void* stream) {
   return guard([&] {
     require(g && g->exec, "frame_graph_launch: null graph");
+    if (g->ws->gen != g->ws_gen)
+      throw std::invalid_argument(
+          "frame_graph_launch: the model workspace was reallocated since this graph was captured (a larger "
+          "render, a camera / shard change or an overflow regrow); destroy the graph and create it again");
     ARFX_CUDA(cudaSetDevice(g->device));
     ARFX_CUDA(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
   });
@@ -1080,7 +1098,7 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
     validate_render(hc, opt, shard, nshards);
     ARFX_CUDA(cudaSetDevice(m.device));
     const cudaStream_t s = stream_of(m, stream);
-    if (!t_rb) t_rb = std::make_unique<RenderBuffers>();
+    RenderBuffers* t_rb = &render_buffers(m.device);
     const size_t npix = static_cast<size_t>(hc.width) * hc.height;
     t_rb->rgb.ensure(npix * 3);
     t_rb->alpha.ensure(npix);
@@ -1950,7 +1968,7 @@ int arfx_train_density_step_device(arfx_model mh, arfx_pose ph, const arfx_camer
 // the parameter fence (arfx_model_set_param_fence). The backward = composite + fused losses
 // + field backward of that slot (+ the L_density step as in arfx_train_density_step_device).
 namespace {
-Workspace& train_slot(ModelImpl& m, int slot) { return slot ? m.ws_alt : m.ws_main; }
+Workspace& train_slot(ModelImpl& m, int slot) { return slot ? m.ws_alt : m.ws_t0; }
 }  // namespace
 
 int arfx_train_rays_device(uint64_t seed, uint64_t step, uint64_t rank, int64_t n, int width, int height,
@@ -2052,6 +2070,24 @@ int arfx_adam_step(arfx_model mh, const arfx_adam_config* cfg, int64_t step, int
     const cudaStream_t s = stream_of(m, stream);
     ensure_grad_store(m, s);
     adam_step(m, c, step, begin, end, s);
+  });
+}
+
+int arfx_adam_step_guarded(arfx_model mh, const arfx_adam_config* cfg, int64_t step, int64_t begin, int64_t end,
+                           const double* d_loss, int n_loss, int* d_bad, void* stream) {
+  return guard([&] {
+    require(mh != nullptr, "adam: null model");
+    require(d_loss && d_bad && n_loss > 0 && n_loss <= 64, "adam_guarded: loss row (1..64 doubles) and flag required");
+    const AdamCfg c = adam_of(cfg);
+    require(step >= 1, "adam: step must be >= 1");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    if (end < 0) end = static_cast<int64_t>(m.n_flat);
+    require(begin >= 0 && begin <= end && end <= static_cast<int64_t>(m.n_flat) && begin % 4 == 0 && end % 4 == 0,
+            "adam: range must be a multiple-of-4 slice of the flat vector");
+    const cudaStream_t s = stream_of(m, stream);
+    ensure_grad_store(m, s);
+    adam_step(m, c, step, begin, end, s, d_loss, n_loss, d_bad);
   });
 }
 

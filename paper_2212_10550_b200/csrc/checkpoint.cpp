@@ -254,8 +254,8 @@ int arfx_checkpoint_load(const char* path, arfx_model* m_out, arfx_occ_grid* occ
     const std::vector<double> sw = r.arr<double>(ns);
     arfx_model m = nullptr;
     pass(arfx_model_create(&d, gp.data(), mp.data(), sw.data(), &m));
+    arfx_occ_grid og = nullptr;
     try {
-      arfx_occ_grid og = nullptr;
       if (flags & 1u) {
         const int res = r.get<int32_t>();
         double lo[3], hi[3];
@@ -289,6 +289,7 @@ int arfx_checkpoint_load(const char* path, arfx_model* m_out, arfx_occ_grid* occ
       if (occ_out) *occ_out = og;
       if (step_out) *step_out = step;
     } catch (...) {
+      if (og) arfx_occ_destroy(og);
       arfx_model_destroy(m);
       throw;
     }

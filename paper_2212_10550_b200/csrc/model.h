@@ -21,6 +21,7 @@ struct DevBuf {
   T* ptr = nullptr;
   size_t n = 0;
   bool owned = true;
+  unsigned long long* gen = nullptr;  // bumped on every (re)allocation (Workspace::gen)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -40,12 +41,14 @@ struct DevBuf {
   void ensure(size_t count) {  // grow-only, contents not preserved
     if (count <= n) return;
     release();
+    if (gen) ++*gen;
     if (count == 0) return;
     ARFX_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
     n = count;
   }
   void alloc(size_t count) {
     release();
+    if (gen) ++*gen;
     if (count) ARFX_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
     n = count;
   }
@@ -89,6 +92,22 @@ struct Workspace {
   DevBuf<uint32_t> bwd_own;   // deterministic mode: per-owner flagged count -> list offset
   DevBuf<unsigned long long> bwd_n;
   int last_rows = -1, last_shard = -1, last_nshards = -1, last_w = -1, n_rows = 0;
+  // Generation: bumped whenever any buffer above is (re)allocated (or the row list is
+  // rewritten). A captured frame graph holds raw pointers into this workspace and refuses to
+  // replay once the generation moved (arfx_frame_graph_launch).
+  unsigned long long gen = 0;
+  Workspace() {
+    bind(sx, sy, sz, sdelta, sray, sidx, snroot, sbase, ssel, px, py, pz, powner, pres, ray_first, ray_count,
+         row_list, train_terms, tc_tiles, dens_pts, dens_empty, dens_scale, train_rgb, train_alpha, counters,
+         occ_box, fwd_act, smask, scount, scan_sums, items, keys, unsorted, key_hist, res4, strans, pgs, pgc,
+         pflag, bwd_rec, bwd_list, bwd_partial, bwd_own, bwd_n);
+  }
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+  template <typename... B>
+  void bind(B&... b) {
+    ((b.gen = &gen), ...);
+  }
   void ensure(size_t posed, size_t pix);
   void reserve_worst(size_t targets, size_t n_bones);
   size_t learned_starts = 0;  // raised when a frame overflowed the start slots
@@ -157,7 +176,9 @@ struct ModelImpl {
   SkinView sv{};
   // Workspaces: ws() is the one the launch helpers use; a second one lets the L_density
   // forward run on the side stream concurrently with the train step (WorkspaceScope).
-  Workspace ws_main, ws_side, ws_alt;  // ws_alt: second train slot (pipelined forward/backward)
+  // ws_t0 / ws_alt: the two train slots of the pipelined trainer (a slot's forward state lives
+  // across calls, so nothing else may use them); ws_main serves every other call.
+  Workspace ws_main, ws_side, ws_t0, ws_alt;
   Workspace* ws_cur = &ws_main;
   Workspace& ws() { return *ws_cur; }
   cudaStream_t side = nullptr;  // lazily created non-blocking stream
@@ -274,7 +295,8 @@ struct AdamCfg {
   double final_lr_factor;
 };
 double cosine_lr(double lr0, const AdamCfg& c, long long step);
-void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s);
+void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s,
+               const double* guard = nullptr, int n_guard = 0, int* bad = nullptr);
 void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const float* d_dC, const float* d_dA,
                      float* d_rgb, float* d_alpha, cudaStream_t s, const LossTargets* lt = nullptr);
 // Points the launch helpers at another workspace for a scope (host-side; the kernels

@@ -35,11 +35,22 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
 // acc (deterministic mode, pending hash-grid sums): the first n4_acc float4s of the
 // gradient also take acc's fixed-point sums, which are cleared -- the same f32 expression
 // as flush_grad_acc (train.cu), so folding here or flushing first gives equal bits.
+// guard (optional): the step's loss row; if any entry is non-finite, or *bad is already set
+// by an earlier step, the whole step is skipped (parameters, moments and gradients untouched)
+// and *bad is set -- the trainer raises NumericError when it next reads the flag, with the
+// model still at its last finite state (SPEC.md:494 abort on a non-finite loss).
 template <bool Acc>
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ g,
                                                    float* __restrict__ m, float* __restrict__ v, long long b4,
                                                    long long e4, AdamScalars k, longlong2* __restrict__ acc,
-                                                   long long n4_acc) {
+                                                   long long n4_acc, const double* __restrict__ guard,
+                                                   int n_guard, int* bad) {
+  if (guard) {
+    bool nonfinite = false;
+    for (int j = 0; j < n_guard; ++j) nonfinite |= !isfinite(guard[j]);
+    if (nonfinite && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(bad, 1);
+    if (nonfinite || *reinterpret_cast<volatile int*>(bad)) return;
+  }
   for (long long i = b4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < e4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float4 P = reinterpret_cast<float4*>(p)[i], G = reinterpret_cast<float4*>(g)[i];
@@ -77,7 +88,8 @@ double cosine_lr(double lr0, const AdamCfg& c, long long step) {
   return lr0 * (f + (1.0 - f) * 0.5 * (1.0 + std::cos(3.14159265358979323846 * t)));
 }
 
-void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s) {
+void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, long long end, cudaStream_t s,
+               const double* guard, int n_guard, int* bad) {
   const size_t n = m.n_flat;
   if (!m.adam_m.ptr) {
     m.adam_m.alloc(n);
@@ -105,11 +117,13 @@ void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, 
   if (m.acc_pending) {
     adam_kernel<true><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
         m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr, m.adam_v.ptr, b4, e4, k,
-        reinterpret_cast<longlong2*>(m.grid_acc.ptr), static_cast<long long>(m.grid_acc.n / 4));
+        reinterpret_cast<longlong2*>(m.grid_acc.ptr), static_cast<long long>(m.grid_acc.n / 4), guard, n_guard,
+        bad);
     m.acc_pending = false;
   } else {
     adam_kernel<false><<<static_cast<unsigned>(blocks), 256, 0, s>>>(m.flat_params.ptr, m.flat_grads.ptr, m.adam_m.ptr,
-                                                                     m.adam_v.ptr, b4, e4, k, nullptr, 0);
+                                                                     m.adam_v.ptr, b4, e4, k, nullptr, 0, guard,
+                                                                     n_guard, bad);
   }
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);

@@ -181,6 +181,9 @@ class Trainer:
         self._hrow_next = 0
         self._hist = []       # per step: device tensor (L_rgb, L_alpha, L_hard, L_density, total)
         self._checked = 0     # steps whose loss has been checked for finiteness
+        # set on the device by the guarded Adam when a step's loss is non-finite: that step and
+        # every later one leave the model untouched, _check raises
+        self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
         self._h_pix = [torch.zeros((2, self.n_local), dtype=torch.int32).pin_memory() for _ in range(2)]
         self._h_evt = [torch.cuda.Event(), torch.cuda.Event()]
@@ -250,7 +253,8 @@ class Trainer:
         self.ev_bwd[k].record(self.stream)
         t1 = t + 1
         self.adam_stream.wait_event(self.ev_bwd[k])  # this step's gradients are complete
-        L.call("arfx_adam_step", self.model._h, C.byref(self._adam_c), t1, 0, self.n_flat,
+        L.call("arfx_adam_step_guarded", self.model._h, C.byref(self._adam_c), t1, 0, self.n_flat,
+               C.c_void_p(row.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()),
                C.c_void_p(self.adam_stream.cuda_stream))
         self.ev_params.record(self.adam_stream)
         if not self._fence_set:
@@ -302,6 +306,17 @@ class Trainer:
         if not dens:
             self.loss_d.zero_()
         t = self.step_id + 1
+        loss = self._history_row()
+        loss[0:4].copy_(self.loss4)
+        loss[4:6].copy_(self.loss_d)
+        self._hist.append(loss)
+        guard = loss
+        if self.world > 1:
+            # every rank must skip together: the guard is the sum of the ranks' loss rows
+            import torch.distributed as dist
+            guard = loss.clone()
+            dist.all_reduce(guard, op=dist.ReduceOp.SUM, group=self.dp.group)
+        gd = (C.c_void_p(guard.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()))
         if cfg.deterministic and self.world > 1:
             self.model.flush_grads(sp)  # the reduce-scatter reads the gradient array directly
         if self.adam_stream is not None:
@@ -309,17 +324,13 @@ class Trainer:
             # (which read neither parameters nor gradients) run beside it, its field kernels
             # wait on ev_params (arfx_model_set_param_fence)
             self.adam_stream.wait_stream(self.stream)
-            self.model.adam_step(cfg.adam, t, 0, self.n_flat, C.c_void_p(self.adam_stream.cuda_stream))
+            self.model.adam_step(cfg.adam, t, 0, self.n_flat, C.c_void_p(self.adam_stream.cuda_stream), gd)
             self.ev_params.record(self.adam_stream)
             if not self._fence_set:
                 self.model.set_param_fence(self.ev_params.cuda_event)
                 self._fence_set = True
         else:
-            self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp))
-        loss = self._history_row()
-        loss[0:4].copy_(self.loss4)
-        loss[4:6].copy_(self.loss_d)
-        self._hist.append(loss)
+            self.dp.step(lambda b, e: self.model.adam_step(cfg.adam, t, b, e, sp, gd))
         self.step_id = t
         if cfg.occupancy_interval > 0 and t % cfg.occupancy_interval == 0:
             self._sync()  # the host-buffer API below runs on the library's stream
@@ -347,6 +358,12 @@ class Trainer:
             pass
 
     def _check(self):
+        if int(self.bad.item()):
+            h = self._rows_cpu(self._hist[self._checked:]) if self._checked < len(self._hist) else np.zeros((0, 5))
+            bad = ~np.all(np.isfinite(h), axis=1)
+            k = self._checked + int(np.argmax(bad)) + 1 if bad.any() else self._checked
+            raise L.NumericError(3, f"train_step: non-finite loss at step {k}; the optimizer skipped that step and "
+                                    "every later one, so the model holds its last finite state")
         if self._checked < len(self._hist):
             h = self._rows_cpu(self._hist[self._checked:])
             bad = ~np.all(np.isfinite(h), axis=1)

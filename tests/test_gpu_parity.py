@@ -375,9 +375,11 @@ def test_frame_graph_replays_updated_poses(gpu):
     sp = C.c_void_p(st.cuda_stream)
     rgb = torch.zeros(96 * 96 * 3, device="cuda")
     alpha = torch.zeros(96 * 96, device="cuda")
+    cnt = torch.zeros((2, 4), dtype=torch.int64, device="cuda")
     g = C.c_void_p()
     call("arfx_frame_graph_create", m._h, gview._h, C.byref(cam.to_c()), occ._h, C.byref(opt.to_c()), 0, 1,
-         1 | 8, C.c_void_p(rgb.data_ptr()), C.c_void_p(alpha.data_ptr()), None, sp, C.byref(g))
+         1 | 8, C.c_void_p(rgb.data_ptr()), C.c_void_p(alpha.data_ptr()), C.c_void_p(cnt.data_ptr()), sp,
+         C.byref(g))
     try:
         for p, v in zip(poses, views):
             call("arfx_pose_copy", gview._h, v._h, sp)
@@ -388,6 +390,13 @@ def test_frame_graph_replays_updated_poses(gpu):
             assert np.array_equal(occ.mask, ref_occ.mask)
             assert np.array_equal(rgb.cpu().numpy().reshape(96, 96, 3), ref_img.rgb)
             assert np.array_equal(alpha.cpu().numpy().reshape(96, 96), ref_img.alpha)
+            assert int(cnt[:, 3].sum()) == 0
+        # a render that grows the workspace (larger frame) invalidates the captured pointers:
+        # the replay is refused instead of reading freed buffers
+        arf.render_model(m, poses[0], fx.default_camera(sk, 300, 280), occ, opt)
+        from paper_2212_10550_b200 import InvalidArgument
+        with pytest.raises(InvalidArgument, match="reallocated"):
+            call("arfx_frame_graph_launch", g, sp)
     finally:
         call("arfx_frame_graph_destroy", g)
 

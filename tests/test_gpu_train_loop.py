@@ -422,3 +422,44 @@ def test_frame_targets_match_per_ray_targets(gpu):
     assert out[0][0][0] > 0
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+def test_render_between_train_calls_does_not_disturb_training(gpu):
+    """Pipelined trainer: after train(n) with n odd, step n's forward sits in a train slot; a
+    540x540 render (which grows the render workspace) and an inference grid between train()
+    calls must not touch it -- the continuation equals an uninterrupted run bit for bit."""
+    a = _det_trainer()
+    ha = a.train(24)
+    b = _det_trainer()
+    b.train(11)
+    pose = b.poses[1]
+    arf.render_model(b.model, pose, fx.default_camera(fx.default_figure_skeleton(), 540, 540),
+                     arf.build_model_inference_grid(b.model, pose, arf.OccupancyConfig()), arf.RenderOptions())
+    hb = b.train(13)
+    assert np.array_equal(hb, ha)
+    for x, y in zip(a.model.params(), b.model.params()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("pipelined", [True, False])
+def test_nonfinite_loss_freezes_model_and_raises(gpu, pipelined):
+    """SPEC.md:494 abort on a non-finite loss: the guarded Adam skips the poisoned step and
+    every later one on the device, so the error (raised at the next check) leaves the model
+    at its last finite state -- parameters and Adam moments equal a clean run stopped there."""
+    from paper_2212_10550_b200 import NumericError
+    ref_tr = _det_trainer()
+    ref_tr.pipelined = pipelined
+    ref_tr.train(5)
+    ref_tr._sync()
+    tr = _det_trainer()
+    tr.pipelined = pipelined
+    tr.train(5)
+    gp, mp = tr.model.params()[:2]
+    tr.gt_rgb[:] = float("nan")  # poisons every later loss
+    with pytest.raises(NumericError, match="last finite state"):
+        tr.train(4)              # crosses the occupancy refresh at step 8 -> checked there
+    tr._sync()
+    for x, y in zip(ref_tr.model.params()[:2], tr.model.params()[:2]):
+        assert np.array_equal(x, y)
+    for x, y in zip(ref_tr.model.adam_state(), tr.model.adam_state()):
+        assert np.array_equal(x, y)

@@ -148,3 +148,31 @@ def test_header_is_plain_c(tmp_path):
         r = subprocess.run([cc, *flags, "-I", str(inc), "-c", str(src), "-o", str(tmp_path / f"{cc}.o")],
                            capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
+
+
+def test_reference_workload_matches_fixtures(ref):
+    """bench.py --impl reference builds its workload through the reference alone
+    (oracle/workload.py + ref_driver.cpp arfr_random_pose / arfr_default_camera); it must be
+    the product arm's workload bit for bit: skeleton, all 100 animation poses, the camera."""
+    from oracle import workload as wl
+    sk = fx.smpl24()
+    rsk = wl.smpl24()
+    assert [(b.parent, tuple(b.head), tuple(b.tail), b.radius) for b in sk.bones] == \
+        [(b.parent, tuple(b.head), tuple(b.tail), b.radius) for b in rsk.bones]
+    poses = fx.animation_poses(sk, 100)
+    rposes = wl.animation_poses(ref, rsk)
+    for p, q in zip(poses, rposes):
+        assert np.array_equal(p.bone_transforms.view(np.uint64), q.bone_transforms.view(np.uint64))
+        assert np.array_equal(p.global_transform.view(np.uint64), q.global_transform.view(np.uint64))
+    cam = fx.default_camera(sk, 540, 540)
+    rc = ref.default_camera(rsk, 540, 540)
+    assert (cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height) == (rc.fx, rc.fy, rc.cx, rc.cy, rc.width, rc.height)
+    assert np.array_equal(np.array(cam.extrinsic, np.float64).view(np.uint64),
+                          np.array(rc.extrinsic[:], np.float64).view(np.uint64))
+    g, m, o, r = fx.config1_grid(), fx.config1_mlp(), fx.config1_occupancy(), fx.config1_render_options()
+    rg, rmc, ro, rr = wl.GridConfig(), wl.MlpConfig(), wl.OccupancyConfig(), wl.RenderOptions()
+    assert (g.levels, g.features_per_level, g.table_size_log2, g.base_resolution, g.max_resolution) == \
+        (rg.levels, rg.features_per_level, rg.table_size_log2, rg.base_resolution, rg.max_resolution)
+    assert (m.input_dim, m.hidden_dim, m.hidden_layers, m.output_dim) == \
+        (rmc.input_dim, rmc.hidden_dim, rmc.hidden_layers, rmc.output_dim)
+    assert vars(o) == vars(ro) and vars(r) == vars(rr) and fx.CONFIG1_SEED == wl.SEED
