@@ -423,7 +423,7 @@ def run_ours(args):
         if world == 1 and not args.no_extra:
             line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
                                      "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline),
-                                     "train_step_full": bench_train_full(30)}
+                                     "train_step_full": bench_train_full(200)}
     if (world > 1 or args.force_dist_paths) and not args.no_dp_train:
         # config 5: data-parallel SPEC training over NCCL (reduce-scatter grads, sharded Adam,
         # all-gather params); also run at N = 1 under torchrun with --force-dist-paths

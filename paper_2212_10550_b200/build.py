@@ -16,9 +16,10 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 CSRC = HERE / "csrc"
-OBJ = ROOT / "build" / "obj"
-LIB = HERE / "lib"
-LIBNAME = LIB / "libarfx.so"
+# tuning variants (tools/build_variant.sh) build into their own object dir / library path
+OBJ = Path(os.environ.get("ARFX_BUILD_DIR", ROOT / "build" / "obj"))
+LIBNAME = Path(os.environ.get("ARFX_LIB_OUT", HERE / "lib" / "libarfx.so"))
+LIB = LIBNAME.parent
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

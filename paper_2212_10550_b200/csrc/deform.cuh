@@ -53,6 +53,14 @@ __device__ __forceinline__ void roots_push(Roots& R, d3 p, double res, double de
   }
 }
 
+#ifndef ARFX_DS_LD256
+#define ARFX_DS_LD256 1
+#endif
+// 32 bytes (4 doubles, 32-B aligned) through the read-only path in one 256-bit request
+__device__ __forceinline__ void ldg256(const double* p, double* o) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+}
+
 // Skinning weights at x (trilinear over the packed cell table + renormalisation),
 // then g = lbs(x) - x_target, |g| and J = sum_{w_i != 0} w_i R_i.
 // `ws` is per-thread scratch for the union bones' raw weights (smem, stride apart).
@@ -94,6 +102,17 @@ __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __res
   const int nu = __popc(mask);
   for (int j = 0; j < nu; j += 2) {
     const bool two = j + 1 < nu;
+#if ARFX_DS_LD256
+    // 256-bit loads (LDG.E.ENL2.256): a lane's 64-B bone row in two requests instead of four;
+    // scattered lanes cost one L1 data wavefront per line per request
+    double va[8], vb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    ldg256(vals + 8 * j, va);
+    ldg256(vals + 8 * j + 4, va + 4);
+    if (two) {
+      ldg256(vals + 8 * j + 8, vb);
+      ldg256(vals + 8 * j + 12, vb + 4);
+    }
+#else
     const double2* v2 = reinterpret_cast<const double2*>(vals + 8 * j);
     const double2 a0 = __ldg(v2 + 0), a1 = __ldg(v2 + 1), a2 = __ldg(v2 + 2), a3 = __ldg(v2 + 3);
     double2 b0 = make_double2(0, 0), b1 = b0, b2 = b0, b3 = b0;
@@ -105,6 +124,7 @@ __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __res
     }
     const double va[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
     const double vb[8] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x, b3.y};
+#endif
     // The reference skips corners with wt == 0 (R/skinning.hpp:45); adding the
     // product instead is bit-identical: wt * v = +-0 for finite v, acc starts at +0 and
     // x + (+-0) == x, (+0) + (-0) == +0 -- so the data-dependent branch (and its DSETP/FSEL
