@@ -6,7 +6,7 @@ at 540x540 with a per-frame occupancy refresh, on the config-1 avatar (24-bone s
 capsule skeleton, 16-level hash grid 2^19 x 2 f32, 32-64-64-4 MLP, 32^3 skinning grid,
 64^3 occupancy, N=128 midpoint samples, random init seed 1234). One step = one frame:
 build_model_inference_grid + render_model. With N GPUs each frame's rays are sharded
-over ranks in interleaved 16-row tiles (no data-path collective).
+over ranks in interleaved 4-row tiles (no data-path collective).
 
   value : frames/s with inputs resident in HBM (per-pose contexts pre-uploaded), device
           outputs; timed with CUDA events per frame, L2 flushed between frames.
@@ -39,6 +39,11 @@ WORKLOAD = ("100-frame novel-pose animation at 540x540, per-frame 64^3 occupancy
             "avatar, 16-level 2^19 hash grid, 32-64-64-4 MLP, N=128 (BASELINE configs[3] on configs[0]'s avatar)")
 W_IMG = H_IMG = 540
 N_FRAMES = 100
+ROW_TILE = 4  # libarfx kRowTile: ray shards = interleaved 4-row tiles
+
+
+def shard_rows(world: int, rank: int) -> int:
+    return sum(1 for y in range(H_IMG) if (y // ROW_TILE) % world == rank)
 
 
 def env_rank():
@@ -105,7 +110,7 @@ def bench_config(world: int) -> dict:
     """The `config` both arms print (identical by construction)."""
     return {"workload": WORKLOAD, "image": [W_IMG, H_IMG], "frames": N_FRAMES, "samples_per_ray": 128,
             "occupancy": "64^3, rebuilt per frame", "l2": "flushed between timed frames (256 MB write)",
-            "parallelism": f"rays sharded over {world} GPU(s) in interleaved 16-row tiles"}
+            "parallelism": f"rays sharded over {world} GPU(s) in interleaved {ROW_TILE}-row tiles"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -193,9 +198,10 @@ def run_ours(args):
     model.set_mlp_mode(args.mlp)
     arf.render_model(model, views[0], cam, occ, opt, rank, world)
 
-    # multi-GPU: each rank builds one z-slab of the per-pose occupancy grid, the slabs are
-    # all-gathered over NCCL (1 MiB of f32 values) and every rank re-thresholds / dilates
-    shard_grid = (world > 1 or args.force_dist_paths) and not args.no_shard_grid and occ_cfg.resolution % world == 0
+    # multi-GPU: each rank builds one cell-interleaved shard of the per-pose occupancy grid,
+    # the rank-major blocks are all-gathered over NCCL (1 MiB of f32 values) and every rank
+    # permutes them into cell order and re-thresholds / dilates
+    shard_grid = (world > 1 or args.force_dist_paths) and not args.no_shard_grid and occ_cfg.resolution ** 3 % world == 0
     if shard_grid:
         from paper_2212_10550_b200.trainer import device_view
         occ_vals = device_view(occ.device_arrays()[0], occ.cell_count())
@@ -208,7 +214,7 @@ def run_ours(args):
             check(L.arfx_build_inference_grid_shard_device(model._h, v._h, occ._h, rank, world,
                                                            C.c_void_p(d_cnt[slot, 0].data_ptr()), sp))
             dist.all_gather_into_tensor(occ_vals, my_slab)
-            check(L.arfx_occ_rebuild_mask_async(occ._h, sp))
+            check(L.arfx_occ_rebuild_mask_shards_async(occ._h, world, sp))
         else:
             check(L.arfx_build_inference_grid_device(model._h, v._h, occ._h,
                                                      C.c_void_p(d_cnt[slot, 0].data_ptr()), sp))
@@ -226,7 +232,7 @@ def run_ours(args):
         hs = []
         if args.no_graph:
             return hs
-        for pmask in ([2, 4 | 8] if shard_grid else [1 | 8]):
+        for pmask in ([2, 16 | 8] if shard_grid else [1 | 8]):
             h = C.c_void_p()
             check(L.arfx_frame_graph_create(model._h, gview._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
                                             pmask, C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
@@ -390,7 +396,8 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": DTYPE if args.mlp != "exact" else DTYPE_EXACT,
                 "data": "synthetic (random-init avatar, synthetic animation poses)",
                 "config": bench_config(world),
-                "multi_gpu": ("occupancy grid cell-interleaved shards + NCCL all-gather" if shard_grid else
+                "multi_gpu": ("occupancy grid cell-interleaved shards + NCCL all-gather of the rank-major blocks"
+                              if shard_grid else
                               ("occupancy grid built redundantly per rank" if world > 1 else "n/a (1 GPU)")),
                 "posed_samples_per_s": posed_all / (total_ms / 1000.0),
                 "rays_per_s": npix * K / (total_ms / 1000.0),
@@ -403,7 +410,7 @@ def run_ours(args):
                 "frame_launch": "cuda_graph (pose copied into the captured handle per frame)" if graphs else "direct",
                 "graph_recaptures_outside_timed_region": recaptures[0],
                 "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}
-        rays_rank = sum(1 for y in range(H_IMG) if (y // 16) % world == rank) * W_IMG
+        rays_rank = shard_rows(world, rank) * W_IMG
         dom, per_kernel = roofline(prof, stats, K, rays_rank, opt.samples_per_ray, posed, peaks, peak_kind,
                                    (p64.value, p32.value))
         line["roofline"] = dom
@@ -427,7 +434,7 @@ def run_ours(args):
     if (world > 1 or args.force_dist_paths) and not args.no_dp_train:
         # config 5: data-parallel SPEC training over NCCL (reduce-scatter grads, sharded Adam,
         # all-gather params); also run at N = 1 under torchrun with --force-dist-paths
-        dp = bench_train_full(20, rank, world, None)
+        dp = bench_train_full(50, rank, world, None, args.force_dist_paths)
         if rank == 0:
             line["extra_configs"] = {"train_step_dp": dp}
     if dist.is_initialized():
@@ -638,7 +645,7 @@ def run_e2e(args, model, poses, cam, opt, occ, rank, world, views):
         check(L.arfx_frame_graph_destroy(h))
     if int(h_cnt[:, 3].sum()):
         raise RuntimeError("e2e: workspace overflow in the graph frames")
-    rows = sum(1 for y in range(H_IMG) if (y // 16) % world == rank)
+    rows = shard_rows(world, rank)
     pose_ctx_bytes = 8 + 32 * (12 + 12 + 3 + 3 + 1) * 8 + 12 * 8 + 32 * 16  # sizeof(PoseCtx), kMaxBones 32
     async_value = K / dt
     graph_value = K / dt_graph
@@ -768,7 +775,7 @@ def bench_train(model, steps: int, with_cpu: bool):
     return out
 
 
-def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
+def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None, force_collectives: bool = False):
     """SPEC train_step at config 3 (config 5 when world > 1: 4096 rays per rank, weak scaling):
     rays + ground truth gathered on the device, forward + fused losses + backward
     (arfx_train_step_device), reduce-scatter / sharded Adam / all-gather of the flat vectors over
@@ -785,7 +792,7 @@ def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
     poses = [fx.random_pose(sk, 100 + i) for i in range(8)]
     cfg = TrainConfig(iterations=steps, rays_per_batch=4096 * world, samples_per_ray=128, occupancy_interval=16,
                       seed=9, adam=arf.AdamConfig(total_steps=1000))
-    tr = Trainer(model, fx.figure_for(sk), poses, cam, cfg, rank, world, group)
+    tr = Trainer(model, fx.figure_for(sk), poses, cam, cfg, rank, world, group, force_collectives)
     # warm-up through the first occupancy update too (its one-time workspace sizing is not
     # a per-step cost)
     for _ in range(cfg.occupancy_interval + 3):
@@ -808,7 +815,8 @@ def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None):
     h = np.array(tr.history)
     return {"workload": f"SPEC train_step, config {'5' if world > 1 else '3'}: 4096 rays/rank x {world} rank(s), "
                         "fwd + fused losses + bwd + Adam (+ occupancy update every 16 steps)"
-                        + (", grads reduce-scatter + params all-gather over NCCL" if world > 1 else ""),
+                        + (", grads reduce-scatter + params all-gather over NCCL on the Adam stream (pipelined)"
+                           if world > 1 or force_collectives else ""),
             "iters_per_s": steps / (ms / 1000.0), "ms_per_iter": ms / steps, "rays_per_s": 4096 * world * steps /
             (ms / 1000.0), "n_flat_params": tr.n_flat, "loss_first": h[0].tolist(), "loss_last": h[-1].tolist(),
             "posed_samples_per_iter_rank0": (model.counters.posed_queries - c0) / steps}
@@ -842,7 +850,7 @@ def main():
                     help="exercise the multi-GPU code paths (grid all-gather, DP train) at N = 1 under torchrun")
     ap.add_argument("--no-graph", action="store_true", help="launch each frame's kernels directly (no CUDA graph)")
     ap.add_argument("--no-shard-grid", action="store_true",
-                    help="N > 1: build the occupancy grid redundantly on every rank instead of z-slab shards")
+                    help="N > 1: build the occupancy grid redundantly on every rank instead of cell-interleaved shards")
     ap.add_argument("--no-dp-train", action="store_true",
                     help="N > 1: skip the data-parallel SPEC train step side measurement (config 5)")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2/3 side measurements")

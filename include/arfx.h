@@ -233,23 +233,28 @@ int arfx_build_inference_grid(arfx_model m, arfx_pose p, arfx_occ_grid g, arfx_c
 /* asynchronous variant: counters (u64 x4: posed, canonical, pool, overflow) to device memory */
 int arfx_build_inference_grid_device(arfx_model m, arfx_pose p, arfx_occ_grid g,
                                      uint64_t* d_counters, void* stream);
-/* Multi-GPU: the inference grid's cell values for z-slab `shard` of
- * `n_shards` only (slices [res*shard/n, res*(shard+1)/n)); all-gather the values across ranks
- * (arfx_occ_device_arrays: z-major, so slabs are contiguous) and then rebuild the mask with
- * arfx_occ_rebuild_mask_async. Per-cell values are bit-identical to the full build. */
+/* Multi-GPU: the inference grid's cell values for shard `shard` of
+ * `n_shards` only -- the cell-interleaved cells c = shard + n_shards*j (j < cells/n_shards;
+ * res^3 must divide by n_shards), written as the rank-major block values[shard*cells/n + j].
+ * All-gather the blocks in place across ranks (arfx_occ_device_arrays), then
+ * arfx_occ_rebuild_mask_shards_async permutes them into cell order and rebuilds the mask.
+ * Per-cell values are bit-identical to the full build. */
 int arfx_build_inference_grid_shard_device(arfx_model m, arfx_pose p, arfx_occ_grid g, int shard, int n_shards,
                                            uint64_t* d_counters, void* stream);
 /* device pointers of the occupancy values [z][y][x] f32 and mask u8 */
 int arfx_occ_device_arrays(arfx_occ_grid g, float** values, uint8_t** mask);
 /* threshold + dilation of the current values, asynchronous on stream */
 int arfx_occ_rebuild_mask_async(arfx_occ_grid g, void* stream);
+/* values hold n_shards rank-major shard blocks (arfx_build_inference_grid_shard_device, then
+ * an all-gather): permute them into [z][y][x] cell order, then threshold + dilation. */
+int arfx_occ_rebuild_mask_shards_async(arfx_occ_grid g, int n_shards, void* stream);
 int arfx_update_training_grid(arfx_model m, const arfx_pose* poses, int n_poses, double decay,
                               uint64_t seed, uint64_t step, arfx_occ_grid g, arfx_counters* c,
                               void* stream);
 
 /* ---- render ------------------------------------------------------------- */
 /* Host buffers: rgb[H*W*3], alpha[H*W] (arf::RenderImages layout R/render.hpp:167-171).
- * occ may be NULL (no skipping). row_shard/n_shards select interleaved 16-row tiles
+ * occ may be NULL (no skipping). row_shard/n_shards select interleaved 4-row tiles
  * (tile % n_shards == row_shard) for multi-GPU sharding; use 0/1 for a full frame --
  * rows of other shards are left untouched. */
 int arfx_render_model(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
@@ -422,7 +427,13 @@ int arfx_model_set_adam(arfx_model m, const float* adam_m, const float* adam_v);
 
 /* ---- CUDA-graph frames ---------------------------------------------------------------- */
 
-enum { ARFX_GRAPH_GRID = 1, ARFX_GRAPH_GRID_SHARD = 2, ARFX_GRAPH_MASK = 4, ARFX_GRAPH_RENDER = 8 };
+enum {
+  ARFX_GRAPH_GRID = 1,
+  ARFX_GRAPH_GRID_SHARD = 2,
+  ARFX_GRAPH_MASK = 4,
+  ARFX_GRAPH_RENDER = 8,
+  ARFX_GRAPH_MASK_SHARDS = 16 /* as arfx_occ_rebuild_mask_shards_async(occ, nshards) */
+};
 /* Captures the chosen parts of one frame for pose handle p as a CUDA graph: the inference
  * grid (GRID) or its z-slab shard (GRID_SHARD), the mask rebuild (MASK), the render into
  * device buffers (RENDER). d_counters [2][4] (grid, render: posed, canonical, pool, overflow)

@@ -134,6 +134,7 @@ _PROTOS = {
     "arfx_build_inference_grid_shard_device": (C.c_int, [H, H, H, C.c_int, C.c_int, P, P]),
     "arfx_occ_device_arrays": (C.c_int, [H, C.POINTER(P), C.POINTER(P)]),
     "arfx_occ_rebuild_mask_async": (C.c_int, [H, P]),
+    "arfx_occ_rebuild_mask_shards_async": (C.c_int, [H, C.c_int, P]),
     "arfx_occ_is_occupied": (C.c_int, [H, c_double_p, C.c_int64, c_uint8_p]),
     "arfx_stats_enable": (C.c_int, [H, C.c_int]),
     "arfx_stats_read": (C.c_int, [H, c_uint64_p]),

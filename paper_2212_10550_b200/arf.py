@@ -534,9 +534,15 @@ def build_model_inference_grid(model: Model, pose: SkeletonPose, cfg: OccupancyC
 
 def build_inference_grid_shard(model: Model, view: "PosedModelView", grid: OccupancyGrid, shard: int,
                                n_shards: int, stream=None) -> None:
-    """Cell values of z-slab `shard` of `n_shards` (multi-GPU: all-gather the values, then
-    grid.rebuild_mask()); asynchronous on `stream` (NULL: the library stream)."""
+    """Cell values of shard `shard` of `n_shards` (cells c = shard + n_shards * j, written as the
+    rank-major block values[shard * cells / n_shards + j]); multi-GPU: all-gather the blocks,
+    then occ_rebuild_mask_shards(). Asynchronous on `stream` (NULL: the library stream)."""
     call("arfx_build_inference_grid_shard_device", model._h, view._h, grid._h, shard, n_shards, None, stream)
+
+
+def occ_rebuild_mask_shards(grid: OccupancyGrid, n_shards: int, stream=None) -> None:
+    """Rank-major shard blocks -> cell order, then threshold + dilation (asynchronous)."""
+    call("arfx_occ_rebuild_mask_shards_async", grid._h, n_shards, stream)
 
 
 def update_training_grid(model: Model, grid: OccupancyGrid, poses: Sequence[SkeletonPose], decay: float,
@@ -847,10 +853,27 @@ def figure_render(fig: CapsuleFigure, pose: SkeletonPose, normalized_box: Aabb, 
     return out, mask
 
 
-def shard_rows(height: int, rank: int, world: int, tile: int = 16) -> list:
+ROW_TILE = 4  # kRowTile (arfx_internal.h)
+
+
+def shard_rows(height: int, rank: int, world: int, tile: int = ROW_TILE) -> list:
     """Rows rendered by `rank` of `world`: interleaved `tile`-row tiles (tile % world == rank),
     the same partition libarfx applies for arfx_render_model(..., rank, world, ...)."""
     return [y for y in range(height) if (y // tile) % world == rank]
+
+
+def shard_cells(n_cells: int, rank: int, world: int) -> np.ndarray:
+    """Occupancy cells computed by `rank` of `world` (arfx_build_inference_grid_shard_device):
+    c = rank + world * j, stored as the rank-major block [rank * n_cells / world + j]."""
+    if n_cells % world:
+        raise L.InvalidArgument(1, "build_inference_grid_shard: the cell count must divide by n_shards")
+    return np.arange(rank, n_cells, world, dtype=np.int64)
+
+
+def unshard_cells(blocks: np.ndarray, world: int) -> np.ndarray:
+    """Rank-major shard blocks (after the all-gather) -> cell order (occ_unshard_kernel)."""
+    b = np.asarray(blocks).reshape(world, -1)
+    return b.T.reshape(-1).copy()
 
 
 def device_count() -> int:

@@ -932,6 +932,16 @@ int arfx_occ_rebuild_mask_async(arfx_occ_grid gh, void* stream) {
   });
 }
 
+int arfx_occ_rebuild_mask_shards_async(arfx_occ_grid gh, int n_shards, void* stream) {
+  return guard([&] {
+    require(n_shards >= 1, "occ_rebuild_mask_shards: n_shards >= 1");
+    OccImpl& g = occ_ref(gh);
+    ARFX_CUDA(cudaSetDevice(g.device));
+    occ_unshard(g, n_shards, static_cast<cudaStream_t>(stream));
+    occ_rebuild(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses, double decay,
                               uint64_t seed, uint64_t step, arfx_occ_grid gh, arfx_counters* c, void* stream) {
   return guard([&] {
@@ -1007,10 +1017,12 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
                             float* d_alpha, uint64_t* d_counters, void* stream, arfx_frame_graph* out) {
   return guard([&] {
     require(mh && ph && out, "frame_graph_create: null argument");
-    require(parts > 0 && (parts & ~(ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK | ARFX_GRAPH_RENDER)) == 0,
+    require(parts > 0 && (parts & ~(ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK | ARFX_GRAPH_RENDER |
+                                    ARFX_GRAPH_MASK_SHARDS)) == 0,
             "frame_graph_create: bad parts");
+    require(!((parts & ARFX_GRAPH_MASK) && (parts & ARFX_GRAPH_MASK_SHARDS)), "frame_graph_create: mask or shard mask");
     require(!((parts & ARFX_GRAPH_GRID) && (parts & ARFX_GRAPH_GRID_SHARD)), "frame_graph_create: grid or shard");
-    require(!(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK)) || occ,
+    require(!(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK | ARFX_GRAPH_MASK_SHARDS)) || occ,
             "frame_graph_create: the grid parts need an occupancy grid");
     require(!(parts & ARFX_GRAPH_RENDER) || (d_rgb && d_alpha && opt), "frame_graph_create: render outputs");
     require(d_counters != nullptr || !(parts & (ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_RENDER)),
@@ -1030,6 +1042,10 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
       if (parts & ARFX_GRAPH_GRID) inference_grid(m, ph->impl, occ->impl, cnt, s);
       if (parts & ARFX_GRAPH_GRID_SHARD) inference_grid_shard(m, ph->impl, occ->impl, shard, nshards, cnt, s);
       if (parts & ARFX_GRAPH_MASK) occ_rebuild(occ->impl, s);
+      if (parts & ARFX_GRAPH_MASK_SHARDS) {
+        occ_unshard(occ->impl, nshards, s);
+        occ_rebuild(occ->impl, s);
+      }
       if (parts & ARFX_GRAPH_RENDER)
         render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
                      opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha,

@@ -16,6 +16,9 @@ namespace arfx {
 
 constexpr int kMaxBones = 32;   // R/articulation.hpp:10
 constexpr int kMaxRoots = 8;    // R/articulation.hpp:11
+// multi-GPU ray shards: interleaved tiles of kRowTile image rows (tile % n_shards == shard);
+// 4-row tiles keep the per-rank ray counts within one tile (<1 % at 540 rows / 8 ranks)
+constexpr int kRowTile = 4;
 constexpr int kMaxLevels = 32;
 constexpr int kMaxMlpLayers = 9;  // hidden_layers <= 8 (R/mlp.hpp:17) + output layer
 

@@ -243,6 +243,7 @@ void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d
                     cudaStream_t s);
 void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int n_shards,
                           unsigned long long* d_counters, cudaStream_t s);
+void occ_unshard(OccImpl& g, int n_shards, cudaStream_t s);
 void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,
                           uint64_t seed, uint64_t step, OccImpl& g, unsigned long long* d_counters,
                           cudaStream_t s);

@@ -13,7 +13,7 @@
 //                       field_tile_kernel, or the tcgen05 decoder (field_tc.cu) for renders.
 //   K4 composite_kernel max-density root selection (R/articulation.hpp:174) then
 //                       composite (R/render.hpp:98-119), one thread per ray.
-//   K5 occupancy        build_inference_grid (full or z-slab shard) / update_training_grid /
+//   K5 occupancy        build_inference_grid (full or cell-interleaved shard) / update_training_grid /
 //                       rebuild_mask / dilated_mask (R/occupancy.hpp:87-171) reuse K2 + K3.
 //   L_density           density_points / reduce / flag kernels + K2/K3/K8.
 #include <cuda_runtime.h>
@@ -430,14 +430,19 @@ struct AosSrc {  // user batch of xyz triples (inverse_lbs API / microbench)
 
 struct CellSrc {  // cell centres of an occupancy grid  R/occupancy.hpp:53-58, :141-144
   static constexpr bool kSinglePose = true;
-  int rx, ry, rz;       // rz: z-slices of this (possibly sharded) range
+  int rx, ry, rz;
   double lo[3], cs[3];
-  int z0 = 0;           // first z-slice (multi-GPU z-slab shard)
-  __device__ long long count() const { return static_cast<long long>(rx) * ry * rz; }
+  // multi-GPU shard: cells c = offset + stride * i (cell-interleaved, so every rank gets an
+  // equal share of the body's cells whatever its shape); 0 / 1 for the whole grid
+  int offset = 0, stride = 1;
+  __device__ long long count() const {
+    return (static_cast<long long>(rx) * ry * rz - offset + stride - 1) / stride;
+  }
   __device__ d3 point(long long i, int& pose) const {
     pose = 0;
-    const int ix = static_cast<int>(i % rx), iy = static_cast<int>((i / rx) % ry),
-              iz = z0 + static_cast<int>(i / (static_cast<long long>(rx) * ry));
+    const long long c = offset + static_cast<long long>(stride) * i;
+    const int ix = static_cast<int>(c % rx), iy = static_cast<int>((c / rx) % ry),
+              iz = static_cast<int>(c / (static_cast<long long>(rx) * ry));
     return make3(dadd(lo[0], dmul(dadd(static_cast<double>(ix), 0.5), cs[0])),
                  dadd(lo[1], dmul(dadd(static_cast<double>(iy), 0.5), cs[1])),
                  dadd(lo[2], dmul(dadd(static_cast<double>(iz), 0.5), cs[2])));
@@ -1109,12 +1114,12 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
                   int nshards, float* d_rgb, float* d_alpha, unsigned long long* d_counters,
                   cudaStream_t s) {
   Workspace& w = m.ws();
-  // rows of this shard: interleaved 16-row tiles
+  // rows of this shard: interleaved kRowTile-row tiles
   if (w.last_shard != shard || w.last_nshards != nshards || w.last_rows != cam.height ||
       w.last_w != cam.width) {
     std::vector<int32_t> rows;
     for (int y = 0; y < cam.height; ++y)
-      if ((y / 16) % nshards == shard) rows.push_back(y);
+      if ((y / kRowTile) % nshards == shard) rows.push_back(y);
     w.row_list.alloc(rows.size() + 1);
     if (!rows.empty())
       ARFX_CUDA(cudaMemcpyAsync(w.row_list.ptr, rows.data(), rows.size() * sizeof(int32_t),
@@ -1324,32 +1329,56 @@ void inference_grid(ModelImpl& m, PoseImpl& p, OccImpl& g, unsigned long long* d
                               cudaMemcpyDeviceToDevice, s));
 }
 
-// z-slab shard of the inference grid (multi-GPU): cell values for slices
-// [z0, z1) only; the caller all-gathers the values (z-major layout: slabs are contiguous)
-// and rebuilds the mask (threshold + dilation) on the full grid. Bit-identical per cell.
+// Cell-interleaved shard of the inference grid (multi-GPU): shard s of n
+// computes the cells c = s + n*j, j < cells/n, into values[s*cells/n + j] (rank-major shard
+// blocks, so an in-place all-gather of the blocks assembles the grid); occ_unshard then
+// permutes the blocks into cell order before the mask rebuild. Interleaving balances the
+// ranks (the body is thin in normalized z: contiguous z-slabs left most ranks idle).
+// Bit-identical per cell to the full build.
 void inference_grid_shard(ModelImpl& m, PoseImpl& p, OccImpl& g, int shard, int n_shards,
                           unsigned long long* d_counters, cudaStream_t s) {
   Workspace& w = m.ws();
-  const int z0 = static_cast<int>(static_cast<long long>(g.res) * shard / n_shards);
-  const int z1 = static_cast<int>(static_cast<long long>(g.res) * (shard + 1) / n_shards);
-  const long long plane = static_cast<long long>(g.res) * g.res;
-  const long long n = plane * (z1 - z0);
+  const long long cells = static_cast<long long>(g.res) * g.res * g.res;
+  if (cells % n_shards != 0)
+    throw std::invalid_argument("build_inference_grid_shard: the cell count must divide by n_shards");
+  const long long n = cells / n_shards;
   w.ensure(static_cast<size_t>(std::max<long long>(n, 1)), 0);
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   if (n > 0) {
-    CellSrc src{g.res, g.res, z1 - z0, {}, {}, z0};
+    CellSrc src{g.res, g.res, g.res, {}, {}, shard, n_shards};
     occ_source_common(g, src.lo, src.cs);
     launch_deform(m, p.dev.ptr, src, n, s);
     launch_field_pool(m, s, n);
     m.prof.begin("occ_values+mask", s);
     occ_values_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, w.snroot.ptr, w.sbase.ptr, w.pres.ptr,
-                                                         g.values.ptr + plane * z0, 1.0f, 0);
+                                                         g.values.ptr + n * shard, 1.0f, 0);
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
   }
   if (d_counters)
     ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToDevice, s));
+}
+
+__global__ void occ_unshard_kernel(const float* __restrict__ blocks, float* __restrict__ out, long long cells,
+                                   int n_shards) {
+  const long long per = cells / n_shards;
+  for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < cells;
+       c += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[c] = blocks[(c % n_shards) * per + c / n_shards];
+}
+
+// rank-major shard blocks (after the all-gather) -> cell order, in place via the grid's
+// scratch buffer
+void occ_unshard(OccImpl& g, int n_shards, cudaStream_t s) {
+  if (n_shards <= 1) return;
+  const long long cells = static_cast<long long>(g.res) * g.res * g.res;
+  if (cells % n_shards != 0) throw std::invalid_argument("occ_unshard: the cell count must divide by n_shards");
+  g.saved.ensure(static_cast<size_t>(cells));
+  occ_unshard_kernel<<<grid_for(cells, 256, 8), 256, 0, s>>>(g.values.ptr, g.saved.ptr, cells, n_shards);
+  ARFX_CUDA(cudaGetLastError());
+  ARFX_CUDA(cudaMemcpyAsync(g.values.ptr, g.saved.ptr, static_cast<size_t>(cells) * sizeof(float),
+                            cudaMemcpyDeviceToDevice, s));
 }
 
 void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, double decay,

@@ -67,9 +67,12 @@ class FlatDataParallel:
     its own). With world == 1 it is just optimizer(0, n). Backends without reduce-scatter
     (gloo, used by the CPU tests) fall back to all-reduce + slicing, same result."""
 
-    def __init__(self, params, grads, n_flat: int, rank: int = 0, world: int = 1, group=None):
+    def __init__(self, params, grads, n_flat: int, rank: int = 0, world: int = 1, group=None,
+                 force_collectives: bool = False):
         self.params, self.grads, self.n = params, grads, int(n_flat)
         self.rank, self.world, self.group = rank, world, group
+        # run the collectives even at world == 1 (exercises the multi-GPU path on one GPU)
+        self.collect = world > 1 or force_collectives
         if self.n % (4 * world):
             raise ValueError("flat vector length must split into multiple-of-4 shards")
         self.chunk = self.n // world
@@ -80,7 +83,7 @@ class FlatDataParallel:
 
     def step(self, optimizer) -> None:
         b, e = self.shard()
-        if self.world > 1:
+        if self.collect:
             import torch.distributed as dist
             backend = dist.get_backend(self.group)
             if backend == "nccl":
@@ -89,7 +92,7 @@ class FlatDataParallel:
                 dist.all_reduce(self.grads, op=dist.ReduceOp.SUM, group=self.group)
                 self.grads.div_(self.world)
         optimizer(b, e)
-        if self.world > 1:
+        if self.collect:
             import torch.distributed as dist
             if dist.get_backend(self.group) == "nccl":
                 dist.all_gather_into_tensor(self.params, self.params[b:e], group=self.group)
@@ -119,7 +122,7 @@ class Trainer:
     """SPEC train_step loop on one GPU per rank (world from torch.distributed when initialised)."""
 
     def __init__(self, model: arf.Model, figure: arf.CapsuleFigure, poses, camera: arf.Camera, cfg: TrainConfig,
-                 rank: int = 0, world: int = 1, group=None):
+                 rank: int = 0, world: int = 1, group=None, force_collectives: bool = False):
         import torch
         self.torch = torch
         self.model, self.figure, self.poses, self.camera, self.cfg = model, figure, list(poses), camera, cfg
@@ -144,7 +147,7 @@ class Trainer:
         self.n_flat = fl["n_flat"]
         self.params = device_view(fl["params"], self.n_flat)
         self.grads = device_view(fl["grads"], self.n_flat)
-        self.dp = FlatDataParallel(self.params, self.grads, self.n_flat, rank, world, group)
+        self.dp = FlatDataParallel(self.params, self.grads, self.n_flat, rank, world, group, force_collectives)
         # one non-default stream carries every step: libarfx launches, torch copies/gathers and
         # the NCCL collectives are then ordered without host synchronisation
         self.stream = torch.cuda.Stream()
@@ -158,13 +161,15 @@ class Trainer:
         arf.update_training_grid(model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, 0)
         self.step_id = 0
         self.fused_density = True  # arfx_train_density_step_device (False: the two calls in sequence)
-        # single rank: Adam on its own stream behind a parameter fence (overlaps the next step)
-        self.adam_stream = torch.cuda.Stream() if world == 1 else None
+        # Adam on its own stream behind a parameter fence (overlaps the next step); with several
+        # ranks the gradient reduce-scatter / parameter all-gather run on that stream too
+        self.adam_stream = torch.cuda.Stream()
         self.ev_params = torch.cuda.Event()
         self._fence_set = False
-        # single rank: step t+1's forward (march, deformer, field) is enqueued on fstream into
-        # the other train slot right after step t's backward, so the two overlap on the GPU
-        self.pipelined = world == 1
+        # step t+1's forward (march, deformer, field) is enqueued on fstream into the other
+        # train slot right after step t's backward (and, with several ranks, beside step t's
+        # collectives), so they overlap on the GPU
+        self.pipelined = True
         self.fstream = torch.cuda.Stream()
         self.pxs = [torch.zeros(self.n_local, dtype=torch.int32, device="cuda") for _ in range(2)]
         self.pys = [torch.zeros(self.n_local, dtype=torch.int32, device="cuda") for _ in range(2)]
@@ -253,9 +258,22 @@ class Trainer:
         self.ev_bwd[k].record(self.stream)
         t1 = t + 1
         self.adam_stream.wait_event(self.ev_bwd[k])  # this step's gradients are complete
-        L.call("arfx_adam_step_guarded", self.model._h, C.byref(self._adam_c), t1, 0, self.n_flat,
-               C.c_void_p(row.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()),
-               C.c_void_p(self.adam_stream.cuda_stream))
+        asp = C.c_void_p(self.adam_stream.cuda_stream)
+        if self.dp.collect:
+            # reduce-scatter(AVG) grads -> guarded Adam on this rank's shard -> all-gather params,
+            # on the Adam stream (torch orders the NCCL work after it); the guard is the sum of
+            # the ranks' loss rows, so every rank skips a non-finite step together
+            import torch.distributed as dist
+            with self.torch.cuda.stream(self.adam_stream):
+                guard = row.clone()
+                dist.all_reduce(guard, op=dist.ReduceOp.SUM, group=self.dp.group)
+                if self.cfg.deterministic:
+                    self.model.flush_grads(asp)  # the reduce-scatter reads the gradient array directly
+                gd = (C.c_void_p(guard.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()))
+                self.dp.step(lambda b, e: self.model.adam_step(self.cfg.adam, t1, b, e, asp, gd))
+        else:
+            L.call("arfx_adam_step_guarded", self.model._h, C.byref(self._adam_c), t1, 0, self.n_flat,
+                   C.c_void_p(row.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()), asp)
         self.ev_params.record(self.adam_stream)
         if not self._fence_set:
             self.model.set_param_fence(self.ev_params.cuda_event)
@@ -311,15 +329,15 @@ class Trainer:
         loss[4:6].copy_(self.loss_d)
         self._hist.append(loss)
         guard = loss
-        if self.world > 1:
+        if self.dp.collect:
             # every rank must skip together: the guard is the sum of the ranks' loss rows
             import torch.distributed as dist
             guard = loss.clone()
             dist.all_reduce(guard, op=dist.ReduceOp.SUM, group=self.dp.group)
         gd = (C.c_void_p(guard.data_ptr()), 6, C.c_void_p(self.bad.data_ptr()))
-        if cfg.deterministic and self.world > 1:
+        if cfg.deterministic and self.dp.collect:
             self.model.flush_grads(sp)  # the reduce-scatter reads the gradient array directly
-        if self.adam_stream is not None:
+        if not self.dp.collect:
             # Adam of step t on its own stream, fenced: the next step's march and deformer
             # (which read neither parameters nor gradients) run beside it, its field kernels
             # wait on ev_params (arfx_model_set_param_fence)

@@ -333,9 +333,10 @@ def test_render_tcgen05_decoder(gpu, ref, structured, mode):
 
 
 @pytest.mark.parametrize("n_shards", [2, 4, 8])
-def test_inference_grid_z_slab_shards(gpu, n_shards):
-    """Multi-GPU occupancy: the z-slab shards, written into one grid and re-thresholded,
-    equal the single-GPU build bit for bit (values and mask)."""
+def test_inference_grid_interleaved_shards(gpu, n_shards):
+    """Multi-GPU occupancy: the cell-interleaved shards, written as rank-major blocks into one
+    grid (what the in-place all-gather assembles), permuted and re-thresholded, equal the
+    single-GPU build bit for bit (values and mask); every shard holds a share of the body."""
     import ctypes as C
     from paper_2212_10550_b200._lib import call
     sk = fx.smpl24()
@@ -349,12 +350,17 @@ def test_inference_grid_z_slab_shards(gpu, n_shards):
     sp = C.c_void_p(st.cuda_stream)
     for s in range(n_shards):
         arf.build_inference_grid_shard(m, view, part, s, n_shards, sp)
-    call("arfx_occ_rebuild_mask_async", part._h, sp)
+    st.synchronize()
+    blocks = part.download()[0].reshape(n_shards, -1)
+    arf.occ_rebuild_mask_shards(part, n_shards, sp)
     st.synchronize()
     fv, fm = full.download()
     pv, pm = part.download()
     assert np.array_equal(fv.view(np.uint32), pv.view(np.uint32))
     assert np.array_equal(fm, pm) and fm.sum() > 0
+    assert np.array_equal(blocks.view(np.uint32), fv.reshape(-1, n_shards).T.view(np.uint32))
+    busy = (blocks > 0).sum(axis=1)  # cells with density per shard: balanced by interleaving
+    assert busy.min() >= 0.8 * busy.max(), busy
 
 
 def test_frame_graph_replays_updated_poses(gpu):
@@ -406,7 +412,7 @@ def test_thread_per_ray_march_matches_warp_march(gpu, stratified):
     """K1 has two pass-1 forms: thread per ray for full-warp launches (>= ~150 k rays, the
     animation frames) and warp per ray for smaller batches (verified sample for sample
     against the reference above). A 480x420 frame takes the first; each of its two
-    16-row-tile shards (~100 k rays) takes the second: images and posed-sample counts must
+    4-row-tile shards (~100 k rays) takes the second: images and posed-sample counts must
     be identical."""
     sk = fx.smpl24()
     m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)

@@ -463,3 +463,31 @@ def test_nonfinite_loss_freezes_model_and_raises(gpu, pipelined):
         assert np.array_equal(x, y)
     for x, y in zip(ref_tr.model.adam_state(), tr.model.adam_state()):
         assert np.array_equal(x, y)
+
+
+def test_pipelined_data_parallel_path_on_one_gpu(gpu):
+    """The multi-GPU training path (pipelined trainer + reduce-scatter(AVG) / guarded sharded
+    Adam / all-gather over NCCL on the Adam stream) run on one GPU with the collectives
+    forced: bit-identical to the single-rank trainer in deterministic mode (a 1-rank AVG
+    reduce-scatter and all-gather are exact copies)."""
+    import socket
+    import torch.distributed as dist
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        a = _det_trainer()
+        ha = a.train(20)
+        b = _det_trainer()
+        from paper_2212_10550_b200.trainer import FlatDataParallel
+        b.dp = FlatDataParallel(b.params, b.grads, b.n_flat, 0, 1, None, force_collectives=True)
+        assert b.pipelined and b.dp.collect
+        hb = b.train(20)
+        assert np.array_equal(ha, hb)
+        for x, y in zip(a.model.params(), b.model.params()):
+            assert np.array_equal(x, y)
+        for x, y in zip(a.model.adam_state(), b.model.adam_state()):
+            assert np.array_equal(x, y)
+    finally:
+        dist.destroy_process_group()
