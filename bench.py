@@ -431,6 +431,15 @@ def run_ours(args):
             line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
                                      "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline),
                                      "train_step_full": bench_train_full(200)}
+            rk, seq_ms, counts = bench_train_roofline(48, peaks, peak_kind, (p64.value, p32.value))
+            tsf = line["extra_configs"]["train_step_full"]
+            tsf["roofline_kernels"] = rk
+            tsf["roofline_run"] = {"ms_per_step_sequential": seq_ms, "work_counts": counts,
+                                   "note": "kernels timed one stream, no cross-step overlap; ms_per_iter above "
+                                           "is the pipelined step"}
+            if os.environ.get("ARFX_ROOFLINE_MD"):
+                with open(os.environ["ARFX_ROOFLINE_MD"], "a") as fh:
+                    fh.write("\n## SPEC train step (config 3), sequential\n\n" + roofline_table(rk))
     if (world > 1 or args.force_dist_paths) and not args.no_dp_train:
         # config 5: data-parallel SPEC training over NCCL (reduce-scatter grads, sharded Adam,
         # all-gather params); also run at N = 1 under torchrun with --force-dist-paths
@@ -820,6 +829,84 @@ def bench_train_full(steps: int, rank: int = 0, world: int = 1, group=None, forc
             "iters_per_s": steps / (ms / 1000.0), "ms_per_iter": ms / steps, "rays_per_s": 4096 * world * steps /
             (ms / 1000.0), "n_flat_params": tr.n_flat, "loss_first": h[0].tolist(), "loss_last": h[-1].tolist(),
             "posed_samples_per_iter_rank0": (model.counters.posed_queries - c0) / steps}
+
+
+def bench_train_roofline(steps: int, peaks, peak_kind, pipe):
+    """Per-kernel roofline of the SPEC train step (config 3): the step run sequentially on one
+    stream (no cross-step pipelining, density step unfused) so each kernel group's CUDA-event
+    time is its own; algorithmic work from the deterministic device counters of the same steps
+    (DESIGN.md §4). Returns {kernel: roofline entry} and the sequential ms/step."""
+    import torch
+    from paper_2212_10550_b200 import arf, fixtures as fx
+    from paper_2212_10550_b200._lib import check, lib
+    from paper_2212_10550_b200.trainer import Trainer, TrainConfig
+    L = lib()
+    sk = fx.smpl24()
+    model = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    cam = fx.default_camera(sk, W_IMG, H_IMG)
+    poses = [fx.random_pose(sk, 100 + i) for i in range(8)]
+    cfg = TrainConfig(iterations=steps, rays_per_batch=4096, samples_per_ray=128, occupancy_interval=16,
+                      seed=9, adam=arf.AdamConfig(total_steps=1000))
+    tr = Trainer(model, fx.figure_for(sk), poses, cam, cfg)
+    tr.pipelined = False
+    tr.fused_density = False
+    for _ in range(cfg.occupancy_interval + 3):
+        tr.step()
+    torch.cuda.synchronize()
+    check(L.arfx_profile_enable(model._h, 1))
+    _ = read_profile(model, L)
+    check(L.arfx_stats_enable(model._h, 1))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(tr.stream)
+    for _ in range(steps):
+        tr.step()
+    e1.record(tr.stream)
+    torch.cuda.synchronize()
+    prof = read_profile(model, L)
+    stats = np.zeros(16, np.uint64)
+    check(L.arfx_stats_read(model._h, stats.ctypes.data_as(C.POINTER(C.c_uint64))))
+    check(L.arfx_stats_enable(model._h, 0))
+    check(L.arfx_profile_enable(model._h, 0))
+    tr.close()
+    E, U, I, S, P, Q, _, B, PS, R, NP = (float(x) for x in stats[:11])
+    fp64_peak, fp32_peak = pipe
+    hbm = peaks.get("hbm_gbs")
+    f64src = "fp64 add/mul issue roof measured by bench.py (arfx_pipe_peaks; not in MEASURED_PEAKS.json)"
+    f32src = "fp32 add/mul issue roof measured by bench.py (arfx_pipe_peaks)"
+    hsrc = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"
+    n_upd = sum(1 for t in range(cfg.occupancy_interval + 3, cfg.occupancy_interval + 3 + steps)
+                if (t + 1) % cfg.occupancy_interval == 0)
+    targets = PS + steps * cfg.density_points + n_upd * 64 ** 3
+    out = {}
+
+    def entry(name, bound, work, unit, peak, src, note):
+        if name not in prof:
+            return
+        ms, n = prof[name]
+        ach = work / (ms * 1e-3) / (1e12 if unit == "TFLOP/s" else 1e9)
+        out[name] = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                     "frac": ach / peak if peak else None, "ms_per_launch": ms / max(n, 1), "launches": n,
+                     "ms_per_step": ms / steps, "work_per_launch": work / max(n, 1), "peak_source": src, "work": note}
+
+    entry("march", "fp64", R * (80 + 36 * 128), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64 (all 128 samples)")
+    entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
+    entry("deform", "fp64", 41 * E + 60 * U + 66 * I + 18 * S + 7 * max(E - S - I, 0.0), "TFLOP/s", fp64_peak, f64src,
+          "FP64 add/mul/div/sqrt of inverse_lbs_ctx as written (no FMA)")
+    entry("finalize", "hbm", 32.0 * S + 36.0 * Q + 9.0 * targets, "GB/s", hbm, hsrc,
+          "32 B/start + 36 B/pool entry + 9 B/target")
+    entry("field", "fp32", 13312.0 * Q, "TFLOP/s", fp32_peak, f32src, "exact f32 encode + MLP, 13312 flops/query")
+    entry("train_composite", "hbm", 56.0 * PS + 40.0 * R, "GB/s", hbm, hsrc,
+          "56 B/posed sample (field result, delta, index, root slot, transmittance, dsigma/dcolor) + 40 B/ray")
+    entry("bwd_list", "hbm", 5.0 * Q + 4.0 * B, "GB/s", hbm, hsrc, "1 B flag + 4 B per pool entry, 4 B per list entry")
+    entry("bwd_field", "fp32", 13056.0 * B, "TFLOP/s", fp32_peak, f32src,
+          "MLP dX chain 12800 + encode-backward weights 256 f32 flops per backward query")
+    entry("bwd_weights", "fp32", 13064.0 * B, "TFLOP/s", fp32_peak, f32src, "dW + db: 2 x 6532 f32 flops per query")
+    entry("bwd_scatter", "l2 atomics", 1024.0 * B, "GB/s", hbm, hsrc + "; L2 atomics, vs HBM for scale",
+          "16 levels x 8 corners x float2 atomic (8 B) per query")
+    entry("adam", "hbm", 32.0 * NP, "GB/s", hbm, hsrc, "p, g, m, v read + p, m, v, g written: 32 B/param")
+    return out, e0.elapsed_time(e1) / steps, {"evals": int(E), "starts": int(S), "field_queries": int(Q),
+                                              "backward_queries": int(B), "posed_samples": int(PS), "rays": int(R),
+                                              "adam_params": int(NP), "steps": steps}
 
 
 def cpu_baseline():

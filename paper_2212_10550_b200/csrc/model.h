@@ -328,7 +328,9 @@ constexpr long long kTeamMaxQueries = 65536;
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
                          const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own,
                          const float* act = nullptr);
-void flush_grad_acc(ModelImpl& m, cudaStream_t s);  // deterministic mode: grid_acc -> grid_grad
+void flush_grad_acc(ModelImpl& m, cudaStream_t s);
+// roofline accounting: m.stats[i] += *d_src + add (when arfx_stats_enable is on)
+void stat_add(ModelImpl& m, int i, const unsigned long long* d_src, unsigned long long add, cudaStream_t s);  // deterministic mode: grid_acc -> grid_grad
 
 // field_tc.cu
 bool field_tc_supported(const FieldView& F);

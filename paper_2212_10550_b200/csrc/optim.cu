@@ -127,6 +127,7 @@ void adam_step(ModelImpl& m, const AdamCfg& c, long long step, long long begin, 
   }
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
+  stat_add(m, 10, nullptr, static_cast<unsigned long long>(end - begin), s);  // parameters updated
 }
 
 }  // namespace arfx

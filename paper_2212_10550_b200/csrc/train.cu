@@ -671,7 +671,18 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __rest
 
 int sms() { return device_sm_count(); }
 
+// roofline accounting (arfx_stats_*): stats[i] += *src (device count) + add
+__global__ void stat_add_kernel(unsigned long long* stats, int i, const unsigned long long* src, unsigned long long add) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) stats[i] += (src ? *src : 0ull) + add;
+}
+
 }  // namespace
+
+void stat_add(ModelImpl& m, int i, const unsigned long long* d_src, unsigned long long add, cudaStream_t s) {
+  if (!m.stats_on) return;
+  stat_add_kernel<<<1, 32, 0, s>>>(m.stats.ptr, i, d_src, add);
+  ARFX_CUDA(cudaGetLastError());
+}
 
 void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long cap, const uint8_t* flag,
                          const float* gs, const float* gc, cudaStream_t s, const BwdOwners* own, const float* act) {
@@ -684,7 +695,7 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   w.bwd_n.ensure(1);
   ARFX_CUDA(cudaMemsetAsync(w.bwd_n.ptr, 0, sizeof(unsigned long long), s));
   m.wait_params(s);
-  m.prof.begin("field_backward", s);
+  m.prof.begin("bwd_list", s);
   if (m.det && own) {
     w.bwd_own.ensure(static_cast<size_t>(std::max<long long>(own->n_owner, 1)));
     OwnerRanges O{own->n_owner, own->first, own->count, own->pool_is_target};
@@ -698,15 +709,19 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
                                                                                          static_cast<long long>(sms()) * 8))),
                        256, 0, s>>>(flag, d_n, cap, w.bwd_list.ptr, w.bwd_n.ptr);
   }
+  m.prof.end(s);
+  stat_add(m, 7, w.bwd_n.ptr, 0, s);  // backward queries
   const size_t team_smem = (static_cast<size_t>(kHid) * kW0s + kHid * kW1s + kOut * kW1s + 2 * kHid + kOut +
                             static_cast<size_t>(kTeams) * kTQ * kTeamSmem) * sizeof(float);
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
   const int bwd_per_sm =  // persistent: exactly the resident blocks (one wave)
       blocks_per_sm(reinterpret_cast<const void*>(field_bwd_team_kernel), kTeamThreads, team_smem);
+  m.prof.begin("bwd_field", s);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * std::max(bwd_per_sm, 1)), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr, act,
       d_n);
   ARFX_CUDA(cudaGetLastError());
+  m.prof.end(s);
   // K8b + K8d (MLP weights, smem/FP32) run on the aux stream beside K8c (hash-grid
   // scatter, L2 atomics); both only read the K8a records. The join keeps the next
   // gradient writer on `s` ordered after K8d's non-atomic mlp_grad update.
@@ -719,11 +734,14 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
   ARFX_CUDA(cudaEventRecord(m.ev_aux_fork, s));
   ARFX_CUDA(cudaStreamWaitEvent(m.aux, m.ev_aux_fork, 0));
+  m.prof.begin("bwd_weights", m.aux);
   field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, m.aux>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
                                                                                   w.bwd_partial.ptr);
   weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, m.aux>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
   ARFX_CUDA(cudaGetLastError());
+  m.prof.end(m.aux);
   ARFX_CUDA(cudaEventRecord(m.ev_aux_join, m.aux));
+  m.prof.begin("bwd_scatter", s);
   if (m.det) {
     const size_t n_acc = static_cast<size_t>(m.fv.L) * m.fv.T * 2;  // == n_grid
     if (m.grid_acc.n < n_acc) {  // zeroed once; consumers leave it all-zero
@@ -738,9 +756,9 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
     grid_scatter_kernel<false><<<resident_grid(grid_scatter_kernel<false>, 256, 0, 1LL << 40), 256, 0, s>>>(
         m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, w.bwd_rec.ptr, m.grid_grad.ptr, nullptr);
   }
+  m.prof.end(s);
   ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_aux_join, 0));
   ARFX_CUDA(cudaGetLastError());
-  m.prof.end(s);
 }
 
 void flush_grad_acc(ModelImpl& m, cudaStream_t s) {
@@ -775,6 +793,8 @@ void train_composite(ModelImpl& m, long long n_rays, int N, double eps, const fl
   train_composite_warp_kernel<<<static_cast<unsigned>(std::max<long long>(1, (n_rays + 3) / 4)), 128, 0, s>>>(A);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
+  stat_add(m, 8, w.counters.ptr, 0, s);                                   // composited posed samples
+  stat_add(m, 9, nullptr, static_cast<unsigned long long>(n_rays), s);   // rays
 }
 
 namespace {
