@@ -174,6 +174,14 @@ int arfx_model_set_params(arfx_model m, const float* grid_params, const float* m
  * occupancy grids, training and the query APIs always use the exact decoder. */
 enum { ARFX_MLP_EXACT = 0, ARFX_MLP_TCGEN05 = 1, ARFX_MLP_TCGEN05_FP16 = 2 };
 int arfx_model_set_mlp_mode(arfx_model m, int mode);
+/* MLP part of the training backward (query_backward R/field.hpp:91-103, R/mlp.hpp:116-154):
+ * ARFX_BWD_TCGEN05 (default) = dX = delta . W and dW = sum delta^T . [inputs | 1] as split-bf16
+ * tcgen05.mma with f32 accumulation in TMEM (gradients within 1e-4 relative of the reference,
+ * DESIGN.md §5); ARFX_BWD_SIMT = f32 SIMT in the reference's summation order. The tcgen05
+ * path needs the forward's saved activations (batches of <= 65,536 field queries); larger
+ * batches use the SIMT path. Deterministic either way under arfx_model_set_deterministic. */
+enum { ARFX_BWD_SIMT = 0, ARFX_BWD_TCGEN05 = 1 };
+int arfx_model_set_backward_mode(arfx_model m, int mode);
 /* Deterministic gradients (default off): the field backward visits the flagged queries in
  * owner order (rays front to back / points) instead of atomic-compaction order, so the f32
  * MLP weight-gradient sums are fixed, and the hash-grid scatter sums fixed-point int64

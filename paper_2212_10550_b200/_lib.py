@@ -109,6 +109,7 @@ _PROTOS = {
     "arfx_model_get_params": (C.c_int, [H, c_float_p, c_float_p, c_double_p]),
     "arfx_model_set_params": (C.c_int, [H, c_float_p, c_float_p]),
     "arfx_model_set_mlp_mode": (C.c_int, [H, C.c_int]),
+    "arfx_model_set_backward_mode": (C.c_int, [H, C.c_int]),
     "arfx_model_set_deterministic": (C.c_int, [H, C.c_int]),
     "arfx_model_flush_grads": (C.c_int, [H, C.c_void_p]),
     "arfx_model_set_param_fence": (C.c_int, [H, C.c_void_p]),

@@ -256,6 +256,11 @@ class Model:
         Render only."""
         call("arfx_model_set_mlp_mode", self._h, {"exact": 0, "tcgen05": 1, "tcgen05_fp16": 2}[mode])
 
+    def set_backward_mode(self, mode: str) -> None:
+        """Training MLP backward: 'tcgen05' (default; split-bf16 tensor-core dX / dW with f32
+        accumulation) or 'simt' (f32, the reference's summation order)."""
+        call("arfx_model_set_backward_mode", self._h, {"simt": 0, "tcgen05": 1}[mode])
+
     def set_deterministic(self, on: bool = True) -> None:
         """Bit-reproducible gradients (arfx_model_set_deterministic): owner-ordered backward
         lists and fixed-point int64 hash-grid sums, so repeated train / density steps on the

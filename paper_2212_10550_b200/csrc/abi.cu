@@ -614,6 +614,14 @@ int arfx_model_set_mlp_mode(arfx_model mh, int mode) {
   });
 }
 
+int arfx_model_set_backward_mode(arfx_model mh, int mode) {
+  return guard([&] {
+    require(mh != nullptr, "set_backward_mode: null model");
+    require(mode == ARFX_BWD_SIMT || mode == ARFX_BWD_TCGEN05, "set_backward_mode: unknown mode");
+    mh->impl.bwd_tc = mode == ARFX_BWD_TCGEN05;
+  });
+}
+
 int arfx_model_set_deterministic(arfx_model mh, int on) {
   return guard([&] {
     require(mh != nullptr, "set_deterministic: null model");

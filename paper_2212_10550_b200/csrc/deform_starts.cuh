@@ -106,9 +106,16 @@ __global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restri
   }
 }
 
+// Sort-key cell grid: the skinning cells coarsened by 2^shift per axis (small batches use a
+// coarser key space so the key histogram / scan stay proportional to the work).
+struct KeyGrid {
+  int shift, cx, cy, cz;  // coarse dims
+  __host__ __device__ int cells() const { return cx * cy * cz; }
+};
+
 // Approximate (f32) skinning cell of a point: only a sort key for locality, never used
 // in the arithmetic (skin_eval recomputes the exact cell in FP64).
-__device__ __forceinline__ int approx_skin_cell(const SkinView& S, d3 x) {
+__device__ __forceinline__ int approx_skin_cell(const SkinView& S, d3 x, const KeyGrid& kg) {
   const float p[3] = {static_cast<float>(x.x), static_cast<float>(x.y), static_cast<float>(x.z)};
   const int res[3] = {S.rx, S.ry, S.rz};
   int c[3];
@@ -117,22 +124,23 @@ __device__ __forceinline__ int approx_skin_cell(const SkinView& S, d3 x) {
     const float lo = static_cast<float>(S.lo[a]), e = static_cast<float>(S.e[a]);
     float u = (p[a] - lo) / e * static_cast<float>(res[a] - 1);
     u = fminf(fmaxf(u, 0.0f), static_cast<float>(res[a] - 2));
-    c[a] = static_cast<int>(u);
+    c[a] = static_cast<int>(u) >> kg.shift;
   }
-  return (c[2] * (S.ry - 1) + c[1]) * (S.rx - 1) + c[0];
+  return (c[2] * kg.cy + c[1]) * kg.cx + c[0];
 }
 
 // K2b (counting sort by (bone, skinning cell of the start point x0 = B_b^-1 x')):
 // pass 1 -- per target, per surviving bone: key, unsorted item, key histogram.
 template <class Src, bool kSinglePose>
-__global__ void __launch_bounds__(256) start_key_kernel(SkinView S, const PoseCtx* __restrict__ poses, Src src,
+__global__ void __launch_bounds__(256) start_key_kernel(SkinView S, KeyGrid kg, const PoseCtx* __restrict__ poses,
+                                                        Src src,
                                                         const uint32_t* __restrict__ mask_in,
                                                         const uint32_t* __restrict__ slot_base,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ unsorted,
                                                         uint32_t* __restrict__ key_hist, long long cap) {
   extern __shared__ double sk_smem[];
   const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sk_smem);
-  const int ncell = (S.rx - 1) * (S.ry - 1) * (S.rz - 1);
+  const int ncell = kg.cells();
   const long long n = src.count();
   for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
        s += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -144,7 +152,7 @@ __global__ void __launch_bounds__(256) start_key_kernel(SkinView S, const PoseCt
     long long slot = slot_base[s];
     for (uint32_t m = mask; m; m &= m - 1, ++slot) {
       const int b = __ffs(m) - 1;
-      const uint32_t key = static_cast<uint32_t>(b * ncell + approx_skin_cell(S, rigid_apply(P->bone_inv[b], xt)));
+      const uint32_t key = static_cast<uint32_t>(b * ncell + approx_skin_cell(S, rigid_apply(P->bone_inv[b], xt), kg));
       if (slot < cap) {
         keys[slot] = key;
         unsorted[slot] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);

@@ -141,6 +141,7 @@ struct ModelImpl {
   // [2] Newton steps [3] starts [4] exact prune tests [5] field queries
   bool stats_on = false;
   DevBuf<unsigned long long> stats;
+  bool bwd_tc = true;  // training MLP backward on tcgen05 (arfx_model_set_backward_mode)
   int mlp_mode = 0;  // render decoder: 0 exact f32 SIMT (bit-faithful sums), 1 tcgen05 split-bf16 (3-term,
                      // f32 accumulate), 2 = 1 with fp16 hash-table gathers
   DevBuf<__half2> grid_h2;  // fp16 copy of the hash table (mode 2), refreshed per render

@@ -924,9 +924,19 @@ void launch_finalize(ModelImpl& m, const Src& src, const RootsSink& K, long long
 
 // K2 = K2a start masks -> scan -> K2b bone-major scatter -> K2c Newton -> K2d finalize
 // (deform_starts.cuh). Counters: [4] item cursor, [6] total starts, [7] items.
+// sort-key grid for ~`expect` live targets: the skinning cells coarsened until the key
+// count is <= 3x the expected targets (full resolution for frames and occupancy grids)
+KeyGrid key_grid(const SkinView& S, long long expect) {
+  KeyGrid kg{};
+  for (int sh = 0;; ++sh) {
+    kg = KeyGrid{sh, ((S.rx - 2) >> sh) + 1, ((S.ry - 2) >> sh) + 1, ((S.rz - 2) >> sh) + 1};
+    if (static_cast<long long>(S.nb) * kg.cells() <= 3 * std::max<long long>(expect, 1) || sh >= 5) return kg;
+  }
+}
+
 template <class Src, class Sink>
 void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, const Sink& K, long long n_hint,
-                        const char* name, cudaStream_t s) {
+                        const char* name, cudaStream_t s, long long expect = -1) {
   Workspace& w = m.ws();
   constexpr bool single = Src::kSinglePose;
   const long long n = std::max<long long>(n_hint, 1);
@@ -936,12 +946,12 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   // the batched inverse_lbs API runs asynchronously and cannot re-run: size its start slots
   // for the worst case (every bone survives pruning); render/occupancy learn from overflow
   const size_t worst = std::is_same<Sink, RootsSink>::value ? static_cast<size_t>(n) * m.sv.nb : 0;
-  w.ensure_starts(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1),
-                  worst);
+  const KeyGrid kg = key_grid(m.sv, expect >= 0 ? expect : n);
+  w.ensure_starts(static_cast<size_t>(n), static_cast<size_t>(m.sv.nb) * kg.cells(), worst);
   const size_t pose_smem = single ? (sizeof(PoseCtx) + 7) / 8 * 8 : 0;
   unsigned long long* C = w.counters.ptr;
   unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
-  const long long nkeys = static_cast<long long>(m.sv.nb) * (m.sv.rx - 1) * (m.sv.ry - 1) * (m.sv.rz - 1);
+  const long long nkeys = static_cast<long long>(m.sv.nb) * kg.cells();
   const long long cap = static_cast<long long>(w.cap_starts);
   ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
   ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
@@ -960,7 +970,7 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   // counting sort of the starts by (bone, skinning cell of x0)
   start_key_kernel<Src, single><<<resident_grid(start_key_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
                                   s>>>(
-      m.sv, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
+      m.sv, kg, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
   const long long nbk = (nkeys + kScanBlock - 1) / kScanBlock;
   scan_blocks_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
   scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 8, C + 9);
@@ -988,11 +998,11 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
 // K2 feeding the root pool.
 template <class Src>
 void launch_deform(ModelImpl& m, const PoseCtx* d_poses, const Src& src, long long n_hint,
-                   cudaStream_t s) {
+                   cudaStream_t s, long long expect = -1) {
   Workspace& w = m.ws();
   PoolSink K{w.snroot.ptr, w.sbase.ptr, w.px.ptr, w.py.ptr, w.pz.ptr, w.powner.ptr,
              w.counters.ptr, static_cast<long long>(w.cap_pool), m.fv};
-  launch_deform_sink(m, d_poses, src, K, n_hint, "deform", s);
+  launch_deform_sink(m, d_poses, src, K, n_hint, "deform", s, expect);
 }
 
 // allow_tc: the render may use the tcgen05 decoder (arfx_model_set_mlp_mode); occupancy
@@ -1253,7 +1263,8 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
     m.prof.end(s);
   }
   ListSrc src{w.sx.ptr, w.sy.ptr, w.sz.ptr, w.counters.ptr, 0, static_cast<long long>(w.cap_posed)};
-  launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s);
+  // training rays: ~13 posed samples per ray size the sort keys
+  launch_deform(m, p.dev.ptr, src, static_cast<long long>(w.cap_posed), s, 16LL * n_rays);
   w.fwd_act.ensure(static_cast<size_t>(kTeamMaxQueries) * kActStride);
   launch_field_pool(m, s, static_cast<long long>(w.cap_pool), false, ARFX_SAVE_ACT ? w.fwd_act.ptr : nullptr);
   finalize_counters_kernel<<<1, 1, 0, s>>>(w.counters.ptr, static_cast<long long>(w.cap_posed));

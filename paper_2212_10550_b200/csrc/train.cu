@@ -27,6 +27,7 @@
 #include "fixed.cuh"
 #include "losses.cuh"
 #include "model.h"
+#include "umma.cuh"
 
 namespace arfx {
 namespace {
@@ -266,7 +267,10 @@ __global__ void __launch_bounds__(kTeamThreads) field_bwd_team_kernel(FieldView 
                                                                       float* __restrict__ grid_grad,
                                                                       float* __restrict__ rec,
                                                                       const float* __restrict__ act,
-                                                                      const unsigned long long* pool_n) {
+                                                                      const unsigned long long* pool_n,
+                                                                      bool tc_active) {
+  // the tensor-core backward (field_bwd_tc_kernel) takes every launch with saved activations
+  if (tc_active && act != nullptr && static_cast<long long>(*pool_n) <= kTeamMaxQueries) return;
   extern __shared__ float bw_smem[];
   float* W0p = bw_smem;                    // [64][33]
   float* W1p = W0p + kHid * kW0s;          // [64][65]
@@ -600,10 +604,18 @@ __global__ void __launch_bounds__(1024) owner_scan_kernel(uint32_t* __restrict__
 constexpr int kWq = 32;
 constexpr int kWThreads = 256;
 constexpr int kNParams = kHid * kIn + kHid + kHid * kHid + kHid + kOut * kHid + kOut;  // 6,532
+constexpr long long kWMin = 128;
+__host__ __device__ __forceinline__ long long wblocks_used(long long n, long long grid) {
+  const long long want = (n + kWMin - 1) / kWMin;
+  return want < 1 ? 1 : (want < grid ? want : grid);
+}
+
 __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const float* __restrict__ rec,
                                                                       const unsigned long long* n_rec,
                                                                       long long rec_cap,
-                                                                      float* __restrict__ partial) {
+                                                                      float* __restrict__ partial,
+                                                                      const unsigned long long* tc_pool_n) {
+  if (tc_pool_n && static_cast<long long>(*tc_pool_n) <= kTeamMaxQueries) return;  // K8-TC wrote the rows
   __shared__ float S[kWq][kRecStride + 1];
   long long n = static_cast<long long>(*n_rec);
   n = n < rec_cap ? n : rec_cap;
@@ -625,10 +637,14 @@ __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const floa
     dOff[j] = d;
     iOff[j] = in;
   }
+  // blocks in use: one per kWMin queries (at most the grid) -- small batches write and reduce
+  // only that many partial rows; the split depends on n alone (deterministic)
+  const long long used = wblocks_used(n, gridDim.x);
+  if (blockIdx.x >= used) return;
   float acc[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) acc[j] = 0.0f;
-  for (long long c0 = static_cast<long long>(blockIdx.x) * kWq; c0 < n; c0 += static_cast<long long>(gridDim.x) * kWq) {
+  for (long long c0 = static_cast<long long>(blockIdx.x) * kWq; c0 < n; c0 += used * kWq) {
     const int nq = static_cast<int>(n - c0 < kWq ? n - c0 : kWq);
     __syncthreads();
     const float* src = rec + c0 * kRecStride;
@@ -652,9 +668,15 @@ __global__ void __launch_bounds__(kWThreads) field_bwd_weights_kernel(const floa
 // K8d: mlp_grad[p] += sum over blocks of partial[b][p]: a block takes 32 parameters, its 8
 // warps sum interleaved row subsets (coalesced 128-B rows), then a fixed-order combine --
 // deterministic, no atomics
-__global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __restrict__ partial, int n_blocks,
-                                                             float* __restrict__ mlp_grad) {
+__global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __restrict__ partial, int grid,
+                                                             const unsigned long long* n_rec, long long rec_cap,
+                                                             float* __restrict__ mlp_grad,
+                                                             const unsigned long long* tc_pool_n, int tc_grid) {
   __shared__ float part[8][32];
+  long long nr = static_cast<long long>(*n_rec);
+  nr = nr < rec_cap ? nr : rec_cap;
+  const bool tc = tc_pool_n && static_cast<long long>(*tc_pool_n) <= kTeamMaxQueries;
+  const int n_blocks = tc ? tc_grid : static_cast<int>(wblocks_used(nr, grid));
   const int pi = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int p = blockIdx.x * 32 + pi;
   float a = 0.0f;
@@ -667,6 +689,293 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float* __rest
     for (int k = 1; k < 8; ++k) t = fadd(t, part[k][pi]);
     mlp_grad[p] = fadd(mlp_grad[p], t);
   }
+}
+
+// ---- K8-TC: the MLP backward on the 5th-gen tensor cores (split-bf16, f32 accumulate) ----
+//
+// One persistent 128-thread CTA per SM; a tile = 128 consecutive entries of the backward
+// list, thread r = row r. Per tile, from the forward's saved activations (X | H1 | H2 |
+// logits, bit-identical to a recompute) and the upstream dsigma / dcolor:
+//   u2  = d logits (R/field.hpp:95-99)                                SIMT, as K8a
+//   d2  = ReLU'(H2) * (u2 . W2)  (R/mlp.hpp:130-150, u != 0 only)     SIMT (K = 4), as K8a
+//   dH1 = d2 . W1          D[128 x 64]  = A[q][o] B[i][o]             tcgen05, TMEM cols [0, 64)
+//   d1  = ReLU'(H1) * dH1
+//   dX  = d1 . W0          D[128 x 32]                                tcgen05, TMEM cols [64, 96)
+//   [dW1 | db1 ; dW0 | db0] += [d2^T ; d1^T] . [H1 | X | 1]           tcgen05, K = the tile's
+//                          128 queries, accumulated over all of the CTA's tiles in TMEM
+//                          cols [128, 240) (rows 0-63: d2^T, rows 64-127: d1^T)
+//   dW2, db2 += u2^T . H2 (4 x 64 + 4)                                SIMT over smem, fixed order
+// dX goes to the record's d-feature slot for the hash-grid scatter (K8c); each CTA writes
+// its MLP-gradient partial row, summed in fixed order by weights_reduce (deterministic).
+// Products are hi*hi + hi*lo + lo*hi of bf16 halves (~16 significant bits); the tolerance
+// vs the reference's serial f32 sums is the gradient parity bar.
+namespace bwdtc {
+using namespace umma;
+constexpr int kT = 128;   // queries per tile (rows of the MMAs)
+constexpr int kThreads = 4 * kT;  // 4 threads per row: column parts
+constexpr int kNW = 112;  // weight-grad B rows: H1^T (64) | X^T (32) | ones (1) | zero pad
+constexpr int kWB1T = 0;                                   // B for dH1: (n=i 64, k=o 64), 2 planes
+constexpr int kW1P = kHid * kHid * 2;
+constexpr int kWB0T = kWB1T + 2 * kW1P;                    // B for dX: (n=i 32, k=o 64)
+constexpr int kW0P = kIn * kHid * 2;
+constexpr int kAD = kWB0T + 2 * kW0P;                      // A for dH1 / dX: (m=q 128, k=o 64)
+constexpr int kADP = kT * kHid * 2;
+constexpr int kAW = kAD + 2 * kADP;                        // A for the weight grads: (m=128, k=q 128)
+constexpr int kAWP = kT * kT * 2;
+constexpr int kBW = kAW + 2 * kAWP;                        // B for the weight grads: (n=112, k=q 128)
+constexpr int kBWP = kNW * kT * 2;
+constexpr int kW2F = kBW + 2 * kBWP;                       // W2 f32 [4][64]
+constexpr int kH2F = kW2F + kOut * kHid * 4;               // H2 f32 [128][65]
+constexpr int kU2F = kH2F + kT * (kHid + 1) * 4;           // u2 f32 [128][4]
+constexpr int kBAR = kU2F + kT * kOut * 4;                 // mbarrier
+constexpr int kTADDR = kBAR + 8;
+constexpr int kSmem = kTADDR + 8;
+constexpr uint32_t kTmemCols = 256;
+constexpr int kColDH1 = 0, kColDX = 64, kColW = 128;
+constexpr int kColOnes = 96;  // B_w row of ones -> bias gradients
+
+__device__ __forceinline__ void put_split(unsigned char* base, int plane, int off, float x) {
+  __nv_bfloat16 hi, lo;
+  split_bf16(x, hi, lo);
+  *reinterpret_cast<__nv_bfloat16*>(base + off) = hi;
+  *reinterpret_cast<__nv_bfloat16*>(base + off + plane) = lo;
+}
+
+// row r, k = [c, c + 8) of a K-major split operand with R rows
+__device__ __forceinline__ void put_row8(unsigned char* base, int plane, int R, int r, int c, const float* x) {
+  __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) split_bf16(x[j], hi[j], lo[j]);
+  *reinterpret_cast<uint4*>(base + kmaj_off(r, c, R)) = *reinterpret_cast<const uint4*>(hi);
+  *reinterpret_cast<uint4*>(base + plane + kmaj_off(r, c, R)) = *reinterpret_cast<const uint4*>(lo);
+}
+}  // namespace bwdtc
+
+__global__ void __launch_bounds__(bwdtc::kThreads, 1) field_bwd_tc_kernel(FieldView F, const int32_t* __restrict__ list,
+                                                                        const unsigned long long* n_list,
+                                                                        const float* __restrict__ pgs,
+                                                                        const float* __restrict__ pgc,
+                                                                        const float* __restrict__ act,
+                                                                        const unsigned long long* pool_n,
+                                                                        float* __restrict__ rec,
+                                                                        float* __restrict__ partial) {
+  using namespace bwdtc;
+  if (static_cast<long long>(*pool_n) > kTeamMaxQueries) return;  // no saved activations: K8a/K8b run
+  extern __shared__ __align__(1024) unsigned char bt_smem[];
+  // 4 threads per tile row: r = row (the TMEM lane of warp quadrant warp % 4), p = column part
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int r = (warp & 3) * 32 + (tid & 31), p = warp >> 2;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(bt_smem));
+  const uint32_t mbar = sbase + kBAR;
+  float* W2f = reinterpret_cast<float*>(bt_smem + kW2F);
+  float* H2f = reinterpret_cast<float*>(bt_smem + kH2F);
+  float* U2f = reinterpret_cast<float*>(bt_smem + kU2F);
+  const long long n = static_cast<long long>(*n_list);
+  // ---- weights: B operands (W1^T, W0^T: element (n = i, k = o) = W[o][i]), W2 in f32 ----
+  const float* W0 = F.mlp;
+  const float* W1 = W0 + kIn * kHid + kHid;
+  const float* W2 = W1 + kHid * kHid + kHid;
+  {  // all weight loads in flight before the first conversion (one L2 round trip)
+    constexpr int n1 = kHid * kHid / kThreads, n0 = kHid * kIn / kThreads;
+    float w1[n1], w0[n0], w2 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < n1; ++j) w1[j] = __ldg(W1 + tid + j * kThreads);
+#pragma unroll
+    for (int j = 0; j < n0; ++j) w0[j] = __ldg(W0 + tid + j * kThreads);
+    if (tid < kOut * kHid) w2 = __ldg(W2 + tid);
+#pragma unroll
+    for (int j = 0; j < n1; ++j) {
+      const int e = tid + j * kThreads, o = e / kHid, i = e % kHid;
+      put_split(bt_smem + kWB1T, kW1P, kmaj_off(i, o, kHid), w1[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < n0; ++j) {
+      const int e = tid + j * kThreads, o = e / kIn, i = e % kIn;
+      put_split(bt_smem + kWB0T, kW0P, kmaj_off(i, o, kIn), w0[j]);
+    }
+    if (tid < kOut * kHid) W2f[tid] = w2;
+  }
+  // B_w rows 96..111 (ones row for the bias gradients, zero padding) are constant
+  for (int e = tid; e < (kNW - kColOnes) * kT; e += kThreads) {
+    const int nrow = kColOnes + e / kT, k = e % kT;
+    put_split(bt_smem + kBW, kBWP, kmaj_off(nrow, k, kNW), nrow == kColOnes ? 1.0f : 0.0f);
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbase + kTADDR),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<uint32_t*>(bt_smem + kTADDR);
+  const uint32_t trow = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  uint32_t phase = 0;
+  float acc2 = 0.0f;  // dW2 (tid < 256: o = tid / 64, i = tid % 64) or db2 (256 <= tid < 260)
+  bool any = false;
+  for (long long k0 = static_cast<long long>(blockIdx.x) * kT; k0 < n; k0 += static_cast<long long>(gridDim.x) * kT) {
+    const long long k = k0 + r;
+    const bool live = k < n;
+    // ---- row r, column part p: saved activations, u2, d2 (SIMT, K8a's expressions) ----
+    const float4* A4 = nullptr;
+    float u2[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (live) {
+      const long long q = list[k];
+      const float* A = act + q * kActStride;
+      A4 = reinterpret_cast<const float4*>(A);
+      const float4 lg = A4[(kIn + 2 * kHid) / 4];
+      const float a[kOut] = {lg.x, lg.y, lg.z, lg.w};
+      u2[0] = fmul(pgs[q], logistic_f(a[0]));
+#pragma unroll
+      for (int o = 1; o < kOut; ++o) {
+        const float v = logistic_f(a[o]);
+        u2[o] = fmul(fmul(pgc[3 * q + o - 1], v), __fsub_rn(1.0f, v));
+      }
+    }
+    if (p == 0) {
+#pragma unroll
+      for (int o = 0; o < kOut; ++o) U2f[r * kOut + o] = u2[o];
+    }
+    {  // X columns [8p, 8p + 8) -> B_w rows 64 + i
+      float x[8];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const float4 t = live ? A4[2 * p + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * v] = t.x, x[4 * v + 1] = t.y, x[4 * v + 2] = t.z, x[4 * v + 3] = t.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) put_split(bt_smem + kBW, kBWP, kmaj_off(kHid + 8 * p + j, r, kNW), x[j]);
+    }
+    {  // H1 columns [16p, 16p + 16) -> B_w rows i
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float4 t = live ? A4[(kIn + 16 * p) / 4 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float h[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) put_split(bt_smem + kBW, kBWP, kmaj_off(16 * p + 4 * v + j, r, kNW), h[j]);
+      }
+    }
+    {  // H2 / d2 columns [16p, 16p + 16)
+      float d2[16];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float4 t = live ? A4[(kIn + kHid + 16 * p) / 4 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float h[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = 16 * p + 4 * v + j;
+          float d = 0.0f;
+#pragma unroll
+          for (int o = 0; o < kOut; ++o)
+            if (u2[o] != 0.0f) d = fadd(d, fmul(u2[o], W2f[o * kHid + i]));
+          d2[4 * v + j] = (h[j] == 0.0f) ? 0.0f : d;
+          H2f[r * (kHid + 1) + i] = h[j];
+          put_split(bt_smem + kAW, kAWP, kmaj_off(i, r, kT), d2[4 * v + j]);  // A_w rows 0-63: d2^T
+        }
+      }
+      put_row8(bt_smem + kAD, kADP, kT, r, 16 * p, d2);  // A for dH1: row r
+      put_row8(bt_smem + kAD, kADP, kT, r, 16 * p + 8, d2 + 8);
+    }
+    tc_fence_before();
+    fence_async_smem();
+    __syncthreads();
+    // ---- dH1 = d2 . W1 ----
+    if (tid == 0) {
+      tc_fence_after();
+      mma_split(tmem + kColDH1, sbase + kAD, kADP, kT, sbase + kWB1T, kW1P, kHid, kHid, idesc_bf16(kT, kHid));
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {  // d1 = ReLU'(H1) * dH1 on columns [16p, 16p + 16) (the mask from the exact H1)
+      float v[16];
+      tmem_ld16(trow + kColDH1 + 16 * p, v);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const float4 t = live ? A4[(kIn + 16 * p) / 4 + q4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float h[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = 4 * q4 + j;
+          v[c] = (h[j] == 0.0f) ? 0.0f : v[c];
+          put_split(bt_smem + kAW, kAWP, kmaj_off(kHid + 16 * p + c, r, kT), v[c]);  // A_w rows 64-127: d1^T
+        }
+      }
+      tc_fence_before();
+      __syncthreads();  // every part has read its dH1 columns before A_d is overwritten
+      put_row8(bt_smem + kAD, kADP, kT, r, 16 * p, v);
+      put_row8(bt_smem + kAD, kADP, kT, r, 16 * p + 8, v + 8);
+    }
+    tc_fence_before();
+    fence_async_smem();
+    __syncthreads();
+    // ---- dX = d1 . W0 ; [dW1 | db1 ; dW0 | db0] += A_w . B_w ----
+    if (tid == 0) {
+      tc_fence_after();
+      mma_split(tmem + kColDX, sbase + kAD, kADP, kT, sbase + kWB0T, kW0P, kIn, kHid, idesc_bf16(kT, kIn));
+      mma_split(tmem + kColW, sbase + kAW, kAWP, kT, sbase + kBW, kBWP, kNW, kT, idesc_bf16(kT, kNW), any);
+      mma_commit(mbar);
+    }
+    any = true;
+    {  // dW2 / db2 (SIMT, fixed order over the tile's rows) while the MMAs run
+      const int nq = static_cast<int>(n - k0 < kT ? n - k0 : kT);
+      float sum = 0.0f;
+      if (tid < kOut * kHid) {
+        const int o = tid / kHid, i = tid % kHid;
+        for (int j = 0; j < nq; ++j) sum = fadd(sum, fmul(U2f[j * kOut + o], H2f[j * (kHid + 1) + i]));
+      } else if (tid < kOut * kHid + kOut) {
+        for (int j = 0; j < nq; ++j) sum = fadd(sum, U2f[j * kOut + tid - kOut * kHid]);
+      }
+      acc2 = fadd(acc2, sum);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    if (p < 2) {  // dX columns [16p, 16p + 16) -> the record's d-feature slot (K8c)
+      float v[16];
+      tmem_ld16(trow + kColDX + 16 * p, v);
+      if (live) {
+        float4* R = reinterpret_cast<float4*>(rec + k * kRecStride + kRecDin + 16 * p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) R[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // smem operands and the dH1 / dX columns are reused by the next tile
+  }
+  // ---- this CTA's partial MLP-gradient row (parameter layout R/mlp.hpp:40-48) ----
+  constexpr int pW0 = 0, pB0 = kHid * kIn, pW1 = pB0 + kHid, pB1 = pW1 + kHid * kHid, pW2 = pB1 + kHid,
+                pB2 = pW2 + kOut * kHid;
+  float* row = partial + static_cast<size_t>(blockIdx.x) * kNParams;
+  tc_fence_after();
+  if (any) {
+    // TMEM rows 0-63: d2^T . [H1 | X | 1] -> dW1[o][i], db1[o]; rows 64-127: d1^T -> dW0, db0
+    const int o = r & (kHid - 1);
+    const bool top = r < kHid;
+    for (int c = 16 * p; c < kNW; c += 64) {  // parts take 16-column chunks 0,4 | 1,5 | 2,6 | 3
+      float v[16];
+      tmem_ld16(trow + kColW + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c + j;
+        if (top && col < kHid) row[pW1 + o * kHid + col] = v[j];
+        if (!top && col >= kHid && col < kHid + kIn) row[pW0 + o * kIn + (col - kHid)] = v[j];
+        if (col == kColOnes) row[(top ? pB1 : pB0) + o] = v[j];
+      }
+    }
+  } else {
+    for (int e = tid; e < pW2; e += kThreads) row[e] = 0.0f;
+  }
+  if (tid < kOut * kHid + kOut) row[pW2 + tid] = acc2;  // pB2 == pW2 + 256
+  static_assert(pB2 == pW2 + kOut * kHid, "dW2 then db2");
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
 int sms() { return device_sm_count(); }
@@ -716,28 +1025,39 @@ void field_backward_pool(ModelImpl& m, const unsigned long long* d_n, long long 
   ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_team_kernel), team_smem);
   const int bwd_per_sm =  // persistent: exactly the resident blocks (one wave)
       blocks_per_sm(reinterpret_cast<const void*>(field_bwd_team_kernel), kTeamThreads, team_smem);
+  // tcgen05 backward (K8-TC) when the forward saved its activations (decided on the device:
+  // pool <= 64 Ki); otherwise the SIMT K8a / K8b below run
+  const bool tc = m.bwd_tc && act != nullptr;
+  const int tc_grid = sms();
+  const int wblocks = sms() * 4;
+  w.bwd_partial.ensure(static_cast<size_t>(std::max(wblocks, tc_grid)) * kNParams);
   m.prof.begin("bwd_field", s);
   field_bwd_team_kernel<<<static_cast<unsigned>(sms() * std::max(bwd_per_sm, 1)), kTeamThreads, team_smem, s>>>(
       m.fv, w.px.ptr, w.py.ptr, w.pz.ptr, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, m.grid_grad.ptr, w.bwd_rec.ptr, act,
-      d_n);
+      d_n, tc);
   ARFX_CUDA(cudaGetLastError());
+  if (tc) {
+    ensure_dyn_smem(reinterpret_cast<const void*>(field_bwd_tc_kernel), bwdtc::kSmem + 1024);
+    field_bwd_tc_kernel<<<static_cast<unsigned>(tc_grid), bwdtc::kThreads, bwdtc::kSmem + 1024, s>>>(
+        m.fv, w.bwd_list.ptr, w.bwd_n.ptr, gs, gc, act, d_n, w.bwd_rec.ptr, w.bwd_partial.ptr);
+    ARFX_CUDA(cudaGetLastError());
+  }
   m.prof.end(s);
   // K8b + K8d (MLP weights, smem/FP32) run on the aux stream beside K8c (hash-grid
   // scatter, L2 atomics); both only read the K8a records. The join keeps the next
   // gradient writer on `s` ordered after K8d's non-atomic mlp_grad update.
-  const int wblocks = sms() * 4;
   if (!m.aux) {
     ARFX_CUDA(cudaStreamCreateWithFlags(&m.aux, cudaStreamNonBlocking));
     ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_aux_fork, cudaEventDisableTiming));
     ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_aux_join, cudaEventDisableTiming));
   }
-  w.bwd_partial.ensure(static_cast<size_t>(wblocks) * kNParams);
   ARFX_CUDA(cudaEventRecord(m.ev_aux_fork, s));
   ARFX_CUDA(cudaStreamWaitEvent(m.aux, m.ev_aux_fork, 0));
   m.prof.begin("bwd_weights", m.aux);
-  field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, m.aux>>>(w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap,
-                                                                                  w.bwd_partial.ptr);
-  weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, m.aux>>>(w.bwd_partial.ptr, wblocks, m.mlp_grad.ptr);
+  field_bwd_weights_kernel<<<static_cast<unsigned>(wblocks), kWThreads, 0, m.aux>>>(
+      w.bwd_rec.ptr, w.bwd_n.ptr, rec_cap, w.bwd_partial.ptr, tc ? d_n : nullptr);
+  weights_reduce_kernel<<<(kNParams + 31) / 32, 256, 0, m.aux>>>(w.bwd_partial.ptr, wblocks, w.bwd_n.ptr, rec_cap,
+                                                                 m.mlp_grad.ptr, tc ? d_n : nullptr, tc_grid);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(m.aux);
   ARFX_CUDA(cudaEventRecord(m.ev_aux_join, m.aux));

@@ -101,3 +101,36 @@ def test_update_training_grid_matches_reference(pair, ref):
         assert np.array_equal(msk, rmsk), step
         np.testing.assert_allclose(v, rv, rtol=2e-6, atol=1e-7)
     assert msk.sum() > 0
+
+
+def test_backward_modes_agree(pair, ref):
+    """Training MLP backward: the tcgen05 path (split-bf16 dX / dW, the default) and the SIMT
+    path in the reference's summation order give the same gradients within the parity bar,
+    and both match the reference."""
+    sk, dm, rm = pair
+    pose = arf.pose_from_joint_rotations(sk, fx.bend_pose_rotations(10, 0.3, 0.2), fx.yaw_about(sk.bones[0].head, 0.2))
+    occ = arf.build_model_inference_grid(dm, pose, arf.OccupancyConfig())
+    rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, arf.OccupancyConfig())
+    cam = fx.default_camera(sk, 80, 80)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=4, frame_id=2)
+    rng = np.random.default_rng(8)
+    n = 2048
+    px = rng.integers(0, 80, n).astype(np.int32)
+    py = rng.integers(0, 80, n).astype(np.int32)
+    dC = rng.normal(size=(n, 3)).astype(np.float32)
+    dA = rng.normal(size=n).astype(np.float32)
+    out = {}
+    try:
+        for mode in ("simt", "tcgen05"):
+            dm.set_backward_mode(mode)
+            dm.zero_grad()
+            arf.train_fwd_bwd(dm, pose, cam, occ, opt, px, py, dC, dA)
+            out[mode] = dm.grads()
+    finally:
+        dm.set_backward_mode("tcgen05")
+    _, _, rgg, rmg, _ = ref.train_fwd_bwd(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt, px, py, dC,
+                                          dA)
+    for mode in ("simt", "tcgen05"):
+        assert_grads_close(out[mode][0], rgg, f"{mode} grid grad")
+        assert_grads_close(out[mode][1], rmg, f"{mode} mlp grad")
+    assert_grads_close(out["tcgen05"][1], out["simt"][1], "tcgen05 vs simt mlp grad")

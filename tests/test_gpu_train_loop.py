@@ -172,8 +172,9 @@ def test_density_step_vs_reference(gpu, ref):
     rg, rw = ref.field_query_backward(rm, canon[sel], np.full(sel.sum(), cfg.w_density / n_empty, np.float32),
                                       np.zeros((sel.sum(), 3), np.float32))
     assert np.abs(rw).max() > 0
-    np.testing.assert_allclose(gm, rw, rtol=1e-4, atol=1e-6 * np.abs(rw).max())
-    np.testing.assert_allclose(gg, rg, rtol=1e-4, atol=1e-6 * np.abs(rg).max())
+    # gradient bar: |d| <= 1e-4 |ref| + 1e-5 max|ref| (tcgen05 split-bf16 backward)
+    np.testing.assert_allclose(gm, rw, rtol=1e-4, atol=1e-5 * np.abs(rw).max())
+    np.testing.assert_allclose(gg, rg, rtol=1e-4, atol=1e-5 * np.abs(rg).max())
 
 
 def test_checkpoint_bitwise_round_trip(gpu, tmp_path):
