@@ -63,10 +63,38 @@ __device__ __forceinline__ void level_corners(const FieldView& F, int l, const d
     cell[a] = static_cast<int>(c);
     f[a] = dsub(p, c);
   }
+  // corner indices (R/hash_grid.hpp:87-101) from per-axis terms in 32-bit arithmetic: the
+  // direct and wrap branches only exist when (n+1)^3 resp. n^3 <= 2^T <= 2^30, so the
+  // reference's 64-bit products equal the 32-bit ones, and the corner coordinate c + d is in
+  // [0, n], so its wrap (c + d) % n is (c + d == n ? 0 : c + d) -- no 64-bit multiplies or
+  // modulos (which dominated this function's instruction count and i-cache footprint)
+  const uint32_t nu = static_cast<uint32_t>(F.res[l]);
+  const int kind = F.kind[l];
+  uint32_t tx[2], ty[2], tz[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const uint32_t cx = static_cast<uint32_t>(cell[0] + d), cy = static_cast<uint32_t>(cell[1] + d),
+                   cz = static_cast<uint32_t>(cell[2] + d);
+    if (kind == kDirect) {
+      const uint32_t c1 = nu + 1u;
+      tx[d] = cx;
+      ty[d] = c1 * cy;
+      tz[d] = c1 * c1 * cz;
+    } else if (kind == kWrap) {
+      tx[d] = cx == nu ? 0u : cx;
+      ty[d] = nu * (cy == nu ? 0u : cy);
+      tz[d] = nu * nu * (cz == nu ? 0u : cz);
+    } else {
+      tx[d] = cx;
+      ty[d] = cy * 2654435761u;
+      tz[d] = cz * 805459861u;
+    }
+  }
+  const bool hashed = kind != kDirect && kind != kWrap;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-    lc.idx[k] = hash_index(F, l, cell[0] + dx, cell[1] + dy, cell[2] + dz);
+    lc.idx[k] = hashed ? ((tx[dx] ^ ty[dy] ^ tz[dz]) & (F.T - 1u)) : (tx[dx] + ty[dy] + tz[dz]);
     lc.w[k] = static_cast<float>(dmul(dmul(dx ? f[0] : dsub(1.0, f[0]), dy ? f[1] : dsub(1.0, f[1])),
                                       dz ? f[2] : dsub(1.0, f[2])));
   }

@@ -18,7 +18,7 @@ PREFIXES = {
     "ELECT": "elect.sync (single issuing thread)",
     "FENCE.VIEW.ASYNC": "fence.proxy.async (generic -> async proxy)",
 }
-KERNELS = ["field_tc_kernel"]
+KERNELS = ["field_tc_kernel", "field_bwd_tc_kernel"]
 
 
 def main(out=None):
