@@ -208,8 +208,6 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
 // the block's samples; the second pass recomputes t / x only for occupied samples.
 __global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A) {
   extern __shared__ unsigned march_bal[];  // [256 rays][K]
-  __shared__ int wsum[kMarchWarps];
-  __shared__ long long bbase;
   __shared__ double w2n[12];
   __shared__ int obox[6];
   if (threadIdx.x < 12) w2n[threadIdx.x] = A.pose->w2n[threadIdx.x];
@@ -338,26 +336,19 @@ __global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A)
         if (lane == j) my_count = count;
       }
     }
-    // ---- block exclusive scan of the 256 ray counts, one atomic per block
+    // ---- warp exclusive scan of the ray counts, one atomic per warp (no block barrier:
+    // a warp whose rays cross few occupied cells does not wait for the block's slowest ray)
     int incl = my_count;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long tot = 0;
-      for (int w = 0; w < kMarchWarps; ++w) {
-        const int c = wsum[w];
-        wsum[w] = static_cast<int>(tot);
-        tot += c;
-      }
-      bbase = tot ? static_cast<long long>(atomicAdd(A.counters, static_cast<unsigned long long>(tot))) : 0;
-    }
-    __syncthreads();
-    const long long first = bbase + wsum[warp] + (incl - my_count);
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    long long wbase = 0;
+    if (lane == 0 && wtot) wbase = static_cast<long long>(atomicAdd(A.counters, static_cast<unsigned long long>(wtot)));
+    wbase = static_cast<long long>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(wbase), 0));
+    const long long first = wbase + (incl - my_count);
     if (r < n_rays) {
       A.ray_first[rid] = static_cast<int32_t>(first < A.cap ? first : A.cap);
       A.ray_count[rid] = (first + my_count <= A.cap) ? my_count : 0;
@@ -396,7 +387,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A)
         run += __popc(b);
       }
     }
-    __syncthreads();
+    __syncwarp();  // march_bal rows are per warp: the next group's pass 1 reuses them
   }
 }
 
