@@ -420,7 +420,7 @@ def run_ours(args):
         line["work_counts"] = {"evals": int(stats[0]), "union_bone_visits": int(stats[1]),
                                "newton_steps": int(stats[2]), "starts": int(stats[3]),
                                "exact_prune_tests": int(stats[4]), "field_queries": int(stats[5]),
-                               "field_queries_tcgen05": int(stats[6]),
+                               "field_queries_tcgen05": int(stats[6]), "march_samples_tested": int(stats[11]),
                                "frames": K}
         line["pipe_peaks_tflops"] = {"fp64_addmul": p64.value, "fp32_addmul": p32.value}
         if cpu is not None:
@@ -501,6 +501,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     Newton steps I, starts S, exact prune tests P, field queries Q.
     """
     E, U, I, S, P, Q, QT = (float(x) for x in stats[:7])
+    tested = float(stats[11])  # samples march pass 1 tested (occupied-box range)
     fp64_peak, fp32_peak = pipe
     traffic = ncu_traffic()
     out = {}
@@ -532,15 +533,20 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     entry("encode_tc", "l2/l1 gathers", QT * (1024 + 128), "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); gathers are L2-resident, so frac is vs HBM for scale only",
           "1024 B gathered + 128 B written per query")
-    # K1 march: ~80 FP64 per ray + 36 per sample (ray.at, to_normalized, t, cell_of)
-    entry("march", "fp64", rays * K * (80 + 36 * N), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64")
-    entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
+    # K1 march: ~80 FP64 per ray + 36 per sample it tests (ray.at, to_normalized, t, cell_of):
+    # pass 1 tests only the samples that can reach the occupied box (device counter)
+    entry("march", "fp64", rays * K * 80 + 36 * tested, "TFLOP/s", fp64_peak, f64src,
+          "80/ray + 36/tested sample FP64 (samples outside the occupied box's range are not tested)")
+    # K2a/K2b prune + counting sort: HBM/L2 bytes -- per target x' read (24 B), mask + count
+    # written (8 B); per start key + item written, read back, sorted item written (20 B)
+    n_targets = posed + 64 ** 3 * K  # render samples + occupancy cells
+    entry("prune", "hbm", 32.0 * n_targets + 20.0 * S, "GB/s", hbm, f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+          "32 B/target + 20 B/start (mask/count, sort keys, items); 9 launches incl. 3-kernel scans")
     # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
     entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")
     # K2d finalize: per start its 32-B result read, per pool entry its 36-B canonical root +
     # owner + result slot written, per target 9 B of mask / count / base (HBM)
-    n_targets = posed + 64 ** 3 * K  # render samples + occupancy cells
     entry("finalize", "hbm", 32.0 * S + 36.0 * (Q + QT) + 9.0 * n_targets, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "32 B/start + 36 B/pool entry + 9 B/target")
     dom = max(out.values(), key=lambda e: e["ms_per_launch"] * e["launches"]) if out else None
@@ -716,13 +722,13 @@ def bench_microbench(steps: int, with_cpu: bool):
             from oracle.oracle_ctypes import Checker
             ref = Checker("ref")
             rm = ref.build_model(sk9, tiny, arf.MlpConfig(4, 16, 1, 4), (32, 32, 32), 1)
-            k = 200_000
+            k = n
             t0 = time.perf_counter()
             rc, _, _ = ref.inverse_lbs(rm, pose.bone_transforms, pre, 1e30, pts[:k])
             dt = time.perf_counter() - t0
             out["cpu_baseline"] = {"points_per_s": k / dt, "cores": ref.thread_count(), "kind": "reference",
-                                   "sample": f"first {k} of the 1M points, arf::inverse_lbs_ctx via parallel_for"}
-            out["roots_match_reference_on_sample"] = bool(np.array_equal(rc, roots[:k]))
+                                   "sample": f"all {k} points, arf::inverse_lbs_ctx via parallel_for"}
+            out["roots_match_reference"] = bool(np.array_equal(rc, roots[:k]))
         except Exception as e:
             out["cpu_baseline"] = {"unavailable": str(e)}
     L.arfx_pose_destroy(h)
@@ -888,8 +894,9 @@ def bench_train_roofline(steps: int, peaks, peak_kind, pipe):
                      "frac": ach / peak if peak else None, "ms_per_launch": ms / max(n, 1), "launches": n,
                      "ms_per_step": ms / steps, "work_per_launch": work / max(n, 1), "peak_source": src, "work": note}
 
-    entry("march", "fp64", R * (80 + 36 * 128), "TFLOP/s", fp64_peak, f64src, "80/ray + 36/sample FP64 (all 128 samples)")
-    entry("prune", "fp64", 32 * P, "TFLOP/s", fp64_peak, f64src, "32 FP64 per exact capsule-distance test")
+    TS = float(stats[11])
+    entry("march", "fp64", R * 80 + 36 * TS, "TFLOP/s", fp64_peak, f64src, "80/ray + 36/tested sample FP64")
+    entry("prune", "hbm", 32.0 * targets + 20.0 * S, "GB/s", hbm, hsrc, "32 B/target + 20 B/start")
     entry("deform", "fp64", 41 * E + 60 * U + 66 * I + 18 * S + 7 * max(E - S - I, 0.0), "TFLOP/s", fp64_peak, f64src,
           "FP64 add/mul/div/sqrt of inverse_lbs_ctx as written (no FMA)")
     entry("finalize", "hbm", 32.0 * S + 36.0 * Q + 9.0 * targets, "GB/s", hbm, hsrc,

@@ -120,6 +120,7 @@ struct MarchArgs {
   long long cap;
   int rpw;  // rays per warp (1..32): small ray lists (training) spread over more warps
   const int* occ_box;  // occupied-cell bounding box (-x0, -y0, -z0, x1, y1, z1) or nullptr
+  unsigned long long* stats;  // roofline accounting: [11] += samples tested in pass 1
 };
 
 // Bounding box of the occupied cells, for the march's empty-space skip: stored as
@@ -253,6 +254,12 @@ __global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A)
       }
     }
     int my_count = 0;
+    if (A.stats) {  // samples pass 1 tests (the occupied-box range of each valid ray)
+      unsigned long long tested = (R.valid && r_i1 >= r_i0) ? static_cast<unsigned long long>(r_i1 - r_i0 + 1) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tested += __shfl_xor_sync(0xffffffffu, tested, o);
+      if (lane == 0 && tested) atomicAdd(A.stats + 11, tested);
+    }
     if (A.rpw == 32) {
       // ---- pass 1, thread per ray (full warps): each lane walks its own ray's samples
       // (stratified jitter drawn sequentially from the ray's stream: draw i == jitter_at(i)),
@@ -1141,6 +1148,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
 
   MarchArgs A{};
+  A.stats = m.stats_on ? m.stats.ptr : nullptr;
   A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
   for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
   A.pose = p.dev.ptr;
@@ -1210,6 +1218,7 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
            static_cast<size_t>(std::max<long long>(n_rays, 1)));
   ARFX_CUDA(cudaMemsetAsync(w.counters.ptr, 0, 16 * sizeof(unsigned long long), s));
   MarchArgs A{};
+  A.stats = m.stats_on ? m.stats.ptr : nullptr;
   A.cam = CameraView{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, {}};
   for (int k = 0; k < 12; ++k) A.cam.ext[k] = cam.ext[k];
   A.pose = p.dev.ptr;
