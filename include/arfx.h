@@ -256,6 +256,12 @@ int arfx_occ_rebuild_mask_async(arfx_occ_grid g, void* stream);
 /* values hold n_shards rank-major shard blocks (arfx_build_inference_grid_shard_device, then
  * an all-gather): permute them into [z][y][x] cell order, then threshold + dilation. */
 int arfx_occ_rebuild_mask_shards_async(arfx_occ_grid g, int n_shards, void* stream);
+/* Asynchronous variant (no host round trip): the workspace is reserved for the worst case
+ * (every bone a start, kMaxRoots roots per cell), so it cannot overflow; counters (u64 x4)
+ * to device memory when d_counters != NULL. */
+int arfx_update_training_grid_device(arfx_model m, const arfx_pose* poses, int n_poses, double decay,
+                                     uint64_t seed, uint64_t step, arfx_occ_grid g, uint64_t* d_counters,
+                                     void* stream);
 int arfx_update_training_grid(arfx_model m, const arfx_pose* poses, int n_poses, double decay,
                               uint64_t seed, uint64_t step, arfx_occ_grid g, arfx_counters* c,
                               void* stream);

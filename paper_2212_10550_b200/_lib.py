@@ -136,6 +136,8 @@ _PROTOS = {
     "arfx_occ_device_arrays": (C.c_int, [H, C.POINTER(P), C.POINTER(P)]),
     "arfx_occ_rebuild_mask_async": (C.c_int, [H, P]),
     "arfx_occ_rebuild_mask_shards_async": (C.c_int, [H, C.c_int, P]),
+    "arfx_update_training_grid_device": (C.c_int, [H, C.POINTER(H), C.c_int, C.c_double, C.c_uint64,
+                                                   C.c_uint64, H, P, P]),
     "arfx_occ_is_occupied": (C.c_int, [H, c_double_p, C.c_int64, c_uint8_p]),
     "arfx_stats_enable": (C.c_int, [H, C.c_int]),
     "arfx_stats_read": (C.c_int, [H, c_uint64_p]),

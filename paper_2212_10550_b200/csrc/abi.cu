@@ -987,6 +987,27 @@ int arfx_update_training_grid(arfx_model mh, const arfx_pose* poses, int n_poses
   });
 }
 
+int arfx_update_training_grid_device(arfx_model mh, const arfx_pose* poses, int n_poses, double decay,
+                                     uint64_t seed, uint64_t step, arfx_occ_grid gh, uint64_t* d_counters,
+                                     void* stream) {
+  return guard([&] {
+    require(mh && poses && n_poses >= 1, "update_training_grid: need >= 1 pose");
+    ModelImpl& m = mh->impl;
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    std::vector<PoseImpl*> ps;
+    for (int i = 0; i < n_poses; ++i) {
+      require(poses[i] != nullptr, "update_training_grid: null pose");
+      ps.push_back(&poses[i]->impl);
+    }
+    OccImpl& g = occ_ref(gh);
+    const size_t n = static_cast<size_t>(g.res) * g.res * g.res;
+    // no host round trip, so no overflow re-run: the workspace is sized for the worst case
+    // (every bone a start, kMaxRoots roots per cell), which cannot overflow
+    m.ws().reserve_worst(n, static_cast<size_t>(m.sv.nb));
+    training_grid_update(m, ps, decay, seed, step, g, reinterpret_cast<unsigned long long*>(d_counters), s);
+  });
+}
 
 int arfx_render_model_device(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
                              const arfx_render_options* opt, int shard, int nshards, float* d_rgb,

@@ -207,7 +207,10 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
 // each ray's geometry by shuffle and testing its N samples 32 at a time (ballots kept in
 // dynamic smem). One block-wide exclusive scan of the 256 ray counts and one atomic place
 // the block's samples; the second pass recomputes t / x only for occupied samples.
-__global__ void __launch_bounds__(kMarchWarps * 32, 2) march_kernel(MarchArgs A) {
+#ifndef ARFX_MARCH_MIN_BLOCKS
+#define ARFX_MARCH_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kMarchWarps * 32, ARFX_MARCH_MIN_BLOCKS) march_kernel(MarchArgs A) {
   extern __shared__ unsigned march_bal[];  // [256 rays][K]
   __shared__ double w2n[12];
   __shared__ int obox[6];
@@ -1184,8 +1187,11 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
     A.rpw = static_cast<int>(std::min<long long>(
         32, std::max<long long>(1, (n_rays + sm_count() * 4LL * kMarchWarps - 1) / (sm_count() * 4LL * kMarchWarps))));
     const long long groups = (n_rays + kMarchWarps * A.rpw - 1) / (kMarchWarps * A.rpw);
-    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
     const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
+    // exactly one wave of resident blocks (a second partial wave cost 7 % of the kernel)
+    const int grid = static_cast<int>(std::min<long long>(
+        groups, static_cast<long long>(sm_count()) *
+                    std::max(1, blocks_per_sm(reinterpret_cast<const void*>(march_kernel), kMarchWarps * 32, smem))));
     m.prof.begin("march", s);
     march_kernel<<<grid, kMarchWarps * 32, smem, s>>>(A);
     ARFX_CUDA(cudaGetLastError());
@@ -1255,8 +1261,11 @@ void train_forward(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* oc
     A.rpw = static_cast<int>(std::min<long long>(
         32, std::max<long long>(1, (n_rays + sm_count() * 4LL * kMarchWarps - 1) / (sm_count() * 4LL * kMarchWarps))));
     const long long groups = (n_rays + kMarchWarps * A.rpw - 1) / (kMarchWarps * A.rpw);
-    const int grid = static_cast<int>(std::min<long long>(groups, static_cast<long long>(sm_count()) * 4));
     const size_t smem = static_cast<size_t>(kMarchWarps) * 32 * ((A.N + 31) / 32) * sizeof(unsigned);
+    // exactly one wave of resident blocks (a second partial wave cost 7 % of the kernel)
+    const int grid = static_cast<int>(std::min<long long>(
+        groups, static_cast<long long>(sm_count()) *
+                    std::max(1, blocks_per_sm(reinterpret_cast<const void*>(march_kernel), kMarchWarps * 32, smem))));
     m.prof.begin("march", s);
     march_kernel<<<grid, kMarchWarps * 32, smem, s>>>(A);
     ARFX_CUDA(cudaGetLastError());
@@ -1414,7 +1423,6 @@ void training_grid_update(ModelImpl& m, const std::vector<PoseImpl*>& poses, dou
   if (d_counters)
     ARFX_CUDA(cudaMemcpyAsync(d_counters, w.counters.ptr, 4 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToDevice, s));
-  ARFX_CUDA(cudaStreamSynchronize(s));
 }
 
 void inverse_lbs_batch(ModelImpl& m, const PoseCtx* d_ctx, const double* d_pts, int64_t n,

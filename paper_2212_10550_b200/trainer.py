@@ -189,6 +189,11 @@ class Trainer:
         # set on the device by the guarded Adam when a step's loss is non-finite: that step and
         # every later one leave the model untouched, _check raises
         self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._bad_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._bad_ev = torch.cuda.Event()
+        self._bad_pending = False
+        self.ev_grid = torch.cuda.Event()
+        self._pose_arr = (C.c_void_p * len(self.views))(*[v._h.value for v in self.views])
         # two pinned host staging slots for the ray pixels (the host runs ahead of the GPU)
         self._h_pix = [torch.zeros((2, self.n_local), dtype=torch.int32).pin_memory() for _ in range(2)]
         self._h_evt = [torch.cuda.Event(), torch.cuda.Event()]
@@ -281,11 +286,32 @@ class Trainer:
         self._hist.append(row)
         self.step_id = t1
         if cfg.occupancy_interval > 0 and t1 % cfg.occupancy_interval == 0:
-            self._sync()
-            arf.update_training_grid(self.model, self.grid, self.poses, cfg.occupancy.decay, cfg.seed, t1)
-            self._check()
+            # the training-grid update (R/occupancy.hpp:155-171) reads the parameters after this
+            # step's Adam: enqueued on the Adam stream with no host round trip; the next
+            # forward and backward wait for it (the pipeline does not drain)
+            L.call("arfx_update_training_grid_device", self.model._h, self._pose_arr, len(self.views),
+                   cfg.occupancy.decay, cfg.seed & (2**64 - 1), t1, self.grid._h, None, asp)
+            self.ev_grid.record(self.adam_stream)
+            self.fstream.wait_event(self.ev_grid)
+            self.stream.wait_event(self.ev_grid)
+            self._check_async()
         self._forward(t1)  # overlaps this step's backward (its field waits for this Adam)
         return row
+
+    def _check_async(self):
+        """Non-blocking finiteness check: the device flag of the guarded Adam is copied to pinned
+        memory at every occupancy boundary and read at the next one once the copy has landed
+        (a poisoned step has already been skipped on the device, so late detection is safe)."""
+        if self._bad_pending and self._bad_ev.query():
+            self._bad_pending = False
+            if int(self._bad_host[0]):
+                self._sync()
+                self._check()
+        if not self._bad_pending:
+            with self.torch.cuda.stream(self.adam_stream):
+                self._bad_host.copy_(self.bad, non_blocking=True)
+            self._bad_ev.record(self.adam_stream)
+            self._bad_pending = True
 
     def _step(self):
         torch = self.torch
