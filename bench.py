@@ -209,6 +209,7 @@ def run_ours(args):
         my_slab = occ_vals[rank * slab:(rank + 1) * slab]
 
     def frame_direct(i, slot):
+        pstate["next"] = None  # the pipelined graphs' grid A may be overwritten below
         v = views[i % N_FRAMES]
         if shard_grid:
             check(L.arfx_build_inference_grid_shard_device(model._h, v._h, occ._h, rank, world,
@@ -227,10 +228,28 @@ def run_ours(args):
     # pose from device memory). With grid shards the NCCL all-gather sits between two graphs.
     gview = arf.PosedModelView(model, poses[0])
     g_cnt = torch.zeros((2, 4), dtype=torch.int64, device="cuda")
+    # 1 GPU: pipelined frame graphs -- each replay renders frame i with its (already built)
+    # grid while building frame i+1's grid on a concurrent branch; two graphs alternate the
+    # roles of (pose handle, occupancy grid) A/B. Every frame is still one grid build + one
+    # render; only their overlap across consecutive frames changes.
+    pipelined = world == 1 and not args.no_graph and not args.no_pipeline
+    pv = [gview, arf.PosedModelView(model, poses[0])]
+    pocc = [occ, arf.OccupancyGrid(model.normalized_box, occ_cfg)] if pipelined else [occ]
+    pstate = {"phase": 0, "next": None}  # next: the frame whose grid the current handle holds
 
     def make_graphs():
         hs = []
         if args.no_graph:
+            return hs
+        if pipelined:
+            for ph in range(2):
+                h = C.c_void_p()
+                check(L.arfx_frame_graph_create_pipelined(
+                    model._h, pv[ph]._h, pocc[ph]._h, pv[1 - ph]._h, pocc[1 - ph]._h, C.byref(ccam), C.byref(copt),
+                    rank, world, C.c_void_p(d_rgb.data_ptr()), C.c_void_p(d_alpha.data_ptr()),
+                    C.c_void_p(g_cnt.data_ptr()), sp, C.byref(h)))
+                hs.append(h)
+            pstate["next"] = None  # the handles' contents are unknown after a capture's warm-up
             return hs
         for pmask in ([2, 16 | 8] if shard_grid else [1 | 8]):
             h = C.c_void_p()
@@ -257,7 +276,19 @@ def run_ours(args):
             recaptures[0] += 1
             check(L.arfx_frame_graph_launch(graphs[k], sp))
 
+    def frame_pipelined(i, slot):
+        ph = pstate["phase"]
+        if pstate["next"] != i:  # out of sequence (or first frame): build frame i's grid directly
+            check(L.arfx_pose_copy(pv[ph]._h, views[i % N_FRAMES]._h, sp))
+            check(L.arfx_build_inference_grid_device(model._h, pv[ph]._h, pocc[ph]._h, None, sp))
+        check(L.arfx_pose_copy(pv[1 - ph]._h, views[(i + 1) % N_FRAMES]._h, sp))
+        launch_graph(ph)  # render i from (pv[ph], pocc[ph]); build i + 1 into (pv[1-ph], pocc[1-ph])
+        d_cnt[slot, 1].copy_(g_cnt[1])
+        pstate["phase"], pstate["next"] = 1 - ph, i + 1
+
     def frame_graph(i, slot):
+        if pipelined:
+            return frame_pipelined(i, slot)
         # `graphs` is looked up at call time (re-captured for the other decoder below)
         check(L.arfx_pose_copy(gview._h, views[i % N_FRAMES]._h, sp))
         launch_graph(0)
@@ -336,7 +367,8 @@ def run_ours(args):
     fps = K / (total_ms / 1000.0)
 
     # kernel launches per frame, counted by the CUDA profiler (kineto) on 2 untimed frames
-    launches_per_frame = count_launches(lambda i: frame(Wm + i, Wm + K), 2)
+    frame(Wm + K + 2, Wm + K)  # (pipelined graphs: prime the sequence outside the count)
+    launches_per_frame = count_launches(lambda i: frame(Wm + K + 3 + i, Wm + K), 2)
 
     # e2e through the host-buffer public API
     e2e = run_e2e(args, model, poses, cam, opt, occ, rank, world, views)
@@ -357,7 +389,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         rgb = d_rgb.cpu().numpy().reshape(H_IMG, W_IMG, 3)
         alpha = d_alpha.cpu().numpy().reshape(H_IMG, W_IMG)
-        mask = occ.mask
+        mask = pocc[1 - pstate["phase"]].mask if pipelined else occ.mask  # the grid frame j rendered with
         d = np.concatenate([np.abs(rgb - rrgb).ravel(), np.abs(alpha - ralpha).ravel()])
         r = np.concatenate([np.abs(rrgb).ravel(), np.abs(ralpha).ravel()])
         parity[decoder] = {"frame": j, "mask_equal": bool(np.array_equal(mask, rmask)),
@@ -407,7 +439,9 @@ def run_ours(args):
                 "gpu_launches_per_frame": launches_per_frame,
                 "peaks_kind": peak_kind,
                 "render_decoder": args.mlp,
-                "frame_launch": "cuda_graph (pose copied into the captured handle per frame)" if graphs else "direct",
+                "frame_launch": ("cuda_graph, pipelined: frame i's render || frame i+1's grid build (two graphs "
+                                 "alternating pose handles and occupancy grids)" if pipelined else
+                                 "cuda_graph (pose copied into the captured handle per frame)") if graphs else "direct",
                 "graph_recaptures_outside_timed_region": recaptures[0],
                 "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}
         rays_rank = shard_rows(world, rank) * W_IMG
@@ -943,6 +977,9 @@ def main():
     ap.add_argument("--force-dist-paths", action="store_true",
                     help="exercise the multi-GPU code paths (grid all-gather, DP train) at N = 1 under torchrun")
     ap.add_argument("--no-graph", action="store_true", help="launch each frame's kernels directly (no CUDA graph)")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="1 GPU: one grid + render graph per frame instead of overlapping frame i+1's grid build "
+                         "with frame i's render")
     ap.add_argument("--no-shard-grid", action="store_true",
                     help="N > 1: build the occupancy grid redundantly on every rank instead of cell-interleaved shards")
     ap.add_argument("--no-dp-train", action="store_true",

@@ -462,6 +462,17 @@ enum {
 int arfx_frame_graph_create(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
                             const arfx_render_options* opt, int shard, int n_shards, int parts, float* d_rgb,
                             float* d_alpha, uint64_t* d_counters, void* stream, arfx_frame_graph* out);
+/* Pipelined animation frame: one graph with two concurrent branches -- the inference grid of
+ * the NEXT pose (p_next -> occ_next, side stream and workspace) and the render of the
+ * CURRENT pose with its already-built grid (p_cur, occ_cur). Alternate two such graphs with
+ * the (pose, grid) roles swapped: each frame's grid build overlaps the previous frame's
+ * render, every frame bit-identical to a direct grid + render. d_counters [2][4] required
+ * (next grid, render). Same invalidation rule as arfx_frame_graph_create. */
+int arfx_frame_graph_create_pipelined(arfx_model m, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
+                                      arfx_occ_grid occ_next, const arfx_camera* cam,
+                                      const arfx_render_options* opt, int shard, int nshards, float* d_rgb,
+                                      float* d_alpha, uint64_t* d_counters, void* stream,
+                                      arfx_frame_graph* out);
 int arfx_frame_graph_launch(arfx_frame_graph g, void* stream);
 int arfx_frame_graph_destroy(arfx_frame_graph g);
 /* dst <- src (same model): host and device PoseContext, asynchronous on stream */

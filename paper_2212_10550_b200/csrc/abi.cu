@@ -29,6 +29,8 @@ struct arfx_frame_graph_s {
   int device = 0;
   const arfx::Workspace* ws = nullptr;  // the workspace the kernels were captured on
   unsigned long long ws_gen = 0;        // its generation at capture
+  const arfx::Workspace* ws2 = nullptr;  // pipelined graphs: the side branch's workspace
+  unsigned long long ws2_gen = 0;
   ~arfx_frame_graph_s() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -1117,10 +1119,96 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
   });
 }
 
+// Pipelined animation frame: one graph with two concurrent branches -- the inference grid of
+// the NEXT pose (pose handle p_next -> occ_next, on the model's side stream and side
+// workspace) and the render of the CURRENT pose with its already-built grid (p_cur, occ_cur,
+// main workspace). Alternating two such graphs with the roles of (p, occ) swapped renders an
+// animation with each frame's grid build overlapping the previous frame's render; every frame
+// is bit-identical to a direct grid + render (test_pipelined_frame_graphs_match_direct).
+// d_counters [2][4]: the next grid's counters, then the render's.
+int arfx_frame_graph_create_pipelined(arfx_model mh, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
+                                      arfx_occ_grid occ_next, const arfx_camera* cam, const arfx_render_options* opt,
+                                      int shard, int nshards, float* d_rgb, float* d_alpha, uint64_t* d_counters,
+                                      void* stream, arfx_frame_graph* out) {
+  return guard([&] {
+    require(mh && p_cur && occ_cur && p_next && occ_next && out, "frame_graph_create_pipelined: null argument");
+    require(occ_cur != occ_next, "frame_graph_create_pipelined: the two grids must differ");
+    require(d_rgb && d_alpha && opt && d_counters, "frame_graph_create_pipelined: render outputs and counters");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    require(s != nullptr, "frame_graph_create_pipelined: needs a non-NULL stream");
+    if (!m.side) ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+    cudaEvent_t fork = nullptr, join = nullptr;
+    ARFX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    ARFX_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t a, b;
+      ~EvGuard() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } evg{fork, join};
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counters);
+    OccImpl& gn = occ_next->impl;
+    auto enqueue = [&] {
+      ARFX_CUDA(cudaEventRecord(fork, s));
+      ARFX_CUDA(cudaStreamWaitEvent(m.side, fork, 0));
+      {
+        WorkspaceScope side(m, m.ws_side);
+        inference_grid(m, p_next->impl, gn, cnt, m.side);
+      }
+      render_frame(m, p_cur->impl, hc, &occ_cur->impl, opt->samples_per_ray, opt->stratified != 0,
+                   opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha, cnt + 4, s);
+      ARFX_CUDA(cudaEventRecord(join, m.side));
+      ARFX_CUDA(cudaStreamWaitEvent(s, join, 0));
+    };
+    // warm-up (uncaptured): the side workspace for the worst case of a grid build, the main
+    // one from the render's counters
+    {
+      WorkspaceScope side(m, m.ws_side);
+      m.ws().reserve_worst(static_cast<size_t>(gn.res) * gn.res * gn.res, static_cast<size_t>(m.sv.nb));
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      enqueue();
+      unsigned long long hcnt[8];
+      d2h(hcnt, m.ws().counters.ptr, 8, s);
+      ARFX_CUDA(cudaStreamSynchronize(s));
+      bool rerun;
+      check_overflow_and_grow(m, hcnt, rerun);
+      if (!rerun) break;
+    }
+    const bool prof = m.prof.on;
+    m.prof.on = false;
+    auto g = std::make_unique<arfx_frame_graph_s>();
+    g->device = m.device;
+    ARFX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(s, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      m.prof.on = prof;
+      throw;
+    }
+    ARFX_CUDA(cudaStreamEndCapture(s, &g->graph));
+    m.prof.on = prof;
+    ARFX_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+    g->ws = &m.ws_main;
+    g->ws_gen = m.ws_main.gen;
+    g->ws2 = &m.ws_side;
+    g->ws2_gen = m.ws_side.gen;
+    *out = g.release();
+  });
+}
+
 int arfx_frame_graph_launch(arfx_frame_graph g, void* stream) {
   return guard([&] {
     require(g && g->exec, "frame_graph_launch: null graph");
-    if (g->ws->gen != g->ws_gen)
+    if (g->ws->gen != g->ws_gen || (g->ws2 && g->ws2->gen != g->ws2_gen))
       throw std::invalid_argument(
           "frame_graph_launch: the model workspace was reallocated since this graph was captured (a larger "
           "render, a camera / shard change or an overflow regrow); destroy the graph and create it again");

@@ -535,3 +535,50 @@ def test_randomized_cameras_march_parity(models, ref):
         assert np.array_equal(tr.delta[order].view(np.uint64), rtr["s_delta"].view(np.uint64))
 
     check()
+
+
+def test_pipelined_frame_graphs_match_direct(gpu):
+    """Two pipelined frame graphs alternating (render frame i with its grid || build frame i+1's
+    grid on the side branch) over 5 animation poses: every frame's image and the grid it was
+    rendered with equal a direct build_model_inference_grid + render_model bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_2212_10550_b200._lib import call
+    sk = fx.smpl24()
+    m = gpu.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = fx.animation_poses(sk, 5)
+    views = [arf.PosedModelView(m, p) for p in poses]
+    cam = fx.default_camera(sk, 120, 112)
+    opt = arf.RenderOptions()
+    cfg = arf.OccupancyConfig()
+    pv = [arf.PosedModelView(m, poses[0]), arf.PosedModelView(m, poses[0])]
+    occ = [arf.OccupancyGrid(m.normalized_box, cfg), arf.OccupancyGrid(m.normalized_box, cfg)]
+    st = torch.cuda.Stream()
+    sp = C.c_void_p(st.cuda_stream)
+    rgb = torch.zeros(120 * 112 * 3, device="cuda")
+    alpha = torch.zeros(120 * 112, device="cuda")
+    cnt = torch.zeros((2, 4), dtype=torch.int64, device="cuda")
+    gs = []
+    for ph in range(2):
+        g = C.c_void_p()
+        call("arfx_frame_graph_create_pipelined", m._h, pv[ph]._h, occ[ph]._h, pv[1 - ph]._h, occ[1 - ph]._h,
+             C.byref(cam.to_c()), C.byref(opt.to_c()), 0, 1, C.c_void_p(rgb.data_ptr()),
+             C.c_void_p(alpha.data_ptr()), C.c_void_p(cnt.data_ptr()), sp, C.byref(g))
+        gs.append(g)
+    try:
+        call("arfx_pose_copy", pv[0]._h, views[0]._h, sp)
+        call("arfx_build_inference_grid_device", m._h, pv[0]._h, occ[0]._h, None, sp)
+        for i in range(len(poses)):
+            ph = i & 1
+            call("arfx_pose_copy", pv[1 - ph]._h, views[(i + 1) % len(poses)]._h, sp)
+            call("arfx_frame_graph_launch", gs[ph], sp)
+            st.synchronize()
+            ref_occ = arf.build_model_inference_grid(m, poses[i], cfg)
+            ref_img = arf.render_model(m, poses[i], cam, ref_occ, opt)
+            assert np.array_equal(occ[ph].mask, ref_occ.mask), i
+            assert np.array_equal(rgb.cpu().numpy().reshape(112, 120, 3), ref_img.rgb), i
+            assert np.array_equal(alpha.cpu().numpy().reshape(112, 120), ref_img.alpha), i
+            assert int(cnt[:, 3].sum()) == 0 and int(cnt[1, 0]) > 0
+    finally:
+        for g in gs:
+            call("arfx_frame_graph_destroy", g)
