@@ -288,6 +288,15 @@ int arfx_render_model_device(arfx_model m, arfx_pose p, const arfx_camera* cam,
 int arfx_render_model_async(arfx_model m, arfx_pose p, const arfx_camera* cam, arfx_occ_grid occ,
                             const arfx_render_options* opt, int shard, int n_shards, float* rgb, float* alpha,
                             uint64_t* counters4, void* stream);
+/* Pipelined animation through host buffers: builds the inference grid of the NEXT pose
+ * (p_next -> occ_next, side stream + side workspace) while the CURRENT pose renders with its
+ * already-built grid (p_cur, occ_cur) into host buffers exactly as arfx_render_model_async;
+ * later work on `stream` waits for the new grid. Alternate the two (pose, grid) pairs frame
+ * by frame; results are identical to arfx_build_inference_grid + arfx_render_model. */
+int arfx_render_model_pipelined_async(arfx_model m, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
+                                      arfx_occ_grid occ_next, const arfx_camera* cam,
+                                      const arfx_render_options* opt, int row_shard, int n_shards, float* rgb,
+                                      float* alpha, uint64_t* counters4, void* stream);
 int arfx_render_wait(arfx_model m);
 /* Trace of the last render on this model (posed-sample list), for parity tests:
  * per posed sample: pixel, sample index, has_root, density, rgb, canonical root. */

@@ -205,6 +205,8 @@ _PROTOS = {
                                           C.c_int, C.c_int, P, P, P, P, C.POINTER(H)]),
     "arfx_frame_graph_create_pipelined": (C.c_int, [H, H, H, H, H, C.POINTER(ArfxCamera), C.POINTER(ArfxRenderOptions),
                                                     C.c_int, C.c_int, P, P, P, P, C.POINTER(H)]),
+    "arfx_render_model_pipelined_async": (C.c_int, [H, H, H, H, H, C.POINTER(ArfxCamera), C.POINTER(ArfxRenderOptions),
+                                                    C.c_int, C.c_int, P, P, P, P]),
     "arfx_frame_graph_launch": (C.c_int, [H, P]),
     "arfx_frame_graph_destroy": (C.c_int, [H]),
     "arfx_figure_query": (C.c_int, [C.POINTER(ArfxFigure), c_double_p, c_double_p, C.c_int64, c_double_p,

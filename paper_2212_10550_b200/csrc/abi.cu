@@ -280,6 +280,8 @@ ModelImpl::~ModelImpl() {
   }
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_pipe_fork) cudaEventDestroy(ev_pipe_fork);
+  if (ev_pipe_join) cudaEventDestroy(ev_pipe_join);
   if (aux) {
     cudaStreamSynchronize(aux);
     cudaStreamDestroy(aux);
@@ -1244,7 +1246,7 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
       // this shard's row tiles (other shards' rows are left untouched), enqueued behind the
       // counters so one synchronisation covers both; on overflow the frame re-runs and
       // copies again. Full tiles of a shard are one strided 2-D copy per image.
-      const int W = hc.width, H = hc.height, T = 16;
+      const int W = hc.width, H = hc.height, T = kRowTile;
       const int full_tiles = H / T;  // tiles 0..full_tiles-1 have T rows
       const int first = shard;        // tiles of this shard: first, first + nshards, ...
       const int n_full = first < full_tiles ? (full_tiles - 1 - first) / nshards + 1 : 0;
@@ -1283,16 +1285,11 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
 // image slots on `stream`; the slot's D2H copies (this shard's row tiles, counters) run on
 // the model's copy stream while the next frame renders. A slot is re-used only after its
 // previous copies completed (device-side wait).
-int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
-                            const arfx_render_options* opt, int shard, int nshards, float* rgb, float* alpha,
-                            uint64_t* counters4, void* stream) {
-  return guard([&] {
-    require(mh && ph && rgb && alpha, "render_model_async: null argument");
-    ModelImpl& m = mh->impl;
-    const HostCamera hc = camera_of(cam);
-    validate_render(hc, opt, shard, nshards);
-    ARFX_CUDA(cudaSetDevice(m.device));
-    const cudaStream_t s = stream_of(m, stream);
+namespace {
+// arfx_render_model_async's device side: render into one of two device image slots on `s`,
+// then copy this shard's rows to the host buffers on the model's copy stream
+void render_async_impl(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, const arfx_render_options* opt,
+                       int shard, int nshards, float* rgb, float* alpha, uint64_t* counters4, cudaStream_t s) {
     if (!m.copy_stream) {
       ARFX_CUDA(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
       for (auto& a : m.async_slot) {
@@ -1310,13 +1307,13 @@ int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
       a.counters.ensure(4);
     }
     ARFX_CUDA(cudaStreamWaitEvent(s, a.copied, 0));  // the slot's previous copies are done
-    render_frame(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt->samples_per_ray, opt->stratified != 0,
+    render_frame(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0,
                  opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, a.rgb.ptr, a.alpha.ptr,
                  a.counters.ptr, s);
     ARFX_CUDA(cudaEventRecord(a.rendered, s));
     const cudaStream_t c = m.copy_stream;
     ARFX_CUDA(cudaStreamWaitEvent(c, a.rendered, 0));
-    const int W = hc.width, H = hc.height, T = 16;
+    const int W = hc.width, H = hc.height, T = kRowTile;
     const int full_tiles = H / T;
     const int n_full = shard < full_tiles ? (full_tiles - 1 - shard) / nshards + 1 : 0;
     if (n_full > 0) {
@@ -1341,6 +1338,60 @@ int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
     if (counters4)
       ARFX_CUDA(cudaMemcpyAsync(counters4, a.counters.ptr, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c));
     ARFX_CUDA(cudaEventRecord(a.copied, c));
+}
+}  // namespace
+
+int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_occ_grid occ,
+                            const arfx_render_options* opt, int shard, int nshards, float* rgb, float* alpha,
+                            uint64_t* counters4, void* stream) {
+  return guard([&] {
+    require(mh && ph && rgb && alpha, "render_model_async: null argument");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    render_async_impl(m, ph->impl, hc, occ ? &occ->impl : nullptr, opt, shard, nshards, rgb, alpha, counters4,
+                      stream_of(m, stream));
+  });
+}
+
+// Pipelined animation through host buffers: the inference grid of the NEXT pose (p_next ->
+// occ_next) is built on the model's side stream in the side workspace while the CURRENT pose
+// renders with its already-built grid (p_cur, occ_cur) into host buffers as
+// arfx_render_model_async does; later work on `stream` waits for the grid. Alternate the two
+// (pose, grid) pairs frame by frame (the C-ABI twin of arfx_frame_graph_create_pipelined).
+int arfx_render_model_pipelined_async(arfx_model mh, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
+                                      arfx_occ_grid occ_next, const arfx_camera* cam, const arfx_render_options* opt,
+                                      int shard, int nshards, float* rgb, float* alpha, uint64_t* counters4,
+                                      void* stream) {
+  return guard([&] {
+    require(mh && p_cur && occ_cur && p_next && occ_next && rgb && alpha, "render_model_pipelined_async: null argument");
+    require(occ_cur != occ_next, "render_model_pipelined_async: the two grids must differ");
+    ModelImpl& m = mh->impl;
+    const HostCamera hc = camera_of(cam);
+    validate_render(hc, opt, shard, nshards);
+    ARFX_CUDA(cudaSetDevice(m.device));
+    const cudaStream_t s = stream_of(m, stream);
+    if (!m.side) ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+    if (!m.ev_pipe_fork) {
+      ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_pipe_fork, cudaEventDisableTiming));
+      ARFX_CUDA(cudaEventCreateWithFlags(&m.ev_pipe_join, cudaEventDisableTiming));
+    }
+    OccImpl& gn = occ_next->impl;
+    const size_t cells = static_cast<size_t>(gn.res) * gn.res * gn.res;
+    {
+      WorkspaceScope side(m, m.ws_side);
+      if (m.ws().cap_pool < cells * kMaxRoots + 1024) {  // worst case once (no overflow re-run possible)
+        ARFX_CUDA(cudaDeviceSynchronize());
+        m.ws().reserve_worst(cells, static_cast<size_t>(m.sv.nb));
+      }
+      ARFX_CUDA(cudaEventRecord(m.ev_pipe_fork, s));
+      ARFX_CUDA(cudaStreamWaitEvent(m.side, m.ev_pipe_fork, 0));
+      inference_grid(m, p_next->impl, gn, nullptr, m.side);
+      ARFX_CUDA(cudaEventRecord(m.ev_pipe_join, m.side));
+    }
+    render_async_impl(m, p_cur->impl, hc, &occ_cur->impl, opt, shard, nshards, rgb, alpha, counters4, s);
+    ARFX_CUDA(cudaStreamWaitEvent(s, m.ev_pipe_join, 0));
   });
 }
 

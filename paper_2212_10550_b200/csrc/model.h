@@ -184,6 +184,7 @@ struct ModelImpl {
   Workspace& ws() { return *ws_cur; }
   cudaStream_t side = nullptr;  // lazily created non-blocking stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_pipe_fork = nullptr, ev_pipe_join = nullptr;  // arfx_render_model_pipelined_async
   cudaStream_t aux = nullptr;   // K8b/K8d next to K8c (field_backward_pool)
   // arfx_render_model_async: two device image slots; their D2H copies run on copy_stream
   // while the next frame renders

@@ -281,12 +281,26 @@ def test_sharded_render_equals_full_frame(models):
     cam = fx.default_camera(sk, 72, 70)
     occ = arf.build_model_inference_grid(dm, pose, arf.OccupancyConfig())
     opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=4, frame_id=2)
-    full = arf.render_model(dm, pose, cam, occ, opt)
+    # shards first (the library's device staging must not be able to hold a full frame of
+    # this pose yet), then the full frame; the async host-buffer path copies the same rows
     parts = arf.RenderImages(cam.width, cam.height, np.full((70, 72, 3), -1, np.float32),
                              np.full((70, 72), -1, np.float32))
     for r in range(3):
         arf.render_model(dm, pose, cam, occ, opt, shard=r, n_shards=3, out=parts)
+    full = arf.render_model(dm, pose, cam, occ, opt)
     assert np.array_equal(parts.rgb, full.rgb) and np.array_equal(parts.alpha, full.alpha)
+    import torch
+    view = arf.PosedModelView(dm, pose)
+    for r in range(3):
+        pin = arf.RenderImages(72, 70, torch.full((70, 72, 3), -1.0).pin_memory().numpy(),
+                               torch.full((70, 72), -1.0).pin_memory().numpy())
+        cnt = np.zeros(4, np.uint64)
+        arf.render_model_async(dm, view, cam, occ, opt, pin, cnt, r, 3)
+        arf.render_wait(dm)
+        rows = arf.shard_rows(70, r, 3)
+        other = np.setdiff1d(np.arange(70), rows)
+        assert np.array_equal(pin.rgb[rows], full.rgb[rows]) and np.array_equal(pin.alpha[rows], full.alpha[rows])
+        assert np.all(pin.rgb[other] == -1) and np.all(pin.alpha[other] == -1)
 
 
 def test_cpp_dropin_adapter():
@@ -582,3 +596,36 @@ def test_pipelined_frame_graphs_match_direct(gpu):
     finally:
         for g in gs:
             call("arfx_frame_graph_destroy", g)
+
+
+def test_pipelined_host_render_matches_sync(gpu):
+    """arfx_render_model_pipelined_async (frame k renders into host buffers while frame k+1's
+    grid builds on the side stream, alternating pose handles and grids) == the synchronous
+    build_model_inference_grid + render_model, frame by frame, bit for bit."""
+    import torch
+    sk = fx.smpl24()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = fx.animation_poses(sk, 4)
+    cam = fx.default_camera(sk, 160, 150)
+    opt, cfg = fx.config1_render_options(), fx.config1_occupancy()
+    ref = [arf.render_model(m, p, cam, arf.build_model_inference_grid(m, p, cfg), opt) for p in poses]
+    import ctypes as C
+    from paper_2212_10550_b200._lib import check, lib
+    L = lib()
+    pv = [arf.PosedModelView(m, poses[0]), arf.PosedModelView(m, poses[0])]
+    occ = [arf.OccupancyGrid(m.normalized_box, cfg) for _ in range(2)]
+    check(L.arfx_build_inference_grid(m._h, pv[0]._h, occ[0]._h, None, None))
+    pin = lambda shape: torch.zeros(shape, dtype=torch.float32).pin_memory().numpy()  # noqa: E731
+    outs = [arf.RenderImages(160, 150, pin((150, 160, 3)), pin((150, 160))) for _ in poses]
+    cnts = [np.zeros(4, np.uint64) for _ in poses]
+    for k in range(len(poses)):
+        cur, nxt = k & 1, (k + 1) & 1
+        pv[nxt].update(poses[(k + 1) % len(poses)], sync=False)
+        check(L.arfx_render_model_pipelined_async(m._h, pv[cur]._h, occ[cur]._h, pv[nxt]._h, occ[nxt]._h,
+                                                  C.byref(cam.to_c()), C.byref(opt.to_c()), 0, 1,
+                                                  arf.ptr(outs[k].rgb, C.c_float), arf.ptr(outs[k].alpha, C.c_float),
+                                                  cnts[k].ctypes.data_as(C.POINTER(C.c_uint64)), None))
+    arf.render_wait(m)
+    for r, o, c in zip(ref, outs, cnts):
+        assert c[3] == 0 and c[0] > 0
+        assert np.array_equal(r.rgb, o.rgb) and np.array_equal(r.alpha, o.alpha)
