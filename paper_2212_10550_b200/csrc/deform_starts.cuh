@@ -566,6 +566,101 @@ __global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restr
   }
 }
 
+// ---- single-pass exclusive scan (decoupled look-back) -----------------------------------
+// Tiles of 1024 elements are taken in ticket order (so every predecessor is already running);
+// a tile publishes its aggregate, warp 0 looks back 32 predecessors at a time until an
+// inclusive prefix, then publishes its own (status word = 2-bit flag | 32-bit value, one
+// 64-bit store). One launch instead of scan_blocks + scan_sums + scan_add.
+constexpr int kLbThreads = 256, kLbItems = 4, kLbTile = kLbThreads * kLbItems;
+
+__device__ __forceinline__ uint32_t lb_exclusive_prefix(unsigned long long* status, long long t, uint32_t tile_total) {
+  volatile unsigned long long* st = status;
+  const int lane = threadIdx.x & 31;
+  constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62;
+  if (t == 0) {
+    if (lane == 0) st[0] = kInc | tile_total;
+    return 0u;
+  }
+  if (lane == 0) st[t] = kAgg | tile_total;
+  uint32_t prefix = 0;
+  for (long long p = t - 1;; p -= 32) {
+    const long long q = p - lane;  // lane 0 = the closest predecessor
+    unsigned long long v = q >= 0 ? st[q] : kInc;
+    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+      if ((v >> 62) == 0) v = st[q];
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const int last = inc ? __ffs(inc) - 1 : 31;
+    uint32_t x = lane <= last ? static_cast<uint32_t>(v) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    prefix += x;
+    if (inc) break;
+  }
+  if (lane == 0) st[t] = kInc | static_cast<unsigned long long>(prefix + tile_total);
+  return prefix;
+}
+
+// In-place exclusive scan of *n_dev u32 (status: [0] ticket, [1..] tile words, zeroed);
+// the grand total to *total, and *overflow += 1 when it exceeds cap (if given).
+__global__ void __launch_bounds__(kLbThreads) scan_lookback_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
+                                                                   unsigned long long* status, unsigned long long* total,
+                                                                   unsigned long long cap = 0,
+                                                                   unsigned long long* overflow = nullptr) {
+  __shared__ uint32_t wsum[33];
+  __shared__ long long s_tile;
+  __shared__ uint32_t s_prefix;
+  const long long n = static_cast<long long>(*n_dev);
+  const long long n_tiles = (n + kLbTile - 1) / kLbTile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = static_cast<long long>(atomicAdd(status, 1ull));
+    __syncthreads();
+    const long long t = s_tile;
+    if (t >= (n_tiles > 0 ? n_tiles : 1)) break;
+    const long long i0 = t * kLbTile + static_cast<long long>(threadIdx.x) * kLbItems;
+    uint32_t v[kLbItems];
+    uint32_t mine = 0;
+    if (i0 + kLbItems <= n && (reinterpret_cast<uintptr_t>(a + i0) & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4*>(a + i0);
+      v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kLbItems; ++k) v[k] = i0 + k < n ? a[i0 + k] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kLbItems; ++k) mine += v[k];
+    uint32_t tile_total;
+    const uint32_t off = block_exclusive_scan(mine, wsum, tile_total);
+    if (threadIdx.x < 32) {
+      const uint32_t pre = lb_exclusive_prefix(status + 1, t, tile_total);
+      if (threadIdx.x == 0) {
+        s_prefix = pre;
+        if (t == (n_tiles > 0 ? n_tiles - 1 : 0)) {
+          const unsigned long long tot = static_cast<unsigned long long>(pre) + tile_total;
+          *total = tot;
+          if (overflow && tot > cap) *overflow += 1;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t run = s_prefix + off;
+    uint32_t o[kLbItems];
+#pragma unroll
+    for (int k = 0; k < kLbItems; ++k) {
+      o[k] = run;
+      run += v[k];
+    }
+    if (i0 + kLbItems <= n && (reinterpret_cast<uintptr_t>(a + i0) & 15) == 0) {
+      *reinterpret_cast<uint4*>(a + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kLbItems; ++k)
+        if (i0 + k < n) a[i0 + k] = o[k];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
                                                                const uint32_t* __restrict__ sums) {
   const long long n = static_cast<long long>(*n_dev);

@@ -956,26 +956,29 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   const long long cap = static_cast<long long>(w.cap_starts);
   ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
   ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
+  ARFX_CUDA(cudaMemsetAsync(w.lb_status.ptr, 0,
+                            static_cast<size_t>((n + kLbTile - 1) / kLbTile + (nkeys + kLbTile - 1) / kLbTile + 4) *
+                                sizeof(unsigned long long),
+                            s));
   m.prof.begin("prune", s);
   src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5, C + 8, static_cast<unsigned long long>(nkeys));
   start_mask_kernel<Src, single><<<resident_grid(start_mask_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
                                    s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
                                                                             stats);
   ARFX_CUDA(cudaGetLastError());
-  // start slots: exclusive scan of the per-target start counts (C6 = total starts)
-  const long long nb = (n + kScanBlock - 1) / kScanBlock;
-  scan_blocks_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
-  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 5, C + 6, static_cast<unsigned long long>(cap),
-                                            C + 3);  // C3 += 1 when the starts exceed the slots
-  scan_add_kernel<<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(w.scount.ptr, C + 5, w.scan_sums.ptr);
+  // start slots: exclusive scan of the per-target start counts (C6 = total starts, C3 += 1
+  // when they exceed the slots), single pass
+  const long long tiles_t = (n + kLbTile - 1) / kLbTile, tiles_k = (nkeys + kLbTile - 1) / kLbTile;
+  unsigned long long* st_t = w.lb_status.ptr;                // [ticket | tiles_t]
+  unsigned long long* st_k = w.lb_status.ptr + tiles_t + 2;  // [ticket | tiles_k]
+  scan_lookback_kernel<<<persistent_grid(scan_lookback_kernel, kLbThreads, 0, n / kLbItems + 1), kLbThreads, 0, s>>>(
+      w.scount.ptr, C + 5, st_t, C + 6, static_cast<unsigned long long>(cap), C + 3);
   // counting sort of the starts by (bone, skinning cell of x0)
   start_key_kernel<Src, single><<<resident_grid(start_key_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
                                   s>>>(
       m.sv, kg, d_poses, src, w.smask.ptr, w.scount.ptr, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr, cap);
-  const long long nbk = (nkeys + kScanBlock - 1) / kScanBlock;
-  scan_blocks_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
-  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(w.scan_sums.ptr, C + 8, C + 9);
-  scan_add_kernel<<<static_cast<unsigned>(nbk), kScanBlock, 0, s>>>(w.key_hist.ptr, C + 8, w.scan_sums.ptr);
+  scan_lookback_kernel<<<persistent_grid(scan_lookback_kernel, kLbThreads, 0, nkeys / kLbItems + 1), kLbThreads, 0,
+                         s>>>(w.key_hist.ptr, C + 8, st_k, C + 9);
   start_place_kernel<<<grid_for(2 * n, 256, 8), 256, 0, s>>>(C + 6, w.keys.ptr, w.unsorted.ptr, w.key_hist.ptr,
                                                             w.items.ptr, cap);
   ARFX_CUDA(cudaGetLastError());
@@ -1063,6 +1066,7 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
   }
   key_hist.ensure(nkeys);
   scan_sums.ensure(std::max(targets, nkeys) / kScanBlock + 2);
+  lb_status.ensure(cap_targets / kLbTile + nkeys / kLbTile + 8);
   // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
   const size_t want = std::max<size_t>({targets * 5 / 2, static_cast<size_t>(1) << 16, min_starts, learned_starts});
   if (want > cap_starts) {
