@@ -488,9 +488,7 @@ __global__ void __launch_bounds__(256) finalize_roots_kernel(Src src, const uint
   }
 }
 
-// ---- exclusive scan of u32 counts (in place), 3 phases --------------------------------
-
-constexpr int kScanBlock = 1024;
+// ---- block-wide exclusive scan (shared by the single-pass scan below) ------------------
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -530,47 +528,11 @@ __global__ void src_count_kernel(Src src, unsigned long long* out, unsigned long
   }
 }
 
-// n: the live element count on the device (grid sized for the capacity; blocks past n exit)
-__global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
-                                                                  uint32_t* __restrict__ block_sums) {
-  __shared__ uint32_t ws[33];
-  const long long n = static_cast<long long>(*n_dev);
-  if (static_cast<long long>(blockIdx.x) * kScanBlock >= n) return;
-  const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
-  const uint32_t v = i < n ? a[i] : 0u;
-  uint32_t total;
-  const uint32_t ex = block_exclusive_scan(v, ws, total);
-  if (i < n) a[i] = ex;
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
-}
-
-// overflow (optional): counted when the grand total exceeds cap
-__global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(uint32_t* __restrict__ sums, const unsigned long long* n_dev,
-                                                                unsigned long long* __restrict__ grand,
-                                                                unsigned long long cap = 0,
-                                                                unsigned long long* overflow = nullptr) {
-  __shared__ uint32_t ws[33];
-  const long long nb = (static_cast<long long>(*n_dev) + kScanBlock - 1) / kScanBlock;
-  uint32_t carry = 0;
-  for (long long b0 = 0; b0 < nb; b0 += kScanBlock) {
-    const long long i = b0 + threadIdx.x;
-    const uint32_t v = i < nb ? sums[i] : 0u;
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan(v, ws, total);
-    if (i < nb) sums[i] = ex + carry;
-    carry += total;
-  }
-  if (threadIdx.x == 0) {
-    *grand = carry;
-    if (overflow && carry > cap) *overflow += 1;
-  }
-}
-
 // ---- single-pass exclusive scan (decoupled look-back) -----------------------------------
 // Tiles of 1024 elements are taken in ticket order (so every predecessor is already running);
 // a tile publishes its aggregate, warp 0 looks back 32 predecessors at a time until an
 // inclusive prefix, then publishes its own (status word = 2-bit flag | 32-bit value, one
-// 64-bit store). One launch instead of scan_blocks + scan_sums + scan_add.
+// 64-bit store). One launch instead of a 3-kernel (blocks, block sums, add) scan.
 constexpr int kLbThreads = 256, kLbItems = 4, kLbTile = kLbThreads * kLbItems;
 
 __device__ __forceinline__ uint32_t lb_exclusive_prefix(unsigned long long* status, long long t, uint32_t tile_total) {
@@ -659,13 +621,6 @@ __global__ void __launch_bounds__(kLbThreads) scan_lookback_kernel(uint32_t* __r
     }
     __syncthreads();
   }
-}
-
-__global__ void __launch_bounds__(kScanBlock) scan_add_kernel(uint32_t* __restrict__ a, const unsigned long long* n_dev,
-                                                               const uint32_t* __restrict__ sums) {
-  const long long n = static_cast<long long>(*n_dev);
-  const long long i = static_cast<long long>(blockIdx.x) * kScanBlock + threadIdx.x;
-  if (i < n) a[i] += sums[blockIdx.x];
 }
 
 }  // namespace arfx

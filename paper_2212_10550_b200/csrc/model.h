@@ -78,7 +78,7 @@ struct Workspace {
   DevBuf<float> fwd_act;  // training forwards: per pool entry X | H1 | H2 | logits (K8a reuses them)
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
-  DevBuf<uint32_t> smask, scount, scan_sums;  // per target: start mask, start count -> slot base
+  DevBuf<uint32_t> smask, scount;  // per target: start mask, start count -> slot base
   DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
   DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
   DevBuf<unsigned long long> lb_status;        // single-pass scans: tickets + tile status words
@@ -100,7 +100,7 @@ struct Workspace {
   Workspace() {
     bind(sx, sy, sz, sdelta, sray, sidx, snroot, sbase, ssel, px, py, pz, powner, pres, ray_first, ray_count,
          row_list, train_terms, tc_tiles, dens_pts, dens_empty, dens_scale, train_rgb, train_alpha, counters,
-         occ_box, fwd_act, smask, scount, scan_sums, items, keys, unsorted, key_hist, lb_status, res4, strans, pgs, pgc,
+         occ_box, fwd_act, smask, scount, items, keys, unsorted, key_hist, lb_status, res4, strans, pgs, pgc,
          pflag, bwd_rec, bwd_list, bwd_partial, bwd_own, bwd_n);
   }
   Workspace(const Workspace&) = delete;

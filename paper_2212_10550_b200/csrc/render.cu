@@ -1065,7 +1065,6 @@ void Workspace::ensure_starts(size_t targets, size_t nkeys, size_t min_starts) {
     cap_targets = targets;
   }
   key_hist.ensure(nkeys);
-  scan_sums.ensure(std::max(targets, nkeys) / kScanBlock + 2);
   lb_status.ensure(cap_targets / kLbTile + nkeys / kLbTile + 8);
   // starts per target: mean ~2 on the body, 0 for most occupancy cells; overflow -> regrow
   const size_t want = std::max<size_t>({targets * 5 / 2, static_cast<size_t>(1) << 16, min_starts, learned_starts});
