@@ -232,9 +232,19 @@ def run_ours(args):
     # grid while building frame i+1's grid on a concurrent branch; two graphs alternate the
     # roles of (pose handle, occupancy grid) A/B. Every frame is still one grid build + one
     # render; only their overlap across consecutive frames changes.
-    pipelined = world == 1 and not args.no_graph and not args.no_pipeline
+    pipelined = world == 1 and not shard_grid and not args.no_graph and not args.no_pipeline
+    # N > 1 (grid shards): the same overlap with the exchange -- frame i+1's grid shard, the
+    # all-gather of its blocks and the unshard + mask run on a side stream (side workspace)
+    # while frame i renders on the main stream
+    pipe_dist = shard_grid and not args.no_graph and not args.no_pipeline
     pv = [gview, arf.PosedModelView(model, poses[0])]
-    pocc = [occ, arf.OccupancyGrid(model.normalized_box, occ_cfg)] if pipelined else [occ]
+    pocc = [occ, arf.OccupancyGrid(model.normalized_box, occ_cfg)] if (pipelined or pipe_dist) else [occ]
+    if pipe_dist:
+        side = torch.cuda.Stream()
+        ssp = C.c_void_p(side.cuda_stream)
+        dvals = [device_view(o.device_arrays()[0], o.cell_count()) for o in pocc]
+        dslab = [v[rank * slab:(rank + 1) * slab] for v in dvals]
+        s_cnt = torch.zeros((2, 4), dtype=torch.int64, device="cuda")
     pstate = {"phase": 0, "next": None}  # next: the frame whose grid the current handle holds
 
     def make_graphs():
@@ -251,6 +261,18 @@ def run_ours(args):
                 hs.append(h)
             pstate["next"] = None  # the handles' contents are unknown after a capture's warm-up
             return hs
+        if pipe_dist:  # per grid X: shard (side workspace), unshard + mask, render
+            for x in range(2):
+                for pmask, stream_p, cnt_p in ((2 | 64, ssp, s_cnt), (16, ssp, s_cnt), (8, sp, g_cnt)):
+                    h = C.c_void_p()
+                    check(L.arfx_frame_graph_create(model._h, pv[x]._h, C.byref(ccam), pocc[x]._h, C.byref(copt), rank,
+                                                    world, pmask, C.c_void_p(d_rgb.data_ptr()),
+                                                    C.c_void_p(d_alpha.data_ptr()), C.c_void_p(cnt_p.data_ptr()),
+                                                    stream_p, C.byref(h)))
+                    hs.append(h)
+            pstate["next"] = None
+            torch.cuda.synchronize()
+            return hs
         for pmask in ([2, 16 | 8] if shard_grid else [1 | 8]):
             h = C.c_void_p()
             check(L.arfx_frame_graph_create(model._h, gview._h, C.byref(ccam), occ._h, C.byref(copt), rank, world,
@@ -263,18 +285,21 @@ def run_ours(args):
 
     recaptures = [0]
 
-    def launch_graph(k):
+    def launch_graph_on(k, stream_p):
         # a graph whose workspace grew since capture is refused by the library (stale pointers):
         # re-capture it (never inside the timed region: the warm-up frames size the workspace)
         nonlocal graphs
         try:
-            check(L.arfx_frame_graph_launch(graphs[k], sp))
+            check(L.arfx_frame_graph_launch(graphs[k], stream_p))
         except InvalidArgument:
             for h in graphs:
                 check(L.arfx_frame_graph_destroy(h))
             graphs = make_graphs()
             recaptures[0] += 1
-            check(L.arfx_frame_graph_launch(graphs[k], sp))
+            check(L.arfx_frame_graph_launch(graphs[k], stream_p))
+
+    def launch_graph(k):
+        launch_graph_on(k, sp)
 
     def frame_pipelined(i, slot):
         ph = pstate["phase"]
@@ -286,9 +311,31 @@ def run_ours(args):
         d_cnt[slot, 1].copy_(g_cnt[1])
         pstate["phase"], pstate["next"] = 1 - ph, i + 1
 
+    def grid_dist(x, i, stream_obj, stream_p, launch):
+        """frame i's grid into pocc[x] through graphs: shard, all-gather of the blocks, mask."""
+        check(L.arfx_pose_copy(pv[x]._h, views[i % N_FRAMES]._h, stream_p))
+        launch(3 * x + 0, stream_p)
+        with torch.cuda.stream(stream_obj):
+            dist.all_gather_into_tensor(dvals[x], dslab[x])
+        launch(3 * x + 1, stream_p)
+
+    def frame_dist_pipelined(i, slot):
+        ph = pstate["phase"]
+        nx = 1 - ph
+        if pstate["next"] != i:  # prime: frame i's grid on the main stream
+            grid_dist(ph, i, torch.cuda.current_stream(), sp, launch_graph_on)
+        side.wait_stream(torch.cuda.current_stream())  # render i-1 (grid nx) is done with it
+        grid_dist(nx, i + 1, side, ssp, launch_graph_on)
+        launch_graph_on(3 * ph + 2, sp)  # render frame i with pocc[ph]
+        torch.cuda.current_stream().wait_stream(side)
+        d_cnt[slot, 1].copy_(g_cnt[1])
+        pstate["phase"], pstate["next"] = nx, i + 1
+
     def frame_graph(i, slot):
         if pipelined:
             return frame_pipelined(i, slot)
+        if pipe_dist:
+            return frame_dist_pipelined(i, slot)
         # `graphs` is looked up at call time (re-captured for the other decoder below)
         check(L.arfx_pose_copy(gview._h, views[i % N_FRAMES]._h, sp))
         launch_graph(0)
@@ -389,7 +436,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         rgb = d_rgb.cpu().numpy().reshape(H_IMG, W_IMG, 3)
         alpha = d_alpha.cpu().numpy().reshape(H_IMG, W_IMG)
-        mask = pocc[1 - pstate["phase"]].mask if pipelined else occ.mask  # the grid frame j rendered with
+        mask = pocc[1 - pstate["phase"]].mask if (pipelined or pipe_dist) else occ.mask  # frame j's grid
         d = np.concatenate([np.abs(rgb - rrgb).ravel(), np.abs(alpha - ralpha).ravel()])
         r = np.concatenate([np.abs(rrgb).ravel(), np.abs(ralpha).ravel()])
         parity[decoder] = {"frame": j, "mask_equal": bool(np.array_equal(mask, rmask)),
@@ -441,6 +488,8 @@ def run_ours(args):
                 "render_decoder": args.mlp,
                 "frame_launch": ("cuda_graph, pipelined: frame i's render || frame i+1's grid build (two graphs "
                                  "alternating pose handles and occupancy grids)" if pipelined else
+                                 "cuda_graphs, pipelined: frame i's render || frame i+1's grid shard + NCCL all-gather "
+                                 "+ mask on a side stream" if pipe_dist else
                                  "cuda_graph (pose copied into the captured handle per frame)") if graphs else "direct",
                 "graph_recaptures_outside_timed_region": recaptures[0],
                 "other_decoder": {"mlp": other, "value": K / (ms_other / 1000.0), "ms_per_step": ms_other / K}}

@@ -455,7 +455,8 @@ enum {
   ARFX_GRAPH_GRID_SHARD = 2,
   ARFX_GRAPH_MASK = 4,
   ARFX_GRAPH_RENDER = 8,
-  ARFX_GRAPH_MASK_SHARDS = 16 /* as arfx_occ_rebuild_mask_shards_async(occ, nshards) */
+  ARFX_GRAPH_MASK_SHARDS = 16, /* as arfx_occ_rebuild_mask_shards_async(occ, nshards) */
+  ARFX_GRAPH_SIDE_WORKSPACE = 64 /* capture on the side workspace: may run beside a main-workspace graph */
 };
 /* Captures the chosen parts of one frame for pose handle p as a CUDA graph: the inference
  * grid (GRID) or its z-slab shard (GRID_SHARD), the mask rebuild (MASK), the render into

@@ -1051,7 +1051,7 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
   return guard([&] {
     require(mh && ph && out, "frame_graph_create: null argument");
     require(parts > 0 && (parts & ~(ARFX_GRAPH_GRID | ARFX_GRAPH_GRID_SHARD | ARFX_GRAPH_MASK | ARFX_GRAPH_RENDER |
-                                    ARFX_GRAPH_MASK_SHARDS)) == 0,
+                                    ARFX_GRAPH_MASK_SHARDS | ARFX_GRAPH_SIDE_WORKSPACE)) == 0,
             "frame_graph_create: bad parts");
     require(!((parts & ARFX_GRAPH_MASK) && (parts & ARFX_GRAPH_MASK_SHARDS)), "frame_graph_create: mask or shard mask");
     require(!((parts & ARFX_GRAPH_GRID) && (parts & ARFX_GRAPH_GRID_SHARD)), "frame_graph_create: grid or shard");
@@ -1071,6 +1071,10 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
     const cudaStream_t s = stream_of(m, stream);
     require(s != nullptr, "frame_graph_create: needs a non-NULL stream");
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counters);
+    // SIDE_WORKSPACE: capture on the model's side workspace, so this graph may run
+    // concurrently with one captured on the main workspace (e.g. the next frame's grid shard
+    // beside the current frame's render)
+    WorkspaceScope scope(m, (parts & ARFX_GRAPH_SIDE_WORKSPACE) ? m.ws_side : m.ws());
     auto enqueue = [&] {
       if (parts & ARFX_GRAPH_GRID) inference_grid(m, ph->impl, occ->impl, cnt, s);
       if (parts & ARFX_GRAPH_GRID_SHARD) inference_grid_shard(m, ph->impl, occ->impl, shard, nshards, cnt, s);
