@@ -446,54 +446,87 @@ __global__ void __launch_bounds__(256) grid_scatter_kernel(FieldView F, const do
   const long long n = static_cast<long long>(*n_list);
   const int lane = threadIdx.x & 31;
   const long long chunks = (n + 31) / 32;
-  const long long total = chunks * F.L;
+  // a warp task = 32 consecutive queries x kScatterLevels levels (1: the most tasks -- more
+  // levels per task normalise the point fewer times but were measured slower, 30 -> 35 / 41 /
+  // 102 us for 2 / 4 / 16); each level's corners are aggregated over the warp
+#ifndef ARFX_SCATTER_LEVELS
+#define ARFX_SCATTER_LEVELS 1
+#endif
+  constexpr int kScatterLevels = ARFX_SCATTER_LEVELS;
+  const int groups = (F.L + kScatterLevels - 1) / kScatterLevels;
+  const long long total = chunks * groups;
   for (long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gw < total;
        gw += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const int l = static_cast<int>(gw % F.L);
-    const long long k = (gw / F.L) * 32 + lane;
+    const int l0 = static_cast<int>(gw % groups) * kScatterLevels;
+    const long long k = (gw / groups) * 32 + lane;
     const bool act = k < n;
-    LevelCorners lc;
-    float d0 = 0.0f, d1 = 0.0f;
+    double u[3] = {0.0, 0.0, 0.0};
     if (act) {
       const long long q = list[k];
-      double u[3];
       normalize_point(F, make3(px[q], py[q], pz[q]), u);
-      level_corners(F, l, u, lc);
-      d0 = rec[k * kRecStride + kRecDin + 2 * l];
-      d1 = rec[k * kRecStride + kRecDin + 2 * l + 1];
     }
-    float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
+    for (int l = l0; l < l0 + kScatterLevels && l < F.L; ++l) {
+      LevelCorners lc;
+      float d0 = 0.0f, d1 = 0.0f;
+      if (act) {
+        level_corners(F, l, u, lc);
+        d0 = rec[k * kRecStride + kRecDin + 2 * l];
+        d1 = rec[k * kRecStride + kRecDin + 2 * l + 1];
+      }
+      float* gt = grid_grad + static_cast<size_t>(l) * F.T * 2;
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      const bool has = act && lc.w[c] != 0.0f;
-      const uint32_t key = has ? lc.idx[c] : 0xffffffffu;
-      const float v0 = has ? fmul(lc.w[c], d0) : 0.0f, v1 = has ? fmul(lc.w[c], d1) : 0.0f;
-      const unsigned g = __match_any_sync(0xffffffffu, key);
-      if (Det) {
-        // fixed point: exact integer sums, independent of which lanes / warps meet a row
-        const long long i0 = f32_to_fix(v0), i1 = f32_to_fix(v1);
-        long long a0 = 0, a1 = 0;
-        for (unsigned mm = g; mm; mm &= mm - 1) {
-          const int src = __ffs(mm) - 1;
-          a0 += __shfl_sync(g, i0, src);
-          a1 += __shfl_sync(g, i1, src);
+      for (int c = 0; c < 8; ++c) {
+        const bool has = act && lc.w[c] != 0.0f;
+        const uint32_t key = has ? lc.idx[c] : 0xffffffffu;
+        const float v0 = has ? fmul(lc.w[c], d0) : 0.0f, v1 = has ? fmul(lc.w[c], d1) : 0.0f;
+        const unsigned g = __match_any_sync(0xffffffffu, key);
+        if (Det) {
+          // fixed point: exact integer sums, independent of which lanes / warps meet a row
+          long long a0 = f32_to_fix(v0), a1 = f32_to_fix(v1);
+          if (g == 0xffffffffu) {  // the whole warp on one row (coarse levels): butterfly
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+              a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            }
+          } else {
+            const long long i0 = a0, i1 = a1;
+            a0 = a1 = 0;
+            for (unsigned mm = g; mm; mm &= mm - 1) {
+              const int src = __ffs(mm) - 1;
+              a0 += __shfl_sync(g, i0, src);
+              a1 += __shfl_sync(g, i1, src);
+            }
+          }
+          if (has && lane == __ffs(g) - 1) {
+            unsigned long long* ga =
+                reinterpret_cast<unsigned long long*>(grid_acc + 2 * (static_cast<size_t>(l) * F.T + key));
+            atomicAdd(ga + 0, static_cast<unsigned long long>(a0));
+            atomicAdd(ga + 1, static_cast<unsigned long long>(a1));
+          }
+          continue;
         }
-        if (has && lane == __ffs(g) - 1) {
-          unsigned long long* ga =
-              reinterpret_cast<unsigned long long*>(grid_acc + 2 * (static_cast<size_t>(l) * F.T + key));
-          atomicAdd(ga + 0, static_cast<unsigned long long>(a0));
-          atomicAdd(ga + 1, static_cast<unsigned long long>(a1));
+        float s0, s1;
+        if (g == 0xffffffffu) {  // f32 atomics are unordered anyway: any summation order
+          s0 = v0;
+          s1 = v1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            s0 = fadd(s0, __shfl_xor_sync(0xffffffffu, s0, o));
+            s1 = fadd(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+          }
+        } else {
+          s0 = 0.0f;
+          s1 = 0.0f;
+          for (unsigned mm = g; mm; mm &= mm - 1) {
+            const int src = __ffs(mm) - 1;
+            s0 = fadd(s0, __shfl_sync(g, v0, src));
+            s1 = fadd(s1, __shfl_sync(g, v1, src));
+          }
         }
-        continue;
+        // one 8-byte vector atomic per row (sm_90+), both features
+        if (has && lane == __ffs(g) - 1) atomicAdd(reinterpret_cast<float2*>(gt) + key, make_float2(s0, s1));
       }
-      float s0 = 0.0f, s1 = 0.0f;
-      for (unsigned mm = g; mm; mm &= mm - 1) {
-        const int src = __ffs(mm) - 1;
-        s0 = fadd(s0, __shfl_sync(g, v0, src));
-        s1 = fadd(s1, __shfl_sync(g, v1, src));
-      }
-      // one 8-byte vector atomic per row (sm_90+), both features
-      if (has && lane == __ffs(g) - 1) atomicAdd(reinterpret_cast<float2*>(gt) + key, make_float2(s0, s1));
     }
   }
 }

@@ -42,7 +42,8 @@ def main(steps=4):
         print(f"\n== stream {s}: {len(es)} kernels, busy {busy / steps:.1f} us/step")
         agg = {}
         for e in es:
-            nm = e["name"].split("(")[0].replace("void ", "").replace("arfx::", "").replace("(anonymous namespace)::", "")
+            nm = e["name"].replace("(anonymous namespace)::", "").replace("void ", "").replace("arfx::", "")
+            nm = nm.split("(")[0]
             a = agg.setdefault(nm[:60], [0, 0.0])
             a[0] += 1
             a[1] += e["dur"]
