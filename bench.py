@@ -512,7 +512,7 @@ def run_ours(args):
                                       reference="oracle/_ref arf::build_model_inference_grid + render_model")
         if world == 1 and not args.no_extra:
             line["extra_configs"] = {"correspondence_microbench": bench_microbench(5, not args.no_cpu_baseline),
-                                     "train_step_4096": bench_train(model, 10, not args.no_cpu_baseline),
+                                     "train_step_4096": bench_train(model, 50, not args.no_cpu_baseline),
                                      "train_step_full": bench_train_full(200)}
             rk, seq_ms, counts = bench_train_roofline(48, peaks, peak_kind, (p64.value, p32.value))
             tsf = line["extra_configs"]["train_step_full"]

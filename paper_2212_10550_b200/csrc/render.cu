@@ -991,7 +991,7 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   m.prof.begin(name, s);
   kern<<<grid, kDsThreads, smem, s>>>(m.sv, d_poses, m.inv, src, w.items.ptr, C + 6, w.smask.ptr, w.scount.ptr,
                                       w.res4.ptr, C + 4, stats,
-                                      static_cast<long long>(w.cap_starts));
+                                      static_cast<long long>(w.cap_starts), (expect >= 0 ? expect : n) < kBlockQueueMaxTargets);
   ARFX_CUDA(cudaGetLastError());
   m.prof.end(s);
   m.prof.begin("finalize", s);
