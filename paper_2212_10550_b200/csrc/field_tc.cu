@@ -40,6 +40,9 @@ namespace {
 using namespace umma;
 
 constexpr int kTcTile = 128;
+#ifndef ARFX_TC_REVERSE
+#define ARFX_TC_REVERSE 1
+#endif
 constexpr int kIn = 32, kHid = 64, kOutPad = 16;
 constexpr uint32_t kTmemCols = 512;  // 4 groups x 128 columns (whole TMEM: one CTA per SM)
 
@@ -227,9 +230,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
         : "memory");
   };
   const long long stride = static_cast<long long>(gridDim.x) * kGroups * kTcTile;
+  // tiles are consumed in reverse order of production: the encode pass writes ~150 MB of
+  // tiles through a 126 MB L2, so the last-written tiles are the ones still resident
+  const long long n_tiles = (n + kTcTile - 1) / kTcTile;
+  auto phys = [&](long long lt) { return ARFX_TC_REVERSE ? (n_tiles - 1 - lt / kTcTile) * kTcTile : lt; };
   const long long first = (static_cast<long long>(blockIdx.x) * kGroups + g) * kTcTile;
-  if (tid == 0 && first < n) load_tile(first);
-  for (long long t0 = first; t0 < n; t0 += stride) {
+  if (tid == 0 && first < n) load_tile(phys(first));
+  for (long long lt0 = first; lt0 < n; lt0 += stride) {
+    const long long t0 = phys(lt0);
     const long long q = t0 + tid;
     const bool ok = q < n && owner[q] >= 0;
     mbar_wait(lbar, lphase);  // this tile's features have landed in A0
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
     phase ^= 1;
     tc_fence_after();
     // A0 is free again: the next tile's copy overlaps the rest of this one
-    if (tid == 0 && t0 + stride < n) load_tile(t0 + stride);
+    if (tid == 0 && lt0 + stride < n) load_tile(phys(lt0 + stride));
     // ---- epilogue 0: + b0, ReLU -> A1 ----
 #pragma unroll
     for (int c = 0; c < kHid; c += 16) {
