@@ -609,8 +609,17 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     entry("field", "fp32", Q * 13312, "TFLOP/s", fp32_peak, f32src, "f32 mul+add of encode+MLP, 13312/query")
     # K3 field on tcgen05: 2*(32*64 + 64*64 + 64*4) = 12800 algorithmic MLP flops per query
     # (the split-bf16 scheme issues 3 MMAs per product and pads the head to N=16: not counted)
-    entry("field_tc", "tensor", QT * 12800, "TFLOP/s", peaks.get("bf16_tflops"),
-          f"MEASURED_PEAKS.json bf16_tflops ({peak_kind})", "12800 MLP flops/query (algorithmic)")
+    if "encode_tc" in prof:  # two-stage build (ARFX_TC_FUSED=0): the MMA stage streams tiles
+        entry("field_tc", "tensor", QT * 12800, "TFLOP/s", peaks.get("bf16_tflops"),
+              f"MEASURED_PEAKS.json bf16_tflops ({peak_kind})", "12800 MLP flops/query (algorithmic)")
+    else:  # fused encode -> tcgen05 MLP: the hash-table gathers bind, the tensor pipe idles
+        entry("field_tc", "l2/l1 gathers", QT * (1024 + 16), "GB/s", hbm,
+              f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); gathers are L2-resident, so frac is vs HBM for scale only",
+              "1024 B gathered + 16 B (density, rgb) written per query; + 12800 MLP flops/query on tcgen05")
+        if "field_tc" in out and peaks.get("bf16_tflops"):
+            e = out["field_tc"]
+            e["tensor_tflops"] = QT * 12800 / (prof["field_tc"][0] * 1e-3) / 1e12
+            e["tensor_frac"] = e["tensor_tflops"] / peaks["bf16_tflops"]
     # K3 encode stage of the tcgen05 decoder: 16 levels x 8 corners x 8 B gathered (f32 table)
     # + 128 B of split-bf16 features written per query; the table is L2-resident (64 MiB)
     entry("encode_tc", "l2/l1 gathers", QT * (1024 + 128), "GB/s", hbm,
@@ -624,7 +633,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     # written (8 B); per start key + item written, read back, sorted item written (20 B)
     n_targets = posed + 64 ** 3 * K  # render samples + occupancy cells
     entry("prune", "hbm", 32.0 * n_targets + 20.0 * S, "GB/s", hbm, f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-          "32 B/target + 20 B/start (mask/count, sort keys, items); 9 launches incl. 3-kernel scans")
+          "32 B/target + 20 B/start (mask/count, sort keys, items); 6 launches incl. 2 single-pass look-back scans")
     # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
     entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")

@@ -12,6 +12,10 @@
 #include "arfx_internal.h"
 #include "exact.cuh"
 
+#ifndef ARFX_PAIR_GATHER
+#define ARFX_PAIR_GATHER 1
+#endif
+
 namespace arfx {
 
 constexpr int kMlpGenericMaxWidth = 256;
@@ -264,8 +268,23 @@ __device__ __forceinline__ float2 encode_level_f2(const FieldView& F, int l, con
   level_corners(F, l, u, lc);
   const float2* t = reinterpret_cast<const float2*>(F.grid) + static_cast<size_t>(l) * F.T;
   float2 row[8];
+#if ARFX_PAIR_GATHER
+  // x-neighbour corners (k, k+1) often share one 16-B aligned row pair: always for hashed
+  // levels with an even x (idx ^ 1), for direct/wrap levels when idx is even. One 16-B load of
+  // the aligned pair holding corner k, plus an 8-B load of corner k+1 only where it lies
+  // outside that pair: fewer L1 wavefronts for the same rows (the table base is 256-B aligned)
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t a = lc.idx[k], b = lc.idx[k + 1];
+    const float4 c = __ldg(reinterpret_cast<const float4*>(t + (a & ~1u)));
+    const float2 e0 = make_float2(c.x, c.y), e1 = make_float2(c.z, c.w);
+    row[k] = (a & 1u) ? e1 : e0;
+    row[k + 1] = ((a ^ b) <= 1u) ? ((b & 1u) ? e1 : e0) : __ldg(t + b);
+  }
+#else
 #pragma unroll
   for (int k = 0; k < 8; ++k) row[k] = __ldg(t + lc.idx[k]);
+#endif
   float o0 = 0.0f, o1 = 0.0f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {

@@ -1,11 +1,15 @@
-// field_tc.cu -- K3 on the 5th-gen tensor cores, in two stages:
+// field_tc.cu -- K3 on the 5th-gen tensor cores.
 //
+// Default (ARFX_TC_FUSED=1): field_fused_kernel, encode and the 32-64-64-4 decoder in one
+// persistent warp-specialised kernel (no feature tiles in HBM; see the comment above it).
+//
+// Two-stage alternative (ARFX_TC_FUSED=0, measured 0.463 vs 0.426 ms/frame for the fused one):
 //   encode_tiles_kernel  thread = query, 16 hash-grid levels (warp-uniform level, exact f64
 //                        corner weights as field_tile_kernel); the 32 features are split into
 //                        bf16 hi / lo planes and written straight into the UMMA K-major,
 //                        no-swizzle canonical layout of their 128-query tile in global memory
 //                        (coalesced 512-B stores). High occupancy: this stage is the gathers.
-//   field_tc_kernel      the 32-64-64-4 decoder: one persistent 512-thread CTA per SM runs 4
+//   field_tc_kernel      the decoder: one persistent 512-thread CTA per SM runs 4
 //                        independent 128-query pipelines (own TMEM columns, mbarriers, named
 //                        barrier) over weights staged once in smem. Per tile:
 //     load     one cp.async.bulk of the 16-KB feature tile into the group's A0 buffer (the
@@ -17,7 +21,7 @@
 //     layer 2  D[128x16] = A1[128x64] * W2p^T   4 x 3 MMAs, W2 padded to N = 16, cols [64, 80)
 //     epi 2    + b2, softplus / logistic (R/field.hpp:78-81) -> (density, rgb)
 //   One thread issues the MMAs (tcgen05.mma kind::f16); completion is signalled with
-//   tcgen05.commit on an mbarrier.
+//   tcgen05.commit on an mbarrier. The fused kernel runs the same three layers.
 //
 // Operands are split bf16 pairs (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)) and every
 // product is formed as hi*hi + hi*lo + lo*hi (bf16 in, fp32 accumulate in TMEM): ~16
@@ -40,6 +44,9 @@ namespace {
 using namespace umma;
 
 constexpr int kTcTile = 128;
+#ifndef ARFX_TC_FUSED
+#define ARFX_TC_FUSED 1
+#endif
 #ifndef ARFX_TC_REVERSE
 #define ARFX_TC_REVERSE 1
 #endif
@@ -315,6 +322,260 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
                  : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused encode -> MLP (K3-TC fused, warp-specialised): no feature tiles in HBM. One persistent
+// CTA per SM:
+//   gather groups  kWG groups of kWS x 4 warps; a group owns kWB A0 buffers (split-bf16
+//                  K-major, 2 x 8 KB) and loops over its 128-query tiles: wait until the
+//                  buffer is free, thread (row r, level slice s) gathers levels
+//                  [16 s / kWS, 16 (s+1) / kWS) of query r straight into it, then one arrive
+//                  on the buffer's `full` barrier. These warps never wait on the tensor core
+//                  beyond the buffer hand-back, so they keep the L1 gather pipe busy.
+//   MMA team       4 warps (TMEM lane quarters 0-3): takes the filled buffers in a fixed
+//                  round-robin order, issues layer 0 (whose completion, committed to the
+//                  buffer's `empty` barrier, hands the buffer back), runs the three epilogues
+//                  through its own hidden tile A1 (2 x 16 KB) and writes (density, rgb).
+// The smem footprint (weights 29 KB + A1 32 KB + 16 KB per A0 buffer) stays small so the
+// unified L1 keeps most of its capacity for the hash-table gathers.
+#ifndef ARFX_WS_GROUPS
+#define ARFX_WS_GROUPS 3
+#endif
+#ifndef ARFX_WS_SPLIT
+#define ARFX_WS_SPLIT 2
+#endif
+#ifndef ARFX_WS_BUFS
+#define ARFX_WS_BUFS 1
+#endif
+constexpr int kWG = ARFX_WS_GROUPS, kWS = ARFX_WS_SPLIT, kWB = ARFX_WS_BUFS;
+constexpr int kWGroupThreads = kTcTile * kWS, kWMma = 128;
+constexpr int kWThreads = kWMma + kWG * kWGroupThreads;
+constexpr int kWBarMma = 15;  // named barrier of the MMA team (gather groups use 1..kWG)
+static_assert(kWThreads <= 1024 && kWG < kWBarMma && (kWS == 1 || kWS == 2 || kWS == 4), "fused layout");
+
+struct WsSmem {
+  static constexpr int B0 = TcSmem::B0, B1 = TcSmem::B1, B2 = TcSmem::B2, BIAS = TcSmem::BIAS;
+  static constexpr int A0P = TcSmem::A0P, A1P = TcSmem::A1P;
+  static constexpr int A1 = TcSmem::ACT;                  // MMA team's hidden tile (2 x 16 KB)
+  static constexpr int A0 = A1 + 2 * A1P;                 // [kWG][kWB] feature tiles (2 x 8 KB)
+  static constexpr int FULL = A0 + kWG * kWB * 2 * A0P;   // u64 [kWG * kWB]
+  static constexpr int EMPTY = FULL + 8 * kWG * kWB;      // u64 [kWG * kWB]
+  static constexpr int MMA = EMPTY + 8 * kWG * kWB;       // u64
+  static constexpr int TADDR = MMA + 8;
+  static constexpr int TOTAL = TADDR + 16;
+};
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+template <bool kHalf>
+__global__ void __launch_bounds__(kWThreads, 1)
+    field_fused_kernel(FieldView F, const __half2* __restrict__ table_h2, const double* __restrict__ px,
+                       const double* __restrict__ py, const double* __restrict__ pz,
+                       const int32_t* __restrict__ owner, float4* __restrict__ res, const unsigned long long* n_dev,
+                       long long cap, unsigned long long* stats) {
+  extern __shared__ __align__(1024) unsigned char tc_smem[];
+  long long n = static_cast<long long>(*n_dev);
+  n = n < cap ? n : cap;
+  if (static_cast<long long>(blockIdx.x) * kTcTile * kWG >= n) return;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem));
+  float* bias = reinterpret_cast<float*>(tc_smem + WsSmem::BIAS);
+  uint32_t* taddr_smem = reinterpret_cast<uint32_t*>(tc_smem + WsSmem::TADDR);
+  const int ctid = threadIdx.x;
+  auto full_bar = [&](int g, int b) { return sbase + WsSmem::FULL + 8 * (g * kWB + b); };
+  auto empty_bar = [&](int g, int b) { return sbase + WsSmem::EMPTY + 8 * (g * kWB + b); };
+  auto a0_off = [&](int g, int b) { return WsSmem::A0 + (g * kWB + b) * 2 * WsSmem::A0P; };
+  const uint32_t mma_bar = sbase + WsSmem::MMA;
+  // tile of group g in round r (static round-robin over the grid's groups)
+  auto tile_q0 = [&](int g, int r) {
+    return ((static_cast<long long>(r) * gridDim.x + blockIdx.x) * kWG + g) * kTcTile;
+  };
+
+  // ---- stage the weights (W[o][i] is N x K, K-major), barriers, TMEM ----
+  const float* W0 = F.mlp;
+  const float* b0 = W0 + kIn * kHid;
+  const float* W1 = b0 + kHid;
+  const float* b1 = W1 + kHid * kHid;
+  const float* W2 = b1 + kHid;
+  const float* b2 = W2 + 4 * kHid;
+  auto put = [&](int off, int plane, float x) {
+    __nv_bfloat16 hi, lo;
+    split_bf16(x, hi, lo);
+    *reinterpret_cast<__nv_bfloat16*>(tc_smem + off) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(tc_smem + off + plane) = lo;
+  };
+  for (int i = ctid; i < kHid * kIn; i += kWThreads) {
+    const int o = i / kIn, k = i % kIn;
+    put(WsSmem::B0 + kmaj_off(o, k, kHid), TcSmem::B0P, __ldg(W0 + i));
+  }
+  for (int i = ctid; i < kHid * kHid; i += kWThreads) {
+    const int o = i / kHid, k = i % kHid;
+    put(WsSmem::B1 + kmaj_off(o, k, kHid), TcSmem::B1P, __ldg(W1 + i));
+  }
+  for (int i = ctid; i < kOutPad * kHid; i += kWThreads) {
+    const int o = i / kHid, k = i % kHid;
+    put(WsSmem::B2 + kmaj_off(o, k, kOutPad), TcSmem::B2P, o < 4 ? __ldg(W2 + o * kHid + k) : 0.0f);
+  }
+  for (int i = ctid; i < kHid; i += kWThreads) {
+    bias[i] = __ldg(b0 + i);
+    bias[64 + i] = __ldg(b1 + i);
+  }
+  if (ctid < 4) bias[128 + ctid] = __ldg(b2 + ctid);
+  if (ctid < kWG * kWB) {
+    const int g = ctid / kWB, b = ctid % kWB;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(g, b)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(g, b)) : "memory");
+  }
+  if (ctid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_bar) : "memory");
+  if (ctid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbase + WsSmem::TADDR),
+                 "n"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (ctid >= kWMma) {
+    // ================= gather group =================
+    const int g = (ctid - kWMma) / kWGroupThreads;
+    const int gt = (ctid - kWMma) % kWGroupThreads;
+    const int wg = gt >> 5;
+    const int row = (wg & 3) * 32 + (gt & 31);
+    const int slice = wg >> 2;
+    constexpr int kLv = 16 / kWS;
+    for (int r = 0;; ++r) {
+      const long long q0 = tile_q0(g, r);
+      if (q0 >= n) break;
+      const int b = r % kWB;
+      const long long q = q0 + row;
+      const bool ok = q < n && owner[q] >= 0;
+      if (stats && slice == 0) {
+        const unsigned c = __popc(__ballot_sync(0xffffffffu, ok));
+        if ((gt & 31) == 0 && c) atomicAdd(stats + 6, static_cast<unsigned long long>(c));
+      }
+      double u[3];
+      if (ok) normalize_point(F, make3(px[q], py[q], pz[q]), u);
+      mbar_wait(empty_bar(g, b), ((r / kWB) & 1) ^ 1);  // layer 0 has consumed this buffer
+      if (ok) {
+        const int A = a0_off(g, b);
+#pragma unroll 1
+        for (int l = slice * kLv; l < (slice + 1) * kLv; l += 4) {
+          __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 o = kHalf ? encode_level_h2(F, table_h2, l + j, u) : encode_level_f2(F, l + j, u);
+            split_bf16(o.x, hi[2 * j], lo[2 * j]);
+            split_bf16(o.y, hi[2 * j + 1], lo[2 * j + 1]);
+          }
+          *reinterpret_cast<uint4*>(tc_smem + A + kmaj_off(row, 2 * l, kTcTile)) =
+              *reinterpret_cast<const uint4*>(hi);
+          *reinterpret_cast<uint4*>(tc_smem + A + WsSmem::A0P + kmaj_off(row, 2 * l, kTcTile)) =
+              *reinterpret_cast<const uint4*>(lo);
+        }
+      }
+      fence_async_smem();  // generic-proxy stores -> visible to the tensor core
+      named_sync(1 + g, kWGroupThreads);
+      if (gt == 0) mbar_arrive(full_bar(g, b));
+    }
+  } else {
+    // ================= MMA team =================
+    const int row = ctid;  // TMEM lane = warp quarter * 32 + lane
+    const uint32_t lane_off = static_cast<uint32_t>((ctid >> 5) * 32) << 16;
+    const uint32_t t_hid = *taddr_smem, t_out = *taddr_smem + 64;
+    constexpr uint32_t ID64 = idesc_bf16(128, 64);
+    constexpr uint32_t ID16 = idesc_bf16(128, 16);
+    uint32_t mphase = 0;
+    auto put8 = [&](int c, const float* x) {  // row `row`, columns [c, c+8) of A1
+      __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) split_bf16(x[j], hi[j], lo[j]);
+      *reinterpret_cast<uint4*>(tc_smem + WsSmem::A1 + kmaj_off(row, c, kTcTile)) =
+          *reinterpret_cast<const uint4*>(hi);
+      *reinterpret_cast<uint4*>(tc_smem + WsSmem::A1 + WsSmem::A1P + kmaj_off(row, c, kTcTile)) =
+          *reinterpret_cast<const uint4*>(lo);
+    };
+    auto hidden_epilogue = [&](int boff) {
+#pragma unroll
+      for (int c = 0; c < kHid; c += 16) {
+        float v[16];
+        tmem_ld16(t_hid + lane_off + c, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias[boff + c + j], 0.f);
+        put8(c, v);
+        put8(c + 8, v + 8);
+      }
+    };
+    auto wait_mma = [&]() {
+      mbar_wait(mma_bar, mphase);
+      mphase ^= 1;
+      tc_fence_after();
+    };
+    for (int r = 0;; ++r) {
+      if (tile_q0(0, r) >= n) break;
+      for (int g = 0; g < kWG; ++g) {
+        const long long q0 = tile_q0(g, r);
+        if (q0 >= n) break;
+        const int b = r % kWB;
+        mbar_wait(full_bar(g, b), (r / kWB) & 1);
+        tc_fence_after();
+        // ---- layer 0: its completion also hands the feature buffer back ----
+        if (row == 0) {
+          mma_split(t_hid, sbase + a0_off(g, b), WsSmem::A0P, kTcTile, sbase + WsSmem::B0, TcSmem::B0P, kHid, kIn,
+                    ID64);
+          mma_commit(empty_bar(g, b));
+          mma_commit(mma_bar);
+        }
+        wait_mma();
+        hidden_epilogue(0);  // + b0, ReLU -> A1
+        tc_fence_before();
+        fence_async_smem();
+        named_sync(kWBarMma, kWMma);
+        // ---- layer 1 ----
+        if (row == 0) {
+          tc_fence_after();
+          mma_split(t_hid, sbase + WsSmem::A1, WsSmem::A1P, kTcTile, sbase + WsSmem::B1, TcSmem::B1P, kHid, kHid,
+                    ID64);
+          mma_commit(mma_bar);
+        }
+        wait_mma();
+        hidden_epilogue(64);  // + b1, ReLU -> A1 in place (layer 1 has completed)
+        tc_fence_before();
+        fence_async_smem();
+        named_sync(kWBarMma, kWMma);
+        // ---- layer 2 (N padded to 16) ----
+        if (row == 0) {
+          tc_fence_after();
+          mma_split(t_out, sbase + WsSmem::A1, WsSmem::A1P, kTcTile, sbase + WsSmem::B2, TcSmem::B2P, kOutPad,
+                    kHid, ID16);
+          mma_commit(mma_bar);
+        }
+        wait_mma();
+        {
+          float v[16];
+          tmem_ld16(t_out + lane_off, v);
+          const long long q = q0 + row;
+          if (q < n && owner[q] >= 0) {
+            const float l0 = v[0] + bias[128], l1 = v[1] + bias[129], l2 = v[2] + bias[130], l3 = v[3] + bias[131];
+            res[q] = make_float4(softplus_f(l0), logistic_f(l1), logistic_f(l2), logistic_f(l3));
+          }
+        }
+        tc_fence_before();
+        // every team thread has seen this tile's last completion before the next commit
+        named_sync(kWBarMma, kWMma);
+      }
+    }
+  }
+  __syncthreads();
+  if (ctid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*taddr_smem), "n"(128) : "memory");
+}
+
 }  // namespace
 
 bool field_tc_supported(const FieldView& F) {
@@ -328,8 +589,6 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
   // persistent: one CTA per SM (it owns all 512 TMEM columns)
   const long long tiles = (n_hint + kTcTile * kGroups - 1) / (kTcTile * kGroups);
   const int grid = static_cast<int>(std::max(1LL, std::min(tiles, static_cast<long long>(sms))));
-  const size_t tile_bytes = static_cast<size_t>(2 * TcSmem::A0P);
-  m.ws().tc_tiles.ensure(static_cast<size_t>((m.ws().cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
   const bool half = m.mlp_mode == 2;
   if (half) {  // refresh the fp16 copy of the table (params may have changed since the last render)
     const long long nrow = static_cast<long long>(m.n_grid / 2);
@@ -340,6 +599,24 @@ void launch_field_tc(ModelImpl& m, cudaStream_t s, long long n_hint) {
     ARFX_CUDA(cudaGetLastError());
     m.prof.end(s);
   }
+#if ARFX_TC_FUSED
+  {
+    const size_t fsmem = WsSmem::TOTAL + 1024;
+    auto fk = half ? field_fused_kernel<true> : field_fused_kernel<false>;
+    ensure_dyn_smem(reinterpret_cast<const void*>(fk), fsmem);
+    const long long ft = (n_hint + kTcTile * kWG - 1) / (kTcTile * kWG);
+    const int fgrid = static_cast<int>(std::max(1LL, std::min(ft, static_cast<long long>(sms))));
+    m.prof.begin("field_tc", s);
+    fk<<<fgrid, kWThreads, fsmem, s>>>(m.fv, m.grid_h2.ptr, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr,
+                                       m.ws().powner.ptr, m.ws().pres.ptr, m.ws().counters.ptr + 2,
+                                       static_cast<long long>(m.ws().cap_pool), m.stats_on ? m.stats.ptr : nullptr);
+    ARFX_CUDA(cudaGetLastError());
+    m.prof.end(s);
+    return;
+  }
+#endif
+  const size_t tile_bytes = static_cast<size_t>(2 * TcSmem::A0P);
+  m.ws().tc_tiles.ensure(static_cast<size_t>((m.ws().cap_pool + kTcTile - 1) / kTcTile + 1) * tile_bytes);
   m.prof.begin("encode_tc", s);
   auto enc = half ? encode_tiles_kernel<true> : encode_tiles_kernel<false>;
   enc<<<resident_grid(enc, kEncThreads, 0, n_hint), kEncThreads, 0, s>>>(m.fv, m.grid_h2.ptr, m.ws().px.ptr, m.ws().py.ptr, m.ws().pz.ptr, m.ws().powner.ptr,

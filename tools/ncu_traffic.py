@@ -6,8 +6,8 @@ Usage: python tools/ncu_traffic.py profiles/ncu_r1_frame.json profiles/ncu_traff
 import json
 import sys
 
-GROUPS = {"deform": ["start_newton_kernel"], "prune": ["start_mask_kernel", "start_key_kernel", "start_place_kernel"],
-          "finalize": ["finalize_pool_kernel"], "field": ["field_tile_kernel"], "field_tc": ["field_tc_kernel"], "encode_tc": ["encode_tiles_kernel"],
+GROUPS = {"deform": ["start_newton_kernel"], "prune": ["start_mask_kernel", "scan_lookback_kernel", "start_key_kernel", "start_place_kernel"],
+          "finalize": ["finalize_pool_kernel"], "field": ["field_tile_kernel"], "field_tc": ["field_fused_kernel", "field_tc_kernel"], "encode_tc": ["encode_tiles_kernel"],
           "march": ["march_kernel"], "composite": ["composite_kernel"]}
 
 

@@ -18,7 +18,7 @@ PREFIXES = {
     "ELECT": "elect.sync (single issuing thread)",
     "FENCE.VIEW.ASYNC": "fence.proxy.async (generic -> async proxy)",
 }
-KERNELS = ["field_tc_kernel", "field_bwd_tc_kernel"]
+KERNELS = ["field_fused_kernel", "field_bwd_tc_kernel"]
 
 
 def main(out=None):
@@ -31,7 +31,9 @@ def main(out=None):
             continue
         ops = collections.Counter(m.group(1) for m in re.finditer(
             r"/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*(?:\.[A-Za-z0-9_]+)*)", f))
-        short = kern
+        # template instantiations are told apart by their mangled suffix (e.g. Lb0 / Lb1)
+        inst = re.search(r"ILb([01])E", name)
+        short = kern + (f"<{'true' if inst.group(1) == '1' else 'false'}>" if inst else "")
         for op, c in sorted(ops.items()):
             for p, meaning in PREFIXES.items():
                 if op.startswith(p):
