@@ -334,8 +334,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 //   MMA team       4 warps (TMEM lane quarters 0-3): takes the filled buffers in a fixed
 //                  round-robin order, issues layer 0 (whose completion, committed to the
 //                  buffer's `empty` barrier, hands the buffer back), runs the three epilogues
-//                  through its own hidden tile A1 (2 x 16 KB) and writes (density, rgb).
-// The smem footprint (weights 29 KB + A1 32 KB + 16 KB per A0 buffer) stays small so the
+//                  and writes (density, rgb). The hidden activations never leave TMEM: each
+//                  epilogue reads the fp32 accumulator (tcgen05.ld), adds the bias, applies
+//                  ReLU, splits into bf16 hi / lo and stores them back (tcgen05.st) as the
+//                  A operand of the next layer (`.kind::f16 [d], [a_tmem], b_desc`).
+// The smem footprint (weights 29 KB + 16 KB per A0 buffer = 77 KB) stays small so the
 // unified L1 keeps most of its capacity for the hash-table gathers.
 #ifndef ARFX_WS_GROUPS
 #define ARFX_WS_GROUPS 3
@@ -349,14 +352,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 constexpr int kWG = ARFX_WS_GROUPS, kWS = ARFX_WS_SPLIT, kWB = ARFX_WS_BUFS;
 constexpr int kWGroupThreads = kTcTile * kWS, kWMma = 128;
 constexpr int kWThreads = kWMma + kWG * kWGroupThreads;
+constexpr int kWTmemCols = 256;
 constexpr int kWBarMma = 15;  // named barrier of the MMA team (gather groups use 1..kWG)
 static_assert(kWThreads <= 1024 && kWG < kWBarMma && (kWS == 1 || kWS == 2 || kWS == 4), "fused layout");
 
 struct WsSmem {
   static constexpr int B0 = TcSmem::B0, B1 = TcSmem::B1, B2 = TcSmem::B2, BIAS = TcSmem::BIAS;
   static constexpr int A0P = TcSmem::A0P, A1P = TcSmem::A1P;
-  static constexpr int A1 = TcSmem::ACT;                  // MMA team's hidden tile (2 x 16 KB)
-  static constexpr int A0 = A1 + 2 * A1P;                 // [kWG][kWB] feature tiles (2 x 8 KB)
+  static constexpr int A0 = TcSmem::ACT;                  // [kWG][kWB] feature tiles (2 x 8 KB)
   static constexpr int FULL = A0 + kWG * kWB * 2 * A0P;   // u64 [kWG * kWB]
   static constexpr int EMPTY = FULL + 8 * kWG * kWB;      // u64 [kWG * kWB]
   static constexpr int MMA = EMPTY + 8 * kWG * kWB;       // u64
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   if (ctid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_bar) : "memory");
   if (ctid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbase + WsSmem::TADDR),
-                 "n"(128)
+                 "n"(kWTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -488,18 +491,12 @@ __global__ void __launch_bounds__(kWThreads, 1)
     const int row = ctid;  // TMEM lane = warp quarter * 32 + lane
     const uint32_t lane_off = static_cast<uint32_t>((ctid >> 5) * 32) << 16;
     const uint32_t t_hid = *taddr_smem, t_out = *taddr_smem + 64;
+    // TMEM columns: hidden accumulator [0, 64), layer-2 output [64, 80), A operand hi plane
+    // [96, 128) and lo plane [128, 160) (two bf16 per column)
+    const uint32_t t_ahi = *taddr_smem + 96, t_alo = *taddr_smem + 128;
     constexpr uint32_t ID64 = idesc_bf16(128, 64);
     constexpr uint32_t ID16 = idesc_bf16(128, 16);
     uint32_t mphase = 0;
-    auto put8 = [&](int c, const float* x) {  // row `row`, columns [c, c+8) of A1
-      __nv_bfloat16 hi[8], lo[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) split_bf16(x[j], hi[j], lo[j]);
-      *reinterpret_cast<uint4*>(tc_smem + WsSmem::A1 + kmaj_off(row, c, kTcTile)) =
-          *reinterpret_cast<const uint4*>(hi);
-      *reinterpret_cast<uint4*>(tc_smem + WsSmem::A1 + WsSmem::A1P + kmaj_off(row, c, kTcTile)) =
-          *reinterpret_cast<const uint4*>(lo);
-    };
     auto hidden_epilogue = [&](int boff) {
 #pragma unroll
       for (int c = 0; c < kHid; c += 16) {
@@ -507,9 +504,21 @@ __global__ void __launch_bounds__(kWThreads, 1)
         tmem_ld16(t_hid + lane_off + c, v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias[boff + c + j], 0.f);
-        put8(c, v);
-        put8(c + 8, v + 8);
+        uint32_t ph[8], pl[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat16 h0, l0, h1, l1;
+          split_bf16(v[2 * j], h0, l0);
+          split_bf16(v[2 * j + 1], h1, l1);
+          ph[j] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+                  (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+          pl[j] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) |
+                  (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+        }
+        tmem_st8(t_ahi + lane_off + c / 2, ph);
+        tmem_st8(t_alo + lane_off + c / 2, pl);
       }
+      tmem_st_wait();
     };
     auto wait_mma = [&]() {
       mbar_wait(mma_bar, mphase);
@@ -532,27 +541,23 @@ __global__ void __launch_bounds__(kWThreads, 1)
           mma_commit(mma_bar);
         }
         wait_mma();
-        hidden_epilogue(0);  // + b0, ReLU -> A1
+        hidden_epilogue(0);  // + b0, ReLU -> TMEM A operand
         tc_fence_before();
-        fence_async_smem();
         named_sync(kWBarMma, kWMma);
         // ---- layer 1 ----
         if (row == 0) {
           tc_fence_after();
-          mma_split(t_hid, sbase + WsSmem::A1, WsSmem::A1P, kTcTile, sbase + WsSmem::B1, TcSmem::B1P, kHid, kHid,
-                    ID64);
+          mma_split_ts(t_hid, t_ahi, t_alo, sbase + WsSmem::B1, TcSmem::B1P, kHid, kHid, ID64);
           mma_commit(mma_bar);
         }
         wait_mma();
-        hidden_epilogue(64);  // + b1, ReLU -> A1 in place (layer 1 has completed)
+        hidden_epilogue(64);  // + b1, ReLU -> TMEM A operand, in place (layer 1 has completed)
         tc_fence_before();
-        fence_async_smem();
         named_sync(kWBarMma, kWMma);
         // ---- layer 2 (N padded to 16) ----
         if (row == 0) {
           tc_fence_after();
-          mma_split(t_out, sbase + WsSmem::A1, WsSmem::A1P, kTcTile, sbase + WsSmem::B2, TcSmem::B2P, kOutPad,
-                    kHid, ID16);
+          mma_split_ts(t_out, t_ahi, t_alo, sbase + WsSmem::B2, TcSmem::B2P, kOutPad, kHid, ID16);
           mma_commit(mma_bar);
         }
         wait_mma();
@@ -573,7 +578,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   }
   __syncthreads();
   if (ctid < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*taddr_smem), "n"(128) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*taddr_smem), "n"(kWTmemCols) : "memory");
 }
 
 }  // namespace

@@ -93,6 +93,37 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// A from tensor memory (".kind::f16 [d], [a], b_desc"): the A operand is M rows x K bf16 in
+// TMEM, row m in lane m, two consecutive K elements packed per 32-bit column (element 2c in
+// the low half) -- K = 16 per MMA = 8 columns.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// split-bf16 product with A (hi plane at column a_hi, lo plane at a_lo) in TMEM, B in smem
+__device__ __forceinline__ void mma_split_ts(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
+                                             uint32_t b_plane, int b_rows, int K, uint32_t idesc) {
+  for (int ks = 0; ks < K / 16; ++ks) {
+    const uint32_t bo = b_hi + ks * 2 * (b_rows * 16);
+    const uint64_t bh = smem_desc(bo, b_rows * 16, 128), bl = smem_desc(bo + b_plane, b_rows * 16, 128);
+    mma_bf16_ts(tmem_d, a_hi + 8 * ks, bh, idesc, ks > 0 ? 1u : 0u);
+    mma_bf16_ts(tmem_d, a_hi + 8 * ks, bl, idesc, 1u);
+    mma_bf16_ts(tmem_d, a_lo + 8 * ks, bh, idesc, 1u);
+  }
+}
+
+// 8 consecutive 32-bit TMEM columns of this thread's lane (caller waits with tmem_st_wait)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 }  // namespace umma
 }  // namespace arfx
