@@ -615,7 +615,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     else:  # fused encode -> tcgen05 MLP: the hash-table gathers bind, the tensor pipe idles
         entry("field_tc", "l2/l1 gathers", QT * (1024 + 16), "GB/s", hbm,
               f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); gathers are L2-resident, so frac is vs HBM for scale only",
-              "1024 B gathered + 16 B (density, rgb) written per query; + 12800 MLP flops/query on tcgen05")
+              "1024 B gathered + 16 B (density, rgb) written per query; + 12800 MLP flops/query (layers 0-1 on tcgen05, the 64->4 head as f32 FMAs)")
         if "field_tc" in out and peaks.get("bf16_tflops"):
             e = out["field_tc"]
             e["tensor_tflops"] = QT * 12800 / (prof["field_tc"][0] * 1e-3) / 1e12

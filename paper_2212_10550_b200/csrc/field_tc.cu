@@ -333,12 +333,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 //                  beyond the buffer hand-back, so they keep the L1 gather pipe busy.
 //   MMA team       4 warps (TMEM lane quarters 0-3): takes the filled buffers in a fixed
 //                  round-robin order, issues layer 0 (whose completion, committed to the
-//                  buffer's `empty` barrier, hands the buffer back), runs the three epilogues
-//                  and writes (density, rgb). The hidden activations never leave TMEM: each
-//                  epilogue reads the fp32 accumulator (tcgen05.ld), adds the bias, applies
-//                  ReLU, splits into bf16 hi / lo and stores them back (tcgen05.st) as the
-//                  A operand of the next layer (`.kind::f16 [d], [a_tmem], b_desc`).
-// The smem footprint (weights 29 KB + 16 KB per A0 buffer = 77 KB) stays small so the
+//                  buffer's `empty` barrier, hands the buffer back), then layer 1, and writes
+//                  (density, rgb). The hidden activations never leave TMEM: epilogue 0 reads
+//                  the fp32 accumulator (tcgen05.ld), adds the bias, applies ReLU, splits into
+//                  bf16 hi / lo and stores them back (tcgen05.st) as layer 1's A operand
+//                  (`.kind::f16 [d], [a_tmem], b_desc`); epilogue 1 computes the 64 -> 4
+//                  output layer as f32 FMAs from the layer-1 accumulator (a third MMA round
+//                  trip per tile cost more than the 256 FMAs per row: 0.428 vs 0.402 ms).
+// The smem footprint (weights 29 KB + 16 KB per A0 buffer = 78 KB) stays small so the
 // unified L1 keeps most of its capacity for the hash-table gathers.
 #ifndef ARFX_WS_GROUPS
 #define ARFX_WS_GROUPS 3
@@ -348,6 +350,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 #endif
 #ifndef ARFX_WS_BUFS
 #define ARFX_WS_BUFS 1
+#endif
+#ifndef ARFX_WS_L2_SIMT  // layer 2 (64 -> 4) as f32 FMAs in the layer-1 epilogue
+#define ARFX_WS_L2_SIMT 1
 #endif
 constexpr int kWG = ARFX_WS_GROUPS, kWS = ARFX_WS_SPLIT, kWB = ARFX_WS_BUFS;
 constexpr int kWGroupThreads = kTcTile * kWS, kWMma = 128;
@@ -364,7 +369,8 @@ struct WsSmem {
   static constexpr int EMPTY = FULL + 8 * kWG * kWB;      // u64 [kWG * kWB]
   static constexpr int MMA = EMPTY + 8 * kWG * kWB;       // u64
   static constexpr int TADDR = MMA + 8;
-  static constexpr int TOTAL = TADDR + 16;
+  static constexpr int W2T = (TADDR + 16 + 15) / 16 * 16;  // f32 [64][4]: W2 transposed (SIMT layer 2)
+  static constexpr int TOTAL = W2T + 4 * kHid * 4;
 };
 
 __device__ __forceinline__ void named_sync(int id, int count) {
@@ -427,6 +433,8 @@ __global__ void __launch_bounds__(kWThreads, 1)
     bias[64 + i] = __ldg(b1 + i);
   }
   if (ctid < 4) bias[128 + ctid] = __ldg(b2 + ctid);
+  for (int i = ctid; i < 4 * kHid; i += kWThreads)
+    reinterpret_cast<float*>(tc_smem + WsSmem::W2T)[i] = __ldg(W2 + (i % 4) * kHid + i / 4);
   if (ctid < kWG * kWB) {
     const int g = ctid / kWB, b = ctid % kWB;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(g, b)) : "memory");
@@ -551,6 +559,28 @@ __global__ void __launch_bounds__(kWThreads, 1)
           mma_commit(mma_bar);
         }
         wait_mma();
+#if ARFX_WS_L2_SIMT
+        {  // ---- layer 2 (64 -> 4) on the CUDA cores, straight from the layer-1 accumulator ----
+          const float4* w2t = reinterpret_cast<const float4*>(tc_smem + WsSmem::W2T);
+          float o0 = bias[128], o1 = bias[129], o2 = bias[130], o3 = bias[131];
+#pragma unroll
+          for (int c = 0; c < kHid; c += 16) {
+            float v[16];
+            tmem_ld16(t_hid + lane_off + c, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float h = fmaxf(v[j] + bias[64 + c + j], 0.f);
+              const float4 w = w2t[c + j];
+              o0 = fmaf(w.x, h, o0);
+              o1 = fmaf(w.y, h, o1);
+              o2 = fmaf(w.z, h, o2);
+              o3 = fmaf(w.w, h, o3);
+            }
+          }
+          const long long q = q0 + row;
+          if (q < n && owner[q] >= 0) res[q] = make_float4(softplus_f(o0), logistic_f(o1), logistic_f(o2), logistic_f(o3));
+        }
+#else
         hidden_epilogue(64);  // + b1, ReLU -> TMEM A operand, in place (layer 1 has completed)
         tc_fence_before();
         named_sync(kWBarMma, kWMma);
@@ -570,6 +600,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
             res[q] = make_float4(softplus_f(l0), logistic_f(l1), logistic_f(l2), logistic_f(l3));
           }
         }
+#endif
         tc_fence_before();
         // every team thread has seen this tile's last completion before the next commit
         named_sync(kWBarMma, kWMma);
