@@ -13,6 +13,7 @@ PREFIXES = {
     "UTCBAR": "tcgen05.commit -> mbarrier",
     "UTCATOMSWS": "tcgen05.alloc / dealloc (TMEM columns)",
     "LDTM": "tcgen05.ld (TMEM -> registers, epilogue)",
+    "STTM": "tcgen05.st (registers -> TMEM: the next layer's A operand)",
     "UBLKCP": "cp.async.bulk (global -> shared, TMA engine)",
     "SYNCS": "mbarrier arrive / expect-tx / try-wait",
     "ELECT": "elect.sync (single issuing thread)",
