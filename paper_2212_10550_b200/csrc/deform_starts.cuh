@@ -60,14 +60,51 @@ __device__ __forceinline__ const PoseCtx* ds_stage_pose(const PoseCtx* poses, do
   return reinterpret_cast<const PoseCtx*>(smem);
 }
 
+// Packed f32x2 add / mul (sm_100 FADD2 / FMUL2) with explicit .rn rounding in PTX.
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "add.rn.f32x2 %0, ra, rb;\n\t}"
+      : "=l"(r)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return make_float2(__uint_as_float(static_cast<unsigned>(r)), __uint_as_float(static_cast<unsigned>(r >> 32)));
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "mul.rn.f32x2 %0, ra, rb;\n\t}"
+      : "=l"(r)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return make_float2(__uint_as_float(static_cast<unsigned>(r)), __uint_as_float(static_cast<unsigned>(r >> 32)));
+}
+
 // Surviving starts: bit b set iff cap_dist(x', b) <= cutoff_b (R/articulation.hpp:101-102).
 __device__ __forceinline__ uint32_t ds_prune(const PoseCtx* __restrict__ P, d3 xt, int& exact_tests) {
   const float fx = static_cast<float>(xt.x), fy = static_cast<float>(xt.y), fz = static_cast<float>(xt.z);
+  // sphere rejects two bones at a time on the packed f32x2 pipe (FADD2 / FMUL2): the same
+  // per-lane operations and roundings as the scalar ((dx^2 + dy^2) + dz^2) > r^2 test
+  uint32_t cand = 0;
+  const int nb = P->nb;
+  const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
+  for (int b = 0; b < nb; b += 2) {
+    // PoseCtx::sph rows are 8-byte aligned: two float2 loads per bone
+    const float2 a0 = *reinterpret_cast<const float2*>(&P->sph[b][0]), a1 = *reinterpret_cast<const float2*>(&P->sph[b][2]);
+    const bool two = b + 1 < nb;
+    const float2 c0 = two ? *reinterpret_cast<const float2*>(&P->sph[b + 1][0]) : make_float2(0.f, 0.f);
+    const float2 c1 = two ? *reinterpret_cast<const float2*>(&P->sph[b + 1][2]) : make_float2(0.f, -1.f);
+    const float2 dx = f2_add(fx2, make_float2(-a0.x, -c0.x));
+    const float2 dy = f2_add(fy2, make_float2(-a0.y, -c0.y));
+    const float2 dz = f2_add(fz2, make_float2(-a1.x, -c1.x));
+    const float2 mx = f2_mul(dx, dx), my = f2_mul(dy, dy), mz = f2_mul(dz, dz);
+    // the sums stay scalar add.rn: ptxas fuses a packed mul into a packed add (FFMA2) even
+    // with -fmad=false, which would change the rounding; scalar .rn adds are never contracted
+    const float2 d2 = make_float2(__fadd_rn(__fadd_rn(mx.x, my.x), mz.x), __fadd_rn(__fadd_rn(mx.y, my.y), mz.y));
+    cand |= (d2.x > a1.y ? 0u : 1u) << b;  // else provably pruned (see PoseCtx::sph)
+    cand |= (d2.y > c1.y ? 0u : 1u) << (b + 1);
+  }
   uint32_t mask = 0;
-  for (int b = 0; b < P->nb; ++b) {
-    const float dx = fx - P->sph[b][0], dy = fy - P->sph[b][1], dz = fz - P->sph[b][2];
-    const float d2 = dx * dx + dy * dy + dz * dz;
-    if (d2 > P->sph[b][3]) continue;  // provably pruned (see PoseCtx::sph)
+  for (uint32_t m = cand; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
     ++exact_tests;
     const d3 ca = make3(P->cap_a[b][0], P->cap_a[b][1], P->cap_a[b][2]);
     const d3 cb = make3(P->cap_b[b][0], P->cap_b[b][1], P->cap_b[b][2]);
@@ -115,15 +152,28 @@ struct KeyGrid {
 };
 
 // Approximate (f32) skinning cell of a point: only a sort key for locality, never used
-// in the arithmetic (skin_eval recomputes the exact cell in FP64).
-__device__ __forceinline__ int approx_skin_cell(const SkinView& S, d3 x, const KeyGrid& kg) {
+// in the arithmetic (skin_eval recomputes the exact cell in FP64). sc = (res - 1) / extent
+// per axis, computed once per thread (no division per start).
+struct KeyScale {
+  float lo[3], sc[3];
+};
+__device__ __forceinline__ KeyScale key_scale(const SkinView& S) {
+  const int res[3] = {S.rx, S.ry, S.rz};
+  KeyScale k;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    k.lo[a] = static_cast<float>(S.lo[a]);
+    k.sc[a] = static_cast<float>(res[a] - 1) / static_cast<float>(S.e[a]);
+  }
+  return k;
+}
+__device__ __forceinline__ int approx_skin_cell(const SkinView& S, const KeyScale& ks, d3 x, const KeyGrid& kg) {
   const float p[3] = {static_cast<float>(x.x), static_cast<float>(x.y), static_cast<float>(x.z)};
   const int res[3] = {S.rx, S.ry, S.rz};
   int c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const float lo = static_cast<float>(S.lo[a]), e = static_cast<float>(S.e[a]);
-    float u = (p[a] - lo) / e * static_cast<float>(res[a] - 1);
+    float u = (p[a] - ks.lo[a]) * ks.sc[a];
     u = fminf(fmaxf(u, 0.0f), static_cast<float>(res[a] - 2));
     c[a] = static_cast<int>(u) >> kg.shift;
   }
@@ -142,6 +192,7 @@ __global__ void __launch_bounds__(256) start_key_kernel(SkinView S, KeyGrid kg, 
   extern __shared__ double sk_smem[];
   const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sk_smem);
   const int ncell = kg.cells();
+  const KeyScale ks = key_scale(S);
   const long long n = src.count();
   for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
        s += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -153,7 +204,7 @@ __global__ void __launch_bounds__(256) start_key_kernel(SkinView S, KeyGrid kg, 
     long long slot = slot_base[s];
     for (uint32_t m = mask; m; m &= m - 1, ++slot) {
       const int b = __ffs(m) - 1;
-      const uint32_t key = static_cast<uint32_t>(b * ncell + approx_skin_cell(S, rigid_apply(P->bone_inv[b], xt), kg));
+      const uint32_t key = static_cast<uint32_t>(b * ncell + approx_skin_cell(S, ks, rigid_apply(P->bone_inv[b], xt), kg));
       if (slot < cap) {
         keys[slot] = key;
         unsorted[slot] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(b) << kItemBoneShift);
