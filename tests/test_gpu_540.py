@@ -135,3 +135,34 @@ def test_540_sample_set_bit_exact(headline, ref, frame):
         o2 = np.lexsort((ttr.index, ttr.ray))
         assert np.array_equal(ttr.ray[o2], rtr["s_ray"]) and np.array_equal(ttr.index[o2], rtr["s_index"])
         np.testing.assert_allclose(ttr.density[o2], rtr["s_density"], rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.parametrize("mode", ["tcgen05", "exact"])
+def test_stratified_thread_per_ray_frame(gpu, ref, mode):
+    """Stratified sampling through the thread-per-ray march (400x400 = 160,000 rays >= the
+    full-warp threshold, so each lane walks its own ray's keyed PCG jitter stream,
+    R/render.hpp:201) on a pose outside the benched set, both decoders, against the
+    reference's render_model with the same seed / frame id."""
+    sk = fx.smpl24()
+    dm = gpu.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    rm = ref.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    pose = fx.random_pose(sk, 4242)
+    cam = fx.default_camera(sk, 400, 400)
+    opt = arf.RenderOptions(samples_per_ray=128, stratified=True, seed=11, frame_id=3)
+    occ_cfg = fx.config1_occupancy()
+    rocc, _ = ref.build_inference_grid(rm, pose.bone_transforms, pose.global_transform, occ_cfg)
+    rrgb, ralpha, rcnt = ref.render(rm, pose.bone_transforms, pose.global_transform, cam, rocc, opt)
+    dm.set_mlp_mode(mode)
+    try:
+        occ = arf.build_model_inference_grid(dm, pose, occ_cfg)
+        assert np.array_equal(occ.mask, ref.occ_arrays(rocc)[1])
+        c0 = dm.counters.posed_queries
+        img = arf.render_model(dm, arf.PosedModelView(dm, pose), cam, occ, opt)
+        posed = dm.counters.posed_queries - c0
+    finally:
+        dm.set_mlp_mode("exact")
+    rtol, atol = (TC_RTOL, TC_ATOL) if mode == "tcgen05" else (EX_RTOL, EX_ATOL)
+    assert (ralpha > 0).sum() > 20_000
+    np.testing.assert_allclose(img.rgb, rrgb, rtol=rtol, atol=atol)
+    np.testing.assert_allclose(img.alpha, ralpha, rtol=rtol, atol=atol)
+    assert posed == int(rcnt[0])
