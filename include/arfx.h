@@ -167,8 +167,9 @@ int arfx_model_get_params(arfx_model m, float* grid_params, float* mlp_params,
                           double* skin_weights);
 int arfx_model_set_params(arfx_model m, const float* grid_params, const float* mlp_params);
 /* Decoder used by arfx_render_model*: ARFX_MLP_EXACT (default) = f32 SIMT with the
- * reference's summation order; ARFX_MLP_TCGEN05 = tcgen05.mma (kind::f16 on split-bf16
- * operands, f32 accumulate); ARFX_MLP_TCGEN05_FP16 = the same decoder fed by fp16 hash-table
+ * reference's summation order; ARFX_MLP_TCGEN05 = hash encode fused with the MLP's hidden
+ * layers on tcgen05.mma (kind::f16 on split-bf16 operands, f32 accumulate in TMEM) and the
+ * 64 -> 4 head in f32; ARFX_MLP_TCGEN05_FP16 = the same decoder fed by fp16 hash-table
  * gathers (an fp16 copy of the table is refreshed at every render: half the gather bytes).
  * The tensor-core modes are stated to 1e-3 relative on rendered RGB;
  * occupancy grids, training and the query APIs always use the exact decoder. */
