@@ -633,7 +633,7 @@ def roofline(prof, stats, K, rays, N, posed, peaks, peak_kind, pipe):
     # written (8 B); per start key + item written, read back, sorted item written (20 B)
     n_targets = posed + 64 ** 3 * K  # render samples + occupancy cells
     entry("prune", "hbm", 32.0 * n_targets + 20.0 * S, "GB/s", hbm, f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-          "32 B/target + 20 B/start (mask/count, sort keys, items); 6 launches incl. 2 single-pass look-back scans")
+          "32 B/target + 20 B/start (mask/count, sort keys, items); 5 launches incl. 2 single-pass look-back scans (K2a does the resets)")
     # K4 composite: 30 B per posed sample + 24 B per ray (HBM)
     entry("composite", "hbm", 30.0 * posed + 24.0 * rays * K, "GB/s", hbm,
           f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "30 B/posed sample + 24 B/ray")

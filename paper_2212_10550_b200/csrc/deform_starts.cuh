@@ -114,12 +114,36 @@ __device__ __forceinline__ uint32_t ds_prune(const PoseCtx* __restrict__ P, d3 x
   return mask;
 }
 
-// K2a
+// K2a. It also performs the deform call's per-call resets for the kernels after it (formerly a
+// 1-thread count kernel and three memsets, i.e. four graph nodes on the critical path):
+// C[4] (Newton cursor) = C[6] = C[7] = 0, C[5] = target count, C[8] = key count, the key
+// histogram and the look-back scan status words zeroed. Nothing before the scans reads them.
+struct PruneResets {
+  unsigned long long* C;  // the workspace counters
+  uint32_t* key_hist;
+  long long nkeys;
+  unsigned long long* lb_status;
+  long long n_status;
+};
+
 template <class Src, bool kSinglePose>
 __global__ void __launch_bounds__(256) start_mask_kernel(const PoseCtx* __restrict__ poses, Src src,
                                                          uint32_t* __restrict__ mask_out,
                                                          uint32_t* __restrict__ count_out,
-                                                         unsigned long long* stats) {
+                                                         unsigned long long* stats, PruneResets z) {
+  {
+    const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long nt = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = t0; i < z.nkeys; i += nt) z.key_hist[i] = 0u;
+    for (long long i = t0; i < z.n_status; i += nt) z.lb_status[i] = 0ull;
+    if (t0 == 0) {
+      z.C[4] = 0ull;
+      z.C[5] = static_cast<unsigned long long>(src.count());
+      z.C[6] = 0ull;
+      z.C[7] = 0ull;
+      z.C[8] = static_cast<unsigned long long>(z.nkeys);
+    }
+  }
   extern __shared__ double sm_smem[];
   const PoseCtx* Pb = ds_stage_pose<kSinglePose>(poses, sm_smem);
   const int lane = threadIdx.x & 31;
@@ -588,15 +612,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   total = warp_sums[32];
   __syncthreads();
   return out;
-}
-
-template <class Src>
-__global__ void src_count_kernel(Src src, unsigned long long* out, unsigned long long* out2 = nullptr,
-                                 unsigned long long v2 = 0) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    *out = static_cast<unsigned long long>(src.count());
-    if (out2) *out2 = v2;  // a second constant counter in the same launch
-  }
 }
 
 // ---- single-pass exclusive scan (decoupled look-back) -----------------------------------

@@ -954,17 +954,12 @@ void launch_deform_sink(ModelImpl& m, const PoseCtx* d_poses, const Src& src, co
   unsigned long long* stats = m.stats_on ? m.stats.ptr : nullptr;
   const long long nkeys = static_cast<long long>(m.sv.nb) * kg.cells();
   const long long cap = static_cast<long long>(w.cap_starts);
-  ARFX_CUDA(cudaMemsetAsync(C + 4, 0, 4 * sizeof(unsigned long long), s));
-  ARFX_CUDA(cudaMemsetAsync(w.key_hist.ptr, 0, static_cast<size_t>(nkeys) * sizeof(uint32_t), s));
-  ARFX_CUDA(cudaMemsetAsync(w.lb_status.ptr, 0,
-                            static_cast<size_t>((n + kLbTile - 1) / kLbTile + (nkeys + kLbTile - 1) / kLbTile + 4) *
-                                sizeof(unsigned long long),
-                            s));
   m.prof.begin("prune", s);
-  src_count_kernel<Src><<<1, 1, 0, s>>>(src, C + 5, C + 8, static_cast<unsigned long long>(nkeys));
+  // K2a also resets the call's counters, key histogram and scan status (PruneResets)
+  const PruneResets z{C, w.key_hist.ptr, nkeys, w.lb_status.ptr,
+                      (n + kLbTile - 1) / kLbTile + (nkeys + kLbTile - 1) / kLbTile + 4};
   start_mask_kernel<Src, single><<<resident_grid(start_mask_kernel<Src, single>, 256, pose_smem, n), 256, pose_smem,
-                                   s>>>(d_poses, src, w.smask.ptr, w.scount.ptr,
-                                                                            stats);
+                                   s>>>(d_poses, src, w.smask.ptr, w.scount.ptr, stats, z);
   ARFX_CUDA(cudaGetLastError());
   // start slots: exclusive scan of the per-target start counts (C6 = total starts, C3 += 1
   // when they exceed the slots), single pass
