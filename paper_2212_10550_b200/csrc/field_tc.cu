@@ -361,6 +361,15 @@ constexpr int kWTmemCols = 256;
 constexpr int kWBarMma = 15;  // named barrier of the MMA team (gather groups use 1..kWG)
 static_assert(kWThreads <= 1024 && kWG < kWBarMma && (kWS == 1 || kWS == 2 || kWS == 4), "fused layout");
 
+// K order of the fused kernel's A0 tile: K chunk c (8 bf16 = 4 levels x 2 features) holds
+// the levels of gather slice c % kWS, group c / kWS; returns the feature index (2 level + f)
+// stored at K position k (W0's columns are staged in the same order)
+__device__ __forceinline__ int ws_feature_of_k(int k) {
+  const int c = k >> 3, t = (k & 7) >> 1, f = k & 1;
+  const int level = (c % kWS) + kWS * (4 * (c / kWS) + t);
+  return 2 * level + f;
+}
+
 struct WsSmem {
   static constexpr int B0 = TcSmem::B0, B1 = TcSmem::B1, B2 = TcSmem::B2, BIAS = TcSmem::BIAS;
   static constexpr int A0P = TcSmem::A0P, A1P = TcSmem::A1P;
@@ -416,9 +425,9 @@ __global__ void __launch_bounds__(kWThreads, 1)
     *reinterpret_cast<__nv_bfloat16*>(tc_smem + off) = hi;
     *reinterpret_cast<__nv_bfloat16*>(tc_smem + off + plane) = lo;
   };
-  for (int i = ctid; i < kHid * kIn; i += kWThreads) {
+  for (int i = ctid; i < kHid * kIn; i += kWThreads) {  // W0's columns in the A0 tile's K order
     const int o = i / kIn, k = i % kIn;
-    put(WsSmem::B0 + kmaj_off(o, k, kHid), TcSmem::B0P, __ldg(W0 + i));
+    put(WsSmem::B0 + kmaj_off(o, k, kHid), TcSmem::B0P, __ldg(W0 + o * kIn + ws_feature_of_k(k)));
   }
   for (int i = ctid; i < kHid * kHid; i += kWThreads) {
     const int o = i / kHid, k = i % kHid;
@@ -475,18 +484,21 @@ __global__ void __launch_bounds__(kWThreads, 1)
       mbar_wait(empty_bar(g, b), ((r / kWB) & 1) ^ 1);  // layer 0 has consumed this buffer
       if (ok) {
         const int A = a0_off(g, b);
+        // slice s gathers levels s, s + kWS, s + 2 kWS, ... (coarse and fine levels mixed, so
+        // the group's slices finish together); four of them fill one 16-B K chunk
 #pragma unroll 1
-        for (int l = slice * kLv; l < (slice + 1) * kLv; l += 4) {
+        for (int m0 = 0; m0 < kLv; m0 += 4) {
           __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float2 o = kHalf ? encode_level_h2(F, table_h2, l + j, u) : encode_level_f2(F, l + j, u);
+            const int l = slice + kWS * (m0 + j);
+            const float2 o = kHalf ? encode_level_h2(F, table_h2, l, u) : encode_level_f2(F, l, u);
             split_bf16(o.x, hi[2 * j], lo[2 * j]);
             split_bf16(o.y, hi[2 * j + 1], lo[2 * j + 1]);
           }
-          *reinterpret_cast<uint4*>(tc_smem + A + kmaj_off(row, 2 * l, kTcTile)) =
-              *reinterpret_cast<const uint4*>(hi);
-          *reinterpret_cast<uint4*>(tc_smem + A + WsSmem::A0P + kmaj_off(row, 2 * l, kTcTile)) =
+          const int k = 8 * ((m0 / 4) * kWS + slice);
+          *reinterpret_cast<uint4*>(tc_smem + A + kmaj_off(row, k, kTcTile)) = *reinterpret_cast<const uint4*>(hi);
+          *reinterpret_cast<uint4*>(tc_smem + A + WsSmem::A0P + kmaj_off(row, k, kTcTile)) =
               *reinterpret_cast<const uint4*>(lo);
         }
       }
