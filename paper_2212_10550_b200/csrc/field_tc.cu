@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 #ifndef ARFX_WS_BUFS
 #define ARFX_WS_BUFS 1
 #endif
+#ifndef ARFX_WS_LV_UNROLL  // 2: a thread's 8 levels gathered in one unrolled pass
+#define ARFX_WS_LV_UNROLL 2
+#endif
 #ifndef ARFX_WS_L2_SIMT  // layer 2 (64 -> 4) as f32 FMAs in the layer-1 epilogue
 #define ARFX_WS_L2_SIMT 1
 #endif
@@ -486,7 +489,11 @@ __global__ void __launch_bounds__(kWThreads, 1)
         const int A = a0_off(g, b);
         // slice s gathers levels s, s + kWS, s + 2 kWS, ... (coarse and fine levels mixed, so
         // the group's slices finish together); four of them fill one 16-B K chunk
+#if ARFX_WS_LV_UNROLL > 1
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
         for (int m0 = 0; m0 < kLv; m0 += 4) {
           __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
