@@ -38,7 +38,10 @@ constexpr int kDsThreads = ARFX_DS_THREADS;
 #define ARFX_DS_MIN_BLOCKS 5
 #endif
 constexpr int kDsMinBlocks = ARFX_DS_MIN_BLOCKS;  // 5 x 128 threads: <= 102 registers
-constexpr int kDsItemChunk = 64;
+#ifndef ARFX_DS_ITEM_CHUNK
+#define ARFX_DS_ITEM_CHUNK 64
+#endif
+constexpr int kDsItemChunk = ARFX_DS_ITEM_CHUNK;
 constexpr long long kBlockQueueMaxTargets = 262144;  // block-local item queues below this
 constexpr int kItemBoneShift = 26;  // item = target | bone << 26 (targets < 2^26)
 
