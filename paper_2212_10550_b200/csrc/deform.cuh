@@ -65,6 +65,9 @@ __device__ __forceinline__ void ldg256(const double* p, double* o) {
 // then g = lbs(x) - x_target, |g| and J = sum_{w_i != 0} w_i R_i.
 // `ws` is per-thread scratch for the union bones' raw weights (smem, stride apart).
 // Returns the number of union bones visited (work accounting for the roofline).
+#ifndef ARFX_DS_NOSKIP_W0
+#define ARFX_DS_NOSKIP_W0 1
+#endif
 __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __restrict__ P, d3 x,
                                          d3 xt, double* ws, int stride, d3& g, double& gn,
                                          double J[9]) {
@@ -154,7 +157,14 @@ __device__ __forceinline__ int skin_eval(const SkinView& S, const PoseCtx* __res
     const int b = __ffs(m) - 1;
     double w = ws[j * stride];
     if (renorm) w = dmul(w, inv);
+#if ARFX_DS_NOSKIP_W0
+    // no w != 0 branch: for w == +-0 every added product is +-0 (T, x finite), and
+    // out / J + (+-0) leaves them bit-identical (they start at +0; x + (+-0) == x for x != 0
+    // and (+0) + (-0) == +0), exactly like skipping the bone
+    {
+#else
     if (w != 0.0) {
+#endif
       const double* T = P->bone[b];
       const d3 a = rigid_apply(T, x);
       out = add3(out, mul3(a, w));
