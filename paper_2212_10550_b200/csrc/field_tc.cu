@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) field_tc_kernel(FieldView F, co
 //   gather groups  kWG groups of kWS x 4 warps; a group owns kWB A0 buffers (split-bf16
 //                  K-major, 2 x 8 KB) and loops over its 128-query tiles: wait until the
 //                  buffer is free, thread (row r, level slice s) gathers levels
-//                  [16 s / kWS, 16 (s+1) / kWS) of query r straight into it, then one arrive
+//                  s, s + kWS, s + 2 kWS, ... of query r (coarse, L1-resident and fine, L2
+//                  levels mixed, so a group's slices finish together) straight into it in a
+//                  permuted K order (ws_feature_of_k; W0 is staged to match), then one arrive
 //                  on the buffer's `full` barrier. These warps never wait on the tensor core
 //                  beyond the buffer hand-back, so they keep the L1 gather pipe busy.
 //   MMA team       4 warps (TMEM lane quarters 0-3): takes the filled buffers in a fixed
