@@ -75,6 +75,7 @@ struct Workspace {
   DevBuf<float> train_rgb, train_alpha;  // training outputs when the caller passes none
   DevBuf<unsigned long long> counters;  // [0] posed [1] canonical [2] pool [3] overflow
   DevBuf<int> occ_box;                  // occupied-cell bounding box (march empty-space skip)
+  DevBuf<uint32_t> occ_bits;            // occupancy mask packed to bits (march pass 1 reads, L1-resident)
   DevBuf<float> fwd_act;  // training forwards: per pool entry X | H1 | H2 | logits (K8a reuses them)
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
@@ -100,7 +101,7 @@ struct Workspace {
   Workspace() {
     bind(sx, sy, sz, sdelta, sray, sidx, snroot, sbase, ssel, px, py, pz, powner, pres, ray_first, ray_count,
          row_list, train_terms, tc_tiles, dens_pts, dens_empty, dens_scale, train_rgb, train_alpha, counters,
-         occ_box, fwd_act, smask, scount, items, keys, unsorted, key_hist, lb_status, res4, strans, pgs, pgc,
+         occ_box, occ_bits, fwd_act, smask, scount, items, keys, unsorted, key_hist, lb_status, res4, strans, pgs, pgc,
          pflag, bwd_rec, bwd_list, bwd_partial, bwd_own, bwd_n);
   }
   Workspace(const Workspace&) = delete;

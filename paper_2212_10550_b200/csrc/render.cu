@@ -120,18 +120,26 @@ struct MarchArgs {
   long long cap;
   int rpw;  // rays per warp (1..32): small ray lists (training) spread over more warps
   const int* occ_box;  // occupied-cell bounding box (-x0, -y0, -z0, x1, y1, z1) or nullptr
+  const uint32_t* occ_bits;  // the mask packed to bits (occ_bbox_kernel) or nullptr: u8 mask
   unsigned long long* stats;  // roofline accounting: [11] += samples tested in pass 1
 };
 
 // Bounding box of the occupied cells, for the march's empty-space skip: stored as
 // (-x0, -y0, -z0, x1, y1, z1) so one atomicMax per entry reduces it; the buffer is preset
 // to 0x80808080 (a large negative int) by a memset, so an all-empty mask leaves x1 < x0.
-__global__ void __launch_bounds__(256) occ_bbox_kernel(OccView g, int* __restrict__ box) {
+__global__ void __launch_bounds__(256) occ_bbox_kernel(OccView g, int* __restrict__ box, uint32_t* __restrict__ bits) {
+  // also packs the mask to bits (one ballot per 32 consecutive cells): march pass 1 tests
+  // occupancy in a 32 KB bit array (64^3) that stays L1-resident instead of the 256 KB u8 mask
   int b[6] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN, INT_MIN, INT_MIN};
   const long long n = static_cast<long long>(g.rx) * g.ry * g.rz;
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    if (!g.mask[i]) continue;
+  const int lane = threadIdx.x & 31;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = base + lane;
+    const bool m = i < n && g.mask[i] != 0;
+    const unsigned word = __ballot_sync(0xffffffffu, m);
+    if (lane == 0) bits[base >> 5] = word;
+    if (!m) continue;
     const int x = static_cast<int>(i % g.rx), y = static_cast<int>((i / g.rx) % g.ry),
               z = static_cast<int>(i / (static_cast<long long>(g.rx) * g.ry));
     b[0] = max(b[0], -x), b[1] = max(b[1], -y), b[2] = max(b[2], -z);
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(256) occ_bbox_kernel(OccView g, int* __restric
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b[k] = max(b[k], __shfl_xor_sync(0xffffffffu, b[k], o));
   }
-  if ((threadIdx.x & 31) == 0 && b[3] >= 0)
+  if (lane == 0 && b[3] >= 0)
     for (int k = 0; k < 6; ++k) atomicMax(box + k, b[k]);
 }
 
@@ -181,12 +189,22 @@ __device__ __forceinline__ void occ_index_range(const int* box, d3 P, d3 Q, doub
 
 const int* launch_occ_bbox(Workspace& w, const OccView& g, cudaStream_t s) {
   w.occ_box.ensure(6);
-  ARFX_CUDA(cudaMemsetAsync(w.occ_box.ptr, 0x80, 6 * sizeof(int), s));
   const long long n = static_cast<long long>(g.rx) * g.ry * g.rz;
+  w.occ_bits.ensure(static_cast<size_t>((n + 31) / 32));
+  ARFX_CUDA(cudaMemsetAsync(w.occ_box.ptr, 0x80, 6 * sizeof(int), s));
   occ_bbox_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 1184))), 256, 0,
-                    s>>>(g, w.occ_box.ptr);
+                    s>>>(g, w.occ_box.ptr, w.occ_bits.ptr);
   ARFX_CUDA(cudaGetLastError());
   return w.occ_box.ptr;
+}
+
+#ifndef ARFX_MARCH_BITS
+#define ARFX_MARCH_BITS 1
+#endif
+// occupancy of cell (cx, cy, cz) (in range): the packed bits when present, else the u8 mask
+__device__ __forceinline__ bool occ_test(const MarchArgs& A, int cx, int cy, int cz) {
+  const size_t i = (static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx;
+  return A.occ_bits ? ((__ldg(A.occ_bits + (i >> 5)) >> (i & 31)) & 1u) != 0 : A.occ.mask[i] != 0;
 }
 
 __device__ __forceinline__ double jitter_at(const MarchArgs& A, Pcg32 base, int i) {
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32, ARFX_MARCH_MIN_BLOCKS) march
             if (cx == -2 || cy == -2 || cz == -2)
               f = occupied(A.occ, rigid_apply(w2n, add3(R.o, mul3(R.d, t))));
             else if (cx >= 0 && cy >= 0 && cz >= 0)
-              f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
+              f = occ_test(A, cx, cy, cz);
             if ((i >> 5) != wk) {
               bal[wk] = word;
               word = 0u;
@@ -333,7 +351,7 @@ __global__ void __launch_bounds__(kMarchWarps * 32, ARFX_MARCH_MIN_BLOCKS) march
                 const RayGeom Rj = make_ray(A.cam, w2n, A.nlo, A.nhi, pj % A.W, pj / A.W);
                 f = occupied(A.occ, rigid_apply(w2n, add3(Rj.o, mul3(Rj.d, t))));
               } else if (cx >= 0 && cy >= 0 && cz >= 0) {
-                f = A.occ.mask[(static_cast<size_t>(cz) * A.occ.ry + cy) * A.occ.rx + cx] != 0;
+                f = occ_test(A, cx, cy, cz);
               }
             } else {
               f = true;
@@ -1163,6 +1181,7 @@ void render_frame(ModelImpl& m, PoseImpl& p, const HostCamera& cam, OccImpl* occ
   if (occ) {
     A.occ = occ->view();
     A.occ_box = launch_occ_bbox(w, A.occ, s);
+    A.occ_bits = ARFX_MARCH_BITS ? w.occ_bits.ptr : nullptr;
   }
   A.N = N;
   A.stratified = stratified;
