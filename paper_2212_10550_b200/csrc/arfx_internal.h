@@ -55,6 +55,17 @@ struct SkinView {
 
 // PoseContext (R/articulation.hpp:17-42) + world->normalized rigid (R/model.hpp:85-98).
 // Rigid = R row-major (9) then t (3).
+// A sorted Newton start: target | bone << 26, and (ARFX_ITEMS64) its result slot in the high
+// word, so the Newton refill needs no slot-base / mask loads
+#ifndef ARFX_ITEMS64
+#define ARFX_ITEMS64 1
+#endif
+#if ARFX_ITEMS64
+using StartItem = unsigned long long;
+#else
+using StartItem = uint32_t;
+#endif
+
 struct PoseCtx {
   int nb;
   int pad_;

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) start_place_kernel(const unsigned long lo
                                                           const uint32_t* __restrict__ keys,
                                                           const uint32_t* __restrict__ unsorted,
                                                           uint32_t* __restrict__ key_cursor,
-                                                          uint32_t* __restrict__ items, long long cap) {
+                                                          StartItem* __restrict__ items, long long cap) {
   long long n = static_cast<long long>(*n_starts);
   n = n < cap ? n : cap;
   const unsigned lane = threadIdx.x & 31;
@@ -266,7 +266,13 @@ __global__ void __launch_bounds__(256) start_place_kernel(const unsigned long lo
     if (act && static_cast<int>(lane) == leader) base = atomicAdd(key_cursor + key, static_cast<uint32_t>(__popc(grp)));
     base = __shfl_sync(0xffffffffu, base, leader);
     const uint32_t pos = base + __popc(grp & ((1u << lane) - 1u));
-    if (act && pos < cap) items[pos] = unsorted[j];
+    if (act && pos < cap) {
+#if ARFX_ITEMS64
+      items[pos] = (static_cast<unsigned long long>(j) << 32) | unsorted[j];  // j is the start's slot
+#else
+      items[pos] = unsorted[j];
+#endif
+    }
   }
 }
 
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(256) start_place_kernel(const unsigned long lo
 template <class Src, bool kSinglePose, bool kStats>
 __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(SkinView S, const PoseCtx* __restrict__ poses,
                                                                   InverseOpts opt, Src src,
-                                                                  const uint32_t* __restrict__ items,
+                                                                  const StartItem* __restrict__ items,
                                                                   const unsigned long long* n_items,
                                                                   const uint32_t* __restrict__ mask_in,
                                                                   const uint32_t* __restrict__ slot_base,
@@ -358,10 +364,15 @@ __global__ void __launch_bounds__(kDsThreads, kDsMinBlocks) start_newton_kernel(
           if (id >= n) {
             state = DS_DONE;
           } else {
-            const uint32_t item = items[id];
+            const StartItem it = items[id];
+            const uint32_t item = static_cast<uint32_t>(it);
             s = item & ((1u << kItemBoneShift) - 1u);
             const int b = static_cast<int>(item >> kItemBoneShift);
+#if ARFX_ITEMS64
+            slot = static_cast<long long>(it >> 32);
+#else
             slot = static_cast<long long>(slot_base[s]) + __popc(mask_in[s] & ((1u << b) - 1u));
+#endif
             if (slot >= cap) slot = cap;  // overflow: scratch slot (result arrays hold cap + 1)
             xt = src.point(s, pose);
             x = rigid_apply((kSinglePose ? Pbase : Pbase + pose)->bone_inv[b], xt);  // x0

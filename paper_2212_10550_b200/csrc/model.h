@@ -80,7 +80,7 @@ struct Workspace {
   // K2 start pipeline (deform_starts.cuh)
   size_t cap_targets = 0, cap_starts = 0;
   DevBuf<uint32_t> smask, scount;  // per target: start mask, start count -> slot base
-  DevBuf<uint32_t> items;                     // sorted by (bone, cell): target | bone << 26
+  DevBuf<StartItem> items;                    // sorted by (bone, cell): target | bone << 26 [| slot << 32]
   DevBuf<uint32_t> keys, unsorted, key_hist;  // counting-sort scratch
   DevBuf<unsigned long long> lb_status;        // single-pass scans: tickets + tile status words
   DevBuf<double4> res4;                        // per start slot: root xyz, residual (-1: no root)
