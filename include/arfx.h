@@ -293,7 +293,10 @@ int arfx_render_model_async(arfx_model m, arfx_pose p, const arfx_camera* cam, a
  * (p_next -> occ_next, side stream + side workspace) while the CURRENT pose renders with its
  * already-built grid (p_cur, occ_cur) into host buffers exactly as arfx_render_model_async;
  * later work on `stream` waits for the new grid. Alternate the two (pose, grid) pairs frame
- * by frame; results are identical to arfx_build_inference_grid + arfx_render_model. */
+ * by frame; results are identical to arfx_build_inference_grid + arfx_render_model.
+ * Internally each (handles, camera, options, shard, image slot, stream) combination is
+ * captured once as a CUDA graph and replayed (up to 8 are cached per model; the first call of
+ * a combination renders the frame twice, and a capture is renewed after workspace growth). */
 int arfx_render_model_pipelined_async(arfx_model m, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
                                       arfx_occ_grid occ_next, const arfx_camera* cam,
                                       const arfx_render_options* opt, int row_shard, int n_shards, float* rgb,

@@ -278,6 +278,8 @@ ModelImpl::~ModelImpl() {
     cudaStreamSynchronize(side);
     cudaStreamDestroy(side);
   }
+  for (auto& e : pipe_graphs) delete static_cast<arfx_frame_graph_s*>(e.graph);
+  pipe_graphs.clear();
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (ev_pipe_fork) cudaEventDestroy(ev_pipe_fork);
@@ -1132,6 +1134,79 @@ int arfx_frame_graph_create(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
 // animation with each frame's grid build overlapping the previous frame's render; every frame
 // is bit-identical to a direct grid + render (test_pipelined_frame_graphs_match_direct).
 // d_counters [2][4]: the next grid's counters, then the render's.
+namespace {
+// Captures one pipelined frame (the next pose's inference grid on the side stream / side
+// workspace beside the current pose's render) as a graph; shared by
+// arfx_frame_graph_create_pipelined and the graph cache of arfx_render_model_pipelined_async.
+arfx_frame_graph_s* make_pipelined_graph(ModelImpl& m, PoseImpl& pc, OccImpl& oc, PoseImpl& pn, OccImpl& on,
+                                         const HostCamera& hc, const arfx_render_options* opt, int shard,
+                                         int nshards, float* d_rgb, float* d_alpha, uint64_t* d_counters,
+                                         cudaStream_t s) {
+  if (!m.side) ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ARFX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  ARFX_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evg{fork, join};
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counters);
+  OccImpl& gn = on;
+  auto enqueue = [&] {
+    ARFX_CUDA(cudaEventRecord(fork, s));
+    ARFX_CUDA(cudaStreamWaitEvent(m.side, fork, 0));
+    {
+      WorkspaceScope side(m, m.ws_side);
+      inference_grid(m, pn, gn, cnt, m.side);
+    }
+    render_frame(m, pc, hc, &oc, opt->samples_per_ray, opt->stratified != 0,
+                 opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha, cnt + 4, s);
+    ARFX_CUDA(cudaEventRecord(join, m.side));
+    ARFX_CUDA(cudaStreamWaitEvent(s, join, 0));
+  };
+  // warm-up (uncaptured): the side workspace for the worst case of a grid build, the main
+  // one from the render's counters
+  {
+    WorkspaceScope side(m, m.ws_side);
+    m.ws().reserve_worst(static_cast<size_t>(gn.res) * gn.res * gn.res, static_cast<size_t>(m.sv.nb));
+  }
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    enqueue();
+    unsigned long long hcnt[8];
+    d2h(hcnt, m.ws().counters.ptr, 8, s);
+    ARFX_CUDA(cudaStreamSynchronize(s));
+    bool rerun;
+    check_overflow_and_grow(m, hcnt, rerun);
+    if (!rerun) break;
+  }
+  const bool prof = m.prof.on;
+  m.prof.on = false;
+  auto g = std::make_unique<arfx_frame_graph_s>();
+  g->device = m.device;
+  ARFX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  try {
+    enqueue();
+  } catch (...) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(s, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    m.prof.on = prof;
+    throw;
+  }
+  ARFX_CUDA(cudaStreamEndCapture(s, &g->graph));
+  m.prof.on = prof;
+  ARFX_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+  g->ws = &m.ws_main;
+  g->ws_gen = m.ws_main.gen;
+  g->ws2 = &m.ws_side;
+  g->ws2_gen = m.ws_side.gen;
+  return g.release();
+}
+}  // namespace
+
 int arfx_frame_graph_create_pipelined(arfx_model mh, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
                                       arfx_occ_grid occ_next, const arfx_camera* cam, const arfx_render_options* opt,
                                       int shard, int nshards, float* d_rgb, float* d_alpha, uint64_t* d_counters,
@@ -1146,68 +1221,8 @@ int arfx_frame_graph_create_pipelined(arfx_model mh, arfx_pose p_cur, arfx_occ_g
     ARFX_CUDA(cudaSetDevice(m.device));
     const cudaStream_t s = stream_of(m, stream);
     require(s != nullptr, "frame_graph_create_pipelined: needs a non-NULL stream");
-    if (!m.side) ARFX_CUDA(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
-    cudaEvent_t fork = nullptr, join = nullptr;
-    ARFX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    ARFX_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-    struct EvGuard {
-      cudaEvent_t a, b;
-      ~EvGuard() {
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-      }
-    } evg{fork, join};
-    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counters);
-    OccImpl& gn = occ_next->impl;
-    auto enqueue = [&] {
-      ARFX_CUDA(cudaEventRecord(fork, s));
-      ARFX_CUDA(cudaStreamWaitEvent(m.side, fork, 0));
-      {
-        WorkspaceScope side(m, m.ws_side);
-        inference_grid(m, p_next->impl, gn, cnt, m.side);
-      }
-      render_frame(m, p_cur->impl, hc, &occ_cur->impl, opt->samples_per_ray, opt->stratified != 0,
-                   opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, d_rgb, d_alpha, cnt + 4, s);
-      ARFX_CUDA(cudaEventRecord(join, m.side));
-      ARFX_CUDA(cudaStreamWaitEvent(s, join, 0));
-    };
-    // warm-up (uncaptured): the side workspace for the worst case of a grid build, the main
-    // one from the render's counters
-    {
-      WorkspaceScope side(m, m.ws_side);
-      m.ws().reserve_worst(static_cast<size_t>(gn.res) * gn.res * gn.res, static_cast<size_t>(m.sv.nb));
-    }
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      enqueue();
-      unsigned long long hcnt[8];
-      d2h(hcnt, m.ws().counters.ptr, 8, s);
-      ARFX_CUDA(cudaStreamSynchronize(s));
-      bool rerun;
-      check_overflow_and_grow(m, hcnt, rerun);
-      if (!rerun) break;
-    }
-    const bool prof = m.prof.on;
-    m.prof.on = false;
-    auto g = std::make_unique<arfx_frame_graph_s>();
-    g->device = m.device;
-    ARFX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    try {
-      enqueue();
-    } catch (...) {
-      cudaGraph_t junk = nullptr;
-      cudaStreamEndCapture(s, &junk);
-      if (junk) cudaGraphDestroy(junk);
-      m.prof.on = prof;
-      throw;
-    }
-    ARFX_CUDA(cudaStreamEndCapture(s, &g->graph));
-    m.prof.on = prof;
-    ARFX_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
-    g->ws = &m.ws_main;
-    g->ws_gen = m.ws_main.gen;
-    g->ws2 = &m.ws_side;
-    g->ws2_gen = m.ws_side.gen;
-    *out = g.release();
+    *out = make_pipelined_graph(m, p_cur->impl, occ_cur->impl, p_next->impl, occ_next->impl, hc, opt, shard, nshards,
+                                d_rgb, d_alpha, d_counters, s);
   });
 }
 
@@ -1292,56 +1307,70 @@ int arfx_render_model(arfx_model mh, arfx_pose ph, const arfx_camera* cam, arfx_
 namespace {
 // arfx_render_model_async's device side: render into one of two device image slots on `s`,
 // then copy this shard's rows to the host buffers on the model's copy stream
+// the next async image slot, sized for the camera; the stream waits until its previous
+// copies are done
+ModelImpl::AsyncSlot& async_slot_acquire(ModelImpl& m, const HostCamera& hc, cudaStream_t s, int& index) {
+  if (!m.copy_stream) {
+    ARFX_CUDA(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
+    for (auto& a : m.async_slot) {
+      ARFX_CUDA(cudaEventCreateWithFlags(&a.rendered, cudaEventDisableTiming));
+      ARFX_CUDA(cudaEventCreateWithFlags(&a.copied, cudaEventDisableTiming));
+    }
+  }
+  index = m.async_next;
+  ModelImpl::AsyncSlot& a = m.async_slot[m.async_next];
+  m.async_next ^= 1;
+  const size_t npix = static_cast<size_t>(hc.width) * hc.height;
+  if (a.rgb.n < npix * 3 || a.counters.n < 8) {
+    ARFX_CUDA(cudaDeviceSynchronize());  // growing a slot: nothing in flight may use it
+    a.rgb.ensure(npix * 3);
+    a.alpha.ensure(npix);
+    a.counters.ensure(8);
+  }
+  ARFX_CUDA(cudaStreamWaitEvent(s, a.copied, 0));  // the slot's previous copies are done
+  return a;
+}
+
+// after the frame was rendered into slot a on s: its rows (of this shard) and the render
+// counters (dev_counters4) to the host buffers on the copy stream
+void async_slot_d2h(ModelImpl& m, ModelImpl::AsyncSlot& a, const HostCamera& hc, int shard, int nshards, float* rgb,
+                    float* alpha, const unsigned long long* dev_counters4, uint64_t* counters4, cudaStream_t s) {
+  ARFX_CUDA(cudaEventRecord(a.rendered, s));
+  const cudaStream_t c = m.copy_stream;
+  ARFX_CUDA(cudaStreamWaitEvent(c, a.rendered, 0));
+  const int W = hc.width, H = hc.height, T = kRowTile;
+  const int full_tiles = H / T;
+  const int n_full = shard < full_tiles ? (full_tiles - 1 - shard) / nshards + 1 : 0;
+  if (n_full > 0) {
+    const size_t off = static_cast<size_t>(shard) * T * W;
+    const size_t pitch3 = static_cast<size_t>(nshards) * T * W * 3 * sizeof(float);
+    const size_t pitch1 = static_cast<size_t>(nshards) * T * W * sizeof(float);
+    ARFX_CUDA(cudaMemcpy2DAsync(rgb + off * 3, pitch3, a.rgb.ptr + off * 3, pitch3,
+                                static_cast<size_t>(T) * W * 3 * sizeof(float), static_cast<size_t>(n_full),
+                                cudaMemcpyDeviceToHost, c));
+    ARFX_CUDA(cudaMemcpy2DAsync(alpha + off, pitch1, a.alpha.ptr + off, pitch1,
+                                static_cast<size_t>(T) * W * sizeof(float), static_cast<size_t>(n_full),
+                                cudaMemcpyDeviceToHost, c));
+  }
+  if (H % T && full_tiles % nshards == shard) {
+    const size_t off = static_cast<size_t>(full_tiles) * T * W;
+    const size_t rows = static_cast<size_t>(H % T);
+    ARFX_CUDA(cudaMemcpyAsync(rgb + off * 3, a.rgb.ptr + off * 3, rows * W * 3 * sizeof(float),
+                              cudaMemcpyDeviceToHost, c));
+    ARFX_CUDA(cudaMemcpyAsync(alpha + off, a.alpha.ptr + off, rows * W * sizeof(float), cudaMemcpyDeviceToHost, c));
+  }
+  if (counters4)
+    ARFX_CUDA(cudaMemcpyAsync(counters4, dev_counters4, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c));
+  ARFX_CUDA(cudaEventRecord(a.copied, c));
+}
+
 void render_async_impl(ModelImpl& m, PoseImpl& p, const HostCamera& hc, OccImpl* occ, const arfx_render_options* opt,
                        int shard, int nshards, float* rgb, float* alpha, uint64_t* counters4, cudaStream_t s) {
-    if (!m.copy_stream) {
-      ARFX_CUDA(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
-      for (auto& a : m.async_slot) {
-        ARFX_CUDA(cudaEventCreateWithFlags(&a.rendered, cudaEventDisableTiming));
-        ARFX_CUDA(cudaEventCreateWithFlags(&a.copied, cudaEventDisableTiming));
-      }
-    }
-    ModelImpl::AsyncSlot& a = m.async_slot[m.async_next];
-    m.async_next ^= 1;
-    const size_t npix = static_cast<size_t>(hc.width) * hc.height;
-    if (a.rgb.n < npix * 3) {
-      ARFX_CUDA(cudaDeviceSynchronize());  // growing a slot: nothing in flight may use it
-      a.rgb.ensure(npix * 3);
-      a.alpha.ensure(npix);
-      a.counters.ensure(4);
-    }
-    ARFX_CUDA(cudaStreamWaitEvent(s, a.copied, 0));  // the slot's previous copies are done
-    render_frame(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0,
-                 opt->epsilon_terminate, opt->seed, opt->frame_id, shard, nshards, a.rgb.ptr, a.alpha.ptr,
-                 a.counters.ptr, s);
-    ARFX_CUDA(cudaEventRecord(a.rendered, s));
-    const cudaStream_t c = m.copy_stream;
-    ARFX_CUDA(cudaStreamWaitEvent(c, a.rendered, 0));
-    const int W = hc.width, H = hc.height, T = kRowTile;
-    const int full_tiles = H / T;
-    const int n_full = shard < full_tiles ? (full_tiles - 1 - shard) / nshards + 1 : 0;
-    if (n_full > 0) {
-      const size_t off = static_cast<size_t>(shard) * T * W;
-      const size_t pitch3 = static_cast<size_t>(nshards) * T * W * 3 * sizeof(float);
-      const size_t pitch1 = static_cast<size_t>(nshards) * T * W * sizeof(float);
-      ARFX_CUDA(cudaMemcpy2DAsync(rgb + off * 3, pitch3, a.rgb.ptr + off * 3, pitch3,
-                                  static_cast<size_t>(T) * W * 3 * sizeof(float), static_cast<size_t>(n_full),
-                                  cudaMemcpyDeviceToHost, c));
-      ARFX_CUDA(cudaMemcpy2DAsync(alpha + off, pitch1, a.alpha.ptr + off, pitch1,
-                                  static_cast<size_t>(T) * W * sizeof(float), static_cast<size_t>(n_full),
-                                  cudaMemcpyDeviceToHost, c));
-    }
-    if (H % T && full_tiles % nshards == shard) {
-      const size_t off = static_cast<size_t>(full_tiles) * T * W;
-      const size_t rows = static_cast<size_t>(H % T);
-      ARFX_CUDA(cudaMemcpyAsync(rgb + off * 3, a.rgb.ptr + off * 3, rows * W * 3 * sizeof(float),
-                                cudaMemcpyDeviceToHost, c));
-      ARFX_CUDA(cudaMemcpyAsync(alpha + off, a.alpha.ptr + off, rows * W * sizeof(float), cudaMemcpyDeviceToHost,
-                                c));
-    }
-    if (counters4)
-      ARFX_CUDA(cudaMemcpyAsync(counters4, a.counters.ptr, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c));
-    ARFX_CUDA(cudaEventRecord(a.copied, c));
+  int index = 0;
+  ModelImpl::AsyncSlot& a = async_slot_acquire(m, hc, s, index);
+  render_frame(m, p, hc, occ, opt->samples_per_ray, opt->stratified != 0, opt->epsilon_terminate, opt->seed,
+               opt->frame_id, shard, nshards, a.rgb.ptr, a.alpha.ptr, a.counters.ptr, s);
+  async_slot_d2h(m, a, hc, shard, nshards, rgb, alpha, a.counters.ptr, counters4, s);
 }
 }  // namespace
 
@@ -1364,6 +1393,9 @@ int arfx_render_model_async(arfx_model mh, arfx_pose ph, const arfx_camera* cam,
 // renders with its already-built grid (p_cur, occ_cur) into host buffers as
 // arfx_render_model_async does; later work on `stream` waits for the grid. Alternate the two
 // (pose, grid) pairs frame by frame (the C-ABI twin of arfx_frame_graph_create_pipelined).
+#ifndef ARFX_PIPE_ASYNC_GRAPH
+#define ARFX_PIPE_ASYNC_GRAPH 1
+#endif
 int arfx_render_model_pipelined_async(arfx_model mh, arfx_pose p_cur, arfx_occ_grid occ_cur, arfx_pose p_next,
                                       arfx_occ_grid occ_next, const arfx_camera* cam, const arfx_render_options* opt,
                                       int shard, int nshards, float* rgb, float* alpha, uint64_t* counters4,
@@ -1389,6 +1421,51 @@ int arfx_render_model_pipelined_async(arfx_model mh, arfx_pose p_cur, arfx_occ_g
         ARFX_CUDA(cudaDeviceSynchronize());
         m.ws().reserve_worst(cells, static_cast<size_t>(m.sv.nb));
       }
+    }
+#if ARFX_PIPE_ASYNC_GRAPH
+    // graph-backed: the frame (next pose's grid beside the current pose's render into the
+    // async slot) is captured once per (handles, camera, options, shard, slot, stream) and
+    // replayed; a capture whose workspace has since grown is re-captured (the capture's
+    // warm-up renders the same frame, so a miss costs one extra frame, never a wrong one)
+    if (s != nullptr) {
+      int slot = 0;
+      ModelImpl::AsyncSlot& a = async_slot_acquire(m, hc, s, slot);
+      std::string key;
+      auto add = [&key](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+      const void* handles[5] = {p_cur, occ_cur, p_next, occ_next, s};
+      add(handles, sizeof(handles));
+      add(cam, sizeof(*cam));
+      add(opt, sizeof(*opt));
+      const int ints[3] = {shard, nshards, slot};
+      add(ints, sizeof(ints));
+      arfx_frame_graph_s* g = nullptr;
+      for (auto it = m.pipe_graphs.begin(); it != m.pipe_graphs.end(); ++it) {
+        if (it->key != key) continue;
+        auto* c = static_cast<arfx_frame_graph_s*>(it->graph);
+        if (c->ws->gen == c->ws_gen && c->ws2->gen == c->ws2_gen) {
+          g = c;
+        } else {
+          delete c;
+          m.pipe_graphs.erase(it);
+        }
+        break;
+      }
+      if (!g) {
+        if (m.pipe_graphs.size() >= 8) {
+          delete static_cast<arfx_frame_graph_s*>(m.pipe_graphs.front().graph);
+          m.pipe_graphs.erase(m.pipe_graphs.begin());
+        }
+        g = make_pipelined_graph(m, p_cur->impl, occ_cur->impl, p_next->impl, gn, hc, opt, shard, nshards, a.rgb.ptr,
+                                 a.alpha.ptr, reinterpret_cast<uint64_t*>(a.counters.ptr), s);
+        m.pipe_graphs.push_back({key, g});
+      }
+      ARFX_CUDA(cudaGraphLaunch(g->exec, s));
+      async_slot_d2h(m, a, hc, shard, nshards, rgb, alpha, a.counters.ptr + 4, counters4, s);
+      return;
+    }
+#endif
+    {
+      WorkspaceScope side(m, m.ws_side);
       ARFX_CUDA(cudaEventRecord(m.ev_pipe_fork, s));
       ARFX_CUDA(cudaStreamWaitEvent(m.side, m.ev_pipe_fork, 0));
       inference_grid(m, p_next->impl, gn, nullptr, m.side);

@@ -196,6 +196,13 @@ struct ModelImpl {
     cudaEvent_t rendered = nullptr, copied = nullptr;
   } async_slot[2];
   int async_next = 0;
+  // arfx_render_model_pipelined_async: captured pipelined frames (grid of the next pose beside
+  // the render into an async slot), keyed by (handles, camera, options, shard, slot, stream)
+  struct PipeGraphEntry {
+    std::string key;
+    void* graph = nullptr;  // arfx_frame_graph_s
+  };
+  std::vector<PipeGraphEntry> pipe_graphs;
   cudaStream_t copy_stream = nullptr;
   // arfx_model_set_param_fence: kernels that read the parameters or write the gradients
   // wait for this event first (an optimizer running on another stream)
