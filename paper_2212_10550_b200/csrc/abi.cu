@@ -1432,8 +1432,20 @@ int arfx_render_model_pipelined_async(arfx_model mh, arfx_pose p_cur, arfx_occ_g
       ModelImpl::AsyncSlot& a = async_slot_acquire(m, hc, s, slot);
       std::string key;
       auto add = [&key](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
-      const void* handles[5] = {p_cur, occ_cur, p_next, occ_next, s};
-      add(handles, sizeof(handles));
+      // handles and every device pointer / by-value parameter the capture bakes in (a freed
+      // and re-allocated handle, grid or image slot can never hit a stale capture)
+      const OccImpl& oc = occ_cur->impl;
+      const void* ptrs[13] = {p_cur, occ_cur, p_next, occ_next, s, p_cur->impl.dev.ptr, p_next->impl.dev.ptr,
+                              oc.values.ptr, oc.mask.ptr, gn.values.ptr, gn.mask.ptr, a.rgb.ptr, a.counters.ptr};
+      add(ptrs, sizeof(ptrs));
+      const void* ptrs2[1] = {a.alpha.ptr};
+      add(ptrs2, sizeof(ptrs2));
+      const double occ_par[4] = {static_cast<double>(oc.res), oc.threshold, static_cast<double>(gn.res), gn.threshold};
+      add(occ_par, sizeof(occ_par));
+      const int occ_dil[2] = {oc.dilation, gn.dilation};
+      add(occ_dil, sizeof(occ_dil));
+      add(&oc.box, sizeof(oc.box));
+      add(&gn.box, sizeof(gn.box));
       add(cam, sizeof(*cam));
       add(opt, sizeof(*opt));
       const int ints[3] = {shard, nshards, slot};
