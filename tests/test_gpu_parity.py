@@ -629,3 +629,52 @@ def test_pipelined_host_render_matches_sync(gpu):
     for r, o, c in zip(ref, outs, cnts):
         assert c[3] == 0 and c[0] > 0
         assert np.array_equal(r.rgb, o.rgb) and np.array_equal(r.alpha, o.alpha)
+
+
+def test_pipelined_host_render_graph_cache_follows_handles_and_cameras(gpu):
+    """The graph-backed arfx_render_model_pipelined_async re-captures instead of replaying a
+    stale frame: a camera change (larger image slots), then new pose handles and grids
+    (the old ones destroyed), then the first camera again -- every frame == the synchronous
+    path, bit for bit."""
+    import ctypes as C
+
+    import torch
+    from paper_2212_10550_b200._lib import check, lib
+    L = lib()
+    sk = fx.smpl24()
+    m = arf.build_model(sk, fx.config1_grid(), fx.config1_mlp(), (32, 32, 32), fx.CONFIG1_SEED)
+    poses = fx.animation_poses(sk, 6)
+    opt, cfg = fx.config1_render_options(), fx.config1_occupancy()
+    pin = lambda shape: torch.zeros(shape, dtype=torch.float32).pin_memory().numpy()  # noqa: E731
+
+    def run(cam, pv, occ, frames):
+        W, H = cam.width, cam.height
+        outs = [arf.RenderImages(W, H, pin((H, W, 3)), pin((H, W))) for _ in frames]
+        cnts = [np.zeros(4, np.uint64) for _ in frames]
+        pv[0].update(poses[frames[0]])
+        check(L.arfx_build_inference_grid(m._h, pv[0]._h, occ[0]._h, None, None))
+        for k, f in enumerate(frames):
+            cur, nxt = k & 1, (k + 1) & 1
+            pv[nxt].update(poses[frames[(k + 1) % len(frames)]], sync=False)
+            check(L.arfx_render_model_pipelined_async(m._h, pv[cur]._h, occ[cur]._h, pv[nxt]._h, occ[nxt]._h,
+                                                      C.byref(cam.to_c()), C.byref(opt.to_c()), 0, 1,
+                                                      arf.ptr(outs[k].rgb, C.c_float),
+                                                      arf.ptr(outs[k].alpha, C.c_float),
+                                                      cnts[k].ctypes.data_as(C.POINTER(C.c_uint64)), None))
+        arf.render_wait(m)
+        for f, o, c in zip(frames, outs, cnts):
+            r = arf.render_model(m, poses[f], cam, arf.build_model_inference_grid(m, poses[f], cfg), opt)
+            assert c[3] == 0 and c[0] > 0
+            assert np.array_equal(r.rgb, o.rgb) and np.array_equal(r.alpha, o.alpha), f
+
+    cam_a, cam_b = fx.default_camera(sk, 96, 80), fx.default_camera(sk, 150, 130)
+    pv = [arf.PosedModelView(m, poses[0]), arf.PosedModelView(m, poses[0])]
+    occ = [arf.OccupancyGrid(m.normalized_box, cfg) for _ in range(2)]
+    run(cam_a, pv, occ, [0, 1, 2])
+    run(cam_b, pv, occ, [3, 4])          # larger image: the async slots grow
+    del pv, occ                          # handles and grids destroyed ...
+    import gc
+    gc.collect()
+    pv = [arf.PosedModelView(m, poses[0]), arf.PosedModelView(m, poses[0])]
+    occ = [arf.OccupancyGrid(m.normalized_box, cfg) for _ in range(2)]
+    run(cam_a, pv, occ, [5, 1, 3, 0])    # ... and re-created: no stale capture replays
